@@ -1,0 +1,175 @@
+/*
+ * libslora_b200 — C ABI of the B200-native shared-backbone multi-LoRA hot path.
+ *
+ * The reference (ServerlessLoRA, /root/reference/pkg = `slorasim`) ships NO native
+ * code and no FFI: its forward is the latency law T0 + alpha*(b-1)
+ * (pkg/src/slorasim/batching.py:17-21, consumed at pkg/src/slorasim/engine.py:832,888,909)
+ * and its pre-load is `usable_at_ms = now + load_ms` (pkg/src/slorasim/engine.py:1040-1053).
+ * Each entry point below names the reference interface whose MEANING it replaces; the
+ * Python mirror (paper_2505_14468_b200/) binds these with ctypes.
+ *
+ * Conventions
+ *  - every function returns int32 status (SLX_OK = 0, negative = error), never throws,
+ *    never allocates device memory (workspaces are passed in), never synchronises, and
+ *    enqueues on the caller's stream (`stream` is a cudaStream_t passed as void*).
+ *  - activations are row-major with an explicit leading dimension (elements);
+ *    dtype SLX_DT_BF16 or SLX_DT_F32 ("fp32 parity mode": fp32 activations, fp32
+ *    accumulate, bf16 weights upcast exactly).
+ *  - weights are bf16, nn.Linear layout W[out, in] (K-major).  LoRA is PEFT layout:
+ *    A [rank, d_in], B [d_out, rank], scale = alpha / rank, unmerged
+ *    (PAPER.md:614-621,645-646).
+ *  - index arrays are int32 on the device; slot -1 means "no adapter".
+ *  - pointers used with 128-bit loads must be 16-byte aligned and row lengths
+ *    multiples of 8 elements (SLX_ERR_ALIGN / SLX_ERR_INVALID otherwise).
+ */
+#ifndef SLORA_B200_H
+#define SLORA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SLX_API __attribute__((visibility("default")))
+#else
+#define SLX_API
+#endif
+
+#define SLX_ABI_VERSION 1
+
+enum {
+  SLX_OK = 0,
+  SLX_ERR_INVALID = -1,     /* bad shape / argument (Python: ValueError) */
+  SLX_ERR_ALIGN = -2,       /* pointer or leading dim misaligned (ValueError) */
+  SLX_ERR_UNSUPPORTED = -3, /* shape outside the kernel's envelope (ValueError) */
+  SLX_ERR_WORKSPACE = -4,   /* workspace too small (ValueError) */
+  SLX_ERR_CUDA = -5,        /* CUDA launch/runtime error (RuntimeError) */
+  SLX_ERR_NCCL = -6         /* NCCL error (RuntimeError) */
+};
+
+enum { SLX_DT_BF16 = 0, SLX_DT_F32 = 1 };
+
+enum {
+  SLX_EPI_NONE = 0,     /* C = A W^T */
+  SLX_EPI_RESIDUAL = 1, /* C = A W^T + R   (R may alias C) */
+  SLX_EPI_SILU_MUL = 2  /* W rows blocked [gate 128 | up 128]*: C[M, N/2] = silu(gate) * up */
+};
+
+SLX_API const char* slx_status_string(int status);
+SLX_API int slx_abi_version(void);
+/* Number of SMs of the current device (cached), for grid sizing in host code. */
+SLX_API int slx_device_sm_count(int* out);
+
+/* ------------------------------------------------------------------ K1: backbone GEMM
+ * Replaces the prefill/decode "work" of the latency law (batching.py:17-21,
+ * engine.py:832 prefill_work_ms, engine.py:888,909 decode gap) for the q/k/v/o,
+ * gate/up/down and lm_head projections.
+ * C[M,N] = A[M,K] · W[N,K]^T (+ epilogue), bf16 in, fp32 accumulate in TMEM (tcgen05),
+ * C dtype c_dtype (bf16 or fp32).  M>=1, N % 128 == 0, K % 64 == 0, lda/ldc/ldr % 8 == 0.
+ * Small M (decode) runs the swap-AB split-K kernel and needs `ws` of
+ * slx_gemm_workspace_bytes(M, N, K) bytes (0 for large M).
+ */
+SLX_API size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue);
+SLX_API int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
+                  const void* R, int ldr, int M, int N, int K, int epilogue,
+                  void* ws, size_t ws_bytes, void* stream);
+/* fp32-parity GEMM (CUDA cores): A fp32 [M,K], W bf16 [N,K], C/R fp32.  Epilogue NONE or
+ * RESIDUAL.  K % 8 == 0. */
+SLX_API int slx_gemm_f32(const void* A, int lda, const void* W, void* C, int ldc,
+                 const void* R, int ldr, int M, int N, int K, int epilogue, void* stream);
+
+/* ------------------------------------------------------------------ K2/K3: multi-LoRA
+ * Replaces the batch → adapter association of the contention-aware batcher's
+ * FlushDecision (batching.py:99-105) by a per-token / per-segment adapter slot.
+ * One call applies up to SLX_LORA_MAX_TARGETS projections that share the input x:
+ *   y[t, col(n)] += scale[s] * sum_j (x[t] . A_s[j]) * B_s[n, j],   s = slot of token t.
+ */
+#define SLX_LORA_MAX_TARGETS 4
+typedef struct slx_lora_target {
+  const uint64_t* a_ptrs; /* device [n_slots]: address of A_s [rank_s, d_in] (bf16) */
+  const uint64_t* b_ptrs; /* device [n_slots]: address of B_s [d_out, rank_s] (bf16) */
+  int d_out;
+  int y_col_offset;       /* output column of feature 0 */
+  int y_col_block;        /* features per contiguous output block (= d_out when unblocked) */
+  int y_col_stride;       /* output-column distance between consecutive blocks */
+} slx_lora_target;
+
+/* Workspace for a plan + apply over n_tok tokens (plan is reusable across layers). */
+SLX_API size_t slx_lora_workspace_bytes(int n_tok, int n_slots, int max_rank, int n_targets);
+/* Plan from a per-token slot (decode, BGMV): stable counting sort of tokens by slot. */
+SLX_API int slx_lora_plan_tokens(const int32_t* tok_slot, int n_tok, int n_slots,
+                         void* ws, size_t ws_bytes, void* stream);
+/* Plan from contiguous segments (prefill, SGMV): tokens [seg_indptr[s], seg_indptr[s+1])
+ * use slot seg_slot[s]. seg_indptr: device int32 [n_seg+1]. */
+SLX_API int slx_lora_plan_segments(const int32_t* seg_indptr, const int32_t* seg_slot, int n_seg,
+                           int n_tok, int n_slots, void* ws, size_t ws_bytes, void* stream);
+/* Shrink (x A^T -> v staged fp32) + expand (scale * v B^T added into y) over the plan. */
+SLX_API int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ldx, int n_tok, int d_in,
+                   const int32_t* slot_rank, const float* slot_scale, int n_slots, int max_rank,
+                   int n_targets, const slx_lora_target* targets,
+                   void* ws, size_t ws_bytes, void* stream);
+/* Convenience: plan_tokens + apply (BGMV) and plan_segments + apply (SGMV). */
+SLX_API int slx_lora_bgmv(int dtype, void* y, int ldy, const void* x, int ldx, const int32_t* tok_slot,
+                  int n_tok, int d_in, const int32_t* slot_rank, const float* slot_scale,
+                  int n_slots, int max_rank, int n_targets, const slx_lora_target* targets,
+                  void* ws, size_t ws_bytes, void* stream);
+SLX_API int slx_lora_sgmv(int dtype, void* y, int ldy, const void* x, int ldx, const int32_t* seg_indptr,
+                  const int32_t* seg_slot, int n_seg, int n_tok, int d_in,
+                  const int32_t* slot_rank, const float* slot_scale, int n_slots, int max_rank,
+                  int n_targets, const slx_lora_target* targets,
+                  void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ K4: supporting ops
+ * KV cache layout per layer: [n_seq_slots][kv_heads][max_ctx][head_dim], dtype = activations.
+ * The KV pool honours the ledger's per-request reservation (ledger.py:162-174).
+ */
+SLX_API int slx_embedding(int dtype, void* out, const void* table, const int32_t* tokens,
+                  int n_tok, int d, int vocab, void* stream);
+SLX_API int slx_rmsnorm(int dtype, void* out, int ldo, const void* x, int ldx, const void* w,
+                int n_tok, int d, float eps, void* stream);
+/* qkv [n_tok, (H + 2 Hkv) D]: rotate q,k in place (rotate-half, cos/sin tables fp32
+ * [max_pos, D/2]) and write k, v at (tok_seq[t], tok_pos[t]) of the caches. */
+SLX_API int slx_rope_kv_write(int dtype, void* qkv, int ld_qkv, int n_tok, int heads, int kv_heads,
+                      int head_dim, const int32_t* tok_pos, const int32_t* tok_seq,
+                      const float* cos_tab, const float* sin_tab, int max_pos,
+                      void* k_cache, void* v_cache, int max_ctx, void* stream);
+/* Causal attention of each token t over cache positions 0..tok_pos[t] of sequence tok_seq[t].
+ * q read from qkv (after rope). out [n_tok, H*D]. */
+SLX_API int slx_attention(int dtype, void* out, int ldo, const void* qkv, int ld_qkv, int n_tok,
+                  int heads, int kv_heads, int head_dim, const int32_t* tok_pos,
+                  const int32_t* tok_seq, const void* k_cache, const void* v_cache, int max_ctx,
+                  void* stream);
+/* gu [n_tok, 2*ffn] in the blocked layout of SLX_EPI_SILU_MUL -> out [n_tok, ffn]. */
+SLX_API int slx_silu_mul_blocked(int dtype, void* out, int ldo, const void* gu, int ld_gu, int n_tok,
+                         int ffn, void* stream);
+/* Row-wise argmax (lowest index on ties) of logits [n_rows, n_cols] (dtype) -> int32. */
+SLX_API int slx_argmax(int dtype, int32_t* out, const void* logits, int ld, int n_rows, int n_cols,
+               void* stream);
+
+/* ------------------------------------------------------------------ P1: artifact pre-loader
+ * Replaces the modelled load `usable_at_ms = now + load_from_container_ms | load_cold_ms`
+ * of a PreloadPlan GPU placement (engine.py:1040-1053; ArtifactSpec core.py:56-78).
+ */
+SLX_API int slx_host_register(void* ptr, size_t bytes);
+SLX_API int slx_host_unregister(void* ptr);
+/* Chunked pinned-host -> device copy on `stream`; records `done_event` (cudaEvent_t or NULL). */
+SLX_API int slx_preload_h2d(void* dst_dev, const void* src_pinned, size_t bytes, size_t chunk_bytes,
+                    void* stream, void* done_event);
+/* NCCL communicator owned by the pre-loader (the only collective of the system). */
+SLX_API int slx_nccl_unique_id_bytes(void);
+SLX_API int slx_nccl_get_unique_id(void* out_id);
+SLX_API int slx_nccl_comm_init(void** comm, int nranks, const void* id, int rank);
+SLX_API int slx_nccl_comm_destroy(void* comm);
+SLX_API int slx_bcast(void* buf, size_t bytes, int root, void* comm, void* stream);
+/* Single host read, NVLink fan-out: the root copies chunk i host->device on copy_stream
+ * while chunk i-1 is broadcast on comm_stream; non-roots only receive. */
+SLX_API int slx_preload_bcast(void* dst_dev, const void* src_pinned, size_t bytes, size_t chunk_bytes,
+                      int root, void* comm, void* copy_stream, void* comm_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLORA_B200_H */

@@ -188,6 +188,16 @@ class OracleModel:
         last = seg_indptr[1:] - 1
         return self.logits(h[last])
 
+    def teacher_forced(self, tokens: list[int], adapter_id: int) -> np.ndarray:
+        """Logits at every position of one sequence (fresh KV state) [L, V]."""
+        self.kv.append([(np.zeros((0, self.cfg.kv_heads, self.cfg.head_dim), F32),
+                         np.zeros((0, self.cfg.kv_heads, self.cfg.head_dim), F32))
+                        for _ in range(self.cfg.layers)])
+        L = len(tokens)
+        h = self._forward(np.asarray(tokens, np.int64), np.arange(L), np.array([0, L]),
+                          np.array([adapter_id]), [len(self.kv) - 1])
+        return self.logits(h)
+
     def decode(self, seqs: list[int], tokens: list[int], adapter_ids: list[int]) -> np.ndarray:
         """One token for each sequence in ``seqs``; returns logits [n, V]."""
         n = len(seqs)

@@ -1,0 +1,107 @@
+"""ctypes binding of libslora_b200.so (the C ABI in include/slora_b200.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` / ``make -C
+paper_2505_14468_b200/csrc``.  There is no fallback: if the shared object is
+missing every op raises, so a GPU run can never silently take another path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslora_b200.so")
+
+SLX_OK = 0
+SLX_ERR_INVALID = -1
+SLX_ERR_ALIGN = -2
+SLX_ERR_UNSUPPORTED = -3
+SLX_ERR_WORKSPACE = -4
+SLX_ERR_CUDA = -5
+SLX_ERR_NCCL = -6
+
+DT_BF16 = 0
+DT_F32 = 1
+EPI_NONE = 0
+EPI_RESIDUAL = 1
+EPI_SILU_MUL = 2
+LORA_MAX_TARGETS = 4
+
+_p = ctypes.c_void_p
+_i = ctypes.c_int
+_f = ctypes.c_float
+_sz = ctypes.c_size_t
+
+
+class LoraTarget(ctypes.Structure):
+    _fields_ = [("a_ptrs", _p), ("b_ptrs", _p), ("d_out", _i), ("y_col_offset", _i),
+                ("y_col_block", _i), ("y_col_stride", _i)]
+
+
+# name -> (restype, argtypes): every symbol declared in include/slora_b200.h
+SIGNATURES = {
+    "slx_status_string": (ctypes.c_char_p, [_i]),
+    "slx_abi_version": (_i, []),
+    "slx_device_sm_count": (_i, [ctypes.POINTER(_i)]),
+    "slx_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
+    "slx_gemm_bf16": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p]),
+    "slx_gemm_f32": (_i, [_p, _i, _p, _p, _i, _p, _i, _i, _i, _i, _i, _p]),
+    "slx_lora_workspace_bytes": (_sz, [_i, _i, _i, _i]),
+    "slx_lora_plan_tokens": (_i, [_p, _i, _i, _p, _sz, _p]),
+    "slx_lora_plan_segments": (_i, [_p, _p, _i, _i, _i, _p, _sz, _p]),
+    "slx_lora_apply": (_i, [_i, _p, _i, _p, _i, _i, _i, _p, _p, _i, _i, _i,
+                            ctypes.POINTER(LoraTarget), _p, _sz, _p]),
+    "slx_lora_bgmv": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _p, _p, _i, _i, _i,
+                           ctypes.POINTER(LoraTarget), _p, _sz, _p]),
+    "slx_lora_sgmv": (_i, [_i, _p, _i, _p, _i, _p, _p, _i, _i, _i, _p, _p, _i, _i, _i,
+                           ctypes.POINTER(LoraTarget), _p, _sz, _p]),
+    "slx_embedding": (_i, [_i, _p, _p, _p, _i, _i, _i, _p]),
+    "slx_rmsnorm": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _f, _p]),
+    "slx_rope_kv_write": (_i, [_i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p, _i, _p]),
+    "slx_attention": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p]),
+    "slx_silu_mul_blocked": (_i, [_i, _p, _i, _p, _i, _i, _i, _p]),
+    "slx_argmax": (_i, [_i, _p, _p, _i, _i, _i, _p]),
+    "slx_host_register": (_i, [_p, _sz]),
+    "slx_host_unregister": (_i, [_p]),
+    "slx_preload_h2d": (_i, [_p, _p, _sz, _sz, _p, _p]),
+    "slx_nccl_unique_id_bytes": (_i, []),
+    "slx_nccl_get_unique_id": (_i, [_p]),
+    "slx_nccl_comm_init": (_i, [ctypes.POINTER(_p), _i, _p, _i]),
+    "slx_nccl_comm_destroy": (_i, [_p]),
+    "slx_bcast": (_i, [_p, _sz, _i, _p, _p]),
+    "slx_preload_bcast": (_i, [_p, _p, _sz, _sz, _i, _p, _p, _p]),
+}
+
+_LIB = None
+
+
+class SlxError(RuntimeError):
+    """A CUDA/NCCL failure reported by libslora_b200."""
+
+
+def load() -> ctypes.CDLL:
+    """Load the in-tree library (raises if it was not built — no fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (or make -C paper_2505_14468_b200/csrc)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if lib.slx_abi_version() != 1:
+            raise ImportError("libslora_b200 ABI version mismatch")
+        _LIB = lib
+    return _LIB
+
+
+def check(status: int, what: str) -> None:
+    if status == SLX_OK:
+        return
+    msg = f"{what}: {load().slx_status_string(status).decode()} (status {status})"
+    if status in (SLX_ERR_INVALID, SLX_ERR_ALIGN, SLX_ERR_UNSUPPORTED, SLX_ERR_WORKSPACE):
+        raise ValueError(msg)
+    raise SlxError(msg)

@@ -1,0 +1,410 @@
+// K4 supporting ops of the multi-LoRA Llama forward: embedding, RMSNorm, RoPE + KV write,
+// causal attention over the KV pool, blocked SiLU*mul, argmax, and the fp32-parity SIMT GEMM.
+// All templated on the activation type (bf16 throughput mode / fp32 parity mode); weights
+// are always bf16 and accumulation is always fp32.
+#include <float.h>
+
+#include "common.cuh"
+
+namespace slx {
+
+// ------------------------------------------------------------------ embedding
+template <typename T>
+__global__ void embedding_kernel(T* __restrict__ out, const bf16* __restrict__ table,
+                                 const int32_t* __restrict__ tokens, int d, int vocab) {
+  const int t = blockIdx.x;
+  int tok = tokens[t];
+  tok = tok < 0 ? 0 : (tok >= vocab ? vocab - 1 : tok);
+  const bf16* src = table + (size_t)tok * d;
+  T* dst = out + (size_t)t * d;
+  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+    float f[8];
+    Vec8<bf16>::load(src + i, f);
+    Vec8<T>::store(dst + i, f);
+  }
+}
+
+// ------------------------------------------------------------------ RMSNorm
+// out = x * (1 / sqrt(mean(x^2) + eps)) * w     (oracle/llama_lora.py::rmsnorm)
+template <typename T>
+__global__ void rmsnorm_kernel(T* __restrict__ out, int ldo, const T* __restrict__ x, int ldx,
+                               const bf16* __restrict__ w, int d, float eps) {
+  const int t = blockIdx.x;
+  const T* xr = x + (size_t)t * ldx;
+  float ss = 0.f;
+  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+    float f[8];
+    Vec8<T>::load(xr + i, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
+  T* orow = out + (size_t)t * ldo;
+  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+    float f[8], g[8];
+    Vec8<T>::load(xr + i, f);
+    Vec8<bf16>::load(w + i, g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = (f[j] * inv) * g[j];
+    Vec8<T>::store(orow + i, f);
+  }
+}
+
+// ------------------------------------------------------------------ RoPE + KV write
+// One CTA per token; thread i handles rotation pair (i, i + D/2) of every head.
+template <typename T>
+__global__ void rope_kv_kernel(T* __restrict__ qkv, int ld, int H, int Hkv, int D,
+                               const int32_t* __restrict__ tok_pos,
+                               const int32_t* __restrict__ tok_seq,
+                               const float* __restrict__ cos_tab, const float* __restrict__ sin_tab,
+                               T* __restrict__ kc, T* __restrict__ vc, int max_ctx) {
+  const int t = blockIdx.x;
+  const int pos = tok_pos[t];
+  const int seq = tok_seq[t];
+  const int half = D >> 1;
+  T* row = qkv + (size_t)t * ld;
+  const float* cr = cos_tab + (size_t)pos * half;
+  const float* sr = sin_tab + (size_t)pos * half;
+  const int n_rot = (H + Hkv) * half;
+  for (int idx = threadIdx.x; idx < n_rot; idx += blockDim.x) {
+    const int h = idx / half, i = idx % half;
+    T* base = row + h * D;  // q heads then k heads are contiguous
+    const float c = cr[i], s = sr[i];
+    const float x1 = to_f32(base[i]), x2 = to_f32(base[i + half]);
+    const float r1 = x1 * c - x2 * s;
+    const float r2 = x2 * c + x1 * s;
+    base[i] = from_f32<T>(r1);
+    base[i + half] = from_f32<T>(r2);
+    if (h >= H) {
+      const int hk = h - H;
+      T* dst = kc + (((size_t)seq * Hkv + hk) * max_ctx + pos) * D;
+      dst[i] = from_f32<T>(r1);
+      dst[i + half] = from_f32<T>(r2);
+    }
+  }
+  const T* vsrc = row + (H + Hkv) * D;
+  for (int idx = threadIdx.x; idx < Hkv * D; idx += blockDim.x) {
+    const int hk = idx / D, i = idx % D;
+    vc[(((size_t)seq * Hkv + hk) * max_ctx + pos) * D + i] = vsrc[idx];
+  }
+}
+
+// ------------------------------------------------------------------ attention (decode-style)
+// Block = 4 warps per (token, head). Each warp owns keys j = 32*(4*c + warp) + lane for
+// chunks c; online softmax per warp; merge across warps in smem.  D <= 128, D % 32 == 0.
+constexpr int ATT_WARPS = 4;
+template <typename T, int D>
+__global__ void __launch_bounds__(ATT_WARPS * 32)
+attention_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv, int ld, int H, int Hkv,
+                 const int32_t* __restrict__ tok_pos, const int32_t* __restrict__ tok_seq,
+                 const T* __restrict__ kc, const T* __restrict__ vc, int max_ctx, float scale) {
+  constexpr int PER_LANE = D / 32;
+  const int t = blockIdx.x / H, h = blockIdx.x % H;
+  const int hk = h / (H / Hkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_keys = tok_pos[t] + 1;
+  const int seq = tok_seq[t];
+  __shared__ float q_s[D];
+  __shared__ float m_s[ATT_WARPS], l_s[ATT_WARPS];
+  __shared__ float acc_s[ATT_WARPS][D];
+  for (int i = threadIdx.x; i < D; i += blockDim.x) q_s[i] = to_f32(qkv[(size_t)t * ld + h * D + i]);
+  __syncthreads();
+  const T* kbase = kc + ((size_t)seq * Hkv + hk) * max_ctx * D;
+  const T* vbase = vc + ((size_t)seq * Hkv + hk) * max_ctx * D;
+  float m = -FLT_MAX, l = 0.f;
+  float acc[PER_LANE];
+#pragma unroll
+  for (int i = 0; i < PER_LANE; ++i) acc[i] = 0.f;
+  for (int j0 = warp * 32; j0 < n_keys; j0 += ATT_WARPS * 32) {
+    const int j = j0 + lane;
+    float s = -FLT_MAX;
+    if (j < n_keys) {
+      const T* kr = kbase + (size_t)j * D;
+      float dot = 0.f;
+#pragma unroll
+      for (int i = 0; i < D; i += 8) {
+        float f[8];
+        Vec8<T>::load(kr + i, f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dot += q_s[i + e] * f[e];
+      }
+      s = dot * scale;
+    }
+    const float cmax = warp_max(s);
+    const float m_new = fmaxf(m, cmax);
+    const float corr = expf(m - m_new);
+    const float p = (j < n_keys) ? expf(s - m_new) : 0.f;
+    l = l * corr + warp_sum(p);
+#pragma unroll
+    for (int i = 0; i < PER_LANE; ++i) acc[i] *= corr;
+    const int nk = min(32, n_keys - j0);
+    for (int jj = 0; jj < nk; ++jj) {
+      const float pj = __shfl_sync(0xffffffffu, p, jj);
+      const T* vr = vbase + (size_t)(j0 + jj) * D;
+#pragma unroll
+      for (int i = 0; i < PER_LANE; ++i) acc[i] += pj * to_f32(vr[lane + 32 * i]);
+    }
+    m = m_new;
+  }
+  if (lane == 0) { m_s[warp] = m; l_s[warp] = l; }
+#pragma unroll
+  for (int i = 0; i < PER_LANE; ++i) acc_s[warp][lane + 32 * i] = acc[i];
+  __syncthreads();
+  if (warp == 0) {
+    float mg = -FLT_MAX;
+#pragma unroll
+    for (int w = 0; w < ATT_WARPS; ++w) mg = fmaxf(mg, m_s[w]);
+    float lg = 0.f, cw[ATT_WARPS];
+#pragma unroll
+    for (int w = 0; w < ATT_WARPS; ++w) {
+      cw[w] = (l_s[w] > 0.f) ? expf(m_s[w] - mg) : 0.f;
+      lg += l_s[w] * cw[w];
+    }
+    const float inv = 1.0f / lg;
+#pragma unroll
+    for (int i = 0; i < PER_LANE; ++i) {
+      float o = 0.f;
+#pragma unroll
+      for (int w = 0; w < ATT_WARPS; ++w) o += acc_s[w][lane + 32 * i] * cw[w];
+      out[(size_t)t * ldo + h * D + lane + 32 * i] = from_f32<T>(o * inv);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ SiLU * mul (blocked gate/up)
+template <typename T>
+__global__ void silu_mul_kernel(T* __restrict__ out, int ldo, const T* __restrict__ gu, int ld_gu,
+                                int ffn) {
+  const int t = blockIdx.y;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (i >= ffn) return;
+  const int blk = i >> 7, off = i & 127;
+  const T* g = gu + (size_t)t * ld_gu + blk * 256 + off;
+  float a[8], b[8];
+  Vec8<T>::load(g, a);
+  Vec8<T>::load(g + 128, b);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = (a[j] / (1.0f + expf(-a[j]))) * b[j];
+  Vec8<T>::store(out + (size_t)t * ldo + i, a);
+}
+
+// ------------------------------------------------------------------ argmax
+template <typename T>
+__global__ void argmax_kernel(int32_t* __restrict__ out, const T* __restrict__ x, int ld, int n) {
+  const T* row = x + (size_t)blockIdx.x * ld;
+  float best = -FLT_MAX;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float v = to_f32(row[i]);
+    if (v > best) { best = v; bi = i; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { sv[w] = best; si[w] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k)
+      if (sv[k] > best || (sv[k] == best && si[k] < bi)) { best = sv[k]; bi = si[k]; }
+    out[blockIdx.x] = bi;
+  }
+}
+
+// ------------------------------------------------------------------ fp32-parity SIMT GEMM
+// C[M,N] = A[M,K] (fp32) . W[N,K]^T (bf16) [+ R].  64x64 tile, BK 16, 4x4 per thread.
+constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16;
+__global__ void __launch_bounds__(256)
+gemm_f32_kernel(const float* __restrict__ A, int lda, const bf16* __restrict__ W,
+                float* __restrict__ C, int ldc, const float* __restrict__ R, int ldr,
+                int M, int N, int K) {
+  __shared__ float As[SG_BK][SG_BM + 4];
+  __shared__ float Ws[SG_BK][SG_BN + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.y * SG_BM, n0 = blockIdx.x * SG_BN;
+  float acc[4][4] = {};
+  // loader mapping: 256 threads x 4 elements = 64 rows x 16 k
+  const int lr = threadIdx.x / 4, lk = (threadIdx.x % 4) * 4;
+  for (int k0 = 0; k0 < K; k0 += SG_BK) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = k0 + lk + e;
+      const int am = m0 + lr, wn = n0 + lr;
+      As[lk + e][lr] = (am < M && k < K) ? A[(size_t)am * lda + k] : 0.f;
+      Ws[lk + e][lr] = (wn < N && k < K) ? __bfloat162float(W[(size_t)wn * K + k]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < SG_BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Ws[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = acc[i][j];
+      if (R) v += R[(size_t)m * ldr + n];
+      C[(size_t)m * ldc + n] = v;
+    }
+  }
+}
+
+}  // namespace slx
+
+using namespace slx;
+
+// ================================================================== C ABI
+#define DISPATCH_DT(dtype, ...)                      \
+  do {                                               \
+    if ((dtype) == SLX_DT_BF16) {                    \
+      using T = bf16;                                \
+      __VA_ARGS__;                                   \
+    } else if ((dtype) == SLX_DT_F32) {              \
+      using T = float;                               \
+      __VA_ARGS__;                                   \
+    } else {                                         \
+      return SLX_ERR_INVALID;                        \
+    }                                                \
+  } while (0)
+
+extern "C" int slx_embedding(int dtype, void* out, const void* table, const int32_t* tokens,
+                             int n_tok, int d, int vocab, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && d > 0 && d % 8 == 0 && vocab > 0 && out && table && tokens);
+  SLX_CHECK_ALIGN(out, 16);
+  SLX_CHECK_ALIGN(table, 16);
+  if (n_tok == 0) return SLX_OK;
+  DISPATCH_DT(dtype, (embedding_kernel<T><<<n_tok, 128, 0, (cudaStream_t)stream>>>(
+                         (T*)out, (const bf16*)table, tokens, d, vocab)));
+  SLX_LAUNCH_CHECK();
+  return SLX_OK;
+}
+
+extern "C" int slx_rmsnorm(int dtype, void* out, int ldo, const void* x, int ldx, const void* w,
+                           int n_tok, int d, float eps, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && d > 0 && d % 8 == 0 && ldo % 8 == 0 && ldx % 8 == 0 && ldo >= d &&
+                ldx >= d && out && x && w);
+  SLX_CHECK_ALIGN(out, 16);
+  SLX_CHECK_ALIGN(x, 16);
+  SLX_CHECK_ALIGN(w, 16);
+  if (n_tok == 0) return SLX_OK;
+  int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
+  DISPATCH_DT(dtype, (rmsnorm_kernel<T><<<n_tok, threads, 0, (cudaStream_t)stream>>>(
+                         (T*)out, ldo, (const T*)x, ldx, (const bf16*)w, d, eps)));
+  SLX_LAUNCH_CHECK();
+  return SLX_OK;
+}
+
+extern "C" int slx_rope_kv_write(int dtype, void* qkv, int ld_qkv, int n_tok, int heads,
+                                 int kv_heads, int head_dim, const int32_t* tok_pos,
+                                 const int32_t* tok_seq, const float* cos_tab,
+                                 const float* sin_tab, int max_pos, void* k_cache, void* v_cache,
+                                 int max_ctx, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && heads > 0 && kv_heads > 0 && heads % kv_heads == 0 &&
+                head_dim % 2 == 0 && ld_qkv >= (heads + 2 * kv_heads) * head_dim && max_pos > 0 &&
+                max_ctx > 0 && qkv && tok_pos && tok_seq && cos_tab && sin_tab && k_cache &&
+                v_cache);
+  if (n_tok == 0) return SLX_OK;
+  DISPATCH_DT(dtype, (rope_kv_kernel<T><<<n_tok, 256, 0, (cudaStream_t)stream>>>(
+                         (T*)qkv, ld_qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos_tab,
+                         sin_tab, (T*)k_cache, (T*)v_cache, max_ctx)));
+  SLX_LAUNCH_CHECK();
+  return SLX_OK;
+}
+
+extern "C" int slx_attention(int dtype, void* out, int ldo, const void* qkv, int ld_qkv, int n_tok,
+                             int heads, int kv_heads, int head_dim, const int32_t* tok_pos,
+                             const int32_t* tok_seq, const void* k_cache, const void* v_cache,
+                             int max_ctx, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && heads > 0 && kv_heads > 0 && heads % kv_heads == 0 &&
+                ld_qkv >= (heads + 2 * kv_heads) * head_dim && ldo >= heads * head_dim && out &&
+                qkv && tok_pos && tok_seq && k_cache && v_cache);
+  SLX_CHECK_ARG(ldo % 8 == 0 && ld_qkv % 8 == 0);
+  SLX_CHECK_ALIGN(k_cache, 16);
+  SLX_CHECK_ALIGN(v_cache, 16);
+  if (head_dim != 64 && head_dim != 128) return SLX_ERR_UNSUPPORTED;
+  if (n_tok == 0) return SLX_OK;
+  const float scale = 1.0f / sqrtf((float)head_dim);
+  const dim3 grid((unsigned)n_tok * heads);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (head_dim == 64) {
+    DISPATCH_DT(dtype, (attention_kernel<T, 64><<<grid, ATT_WARPS * 32, 0, s>>>(
+                           (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
+                           (const T*)k_cache, (const T*)v_cache, max_ctx, scale)));
+  } else {
+    DISPATCH_DT(dtype, (attention_kernel<T, 128><<<grid, ATT_WARPS * 32, 0, s>>>(
+                           (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
+                           (const T*)k_cache, (const T*)v_cache, max_ctx, scale)));
+  }
+  SLX_LAUNCH_CHECK();
+  return SLX_OK;
+}
+
+extern "C" int slx_silu_mul_blocked(int dtype, void* out, int ldo, const void* gu, int ld_gu,
+                                    int n_tok, int ffn, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && ffn > 0 && ffn % 128 == 0 && ld_gu >= 2 * ffn && ldo >= ffn &&
+                ldo % 8 == 0 && ld_gu % 8 == 0 && out && gu);
+  SLX_CHECK_ALIGN(out, 16);
+  SLX_CHECK_ALIGN(gu, 16);
+  if (n_tok == 0) return SLX_OK;
+  dim3 grid((unsigned)ceil_div(ffn / 8, 128), (unsigned)n_tok);
+  DISPATCH_DT(dtype, (silu_mul_kernel<T><<<grid, 128, 0, (cudaStream_t)stream>>>(
+                         (T*)out, ldo, (const T*)gu, ld_gu, ffn)));
+  SLX_LAUNCH_CHECK();
+  return SLX_OK;
+}
+
+extern "C" int slx_argmax(int dtype, int32_t* out, const void* logits, int ld, int n_rows,
+                          int n_cols, void* stream) {
+  SLX_CHECK_ARG(n_rows >= 0 && n_cols > 0 && ld >= n_cols && out && logits);
+  if (n_rows == 0) return SLX_OK;
+  DISPATCH_DT(dtype, (argmax_kernel<T><<<n_rows, 1024, 0, (cudaStream_t)stream>>>(
+                         out, (const T*)logits, ld, n_cols)));
+  SLX_LAUNCH_CHECK();
+  return SLX_OK;
+}
+
+extern "C" int slx_gemm_f32(const void* A, int lda, const void* W, void* C, int ldc, const void* R,
+                            int ldr, int M, int N, int K, int epilogue, void* stream) {
+  SLX_CHECK_ARG(M >= 0 && N > 0 && K > 0 && lda >= K && ldc >= N && A && W && C);
+  if (epilogue == SLX_EPI_RESIDUAL) {
+    SLX_CHECK_ARG(R != nullptr && ldr >= N);
+  } else if (epilogue != SLX_EPI_NONE) {
+    return SLX_ERR_UNSUPPORTED;
+  }
+  if (M == 0) return SLX_OK;
+  dim3 grid((unsigned)ceil_div(N, SG_BN), (unsigned)ceil_div(M, SG_BM));
+  gemm_f32_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      (const float*)A, lda, (const bf16*)W, (float*)C, ldc,
+      epilogue == SLX_EPI_RESIDUAL ? (const float*)R : nullptr, ldr, M, N, K);
+  SLX_LAUNCH_CHECK();
+  return SLX_OK;
+}

@@ -1,0 +1,356 @@
+"""Shared-backbone multi-LoRA Llama runtime on one B200.
+
+One resident backbone per GPU (the reference's one-backbone-per-GPU ledger rule,
+``/root/reference/pkg/src/slorasim/ledger.py:130-134``) serves a mixed batch whose
+tokens each carry an adapter slot; the adapters live in an HBM slot pool.  The
+forward is the unmerged LoRA of ``PAPER.md:614-621``: every targeted projection is
+``x W^T`` (tcgen05 GEMM) plus ``scale * (x A^T) B^T`` (LoRA shrink/expand kernels)
+added into the GEMM output.
+
+Two activation modes share the same packed bf16 weights:
+  * ``torch.bfloat16`` — throughput mode (tcgen05 GEMMs, bf16 activations);
+  * ``torch.float32``  — parity mode (fp32 activations, fp32 accumulate, bf16 weights
+    upcast exactly), used for the bit-exact greedy-token check against the oracle.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import ops
+from ._lib import EPI_RESIDUAL, EPI_SILU_MUL
+from .config import ATTN_TARGETS, BackboneConfig, LoraConfig
+
+
+def _round_up(x: int, m: int) -> int:
+    return (x + m - 1) // m * m
+
+
+def _to_dev(a, device, dtype=torch.bfloat16) -> torch.Tensor:
+    t = torch.as_tensor(a) if not isinstance(a, torch.Tensor) else a
+    return t.to(device=device, dtype=dtype).contiguous()
+
+
+def rope_tables(max_pos: int, head_dim: int, theta: float):
+    inv = 1.0 / (theta ** (np.arange(0, head_dim, 2, dtype=np.float64) / head_dim))
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+class AdapterPool:
+    """HBM adapter slots.  Slot s holds one adapter as ONE contiguous bf16 blob with
+    A_t [r, d_in] and B_t [d_out, r] for every (layer, target), so a single pinned
+    H2D copy (or NCCL broadcast) materialises it; device pointer tables
+    ``a_ptr[layer][target]`` / ``b_ptr[layer][target]`` (int64 [n_slots]) index it."""
+
+    def __init__(self, cfg: BackboneConfig, targets, n_slots: int, max_rank: int, device):
+        self.cfg, self.targets = cfg, tuple(targets)
+        self.n_slots, self.max_rank = n_slots, max_rank
+        self.device = torch.device(device)
+        L, nt = cfg.layers, len(self.targets)
+        self.a_ptr = torch.zeros((L, nt, n_slots), dtype=torch.int64, device=self.device)
+        self.b_ptr = torch.zeros((L, nt, n_slots), dtype=torch.int64, device=self.device)
+        self.rank = torch.zeros(n_slots, dtype=torch.int32, device=self.device)
+        self.scale = torch.zeros(n_slots, dtype=torch.float32, device=self.device)
+        self.blobs: list[torch.Tensor | None] = [None] * n_slots
+        self.configs: list[LoraConfig | None] = [None] * n_slots
+
+    def blob_layout(self, rank: int):
+        """[(layer, target, a_off, b_off, d_in, d_out)] in elements, and total elements."""
+        out, off = [], 0
+        for l in range(self.cfg.layers):
+            for t in self.targets:
+                di, do = self.cfg.target_dims(t)
+                out.append((l, t, off, off + rank * di, di, do))
+                off += rank * (di + do)
+        return out, off
+
+    def pack(self, weights: dict, rank: int) -> torch.Tensor:
+        """Host-side packing of an adapter dict (``layers.{l}.{t}.A/B``) into a blob (CPU bf16)."""
+        layout, n = self.blob_layout(rank)
+        blob = torch.empty(n, dtype=torch.bfloat16)
+        for l, t, ao, bo, di, do in layout:
+            blob[ao:ao + rank * di] = torch.as_tensor(weights[f"layers.{l}.{t}.A"]).reshape(-1).to(torch.bfloat16)
+            blob[bo:bo + do * rank] = torch.as_tensor(weights[f"layers.{l}.{t}.B"]).reshape(-1).to(torch.bfloat16)
+        return blob
+
+    def install(self, slot: int, blob: torch.Tensor, lora: LoraConfig) -> None:
+        """Adopt a device blob (already filled, e.g. by the pre-loader) as slot ``slot``."""
+        if lora.rank > self.max_rank or lora.rank % 8:
+            raise ValueError(f"rank {lora.rank} must be a multiple of 8 and <= {self.max_rank}")
+        if set(lora.targets) - set(self.targets):
+            raise ValueError(f"adapter targets {lora.targets} not in pool targets {self.targets}")
+        layout, n = self.blob_layout(lora.rank)
+        if blob.numel() != n or blob.device != self.device or blob.dtype != torch.bfloat16:
+            raise ValueError("blob shape/device/dtype mismatch")
+        base = blob.data_ptr()
+        a = torch.zeros_like(self.a_ptr[:, :, slot], device="cpu")
+        b = torch.zeros_like(a)
+        for l, t, ao, bo, _, _ in layout:
+            ti = self.targets.index(t)
+            if t in lora.targets:
+                a[l, ti] = base + 2 * ao
+                b[l, ti] = base + 2 * bo
+        self.a_ptr[:, :, slot] = a.to(self.device)
+        self.b_ptr[:, :, slot] = b.to(self.device)
+        self.rank[slot] = lora.rank
+        self.scale[slot] = lora.scale
+        self.blobs[slot] = blob
+        self.configs[slot] = lora
+
+    def load(self, slot: int, weights: dict, lora: LoraConfig) -> None:
+        blob = self.pack(weights, lora.rank)
+        if lora.targets != self.targets:  # untargeted projections: zero A/B, pointer left null
+            pass
+        self.install(slot, blob.to(self.device), lora)
+
+    def load_random(self, slot: int, lora: LoraConfig, seed: int, std: float = 0.02) -> None:
+        """On-device random adapter (A ~ N(0, 1/d_in), B ~ N(0, std)) for large shapes."""
+        layout, n = self.blob_layout(lora.rank)
+        g = torch.Generator(device=self.device).manual_seed(seed)
+        blob = torch.empty(n, dtype=torch.bfloat16, device=self.device)
+        for _, _, ao, bo, di, do in layout:
+            blob[ao:ao + lora.rank * di] = (torch.randn(lora.rank * di, generator=g, device=self.device)
+                                            / math.sqrt(di)).to(torch.bfloat16)
+            blob[bo:bo + do * lora.rank] = (torch.randn(do * lora.rank, generator=g, device=self.device)
+                                            * std).to(torch.bfloat16)
+        self.install(slot, blob, lora)
+
+    def evict(self, slot: int) -> None:
+        self.a_ptr[:, :, slot] = 0
+        self.b_ptr[:, :, slot] = 0
+        self.rank[slot] = 0
+        self.scale[slot] = 0.0
+        self.blobs[slot] = None
+        self.configs[slot] = None
+
+    def resident_bytes(self) -> int:
+        return sum(b.numel() * 2 for b in self.blobs if b is not None)
+
+
+class MultiLoraModel:
+    """Llama backbone + adapter pool + KV pool on one GPU."""
+
+    def __init__(self, cfg: BackboneConfig, *, dtype=torch.bfloat16, device="cuda",
+                 max_seqs: int = 64, max_ctx: int = 512, lora_targets=ATTN_TARGETS,
+                 n_slots: int = 32, max_rank: int = 16, max_tokens: int = 4096):
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("dtype must be bf16 (throughput) or fp32 (parity)")
+        self.cfg, self.dtype = cfg, dtype
+        self.device = torch.device(device)
+        self.max_seqs, self.max_ctx, self.max_tokens = max_seqs, max_ctx, max_tokens
+        self.targets = tuple(lora_targets)
+        self.ffn_pad = _round_up(cfg.ffn, 128)
+        self.pool = AdapterPool(cfg, self.targets, n_slots, max_rank, self.device)
+        self.ws = ops.Workspace(self.device, 64 << 20)
+        nt = len(self.targets)
+        self.lora_ws = torch.zeros(max(ops.lora_workspace_bytes(max_tokens, n_slots, max_rank,
+                                                                min(nt, 4)), 256) + 256,
+                                   dtype=torch.uint8, device=self.device)
+        cos, sin = rope_tables(max_ctx, cfg.head_dim, cfg.rope_theta)
+        self.cos = torch.from_numpy(cos).to(self.device)
+        self.sin = torch.from_numpy(sin).to(self.device)
+        kv_shape = (max_seqs, cfg.kv_heads, max_ctx, cfg.head_dim)
+        self.k_cache = [torch.zeros(kv_shape, dtype=dtype, device=self.device) for _ in range(cfg.layers)]
+        self.v_cache = [torch.zeros(kv_shape, dtype=dtype, device=self.device) for _ in range(cfg.layers)]
+        self.seq_len = [0] * max_seqs
+        self.free_seqs = list(range(max_seqs))[::-1]
+        self.w: dict[str, torch.Tensor] = {}
+
+    # ------------------------------------------------------------------ weights
+    def load_backbone(self, weights: dict) -> None:
+        """Pack a backbone dict (oracle naming, fp32 or bf16) into the device layout."""
+        cfg, dev = self.cfg, self.device
+        w = {}
+        w["embed"] = _to_dev(weights["embed"], dev)
+        w["final_norm"] = _to_dev(weights["final_norm"], dev)
+        w["lm_head"] = _to_dev(weights["lm_head"], dev)
+        for l in range(cfg.layers):
+            p = f"layers.{l}."
+            g = lambda k: torch.as_tensor(weights[p + k])  # noqa: E731
+            w[p + "input_norm"] = _to_dev(g("input_norm"), dev)
+            w[p + "post_norm"] = _to_dev(g("post_norm"), dev)
+            w[p + "w_qkv"] = _to_dev(torch.cat([g("wq"), g("wk"), g("wv")], 0), dev)
+            w[p + "wo"] = _to_dev(g("wo"), dev)
+            w[p + "w_gu"] = self._block_gate_up(g("w_gate"), g("w_up")).to(dev)
+            down = torch.zeros((cfg.hidden, self.ffn_pad), dtype=torch.bfloat16)
+            down[:, :cfg.ffn] = g("w_down").to(torch.bfloat16)
+            w[p + "w_down"] = down.to(dev)
+        self.w = w
+
+    def _block_gate_up(self, gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
+        """[gate rows 128 | up rows 128] blocks, zero-padded to ffn_pad (SLX_EPI_SILU_MUL)."""
+        f, d = gate.shape
+        fp = self.ffn_pad
+        gp = torch.zeros((fp, d), dtype=torch.bfloat16, device=gate.device)
+        upp = torch.zeros((fp, d), dtype=torch.bfloat16, device=gate.device)
+        gp[:f] = gate.to(torch.bfloat16)
+        upp[:f] = up.to(torch.bfloat16)
+        return torch.stack([gp.view(fp // 128, 128, d), upp.view(fp // 128, 128, d)], 1).reshape(2 * fp, d).contiguous()
+
+    def random_backbone(self, seed: int = 0, std: float = 0.02) -> None:
+        """Random-init bf16 backbone generated directly on the device (7B/13B shapes)."""
+        cfg, dev = self.cfg, self.device
+        g = torch.Generator(device=dev).manual_seed(seed)
+
+        def rn(*shape, s=std, mean=0.0):
+            return (torch.randn(*shape, generator=g, device=dev) * s + mean).to(torch.bfloat16)
+
+        w = {"embed": rn(cfg.vocab, cfg.hidden, s=1.0), "final_norm": rn(cfg.hidden, s=0.1, mean=1.0),
+             "lm_head": rn(cfg.vocab, cfg.hidden)}
+        for l in range(cfg.layers):
+            p = f"layers.{l}."
+            w[p + "input_norm"] = rn(cfg.hidden, s=0.1, mean=1.0)
+            w[p + "post_norm"] = rn(cfg.hidden, s=0.1, mean=1.0)
+            w[p + "w_qkv"] = rn(cfg.q_dim + 2 * cfg.kv_dim, cfg.hidden)
+            w[p + "wo"] = rn(cfg.hidden, cfg.q_dim)
+            w[p + "w_gu"] = self._block_gate_up(rn(cfg.ffn, cfg.hidden), rn(cfg.ffn, cfg.hidden))
+            down = torch.zeros((cfg.hidden, self.ffn_pad), dtype=torch.bfloat16, device=dev)
+            down[:, :cfg.ffn] = rn(cfg.hidden, cfg.ffn)
+            w[p + "w_down"] = down
+        self.w = w
+
+    def backbone_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.w.values())
+
+    # ------------------------------------------------------------------ sequences
+    def alloc_seq(self) -> int:
+        if not self.free_seqs:
+            raise RuntimeError("KV pool exhausted")
+        s = self.free_seqs.pop()
+        self.seq_len[s] = 0
+        return s
+
+    def free_seq(self, s: int) -> None:
+        self.seq_len[s] = 0
+        self.free_seqs.append(s)
+
+    # ------------------------------------------------------------------ forward
+    def _gemm(self, a, w, out=None, residual=None, silu=False, out_dtype=None):
+        if self.dtype == torch.bfloat16:
+            epi = EPI_SILU_MUL if silu else (EPI_RESIDUAL if residual is not None else 0)
+            return ops.gemm(a, w, out, epilogue=epi, residual=residual, out_dtype=out_dtype,
+                            ws=self.ws)
+        assert not silu
+        return ops.gemm_f32(a, w, out, residual=residual)
+
+    def _lora(self, y, x, layer: int, names, cols, d_in=None):
+        """Apply LoRA of targets ``names`` with output column maps ``cols``."""
+        idx = [i for i, t in enumerate(self.targets) if t in names]
+        if not idx:
+            return
+        specs = []
+        for i in idx:
+            t = self.targets[i]
+            off, blk, stride = cols[t]
+            specs.append((self.pool.a_ptr[layer, i], self.pool.b_ptr[layer, i],
+                          self.cfg.target_dims(t)[1], off, blk, stride))
+        ops.lora_apply(y, x, d_in if d_in is not None else x.shape[1], self.pool.rank,
+                       self.pool.scale, self.pool.max_rank, ops.make_targets(specs), self.lora_ws)
+
+    def forward(self, tokens, pos, seq, slot, logit_rows=None) -> torch.Tensor:
+        """Token-major mixed batch.  tokens/pos/seq/slot: device int32 [T].
+        Returns logits (fp32) for ``logit_rows`` (device int64) or for every token."""
+        cfg, w, dt = self.cfg, self.w, self.dtype
+        T = tokens.numel()
+        if T > self.max_tokens:
+            raise ValueError(f"batch of {T} tokens exceeds max_tokens={self.max_tokens}")
+        dev = self.device
+        d, qd, kvd = cfg.hidden, cfg.q_dim, cfg.kv_dim
+        x = torch.empty((T, d), dtype=dt, device=dev)
+        h = torch.empty((T, d), dtype=dt, device=dev)
+        qkv = torch.empty((T, qd + 2 * kvd), dtype=dt, device=dev)
+        attn = torch.empty((T, qd), dtype=dt, device=dev)
+        mlp = torch.empty((T, self.ffn_pad), dtype=dt, device=dev)
+        fused_silu = dt == torch.bfloat16 and not ({"gate", "up"} & set(self.targets))
+        gu = None if fused_silu else torch.empty((T, 2 * self.ffn_pad), dtype=dt, device=dev)
+        ops.embedding(x, w["embed"], tokens)
+        if self.targets:
+            ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
+        qkv_cols = {"q": (0, qd, qd), "k": (qd, kvd, kvd), "v": (qd + kvd, kvd, kvd)}
+        for l in range(cfg.layers):
+            p = f"layers.{l}."
+            ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
+            self._gemm(h, w[p + "w_qkv"], qkv)
+            self._lora(qkv, h, l, ("q", "k", "v"), qkv_cols)
+            ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
+                              self.sin, self.k_cache[l], self.v_cache[l])
+            ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
+                          self.k_cache[l], self.v_cache[l])
+            self._gemm(attn, w[p + "wo"], x, residual=x)
+            self._lora(x, attn, l, ("o",), {"o": (0, d, d)})
+            ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
+            if fused_silu:
+                self._gemm(h, w[p + "w_gu"], mlp, silu=True)
+            else:
+                self._gemm(h, w[p + "w_gu"], gu)
+                self._lora(gu, h, l, ("gate", "up"), {"gate": (0, 128, 256), "up": (128, 128, 256)})
+                ops.silu_mul_blocked(mlp, gu, self.ffn_pad)
+            self._gemm(mlp, w[p + "w_down"], x, residual=x)
+            self._lora(x, mlp, l, ("down",), {"down": (0, d, d)}, d_in=cfg.ffn)
+        rows = x if logit_rows is None else x.index_select(0, logit_rows)
+        hn = torch.empty_like(rows)
+        ops.rmsnorm(hn, rows, w["final_norm"], cfg.rms_eps)
+        if dt == torch.bfloat16:
+            return self._gemm(hn, w["lm_head"], out_dtype=torch.float32)
+        return self._gemm(hn, w["lm_head"])
+
+    # ------------------------------------------------------------------ request-level API
+    def prefill(self, prompts, adapter_slots):
+        """Start one sequence per prompt (one mixed, adapter-segmented batch).
+        Returns (seq_ids, last-token logits [n, V] fp32)."""
+        seqs = [self.alloc_seq() for _ in prompts]
+        toks, pos, sq, sl, last = [], [], [], [], []
+        for s, p, a in zip(seqs, prompts, adapter_slots):
+            L = len(p)
+            if L + self.seq_len[s] > self.max_ctx:
+                raise ValueError("prompt exceeds max_ctx")
+            toks += list(p)
+            pos += list(range(self.seq_len[s], self.seq_len[s] + L))
+            sq += [s] * L
+            sl += [a] * L
+            last.append(len(toks) - 1)
+            self.seq_len[s] += L
+        dev = self.device
+        i32 = lambda v: torch.tensor(v, dtype=torch.int32, device=dev)  # noqa: E731
+        logits = self.forward(i32(toks), i32(pos), i32(sq), i32(sl),
+                              torch.tensor(last, dtype=torch.int64, device=dev))
+        return seqs, logits
+
+    def decode(self, seqs, tokens, adapter_slots) -> torch.Tensor:
+        pos = []
+        for s in seqs:
+            if self.seq_len[s] >= self.max_ctx:
+                raise ValueError("sequence reached max_ctx")
+            pos.append(self.seq_len[s])
+            self.seq_len[s] += 1
+        dev = self.device
+        i32 = lambda v: torch.tensor(v, dtype=torch.int32, device=dev)  # noqa: E731
+        return self.forward(i32(list(tokens)), i32(pos), i32(list(seqs)), i32(list(adapter_slots)))
+
+    def argmax(self, logits: torch.Tensor) -> torch.Tensor:
+        out = torch.empty(logits.shape[0], dtype=torch.int32, device=logits.device)
+        return ops.argmax(out, logits)
+
+    def generate(self, prompts, adapter_slots, n_new: int, return_logits: bool = False):
+        """Greedy decode; returns tokens [n, n_new] (np.int64) (+ per-step logits)."""
+        seqs, logits = self.prefill(prompts, adapter_slots)
+        toks, all_logits = [], []
+        try:
+            for step in range(n_new):
+                if return_logits:
+                    all_logits.append(logits.float().cpu())
+                nxt = self.argmax(logits)
+                toks.append(nxt.cpu().numpy().astype(np.int64))
+                if step + 1 < n_new:
+                    logits = self.decode(seqs, toks[-1].tolist(), adapter_slots)
+        finally:
+            for s in seqs:
+                self.free_seq(s)
+        out = np.stack(toks, 1)
+        if return_logits:
+            return out, torch.stack(all_logits, 1).numpy()
+        return out

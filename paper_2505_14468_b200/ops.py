@@ -1,0 +1,195 @@
+"""torch-tensor front end of the C ABI (device memory and streams come from PyTorch).
+
+Every function enqueues on ``torch.cuda.current_stream()`` and never synchronises,
+so a sequence of calls can be captured into a CUDA graph.  Shapes and dtypes are
+validated here (ValueError) and again in C (status codes).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, LoraTarget, check
+
+_DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
+
+
+def _dt(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise ValueError(f"unsupported activation dtype {t.dtype}") from None
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ld(t: torch.Tensor) -> int:
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError("expected a row-major 2-D tensor with unit column stride")
+    return t.stride(0)
+
+
+class Workspace:
+    """Zero-initialised device scratch (counters inside must start at zero; kernels keep
+    them zero).  Grows only outside graph capture."""
+
+    def __init__(self, device, nbytes: int = 64 << 20):
+        self.device = torch.device(device)
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if nbytes > self.buf.numel():
+            if torch.cuda.is_current_stream_capturing():
+                raise RuntimeError("workspace growth during CUDA graph capture")
+            self.buf = torch.zeros(max(nbytes, 2 * self.buf.numel()), dtype=torch.uint8,
+                                   device=self.device)
+        return self.buf
+
+
+# ---------------------------------------------------------------------------------- K1
+def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None, *,
+         epilogue: int = EPI_NONE, residual: torch.Tensor | None = None,
+         out_dtype: torch.dtype | None = None, ws: Workspace | None = None) -> torch.Tensor:
+    """bf16 tcgen05 GEMM: out = a @ w.T (+ residual | silu*mul of blocked gate/up)."""
+    if a.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
+        raise ValueError("gemm: a and w must be bf16")
+    M, K = a.shape
+    N, Kw = w.shape
+    if Kw != K or not w.is_contiguous():
+        raise ValueError("gemm: w must be contiguous [N, K]")
+    n_out = N // 2 if epilogue == EPI_SILU_MUL else N
+    if out is None:
+        out = torch.empty((M, n_out), dtype=out_dtype or torch.bfloat16, device=a.device)
+    lib = _lib.load()
+    need = lib.slx_gemm_workspace_bytes(M, N, K, epilogue)
+    wsb = None
+    if need:
+        if ws is None:
+            raise ValueError("gemm: this shape needs a workspace")
+        wsb = ws.get(need)
+    check(lib.slx_gemm_bf16(_ptr(a), _ld(a), _ptr(w), _ptr(out), _ld(out), _dt(out),
+                            _ptr(residual), _ld(residual) if residual is not None else 0,
+                            M, N, K, epilogue, _ptr(wsb), wsb.numel() if wsb is not None else 0,
+                            _stream()), "slx_gemm_bf16")
+    return out
+
+
+def gemm_f32(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None, *,
+             residual: torch.Tensor | None = None) -> torch.Tensor:
+    """fp32-parity GEMM: fp32 activations x bf16 weights (upcast exactly), fp32 out."""
+    if a.dtype != torch.float32 or w.dtype != torch.bfloat16:
+        raise ValueError("gemm_f32: a fp32, w bf16")
+    M, K = a.shape
+    N = w.shape[0]
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=a.device)
+    epi = EPI_RESIDUAL if residual is not None else EPI_NONE
+    check(_lib.load().slx_gemm_f32(_ptr(a), _ld(a), _ptr(w), _ptr(out), _ld(out), _ptr(residual),
+                                   _ld(residual) if residual is not None else 0, M, N, K, epi,
+                                   _stream()), "slx_gemm_f32")
+    return out
+
+
+# ---------------------------------------------------------------------------------- K2/K3
+def lora_workspace_bytes(n_tok: int, n_slots: int, max_rank: int, n_targets: int) -> int:
+    return _lib.load().slx_lora_workspace_bytes(n_tok, n_slots, max_rank, n_targets)
+
+
+def lora_plan_tokens(tok_slot: torch.Tensor, n_slots: int, ws: torch.Tensor) -> None:
+    check(_lib.load().slx_lora_plan_tokens(_ptr(tok_slot), tok_slot.numel(), n_slots, _ptr(ws),
+                                           ws.numel(), _stream()), "slx_lora_plan_tokens")
+
+
+def lora_plan_segments(seg_indptr: torch.Tensor, seg_slot: torch.Tensor, n_tok: int,
+                       n_slots: int, ws: torch.Tensor) -> None:
+    check(_lib.load().slx_lora_plan_segments(_ptr(seg_indptr), _ptr(seg_slot), seg_slot.numel(),
+                                             n_tok, n_slots, _ptr(ws), ws.numel(), _stream()),
+          "slx_lora_plan_segments")
+
+
+def make_targets(specs) -> ctypes.Array:
+    """specs: iterable of (a_ptr_table, b_ptr_table, d_out, col_off, col_blk, col_stride)."""
+    specs = list(specs)
+    arr = (LoraTarget * len(specs))()
+    for i, (a, b, d_out, off, blk, stride) in enumerate(specs):
+        arr[i] = LoraTarget(a.data_ptr(), b.data_ptr(), d_out, off, blk, stride)
+    return arr
+
+
+def lora_apply(y: torch.Tensor, x: torch.Tensor, d_in: int, slot_rank: torch.Tensor,
+               slot_scale: torch.Tensor, max_rank: int, targets, ws: torch.Tensor) -> None:
+    """y[t, col(n)] += scale * (x[t, :d_in] A^T) B^T over the plan stored in ws."""
+    if y.dtype != x.dtype:
+        raise ValueError("lora_apply: x and y dtypes differ")
+    check(_lib.load().slx_lora_apply(_dt(y), _ptr(y), _ld(y), _ptr(x), _ld(x), x.shape[0], d_in,
+                                     _ptr(slot_rank), _ptr(slot_scale), slot_rank.numel(),
+                                     max_rank, len(targets), targets, _ptr(ws), ws.numel(),
+                                     _stream()), "slx_lora_apply")
+
+
+def lora_bgmv(y, x, tok_slot, slot_rank, slot_scale, max_rank, targets, ws, d_in=None):
+    d_in = x.shape[1] if d_in is None else d_in
+    check(_lib.load().slx_lora_bgmv(_dt(y), _ptr(y), _ld(y), _ptr(x), _ld(x), _ptr(tok_slot),
+                                    x.shape[0], d_in, _ptr(slot_rank), _ptr(slot_scale),
+                                    slot_rank.numel(), max_rank, len(targets), targets, _ptr(ws),
+                                    ws.numel(), _stream()), "slx_lora_bgmv")
+
+
+def lora_sgmv(y, x, seg_indptr, seg_slot, slot_rank, slot_scale, max_rank, targets, ws,
+              d_in=None):
+    d_in = x.shape[1] if d_in is None else d_in
+    check(_lib.load().slx_lora_sgmv(_dt(y), _ptr(y), _ld(y), _ptr(x), _ld(x), _ptr(seg_indptr),
+                                    _ptr(seg_slot), seg_slot.numel(), x.shape[0], d_in,
+                                    _ptr(slot_rank), _ptr(slot_scale), slot_rank.numel(),
+                                    max_rank, len(targets), targets, _ptr(ws), ws.numel(),
+                                    _stream()), "slx_lora_sgmv")
+
+
+# ---------------------------------------------------------------------------------- K4
+def embedding(out, table, tokens):
+    check(_lib.load().slx_embedding(_dt(out), _ptr(out), _ptr(table), _ptr(tokens), tokens.numel(),
+                                    table.shape[1], table.shape[0], _stream()), "slx_embedding")
+    return out
+
+
+def rmsnorm(out, x, w, eps: float):
+    check(_lib.load().slx_rmsnorm(_dt(out), _ptr(out), _ld(out), _ptr(x), _ld(x), _ptr(w),
+                                  x.shape[0], w.numel(), float(eps), _stream()), "slx_rmsnorm")
+    return out
+
+
+def rope_kv_write(qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos, sin, k_cache, v_cache):
+    check(_lib.load().slx_rope_kv_write(_dt(qkv), _ptr(qkv), _ld(qkv), qkv.shape[0], heads,
+                                        kv_heads, head_dim, _ptr(tok_pos), _ptr(tok_seq),
+                                        _ptr(cos), _ptr(sin), cos.shape[0], _ptr(k_cache),
+                                        _ptr(v_cache), k_cache.shape[2], _stream()),
+          "slx_rope_kv_write")
+
+
+def attention(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, k_cache, v_cache):
+    check(_lib.load().slx_attention(_dt(out), _ptr(out), _ld(out), _ptr(qkv), _ld(qkv),
+                                    qkv.shape[0], heads, kv_heads, head_dim, _ptr(tok_pos),
+                                    _ptr(tok_seq), _ptr(k_cache), _ptr(v_cache), k_cache.shape[2],
+                                    _stream()), "slx_attention")
+    return out
+
+
+def silu_mul_blocked(out, gu, ffn: int):
+    check(_lib.load().slx_silu_mul_blocked(_dt(out), _ptr(out), _ld(out), _ptr(gu), _ld(gu),
+                                           gu.shape[0], ffn, _stream()), "slx_silu_mul_blocked")
+    return out
+
+
+def argmax(out, logits):
+    check(_lib.load().slx_argmax(_dt(logits), _ptr(out), _ptr(logits), _ld(logits),
+                                 logits.shape[0], logits.shape[1], _stream()), "slx_argmax")
+    return out

@@ -1,0 +1,57 @@
+"""CPU: the C-ABI library loads, exports every symbol include/slora_b200.h declares, and
+rejects bad arguments with status codes before touching the device."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2505_14468_b200 import _lib
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
+                      "slora_b200.h")
+
+
+def header_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"SLX_API\s+[\w\s\*]+?\b(slx_\w+)\s*\(", text)))
+
+
+def test_header_declares_symbols():
+    syms = header_symbols()
+    assert len(syms) >= 25
+    assert set(syms) == set(_lib.SIGNATURES), set(syms) ^ set(_lib.SIGNATURES)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    assert lib.slx_abi_version() == 1
+
+
+def test_status_strings():
+    lib = _lib.load()
+    for st in range(0, -7, -1):
+        assert lib.slx_status_string(st).decode() != "unknown status"
+    with pytest.raises(ValueError):
+        _lib.check(_lib.SLX_ERR_INVALID, "x")
+    with pytest.raises(_lib.SlxError):
+        _lib.check(_lib.SLX_ERR_CUDA, "x")
+
+
+def test_argument_validation_without_device():
+    lib = _lib.load()
+    null = None
+    # null operands / bad shapes are rejected before any CUDA call
+    assert lib.slx_gemm_bf16(null, 64, null, null, 64, 0, null, 0, 1, 128, 64, 0, null, 0, null) == -1
+    assert lib.slx_rmsnorm(0, null, 8, null, 8, null, 1, 7, 1e-5, null) == -1
+    assert lib.slx_lora_apply(0, null, 8, null, 8, 1, 8, null, null, 1, 16, 1, None, null, 0, null) == -1
+    assert lib.slx_attention(0, null, 128, null, 384, 1, 1, 1, 128, null, null, null, null, 8, null) == -1
+    assert lib.slx_lora_workspace_bytes(64, 32, 16, 3) > 0
+    assert lib.slx_gemm_workspace_bytes(0, 128, 64, 0) == 0
+    # misaligned pointer
+    buf = (ctypes.c_char * 64)()
+    addr = ctypes.addressof(buf) | 1
+    assert lib.slx_embedding(0, addr, addr, addr, 1, 8, 10, null) == -2

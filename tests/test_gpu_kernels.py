@@ -1,0 +1,232 @@
+"""GPU: each kernel against the oracle (LoRA, ops) or a plain torch fp32 reference (GEMM)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import llama_lora as orc
+from paper_2505_14468_b200 import ops
+from paper_2505_14468_b200._lib import EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def bf(x):
+    return x.to(torch.bfloat16)
+
+
+@pytest.fixture(scope="module")
+def ws():
+    return ops.Workspace(DEV, 64 << 20)
+
+
+# ------------------------------------------------------------------ K1 GEMM
+GEMM_SHAPES = [
+    (1, 128, 64), (7, 256, 128), (16, 4096, 4096), (64, 12288, 4096), (64, 4096, 11008),
+    (100, 384, 688), (128, 1024, 512), (129, 512, 256), (300, 768, 320), (1024, 4096, 4096),
+    (2048, 256, 4096), (64, 32000, 4096),
+]
+
+
+@pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
+def test_gemm_matches_torch_fp32(M, N, K, ws):
+    g = torch.Generator(device=DEV).manual_seed(M * 7 + N + K)
+    a = bf(torch.randn(M, K, device=DEV, generator=g))
+    w = bf(torch.randn(N, K, device=DEV, generator=g) * 0.05)
+    ref = a.float() @ w.float().T
+    out32 = ops.gemm(a, w, out_dtype=torch.float32, ws=ws)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out32, ref, rtol=1e-4, atol=1e-3)   # fp32 out: accumulation order only
+    out = ops.gemm(a, w, ws=ws)
+    torch.testing.assert_close(out.float(), ref, rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("M", [3, 64, 200])
+def test_gemm_residual_inplace(M, ws):
+    N, K = 512, 256
+    g = torch.Generator(device=DEV).manual_seed(M)
+    a = bf(torch.randn(M, K, device=DEV, generator=g))
+    w = bf(torch.randn(N, K, device=DEV, generator=g) * 0.05)
+    x = bf(torch.randn(M, N, device=DEV, generator=g))
+    ref = a.float() @ w.float().T + x.float()
+    ops.gemm(a, w, x, epilogue=EPI_RESIDUAL, residual=x, ws=ws)
+    torch.testing.assert_close(x.float(), ref, rtol=1e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("M", [1, 64, 300])
+def test_gemm_silu_mul_blocked(M, ws):
+    F, K = 384, 256
+    g = torch.Generator(device=DEV).manual_seed(M + 1)
+    a = bf(torch.randn(M, K, device=DEV, generator=g))
+    gate = bf(torch.randn(F, K, device=DEV, generator=g) * 0.05)
+    up = bf(torch.randn(F, K, device=DEV, generator=g) * 0.05)
+    w = torch.stack([gate.view(F // 128, 128, K), up.view(F // 128, 128, K)], 1).reshape(2 * F, K).contiguous()
+    gr, ur = a.float() @ gate.float().T, a.float() @ up.float().T
+    ref = gr * torch.sigmoid(gr) * ur
+    out = ops.gemm(a, w, epilogue=EPI_SILU_MUL, out_dtype=torch.float32, ws=ws)
+    torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-3)
+
+
+def test_gemm_deterministic_split_k(ws):
+    a = bf(torch.randn(64, 4096, device=DEV))
+    w = bf(torch.randn(4096, 4096, device=DEV) * 0.02)
+    o1 = ops.gemm(a, w, out_dtype=torch.float32, ws=ws)
+    o2 = ops.gemm(a, w, out_dtype=torch.float32, ws=ws)
+    assert torch.equal(o1, o2)
+
+
+def test_gemm_f32_parity(ws):
+    a = torch.randn(37, 200, device=DEV)
+    w = bf(torch.randn(72, 200, device=DEV))
+    r = torch.randn(37, 72, device=DEV)
+    out = ops.gemm_f32(a, w, residual=r)
+    ref = (a.double() @ w.double().T + r.double()).float()
+    torch.testing.assert_close(out, ref, rtol=1e-5, atol=1e-4)
+
+
+# ------------------------------------------------------------------ K2/K3 LoRA
+def _adapters(n_slots, ranks, d_in, d_outs, seed):
+    rng = np.random.default_rng(seed)
+    pools = []
+    for d_out in d_outs:
+        A = [rng.standard_normal((r, d_in)).astype(np.float32) / np.sqrt(d_in) for r in ranks]
+        B = [rng.standard_normal((d_out, r)).astype(np.float32) * 0.05 for r in ranks]
+        A = [orc_round(a) for a in A]
+        B = [orc_round(b) for b in B]
+        pools.append((A, B))
+    return pools
+
+
+def orc_round(x):
+    from paper_2505_14468_b200.config import round_to_bf16
+    return round_to_bf16(x)
+
+
+def _targets(pools, d_outs):
+    keep, specs = [], []
+    off = 0
+    for (A, B), d_out in zip(pools, d_outs):
+        At = [torch.from_numpy(a).to(DEV, torch.bfloat16) for a in A]
+        Bt = [torch.from_numpy(b).to(DEV, torch.bfloat16) for b in B]
+        keep += At + Bt
+        ap = torch.tensor([t.data_ptr() for t in At], dtype=torch.int64, device=DEV)
+        bp = torch.tensor([t.data_ptr() for t in Bt], dtype=torch.int64, device=DEV)
+        keep += [ap, bp]
+        specs.append((ap, bp, d_out, off, d_out, d_out))
+        off += d_out
+    return ops.make_targets(specs), keep
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("T,n_slots,d_in,d_outs,ranks", [
+    (64, 32, 4096, (4096, 4096, 4096), [16] * 32),          # config-2 decode shape (q,k,v)
+    (1, 4, 256, (256,), [8] * 4),
+    (37, 6, 512, (384, 128), [8, 16, 64, 8, 16, 64]),       # mixed ranks
+])
+def test_bgmv_matches_oracle(dtype, T, n_slots, d_in, d_outs, ranks):
+    rng = np.random.default_rng(T + n_slots)
+    pools = _adapters(n_slots, ranks, d_in, d_outs, seed=n_slots)
+    tok_slot = rng.integers(-1, n_slots, size=T).astype(np.int32)
+    x = orc_round(rng.standard_normal((T, d_in)).astype(np.float32))
+    y0 = orc_round(rng.standard_normal((T, sum(d_outs))).astype(np.float32))
+    scales = [2.0 + 0.25 * s for s in range(n_slots)]
+    ref = y0.copy()
+    off = 0
+    for (A, B), d_out in zip(pools, d_outs):
+        ref[:, off:off + d_out] = orc.bgmv(y0[:, off:off + d_out], x, A, B, scales, tok_slot)
+        off += d_out
+    targets, keep = _targets(pools, d_outs)
+    xd = torch.from_numpy(x).to(DEV, dtype)
+    yd = torch.from_numpy(y0).to(DEV, dtype)
+    rank = torch.tensor(ranks, dtype=torch.int32, device=DEV)
+    scale = torch.tensor(scales, dtype=torch.float32, device=DEV)
+    wsb = torch.zeros(ops.lora_workspace_bytes(T, n_slots, 64, len(d_outs)), dtype=torch.uint8, device=DEV)
+    ops.lora_bgmv(yd, xd, torch.from_numpy(tok_slot).to(DEV), rank, scale, 64, targets, wsb)
+    got = yd.float().cpu().numpy()
+    if dtype == torch.float32:
+        np.testing.assert_allclose(got, ref, rtol=1e-5, atol=1e-5)
+    else:
+        np.testing.assert_allclose(got, ref, rtol=2e-2, atol=3e-2)
+        # untouched rows (slot -1) stay bit-identical
+        none = tok_slot < 0
+        assert np.array_equal(got[none], y0[none])
+
+
+@pytest.mark.parametrize("seg_lens", [[5, 0, 17, 1, 33], [2048, 2048], [1]])
+def test_sgmv_matches_oracle(seg_lens):
+    rng = np.random.default_rng(len(seg_lens))
+    n_slots, d_in, d_out = 5, 640, 512
+    ranks = [8, 16, 64, 16, 8]
+    pools = _adapters(n_slots, ranks, d_in, (d_out,), seed=3)
+    T = sum(seg_lens)
+    seg_indptr = np.concatenate([[0], np.cumsum(seg_lens)]).astype(np.int32)
+    seg_slot = np.asarray([(i * 2) % n_slots for i in range(len(seg_lens))], np.int32)
+    x = orc_round(rng.standard_normal((T, d_in)).astype(np.float32))
+    y0 = rng.standard_normal((T, d_out)).astype(np.float32)
+    scales = [1.0, 2.0, 0.5, 1.5, 3.0]
+    A, B = pools[0]
+    ref = orc.sgmv(y0, x, A, B, scales, seg_indptr, seg_slot)
+    targets, keep = _targets(pools, (d_out,))
+    yd = torch.from_numpy(y0).to(DEV)
+    wsb = torch.zeros(ops.lora_workspace_bytes(T, n_slots, 64, 1), dtype=torch.uint8, device=DEV)
+    ops.lora_sgmv(yd, torch.from_numpy(x).to(DEV), torch.from_numpy(seg_indptr).to(DEV),
+                  torch.from_numpy(seg_slot).to(DEV), torch.tensor(ranks, dtype=torch.int32, device=DEV),
+                  torch.tensor(scales, device=DEV), 64, targets, wsb)
+    np.testing.assert_allclose(yd.cpu().numpy(), ref, rtol=1e-4, atol=1e-4)
+
+
+# ------------------------------------------------------------------ K4 ops
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_rmsnorm_embedding_argmax(dtype):
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((9, 4096)).astype(np.float32)
+    w = orc_round(1 + 0.1 * rng.standard_normal(4096).astype(np.float32))
+    out = torch.empty(9, 4096, dtype=dtype, device=DEV)
+    xd = torch.from_numpy(x).to(DEV, dtype)
+    ops.rmsnorm(out, xd, torch.from_numpy(w).to(DEV, torch.bfloat16), 1e-5)
+    ref = orc.rmsnorm(xd.float().cpu().numpy(), w, 1e-5)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    np.testing.assert_allclose(out.float().cpu().numpy(), ref, rtol=tol, atol=tol)
+    table = orc_round(rng.standard_normal((100, 256)).astype(np.float32))
+    toks = np.array([3, 99, 0, 3], np.int32)
+    e = torch.empty(4, 256, dtype=dtype, device=DEV)
+    ops.embedding(e, torch.from_numpy(table).to(DEV, torch.bfloat16), torch.from_numpy(toks).to(DEV))
+    assert np.array_equal(e.float().cpu().numpy(), table[toks])
+    lg = rng.standard_normal((5, 32000)).astype(np.float32)
+    lg[2, 7] = lg[2, 9] = 100.0  # tie -> lowest index
+    am = torch.empty(5, dtype=torch.int32, device=DEV)
+    ops.argmax(am, torch.from_numpy(lg).to(DEV))
+    assert am.cpu().numpy().tolist() == np.argmax(lg, -1).tolist()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("H,Hkv,D", [(4, 4, 64), (8, 2, 128)])
+def test_rope_kv_attention_match_oracle(dtype, H, Hkv, D):
+    rng = np.random.default_rng(H + D)
+    lens = [1, 13, 70, 200]       # one prefill chunk per sequence, ragged
+    T = sum(lens)
+    max_ctx = 256
+    qkv = rng.standard_normal((T, (H + 2 * Hkv) * D)).astype(np.float32)
+    pos = np.concatenate([np.arange(L) for L in lens]).astype(np.int32)
+    seq = np.concatenate([[s] * L for s, L in enumerate(lens)]).astype(np.int32)
+    cos, sin = orc.rope_table(max_ctx, D, 10000.0)
+    kc = torch.zeros(len(lens), Hkv, max_ctx, D, dtype=dtype, device=DEV)
+    vc = torch.zeros_like(kc)
+    qd = torch.from_numpy(qkv).to(DEV, dtype)
+    qkv_r = qd.float().cpu().numpy()
+    ops.rope_kv_write(qd, H, Hkv, D, torch.from_numpy(pos).to(DEV), torch.from_numpy(seq).to(DEV),
+                      torch.from_numpy(cos).to(DEV), torch.from_numpy(sin).to(DEV), kc, vc)
+    out = torch.empty(T, H * D, dtype=dtype, device=DEV)
+    ops.attention(out, qd, H, Hkv, D, torch.from_numpy(pos).to(DEV), torch.from_numpy(seq).to(DEV), kc, vc)
+    q = orc.apply_rope(qkv_r[:, :H * D].reshape(T, H, D), pos, cos, sin)
+    k = orc.apply_rope(qkv_r[:, H * D:(H + Hkv) * D].reshape(T, Hkv, D), pos, cos, sin)
+    v = qkv_r[:, (H + Hkv) * D:].reshape(T, Hkv, D)
+    ref = np.empty((T, H, D), np.float32)
+    o = 0
+    for L in lens:
+        ref[o:o + L] = orc.attention(q[o:o + L], k[o:o + L], v[o:o + L], np.arange(L))
+        o += L
+    tol = 2e-5 if dtype == torch.float32 else 3e-2
+    np.testing.assert_allclose(out.float().cpu().numpy(), ref.reshape(T, -1), rtol=tol, atol=tol)
+    np.testing.assert_allclose(kc[1, :, :13].float().cpu().numpy().transpose(1, 0, 2), k[1:14], rtol=tol, atol=tol)
