@@ -1,0 +1,377 @@
+"""Benchmark: multi-LoRA decode tokens/s/GPU on the Llama-2-7B shape (BASELINE.json config 2).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one mixed-adapter decode step of 64 sequences (32 rank-16 adapters on
+q,k,v,o, per-token adapter ids uniform with seed 0) at context 128 over the full
+32-layer 7B-shape bf16 backbone (random init, synthetic tokens), lm_head and greedy
+argmax included.  Each GPU runs an independent replica (data parallel, no collective
+in the step); rank 0 prints one JSON line.  Timing: CUDA events on the launching
+stream, barrier + synchronize on both sides, max over ranks.  The 13.5 GB of weights
+streamed every step exceed the 126 MB L2, so no flush is needed between steps.
+
+--impl reference times the oracle port (oracle/llama_lora.py, numpy fp32 on all host
+cores) on a bounded sample (one 7B decoder layer at the same batch/context + lm_head,
+extrapolated x32) — the reference (slorasim) has no forward of its own.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "multi-LoRA decode tokens/s (Llama-2-7B shape, 32 x r16 adapters, batch 64, ctx 128)"
+UNIT = "tokens/s"
+BATCH, N_ADAPTERS, RANK, ALPHA, CTX = 64, 32, 16, 32.0, 128
+WORKLOAD = "config2: llama2-7b-shape bf16 decode, 32 x r16 LoRA (q,k,v,o), batch 64, ctx 128"
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def tok_slots(n=BATCH, n_adapters=N_ADAPTERS, seed=0):
+    return np.random.default_rng(seed).integers(0, n_adapters, size=n).astype(np.int32)
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ CPU oracle
+class CpuOracleSample:
+    """One 7B decoder layer (+ embedding, final norm) and lm_head of the numpy fp32 oracle
+    at batch 64 / ctx 128 with 32 r16 adapters on q,k,v,o; a step extrapolates the layer x32."""
+
+    def __init__(self, seed=0):
+        from oracle.llama_lora import OracleModel
+        from paper_2505_14468_b200.config import LLAMA2_7B, BackboneConfig
+
+        full = self.full = LLAMA2_7B
+        cfg1 = BackboneConfig("7b-one-layer", full.hidden, 1, full.heads, full.kv_heads,
+                              full.head_dim, full.ffn, full.vocab)
+        rng = np.random.default_rng(seed)
+        f32 = np.float32
+
+        def rn(*shape, s=0.02):
+            return rng.standard_normal(shape, dtype=f32) * f32(s)
+
+        d = cfg1.hidden
+        w = {"embed": rn(cfg1.vocab, d, s=1.0), "final_norm": np.ones(d, f32),
+             "lm_head": rn(cfg1.vocab, d), "layers.0.input_norm": np.ones(d, f32),
+             "layers.0.post_norm": np.ones(d, f32), "layers.0.wq": rn(d, d),
+             "layers.0.wk": rn(d, d), "layers.0.wv": rn(d, d), "layers.0.wo": rn(d, d),
+             "layers.0.w_gate": rn(cfg1.ffn, d), "layers.0.w_up": rn(cfg1.ffn, d),
+             "layers.0.w_down": rn(d, cfg1.ffn)}
+        ads = []
+        for _ in range(N_ADAPTERS):
+            ad = {}
+            for t in ("q", "k", "v", "o"):
+                ad[f"layers.0.{t}.A"] = rn(RANK, d, s=1 / np.sqrt(d))
+                ad[f"layers.0.{t}.B"] = rn(d, RANK)
+            ads.append(ad)
+        self.m = OracleModel(cfg1, w, ads, [ALPHA / RANK] * N_ADAPTERS, ("q", "k", "v", "o"),
+                             max_pos=CTX + 8)
+        for _ in range(BATCH):
+            self.m.kv.append([(rn(CTX, cfg1.kv_heads, cfg1.head_dim, s=1.0),
+                               rn(CTX, cfg1.kv_heads, cfg1.head_dim, s=1.0))])
+        self.slots = tok_slots()
+        self.toks = rng.integers(1, cfg1.vocab, size=BATCH)
+        self.cores = len(os.sched_getaffinity(0))
+        self.sample = (f"numpy fp32 oracle on {self.cores} host threads: 1 of 32 decoder layers "
+                       f"(batch {BATCH}, ctx {CTX}, {N_ADAPTERS} r{RANK} adapters on q,k,v,o) + "
+                       f"lm_head per step; layer time x32 extrapolated")
+
+    def step_seconds(self) -> float:
+        m = self.m
+        for s in range(BATCH):  # rewind to context CTX (constant attended length)
+            kc, vc = m.kv[s][0]
+            m.kv[s][0] = (kc[:CTX], vc[:CTX])
+        t0 = time.perf_counter()
+        h = m._forward(self.toks, np.full(BATCH, CTX), np.arange(BATCH + 1), self.slots,
+                       list(range(BATCH)))
+        t1 = time.perf_counter()
+        m.logits(h)
+        t2 = time.perf_counter()
+        return self.full.layers * (t1 - t0) + (t2 - t1)
+
+
+def cpu_baseline_line(min_seconds=10.0):
+    smp = CpuOracleSample()
+    smp.step_seconds()
+    times, t0 = [], time.perf_counter()
+    while time.perf_counter() - t0 < min_seconds or len(times) < 3:
+        times.append(smp.step_seconds())
+    v = BATCH / statistics.median(times)
+    return {"value": v, "unit": UNIT, "cores": smp.cores, "kind": "port",
+            "sample": smp.sample + f", median of {len(times)} steps"}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    smp = CpuOracleSample()
+    for _ in range(args.warmup):
+        smp.step_seconds()
+    t0 = time.perf_counter()
+    times = [smp.step_seconds() for _ in range(args.steps)]
+    elapsed = time.perf_counter() - t0
+    value = BATCH * len(times) / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * BATCH / value, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (random init, seed 0)",
+            "config": {"workload": WORKLOAD, "batch": BATCH, "ctx": CTX, "adapters": N_ADAPTERS,
+                       "rank": RANK, "host_wall_s": round(elapsed, 2)},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": smp.cores, "kind": "port",
+                             "sample": smp.sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------ ours
+def algorithmic_bytes(cfg, slots):
+    """Per-step algorithmic bytes by kernel class (SURVEY.md §8d definitions)."""
+    B, d, qd, kvd, f = BATCH, cfg.hidden, cfg.q_dim, cfg.kv_dim, cfg.ffn
+    gemm = 0
+    for (N, K, n_out, res) in [(qd + 2 * kvd, d, qd + 2 * kvd, 0), (d, qd, d, 1),
+                               (2 * f, d, f, 0), (d, f, d, 1)]:
+        gemm += N * K * 2 + B * K * 2 + B * n_out * 2 + res * B * n_out * 2
+    gemm *= cfg.layers
+    gemm += cfg.vocab * d * 2 + B * d * 2 + B * cfg.vocab * 4      # lm_head (fp32 logits)
+    distinct = len(set(slots.tolist()))
+    lora = 0
+    for t, (di, do) in {"q": (d, qd), "k": (d, kvd), "v": (d, kvd), "o": (qd, d)}.items():
+        lora += distinct * RANK * (di + do) * 2 + B * di * 2 + 2 * B * do * 2
+    lora *= cfg.layers
+    attn = cfg.layers * (B * (CTX + 1) * 2 * kvd * 2 + B * (qd + 2 * kvd) * 2 + B * qd * 2)
+    return {"gemm": gemm, "lora": lora, "attention": attn}, distinct
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_14468_b200 import ops
+    from paper_2505_14468_b200._lib import load
+    from paper_2505_14468_b200.config import LLAMA2_7B, LoraConfig
+    from paper_2505_14468_b200.engine import DecodeGraph
+    from paper_2505_14468_b200.model import MultiLoraModel
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    load()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg = LLAMA2_7B
+    lora = LoraConfig(RANK, ALPHA, ("q", "k", "v", "o"))
+    m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=BATCH, max_ctx=CTX + 1,
+                       n_slots=N_ADAPTERS, max_rank=RANK, max_tokens=BATCH)
+    m.random_backbone(seed=rank)
+    for a in range(N_ADAPTERS):
+        m.pool.load_random(a, lora, seed=1000 + a)
+    g = torch.Generator(device=m.device).manual_seed(7)
+    for l in range(cfg.layers):   # context of 128 resident tokens per sequence
+        m.k_cache[l].normal_(generator=g)
+        m.v_cache[l].normal_(generator=g)
+    seqs = [m.alloc_seq() for _ in range(BATCH)]
+    slots = tok_slots()
+    dg = DecodeGraph(m, seqs, slots.tolist(), fixed_pos=CTX)
+    dg.tok.copy_(torch.randint(1, cfg.vocab, (BATCH,), generator=g, device=m.device, dtype=torch.int32))
+    dg.capture()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=m.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up + timed device loop (tokens fed back on device)
+    for _ in range(args.warmup):
+        dg.replay()
+        dg.feed_back()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            dg.replay()
+            dg.feed_back()
+        ev1.record(stream)
+        barrier()
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    value = world * BATCH * args.steps / (t_ms / 1000.0)
+    launches = dg.kernels_per_step * args.steps
+
+    # ---- end to end through host buffers (H2D inputs, D2H sampled tokens every step)
+    h_tok = np.random.default_rng(1).integers(1, cfg.vocab, size=BATCH).astype(np.int32)
+    for _ in range(2):
+        h_tok = dg.step_host(h_tok, slots).copy()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        h_tok = dg.step_host(h_tok, slots).copy()
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_value = world * BATCH * args.steps / (e2e_ms / 1000.0)
+
+    # ---- per-kernel-class device time (events around each op, gap-free queue behind a sleep)
+    with ops.KernelTimer() as kt:
+        torch.cuda._sleep(400_000_000)
+        dg._step()
+    torch.cuda.synchronize()
+    dur = kt.durations()
+    step_ms_instr = sum(v[0] for v in dur.values())
+    abytes, distinct = algorithmic_bytes(cfg, slots)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    kernels = {}
+    for cat, (ms, n, _) in sorted(dur.items(), key=lambda kv: -kv[1][0]):
+        e = {"ms_per_step": round(ms, 4), "launches": n, "share": round(ms / step_ms_instr, 4)}
+        if cat in abytes:
+            gbs = abytes[cat] / (ms / 1000.0) / 1e9
+            e.update({"GB/s": round(gbs, 1), "frac_hbm": round(gbs / hbm_peak, 4),
+                      "bytes_per_step": abytes[cat]})
+        kernels[cat] = e
+    gemm_ms, gemm_n, _ = dur["gemm"]
+    gemm_gbs = abytes["gemm"] / (gemm_ms / 1000.0) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("gemm_tc_kernel_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {"bound": "hbm", "achieved": round(gemm_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(gemm_gbs / hbm_peak, 4), "traffic": traffic,
+                "kernel": "gemm_tc_kernel<SWAP> (tcgen05 swap-AB split-K decode GEMM)",
+                "bytes_per_launch": abytes["gemm"] / gemm_n, "peak_source": peak_src}
+    lora_ms = dur.get("lora", (0.0, 1, []))[0]
+    lora_gbs = abytes["lora"] / (lora_ms / 1000.0) / 1e9 if lora_ms else None
+
+    cpu_baseline = cpu_baseline_line() if (world == 1 and not args.no_cpu_baseline) else None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init 7B-shape weights and adapters, random tokens)",
+            "config": {"workload": WORKLOAD, "batch_per_gpu": BATCH, "global_batch": BATCH * world,
+                       "ctx": CTX, "adapters": N_ADAPTERS, "distinct_adapters_in_batch": distinct,
+                       "rank": RANK, "lora_targets": "q,k,v,o", "parallelism": f"dp{world} (replicas)",
+                       "l2": "inputs > L2: 13.5 GB weights + 4.3 GB KV streamed per step",
+                       "cuda_graph": True, "kernels_per_step": dg.kernels_per_step},
+            "tokens_per_s_per_gpu": value / world,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": dg.h2d_bytes(),
+                    "d2h_bytes_per_step": dg.d2h_bytes()},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "lora_kernels": {"GB/s": None if lora_gbs is None else round(lora_gbs, 1),
+                             "frac_hbm": None if lora_gbs is None else round(lora_gbs / hbm_peak, 4),
+                             "bytes_per_step": abytes["lora"], "ms_per_step": round(lora_ms, 4)},
+            "kernels": kernels,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu_baseline,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the CPU oracle leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

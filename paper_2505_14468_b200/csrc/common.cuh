@@ -24,6 +24,9 @@ using bf16 = __nv_bfloat16;
   do {                                                                   \
     if ((reinterpret_cast<uintptr_t>(ptr) % (n)) != 0) return SLX_ERR_ALIGN; \
   } while (0)
+// Clear a stale (non-sticky) error left by an earlier unrelated runtime call so that the
+// check after our launch reports only our launch.
+#define SLX_CLEAR_STALE() (void)cudaGetLastError()
 #define SLX_LAUNCH_CHECK()                                   \
   do {                                                       \
     cudaError_t _e = cudaGetLastError();                     \

@@ -25,6 +25,7 @@ constexpr int TC_THREADS = 128;
 constexpr int TC_BK = 64;  // 64 bf16 = one 128-byte swizzle row
 constexpr int TC_MAX_STAGES = 8;
 constexpr int P_TILE_BYTES = 128 * TC_BK * 2;  // 16 KB
+constexpr size_t TC_CNT_BYTES = 64 * 1024;     // split-K tile counters (<= 16384 tiles)
 
 struct GemmArgs {
   int M, N, K;
@@ -289,6 +290,10 @@ static GemmPlan plan_gemm(int M, int N, int K, int epi) {
     p.nsub = (epi == SLX_EPI_SILU_MUL) ? 2 : 1;
     const int stage = p.nsub * P_TILE_BYTES + p.bn * TC_BK * 2;
     p.n_tiles = ceil_div(N, 128 * p.nsub);
+    if (p.n_tiles > (int)(TC_CNT_BYTES / 4)) {  // rejected by the caller
+      p.n_tiles = -1;
+      return p;
+    }
     const size_t two_cta_budget = 112 * 1024 - 1024 - bar_bytes;
     int st2 = (int)(two_cta_budget / stage);
     int ctas_per_sm;
@@ -309,7 +314,9 @@ static GemmPlan plan_gemm(int M, int N, int K, int epi) {
     p.splits = s;
     p.smem = (size_t)p.stages * stage + bar_bytes + 1024;
     p.part_bytes = p.splits > 1 ? (size_t)p.splits * p.n_tiles * p.nsub * p.bn * 128 * 4 : 0;
-    p.cnt_bytes = p.splits > 1 ? (size_t)((p.n_tiles * 4 + 255) / 256) * 256 : 0;
+    // fixed-size counter region at the head of ws, independent of the shape, so counters of
+    // one call are never overlapped by another call's partial tiles (they stay zero)
+    p.cnt_bytes = p.splits > 1 ? TC_CNT_BYTES : 0;
   } else {
     p.bn = 256;
     p.nsub = 1;
@@ -327,13 +334,14 @@ template <bool SWAP, int EPI, typename OutT>
 static int launch_tc(const CUtensorMap& mp, const CUtensorMap& mq, const GemmArgs& a, dim3 grid,
                      size_t smem, cudaStream_t s) {
   auto k = gemm_tc_kernel<SWAP, EPI, OutT>;
-  static bool configured = false;  // per instantiation; attribute is per-function, set once
-  if (!configured) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+  static size_t configured = 0;  // per instantiation: largest dynamic smem opted into so far
+  if (smem > configured) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return SLX_ERR_CUDA;
-    configured = true;
+    configured = smem;
   }
+  SLX_CLEAR_STALE();
   k<<<grid, TC_THREADS, smem, s>>>(mp, mq, a);
   SLX_LAUNCH_CHECK();
   return SLX_OK;
@@ -381,6 +389,7 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= N);
   if (M == 0) return SLX_OK;
   GemmPlan p = plan_gemm(M, N, K, epilogue);
+  if (p.n_tiles <= 0) return SLX_ERR_UNSUPPORTED;
   const size_t need = p.cnt_bytes + p.part_bytes;
   if (need > 0) {
     if (!ws || ws_bytes < need) return SLX_ERR_WORKSPACE;

@@ -310,6 +310,7 @@ extern "C" int slx_lora_plan_tokens(const int32_t* tok_slot, int n_tok, int n_sl
   // plan only touches the header/perm/tiles region, which does not depend on rank/targets
   int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
   if (st) return st;
+  SLX_CLEAR_STALE();
   plan_tokens_kernel<<<1, PLAN_THREADS, 0, (cudaStream_t)stream>>>(tok_slot, n_tok, n_slots, w);
   SLX_LAUNCH_CHECK();
   return SLX_OK;
@@ -323,6 +324,7 @@ extern "C" int slx_lora_plan_segments(const int32_t* seg_indptr, const int32_t* 
   LoraWs w;
   int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
   if (st) return st;
+  SLX_CLEAR_STALE();
   plan_segments_kernel<<<1, PLAN_THREADS, 0, (cudaStream_t)stream>>>(seg_indptr, seg_slot, n_seg,
                                                                      n_tok, n_slots, w);
   SLX_LAUNCH_CHECK();
@@ -367,13 +369,17 @@ extern "C" int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ld
   dim3 gs((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)ks);
   dim3 ge((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)n_split);
   if (dtype == SLX_DT_BF16) {
+    SLX_CLEAR_STALE();
     lora_shrink_kernel<bf16><<<gs, 256, 0, s>>>((const bf16*)x, ldx, n_tok, d_in, ks, slot_rank,
                                                 max_rank, ta, w);
+    SLX_CLEAR_STALE();
     lora_expand_kernel<bf16><<<ge, 256, 0, s>>>((bf16*)y, ldy, n_tok, ks, n_split, slot_rank,
                                                 slot_scale, max_rank, ta, w);
   } else if (dtype == SLX_DT_F32) {
+    SLX_CLEAR_STALE();
     lora_shrink_kernel<float><<<gs, 256, 0, s>>>((const float*)x, ldx, n_tok, d_in, ks, slot_rank,
                                                  max_rank, ta, w);
+    SLX_CLEAR_STALE();
     lora_expand_kernel<float><<<ge, 256, 0, s>>>((float*)y, ldy, n_tok, ks, n_split, slot_rank,
                                                  slot_scale, max_rank, ta, w);
   } else {

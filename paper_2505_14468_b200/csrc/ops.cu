@@ -284,6 +284,7 @@ using namespace slx;
 
 // ================================================================== C ABI
 #define DISPATCH_DT(dtype, ...)                      \
+  SLX_CLEAR_STALE();                                 \
   do {                                               \
     if ((dtype) == SLX_DT_BF16) {                    \
       using T = bf16;                                \
@@ -402,6 +403,7 @@ extern "C" int slx_gemm_f32(const void* A, int lda, const void* W, void* C, int 
   }
   if (M == 0) return SLX_OK;
   dim3 grid((unsigned)ceil_div(N, SG_BN), (unsigned)ceil_div(M, SG_BM));
+  SLX_CLEAR_STALE();
   gemm_f32_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
       (const float*)A, lda, (const bf16*)W, (float*)C, ldc,
       epilogue == SLX_EPI_RESIDUAL ? (const float*)R : nullptr, ldr, M, N, K);

@@ -25,6 +25,13 @@ from ._lib import EPI_RESIDUAL, EPI_SILU_MUL
 from .config import ATTN_TARGETS, BackboneConfig, LoraConfig
 
 
+def resolve_device(device) -> torch.device:
+    d = torch.device(device)
+    if d.type == "cuda" and d.index is None:
+        d = torch.device("cuda", torch.cuda.current_device())
+    return d
+
+
 def _round_up(x: int, m: int) -> int:
     return (x + m - 1) // m * m
 
@@ -49,7 +56,7 @@ class AdapterPool:
     def __init__(self, cfg: BackboneConfig, targets, n_slots: int, max_rank: int, device):
         self.cfg, self.targets = cfg, tuple(targets)
         self.n_slots, self.max_rank = n_slots, max_rank
-        self.device = torch.device(device)
+        self.device = resolve_device(device)
         L, nt = cfg.layers, len(self.targets)
         self.a_ptr = torch.zeros((L, nt, n_slots), dtype=torch.int64, device=self.device)
         self.b_ptr = torch.zeros((L, nt, n_slots), dtype=torch.int64, device=self.device)
@@ -140,7 +147,7 @@ class MultiLoraModel:
         if dtype not in (torch.bfloat16, torch.float32):
             raise ValueError("dtype must be bf16 (throughput) or fp32 (parity)")
         self.cfg, self.dtype = cfg, dtype
-        self.device = torch.device(device)
+        self.device = resolve_device(device)
         self.max_seqs, self.max_ctx, self.max_tokens = max_seqs, max_ctx, max_tokens
         self.targets = tuple(lora_targets)
         self.ffn_pad = _round_up(cfg.ffn, 128)

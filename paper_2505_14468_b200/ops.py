@@ -16,6 +16,60 @@ from ._lib import DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, LoraTar
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
 
+# ------------------------------------------------------------------ launch accounting / timing
+_LAUNCHES = 0
+_TIMER = None   # optional KernelTimer: CUDA events around every op, by category
+
+
+def launch_count() -> int:
+    """Number of libslora_b200 kernel launches issued through this module so far."""
+    return _LAUNCHES
+
+
+class KernelTimer:
+    """Records a CUDA event pair around each op on the current stream; durations are read
+    after a synchronize.  Used by bench.py for per-kernel-class roofline numbers."""
+
+    def __init__(self):
+        self.records = []   # (category, start_event, end_event, meta)
+
+    def __enter__(self):
+        global _TIMER
+        _TIMER = self
+        return self
+
+    def __exit__(self, *exc):
+        global _TIMER
+        _TIMER = None
+
+    def durations(self):
+        out = {}
+        for cat, a, b, meta in self.records:
+            ms, n, metas = out.get(cat, (0.0, 0, []))
+            out[cat] = (ms + a.elapsed_time(b), n + 1, metas + [meta])
+        return out
+
+
+def _op(category: str, n_launch: int = 1):
+    def deco(fn):
+        def wrapped(*args, **kwargs):
+            global _LAUNCHES
+            _LAUNCHES += n_launch
+            if _TIMER is None:
+                return fn(*args, **kwargs)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            out = fn(*args, **kwargs)
+            b.record()
+            meta = tuple(tuple(x.shape) for x in args if isinstance(x, torch.Tensor))
+            _TIMER.records.append((category, a, b, meta))
+            return out
+        wrapped.__name__ = fn.__name__
+        wrapped.__doc__ = fn.__doc__
+        return wrapped
+    return deco
+
 
 def _dt(t: torch.Tensor) -> int:
     try:
@@ -56,6 +110,7 @@ class Workspace:
 
 
 # ---------------------------------------------------------------------------------- K1
+@_op("gemm", 1)
 def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None, *,
          epilogue: int = EPI_NONE, residual: torch.Tensor | None = None,
          out_dtype: torch.dtype | None = None, ws: Workspace | None = None) -> torch.Tensor:
@@ -83,6 +138,7 @@ def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None, *,
     return out
 
 
+@_op("gemm", 1)
 def gemm_f32(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None, *,
              residual: torch.Tensor | None = None) -> torch.Tensor:
     """fp32-parity GEMM: fp32 activations x bf16 weights (upcast exactly), fp32 out."""
@@ -104,11 +160,13 @@ def lora_workspace_bytes(n_tok: int, n_slots: int, max_rank: int, n_targets: int
     return _lib.load().slx_lora_workspace_bytes(n_tok, n_slots, max_rank, n_targets)
 
 
+@_op("lora_plan", 1)
 def lora_plan_tokens(tok_slot: torch.Tensor, n_slots: int, ws: torch.Tensor) -> None:
     check(_lib.load().slx_lora_plan_tokens(_ptr(tok_slot), tok_slot.numel(), n_slots, _ptr(ws),
                                            ws.numel(), _stream()), "slx_lora_plan_tokens")
 
 
+@_op("lora_plan", 1)
 def lora_plan_segments(seg_indptr: torch.Tensor, seg_slot: torch.Tensor, n_tok: int,
                        n_slots: int, ws: torch.Tensor) -> None:
     check(_lib.load().slx_lora_plan_segments(_ptr(seg_indptr), _ptr(seg_slot), seg_slot.numel(),
@@ -125,6 +183,7 @@ def make_targets(specs) -> ctypes.Array:
     return arr
 
 
+@_op("lora", 2)
 def lora_apply(y: torch.Tensor, x: torch.Tensor, d_in: int, slot_rank: torch.Tensor,
                slot_scale: torch.Tensor, max_rank: int, targets, ws: torch.Tensor) -> None:
     """y[t, col(n)] += scale * (x[t, :d_in] A^T) B^T over the plan stored in ws."""
@@ -136,6 +195,7 @@ def lora_apply(y: torch.Tensor, x: torch.Tensor, d_in: int, slot_rank: torch.Ten
                                      _stream()), "slx_lora_apply")
 
 
+@_op("lora", 3)
 def lora_bgmv(y, x, tok_slot, slot_rank, slot_scale, max_rank, targets, ws, d_in=None):
     d_in = x.shape[1] if d_in is None else d_in
     check(_lib.load().slx_lora_bgmv(_dt(y), _ptr(y), _ld(y), _ptr(x), _ld(x), _ptr(tok_slot),
@@ -144,6 +204,7 @@ def lora_bgmv(y, x, tok_slot, slot_rank, slot_scale, max_rank, targets, ws, d_in
                                     ws.numel(), _stream()), "slx_lora_bgmv")
 
 
+@_op("lora", 3)
 def lora_sgmv(y, x, seg_indptr, seg_slot, slot_rank, slot_scale, max_rank, targets, ws,
               d_in=None):
     d_in = x.shape[1] if d_in is None else d_in
@@ -155,18 +216,21 @@ def lora_sgmv(y, x, seg_indptr, seg_slot, slot_rank, slot_scale, max_rank, targe
 
 
 # ---------------------------------------------------------------------------------- K4
+@_op("embedding", 1)
 def embedding(out, table, tokens):
     check(_lib.load().slx_embedding(_dt(out), _ptr(out), _ptr(table), _ptr(tokens), tokens.numel(),
                                     table.shape[1], table.shape[0], _stream()), "slx_embedding")
     return out
 
 
+@_op("rmsnorm", 1)
 def rmsnorm(out, x, w, eps: float):
     check(_lib.load().slx_rmsnorm(_dt(out), _ptr(out), _ld(out), _ptr(x), _ld(x), _ptr(w),
                                   x.shape[0], w.numel(), float(eps), _stream()), "slx_rmsnorm")
     return out
 
 
+@_op("rope_kv", 1)
 def rope_kv_write(qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos, sin, k_cache, v_cache):
     check(_lib.load().slx_rope_kv_write(_dt(qkv), _ptr(qkv), _ld(qkv), qkv.shape[0], heads,
                                         kv_heads, head_dim, _ptr(tok_pos), _ptr(tok_seq),
@@ -175,6 +239,7 @@ def rope_kv_write(qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos, sin, k_
           "slx_rope_kv_write")
 
 
+@_op("attention", 1)
 def attention(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, k_cache, v_cache):
     check(_lib.load().slx_attention(_dt(out), _ptr(out), _ld(out), _ptr(qkv), _ld(qkv),
                                     qkv.shape[0], heads, kv_heads, head_dim, _ptr(tok_pos),
@@ -183,12 +248,14 @@ def attention(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, k_cache, v_
     return out
 
 
+@_op("silu_mul", 1)
 def silu_mul_blocked(out, gu, ffn: int):
     check(_lib.load().slx_silu_mul_blocked(_dt(out), _ptr(out), _ld(out), _ptr(gu), _ld(gu),
                                            gu.shape[0], ffn, _stream()), "slx_silu_mul_blocked")
     return out
 
 
+@_op("argmax", 1)
 def argmax(out, logits):
     check(_lib.load().slx_argmax(_dt(logits), _ptr(out), _ptr(logits), _ld(logits),
                                  logits.shape[0], logits.shape[1], _stream()), "slx_argmax")
