@@ -6,6 +6,8 @@
 // (/root/reference/pkg/src/slorasim/engine.py:1040-1053, ArtifactSpec core.py:56-78), with
 // real transfers whose measured time calibrates ArtifactSpec.load_from_container_ms.
 #include <nccl.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
 
@@ -19,6 +21,14 @@ int sm_count() {
       n = 148;
   }
   return n;
+}
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SLX_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 }  // namespace slx
 

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/slora_b200.h"
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -93,5 +95,51 @@ __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; 
 
 // Cached per-device attributes (read once; no other global mutable state).
 int sm_count();
+
+}  // namespace slx
+
+// ---------------------------------------------------------------- launch plumbing (PDL + clusters)
+namespace slx {
+
+// Programmatic dependent launch: every kernel of the library calls pdl_wait() before it
+// touches global memory produced or consumed by earlier kernels on the stream, and
+// pdl_trigger() once its own CTAs are resident, so the next kernel's prologue (barrier
+// init, TMEM alloc, weight prefetch) overlaps this kernel's tail.  Both are no-ops when the
+// kernel was launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // SLX_PDL=0 disables (debug)
+
+template <typename... KArgs, typename... Args>
+inline int launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t stream, unsigned cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  unsigned n = 0;
+  if (pdl_enabled()) {
+    attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    attrs[n].id = cudaLaunchAttributeClusterDimension;
+    attrs[n].val.clusterDim.x = cluster_x;
+    attrs[n].val.clusterDim.y = 1;
+    attrs[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = n;
+  (void)cudaGetLastError();
+  if (cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...) != cudaSuccess) return SLX_ERR_CUDA;
+  return cudaGetLastError() == cudaSuccess ? SLX_OK : SLX_ERR_CUDA;
+}
 
 }  // namespace slx

@@ -5,10 +5,14 @@
 // Two tilings of one warp-specialised kernel (warp 0 lane 0: TMA producer, warp 1 lane 0:
 // MMA issuer, all 4 warps: TMEM -> register epilogue):
 //  * NORMAL (prefill, M > 128): D tile = 128 rows of A x BN rows of W, TMEM lane = token.
-//  * SWAP   (decode,  M <= 128): D tile = 128 rows of W x BN(=M padded to 16) tokens,
-//    TMEM lane = output feature.  The weight stream is split along K over `splits` CTAs
-//    so that all 148 SMs pull weights; partial tiles are reduced deterministically by the
-//    last-arriving CTA (tile counter, split order 0..S-1), which applies the epilogue.
+//  * SWAP   (decode,  M <= 128): D tile = 128 rows of W x BN (= M padded to 16) tokens;
+//    TMEM lane = output feature.  The weight stream of one tile is split along K over the
+//    S CTAs of a thread-block CLUSTER (S <= 8) so that every SM pulls weights; the S fp32
+//    partial tiles are reduced through distributed shared memory (DSMEM) in a fixed order
+//    (deterministic), each CTA finishing 1/S of the tile's columns with the epilogue.
+//    No global workspace, no atomics, no serial last-CTA tail.
+// PDL: the weight tiles of the first pipeline stages are fetched BEFORE griddepcontrol.wait,
+// overlapping the previous kernel's tail; activations are loaded after it.
 // SiLU*mul: W rows are blocked [gate 128 | up 128] per 128 output features, so one TMEM
 // row (NORMAL) or two accumulators of one CTA (SWAP, nsub = 2) hold gate and up together.
 //
@@ -25,7 +29,7 @@ constexpr int TC_THREADS = 128;
 constexpr int TC_BK = 64;  // 64 bf16 = one 128-byte swizzle row
 constexpr int TC_MAX_STAGES = 8;
 constexpr int P_TILE_BYTES = 128 * TC_BK * 2;  // 16 KB
-constexpr size_t TC_CNT_BYTES = 64 * 1024;     // split-K tile counters (<= 16384 tiles)
+constexpr int TC_MAX_CLUSTER = 8;
 
 struct GemmArgs {
   int M, N, K;
@@ -33,14 +37,12 @@ struct GemmArgs {
   int nsub;     // P sub-tiles per CTA (SWAP SiLU: 2)
   int stages;
   int kblocks;
-  int splits;
+  int splits;   // SWAP: cluster size along K
   int n_tiles;
   void* C;
   int ldc;
   const void* R;
   int ldr;
-  float* part;
-  int* cnt;
 };
 
 template <typename OutT>
@@ -62,20 +64,20 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
   uint64_t* empty = full + TC_MAX_STAGES;
   uint64_t* accum = empty + TC_MAX_STAGES;
   uint32_t* tmem_slot = (uint32_t*)(accum + 1);
-  __shared__ int is_last_s;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
-  const int split = SWAP ? blockIdx.y : 0;
-  const int kb_per = (g.kblocks + g.splits - 1) / g.splits;
+  const int S = SWAP ? g.splits : 1;
+  const int tile = SWAP ? blockIdx.x / S : blockIdx.x;
+  const int split = SWAP ? blockIdx.x % S : 0;   // == cluster rank (cluster dims (S,1,1))
+  const int kb_per = (g.kblocks + S - 1) / S;
   const int kb_lo = split * kb_per;
   const int kb_hi = min(g.kblocks, kb_lo + kb_per);
-  const int n_kb = kb_hi - kb_lo;
-  // P rows (TMEM lanes) and Q rows (TMEM columns) of this tile
+  const int n_kb = max(0, kb_hi - kb_lo);
   const int p_row0 = SWAP ? tile * 128 * g.nsub : blockIdx.y * 128;
   const int q_row0 = SWAP ? 0 : tile * g.bn;
-  const uint32_t tmem_cols_alloc = (g.nsub * g.bn <= 32) ? 32 : (g.nsub * g.bn <= 64) ? 64
-                                   : (g.nsub * g.bn <= 128) ? 128 : (g.nsub * g.bn <= 256) ? 256 : 512;
+  const int cols = g.nsub * g.bn;
+  const uint32_t tmem_cols_alloc = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128
+                                   : cols <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
     tc::tma_prefetch_desc(&tmap_p);
@@ -92,20 +94,45 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_trigger();
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
-    const uint64_t pol_p = SWAP ? tc::policy_evict_first() : tc::policy_evict_last();
-    const uint64_t pol_q = SWAP ? tc::policy_evict_last() : tc::policy_evict_first();
-    for (int i = 0; i < n_kb; ++i) {
+    const uint64_t pol_w = tc::policy_evict_first();  // weights: streamed once
+    const uint64_t pol_x = tc::policy_evict_last();   // activations: re-read by every tile
+    const int npre = min(n_kb, g.stages);
+    // the weight operand of the first stages does not depend on the previous kernel
+    for (int i = 0; i < npre; ++i) {
+      uint8_t* st = smem + i * stage_bytes;
+      tc::mbar_arrive_expect_tx(&full[i], stage_bytes);
+      const int kc = (kb_lo + i) * TC_BK;
+      if (SWAP) {
+        for (int sub = 0; sub < g.nsub; ++sub)
+          tc::tma_load_2d(st + sub * P_TILE_BYTES, &tmap_p, &full[i], kc, p_row0 + sub * 128, pol_w);
+      } else {
+        tc::tma_load_2d(st + P_TILE_BYTES, &tmap_q, &full[i], kc, q_row0, pol_w);
+      }
+    }
+    pdl_wait();
+    for (int i = 0; i < npre; ++i) {
+      uint8_t* st = smem + i * stage_bytes;
+      const int kc = (kb_lo + i) * TC_BK;
+      if (SWAP)
+        tc::tma_load_2d(st + g.nsub * P_TILE_BYTES, &tmap_q, &full[i], kc, q_row0, pol_x);
+      else
+        tc::tma_load_2d(st, &tmap_p, &full[i], kc, p_row0, pol_x);
+    }
+    for (int i = npre; i < n_kb; ++i) {
       const int s = i % g.stages;
       tc::mbar_wait(&empty[s], ((i / g.stages) & 1) ^ 1);
       uint8_t* st = smem + s * stage_bytes;
       tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
       const int kc = (kb_lo + i) * TC_BK;
       for (int sub = 0; sub < g.nsub; ++sub)
-        tc::tma_load_2d(st + sub * P_TILE_BYTES, &tmap_p, &full[s], kc, p_row0 + sub * 128, pol_p);
-      tc::tma_load_2d(st + g.nsub * P_TILE_BYTES, &tmap_q, &full[s], kc, q_row0, pol_q);
+        tc::tma_load_2d(st + sub * P_TILE_BYTES, &tmap_p, &full[s], kc, p_row0 + sub * 128,
+                        SWAP ? pol_w : pol_x);
+      tc::tma_load_2d(st + g.nsub * P_TILE_BYTES, &tmap_q, &full[s], kc, q_row0,
+                      SWAP ? pol_x : pol_w);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread)
@@ -130,6 +157,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
   }
 
   // ---------------- epilogue: all 4 warps; warp w owns TMEM lanes [32w, 32w+32)
+  pdl_wait();
   tc::mbar_wait(accum, 0);
   __syncwarp();
   tc::fence_after_sync();
@@ -147,9 +175,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
         tc::tmem_ld16(t_row + 128 + c0, uv);
         const int f0 = tile * 128 + c0;
         if (m < g.M) {
+          if (f0 + 16 <= g.N / 2 && sizeof(OutT) == 2) {
+            float o[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (f0 + j < g.N / 2) store_out(C + (size_t)m * g.ldc + f0 + j, silu_f(gv[j]) * uv[j]);
+            for (int j = 0; j < 16; ++j) o[j] = silu_f(gv[j]) * uv[j];
+            Vec8<bf16>::store((bf16*)(C + (size_t)m * g.ldc + f0), o);
+            Vec8<bf16>::store((bf16*)(C + (size_t)m * g.ldc + f0 + 8), o + 8);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (f0 + j < g.N / 2) store_out(C + (size_t)m * g.ldc + f0 + j, silu_f(gv[j]) * uv[j]);
+          }
         }
       }
     } else {
@@ -174,64 +210,70 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
         }
       }
     }
-  } else {
-    // SWAP: TMEM lane r = output feature row, column c = token
-    const int nrows_total = g.nsub * 128;
-    if (g.splits > 1) {
-      float* part = g.part + ((size_t)(split * g.n_tiles + tile) * g.nsub) * g.bn * 128;
-      for (int sub = 0; sub < g.nsub; ++sub)
-        for (int c0 = 0; c0 < g.bn; c0 += 16) {
-          float v[16];
-          tc::tmem_ld16(t_row + sub * g.bn + c0, v);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) part[((size_t)sub * g.bn + c0 + j) * 128 + r] = v[j];
-        }
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const int old = atomicAdd(&g.cnt[tile], 1);
-        is_last_s = (old == g.splits - 1);
-      }
-      __syncthreads();
-      if (!is_last_s) goto teardown;
-      __threadfence();
-    }
-    for (int c0 = 0; c0 < g.bn; c0 += 16) {
-      float v[2][16];
-      for (int sub = 0; sub < g.nsub; ++sub) {
-        if (g.splits == 1) {
-          tc::tmem_ld16(t_row + sub * g.bn + c0, v[sub]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[sub][j] = 0.f;
-          for (int s = 0; s < g.splits; ++s) {
-            const float* p = g.part + ((size_t)(s * g.n_tiles + tile) * g.nsub + sub) * g.bn * 128;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[sub][j] += __ldcg(p + (size_t)(c0 + j) * 128 + r);
-          }
-        }
-      }
+  } else if (S == 1) {
+    // SWAP, whole K in this CTA: TMEM lane r = output feature, column c = token
+    for (int c0 = 0; c0 < g.bn && c0 < g.M; c0 += 16) {
+      float v0[16], v1[16];
+      tc::tmem_ld16(t_row + c0, v0);
+      if (EPI == SLX_EPI_SILU_MUL) tc::tmem_ld16(t_row + g.bn + c0, v1);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int m = c0 + j;
         if (m >= g.M) break;
         if (EPI == SLX_EPI_SILU_MUL) {
           const int f = tile * 128 + r;
-          if (f < g.N / 2) store_out(C + (size_t)m * g.ldc + f, silu_f(v[0][j]) * v[1][j]);
+          if (f < g.N / 2) store_out(C + (size_t)m * g.ldc + f, silu_f(v0[j]) * v1[j]);
         } else {
-          const int n = tile * nrows_total + r;
+          const int n = tile * 128 + r;
           if (n < g.N) {
-            float o = v[0][j];
+            float o = v0[j];
             if (EPI == SLX_EPI_RESIDUAL) o += to_f32(R[(size_t)m * g.ldr + n]);
             store_out(C + (size_t)m * g.ldc + n, o);
           }
         }
       }
     }
-    if (g.splits > 1 && threadIdx.x == 0) g.cnt[tile] = 0;  // self-cleaning for replay
+  } else {
+    // SWAP split-K over the cluster: stage this CTA's partial tile in its (now idle) pipeline
+    // smem as red[sub][c][r], then reduce 1/S of the columns across the cluster via DSMEM.
+    float* red = reinterpret_cast<float*>(smem);
+    for (int sub = 0; sub < g.nsub; ++sub)
+      for (int c0 = 0; c0 < g.bn && c0 < g.M; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(t_row + sub * g.bn + c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) red[(sub * g.bn + c0 + j) * 128 + r] = v[j];
+      }
+    tc::cluster_sync();
+    const uint32_t red_base = tc::smem_u32(red);
+    for (int m = split; m < g.M && m < g.bn; m += S) {
+      float acc[2] = {0.f, 0.f};
+      for (int sub = 0; sub < g.nsub; ++sub) {
+        const uint32_t off = red_base + (uint32_t)(((sub * g.bn + m) * 128 + r) * 4);
+        float part[TC_MAX_CLUSTER];
+#pragma unroll
+        for (int s = 0; s < TC_MAX_CLUSTER; ++s)
+          part[s] = s < S ? tc::ld_dsmem(tc::mapa(off, (uint32_t)s)) : 0.f;
+        float a = 0.f;
+#pragma unroll
+        for (int s = 0; s < TC_MAX_CLUSTER; ++s) a += part[s];   // fixed order: deterministic
+        acc[sub] = a;
+      }
+      if (EPI == SLX_EPI_SILU_MUL) {
+        const int f = tile * 128 + r;
+        if (f < g.N / 2) store_out(C + (size_t)m * g.ldc + f, silu_f(acc[0]) * acc[1]);
+      } else {
+        const int n = tile * 128 + r;
+        if (n < g.N) {
+          float o = acc[0];
+          if (EPI == SLX_EPI_RESIDUAL) o += to_f32(R[(size_t)m * g.ldr + n]);
+          store_out(C + (size_t)m * g.ldc + n, o);
+        }
+      }
+    }
+    tc::cluster_sync();  // keep our smem alive until every peer finished reading it
   }
 
-teardown:
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 1) {
@@ -276,63 +318,59 @@ static bool make_tmap(CUtensorMap* map, const void* ptr, int rows, int cols, int
 struct GemmPlan {
   bool swap;
   int bn, nsub, stages, kblocks, splits, n_tiles;
-  size_t smem, part_bytes, cnt_bytes;
+  size_t smem;
 };
+
+static constexpr size_t BAR_BYTES = 2 * TC_MAX_STAGES * 8 + 8 + 16;
 
 static GemmPlan plan_gemm(int M, int N, int K, int epi) {
   GemmPlan p{};
   p.kblocks = ceil_div(K, TC_BK);
   p.swap = M <= 128;
-  const size_t bar_bytes = 2 * TC_MAX_STAGES * 8 + 8 + 16;
   if (p.swap) {
     p.bn = ((M + 15) / 16) * 16;
     if (p.bn < 16) p.bn = 16;
     p.nsub = (epi == SLX_EPI_SILU_MUL) ? 2 : 1;
-    const int stage = p.nsub * P_TILE_BYTES + p.bn * TC_BK * 2;
+    const size_t stage = (size_t)p.nsub * P_TILE_BYTES + (size_t)p.bn * TC_BK * 2;
+    const size_t red = (size_t)p.nsub * p.bn * 128 * 4;
     p.n_tiles = ceil_div(N, 128 * p.nsub);
-    if (p.n_tiles > (int)(TC_CNT_BYTES / 4)) {  // rejected by the caller
-      p.n_tiles = -1;
-      return p;
-    }
-    const size_t two_cta_budget = 112 * 1024 - 1024 - bar_bytes;
-    int st2 = (int)(two_cta_budget / stage);
+    const size_t budget2 = 112 * 1024 - 1024 - BAR_BYTES;   // two CTAs per SM
+    const size_t budget1 = 225 * 1024 - 1024 - BAR_BYTES;   // one CTA per SM
+    int st2 = (int)(budget2 / stage);
+    if (st2 > 6) st2 = 6;
     int ctas_per_sm;
-    if (st2 >= 2) {
-      p.stages = st2 > 6 ? 6 : st2;
+    if (st2 >= 2 && (size_t)st2 * stage >= red) {
+      p.stages = st2;
       ctas_per_sm = 2;
     } else {
-      int st1 = (int)((220 * 1024 - bar_bytes) / stage);
+      int st1 = (int)(budget1 / stage);
       p.stages = st1 > TC_MAX_STAGES ? TC_MAX_STAGES : st1;
       ctas_per_sm = 1;
     }
     const int slots = ctas_per_sm * sm_count();
     int s = slots / p.n_tiles;
-    const int max_s = p.kblocks / 4 > 1 ? p.kblocks / 4 : 1;
-    s = s < 1 ? 1 : (s > max_s ? max_s : s);
-    // every split must own >= 1 k-block
-    while (s > 1 && (s - 1) * ceil_div(p.kblocks, s) >= p.kblocks) --s;
+    const int max_s = p.kblocks / 4 > 1 ? p.kblocks / 4 : 1;   // >= 4 k-blocks per split
+    s = s < 1 ? 1 : s;
+    s = s > max_s ? max_s : s;
+    s = s > TC_MAX_CLUSTER ? TC_MAX_CLUSTER : s;
+    while (s > 1 && (s - 1) * ceil_div(p.kblocks, s) >= p.kblocks) --s;  // no empty split
     p.splits = s;
-    p.smem = (size_t)p.stages * stage + bar_bytes + 1024;
-    p.part_bytes = p.splits > 1 ? (size_t)p.splits * p.n_tiles * p.nsub * p.bn * 128 * 4 : 0;
-    // fixed-size counter region at the head of ws, independent of the shape, so counters of
-    // one call are never overlapped by another call's partial tiles (they stay zero)
-    p.cnt_bytes = p.splits > 1 ? TC_CNT_BYTES : 0;
+    if (p.splits > 1 && (size_t)p.stages * stage < red) p.splits = 1;  // cannot stage partials
+    p.smem = (size_t)p.stages * stage + BAR_BYTES + 1024;
   } else {
     p.bn = 256;
     p.nsub = 1;
     p.stages = 4;
     p.n_tiles = ceil_div(N, p.bn);
     p.splits = 1;
-    p.smem = (size_t)p.stages * (P_TILE_BYTES + p.bn * TC_BK * 2) + bar_bytes + 1024;
-    p.part_bytes = 0;
-    p.cnt_bytes = 0;
+    p.smem = (size_t)p.stages * (P_TILE_BYTES + p.bn * TC_BK * 2) + BAR_BYTES + 1024;
   }
   return p;
 }
 
 template <bool SWAP, int EPI, typename OutT>
 static int launch_tc(const CUtensorMap& mp, const CUtensorMap& mq, const GemmArgs& a, dim3 grid,
-                     size_t smem, cudaStream_t s) {
+                     size_t smem, unsigned cluster, cudaStream_t s) {
   auto k = gemm_tc_kernel<SWAP, EPI, OutT>;
   static size_t configured = 0;  // per instantiation: largest dynamic smem opted into so far
   if (smem > configured) {
@@ -341,23 +379,22 @@ static int launch_tc(const CUtensorMap& mp, const CUtensorMap& mq, const GemmArg
       return SLX_ERR_CUDA;
     configured = smem;
   }
-  SLX_CLEAR_STALE();
-  k<<<grid, TC_THREADS, smem, s>>>(mp, mq, a);
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  return launch_ex(k, grid, dim3(TC_THREADS), smem, s, cluster, mp, mq, a);
 }
 
 template <bool SWAP>
 static int dispatch_tc(int epi, int c_dtype, const CUtensorMap& mp, const CUtensorMap& mq,
-                       const GemmArgs& a, dim3 grid, size_t smem, cudaStream_t s) {
+                       const GemmArgs& a, dim3 grid, size_t smem, unsigned cl, cudaStream_t s) {
   if (c_dtype == SLX_DT_BF16) {
-    if (epi == SLX_EPI_NONE) return launch_tc<SWAP, SLX_EPI_NONE, bf16>(mp, mq, a, grid, smem, s);
-    if (epi == SLX_EPI_RESIDUAL) return launch_tc<SWAP, SLX_EPI_RESIDUAL, bf16>(mp, mq, a, grid, smem, s);
-    return launch_tc<SWAP, SLX_EPI_SILU_MUL, bf16>(mp, mq, a, grid, smem, s);
+    if (epi == SLX_EPI_NONE) return launch_tc<SWAP, SLX_EPI_NONE, bf16>(mp, mq, a, grid, smem, cl, s);
+    if (epi == SLX_EPI_RESIDUAL)
+      return launch_tc<SWAP, SLX_EPI_RESIDUAL, bf16>(mp, mq, a, grid, smem, cl, s);
+    return launch_tc<SWAP, SLX_EPI_SILU_MUL, bf16>(mp, mq, a, grid, smem, cl, s);
   }
-  if (epi == SLX_EPI_NONE) return launch_tc<SWAP, SLX_EPI_NONE, float>(mp, mq, a, grid, smem, s);
-  if (epi == SLX_EPI_RESIDUAL) return launch_tc<SWAP, SLX_EPI_RESIDUAL, float>(mp, mq, a, grid, smem, s);
-  return launch_tc<SWAP, SLX_EPI_SILU_MUL, float>(mp, mq, a, grid, smem, s);
+  if (epi == SLX_EPI_NONE) return launch_tc<SWAP, SLX_EPI_NONE, float>(mp, mq, a, grid, smem, cl, s);
+  if (epi == SLX_EPI_RESIDUAL)
+    return launch_tc<SWAP, SLX_EPI_RESIDUAL, float>(mp, mq, a, grid, smem, cl, s);
+  return launch_tc<SWAP, SLX_EPI_SILU_MUL, float>(mp, mq, a, grid, smem, cl, s);
 }
 
 }  // namespace slx
@@ -365,14 +402,14 @@ static int dispatch_tc(int epi, int c_dtype, const CUtensorMap& mp, const CUtens
 using namespace slx;
 
 extern "C" size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
-  if (M <= 0 || N <= 0 || K <= 0) return 0;
-  GemmPlan p = plan_gemm(M, N, K, epilogue);
-  return p.cnt_bytes + p.part_bytes;
+  (void)M; (void)N; (void)K; (void)epilogue;
+  return 0;  // split-K partials live in cluster shared memory
 }
 
 extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                              const void* R, int ldr, int M, int N, int K, int epilogue, void* ws,
                              size_t ws_bytes, void* stream) {
+  (void)ws; (void)ws_bytes;
   SLX_CHECK_ARG(A && W && C && M >= 0 && N > 0 && K > 0 && lda >= K && K % 8 == 0 &&
                 lda % 8 == 0 && ldc % 8 == 0);
   SLX_CHECK_ARG(c_dtype == SLX_DT_BF16 || c_dtype == SLX_DT_F32);
@@ -389,27 +426,19 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= N);
   if (M == 0) return SLX_OK;
   GemmPlan p = plan_gemm(M, N, K, epilogue);
-  if (p.n_tiles <= 0) return SLX_ERR_UNSUPPORTED;
-  const size_t need = p.cnt_bytes + p.part_bytes;
-  if (need > 0) {
-    if (!ws || ws_bytes < need) return SLX_ERR_WORKSPACE;
-    SLX_CHECK_ALIGN(ws, 256);
-  }
   CUtensorMap mp, mq;
   GemmArgs a{};
   a.M = M; a.N = N; a.K = K;
   a.bn = p.bn; a.nsub = p.nsub; a.stages = p.stages; a.kblocks = p.kblocks;
   a.splits = p.splits; a.n_tiles = p.n_tiles;
   a.C = C; a.ldc = ldc; a.R = R; a.ldr = ldr;
-  a.cnt = need ? (int*)ws : nullptr;
-  a.part = need ? (float*)((char*)ws + p.cnt_bytes) : nullptr;
   cudaStream_t s = (cudaStream_t)stream;
   if (p.swap) {
     if (!make_tmap(&mp, W, N, K, K, 128) || !make_tmap(&mq, A, M, K, lda, p.bn)) return SLX_ERR_CUDA;
-    dim3 grid((unsigned)p.n_tiles, (unsigned)p.splits);
-    return dispatch_tc<true>(epilogue, c_dtype, mp, mq, a, grid, p.smem, s);
+    dim3 grid((unsigned)(p.n_tiles * p.splits), 1);
+    return dispatch_tc<true>(epilogue, c_dtype, mp, mq, a, grid, p.smem, (unsigned)p.splits, s);
   }
   if (!make_tmap(&mp, A, M, K, lda, 128) || !make_tmap(&mq, W, N, K, K, p.bn)) return SLX_ERR_CUDA;
   dim3 grid((unsigned)p.n_tiles, (unsigned)ceil_div(M, 128));
-  return dispatch_tc<false>(epilogue, c_dtype, mp, mq, a, grid, p.smem, s);
+  return dispatch_tc<false>(epilogue, c_dtype, mp, mq, a, grid, p.smem, 1u, s);
 }

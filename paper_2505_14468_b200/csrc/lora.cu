@@ -11,6 +11,7 @@
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace slx {
 
@@ -19,6 +20,7 @@ constexpr int LORA_MAX_RANK = 64;
 constexpr int LORA_MAX_KS = 8;    // k-splits of the shrink
 constexpr int PLAN_THREADS = 1024;
 constexpr int PLAN_MAX_GROUPS = 2048;
+constexpr int LORA_FUSED_MAX_TOK = 256;  // decode-sized batches use the fused cluster kernel
 
 struct LoraTile {
   int slot, start, count, pad;
@@ -88,6 +90,8 @@ __device__ void emit_tiles(const int* g_slot, const int* g_start, const int* g_c
 
 __global__ void __launch_bounds__(PLAN_THREADS)
 plan_tokens_kernel(const int32_t* __restrict__ tok_slot, int n_tok, int n_slots, LoraWs ws) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int cnt[PLAN_MAX_GROUPS];
   __shared__ int start[PLAN_MAX_GROUPS];
   __shared__ int slot_id[PLAN_MAX_GROUPS];
@@ -126,6 +130,8 @@ plan_tokens_kernel(const int32_t* __restrict__ tok_slot, int n_tok, int n_slots,
 __global__ void __launch_bounds__(PLAN_THREADS)
 plan_segments_kernel(const int32_t* __restrict__ seg_indptr, const int32_t* __restrict__ seg_slot,
                      int n_seg, int n_tok, int n_slots, LoraWs ws) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ int cnt[PLAN_MAX_GROUPS];
   __shared__ int start[PLAN_MAX_GROUPS];
   __shared__ int slot_id[PLAN_MAX_GROUPS];
@@ -157,6 +163,8 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 lora_shrink_kernel(const T* __restrict__ x, int ldx, int n_tok, int d_in, int ks,
                    const int32_t* __restrict__ slot_rank, int max_rank, TargetArgs ta, LoraWs ws) {
+  pdl_trigger();
+  pdl_wait();
   const int tile_id = blockIdx.x;
   if (tile_id >= *ws.n_tiles) return;
   const LoraTile tile = ws.tiles[tile_id];
@@ -249,6 +257,8 @@ __global__ void __launch_bounds__(256)
 lora_expand_kernel(T* __restrict__ y, int ldy, int n_tok, int ks, int n_split,
                    const int32_t* __restrict__ slot_rank, const float* __restrict__ slot_scale,
                    int max_rank, TargetArgs ta, LoraWs ws) {
+  pdl_trigger();
+  pdl_wait();
   const int tile_id = blockIdx.x;
   if (tile_id >= *ws.n_tiles) return;
   const LoraTile tile = ws.tiles[tile_id];
@@ -286,6 +296,151 @@ lora_expand_kernel(T* __restrict__ y, int ldy, int n_tok, int ks, int n_split,
     expand_body<T, 64>(y, ldy, B, rank, n_lo, n_hi, d_out, vs, toks, tile.count, co, cb, cs);
 }
 
+
+// ---------------------------------------------------------------- fused decode kernel (BGMV)
+// One cluster of KS CTAs per (tile, target).  CTA q of the cluster:
+//   1. stages x[tile tokens, k-chunk q], A_s[:, k-chunk q] and B_s[n-range q, :] in smem
+//      (all loads in flight at once: one HBM round trip),
+//   2. computes the partial shrink v_q[i][j] over its k-chunk (warp-per-output, shuffle reduce),
+//   3. reduces v = sum_q v_q through DSMEM (fixed order, deterministic) -> smem, x scale,
+//   4. expands its n-range: y[t, col(n)] += sum_j v[i][j] B_s[n][j]  (scale-and-add fused).
+constexpr int FU_THREADS = 256;
+constexpr int FU_MAX_KS = 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(FU_THREADS)
+lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, int n_tok, int d_in,
+                  int ks, int kc, const int32_t* __restrict__ slot_rank,
+                  const float* __restrict__ slot_scale, int max_rank, TargetArgs ta, LoraWs ws) {
+  extern __shared__ __align__(16) uint8_t fsm[];
+  pdl_trigger();
+  pdl_wait();
+  const int q = (int)tc::cluster_ctarank();
+  const int tile_id = blockIdx.x / ks;
+  const int tgt = blockIdx.y;
+  if (tile_id >= *ws.n_tiles) return;   // uniform over the cluster: no barrier is skipped unevenly
+  const LoraTile tile = ws.tiles[tile_id];
+  const int rank = min(slot_rank[tile.slot], max_rank);
+  const int R8 = (rank + 7) & ~7;
+  const float scale = slot_scale[tile.slot];
+  const int d_out = ta.d_out[tgt];
+  const int ns = ((d_out + ks - 1) / ks + 7) & ~7;         // rows of B per CTA
+  const int n_lo = min(d_out, q * ns), n_hi = min(d_out, n_lo + ns);
+  const int k_lo = min(d_in, q * kc), k_hi = min(d_in, k_lo + kc);
+  const int kl = k_hi - k_lo;
+  const bf16* A = reinterpret_cast<const bf16*>(ta.a_ptrs[tgt][tile.slot]);
+  const bf16* B = reinterpret_cast<const bf16*>(ta.b_ptrs[tgt][tile.slot]);
+
+  // smem carve: xs [TT][kc] T | as [max_rank][kc] bf16 | bs [ns][max_rank] bf16 | vpart, vfull, toks
+  T* xs = reinterpret_cast<T*>(fsm);
+  bf16* as = reinterpret_cast<bf16*>(fsm + (size_t)LORA_TT * kc * sizeof(T));
+  bf16* bs = as + (size_t)max_rank * kc;
+  float* vpart = reinterpret_cast<float*>(bs + (size_t)ns * max_rank);
+  float* vfull = vpart + LORA_TT * LORA_MAX_RANK;
+  int* toks = reinterpret_cast<int*>(vfull + LORA_TT * LORA_MAX_RANK);
+
+  if (threadIdx.x < LORA_TT)
+    toks[threadIdx.x] = threadIdx.x < tile.count ? ws.perm[tile.start + threadIdx.x] : 0;
+  __syncthreads();
+  // ---- 1. all loads in flight (16-byte cp.async)
+  constexpr int XV = 16 / sizeof(T);
+  const int xchunks = kl / XV;
+  for (int e = threadIdx.x; e < tile.count * xchunks; e += FU_THREADS) {
+    const int i = e / xchunks, c = e % xchunks;
+    cp_async16(xs + (size_t)i * kc + c * XV, x + (size_t)toks[i] * ldx + k_lo + c * XV);
+  }
+  const int achunks = kl / 8;
+  for (int e = threadIdx.x; e < rank * achunks; e += FU_THREADS) {
+    const int j = e / achunks, c = e % achunks;
+    cp_async16(as + (size_t)j * kc + c * 8, A + (size_t)j * d_in + k_lo + c * 8);
+  }
+  // B rows n_lo..n_hi are contiguous: (n_hi - n_lo) * rank elements
+  const int bchunks = (n_hi - n_lo) * rank / 8;
+  for (int e = threadIdx.x; e < bchunks; e += FU_THREADS) {
+    const int flat = e * 8;
+    const int n = flat / rank, j = flat % rank;
+    cp_async16(bs + (size_t)n * max_rank + j, B + (size_t)n_lo * rank + flat);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+
+  // ---- 2. partial shrink over this k-chunk: one warp per (i, j) output
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_out = tile.count * rank;
+  for (int o = warp; o < LORA_TT * LORA_MAX_RANK; o += FU_THREADS / 32) {
+    float acc = 0.f;
+    if (o < n_out) {
+      const int i = o / rank, j = o % rank;
+      const T* xr = xs + (size_t)i * kc;
+      const bf16* ar = as + (size_t)j * kc;
+      for (int k = lane * 8; k < kl; k += 32 * 8) {
+        float xf[8], af[8];
+        Vec8<T>::load(xr + k, xf);
+        Vec8<bf16>::load(ar + k, af);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc = fmaf(xf[e], af[e], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) vpart[i * LORA_MAX_RANK + j] = acc;
+    } else {
+      break;
+    }
+  }
+  tc::cluster_sync();
+  // ---- 3. v = sum over the cluster's k-chunks (DSMEM), fixed order
+  const uint32_t vp_base = tc::smem_u32(vpart);
+  for (int o = threadIdx.x; o < n_out; o += FU_THREADS) {
+    const int i = o / rank, j = o % rank;
+    const uint32_t off = vp_base + (uint32_t)((i * LORA_MAX_RANK + j) * 4);
+    float part[FU_MAX_KS];
+#pragma unroll
+    for (int s = 0; s < FU_MAX_KS; ++s) part[s] = s < ks ? tc::ld_dsmem(tc::mapa(off, (uint32_t)s)) : 0.f;
+    float a = 0.f;
+#pragma unroll
+    for (int s = 0; s < FU_MAX_KS; ++s) a += part[s];
+    vfull[i * LORA_MAX_RANK + j] = a * scale;
+  }
+  // peers may still read our vpart: arrive now, wait before exit
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  __syncthreads();
+  // ---- 4. expand + fused add over this CTA's n-range: thread owns 2 consecutive rows
+  const int cb = ta.col_blk[tgt], cstr = ta.col_stride[tgt], co = ta.col_off[tgt];
+  for (int n = n_lo + threadIdx.x * 2; n < n_hi; n += FU_THREADS * 2) {
+    const bf16* br0 = bs + (size_t)(n - n_lo) * max_rank;
+    const bf16* br1 = br0 + max_rank;
+    const bool two = n + 1 < n_hi;
+    const int col0 = co + (n / cb) * cstr + (n % cb);
+    const int col1 = co + ((n + 1) / cb) * cstr + ((n + 1) % cb);
+    for (int i = 0; i < tile.count; ++i) {
+      const float* vr = vfull + i * LORA_MAX_RANK;
+      float d0 = 0.f, d1 = 0.f;
+      for (int j = 0; j < R8; j += 8) {
+        float b0[8], b1[8];
+        Vec8<bf16>::load(br0 + j, b0);
+        Vec8<bf16>::load(br1 + j, b1);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float v = (j + e < rank) ? vr[j + e] : 0.f;
+          d0 = fmaf(v, b0[e], d0);
+          d1 = fmaf(v, b1[e], d1);
+        }
+      }
+      T* yr = y + (size_t)toks[i] * ldy;
+      yr[col0] = from_f32<T>(to_f32(yr[col0]) + d0);
+      if (two) yr[col1] = from_f32<T>(to_f32(yr[col1]) + d1);
+    }
+  }
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 }  // namespace slx
 
 using namespace slx;
@@ -310,10 +465,8 @@ extern "C" int slx_lora_plan_tokens(const int32_t* tok_slot, int n_tok, int n_sl
   // plan only touches the header/perm/tiles region, which does not depend on rank/targets
   int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
   if (st) return st;
-  SLX_CLEAR_STALE();
-  plan_tokens_kernel<<<1, PLAN_THREADS, 0, (cudaStream_t)stream>>>(tok_slot, n_tok, n_slots, w);
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  return launch_ex(plan_tokens_kernel, dim3(1), dim3(PLAN_THREADS), 0, (cudaStream_t)stream, 1u,
+                   tok_slot, n_tok, n_slots, w);
 }
 
 extern "C" int slx_lora_plan_segments(const int32_t* seg_indptr, const int32_t* seg_slot,
@@ -324,11 +477,8 @@ extern "C" int slx_lora_plan_segments(const int32_t* seg_indptr, const int32_t* 
   LoraWs w;
   int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
   if (st) return st;
-  SLX_CLEAR_STALE();
-  plan_segments_kernel<<<1, PLAN_THREADS, 0, (cudaStream_t)stream>>>(seg_indptr, seg_slot, n_seg,
-                                                                     n_tok, n_slots, w);
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  return launch_ex(plan_segments_kernel, dim3(1), dim3(PLAN_THREADS), 0, (cudaStream_t)stream,
+                   1u, seg_indptr, seg_slot, n_seg, n_tok, n_slots, w);
 }
 
 extern "C" int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ldx, int n_tok,
@@ -361,6 +511,35 @@ extern "C" int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ld
   if (st) return st;
   if (n_tok == 0) return SLX_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (n_tok <= LORA_FUSED_MAX_TOK) {
+    int fks = d_in / 512;
+    fks = fks < 1 ? 1 : (fks > FU_MAX_KS ? FU_MAX_KS : fks);
+    const int kc = ceil_div(ceil_div(d_in, fks), 8) * 8;
+    int max_dout = 0;
+    for (int i = 0; i < n_targets; ++i) max_dout = targets[i].d_out > max_dout ? targets[i].d_out : max_dout;
+    const int ns = ceil_div(ceil_div(max_dout, fks), 8) * 8;
+    const size_t tsz = dtype == SLX_DT_BF16 ? 2 : 4;
+    const size_t smem = (size_t)LORA_TT * kc * tsz + (size_t)max_rank * kc * 2 +
+                        (size_t)ns * max_rank * 2 + 2 * LORA_TT * LORA_MAX_RANK * 4 + LORA_TT * 4;
+    if (smem > 200 * 1024) return SLX_ERR_UNSUPPORTED;
+    dim3 gf((unsigned)(w.max_tiles * fks), (unsigned)n_targets);
+    if (dtype == SLX_DT_BF16) {
+      auto k = lora_fused_kernel<bf16>;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return SLX_ERR_CUDA;
+      return launch_ex(k, gf, dim3(FU_THREADS), smem, s, (unsigned)fks, (bf16*)y, ldy,
+                       (const bf16*)x, ldx, n_tok, d_in, fks, kc, slot_rank, slot_scale, max_rank,
+                       ta, w);
+    } else if (dtype == SLX_DT_F32) {
+      auto k = lora_fused_kernel<float>;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return SLX_ERR_CUDA;
+      return launch_ex(k, gf, dim3(FU_THREADS), smem, s, (unsigned)fks, (float*)y, ldy,
+                       (const float*)x, ldx, n_tok, d_in, fks, kc, slot_rank, slot_scale, max_rank,
+                       ta, w);
+    }
+    return SLX_ERR_INVALID;
+  }
   int ks = d_in / 512;
   ks = ks < 1 ? 1 : (ks > LORA_MAX_KS ? LORA_MAX_KS : ks);
   int max_dout = 0;
@@ -369,24 +548,21 @@ extern "C" int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ld
   dim3 gs((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)ks);
   dim3 ge((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)n_split);
   if (dtype == SLX_DT_BF16) {
-    SLX_CLEAR_STALE();
-    lora_shrink_kernel<bf16><<<gs, 256, 0, s>>>((const bf16*)x, ldx, n_tok, d_in, ks, slot_rank,
-                                                max_rank, ta, w);
-    SLX_CLEAR_STALE();
-    lora_expand_kernel<bf16><<<ge, 256, 0, s>>>((bf16*)y, ldy, n_tok, ks, n_split, slot_rank,
-                                                slot_scale, max_rank, ta, w);
+    st = launch_ex(lora_shrink_kernel<bf16>, gs, dim3(256), 0, s, 1u, (const bf16*)x, ldx, n_tok,
+                   d_in, ks, slot_rank, max_rank, ta, w);
+    if (st) return st;
+    st = launch_ex(lora_expand_kernel<bf16>, ge, dim3(256), 0, s, 1u, (bf16*)y, ldy, n_tok, ks,
+                   n_split, slot_rank, slot_scale, max_rank, ta, w);
   } else if (dtype == SLX_DT_F32) {
-    SLX_CLEAR_STALE();
-    lora_shrink_kernel<float><<<gs, 256, 0, s>>>((const float*)x, ldx, n_tok, d_in, ks, slot_rank,
-                                                 max_rank, ta, w);
-    SLX_CLEAR_STALE();
-    lora_expand_kernel<float><<<ge, 256, 0, s>>>((float*)y, ldy, n_tok, ks, n_split, slot_rank,
-                                                 slot_scale, max_rank, ta, w);
+    st = launch_ex(lora_shrink_kernel<float>, gs, dim3(256), 0, s, 1u, (const float*)x, ldx, n_tok,
+                   d_in, ks, slot_rank, max_rank, ta, w);
+    if (st) return st;
+    st = launch_ex(lora_expand_kernel<float>, ge, dim3(256), 0, s, 1u, (float*)y, ldy, n_tok, ks,
+                   n_split, slot_rank, slot_scale, max_rank, ta, w);
   } else {
     return SLX_ERR_INVALID;
   }
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  return st;
 }
 
 extern "C" int slx_lora_bgmv(int dtype, void* y, int ldy, const void* x, int ldx,

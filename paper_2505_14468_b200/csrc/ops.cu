@@ -12,6 +12,8 @@ namespace slx {
 template <typename T>
 __global__ void embedding_kernel(T* __restrict__ out, const bf16* __restrict__ table,
                                  const int32_t* __restrict__ tokens, int d, int vocab) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   int tok = tokens[t];
   tok = tok < 0 ? 0 : (tok >= vocab ? vocab - 1 : tok);
@@ -29,6 +31,8 @@ __global__ void embedding_kernel(T* __restrict__ out, const bf16* __restrict__ t
 template <typename T>
 __global__ void rmsnorm_kernel(T* __restrict__ out, int ldo, const T* __restrict__ x, int ldx,
                                const bf16* __restrict__ w, int d, float eps) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const T* xr = x + (size_t)t * ldx;
   float ss = 0.f;
@@ -68,6 +72,8 @@ __global__ void rope_kv_kernel(T* __restrict__ qkv, int ld, int H, int Hkv, int 
                                const int32_t* __restrict__ tok_seq,
                                const float* __restrict__ cos_tab, const float* __restrict__ sin_tab,
                                T* __restrict__ kc, T* __restrict__ vc, int max_ctx) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x;
   const int pos = tok_pos[t];
   const int seq = tok_seq[t];
@@ -99,92 +105,131 @@ __global__ void rope_kv_kernel(T* __restrict__ qkv, int ld, int H, int Hkv, int 
   }
 }
 
-// ------------------------------------------------------------------ attention (decode-style)
-// Block = 4 warps per (token, head). Each warp owns keys j = 32*(4*c + warp) + lane for
-// chunks c; online softmax per warp; merge across warps in smem.  D <= 128, D % 32 == 0.
-constexpr int ATT_WARPS = 4;
+// ------------------------------------------------------------------ attention over the KV pool
+// One CTA (D threads) per (token, head).  Keys are processed in blocks of KB: the block's K
+// and V rows are staged in shared memory with 16-byte cp.async by the whole CTA (double
+// buffered, so the next block streams while this one is consumed); a thread pair computes
+// one key's score, an online softmax (exp2, fp32) rescales the running output, and thread d
+// accumulates output dimension d.  Causal: token t attends cache positions 0..tok_pos[t].
+template <typename T> struct AttCfg { static constexpr int KB = 64; };
+template <> struct AttCfg<float> { static constexpr int KB = 32; };
+
+__device__ __forceinline__ void att_cp16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+
 template <typename T, int D>
-__global__ void __launch_bounds__(ATT_WARPS * 32)
+__global__ void __launch_bounds__(D)
 attention_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv, int ld, int H, int Hkv,
                  const int32_t* __restrict__ tok_pos, const int32_t* __restrict__ tok_seq,
-                 const T* __restrict__ kc, const T* __restrict__ vc, int max_ctx, float scale) {
-  constexpr int PER_LANE = D / 32;
+                 const T* __restrict__ kc, const T* __restrict__ vc, int max_ctx, float scale_log2) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int KB = AttCfg<T>::KB;
+  constexpr int DP = D + 16 / sizeof(T);       // padded row (16 B) against bank conflicts
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int CH = D / VEC;                   // 16-byte chunks per row
+  extern __shared__ __align__(16) uint8_t asmem[];
+  T* Ks = reinterpret_cast<T*>(asmem);                      // [2][KB][DP]
+  T* Vs = Ks + 2 * KB * DP;                                  // [2][KB][DP]
+  float* qs = reinterpret_cast<float*>(Vs + 2 * KB * DP);    // [D]
+  float* ps = qs + D;                                        // [KB]
+  float* red = ps + KB;                                      // [D/32]
+
   const int t = blockIdx.x / H, h = blockIdx.x % H;
   const int hk = h / (H / Hkv);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_keys = tok_pos[t] + 1;
   const int seq = tok_seq[t];
-  __shared__ float q_s[D];
-  __shared__ float m_s[ATT_WARPS], l_s[ATT_WARPS];
-  __shared__ float acc_s[ATT_WARPS][D];
-  for (int i = threadIdx.x; i < D; i += blockDim.x) q_s[i] = to_f32(qkv[(size_t)t * ld + h * D + i]);
-  __syncthreads();
   const T* kbase = kc + ((size_t)seq * Hkv + hk) * max_ctx * D;
   const T* vbase = vc + ((size_t)seq * Hkv + hk) * max_ctx * D;
-  float m = -FLT_MAX, l = 0.f;
-  float acc[PER_LANE];
+  const int tid = threadIdx.x;
+  qs[tid] = to_f32(qkv[(size_t)t * ld + h * D + tid]) * scale_log2;
+
+  auto stage = [&](int blk, int buf) {
+    const int k0 = blk * KB;
+    const int nk = min(KB, n_keys - k0);
+    for (int e = tid; e < nk * CH; e += D) {
+      const int r = e / CH, c = e % CH;
+      att_cp16(Ks + ((size_t)buf * KB + r) * DP + c * VEC, kbase + (size_t)(k0 + r) * D + c * VEC);
+      att_cp16(Vs + ((size_t)buf * KB + r) * DP + c * VEC, vbase + (size_t)(k0 + r) * D + c * VEC);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  const int nblk = (n_keys + KB - 1) / KB;
+  stage(0, 0);
+  float m = -INFINITY, l = 0.f, acc = 0.f;
+  constexpr int TPK = D / KB;   // threads per key for the score (2 for bf16, 4 for f32 @ D=128)
+  for (int b = 0; b < nblk; ++b) {
+    if (b + 1 < nblk) {
+      stage(b + 1, (b + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const int buf = b & 1;
+    const int k0 = b * KB;
+    // scores: TPK threads per key, each a D/TPK slice, shuffle-combined
+    const int key = tid / TPK, part = tid % TPK;
+    float sc = 0.f;
+    {
+      const T* kr = Ks + ((size_t)buf * KB + key) * DP + part * (D / TPK);
+      const float* qr = qs + part * (D / TPK);
 #pragma unroll
-  for (int i = 0; i < PER_LANE; ++i) acc[i] = 0.f;
-  for (int j0 = warp * 32; j0 < n_keys; j0 += ATT_WARPS * 32) {
-    const int j = j0 + lane;
-    float s = -FLT_MAX;
-    if (j < n_keys) {
-      const T* kr = kbase + (size_t)j * D;
-      float dot = 0.f;
-#pragma unroll
-      for (int i = 0; i < D; i += 8) {
+      for (int i = 0; i < D / TPK; i += 8) {
         float f[8];
         Vec8<T>::load(kr + i, f);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) dot += q_s[i + e] * f[e];
+        for (int e = 0; e < 8; ++e) sc = fmaf(qr[i + e], f[e], sc);
       }
-      s = dot * scale;
-    }
-    const float cmax = warp_max(s);
-    const float m_new = fmaxf(m, cmax);
-    const float corr = expf(m - m_new);
-    const float p = (j < n_keys) ? expf(s - m_new) : 0.f;
-    l = l * corr + warp_sum(p);
 #pragma unroll
-    for (int i = 0; i < PER_LANE; ++i) acc[i] *= corr;
-    const int nk = min(32, n_keys - j0);
-    for (int jj = 0; jj < nk; ++jj) {
-      const float pj = __shfl_sync(0xffffffffu, p, jj);
-      const T* vr = vbase + (size_t)(j0 + jj) * D;
-#pragma unroll
-      for (int i = 0; i < PER_LANE; ++i) acc[i] += pj * to_f32(vr[lane + 32 * i]);
+      for (int o = 1; o < TPK; o <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
     }
+    if (k0 + key >= n_keys) sc = -INFINITY;
+    // block max over the KB scores
+    float bm = warp_max(sc);
+    if ((tid & 31) == 0) red[tid >> 5] = bm;
+    __syncthreads();
+    bm = red[0];
+#pragma unroll
+    for (int w = 1; w < D / 32; ++w) bm = fmaxf(bm, red[w]);
+    const float m_new = fmaxf(m, bm);
+    const float corr = exp2f(m - m_new);
+    const float p = exp2f(sc - m_new);
+    if (part == 0) ps[key] = p;
+    __syncthreads();   // ps complete; red free
+    float bl = 0.f;
+    const int nk = min(KB, n_keys - k0);
+    const T* vcol = Vs + (size_t)buf * KB * DP + tid;
+    for (int j = 0; j < nk; ++j) {
+      const float pj = ps[j];
+      bl += pj;
+      acc = fmaf(pj, to_f32(vcol[(size_t)j * DP]), acc * (j == 0 ? corr : 1.f));
+    }
+    if (nk == 0) acc *= corr;
+    l = l * corr + bl;
     m = m_new;
+    __syncthreads();   // buffers reused by the next stage()
   }
-  if (lane == 0) { m_s[warp] = m; l_s[warp] = l; }
-#pragma unroll
-  for (int i = 0; i < PER_LANE; ++i) acc_s[warp][lane + 32 * i] = acc[i];
-  __syncthreads();
-  if (warp == 0) {
-    float mg = -FLT_MAX;
-#pragma unroll
-    for (int w = 0; w < ATT_WARPS; ++w) mg = fmaxf(mg, m_s[w]);
-    float lg = 0.f, cw[ATT_WARPS];
-#pragma unroll
-    for (int w = 0; w < ATT_WARPS; ++w) {
-      cw[w] = (l_s[w] > 0.f) ? expf(m_s[w] - mg) : 0.f;
-      lg += l_s[w] * cw[w];
-    }
-    const float inv = 1.0f / lg;
-#pragma unroll
-    for (int i = 0; i < PER_LANE; ++i) {
-      float o = 0.f;
-#pragma unroll
-      for (int w = 0; w < ATT_WARPS; ++w) o += acc_s[w][lane + 32 * i] * cw[w];
-      out[(size_t)t * ldo + h * D + lane + 32 * i] = from_f32<T>(o * inv);
-    }
-  }
+  out[(size_t)t * ldo + h * D + tid] = from_f32<T>(acc / l);
+}
+
+template <typename T, int D>
+constexpr size_t att_smem() {
+  return (size_t)4 * AttCfg<T>::KB * (D + 16 / sizeof(T)) * sizeof(T) +
+         (size_t)(D + AttCfg<T>::KB + D / 32) * 4;
 }
 
 // ------------------------------------------------------------------ SiLU * mul (blocked gate/up)
 template <typename T>
 __global__ void silu_mul_kernel(T* __restrict__ out, int ldo, const T* __restrict__ gu, int ld_gu,
                                 int ffn) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.y;
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (i >= ffn) return;
@@ -201,6 +246,8 @@ __global__ void silu_mul_kernel(T* __restrict__ out, int ldo, const T* __restric
 // ------------------------------------------------------------------ argmax
 template <typename T>
 __global__ void argmax_kernel(int32_t* __restrict__ out, const T* __restrict__ x, int ld, int n) {
+  pdl_trigger();
+  pdl_wait();
   const T* row = x + (size_t)blockIdx.x * ld;
   float best = -FLT_MAX;
   int bi = 0x7fffffff;
@@ -233,6 +280,8 @@ __global__ void __launch_bounds__(256)
 gemm_f32_kernel(const float* __restrict__ A, int lda, const bf16* __restrict__ W,
                 float* __restrict__ C, int ldc, const float* __restrict__ R, int ldr,
                 int M, int N, int K) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float As[SG_BK][SG_BM + 4];
   __shared__ float Ws[SG_BK][SG_BN + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -282,9 +331,20 @@ gemm_f32_kernel(const float* __restrict__ A, int lda, const bf16* __restrict__ W
 
 using namespace slx;
 
+template <typename T, int D>
+static int att_attr() {
+  static bool done = false;
+  if (!done) {
+    if (cudaFuncSetAttribute(attention_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)att_smem<T, D>()) != cudaSuccess)
+      return 1;
+    done = true;
+  }
+  return 0;
+}
+
 // ================================================================== C ABI
 #define DISPATCH_DT(dtype, ...)                      \
-  SLX_CLEAR_STALE();                                 \
   do {                                               \
     if ((dtype) == SLX_DT_BF16) {                    \
       using T = bf16;                                \
@@ -303,10 +363,9 @@ extern "C" int slx_embedding(int dtype, void* out, const void* table, const int3
   SLX_CHECK_ALIGN(out, 16);
   SLX_CHECK_ALIGN(table, 16);
   if (n_tok == 0) return SLX_OK;
-  DISPATCH_DT(dtype, (embedding_kernel<T><<<n_tok, 128, 0, (cudaStream_t)stream>>>(
-                         (T*)out, (const bf16*)table, tokens, d, vocab)));
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  int st = SLX_OK;
+  DISPATCH_DT(dtype, st = launch_ex(embedding_kernel<T>, dim3(n_tok), dim3(128), 0, (cudaStream_t)stream, 1u, (T*)out, (const bf16*)table, tokens, d, vocab));
+  return st;
 }
 
 extern "C" int slx_rmsnorm(int dtype, void* out, int ldo, const void* x, int ldx, const void* w,
@@ -318,10 +377,9 @@ extern "C" int slx_rmsnorm(int dtype, void* out, int ldo, const void* x, int ldx
   SLX_CHECK_ALIGN(w, 16);
   if (n_tok == 0) return SLX_OK;
   int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
-  DISPATCH_DT(dtype, (rmsnorm_kernel<T><<<n_tok, threads, 0, (cudaStream_t)stream>>>(
-                         (T*)out, ldo, (const T*)x, ldx, (const bf16*)w, d, eps)));
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  int st = SLX_OK;
+  DISPATCH_DT(dtype, st = launch_ex(rmsnorm_kernel<T>, dim3(n_tok), dim3(threads), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (const T*)x, ldx, (const bf16*)w, d, eps));
+  return st;
 }
 
 extern "C" int slx_rope_kv_write(int dtype, void* qkv, int ld_qkv, int n_tok, int heads,
@@ -334,11 +392,10 @@ extern "C" int slx_rope_kv_write(int dtype, void* qkv, int ld_qkv, int n_tok, in
                 max_ctx > 0 && qkv && tok_pos && tok_seq && cos_tab && sin_tab && k_cache &&
                 v_cache);
   if (n_tok == 0) return SLX_OK;
-  DISPATCH_DT(dtype, (rope_kv_kernel<T><<<n_tok, 256, 0, (cudaStream_t)stream>>>(
-                         (T*)qkv, ld_qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos_tab,
-                         sin_tab, (T*)k_cache, (T*)v_cache, max_ctx)));
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  int st = SLX_OK;
+  DISPATCH_DT(dtype, st = launch_ex(rope_kv_kernel<T>, dim3(n_tok), dim3(256), 0, (cudaStream_t)stream, 1u, (T*)qkv, ld_qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos_tab,
+                         sin_tab, (T*)k_cache, (T*)v_cache, max_ctx));
+  return st;
 }
 
 extern "C" int slx_attention(int dtype, void* out, int ldo, const void* qkv, int ld_qkv, int n_tok,
@@ -353,20 +410,18 @@ extern "C" int slx_attention(int dtype, void* out, int ldo, const void* qkv, int
   SLX_CHECK_ALIGN(v_cache, 16);
   if (head_dim != 64 && head_dim != 128) return SLX_ERR_UNSUPPORTED;
   if (n_tok == 0) return SLX_OK;
-  const float scale = 1.0f / sqrtf((float)head_dim);
+  const float scale = 1.4426950408889634f / sqrtf((float)head_dim);   // log2(e)/sqrt(D)
   const dim3 grid((unsigned)n_tok * heads);
   cudaStream_t s = (cudaStream_t)stream;
+  int st = SLX_OK;
   if (head_dim == 64) {
-    DISPATCH_DT(dtype, (attention_kernel<T, 64><<<grid, ATT_WARPS * 32, 0, s>>>(
-                           (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
-                           (const T*)k_cache, (const T*)v_cache, max_ctx, scale)));
+    DISPATCH_DT(dtype, st = att_attr<T, 64>() ? SLX_ERR_CUDA : launch_ex(attention_kernel<T, 64>, dim3(grid), dim3(64), att_smem<T, 64>(), s, 1u, (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
+                           (const T*)k_cache, (const T*)v_cache, max_ctx, scale));
   } else {
-    DISPATCH_DT(dtype, (attention_kernel<T, 128><<<grid, ATT_WARPS * 32, 0, s>>>(
-                           (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
-                           (const T*)k_cache, (const T*)v_cache, max_ctx, scale)));
+    DISPATCH_DT(dtype, st = att_attr<T, 128>() ? SLX_ERR_CUDA : launch_ex(attention_kernel<T, 128>, dim3(grid), dim3(128), att_smem<T, 128>(), s, 1u, (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
+                           (const T*)k_cache, (const T*)v_cache, max_ctx, scale));
   }
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  return st;
 }
 
 extern "C" int slx_silu_mul_blocked(int dtype, void* out, int ldo, const void* gu, int ld_gu,
@@ -377,20 +432,18 @@ extern "C" int slx_silu_mul_blocked(int dtype, void* out, int ldo, const void* g
   SLX_CHECK_ALIGN(gu, 16);
   if (n_tok == 0) return SLX_OK;
   dim3 grid((unsigned)ceil_div(ffn / 8, 128), (unsigned)n_tok);
-  DISPATCH_DT(dtype, (silu_mul_kernel<T><<<grid, 128, 0, (cudaStream_t)stream>>>(
-                         (T*)out, ldo, (const T*)gu, ld_gu, ffn)));
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  int st = SLX_OK;
+  DISPATCH_DT(dtype, st = launch_ex(silu_mul_kernel<T>, dim3(grid), dim3(128), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (const T*)gu, ld_gu, ffn));
+  return st;
 }
 
 extern "C" int slx_argmax(int dtype, int32_t* out, const void* logits, int ld, int n_rows,
                           int n_cols, void* stream) {
   SLX_CHECK_ARG(n_rows >= 0 && n_cols > 0 && ld >= n_cols && out && logits);
   if (n_rows == 0) return SLX_OK;
-  DISPATCH_DT(dtype, (argmax_kernel<T><<<n_rows, 1024, 0, (cudaStream_t)stream>>>(
-                         out, (const T*)logits, ld, n_cols)));
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  int st = SLX_OK;
+  DISPATCH_DT(dtype, st = launch_ex(argmax_kernel<T>, dim3(n_rows), dim3(1024), 0, (cudaStream_t)stream, 1u, out, (const T*)logits, ld, n_cols));
+  return st;
 }
 
 extern "C" int slx_gemm_f32(const void* A, int lda, const void* W, void* C, int ldc, const void* R,
@@ -403,10 +456,7 @@ extern "C" int slx_gemm_f32(const void* A, int lda, const void* W, void* C, int 
   }
   if (M == 0) return SLX_OK;
   dim3 grid((unsigned)ceil_div(N, SG_BN), (unsigned)ceil_div(M, SG_BM));
-  SLX_CLEAR_STALE();
-  gemm_f32_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
-      (const float*)A, lda, (const bf16*)W, (float*)C, ldc,
-      epilogue == SLX_EPI_RESIDUAL ? (const float*)R : nullptr, ldr, M, N, K);
-  SLX_LAUNCH_CHECK();
-  return SLX_OK;
+  return launch_ex(gemm_f32_kernel, grid, dim3(256), 0, (cudaStream_t)stream, 1u,
+                   (const float*)A, lda, (const bf16*)W, (float*)C, ldc,
+                   epilogue == SLX_EPI_RESIDUAL ? (const float*)R : nullptr, ldr, M, N, K);
 }
