@@ -68,14 +68,24 @@ SLX_API int slx_device_sm_count(int* out);
  * engine.py:832 prefill_work_ms, engine.py:888,909 decode gap) for the q/k/v/o,
  * gate/up/down and lm_head projections.
  * C[M,N] = A[M,K] · W[N,K]^T (+ epilogue), bf16 in, fp32 accumulate in TMEM (tcgen05),
- * C dtype c_dtype (bf16 or fp32).  M>=1, N % 128 == 0, K % 64 == 0, lda/ldc/ldr % 8 == 0.
- * Small M (decode) runs the swap-AB split-K kernel and needs `ws` of
- * slx_gemm_workspace_bytes(M, N, K) bytes (0 for large M).
+ * C dtype c_dtype (bf16 or fp32).  N % 16 == 0 (SiLU: N % 256 == 0), K % 8 == 0,
+ * lda/ldc/ldr % 8 == 0.  M <= 128 (decode) runs the swap-AB kernel whose K split is reduced
+ * across a thread-block cluster in distributed shared memory (no workspace: the
+ * workspace query returns 0 and is kept for ABI stability).
  */
+enum {
+  SLX_W_ROWMAJOR = 0, /* W[N, K] row-major (nn.Linear) */
+  SLX_W_TILED = 1     /* W packed as [ceil(N/128)][ceil(K/64)][128][64] bf16, zero-padded: every
+                         TMA box of the GEMM is one contiguous 16 KB burst (slx_pack_weight) */
+};
 SLX_API size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 SLX_API int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
-                  const void* R, int ldr, int M, int N, int K, int epilogue,
-                  void* ws, size_t ws_bytes, void* stream);
+                  const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
+                  void* stream);
+/* Pack a row-major bf16 W[N, K] (row stride ld) into the SLX_W_TILED layout (device kernel).
+ * dst must hold slx_packed_weight_elems(N, K) elements. */
+SLX_API size_t slx_packed_weight_elems(int N, int K);
+SLX_API int slx_pack_weight(void* dst, const void* src, int N, int K, int ld, void* stream);
 /* fp32-parity GEMM (CUDA cores): A fp32 [M,K], W bf16 [N,K], C/R fp32.  Epilogue NONE or
  * RESIDUAL.  K % 8 == 0. */
 SLX_API int slx_gemm_f32(const void* A, int lda, const void* W, void* C, int ldc,

@@ -25,6 +25,8 @@ DT_F32 = 1
 EPI_NONE = 0
 EPI_RESIDUAL = 1
 EPI_SILU_MUL = 2
+W_ROWMAJOR = 0
+W_TILED = 1
 LORA_MAX_TARGETS = 4
 
 _p = ctypes.c_void_p
@@ -44,7 +46,9 @@ SIGNATURES = {
     "slx_abi_version": (_i, []),
     "slx_device_sm_count": (_i, [ctypes.POINTER(_i)]),
     "slx_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
-    "slx_gemm_bf16": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _p, _sz, _p]),
+    "slx_gemm_bf16": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _p]),
+    "slx_packed_weight_elems": (_sz, [_i, _i]),
+    "slx_pack_weight": (_i, [_p, _p, _i, _i, _i, _p]),
     "slx_gemm_f32": (_i, [_p, _i, _p, _p, _i, _p, _i, _i, _i, _i, _i, _p]),
     "slx_lora_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "slx_lora_plan_tokens": (_i, [_p, _i, _i, _p, _sz, _p]),

@@ -19,6 +19,7 @@
 // Replaces the modelled prefill/decode time of the reference (batching.py:17-21 T0+alpha(b-1);
 // engine.py:832 prefill work, engine.py:888,909 decode_ms_per_token) with the real projections.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -43,6 +44,7 @@ struct GemmArgs {
   int ldc;
   const void* R;
   int ldr;
+  int w_tiled;  // W packed as [N/128][kblocks][128][64] (SLX_W_TILED)
 };
 
 template <typename OutT>
@@ -51,6 +53,17 @@ __device__ __forceinline__ void store_out(OutT* p, float v) {
 }
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+
+// TMA coordinates of the 128-row weight block `row0` (multiple of 128) at k-block `kb`.
+__device__ __forceinline__ void w_coord(const GemmArgs& g, int row0, int kb, int& c0, int& c1) {
+  if (g.w_tiled) {
+    c0 = 0;
+    c1 = ((row0 >> 7) * g.kblocks + kb) * 128;
+  } else {
+    c0 = kb * TC_BK;
+    c1 = row0;
+  }
+}
 
 template <bool SWAP, int EPI, typename OutT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -101,38 +114,37 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
     const uint64_t pol_w = tc::policy_evict_first();  // weights: streamed once
     const uint64_t pol_x = tc::policy_evict_last();   // activations: re-read by every tile
     const int npre = min(n_kb, g.stages);
+    // weight operand: SWAP -> P (nsub blocks of 128 rows), NORMAL -> Q (bn/128 blocks)
+    auto load_w = [&](uint8_t* st, uint64_t* bar, int kb) {
+      const int nblk = SWAP ? g.nsub : g.bn / 128;
+      uint8_t* dst = SWAP ? st : st + P_TILE_BYTES;
+      const int row0 = SWAP ? p_row0 : q_row0;
+      for (int b = 0; b < nblk; ++b) {
+        int c0, c1;
+        w_coord(g, row0 + b * 128, kb, c0, c1);
+        tc::tma_load_2d(dst + b * P_TILE_BYTES, SWAP ? &tmap_p : &tmap_q, bar, c0, c1, pol_w);
+      }
+    };
+    auto load_x = [&](uint8_t* st, uint64_t* bar, int kb) {
+      if (SWAP)
+        tc::tma_load_2d(st + g.nsub * P_TILE_BYTES, &tmap_q, bar, kb * TC_BK, q_row0, pol_x);
+      else
+        tc::tma_load_2d(st, &tmap_p, bar, kb * TC_BK, p_row0, pol_x);
+    };
     // the weight operand of the first stages does not depend on the previous kernel
     for (int i = 0; i < npre; ++i) {
-      uint8_t* st = smem + i * stage_bytes;
       tc::mbar_arrive_expect_tx(&full[i], stage_bytes);
-      const int kc = (kb_lo + i) * TC_BK;
-      if (SWAP) {
-        for (int sub = 0; sub < g.nsub; ++sub)
-          tc::tma_load_2d(st + sub * P_TILE_BYTES, &tmap_p, &full[i], kc, p_row0 + sub * 128, pol_w);
-      } else {
-        tc::tma_load_2d(st + P_TILE_BYTES, &tmap_q, &full[i], kc, q_row0, pol_w);
-      }
+      load_w(smem + i * stage_bytes, &full[i], kb_lo + i);
     }
     pdl_wait();
-    for (int i = 0; i < npre; ++i) {
-      uint8_t* st = smem + i * stage_bytes;
-      const int kc = (kb_lo + i) * TC_BK;
-      if (SWAP)
-        tc::tma_load_2d(st + g.nsub * P_TILE_BYTES, &tmap_q, &full[i], kc, q_row0, pol_x);
-      else
-        tc::tma_load_2d(st, &tmap_p, &full[i], kc, p_row0, pol_x);
-    }
+    for (int i = 0; i < npre; ++i) load_x(smem + i * stage_bytes, &full[i], kb_lo + i);
     for (int i = npre; i < n_kb; ++i) {
       const int s = i % g.stages;
       tc::mbar_wait(&empty[s], ((i / g.stages) & 1) ^ 1);
       uint8_t* st = smem + s * stage_bytes;
       tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
-      const int kc = (kb_lo + i) * TC_BK;
-      for (int sub = 0; sub < g.nsub; ++sub)
-        tc::tma_load_2d(st + sub * P_TILE_BYTES, &tmap_p, &full[s], kc, p_row0 + sub * 128,
-                        SWAP ? pol_w : pol_x);
-      tc::tma_load_2d(st + g.nsub * P_TILE_BYTES, &tmap_q, &full[s], kc, q_row0,
-                      SWAP ? pol_x : pol_w);
+      load_w(st, &full[s], kb_lo + i);
+      load_x(st, &full[s], kb_lo + i);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread)
@@ -211,28 +223,36 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
       }
     }
   } else if (S == 1) {
-    // SWAP, whole K in this CTA: TMEM lane r = output feature, column c = token
-    for (int c0 = 0; c0 < g.bn && c0 < g.M; c0 += 16) {
-      float v0[16], v1[16];
-      tc::tmem_ld16(t_row + c0, v0);
-      if (EPI == SLX_EPI_SILU_MUL) tc::tmem_ld16(t_row + g.bn + c0, v1);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int m = c0 + j;
-        if (m >= g.M) break;
+    // SWAP, whole K in this CTA: TMEM lane r = output feature, column c = token.
+    // Non-SiLU: sub-tile `sub` covers W rows tile*128*nsub + sub*128.  SiLU: sub pair
+    // (2p, 2p+1) = (gate, up) of feature block tile*nsub/2 + p.
+    const int npair = EPI == SLX_EPI_SILU_MUL ? g.nsub / 2 : g.nsub;
+    for (int p = 0; p < npair; ++p)
+      for (int c0 = 0; c0 < g.bn && c0 < g.M; c0 += 16) {
+        float v0[16], v1[16];
         if (EPI == SLX_EPI_SILU_MUL) {
-          const int f = tile * 128 + r;
-          if (f < g.N / 2) store_out(C + (size_t)m * g.ldc + f, silu_f(v0[j]) * v1[j]);
+          tc::tmem_ld16(t_row + (2 * p) * g.bn + c0, v0);
+          tc::tmem_ld16(t_row + (2 * p + 1) * g.bn + c0, v1);
         } else {
-          const int n = tile * 128 + r;
-          if (n < g.N) {
-            float o = v0[j];
-            if (EPI == SLX_EPI_RESIDUAL) o += to_f32(R[(size_t)m * g.ldr + n]);
-            store_out(C + (size_t)m * g.ldc + n, o);
+          tc::tmem_ld16(t_row + p * g.bn + c0, v0);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int m = c0 + j;
+          if (m >= g.M) break;
+          if (EPI == SLX_EPI_SILU_MUL) {
+            const int f = (tile * npair + p) * 128 + r;
+            if (f < g.N / 2) store_out(C + (size_t)m * g.ldc + f, silu_f(v0[j]) * v1[j]);
+          } else {
+            const int n = (tile * npair + p) * 128 + r;
+            if (n < g.N) {
+              float o = v0[j];
+              if (EPI == SLX_EPI_RESIDUAL) o += to_f32(R[(size_t)m * g.ldr + n]);
+              store_out(C + (size_t)m * g.ldc + n, o);
+            }
           }
         }
       }
-    }
   } else {
     // SWAP split-K over the cluster: stage this CTA's partial tile in its (now idle) pipeline
     // smem as red[sub][c][r], then reduce 1/S of the columns across the cluster via DSMEM.
@@ -246,31 +266,33 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
       }
     tc::cluster_sync();
     const uint32_t red_base = tc::smem_u32(red);
-    for (int m = split; m < g.M && m < g.bn; m += S) {
-      float acc[2] = {0.f, 0.f};
-      for (int sub = 0; sub < g.nsub; ++sub) {
-        const uint32_t off = red_base + (uint32_t)(((sub * g.bn + m) * 128 + r) * 4);
-        float part[TC_MAX_CLUSTER];
+    const int npair = EPI == SLX_EPI_SILU_MUL ? g.nsub / 2 : g.nsub;
+    const int per = EPI == SLX_EPI_SILU_MUL ? 2 : 1;
+    // work items (p, m): this CTA takes m = split, split + S, ...
+    for (int p = 0; p < npair; ++p)
+      for (int m = split; m < g.M && m < g.bn; m += S) {
+        float acc[2] = {0.f, 0.f};
+        for (int u = 0; u < per; ++u) {
+          const int sub = p * per + u;
+          const uint32_t off = red_base + (uint32_t)(((sub * g.bn + m) * 128 + r) * 4);
+          float part[TC_MAX_CLUSTER];
 #pragma unroll
-        for (int s = 0; s < TC_MAX_CLUSTER; ++s)
-          part[s] = s < S ? tc::ld_dsmem(tc::mapa(off, (uint32_t)s)) : 0.f;
-        float a = 0.f;
+          for (int s = 0; s < TC_MAX_CLUSTER; ++s)
+            part[s] = s < S ? tc::ld_dsmem(tc::mapa(off, (uint32_t)s)) : 0.f;
+          float a = 0.f;
 #pragma unroll
-        for (int s = 0; s < TC_MAX_CLUSTER; ++s) a += part[s];   // fixed order: deterministic
-        acc[sub] = a;
-      }
-      if (EPI == SLX_EPI_SILU_MUL) {
-        const int f = tile * 128 + r;
-        if (f < g.N / 2) store_out(C + (size_t)m * g.ldc + f, silu_f(acc[0]) * acc[1]);
-      } else {
-        const int n = tile * 128 + r;
-        if (n < g.N) {
+          for (int s = 0; s < TC_MAX_CLUSTER; ++s) a += part[s];   // fixed order: deterministic
+          acc[u] = a;
+        }
+        const int n = (tile * npair + p) * 128 + r;
+        if (EPI == SLX_EPI_SILU_MUL) {
+          if (n < g.N / 2) store_out(C + (size_t)m * g.ldc + n, silu_f(acc[0]) * acc[1]);
+        } else if (n < g.N) {
           float o = acc[0];
           if (EPI == SLX_EPI_RESIDUAL) o += to_f32(R[(size_t)m * g.ldr + n]);
           store_out(C + (size_t)m * g.ldc + n, o);
         }
       }
-    }
     tc::cluster_sync();  // keep our smem alive until every peer finished reading it
   }
 
@@ -323,6 +345,14 @@ struct GemmPlan {
 
 static constexpr size_t BAR_BYTES = 2 * TC_MAX_STAGES * 8 + 8 + 16;
 
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
+// SWAP (decode) tiling: one CTA streams nsub x 128 weight rows over a k-range; the k-range
+// of a tile is split over a cluster of S CTAs.  Defaults come from a sweep on B200
+// (tools/gemm_sweep.py); SLX_GEMM_{NSUB,CTAS,STAGES,SPLITS} override for tuning.
 static GemmPlan plan_gemm(int M, int N, int K, int epi) {
   GemmPlan p{};
   p.kblocks = ceil_div(K, TC_BK);
@@ -330,25 +360,31 @@ static GemmPlan plan_gemm(int M, int N, int K, int epi) {
   if (p.swap) {
     p.bn = ((M + 15) / 16) * 16;
     if (p.bn < 16) p.bn = 16;
-    p.nsub = (epi == SLX_EPI_SILU_MUL) ? 2 : 1;
+    const bool silu = epi == SLX_EPI_SILU_MUL;
+    int nsub = env_int("SLX_GEMM_NSUB", 2);
+    if (nsub != 1 && nsub != 2 && nsub != 4) nsub = 2;
+    if (silu && nsub == 1) nsub = 2;
+    while (nsub * p.bn > 512) nsub /= 2;
+    if (silu && nsub < 2) nsub = 2;   // bn <= 128 always leaves room for a gate/up pair
+    p.nsub = nsub;
     const size_t stage = (size_t)p.nsub * P_TILE_BYTES + (size_t)p.bn * TC_BK * 2;
     const size_t red = (size_t)p.nsub * p.bn * 128 * 4;
     p.n_tiles = ceil_div(N, 128 * p.nsub);
     const size_t budget2 = 112 * 1024 - 1024 - BAR_BYTES;   // two CTAs per SM
     const size_t budget1 = 225 * 1024 - 1024 - BAR_BYTES;   // one CTA per SM
+    int ctas = env_int("SLX_GEMM_CTAS", 0);
     int st2 = (int)(budget2 / stage);
     if (st2 > 6) st2 = 6;
-    int ctas_per_sm;
-    if (st2 >= 2 && (size_t)st2 * stage >= red) {
-      p.stages = st2;
-      ctas_per_sm = 2;
-    } else {
-      int st1 = (int)(budget1 / stage);
-      p.stages = st1 > TC_MAX_STAGES ? TC_MAX_STAGES : st1;
-      ctas_per_sm = 1;
-    }
-    const int slots = ctas_per_sm * sm_count();
-    int s = slots / p.n_tiles;
+    int st1 = (int)(budget1 / stage);
+    if (st1 > TC_MAX_STAGES) st1 = TC_MAX_STAGES;
+    if (ctas == 0) ctas = (st2 >= 3 && (size_t)st2 * stage >= red) ? 2 : 1;
+    if (ctas == 2 && (st2 < 2 || (size_t)st2 * stage < red)) ctas = 1;
+    p.stages = ctas == 2 ? st2 : st1;
+    const int want_st = env_int("SLX_GEMM_STAGES", 0);
+    if (want_st >= 2 && want_st < p.stages) p.stages = want_st;
+    const int slots = ctas * sm_count();
+    int s = env_int("SLX_GEMM_SPLITS", 0);
+    if (s <= 0) s = slots / p.n_tiles;
     const int max_s = p.kblocks / 4 > 1 ? p.kblocks / 4 : 1;   // >= 4 k-blocks per split
     s = s < 1 ? 1 : s;
     s = s > max_s ? max_s : s;
@@ -407,9 +443,9 @@ extern "C" size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
 }
 
 extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
-                             const void* R, int ldr, int M, int N, int K, int epilogue, void* ws,
-                             size_t ws_bytes, void* stream) {
-  (void)ws; (void)ws_bytes;
+                             const void* R, int ldr, int M, int N, int K, int epilogue,
+                             int w_layout, void* stream) {
+  SLX_CHECK_ARG(w_layout == SLX_W_ROWMAJOR || w_layout == SLX_W_TILED);
   SLX_CHECK_ARG(A && W && C && M >= 0 && N > 0 && K > 0 && lda >= K && K % 8 == 0 &&
                 lda % 8 == 0 && ldc % 8 == 0);
   SLX_CHECK_ARG(c_dtype == SLX_DT_BF16 || c_dtype == SLX_DT_F32);
@@ -432,13 +468,57 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   a.bn = p.bn; a.nsub = p.nsub; a.stages = p.stages; a.kblocks = p.kblocks;
   a.splits = p.splits; a.n_tiles = p.n_tiles;
   a.C = C; a.ldc = ldc; a.R = R; a.ldr = ldr;
+  a.w_tiled = w_layout == SLX_W_TILED;
   cudaStream_t s = (cudaStream_t)stream;
+  // tiled W: a [n_blocks * kblocks * 128, 64] matrix of contiguous 16 KB boxes
+  const int w_rows = a.w_tiled ? ceil_div(N, 128) * p.kblocks * 128 : N;
+  const int w_cols = a.w_tiled ? TC_BK : K;
   if (p.swap) {
-    if (!make_tmap(&mp, W, N, K, K, 128) || !make_tmap(&mq, A, M, K, lda, p.bn)) return SLX_ERR_CUDA;
+    if (!make_tmap(&mp, W, w_rows, w_cols, w_cols, 128) || !make_tmap(&mq, A, M, K, lda, p.bn))
+      return SLX_ERR_CUDA;
     dim3 grid((unsigned)(p.n_tiles * p.splits), 1);
     return dispatch_tc<true>(epilogue, c_dtype, mp, mq, a, grid, p.smem, (unsigned)p.splits, s);
   }
-  if (!make_tmap(&mp, A, M, K, lda, 128) || !make_tmap(&mq, W, N, K, K, p.bn)) return SLX_ERR_CUDA;
+  if (!make_tmap(&mp, A, M, K, lda, 128) || !make_tmap(&mq, W, w_rows, w_cols, w_cols, 128))
+    return SLX_ERR_CUDA;
   dim3 grid((unsigned)p.n_tiles, (unsigned)ceil_div(M, 128));
   return dispatch_tc<false>(epilogue, c_dtype, mp, mq, a, grid, p.smem, 1u, s);
+}
+
+// ------------------------------------------------------------------ weight packing
+namespace slx {
+__global__ void pack_weight_kernel(bf16* __restrict__ dst, const bf16* __restrict__ src, int N,
+                                   int K, int ld, int kblocks) {
+  pdl_trigger();
+  pdl_wait();
+  // one thread per 16-byte chunk of the packed tensor
+  const size_t chunk = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t total = (size_t)ceil_div(N, 128) * kblocks * 128 * 8;
+  if (chunk >= total) return;
+  const int c8 = (int)(chunk % 8);
+  const size_t row = chunk / 8;           // row of the [blocks*kblocks*128, 64] view
+  const int r = (int)(row % 128);
+  const size_t bk = row / 128;
+  const int kb = (int)(bk % kblocks);
+  const int nb = (int)(bk / kblocks);
+  const int n = nb * 128 + r, k = kb * TC_BK + c8 * 8;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (n < N && k < K) v = *reinterpret_cast<const uint4*>(src + (size_t)n * ld + k);  // K % 8 == 0
+  *reinterpret_cast<uint4*>(dst + row * TC_BK + c8 * 8) = v;
+}
+}  // namespace slx
+
+extern "C" size_t slx_packed_weight_elems(int N, int K) {
+  if (N <= 0 || K <= 0) return 0;
+  return (size_t)ceil_div(N, 128) * 128 * (size_t)ceil_div(K, TC_BK) * TC_BK;
+}
+
+extern "C" int slx_pack_weight(void* dst, const void* src, int N, int K, int ld, void* stream) {
+  SLX_CHECK_ARG(dst && src && N > 0 && K > 0 && K % 8 == 0 && ld >= K && ld % 8 == 0);
+  SLX_CHECK_ALIGN(dst, 16);
+  SLX_CHECK_ALIGN(src, 16);
+  const int kb = ceil_div(K, TC_BK);
+  const size_t total = (size_t)ceil_div(N, 128) * kb * 128 * 8;
+  return launch_ex(pack_weight_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0,
+                   (cudaStream_t)stream, 1u, (bf16*)dst, (const bf16*)src, N, K, ld, kb);
 }

@@ -152,7 +152,6 @@ class MultiLoraModel:
         self.targets = tuple(lora_targets)
         self.ffn_pad = _round_up(cfg.ffn, 128)
         self.pool = AdapterPool(cfg, self.targets, n_slots, max_rank, self.device)
-        self.ws = ops.Workspace(self.device, 64 << 20)
         nt = len(self.targets)
         self.lora_ws = torch.zeros(max(ops.lora_workspace_bytes(max_tokens, n_slots, max_rank,
                                                                 min(nt, 4)), 256) + 256,
@@ -187,6 +186,7 @@ class MultiLoraModel:
             down[:, :cfg.ffn] = g("w_down").to(torch.bfloat16)
             w[p + "w_down"] = down.to(dev)
         self.w = w
+        self._pack()
 
     def _block_gate_up(self, gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
         """[gate rows 128 | up rows 128] blocks, zero-padded to ffn_pad (SLX_EPI_SILU_MUL)."""
@@ -218,7 +218,23 @@ class MultiLoraModel:
             down = torch.zeros((cfg.hidden, self.ffn_pad), dtype=torch.bfloat16, device=dev)
             down[:, :cfg.ffn] = rn(cfg.hidden, cfg.ffn)
             w[p + "w_down"] = down
+            if self.dtype == torch.bfloat16:   # pack layer by layer to bound peak memory
+                for k in self.PROJ:
+                    w[p + k] = ops.pack_weight(w[p + k])
+        if self.dtype == torch.bfloat16:
+            w["lm_head"] = ops.pack_weight(w["lm_head"])
         self.w = w
+
+    PROJ = ("w_qkv", "wo", "w_gu", "w_down")
+
+    def _pack(self) -> None:
+        """bf16 mode: re-lay every projection (and lm_head) in the tiled TMA layout."""
+        if self.dtype != torch.bfloat16:
+            return
+        for k in list(self.w):
+            if k == "lm_head" or k.split(".")[-1] in self.PROJ:
+                self.w[k] = ops.pack_weight(self.w[k])
+        torch.cuda.synchronize(self.device)
 
     def backbone_bytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in self.w.values())
@@ -239,8 +255,7 @@ class MultiLoraModel:
     def _gemm(self, a, w, out=None, residual=None, silu=False, out_dtype=None):
         if self.dtype == torch.bfloat16:
             epi = EPI_SILU_MUL if silu else (EPI_RESIDUAL if residual is not None else 0)
-            return ops.gemm(a, w, out, epilogue=epi, residual=residual, out_dtype=out_dtype,
-                            ws=self.ws)
+            return ops.gemm(a, w, out, epilogue=epi, residual=residual, out_dtype=out_dtype)
         assert not silu
         return ops.gemm_f32(a, w, out, residual=residual)
 

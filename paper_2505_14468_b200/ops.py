@@ -12,7 +12,8 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, LoraTarget, check
+from ._lib import (DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED,
+                   LoraTarget, check)
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
 
@@ -110,31 +111,57 @@ class Workspace:
 
 
 # ---------------------------------------------------------------------------------- K1
+class PackedWeight:
+    """bf16 W[N, K] packed in the SLX_W_TILED layout ([N/128][K/64][128][64], zero-padded):
+    every TMA box the GEMM loads is one contiguous 16 KB HBM burst."""
+
+    def __init__(self, data: torch.Tensor, n: int, k: int):
+        self.data, self.n, self.k = data, n, k
+        self.shape = (n, k)
+        self.dtype = torch.bfloat16
+
+    def numel(self) -> int:
+        return self.n * self.k
+
+    def element_size(self) -> int:
+        return 2
+
+
+@_op("pack", 1)
+def pack_weight(w: torch.Tensor) -> PackedWeight:
+    if w.dtype != torch.bfloat16 or w.dim() != 2 or w.stride(1) != 1:
+        raise ValueError("pack_weight: bf16 row-major [N, K] expected")
+    N, K = w.shape
+    lib = _lib.load()
+    out = torch.empty(lib.slx_packed_weight_elems(N, K), dtype=torch.bfloat16, device=w.device)
+    check(lib.slx_pack_weight(_ptr(out), _ptr(w), N, K, w.stride(0), _stream()), "slx_pack_weight")
+    return PackedWeight(out, N, K)
+
+
 @_op("gemm", 1)
-def gemm(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None, *,
+def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
          epilogue: int = EPI_NONE, residual: torch.Tensor | None = None,
-         out_dtype: torch.dtype | None = None, ws: Workspace | None = None) -> torch.Tensor:
-    """bf16 tcgen05 GEMM: out = a @ w.T (+ residual | silu*mul of blocked gate/up)."""
+         out_dtype: torch.dtype | None = None, ws=None) -> torch.Tensor:
+    """bf16 tcgen05 GEMM: out = a @ w.T (+ residual | silu*mul of blocked gate/up).
+    ``w`` is a row-major bf16 [N, K] tensor or a :class:`PackedWeight`."""
     if a.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
         raise ValueError("gemm: a and w must be bf16")
     M, K = a.shape
     N, Kw = w.shape
-    if Kw != K or not w.is_contiguous():
-        raise ValueError("gemm: w must be contiguous [N, K]")
+    if isinstance(w, PackedWeight):
+        layout, wt = W_TILED, w.data
+    else:
+        if not w.is_contiguous():
+            raise ValueError("gemm: w must be contiguous [N, K]")
+        layout, wt = W_ROWMAJOR, w
+    if Kw != K:
+        raise ValueError("gemm: K mismatch")
     n_out = N // 2 if epilogue == EPI_SILU_MUL else N
     if out is None:
         out = torch.empty((M, n_out), dtype=out_dtype or torch.bfloat16, device=a.device)
-    lib = _lib.load()
-    need = lib.slx_gemm_workspace_bytes(M, N, K, epilogue)
-    wsb = None
-    if need:
-        if ws is None:
-            raise ValueError("gemm: this shape needs a workspace")
-        wsb = ws.get(need)
-    check(lib.slx_gemm_bf16(_ptr(a), _ld(a), _ptr(w), _ptr(out), _ld(out), _dt(out),
-                            _ptr(residual), _ld(residual) if residual is not None else 0,
-                            M, N, K, epilogue, _ptr(wsb), wsb.numel() if wsb is not None else 0,
-                            _stream()), "slx_gemm_bf16")
+    check(_lib.load().slx_gemm_bf16(_ptr(a), _ld(a), _ptr(wt), _ptr(out), _ld(out), _dt(out),
+                                    _ptr(residual), _ld(residual) if residual is not None else 0,
+                                    M, N, K, epilogue, layout, _stream()), "slx_gemm_bf16")
     return out
 
 

@@ -16,11 +16,6 @@ def bf(x):
     return x.to(torch.bfloat16)
 
 
-@pytest.fixture(scope="module")
-def ws():
-    return ops.Workspace(DEV, 64 << 20)
-
-
 # ------------------------------------------------------------------ K1 GEMM
 GEMM_SHAPES = [
     (1, 128, 64), (7, 256, 128), (16, 4096, 4096), (64, 12288, 4096), (64, 4096, 11008),
@@ -29,33 +24,49 @@ GEMM_SHAPES = [
 ]
 
 
+@pytest.mark.parametrize("tiled", [False, True])
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
-def test_gemm_matches_torch_fp32(M, N, K, ws):
+def test_gemm_matches_torch_fp32(M, N, K, tiled):
     g = torch.Generator(device=DEV).manual_seed(M * 7 + N + K)
     a = bf(torch.randn(M, K, device=DEV, generator=g))
     w = bf(torch.randn(N, K, device=DEV, generator=g) * 0.05)
     ref = a.float() @ w.float().T
-    out32 = ops.gemm(a, w, out_dtype=torch.float32, ws=ws)
+    wk = ops.pack_weight(w) if tiled else w
+    out32 = ops.gemm(a, wk, out_dtype=torch.float32)
     torch.cuda.synchronize()
     torch.testing.assert_close(out32, ref, rtol=1e-4, atol=1e-3)   # fp32 out: accumulation order only
-    out = ops.gemm(a, w, ws=ws)
+    out = ops.gemm(a, wk)
     torch.testing.assert_close(out.float(), ref, rtol=1e-2, atol=1e-2)
 
 
+@pytest.mark.parametrize("nsub,ctas,splits", [(1, 1, 1), (1, 2, 8), (2, 1, 3), (4, 1, 6), (4, 2, 2)])
+def test_gemm_decode_tilings(nsub, ctas, splits, monkeypatch):
+    """Every swap-AB tiling the planner can pick gives the same (deterministic) result."""
+    M, N, K = 64, 3072, 4096
+    a = bf(torch.randn(M, K, device=DEV))
+    w = bf(torch.randn(N, K, device=DEV) * 0.05)
+    ref = a.float() @ w.float().T
+    monkeypatch.setenv("SLX_GEMM_NSUB", str(nsub))
+    monkeypatch.setenv("SLX_GEMM_CTAS", str(ctas))
+    monkeypatch.setenv("SLX_GEMM_SPLITS", str(splits))
+    out = ops.gemm(a, ops.pack_weight(w), out_dtype=torch.float32)
+    torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
+
+
 @pytest.mark.parametrize("M", [3, 64, 200])
-def test_gemm_residual_inplace(M, ws):
+def test_gemm_residual_inplace(M):
     N, K = 512, 256
     g = torch.Generator(device=DEV).manual_seed(M)
     a = bf(torch.randn(M, K, device=DEV, generator=g))
     w = bf(torch.randn(N, K, device=DEV, generator=g) * 0.05)
     x = bf(torch.randn(M, N, device=DEV, generator=g))
     ref = a.float() @ w.float().T + x.float()
-    ops.gemm(a, w, x, epilogue=EPI_RESIDUAL, residual=x, ws=ws)
+    ops.gemm(a, ops.pack_weight(w), x, epilogue=EPI_RESIDUAL, residual=x)
     torch.testing.assert_close(x.float(), ref, rtol=1e-2, atol=2e-2)
 
 
 @pytest.mark.parametrize("M", [1, 64, 300])
-def test_gemm_silu_mul_blocked(M, ws):
+def test_gemm_silu_mul_blocked(M):
     F, K = 384, 256
     g = torch.Generator(device=DEV).manual_seed(M + 1)
     a = bf(torch.randn(M, K, device=DEV, generator=g))
@@ -64,19 +75,21 @@ def test_gemm_silu_mul_blocked(M, ws):
     w = torch.stack([gate.view(F // 128, 128, K), up.view(F // 128, 128, K)], 1).reshape(2 * F, K).contiguous()
     gr, ur = a.float() @ gate.float().T, a.float() @ up.float().T
     ref = gr * torch.sigmoid(gr) * ur
-    out = ops.gemm(a, w, epilogue=EPI_SILU_MUL, out_dtype=torch.float32, ws=ws)
+    out = ops.gemm(a, w, epilogue=EPI_SILU_MUL, out_dtype=torch.float32)
+    torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-3)
+    out = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_SILU_MUL, out_dtype=torch.float32)
     torch.testing.assert_close(out, ref, rtol=1e-3, atol=1e-3)
 
 
-def test_gemm_deterministic_split_k(ws):
+def test_gemm_deterministic_split_k():
     a = bf(torch.randn(64, 4096, device=DEV))
     w = bf(torch.randn(4096, 4096, device=DEV) * 0.02)
-    o1 = ops.gemm(a, w, out_dtype=torch.float32, ws=ws)
-    o2 = ops.gemm(a, w, out_dtype=torch.float32, ws=ws)
+    o1 = ops.gemm(a, w, out_dtype=torch.float32)
+    o2 = ops.gemm(a, w, out_dtype=torch.float32)
     assert torch.equal(o1, o2)
 
 
-def test_gemm_f32_parity(ws):
+def test_gemm_f32_parity():
     a = torch.randn(37, 200, device=DEV)
     w = bf(torch.randn(72, 200, device=DEV))
     r = torch.randn(37, 72, device=DEV)

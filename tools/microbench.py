@@ -33,17 +33,16 @@ def timeit(fn, iters=20):
 
 
 def gemm_shapes(M=64):
-    ws = ops.Workspace(DEV, 256 << 20)
     out = []
     for name, N, K, epi in [("qkv", 12288, 4096, EPI_NONE), ("o", 4096, 4096, EPI_RESIDUAL),
                             ("gate_up", 22016, 4096, EPI_SILU_MUL), ("down", 4096, 11008, EPI_RESIDUAL),
                             ("lm_head", 32000, 4096, EPI_NONE)]:
         a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
-        w = (torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16)
+        w = ops.pack_weight((torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16))
         nout = N // 2 if epi == EPI_SILU_MUL else N
         c = torch.empty(M, nout, device=DEV, dtype=torch.bfloat16)
         r = torch.randn(M, N, device=DEV).to(torch.bfloat16) if epi == EPI_RESIDUAL else None
-        ms = timeit(lambda: ops.gemm(a, w, c, epilogue=epi, residual=r, ws=ws))
+        ms = timeit(lambda: ops.gemm(a, w, c, epilogue=epi, residual=r))
         byts = N * K * 2 + M * K * 2 + M * nout * 2 * (2 if r is not None else 1)
         gbs = byts / ms / 1e6
         out.append({"gemm": name, "M": M, "N": N, "K": K, "us": round(ms * 1000, 2),
