@@ -19,6 +19,7 @@
 // Replaces the modelled prefill/decode time of the reference (batching.py:17-21 T0+alpha(b-1);
 // engine.py:832 prefill work, engine.py:888,909 decode_ms_per_token) with the real projections.
 #include <cuda.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -350,56 +351,108 @@ static int env_int(const char* name, int dflt) {
   return (e && *e) ? atoi(e) : dflt;
 }
 
+static void configure_kernel(const void* k, size_t smem) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // without this the driver may pick an L1-heavy carveout that fits only one CTA per SM
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+
+// Max co-resident clusters of `cluster` CTAs with `smem` bytes each (cached; queried on the
+// swap-AB kernel, whose resource footprint is the same for every epilogue instantiation).
+static int max_active_clusters(size_t smem, int cluster) {
+  struct Key { size_t smem; int cluster; int value; };
+  static Key cache[64];
+  static int n_cache = 0;
+  for (int i = 0; i < n_cache; ++i)
+    if (cache[i].smem == smem && cache[i].cluster == cluster) return cache[i].value;
+  const void* k = (const void*)gemm_tc_kernel<true, SLX_EPI_NONE, bf16>;
+  configure_kernel(k, 227 * 1024);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cluster * 64);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = (unsigned)cluster;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<true, SLX_EPI_NONE, bf16>, &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    n = sm_count() / cluster;  // conservative fallback
+  }
+  if (n_cache < 64) cache[n_cache++] = Key{smem, cluster, n};
+  return n;
+}
+
 // SWAP (decode) tiling: one CTA streams nsub x 128 weight rows over a k-range; the k-range
-// of a tile is split over a cluster of S CTAs.  Defaults come from a sweep on B200
-// (tools/gemm_sweep.py); SLX_GEMM_{NSUB,CTAS,STAGES,SPLITS} override for tuning.
+// of a tile is split over a cluster of S CTAs.  The planner picks, among nsub in {1,2}
+// (SiLU: 2) and 2 or 1 CTAs per SM, the split S that puts the most CTAs in flight while all
+// clusters stay co-resident (one wave, cudaOccupancyMaxActiveClusters) and every split keeps
+// >= 4 k-blocks.  SLX_GEMM_{NSUB,CTAS,STAGES,SPLITS} override for tuning (tools/gemm_sweep.py).
+
 static GemmPlan plan_gemm(int M, int N, int K, int epi) {
   GemmPlan p{};
   p.kblocks = ceil_div(K, TC_BK);
   p.swap = M <= 128;
-  if (p.swap) {
-    p.bn = ((M + 15) / 16) * 16;
-    if (p.bn < 16) p.bn = 16;
-    const bool silu = epi == SLX_EPI_SILU_MUL;
-    int nsub = env_int("SLX_GEMM_NSUB", 2);
-    if (nsub != 1 && nsub != 2 && nsub != 4) nsub = 2;
-    if (silu && nsub == 1) nsub = 2;
-    while (nsub * p.bn > 512) nsub /= 2;
-    if (silu && nsub < 2) nsub = 2;   // bn <= 128 always leaves room for a gate/up pair
-    p.nsub = nsub;
-    const size_t stage = (size_t)p.nsub * P_TILE_BYTES + (size_t)p.bn * TC_BK * 2;
-    const size_t red = (size_t)p.nsub * p.bn * 128 * 4;
-    p.n_tiles = ceil_div(N, 128 * p.nsub);
-    const size_t budget2 = 112 * 1024 - 1024 - BAR_BYTES;   // two CTAs per SM
-    const size_t budget1 = 225 * 1024 - 1024 - BAR_BYTES;   // one CTA per SM
-    int ctas = env_int("SLX_GEMM_CTAS", 0);
-    int st2 = (int)(budget2 / stage);
-    if (st2 > 6) st2 = 6;
-    int st1 = (int)(budget1 / stage);
-    if (st1 > TC_MAX_STAGES) st1 = TC_MAX_STAGES;
-    if (ctas == 0) ctas = (st2 >= 3 && (size_t)st2 * stage >= red) ? 2 : 1;
-    if (ctas == 2 && (st2 < 2 || (size_t)st2 * stage < red)) ctas = 1;
-    p.stages = ctas == 2 ? st2 : st1;
-    const int want_st = env_int("SLX_GEMM_STAGES", 0);
-    if (want_st >= 2 && want_st < p.stages) p.stages = want_st;
-    const int slots = ctas * sm_count();
-    int s = env_int("SLX_GEMM_SPLITS", 0);
-    if (s <= 0) s = slots / p.n_tiles;
-    const int max_s = p.kblocks / 4 > 1 ? p.kblocks / 4 : 1;   // >= 4 k-blocks per split
-    s = s < 1 ? 1 : s;
-    s = s > max_s ? max_s : s;
-    s = s > TC_MAX_CLUSTER ? TC_MAX_CLUSTER : s;
-    while (s > 1 && (s - 1) * ceil_div(p.kblocks, s) >= p.kblocks) --s;  // no empty split
-    p.splits = s;
-    if (p.splits > 1 && (size_t)p.stages * stage < red) p.splits = 1;  // cannot stage partials
-    p.smem = (size_t)p.stages * stage + BAR_BYTES + 1024;
-  } else {
+  if (!p.swap) {
     p.bn = 256;
     p.nsub = 1;
     p.stages = 4;
     p.n_tiles = ceil_div(N, p.bn);
     p.splits = 1;
     p.smem = (size_t)p.stages * (P_TILE_BYTES + p.bn * TC_BK * 2) + BAR_BYTES + 1024;
+    return p;
+  }
+  p.bn = ((M + 15) / 16) * 16;
+  if (p.bn < 16) p.bn = 16;
+  const bool silu = epi == SLX_EPI_SILU_MUL;
+  const int e_nsub = env_int("SLX_GEMM_NSUB", 0), e_ctas = env_int("SLX_GEMM_CTAS", 0);
+  const int e_st = env_int("SLX_GEMM_STAGES", 0), e_s = env_int("SLX_GEMM_SPLITS", 0);
+  double best_score = -1.0;
+  for (int nsub = 1; nsub <= 4; nsub *= 2) {
+    if (silu && nsub == 1) continue;
+    if (nsub * p.bn > 512) continue;
+    if (e_nsub ? nsub != e_nsub : nsub == 4) continue;   // nsub 4 only on request
+    const size_t stage = (size_t)nsub * P_TILE_BYTES + (size_t)p.bn * TC_BK * 2;
+    const size_t red = (size_t)nsub * p.bn * 128 * 4;
+    const int n_tiles = ceil_div(N, 128 * nsub);
+    for (int ctas = 2; ctas >= 1; --ctas) {
+      if (e_ctas && ctas != e_ctas) continue;
+      const size_t budget = ctas == 2 ? 112 * 1024 - 1024 - BAR_BYTES : 225 * 1024 - 1024 - BAR_BYTES;
+      int st = (int)(budget / stage);
+      st = st > (ctas == 2 ? 6 : TC_MAX_STAGES) ? (ctas == 2 ? 6 : TC_MAX_STAGES) : st;
+      if (e_st >= 2 && e_st < st) st = e_st;
+      if (st < 2) continue;
+      const size_t smem = (size_t)st * stage + BAR_BYTES + 1024;
+      for (int s = TC_MAX_CLUSTER; s >= 1; --s) {
+        if (e_s && s != e_s) continue;
+        if (s > 1 && (size_t)st * stage < red) continue;            // partials must fit in smem
+        if (s > 1 && ceil_div(p.kblocks, s) < 4 && !e_s) continue;   // >= 4 k-blocks per split
+        if ((s - 1) * ceil_div(p.kblocks, s) >= p.kblocks) continue; // no empty split
+        const int cap = max_active_clusters(smem, s);
+        if (n_tiles > cap && !e_s) continue;                         // single wave only
+        // score: CTAs in flight, weighted by bytes each keeps in flight
+        const double score = (double)n_tiles * s * (double)st * nsub * P_TILE_BYTES +
+                             (ctas == 2 ? 1.0 : 0.0);
+        if (score > best_score) {
+          best_score = score;
+          p.nsub = nsub; p.stages = st; p.splits = s; p.n_tiles = n_tiles; p.smem = smem;
+        }
+        break;   // the largest feasible split for this (nsub, ctas)
+      }
+    }
+  }
+  if (best_score < 0) {   // nothing fits in one wave: smallest footprint, no split
+    p.nsub = silu ? 2 : 1;
+    const size_t stage = (size_t)p.nsub * P_TILE_BYTES + (size_t)p.bn * TC_BK * 2;
+    p.stages = (int)((225 * 1024 - 1024 - BAR_BYTES) / stage);
+    if (p.stages > TC_MAX_STAGES) p.stages = TC_MAX_STAGES;
+    p.splits = 1;
+    p.n_tiles = ceil_div(N, 128 * p.nsub);
+    p.smem = (size_t)p.stages * stage + BAR_BYTES + 1024;
   }
   return p;
 }
@@ -408,12 +461,10 @@ template <bool SWAP, int EPI, typename OutT>
 static int launch_tc(const CUtensorMap& mp, const CUtensorMap& mq, const GemmArgs& a, dim3 grid,
                      size_t smem, unsigned cluster, cudaStream_t s) {
   auto k = gemm_tc_kernel<SWAP, EPI, OutT>;
-  static size_t configured = 0;  // per instantiation: largest dynamic smem opted into so far
-  if (smem > configured) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return SLX_ERR_CUDA;
-    configured = smem;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    configure_kernel((const void*)k, 227 * 1024);
+    configured = true;
   }
   return launch_ex(k, grid, dim3(TC_THREADS), smem, s, cluster, mp, mq, a);
 }
@@ -462,6 +513,9 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= N);
   if (M == 0) return SLX_OK;
   GemmPlan p = plan_gemm(M, N, K, epilogue);
+  if (env_int("SLX_GEMM_DEBUG", 0))
+    fprintf(stderr, "[slx_gemm] M=%d N=%d K=%d epi=%d swap=%d bn=%d nsub=%d stages=%d splits=%d tiles=%d smem=%zu\n",
+            M, N, K, epilogue, (int)p.swap, p.bn, p.nsub, p.stages, p.splits, p.n_tiles, p.smem);
   CUtensorMap mp, mq;
   GemmArgs a{};
   a.M = M; a.N = N; a.K = K;

@@ -527,6 +527,7 @@ extern "C" int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ld
       auto k = lora_fused_kernel<bf16>;
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return SLX_ERR_CUDA;
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       return launch_ex(k, gf, dim3(FU_THREADS), smem, s, (unsigned)fks, (bf16*)y, ldy,
                        (const bf16*)x, ldx, n_tok, d_in, fks, kc, slot_rank, slot_scale, max_rank,
                        ta, w);
@@ -534,6 +535,7 @@ extern "C" int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ld
       auto k = lora_fused_kernel<float>;
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return SLX_ERR_CUDA;
+      cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       return launch_ex(k, gf, dim3(FU_THREADS), smem, s, (unsigned)fks, (float*)y, ldy,
                        (const float*)x, ldx, n_tok, d_in, fks, kc, slot_rank, slot_scale, max_rank,
                        ta, w);

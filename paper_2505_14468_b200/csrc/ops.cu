@@ -338,6 +338,7 @@ static int att_attr() {
     if (cudaFuncSetAttribute(attention_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)att_smem<T, D>()) != cudaSuccess)
       return 1;
+    cudaFuncSetAttribute(attention_kernel<T, D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     done = true;
   }
   return 0;
