@@ -415,7 +415,8 @@ static GemmPlan plan_gemm(int M, int N, int K, int epi) {
   for (int nsub = 1; nsub <= 4; nsub *= 2) {
     if (silu && nsub == 1) continue;
     if (nsub * p.bn > 512) continue;
-    if (e_nsub ? nsub != e_nsub : nsub == 4) continue;   // nsub 4 only on request
+    // measured on B200 (tools/gemm_sweep.py): nsub 1 for plain projections, 2 for SiLU pairs
+    if (e_nsub ? nsub != e_nsub : nsub != (silu ? 2 : 1)) continue;
     const size_t stage = (size_t)nsub * P_TILE_BYTES + (size_t)p.bn * TC_BK * 2;
     const size_t red = (size_t)nsub * p.bn * 128 * 4;
     const int n_tiles = ceil_div(N, 128 * nsub);
@@ -434,9 +435,8 @@ static GemmPlan plan_gemm(int M, int N, int K, int epi) {
         if ((s - 1) * ceil_div(p.kblocks, s) >= p.kblocks) continue; // no empty split
         const int cap = max_active_clusters(smem, s);
         if (n_tiles > cap && !e_s) continue;                         // single wave only
-        // score: CTAs in flight, weighted by bytes each keeps in flight
-        const double score = (double)n_tiles * s * (double)st * nsub * P_TILE_BYTES +
-                             (ctas == 2 ? 1.0 : 0.0);
+        // score: independent weight pipelines in flight (2 CTAs/SM preferred), then stages
+        const double score = (double)n_tiles * s * (ctas == 2 ? 1.0 : 0.75) + 0.01 * st;
         if (score > best_score) {
           best_score = score;
           p.nsub = nsub; p.stages = st; p.splits = s; p.n_tiles = n_tiles; p.smem = smem;
