@@ -15,7 +15,7 @@
 
 namespace slx {
 
-constexpr int LORA_TT = 16;       // tokens per tile
+constexpr int LORA_TT = 8;        // tokens per tile (fused decode kernel: 4 CTAs/SM)
 constexpr int LORA_MAX_RANK = 64;
 constexpr int LORA_MAX_KS = 8;    // k-splits of the shrink
 constexpr int PLAN_THREADS = 1024;
@@ -318,7 +318,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 template <typename T>
 __global__ void __launch_bounds__(FU_THREADS)
 lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, int n_tok, int d_in,
-                  int ks, int kc, const int32_t* __restrict__ slot_rank,
+                  int ks, int kc, int ns, const int32_t* __restrict__ slot_rank,
                   const float* __restrict__ slot_scale, int max_rank, TargetArgs ta, LoraWs ws) {
   extern __shared__ __align__(16) uint8_t fsm[];
   pdl_trigger();
@@ -328,42 +328,55 @@ lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, 
   const int tgt = blockIdx.y;
   if (tile_id >= *ws.n_tiles) return;   // uniform over the cluster: no barrier is skipped unevenly
   const LoraTile tile = ws.tiles[tile_id];
+  const int cnt = tile.count;
   const int rank = min(slot_rank[tile.slot], max_rank);
   const int R8 = (rank + 7) & ~7;
   const float scale = slot_scale[tile.slot];
   const int d_out = ta.d_out[tgt];
-  const int ns = ((d_out + ks - 1) / ks + 7) & ~7;         // rows of B per CTA
   const int n_lo = min(d_out, q * ns), n_hi = min(d_out, n_lo + ns);
+  const int nn = n_hi - n_lo;
   const int k_lo = min(d_in, q * kc), k_hi = min(d_in, k_lo + kc);
   const int kl = k_hi - k_lo;
   const bf16* A = reinterpret_cast<const bf16*>(ta.a_ptrs[tgt][tile.slot]);
   const bf16* B = reinterpret_cast<const bf16*>(ta.b_ptrs[tgt][tile.slot]);
+  const int cb = ta.col_blk[tgt], cstr = ta.col_stride[tgt], co = ta.col_off[tgt];
+  // an n-range that stays inside one output column block can move y with 16-byte copies
+  const int col_lo = co + (n_lo / cb) * cstr + (n_lo % cb);
+  const bool y_contig = nn > 0 && (n_lo / cb) == ((n_hi - 1) / cb) && (col_lo % 8) == 0 &&
+                        (ldy % 8) == 0 && (nn % 8) == 0;
 
-  // smem carve: xs [TT][kc] T | as [max_rank][kc] bf16 | bs [ns][max_rank] bf16 | vpart, vfull, toks
+  // smem: xs [TT][kc] T | ys [TT][ns] T | as [max_rank][kc] bf16 | bs [ns][max_rank] bf16 |
+  //       vpart [TT][max_rank] f32 | vfull [TT][max_rank] f32 | toks [TT]
   T* xs = reinterpret_cast<T*>(fsm);
-  bf16* as = reinterpret_cast<bf16*>(fsm + (size_t)LORA_TT * kc * sizeof(T));
+  T* ys = xs + (size_t)LORA_TT * kc;
+  bf16* as = reinterpret_cast<bf16*>(ys + (size_t)LORA_TT * ns);
   bf16* bs = as + (size_t)max_rank * kc;
   float* vpart = reinterpret_cast<float*>(bs + (size_t)ns * max_rank);
-  float* vfull = vpart + LORA_TT * LORA_MAX_RANK;
-  int* toks = reinterpret_cast<int*>(vfull + LORA_TT * LORA_MAX_RANK);
+  float* vfull = vpart + LORA_TT * max_rank;
+  int* toks = reinterpret_cast<int*>(vfull + LORA_TT * max_rank);
 
-  if (threadIdx.x < LORA_TT)
-    toks[threadIdx.x] = threadIdx.x < tile.count ? ws.perm[tile.start + threadIdx.x] : 0;
+  if (threadIdx.x < LORA_TT) toks[threadIdx.x] = threadIdx.x < cnt ? ws.perm[tile.start + threadIdx.x] : 0;
   __syncthreads();
-  // ---- 1. all loads in flight (16-byte cp.async)
+  // ---- 1. every load in flight at once (16-byte cp.async): x chunk, y slice, A chunk, B rows
   constexpr int XV = 16 / sizeof(T);
   const int xchunks = kl / XV;
-  for (int e = threadIdx.x; e < tile.count * xchunks; e += FU_THREADS) {
+  for (int e = threadIdx.x; e < cnt * xchunks; e += FU_THREADS) {
     const int i = e / xchunks, c = e % xchunks;
     cp_async16(xs + (size_t)i * kc + c * XV, x + (size_t)toks[i] * ldx + k_lo + c * XV);
+  }
+  if (y_contig) {
+    const int ychunks = nn / XV;
+    for (int e = threadIdx.x; e < cnt * ychunks; e += FU_THREADS) {
+      const int i = e / ychunks, c = e % ychunks;
+      cp_async16(ys + (size_t)i * ns + c * XV, y + (size_t)toks[i] * ldy + col_lo + c * XV);
+    }
   }
   const int achunks = kl / 8;
   for (int e = threadIdx.x; e < rank * achunks; e += FU_THREADS) {
     const int j = e / achunks, c = e % achunks;
     cp_async16(as + (size_t)j * kc + c * 8, A + (size_t)j * d_in + k_lo + c * 8);
   }
-  // B rows n_lo..n_hi are contiguous: (n_hi - n_lo) * rank elements
-  const int bchunks = (n_hi - n_lo) * rank / 8;
+  const int bchunks = nn * rank / 8;   // B rows n_lo..n_hi are contiguous
   for (int e = threadIdx.x; e < bchunks; e += FU_THREADS) {
     const int flat = e * 8;
     const int n = flat / rank, j = flat % rank;
@@ -374,68 +387,72 @@ lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, 
 
   // ---- 2. partial shrink over this k-chunk: one warp per (i, j) output
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_out = tile.count * rank;
-  for (int o = warp; o < LORA_TT * LORA_MAX_RANK; o += FU_THREADS / 32) {
+  const int n_out = cnt * rank;
+  for (int o = warp; o < n_out; o += FU_THREADS / 32) {
+    const int i = o / rank, j = o % rank;
+    const T* xr = xs + (size_t)i * kc;
+    const bf16* ar = as + (size_t)j * kc;
     float acc = 0.f;
-    if (o < n_out) {
-      const int i = o / rank, j = o % rank;
-      const T* xr = xs + (size_t)i * kc;
-      const bf16* ar = as + (size_t)j * kc;
-      for (int k = lane * 8; k < kl; k += 32 * 8) {
-        float xf[8], af[8];
-        Vec8<T>::load(xr + k, xf);
-        Vec8<bf16>::load(ar + k, af);
+    for (int k = lane * 8; k < kl; k += 32 * 8) {
+      float xf[8], af[8];
+      Vec8<T>::load(xr + k, xf);
+      Vec8<bf16>::load(ar + k, af);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc = fmaf(xf[e], af[e], acc);
-      }
-      acc = warp_sum(acc);
-      if (lane == 0) vpart[i * LORA_MAX_RANK + j] = acc;
-    } else {
-      break;
+      for (int e = 0; e < 8; ++e) acc = fmaf(xf[e], af[e], acc);
     }
+    acc = warp_sum(acc);
+    if (lane == 0) vpart[i * max_rank + j] = acc;
   }
   tc::cluster_sync();
-  // ---- 3. v = sum over the cluster's k-chunks (DSMEM), fixed order
+  // ---- 3. v = sum over the cluster's k-chunks (DSMEM), fixed order, x scale
   const uint32_t vp_base = tc::smem_u32(vpart);
   for (int o = threadIdx.x; o < n_out; o += FU_THREADS) {
     const int i = o / rank, j = o % rank;
-    const uint32_t off = vp_base + (uint32_t)((i * LORA_MAX_RANK + j) * 4);
+    const uint32_t off = vp_base + (uint32_t)((i * max_rank + j) * 4);
     float part[FU_MAX_KS];
 #pragma unroll
     for (int s = 0; s < FU_MAX_KS; ++s) part[s] = s < ks ? tc::ld_dsmem(tc::mapa(off, (uint32_t)s)) : 0.f;
     float a = 0.f;
 #pragma unroll
     for (int s = 0; s < FU_MAX_KS; ++s) a += part[s];
-    vfull[i * LORA_MAX_RANK + j] = a * scale;
+    vfull[i * max_rank + j] = a * scale;
   }
   // peers may still read our vpart: arrive now, wait before exit
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   __syncthreads();
-  // ---- 4. expand + fused add over this CTA's n-range: thread owns 2 consecutive rows
-  const int cb = ta.col_blk[tgt], cstr = ta.col_stride[tgt], co = ta.col_off[tgt];
-  for (int n = n_lo + threadIdx.x * 2; n < n_hi; n += FU_THREADS * 2) {
-    const bf16* br0 = bs + (size_t)(n - n_lo) * max_rank;
-    const bf16* br1 = br0 + max_rank;
-    const bool two = n + 1 < n_hi;
-    const int col0 = co + (n / cb) * cstr + (n % cb);
-    const int col1 = co + ((n + 1) / cb) * cstr + ((n + 1) % cb);
-    for (int i = 0; i < tile.count; ++i) {
-      const float* vr = vfull + i * LORA_MAX_RANK;
-      float d0 = 0.f, d1 = 0.f;
-      for (int j = 0; j < R8; j += 8) {
-        float b0[8], b1[8];
-        Vec8<bf16>::load(br0 + j, b0);
-        Vec8<bf16>::load(br1 + j, b1);
+  // ---- 4. expand + fused add: thread owns 8 consecutive rows n for one token at a time
+  const int ngrp = (nn + 7) / 8;
+  for (int e = threadIdx.x; e < cnt * ngrp; e += FU_THREADS) {
+    const int i = e / ngrp, g8 = e % ngrp;
+    const int n0 = g8 * 8;
+    const float* vr = vfull + i * max_rank;
+    float d[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < R8; j += 8) {
+      float vv[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float v = (j + e < rank) ? vr[j + e] : 0.f;
-          d0 = fmaf(v, b0[e], d0);
-          d1 = fmaf(v, b1[e], d1);
-        }
+      for (int u = 0; u < 8; ++u) vv[u] = (j + u < rank) ? vr[j + u] : 0.f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (n0 + r >= nn) break;
+        float b[8];
+        Vec8<bf16>::load(bs + (size_t)(n0 + r) * max_rank + j, b);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d[r] = fmaf(vv[u], b[u], d[r]);
       }
-      T* yr = y + (size_t)toks[i] * ldy;
-      yr[col0] = from_f32<T>(to_f32(yr[col0]) + d0);
-      if (two) yr[col1] = from_f32<T>(to_f32(yr[col1]) + d1);
+    }
+    T* yr = y + (size_t)toks[i] * ldy;
+    if (y_contig) {
+      float yv[8];
+      Vec8<T>::load(ys + (size_t)i * ns + n0, yv);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) yv[r] += d[r];
+      Vec8<T>::store(yr + col_lo + n0, yv);
+    } else {
+      for (int r = 0; r < 8 && n0 + r < nn; ++r) {
+        const int n = n_lo + n0 + r;
+        const int col = co + (n / cb) * cstr + (n % cb);
+        yr[col] = from_f32<T>(to_f32(yr[col]) + d[r]);
+      }
     }
   }
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -519,8 +536,8 @@ extern "C" int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ld
     for (int i = 0; i < n_targets; ++i) max_dout = targets[i].d_out > max_dout ? targets[i].d_out : max_dout;
     const int ns = ceil_div(ceil_div(max_dout, fks), 8) * 8;
     const size_t tsz = dtype == SLX_DT_BF16 ? 2 : 4;
-    const size_t smem = (size_t)LORA_TT * kc * tsz + (size_t)max_rank * kc * 2 +
-                        (size_t)ns * max_rank * 2 + 2 * LORA_TT * LORA_MAX_RANK * 4 + LORA_TT * 4;
+    const size_t smem = (size_t)LORA_TT * (kc + ns) * tsz + (size_t)max_rank * kc * 2 +
+                        (size_t)ns * max_rank * 2 + 2 * LORA_TT * max_rank * 4 + LORA_TT * 4;
     if (smem > 200 * 1024) return SLX_ERR_UNSUPPORTED;
     dim3 gf((unsigned)(w.max_tiles * fks), (unsigned)n_targets);
     if (dtype == SLX_DT_BF16) {
@@ -529,7 +546,7 @@ extern "C" int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ld
         return SLX_ERR_CUDA;
       cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       return launch_ex(k, gf, dim3(FU_THREADS), smem, s, (unsigned)fks, (bf16*)y, ldy,
-                       (const bf16*)x, ldx, n_tok, d_in, fks, kc, slot_rank, slot_scale, max_rank,
+                       (const bf16*)x, ldx, n_tok, d_in, fks, kc, ns, slot_rank, slot_scale, max_rank,
                        ta, w);
     } else if (dtype == SLX_DT_F32) {
       auto k = lora_fused_kernel<float>;
@@ -537,7 +554,7 @@ extern "C" int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ld
         return SLX_ERR_CUDA;
       cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       return launch_ex(k, gf, dim3(FU_THREADS), smem, s, (unsigned)fks, (float*)y, ldy,
-                       (const float*)x, ldx, n_tok, d_in, fks, kc, slot_rank, slot_scale, max_rank,
+                       (const float*)x, ldx, n_tok, d_in, fks, kc, ns, slot_rank, slot_scale, max_rank,
                        ta, w);
     }
     return SLX_ERR_INVALID;

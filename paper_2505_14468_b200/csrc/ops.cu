@@ -106,123 +106,130 @@ __global__ void rope_kv_kernel(T* __restrict__ qkv, int ld, int H, int Hkv, int 
 }
 
 // ------------------------------------------------------------------ attention over the KV pool
-// One CTA (D threads) per (token, head).  Keys are processed in blocks of KB: the block's K
-// and V rows are staged in shared memory with 16-byte cp.async by the whole CTA (double
-// buffered, so the next block streams while this one is consumed); a thread pair computes
-// one key's score, an online softmax (exp2, fp32) rescales the running output, and thread d
-// accumulates output dimension d.  Causal: token t attends cache positions 0..tok_pos[t].
-template <typename T> struct AttCfg { static constexpr int KB = 64; };
-template <> struct AttCfg<float> { static constexpr int KB = 32; };
+// One CTA of 4 warps per (token, head); warp w streams key chunks c = w, w+4, ... of 32 keys.
+// Lane j of a chunk loads key row j0+j with 16-byte loads (the whole chunk's K in flight at
+// once), computes its score, the warp does an online-softmax update (exp2, fp32), then the
+// chunk's V rows are loaded (lane owns D/32 output dims) and accumulated.  Warps are merged
+// through shared memory at the end.  Causal: token t attends positions 0..tok_pos[t].
+constexpr int ATT_WARPS = 4;
 
-__device__ __forceinline__ void att_cp16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-               "l"(gmem)
-               : "memory");
+// PL consecutive elements -> floats with one vector load (8 B for 4 x bf16, 16 B for 4 x f32).
+template <typename T, int PL> __device__ __forceinline__ void load_pl(const T* p, float* f);
+template <> __device__ __forceinline__ void load_pl<bf16, 4>(const bf16* p, float* f) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+}
+template <> __device__ __forceinline__ void load_pl<bf16, 2>(const bf16* p, float* f) {
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+  f[0] = a.x; f[1] = a.y;
+}
+template <> __device__ __forceinline__ void load_pl<float, 4>(const float* p, float* f) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+}
+template <> __device__ __forceinline__ void load_pl<float, 2>(const float* p, float* f) {
+  const float2 a = *reinterpret_cast<const float2*>(p);
+  f[0] = a.x; f[1] = a.y;
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(D)
+__global__ void __launch_bounds__(ATT_WARPS * 32)
 attention_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv, int ld, int H, int Hkv,
                  const int32_t* __restrict__ tok_pos, const int32_t* __restrict__ tok_seq,
                  const T* __restrict__ kc, const T* __restrict__ vc, int max_ctx, float scale_log2) {
   pdl_trigger();
   pdl_wait();
-  constexpr int KB = AttCfg<T>::KB;
-  constexpr int DP = D + 16 / sizeof(T);       // padded row (16 B) against bank conflicts
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int CH = D / VEC;                   // 16-byte chunks per row
-  extern __shared__ __align__(16) uint8_t asmem[];
-  T* Ks = reinterpret_cast<T*>(asmem);                      // [2][KB][DP]
-  T* Vs = Ks + 2 * KB * DP;                                  // [2][KB][DP]
-  float* qs = reinterpret_cast<float*>(Vs + 2 * KB * DP);    // [D]
-  float* ps = qs + D;                                        // [KB]
-  float* red = ps + KB;                                      // [D/32]
-
+  constexpr int PL = D / 32;   // output dims per lane
+  __shared__ float qs[D];
+  __shared__ float m_s[ATT_WARPS], l_s[ATT_WARPS];
+  __shared__ float acc_s[ATT_WARPS][D];
   const int t = blockIdx.x / H, h = blockIdx.x % H;
   const int hk = h / (H / Hkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_keys = tok_pos[t] + 1;
   const int seq = tok_seq[t];
+  for (int i = threadIdx.x; i < D; i += blockDim.x)
+    qs[i] = to_f32(qkv[(size_t)t * ld + h * D + i]) * scale_log2;
+  __syncthreads();
   const T* kbase = kc + ((size_t)seq * Hkv + hk) * max_ctx * D;
   const T* vbase = vc + ((size_t)seq * Hkv + hk) * max_ctx * D;
-  const int tid = threadIdx.x;
-  qs[tid] = to_f32(qkv[(size_t)t * ld + h * D + tid]) * scale_log2;
-
-  auto stage = [&](int blk, int buf) {
-    const int k0 = blk * KB;
-    const int nk = min(KB, n_keys - k0);
-    for (int e = tid; e < nk * CH; e += D) {
-      const int r = e / CH, c = e % CH;
-      att_cp16(Ks + ((size_t)buf * KB + r) * DP + c * VEC, kbase + (size_t)(k0 + r) * D + c * VEC);
-      att_cp16(Vs + ((size_t)buf * KB + r) * DP + c * VEC, vbase + (size_t)(k0 + r) * D + c * VEC);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-
-  const int nblk = (n_keys + KB - 1) / KB;
-  stage(0, 0);
-  float m = -INFINITY, l = 0.f, acc = 0.f;
-  constexpr int TPK = D / KB;   // threads per key for the score (2 for bf16, 4 for f32 @ D=128)
-  for (int b = 0; b < nblk; ++b) {
-    if (b + 1 < nblk) {
-      stage(b + 1, (b + 1) & 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const int buf = b & 1;
-    const int k0 = b * KB;
-    // scores: TPK threads per key, each a D/TPK slice, shuffle-combined
-    const int key = tid / TPK, part = tid % TPK;
-    float sc = 0.f;
-    {
-      const T* kr = Ks + ((size_t)buf * KB + key) * DP + part * (D / TPK);
-      const float* qr = qs + part * (D / TPK);
+  float m = -INFINITY, l = 0.f;
+  float acc[PL];
 #pragma unroll
-      for (int i = 0; i < D / TPK; i += 8) {
+  for (int i = 0; i < PL; ++i) acc[i] = 0.f;
+  for (int j0 = warp * 32; j0 < n_keys; j0 += ATT_WARPS * 32) {
+    const int nk = min(32, n_keys - j0);
+    // ---- scores: lane = key
+    float sc = -INFINITY;
+    if (lane < nk) {
+      const T* kr = kbase + (size_t)(j0 + lane) * D;
+      float dot = 0.f;
+#pragma unroll
+      for (int i = 0; i < D; i += 8) {
         float f[8];
         Vec8<T>::load(kr + i, f);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) sc = fmaf(qr[i + e], f[e], sc);
+        for (int e = 0; e < 8; ++e) dot = fmaf(qs[i + e], f[e], dot);
+      }
+      sc = dot;
+    }
+    const float m_new = fmaxf(m, warp_max(sc));
+    const float corr = exp2f(m - m_new);
+    const float p = lane < nk ? exp2f(sc - m_new) : 0.f;
+    l = l * corr + warp_sum(p);
+#pragma unroll
+    for (int i = 0; i < PL; ++i) acc[i] *= corr;
+    m = m_new;
+    // ---- P.V: lane owns dims [lane*PL, lane*PL + PL); 16 rows' loads in flight at a time
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float vv[16][PL];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int jj = half * 16 + u;
+        if (jj < nk) load_pl<T, PL>(vbase + (size_t)(j0 + jj) * D + lane * PL, vv[u]);
+        else {
+#pragma unroll
+          for (int i = 0; i < PL; ++i) vv[u][i] = 0.f;
+        }
       }
 #pragma unroll
-      for (int o = 1; o < TPK; o <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-    }
-    if (k0 + key >= n_keys) sc = -INFINITY;
-    // block max over the KB scores
-    float bm = warp_max(sc);
-    if ((tid & 31) == 0) red[tid >> 5] = bm;
-    __syncthreads();
-    bm = red[0];
+      for (int u = 0; u < 16; ++u) {
+        const float pj = __shfl_sync(0xffffffffu, p, half * 16 + u);
 #pragma unroll
-    for (int w = 1; w < D / 32; ++w) bm = fmaxf(bm, red[w]);
-    const float m_new = fmaxf(m, bm);
-    const float corr = exp2f(m - m_new);
-    const float p = exp2f(sc - m_new);
-    if (part == 0) ps[key] = p;
-    __syncthreads();   // ps complete; red free
-    float bl = 0.f;
-    const int nk = min(KB, n_keys - k0);
-    const T* vcol = Vs + (size_t)buf * KB * DP + tid;
-    for (int j = 0; j < nk; ++j) {
-      const float pj = ps[j];
-      bl += pj;
-      acc = fmaf(pj, to_f32(vcol[(size_t)j * DP]), acc * (j == 0 ? corr : 1.f));
+        for (int i = 0; i < PL; ++i) acc[i] = fmaf(pj, vv[u][i], acc[i]);
+      }
     }
-    if (nk == 0) acc *= corr;
-    l = l * corr + bl;
-    m = m_new;
-    __syncthreads();   // buffers reused by the next stage()
   }
-  out[(size_t)t * ldo + h * D + tid] = from_f32<T>(acc / l);
+  if (lane == 0) { m_s[warp] = m; l_s[warp] = l; }
+#pragma unroll
+  for (int i = 0; i < PL; ++i) acc_s[warp][lane * PL + i] = acc[i];
+  __syncthreads();
+  if (warp == 0) {
+    float mg = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < ATT_WARPS; ++w) mg = fmaxf(mg, m_s[w]);
+    float lg = 0.f, cw[ATT_WARPS];
+#pragma unroll
+    for (int w = 0; w < ATT_WARPS; ++w) {
+      cw[w] = (l_s[w] > 0.f) ? exp2f(m_s[w] - mg) : 0.f;
+      lg += l_s[w] * cw[w];
+    }
+    const float inv = 1.0f / lg;
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+      float o = 0.f;
+#pragma unroll
+      for (int w = 0; w < ATT_WARPS; ++w) o += acc_s[w][lane * PL + i] * cw[w];
+      out[(size_t)t * ldo + h * D + lane * PL + i] = from_f32<T>(o * inv);
+    }
+  }
 }
 
 template <typename T, int D>
-constexpr size_t att_smem() {
-  return (size_t)4 * AttCfg<T>::KB * (D + 16 / sizeof(T)) * sizeof(T) +
-         (size_t)(D + AttCfg<T>::KB + D / 32) * 4;
-}
+constexpr size_t att_smem() { return 0; }
 
 // ------------------------------------------------------------------ SiLU * mul (blocked gate/up)
 template <typename T>
@@ -335,9 +342,6 @@ template <typename T, int D>
 static int att_attr() {
   static bool done = false;
   if (!done) {
-    if (cudaFuncSetAttribute(attention_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)att_smem<T, D>()) != cudaSuccess)
-      return 1;
     cudaFuncSetAttribute(attention_kernel<T, D>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     done = true;
   }
@@ -416,10 +420,10 @@ extern "C" int slx_attention(int dtype, void* out, int ldo, const void* qkv, int
   cudaStream_t s = (cudaStream_t)stream;
   int st = SLX_OK;
   if (head_dim == 64) {
-    DISPATCH_DT(dtype, st = att_attr<T, 64>() ? SLX_ERR_CUDA : launch_ex(attention_kernel<T, 64>, dim3(grid), dim3(64), att_smem<T, 64>(), s, 1u, (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
+    DISPATCH_DT(dtype, st = att_attr<T, 64>() ? SLX_ERR_CUDA : launch_ex(attention_kernel<T, 64>, dim3(grid), dim3(ATT_WARPS * 32), 0, s, 1u, (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
                            (const T*)k_cache, (const T*)v_cache, max_ctx, scale));
   } else {
-    DISPATCH_DT(dtype, st = att_attr<T, 128>() ? SLX_ERR_CUDA : launch_ex(attention_kernel<T, 128>, dim3(grid), dim3(128), att_smem<T, 128>(), s, 1u, (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
+    DISPATCH_DT(dtype, st = att_attr<T, 128>() ? SLX_ERR_CUDA : launch_ex(attention_kernel<T, 128>, dim3(grid), dim3(ATT_WARPS * 32), 0, s, 1u, (T*)out, ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq,
                            (const T*)k_cache, (const T*)v_cache, max_ctx, scale));
   }
   return st;
