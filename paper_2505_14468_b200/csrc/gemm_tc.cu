@@ -2,19 +2,23 @@
 //
 //   C[M,N] = A[M,K] . W[N,K]^T  (+ residual | SiLU*mul epilogue), bf16 in, fp32 accumulate.
 //
-// Two tilings of one warp-specialised kernel (warp 0 lane 0: TMA producer, warp 1 lane 0:
-// MMA issuer, all 4 warps: TMEM -> register epilogue):
-//  * NORMAL (prefill, M > 128): D tile = 128 rows of A x BN rows of W, TMEM lane = token.
-//  * SWAP   (decode,  M <= 128): D tile = 128 rows of W x BN (= M padded to 16) tokens;
-//    TMEM lane = output feature.  The weight stream of one tile is split along K over the
-//    S CTAs of a thread-block CLUSTER (S <= 8) so that every SM pulls weights; the S fp32
-//    partial tiles are reduced through distributed shared memory (DSMEM) in a fixed order
-//    (deterministic), each CTA finishing 1/S of the tile's columns with the epilogue.
-//    No global workspace, no atomics, no serial last-CTA tail.
-// PDL: the weight tiles of the first pipeline stages are fetched BEFORE griddepcontrol.wait,
-// overlapping the previous kernel's tail; activations are loaded after it.
-// SiLU*mul: W rows are blocked [gate 128 | up 128] per 128 output features, so one TMEM
-// row (NORMAL) or two accumulators of one CTA (SWAP, nsub = 2) hold gate and up together.
+// One warp-specialised kernel (warp 0 lane 0: TMA producer, warp 1 lane 0: MMA issuer, all 4
+// warps: TMEM -> register epilogue).  The D tile is 128 token rows (TMEM lanes) x 256 weight
+// rows (TMEM columns): the weight operand is always the N = 256 side of tcgen05.mma.kind::f16.
+// A B200 tcgen05 instruction costs about the same time at N = 64 as at N = 256 (measured,
+// tools/probe/mma_probe.cu), so streaming weights as the wide operand needs 4x fewer MMAs per
+// weight byte than a swap-AB (weights-as-M) tiling — decisive for HBM-bound decode.
+//
+//  * prefill (many 128-row token tiles): grid = (N/256, M/128), full K per CTA.
+//  * decode (M <= 128, few tiles): the activation box is only `bm` = M rounded to 16 rows and
+//    the K range of each weight tile is split over the S CTAs of a thread-block CLUSTER (S <= 8)
+//    so that every SM streams weights; the S fp32 partial tiles are reduced through
+//    distributed shared memory (DSMEM) in a fixed order (deterministic), each CTA finishing a
+//    1/S slice of the tile's columns with the epilogue.  No workspace, no atomics.
+// SiLU*mul: W rows are blocked [gate 128 | up 128] per 128 features, so the two halves of one
+// 256-column TMEM tile hold gate and up of the same features.
+// Weights are stored SLX_W_TILED ([N/128][K/64][128][64]) so every TMA box is one contiguous
+// 16 KB burst; PDL: the first stages' weight boxes are fetched BEFORE griddepcontrol.wait.
 //
 // Replaces the modelled prefill/decode time of the reference (batching.py:17-21 T0+alpha(b-1);
 // engine.py:832 prefill work, engine.py:888,909 decode_ms_per_token) with the real projections.
@@ -28,34 +32,46 @@
 namespace slx {
 
 constexpr int TC_THREADS = 128;
-constexpr int TC_BK = 64;  // 64 bf16 = one 128-byte swizzle row
+constexpr int TC_BK = 64;       // 64 bf16 = one 128-byte swizzle row
+constexpr int TC_BN = 256;      // weight rows per tile (MMA N)
 constexpr int TC_MAX_STAGES = 8;
-constexpr int P_TILE_BYTES = 128 * TC_BK * 2;  // 16 KB
+constexpr int W_BLOCK_BYTES = 128 * TC_BK * 2;   // 16 KB: one 128-row weight box
 constexpr int TC_MAX_CLUSTER = 8;
 
 struct GemmArgs {
   int M, N, K;
-  int bn;       // UMMA N
-  int nsub;     // P sub-tiles per CTA (SWAP SiLU: 2)
+  int bm;        // activation rows per tile actually loaded (<= 128, multiple of 16)
   int stages;
   int kblocks;
-  int splits;   // SWAP: cluster size along K
+  int splits;    // cluster size along K (1 = no split)
   int n_tiles;
   void* C;
   int ldc;
   const void* R;
   int ldr;
-  int w_tiled;  // W packed as [N/128][kblocks][128][64] (SLX_W_TILED)
+  int w_tiled;   // W packed as [N/128][kblocks][128][64] (SLX_W_TILED)
 };
 
 template <typename OutT>
 __device__ __forceinline__ void store_out(OutT* p, float v) {
   *p = from_f32<OutT>(v);
 }
-
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
 
-// TMA coordinates of the 128-row weight block `row0` (multiple of 128) at k-block `kb`.
+// 16 consecutive outputs of one row: vector stores for bf16 when the run is in bounds.
+template <typename OutT>
+__device__ __forceinline__ void store16(OutT* row, int n0, int n_lim, const float* v) {
+  if (sizeof(OutT) == 2 && n0 + 16 <= n_lim) {
+    Vec8<bf16>::store(reinterpret_cast<bf16*>(row + n0), v);
+    Vec8<bf16>::store(reinterpret_cast<bf16*>(row + n0 + 8), v + 8);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (n0 + j < n_lim) store_out(row + n0 + j, v[j]);
+  }
+}
+
+// TMA coordinates of the 128-row weight block starting at row0 (multiple of 128), k-block kb.
 __device__ __forceinline__ void w_coord(const GemmArgs& g, int row0, int kb, int& c0, int& c1) {
   if (g.w_tiled) {
     c0 = 0;
@@ -66,36 +82,33 @@ __device__ __forceinline__ void w_coord(const GemmArgs& g, int row0, int kb, int
   }
 }
 
-template <bool SWAP, int EPI, typename OutT>
+template <int EPI, typename OutT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant__ CUtensorMap tmap_q,
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                GemmArgs g) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const int q_tile_bytes = g.bn * TC_BK * 2;
-  const int stage_bytes = g.nsub * P_TILE_BYTES + q_tile_bytes;
+  const int x_bytes = g.bm * TC_BK * 2;
+  const int stage_bytes = x_bytes + 2 * W_BLOCK_BYTES;
   uint64_t* full = (uint64_t*)(smem + g.stages * stage_bytes);
   uint64_t* empty = full + TC_MAX_STAGES;
   uint64_t* accum = empty + TC_MAX_STAGES;
   uint32_t* tmem_slot = (uint32_t*)(accum + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = SWAP ? g.splits : 1;
-  const int tile = SWAP ? blockIdx.x / S : blockIdx.x;
-  const int split = SWAP ? blockIdx.x % S : 0;   // == cluster rank (cluster dims (S,1,1))
+  const int S = g.splits;
+  const int tile = blockIdx.x / S;
+  const int split = blockIdx.x % S;   // == cluster rank (cluster dims (S,1,1))
   const int kb_per = (g.kblocks + S - 1) / S;
   const int kb_lo = split * kb_per;
   const int kb_hi = min(g.kblocks, kb_lo + kb_per);
   const int n_kb = max(0, kb_hi - kb_lo);
-  const int p_row0 = SWAP ? tile * 128 * g.nsub : blockIdx.y * 128;
-  const int q_row0 = SWAP ? 0 : tile * g.bn;
-  const int cols = g.nsub * g.bn;
-  const uint32_t tmem_cols_alloc = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128
-                                   : cols <= 256 ? 256 : 512;
+  const int m0 = blockIdx.y * 128;
+  const int n0 = tile * TC_BN;
 
   if (threadIdx.x == 0) {
-    tc::tma_prefetch_desc(&tmap_p);
-    tc::tma_prefetch_desc(&tmap_q);
+    tc::tma_prefetch_desc(&tmap_x);
+    tc::tma_prefetch_desc(&tmap_w);
     for (int s = 0; s < g.stages; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -103,7 +116,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
     tc::mbar_init(accum, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, tmem_cols_alloc);
+  if (warp == 1) tc::tmem_alloc(tmem_slot, TC_BN);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -114,186 +127,150 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
     // ---------------- TMA producer
     const uint64_t pol_w = tc::policy_evict_first();  // weights: streamed once
     const uint64_t pol_x = tc::policy_evict_last();   // activations: re-read by every tile
-    const int npre = min(n_kb, g.stages);
-    // weight operand: SWAP -> P (nsub blocks of 128 rows), NORMAL -> Q (bn/128 blocks)
     auto load_w = [&](uint8_t* st, uint64_t* bar, int kb) {
-      const int nblk = SWAP ? g.nsub : g.bn / 128;
-      uint8_t* dst = SWAP ? st : st + P_TILE_BYTES;
-      const int row0 = SWAP ? p_row0 : q_row0;
-      for (int b = 0; b < nblk; ++b) {
+      for (int b = 0; b < 2; ++b) {
         int c0, c1;
-        w_coord(g, row0 + b * 128, kb, c0, c1);
-        tc::tma_load_2d(dst + b * P_TILE_BYTES, SWAP ? &tmap_p : &tmap_q, bar, c0, c1, pol_w);
+        w_coord(g, n0 + b * 128, kb, c0, c1);
+        tc::tma_load_2d(st + x_bytes + b * W_BLOCK_BYTES, &tmap_w, bar, c0, c1, pol_w);
       }
     };
-    auto load_x = [&](uint8_t* st, uint64_t* bar, int kb) {
-      if (SWAP)
-        tc::tma_load_2d(st + g.nsub * P_TILE_BYTES, &tmap_q, bar, kb * TC_BK, q_row0, pol_x);
-      else
-        tc::tma_load_2d(st, &tmap_p, bar, kb * TC_BK, p_row0, pol_x);
-    };
+    const int npre = min(n_kb, g.stages);
     // the weight operand of the first stages does not depend on the previous kernel
     for (int i = 0; i < npre; ++i) {
       tc::mbar_arrive_expect_tx(&full[i], stage_bytes);
       load_w(smem + i * stage_bytes, &full[i], kb_lo + i);
     }
     pdl_wait();
-    for (int i = 0; i < npre; ++i) load_x(smem + i * stage_bytes, &full[i], kb_lo + i);
+    for (int i = 0; i < npre; ++i)
+      tc::tma_load_2d(smem + i * stage_bytes, &tmap_x, &full[i], (kb_lo + i) * TC_BK, m0, pol_x);
     for (int i = npre; i < n_kb; ++i) {
       const int s = i % g.stages;
       tc::mbar_wait(&empty[s], ((i / g.stages) & 1) ^ 1);
       uint8_t* st = smem + s * stage_bytes;
       tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
       load_w(st, &full[s], kb_lo + i);
-      load_x(st, &full[s], kb_lo + i);
+      tc::tma_load_2d(st, &tmap_x, &full[s], (kb_lo + i) * TC_BK, m0, pol_x);
     }
   } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer (single thread)
-    const uint32_t idesc = tc::idesc_bf16_f32(128, g.bn);
+    // ---------------- MMA issuer (single thread): D[128 x 256] += X[128 x 16] . W[256 x 16]^T.
+    // Rows >= bm of the X operand read stale shared memory; they only feed D rows that are
+    // never stored.
+    const uint32_t idesc = tc::idesc_bf16_f32(128, TC_BN);
     for (int i = 0; i < n_kb; ++i) {
       const int s = i % g.stages;
       tc::mbar_wait(&full[s], (i / g.stages) & 1);
       tc::fence_after_sync();
       const uint32_t st = tc::smem_u32(smem + s * stage_bytes);
-      const uint32_t q_addr = st + g.nsub * P_TILE_BYTES;
 #pragma unroll
-      for (int ks = 0; ks < TC_BK / 16; ++ks) {
-        const uint64_t bdesc = tc::smem_desc_sw128(q_addr + ks * 32);
-        for (int sub = 0; sub < g.nsub; ++sub) {
-          const uint64_t adesc = tc::smem_desc_sw128(st + sub * P_TILE_BYTES + ks * 32);
-          tc::mma_bf16_ss(tmem_base + sub * g.bn, adesc, bdesc, idesc, (i > 0 || ks > 0) ? 1u : 0u);
-        }
-      }
+      for (int ks = 0; ks < TC_BK / 16; ++ks)
+        tc::mma_bf16_ss(tmem_base, tc::smem_desc_sw128(st + ks * 32),
+                        tc::smem_desc_sw128(st + x_bytes + ks * 32), idesc,
+                        (i > 0 || ks > 0) ? 1u : 0u);
       tc::mma_commit(&empty[s]);
     }
     tc::mma_commit(accum);
   }
 
-  // ---------------- epilogue: all 4 warps; warp w owns TMEM lanes [32w, 32w+32)
+  // ---------------- epilogue: all 4 warps; warp w owns TMEM lanes (token rows) [32w, 32w+32)
   pdl_wait();
   tc::mbar_wait(accum, 0);
   __syncwarp();
   tc::fence_after_sync();
   const int r = warp * 32 + lane;
+  const int m = m0 + r;
+  const bool warp_live = m0 + warp * 32 < g.M && warp * 32 < g.bm;   // warp-uniform
   const uint32_t t_row = tmem_base + ((uint32_t)(warp * 32) << 16);
   OutT* C = reinterpret_cast<OutT*>(g.C);
   const OutT* R = reinterpret_cast<const OutT*>(g.R);
+  const int n_out = EPI == SLX_EPI_SILU_MUL ? g.N / 2 : g.N;
 
-  if (!SWAP) {
-    const int m = p_row0 + r;
-    if (EPI == SLX_EPI_SILU_MUL) {
-      for (int c0 = 0; c0 < 128; c0 += 16) {
-        float gv[16], uv[16];
-        tc::tmem_ld16(t_row + c0, gv);
-        tc::tmem_ld16(t_row + 128 + c0, uv);
-        const int f0 = tile * 128 + c0;
-        if (m < g.M) {
-          if (f0 + 16 <= g.N / 2 && sizeof(OutT) == 2) {
-            float o[16];
+  if (S == 1) {
+    if (warp_live) {
+      if (EPI == SLX_EPI_SILU_MUL) {
+        for (int c0 = 0; c0 < TC_BN / 2; c0 += 16) {
+          float gv[16], uv[16];
+          tc::tmem_ld16(t_row + c0, gv);
+          tc::tmem_ld16(t_row + TC_BN / 2 + c0, uv);
+          if (m < g.M) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) o[j] = silu_f(gv[j]) * uv[j];
-            Vec8<bf16>::store((bf16*)(C + (size_t)m * g.ldc + f0), o);
-            Vec8<bf16>::store((bf16*)(C + (size_t)m * g.ldc + f0 + 8), o + 8);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (f0 + j < g.N / 2) store_out(C + (size_t)m * g.ldc + f0 + j, silu_f(gv[j]) * uv[j]);
+            for (int j = 0; j < 16; ++j) gv[j] = silu_f(gv[j]) * uv[j];
+            store16(C + (size_t)m * g.ldc, tile * (TC_BN / 2) + c0, n_out, gv);
           }
         }
-      }
-    } else {
-      for (int c0 = 0; c0 < g.bn; c0 += 16) {
-        float v[16];
-        tc::tmem_ld16(t_row + c0, v);
-        const int n0 = q_row0 + c0;
-        if (m < g.M) {
-          if (EPI == SLX_EPI_RESIDUAL) {
+      } else {
+        for (int c0 = 0; c0 < TC_BN; c0 += 16) {
+          float v[16];
+          tc::tmem_ld16(t_row + c0, v);
+          const int n = n0 + c0;
+          if (m < g.M) {
+            if (EPI == SLX_EPI_RESIDUAL) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (n0 + j < g.N) v[j] += to_f32(R[(size_t)m * g.ldr + n0 + j]);
-          }
-          if (n0 + 16 <= g.N && sizeof(OutT) == 2) {
-            Vec8<bf16>::store((bf16*)(C + (size_t)m * g.ldc + n0), v);
-            Vec8<bf16>::store((bf16*)(C + (size_t)m * g.ldc + n0 + 8), v + 8);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (n0 + j < g.N) store_out(C + (size_t)m * g.ldc + n0 + j, v[j]);
+              for (int j = 0; j < 16; ++j)
+                if (n + j < g.N) v[j] += to_f32(R[(size_t)m * g.ldr + n + j]);
+            }
+            store16(C + (size_t)m * g.ldc, n, n_out, v);
           }
         }
       }
     }
-  } else if (S == 1) {
-    // SWAP, whole K in this CTA: TMEM lane r = output feature, column c = token.
-    // Non-SiLU: sub-tile `sub` covers W rows tile*128*nsub + sub*128.  SiLU: sub pair
-    // (2p, 2p+1) = (gate, up) of feature block tile*nsub/2 + p.
-    const int npair = EPI == SLX_EPI_SILU_MUL ? g.nsub / 2 : g.nsub;
-    for (int p = 0; p < npair; ++p)
-      for (int c0 = 0; c0 < g.bn && c0 < g.M; c0 += 16) {
-        float v0[16], v1[16];
-        if (EPI == SLX_EPI_SILU_MUL) {
-          tc::tmem_ld16(t_row + (2 * p) * g.bn + c0, v0);
-          tc::tmem_ld16(t_row + (2 * p + 1) * g.bn + c0, v1);
-        } else {
-          tc::tmem_ld16(t_row + p * g.bn + c0, v0);
-        }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int m = c0 + j;
-          if (m >= g.M) break;
-          if (EPI == SLX_EPI_SILU_MUL) {
-            const int f = (tile * npair + p) * 128 + r;
-            if (f < g.N / 2) store_out(C + (size_t)m * g.ldc + f, silu_f(v0[j]) * v1[j]);
-          } else {
-            const int n = (tile * npair + p) * 128 + r;
-            if (n < g.N) {
-              float o = v0[j];
-              if (EPI == SLX_EPI_RESIDUAL) o += to_f32(R[(size_t)m * g.ldr + n]);
-              store_out(C + (size_t)m * g.ldc + n, o);
-            }
-          }
-        }
-      }
   } else {
-    // SWAP split-K over the cluster: stage this CTA's partial tile in its (now idle) pipeline
-    // smem as red[sub][c][r], then reduce 1/S of the columns across the cluster via DSMEM.
+    // split-K over the cluster: stage this CTA's partial tile (rows < bm) in its idle pipeline
+    // smem as red[col][row], then reduce a 1/S slice of the columns across the cluster (DSMEM).
     float* red = reinterpret_cast<float*>(smem);
-    for (int sub = 0; sub < g.nsub; ++sub)
-      for (int c0 = 0; c0 < g.bn && c0 < g.M; c0 += 16) {
+    if (warp_live) {
+      for (int c0 = 0; c0 < TC_BN; c0 += 16) {
         float v[16];
-        tc::tmem_ld16(t_row + sub * g.bn + c0, v);
+        tc::tmem_ld16(t_row + c0, v);
+        if (r < g.bm) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) red[(sub * g.bn + c0 + j) * 128 + r] = v[j];
+          for (int j = 0; j < 16; ++j) red[(c0 + j) * g.bm + r] = v[j];
+        }
       }
+    }
     tc::cluster_sync();
     const uint32_t red_base = tc::smem_u32(red);
-    const int npair = EPI == SLX_EPI_SILU_MUL ? g.nsub / 2 : g.nsub;
-    const int per = EPI == SLX_EPI_SILU_MUL ? 2 : 1;
-    // work items (p, m): this CTA takes m = split, split + S, ...
-    for (int p = 0; p < npair; ++p)
-      for (int m = split; m < g.M && m < g.bn; m += S) {
-        float acc[2] = {0.f, 0.f};
-        for (int u = 0; u < per; ++u) {
-          const int sub = p * per + u;
-          const uint32_t off = red_base + (uint32_t)(((sub * g.bn + m) * 128 + r) * 4);
+    // this CTA's slice: output features [f_lo, f_hi) of the tile (SiLU: 128 features)
+    const int feats = EPI == SLX_EPI_SILU_MUL ? TC_BN / 2 : TC_BN;
+    const int fw = ((feats + S - 1) / S + 15) / 16 * 16;
+    const int f_lo = min(feats, split * fw), f_hi = min(feats, f_lo + fw);
+    if (warp_live && m < g.M && r < g.bm) {
+      for (int f0 = f_lo; f0 < f_hi; f0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
           float part[TC_MAX_CLUSTER];
+          const uint32_t off = red_base + (uint32_t)(((f0 + j) * g.bm + r) * 4);
 #pragma unroll
           for (int s = 0; s < TC_MAX_CLUSTER; ++s)
             part[s] = s < S ? tc::ld_dsmem(tc::mapa(off, (uint32_t)s)) : 0.f;
           float a = 0.f;
 #pragma unroll
           for (int s = 0; s < TC_MAX_CLUSTER; ++s) a += part[s];   // fixed order: deterministic
-          acc[u] = a;
+          if (EPI == SLX_EPI_SILU_MUL) {
+            const uint32_t offu = off + (uint32_t)(TC_BN / 2 * g.bm * 4);
+#pragma unroll
+            for (int s = 0; s < TC_MAX_CLUSTER; ++s)
+              part[s] = s < S ? tc::ld_dsmem(tc::mapa(offu, (uint32_t)s)) : 0.f;
+            float u = 0.f;
+#pragma unroll
+            for (int s = 0; s < TC_MAX_CLUSTER; ++s) u += part[s];
+            a = silu_f(a) * u;
+          }
+          v[j] = a;
         }
-        const int n = (tile * npair + p) * 128 + r;
         if (EPI == SLX_EPI_SILU_MUL) {
-          if (n < g.N / 2) store_out(C + (size_t)m * g.ldc + n, silu_f(acc[0]) * acc[1]);
-        } else if (n < g.N) {
-          float o = acc[0];
-          if (EPI == SLX_EPI_RESIDUAL) o += to_f32(R[(size_t)m * g.ldr + n]);
-          store_out(C + (size_t)m * g.ldc + n, o);
+          store16(C + (size_t)m * g.ldc, tile * (TC_BN / 2) + f0, n_out, v);
+        } else {
+          const int n = n0 + f0;
+          if (EPI == SLX_EPI_RESIDUAL) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (n + j < g.N) v[j] += to_f32(R[(size_t)m * g.ldr + n + j]);
+          }
+          store16(C + (size_t)m * g.ldc, n, n_out, v);
         }
       }
+    }
     tc::cluster_sync();  // keep our smem alive until every peer finished reading it
   }
 
@@ -301,7 +278,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_p, const __grid_constant
   __syncthreads();
   if (warp == 1) {
     tc::fence_after_sync();
-    tc::tmem_dealloc(tmem_base, tmem_cols_alloc);
+    tc::tmem_dealloc(tmem_base, TC_BN);
   }
 }
 
@@ -338,35 +315,33 @@ static bool make_tmap(CUtensorMap* map, const void* ptr, int rows, int cols, int
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-struct GemmPlan {
-  bool swap;
-  int bn, nsub, stages, kblocks, splits, n_tiles;
-  size_t smem;
-};
-
-static constexpr size_t BAR_BYTES = 2 * TC_MAX_STAGES * 8 + 8 + 16;
-
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return (e && *e) ? atoi(e) : dflt;
 }
 
-static void configure_kernel(const void* k, size_t smem) {
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  // without this the driver may pick an L1-heavy carveout that fits only one CTA per SM
+static void configure_kernel(const void* k) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  // without this the driver may pick an L1-heavy carveout that fits fewer CTAs per SM
   cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
-// Max co-resident clusters of `cluster` CTAs with `smem` bytes each (cached; queried on the
-// swap-AB kernel, whose resource footprint is the same for every epilogue instantiation).
+struct GemmPlan {
+  int bm, stages, kblocks, splits, n_tiles, m_tiles;
+  size_t smem;
+};
+
+static constexpr size_t BAR_BYTES = 2 * TC_MAX_STAGES * 8 + 8 + 16;
+
+// Max co-resident clusters of `cluster` CTAs with `smem` bytes each (cached).
 static int max_active_clusters(size_t smem, int cluster) {
   struct Key { size_t smem; int cluster; int value; };
   static Key cache[64];
   static int n_cache = 0;
   for (int i = 0; i < n_cache; ++i)
     if (cache[i].smem == smem && cache[i].cluster == cluster) return cache[i].value;
-  const void* k = (const void*)gemm_tc_kernel<true, SLX_EPI_NONE, bf16>;
-  configure_kernel(k, 227 * 1024);
+  auto k = gemm_tc_kernel<SLX_EPI_NONE, bf16>;
+  configure_kernel((const void*)k);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cluster * 64);
   cfg.blockDim = dim3(TC_THREADS);
@@ -379,109 +354,86 @@ static int max_active_clusters(size_t smem, int cluster) {
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, gemm_tc_kernel<true, SLX_EPI_NONE, bf16>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n <= 0) {
     (void)cudaGetLastError();
-    n = sm_count() / cluster;  // conservative fallback
+    n = sm_count() / cluster;
   }
   if (n_cache < 64) cache[n_cache++] = Key{smem, cluster, n};
   return n;
 }
 
-// SWAP (decode) tiling: one CTA streams nsub x 128 weight rows over a k-range; the k-range
-// of a tile is split over a cluster of S CTAs.  The planner picks, among nsub in {1,2}
-// (SiLU: 2) and 2 or 1 CTAs per SM, the split S that puts the most CTAs in flight while all
-// clusters stay co-resident (one wave, cudaOccupancyMaxActiveClusters) and every split keeps
-// >= 4 k-blocks.  SLX_GEMM_{NSUB,CTAS,STAGES,SPLITS} override for tuning (tools/gemm_sweep.py).
-
-static GemmPlan plan_gemm(int M, int N, int K, int epi) {
+// Few tiles (decode): pick CTAs/SM (1 or 2) and the cluster split S that cover the most SMs
+// in ONE wave (cudaOccupancyMaxActiveClusters), every split keeping >= 4 k-blocks and its
+// partial tile fitting the pipeline smem.  SLX_GEMM_{CTAS,SPLITS,STAGES} override (tuning).
+static GemmPlan plan_gemm(int M, int N, int K) {
   GemmPlan p{};
   p.kblocks = ceil_div(K, TC_BK);
-  p.swap = M <= 128;
-  if (!p.swap) {
-    p.bn = 256;
-    p.nsub = 1;
-    p.stages = 4;
-    p.n_tiles = ceil_div(N, p.bn);
-    p.splits = 1;
-    p.smem = (size_t)p.stages * (P_TILE_BYTES + p.bn * TC_BK * 2) + BAR_BYTES + 1024;
-    return p;
-  }
-  p.bn = ((M + 15) / 16) * 16;
-  if (p.bn < 16) p.bn = 16;
-  const bool silu = epi == SLX_EPI_SILU_MUL;
-  const int e_nsub = env_int("SLX_GEMM_NSUB", 0), e_ctas = env_int("SLX_GEMM_CTAS", 0);
-  const int e_st = env_int("SLX_GEMM_STAGES", 0), e_s = env_int("SLX_GEMM_SPLITS", 0);
-  double best_score = -1.0;
-  for (int nsub = 1; nsub <= 4; nsub *= 2) {
-    if (silu && nsub == 1) continue;
-    if (nsub * p.bn > 512) continue;
-    // measured on B200 (tools/gemm_sweep.py): nsub 1 for plain projections, 2 for SiLU pairs
-    if (e_nsub ? nsub != e_nsub : nsub != (silu ? 2 : 1)) continue;
-    const size_t stage = (size_t)nsub * P_TILE_BYTES + (size_t)p.bn * TC_BK * 2;
-    const size_t red = (size_t)nsub * p.bn * 128 * 4;
-    const int n_tiles = ceil_div(N, 128 * nsub);
-    for (int ctas = 2; ctas >= 1; --ctas) {
-      if (e_ctas && ctas != e_ctas) continue;
-      const size_t budget = ctas == 2 ? 112 * 1024 - 1024 - BAR_BYTES : 225 * 1024 - 1024 - BAR_BYTES;
-      int st = (int)(budget / stage);
-      st = st > (ctas == 2 ? 6 : TC_MAX_STAGES) ? (ctas == 2 ? 6 : TC_MAX_STAGES) : st;
-      if (e_st >= 2 && e_st < st) st = e_st;
-      if (st < 2) continue;
-      const size_t smem = (size_t)st * stage + BAR_BYTES + 1024;
-      for (int s = TC_MAX_CLUSTER; s >= 1; --s) {
-        if (e_s && s != e_s) continue;
-        if (s > 1 && (size_t)st * stage < red) continue;            // partials must fit in smem
-        if (s > 1 && ceil_div(p.kblocks, s) < 4 && !e_s) continue;   // >= 4 k-blocks per split
-        if ((s - 1) * ceil_div(p.kblocks, s) >= p.kblocks) continue; // no empty split
-        const int cap = max_active_clusters(smem, s);
-        if (n_tiles > cap && !e_s) continue;                         // single wave only
-        // score: independent weight pipelines in flight (2 CTAs/SM preferred), then stages
-        const double score = (double)n_tiles * s * (ctas == 2 ? 1.0 : 0.75) + 0.01 * st;
-        if (score > best_score) {
-          best_score = score;
-          p.nsub = nsub; p.stages = st; p.splits = s; p.n_tiles = n_tiles; p.smem = smem;
-        }
-        break;   // the largest feasible split for this (nsub, ctas)
+  p.n_tiles = ceil_div(N, TC_BN);
+  p.m_tiles = ceil_div(M, 128);
+  p.bm = M >= 128 ? 128 : ((M + 15) / 16) * 16;
+  const size_t stage = (size_t)p.bm * TC_BK * 2 + 2 * W_BLOCK_BYTES;
+  const size_t red = (size_t)TC_BN * p.bm * 4;
+  const int sms = sm_count();
+  const int tiles = p.n_tiles * p.m_tiles;
+  const int e_ctas = env_int("SLX_GEMM_CTAS", 0), e_s = env_int("SLX_GEMM_SPLITS", 0);
+  const int e_st = env_int("SLX_GEMM_STAGES", 0);
+  double best = -1.0;
+  for (int ctas = 1; ctas <= 2; ++ctas) {
+    if (e_ctas && ctas != e_ctas) continue;
+    const size_t budget = ctas == 2 ? 112 * 1024 - 1024 - BAR_BYTES : 225 * 1024 - 1024 - BAR_BYTES;
+    int st = (int)(budget / stage);
+    st = st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
+    if (e_st >= 2 && e_st < st) st = e_st;
+    if (st < 2) continue;
+    const size_t smem = (size_t)st * stage + BAR_BYTES + 1024;
+    for (int s = 1; s <= TC_MAX_CLUSTER; ++s) {
+      if (e_s && s != e_s) continue;
+      if (s > 1 && (p.m_tiles > 1 || (size_t)st * stage < red)) continue;
+      if (!e_s && s > 1 && ceil_div(p.kblocks, s) < 4) continue;
+      if ((s - 1) * ceil_div(p.kblocks, s) >= p.kblocks && s > 1) continue;   // no empty split
+      const int ctas_total = tiles * s;
+      if (!e_s && ctas_total > ctas * sms) continue;                            // one wave
+      if (s > 1 && !e_s && tiles > max_active_clusters(smem, s)) continue;
+      const int covered = ctas_total < sms ? ctas_total : sms;
+      const double score = covered * 1000.0 + st * 10.0 - ctas;   // SMs covered, then depth
+      if (score > best) {
+        best = score;
+        p.stages = st; p.splits = s; p.smem = smem;
       }
     }
   }
-  if (best_score < 0) {   // nothing fits in one wave: smallest footprint, no split
-    p.nsub = silu ? 2 : 1;
-    const size_t stage = (size_t)p.nsub * P_TILE_BYTES + (size_t)p.bn * TC_BK * 2;
-    p.stages = (int)((225 * 1024 - 1024 - BAR_BYTES) / stage);
-    if (p.stages > TC_MAX_STAGES) p.stages = TC_MAX_STAGES;
+  if (best < 0) {   // many tiles (prefill) or overrides that cannot apply: one CTA/SM, no split
     p.splits = 1;
-    p.n_tiles = ceil_div(N, 128 * p.nsub);
+    int st = (int)((225 * 1024 - 1024 - BAR_BYTES) / stage);
+    p.stages = st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
+    if (p.stages > 4 && tiles >= sms) p.stages = 4;
     p.smem = (size_t)p.stages * stage + BAR_BYTES + 1024;
   }
   return p;
 }
 
-template <bool SWAP, int EPI, typename OutT>
-static int launch_tc(const CUtensorMap& mp, const CUtensorMap& mq, const GemmArgs& a, dim3 grid,
+template <int EPI, typename OutT>
+static int launch_tc(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& a, dim3 grid,
                      size_t smem, unsigned cluster, cudaStream_t s) {
-  auto k = gemm_tc_kernel<SWAP, EPI, OutT>;
+  auto k = gemm_tc_kernel<EPI, OutT>;
   static bool configured = false;  // per instantiation
   if (!configured) {
-    configure_kernel((const void*)k, 227 * 1024);
+    configure_kernel((const void*)k);
     configured = true;
   }
-  return launch_ex(k, grid, dim3(TC_THREADS), smem, s, cluster, mp, mq, a);
+  return launch_ex(k, grid, dim3(TC_THREADS), smem, s, cluster, mx, mw, a);
 }
 
-template <bool SWAP>
-static int dispatch_tc(int epi, int c_dtype, const CUtensorMap& mp, const CUtensorMap& mq,
+static int dispatch_tc(int epi, int c_dtype, const CUtensorMap& mx, const CUtensorMap& mw,
                        const GemmArgs& a, dim3 grid, size_t smem, unsigned cl, cudaStream_t s) {
   if (c_dtype == SLX_DT_BF16) {
-    if (epi == SLX_EPI_NONE) return launch_tc<SWAP, SLX_EPI_NONE, bf16>(mp, mq, a, grid, smem, cl, s);
-    if (epi == SLX_EPI_RESIDUAL)
-      return launch_tc<SWAP, SLX_EPI_RESIDUAL, bf16>(mp, mq, a, grid, smem, cl, s);
-    return launch_tc<SWAP, SLX_EPI_SILU_MUL, bf16>(mp, mq, a, grid, smem, cl, s);
+    if (epi == SLX_EPI_NONE) return launch_tc<SLX_EPI_NONE, bf16>(mx, mw, a, grid, smem, cl, s);
+    if (epi == SLX_EPI_RESIDUAL) return launch_tc<SLX_EPI_RESIDUAL, bf16>(mx, mw, a, grid, smem, cl, s);
+    return launch_tc<SLX_EPI_SILU_MUL, bf16>(mx, mw, a, grid, smem, cl, s);
   }
-  if (epi == SLX_EPI_NONE) return launch_tc<SWAP, SLX_EPI_NONE, float>(mp, mq, a, grid, smem, cl, s);
-  if (epi == SLX_EPI_RESIDUAL)
-    return launch_tc<SWAP, SLX_EPI_RESIDUAL, float>(mp, mq, a, grid, smem, cl, s);
-  return launch_tc<SWAP, SLX_EPI_SILU_MUL, float>(mp, mq, a, grid, smem, cl, s);
+  if (epi == SLX_EPI_NONE) return launch_tc<SLX_EPI_NONE, float>(mx, mw, a, grid, smem, cl, s);
+  if (epi == SLX_EPI_RESIDUAL) return launch_tc<SLX_EPI_RESIDUAL, float>(mx, mw, a, grid, smem, cl, s);
+  return launch_tc<SLX_EPI_SILU_MUL, float>(mx, mw, a, grid, smem, cl, s);
 }
 
 }  // namespace slx
@@ -510,33 +462,27 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   } else {
     SLX_CHECK_ARG(N % 16 == 0 && ldc >= N);
   }
-  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= N);
+  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= N && ldr % 8 == 0);
   if (M == 0) return SLX_OK;
-  GemmPlan p = plan_gemm(M, N, K, epilogue);
+  GemmPlan p = plan_gemm(M, N, K);
   if (env_int("SLX_GEMM_DEBUG", 0))
-    fprintf(stderr, "[slx_gemm] M=%d N=%d K=%d epi=%d swap=%d bn=%d nsub=%d stages=%d splits=%d tiles=%d smem=%zu\n",
-            M, N, K, epilogue, (int)p.swap, p.bn, p.nsub, p.stages, p.splits, p.n_tiles, p.smem);
-  CUtensorMap mp, mq;
+    fprintf(stderr, "[slx_gemm] M=%d N=%d K=%d epi=%d bm=%d stages=%d splits=%d tiles=%dx%d smem=%zu\n",
+            M, N, K, epilogue, p.bm, p.stages, p.splits, p.n_tiles, p.m_tiles, p.smem);
   GemmArgs a{};
   a.M = M; a.N = N; a.K = K;
-  a.bn = p.bn; a.nsub = p.nsub; a.stages = p.stages; a.kblocks = p.kblocks;
-  a.splits = p.splits; a.n_tiles = p.n_tiles;
+  a.bm = p.bm; a.stages = p.stages; a.kblocks = p.kblocks; a.splits = p.splits;
+  a.n_tiles = p.n_tiles;
   a.C = C; a.ldc = ldc; a.R = R; a.ldr = ldr;
   a.w_tiled = w_layout == SLX_W_TILED;
-  cudaStream_t s = (cudaStream_t)stream;
   // tiled W: a [n_blocks * kblocks * 128, 64] matrix of contiguous 16 KB boxes
   const int w_rows = a.w_tiled ? ceil_div(N, 128) * p.kblocks * 128 : N;
   const int w_cols = a.w_tiled ? TC_BK : K;
-  if (p.swap) {
-    if (!make_tmap(&mp, W, w_rows, w_cols, w_cols, 128) || !make_tmap(&mq, A, M, K, lda, p.bn))
-      return SLX_ERR_CUDA;
-    dim3 grid((unsigned)(p.n_tiles * p.splits), 1);
-    return dispatch_tc<true>(epilogue, c_dtype, mp, mq, a, grid, p.smem, (unsigned)p.splits, s);
-  }
-  if (!make_tmap(&mp, A, M, K, lda, 128) || !make_tmap(&mq, W, w_rows, w_cols, w_cols, 128))
+  CUtensorMap mx, mw;
+  if (!make_tmap(&mx, A, M, K, lda, p.bm) || !make_tmap(&mw, W, w_rows, w_cols, w_cols, 128))
     return SLX_ERR_CUDA;
-  dim3 grid((unsigned)p.n_tiles, (unsigned)ceil_div(M, 128));
-  return dispatch_tc<false>(epilogue, c_dtype, mp, mq, a, grid, p.smem, 1u, s);
+  dim3 grid((unsigned)(p.n_tiles * p.splits), (unsigned)p.m_tiles);
+  return dispatch_tc(epilogue, c_dtype, mx, mw, a, grid, p.smem, (unsigned)p.splits,
+                     (cudaStream_t)stream);
 }
 
 // ------------------------------------------------------------------ weight packing

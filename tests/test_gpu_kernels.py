@@ -39,18 +39,25 @@ def test_gemm_matches_torch_fp32(M, N, K, tiled):
     torch.testing.assert_close(out.float(), ref, rtol=1e-2, atol=1e-2)
 
 
-@pytest.mark.parametrize("nsub,ctas,splits", [(1, 1, 1), (1, 2, 8), (2, 1, 3), (4, 1, 6), (4, 2, 2)])
-def test_gemm_decode_tilings(nsub, ctas, splits, monkeypatch):
-    """Every swap-AB tiling the planner can pick gives the same (deterministic) result."""
-    M, N, K = 64, 3072, 4096
+@pytest.mark.parametrize("M", [1, 64, 100])
+@pytest.mark.parametrize("ctas,splits", [(1, 1), (2, 8), (1, 3), (1, 6), (2, 2), (1, 5)])
+def test_gemm_decode_tilings(M, ctas, splits, monkeypatch):
+    """Every cluster split-K tiling the planner can pick gives the same result."""
+    N, K = 3072, 4096
     a = bf(torch.randn(M, K, device=DEV))
     w = bf(torch.randn(N, K, device=DEV) * 0.05)
     ref = a.float() @ w.float().T
-    monkeypatch.setenv("SLX_GEMM_NSUB", str(nsub))
     monkeypatch.setenv("SLX_GEMM_CTAS", str(ctas))
     monkeypatch.setenv("SLX_GEMM_SPLITS", str(splits))
     out = ops.gemm(a, ops.pack_weight(w), out_dtype=torch.float32)
     torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
+    # SiLU and residual epilogues through the same split-K reduction
+    r = bf(torch.randn(M, N, device=DEV))
+    o2 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_RESIDUAL, residual=r, out_dtype=torch.float32)
+    torch.testing.assert_close(o2, ref + r.float(), rtol=1e-4, atol=1e-2)
+    g_, u_ = ref.view(M, N // 256, 2, 128)[:, :, 0], ref.view(M, N // 256, 2, 128)[:, :, 1]
+    o3 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_SILU_MUL, out_dtype=torch.float32)
+    torch.testing.assert_close(o3, (g_ * torch.sigmoid(g_) * u_).reshape(M, N // 2), rtol=1e-3, atol=1e-3)
 
 
 @pytest.mark.parametrize("M", [3, 64, 200])

@@ -38,6 +38,16 @@ def main():
               ("gate_up", 22016, 4096, EPI_SILU_MUL), ("down", 4096, 11008, EPI_RESIDUAL),
               ("lm_head", 32000, 4096, EPI_NONE)]
     best = {}
+    for k in ("SLX_GEMM_CTAS", "SLX_GEMM_SPLITS"):
+        os.environ.pop(k, None)
+    for name, N, K, epi in shapes:   # planner's own choice first
+        a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
+        w = ops.pack_weight((torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16))
+        c = torch.empty(M, N // 2 if epi == EPI_SILU_MUL else N, device=DEV, dtype=torch.bfloat16)
+        r = torch.randn(M, N, device=DEV).to(torch.bfloat16) if epi == EPI_RESIDUAL else None
+        ms = timeit(lambda: ops.gemm(a, w, c, epilogue=epi, residual=r))
+        print(json.dumps({"gemm": name, "planner": True, "us": round(ms * 1000, 2),
+                          "GB/s": round(N * K * 2 / ms / 1e6, 1)}), flush=True)
     for name, N, K, epi in shapes:
         a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
         w = ops.pack_weight((torch.randn(N, K, device=DEV) * 0.02).to(torch.bfloat16))
@@ -46,15 +56,13 @@ def main():
         r = torch.randn(M, N, device=DEV).to(torch.bfloat16) if epi == EPI_RESIDUAL else None
         ref = None
         byts = N * K * 2
-        for nsub, ctas, splits in itertools.product([1, 2, 4], [1, 2], [1, 2, 3, 4, 6, 8]):
-            if epi == EPI_SILU_MUL and nsub == 1:
-                continue
-            os.environ.update(SLX_GEMM_NSUB=str(nsub), SLX_GEMM_CTAS=str(ctas),
-                              SLX_GEMM_SPLITS=str(splits))
+        for ctas, splits in itertools.product([1, 2], [1, 2, 3, 4, 5, 6, 8]):
+            nsub = 0
+            os.environ.update(SLX_GEMM_CTAS=str(ctas), SLX_GEMM_SPLITS=str(splits))
             try:
                 ms = timeit(lambda: ops.gemm(a, w, c, epilogue=epi, residual=r))
             except Exception as e:  # noqa: BLE001
-                print(json.dumps({"gemm": name, "nsub": nsub, "ctas": ctas, "splits": splits,
+                print(json.dumps({"gemm": name, "ctas": ctas, "splits": splits,
                                   "error": str(e)[:80]}))
                 continue
             out = c.float()
@@ -62,7 +70,7 @@ def main():
                 ref = out.clone()
             ok = torch.allclose(out, ref, rtol=2e-2, atol=2e-2)
             gbs = byts / ms / 1e6
-            rec = {"gemm": name, "nsub": nsub, "ctas": ctas, "splits": splits,
+            rec = {"gemm": name, "ctas": ctas, "splits": splits,
                    "us": round(ms * 1000, 2), "GB/s": round(gbs, 1), "ok": ok}
             print(json.dumps(rec), flush=True)
             if ok and (name not in best or gbs > best[name]["GB/s"]):
