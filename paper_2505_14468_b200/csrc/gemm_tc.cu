@@ -215,15 +215,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     }
   } else {
     // split-K over the cluster: stage this CTA's partial tile (rows < bm) in its idle pipeline
-    // smem as red[col][row], then reduce a 1/S slice of the columns across the cluster (DSMEM).
+    // smem as red[row][col] (row stride RED_LD floats, padded against bank conflicts), then
+    // reduce a 1/S slice of the columns across the cluster with 16-byte DSMEM loads.
+    constexpr int RED_LD = TC_BN + 4;
     float* red = reinterpret_cast<float*>(smem);
     if (warp_live) {
       for (int c0 = 0; c0 < TC_BN; c0 += 16) {
         float v[16];
         tc::tmem_ld16(t_row + c0, v);
         if (r < g.bm) {
+          float4* dst = reinterpret_cast<float4*>(red + (size_t)r * RED_LD + c0);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) red[(c0 + j) * g.bm + r] = v[j];
+          for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
       }
     }
@@ -233,32 +236,34 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     const int feats = EPI == SLX_EPI_SILU_MUL ? TC_BN / 2 : TC_BN;
     const int fw = ((feats + S - 1) / S + 15) / 16 * 16;
     const int f_lo = min(feats, split * fw), f_hi = min(feats, f_lo + fw);
+    auto reduce16 = [&](int col0, float* out) {   // sum over the cluster of red[r][col0..col0+16)
+#pragma unroll
+      for (int j = 0; j < 16; ++j) out[j] = 0.f;
+      const uint32_t off = red_base + (uint32_t)((r * RED_LD + col0) * 4);
+#pragma unroll
+      for (int s = 0; s < TC_MAX_CLUSTER; ++s) {   // fixed order: deterministic
+        if (s < S) {
+          const uint32_t ra = tc::mapa(off, (uint32_t)s);
+          float4 q[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) q[u] = tc::ld_dsmem4(ra + u * 16);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            out[4 * u] += q[u].x; out[4 * u + 1] += q[u].y;
+            out[4 * u + 2] += q[u].z; out[4 * u + 3] += q[u].w;
+          }
+        }
+      }
+    };
     if (warp_live && m < g.M && r < g.bm) {
       for (int f0 = f_lo; f0 < f_hi; f0 += 16) {
         float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float part[TC_MAX_CLUSTER];
-          const uint32_t off = red_base + (uint32_t)(((f0 + j) * g.bm + r) * 4);
-#pragma unroll
-          for (int s = 0; s < TC_MAX_CLUSTER; ++s)
-            part[s] = s < S ? tc::ld_dsmem(tc::mapa(off, (uint32_t)s)) : 0.f;
-          float a = 0.f;
-#pragma unroll
-          for (int s = 0; s < TC_MAX_CLUSTER; ++s) a += part[s];   // fixed order: deterministic
-          if (EPI == SLX_EPI_SILU_MUL) {
-            const uint32_t offu = off + (uint32_t)(TC_BN / 2 * g.bm * 4);
-#pragma unroll
-            for (int s = 0; s < TC_MAX_CLUSTER; ++s)
-              part[s] = s < S ? tc::ld_dsmem(tc::mapa(offu, (uint32_t)s)) : 0.f;
-            float u = 0.f;
-#pragma unroll
-            for (int s = 0; s < TC_MAX_CLUSTER; ++s) u += part[s];
-            a = silu_f(a) * u;
-          }
-          v[j] = a;
-        }
+        reduce16(f0, v);
         if (EPI == SLX_EPI_SILU_MUL) {
+          float u[16];
+          reduce16(f0 + TC_BN / 2, u);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = silu_f(v[j]) * u[j];
           store16(C + (size_t)m * g.ldc, tile * (TC_BN / 2) + f0, n_out, v);
         } else {
           const int n = n0 + f0;
@@ -372,7 +377,7 @@ static GemmPlan plan_gemm(int M, int N, int K) {
   p.m_tiles = ceil_div(M, 128);
   p.bm = M >= 128 ? 128 : ((M + 15) / 16) * 16;
   const size_t stage = (size_t)p.bm * TC_BK * 2 + 2 * W_BLOCK_BYTES;
-  const size_t red = (size_t)TC_BN * p.bm * 4;
+  const size_t red = (size_t)(TC_BN + 4) * p.bm * 4;
   const int sms = sm_count();
   const int tiles = p.n_tiles * p.m_tiles;
   const int e_ctas = env_int("SLX_GEMM_CTAS", 0), e_s = env_int("SLX_GEMM_SPLITS", 0);

@@ -159,6 +159,8 @@ def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
     n_out = N // 2 if epilogue == EPI_SILU_MUL else N
     if out is None:
         out = torch.empty((M, n_out), dtype=out_dtype or torch.bfloat16, device=a.device)
+    if residual is not None and residual.dtype != out.dtype:
+        raise ValueError("gemm: residual must have the output dtype")
     check(_lib.load().slx_gemm_bf16(_ptr(a), _ld(a), _ptr(wt), _ptr(out), _ld(out), _dt(out),
                                     _ptr(residual), _ld(residual) if residual is not None else 0,
                                     M, N, K, epilogue, layout, _stream()), "slx_gemm_bf16")

@@ -52,9 +52,9 @@ def test_gemm_decode_tilings(M, ctas, splits, monkeypatch):
     out = ops.gemm(a, ops.pack_weight(w), out_dtype=torch.float32)
     torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
     # SiLU and residual epilogues through the same split-K reduction
-    r = bf(torch.randn(M, N, device=DEV))
+    r = torch.randn(M, N, device=DEV)   # residual has the output dtype
     o2 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_RESIDUAL, residual=r, out_dtype=torch.float32)
-    torch.testing.assert_close(o2, ref + r.float(), rtol=1e-4, atol=1e-2)
+    torch.testing.assert_close(o2, ref + r, rtol=1e-4, atol=1e-3)
     g_, u_ = ref.view(M, N // 256, 2, 128)[:, :, 0], ref.view(M, N // 256, 2, 128)[:, :, 1]
     o3 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_SILU_MUL, out_dtype=torch.float32)
     torch.testing.assert_close(o3, (g_ * torch.sigmoid(g_) * u_).reshape(M, N // 2), rtol=1e-3, atol=1e-3)
