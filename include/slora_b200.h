@@ -152,6 +152,13 @@ SLX_API int slx_attention(int dtype, void* out, int ldo, const void* qkv, int ld
                   int heads, int kv_heads, int head_dim, const int32_t* tok_pos,
                   const int32_t* tok_seq, const void* k_cache, const void* v_cache, int max_ctx,
                   void* stream);
+/* Decode step fusion of slx_rope_kv_write + slx_attention when every token is the NEXT
+ * position of its own sequence (tok_pos[t] = cached length): RoPE on q and the new key in
+ * registers, k/v appended to the pool, attention over cached positions [0, pos) + the new key. */
+SLX_API int slx_rope_attention_decode(int dtype, void* out, int ldo, const void* qkv, int ld_qkv,
+                  int n_tok, int heads, int kv_heads, int head_dim, const int32_t* tok_pos,
+                  const int32_t* tok_seq, const float* cos_tab, const float* sin_tab, int max_pos,
+                  void* k_cache, void* v_cache, int max_ctx, void* stream);
 /* gu [n_tok, 2*ffn] in the blocked layout of SLX_EPI_SILU_MUL -> out [n_tok, ffn]. */
 SLX_API int slx_silu_mul_blocked(int dtype, void* out, int ldo, const void* gu, int ld_gu, int n_tok,
                          int ffn, void* stream);

@@ -231,6 +231,155 @@ attention_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv, int ld
 template <typename T, int D>
 constexpr size_t att_smem() { return 0; }
 
+// ------------------------------------------------------------------ fused decode attention
+// Decode (one new token per sequence): CTA (token t, head h) applies RoPE to q and to the new
+// key in registers, appends k/v at tok_pos[t] to the KV pool (the group-leader head of a GQA
+// group writes), then attends over the cached positions [0, pos) — staged KB keys at a time
+// in shared memory with one burst of 16-byte cp.async per block — plus the new key/value.
+// Replaces rope_kv_write + attention for the decode step (one launch instead of two).
+template <typename T> struct DecCfg { static constexpr int KB = 128; };
+template <> struct DecCfg<float> { static constexpr int KB = 64; };
+
+template <typename T, int D>
+constexpr size_t dec_smem() {
+  return (size_t)2 * DecCfg<T>::KB * (D + 16 / sizeof(T)) * sizeof(T) +
+         (size_t)(3 * D + DecCfg<T>::KB + 2 * 128 + 8) * 4;
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(128)
+rope_attn_decode_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv, int ld, int H,
+                        int Hkv, const int32_t* __restrict__ tok_pos,
+                        const int32_t* __restrict__ tok_seq, const float* __restrict__ cos_tab,
+                        const float* __restrict__ sin_tab, T* __restrict__ kc, T* __restrict__ vc,
+                        int max_ctx, float scale_log2) {
+  pdl_trigger();
+  pdl_wait();
+  constexpr int KB = DecCfg<T>::KB;
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int DP = D + VEC;          // padded smem row
+  constexpr int CH = D / VEC;          // 16-byte chunks per row
+  constexpr int NT = 128;
+  constexpr int KP = NT / D;           // key partitions in P.V (1 for D=128, 2 for D=64)
+  extern __shared__ __align__(16) uint8_t dsm[];
+  T* Ks = reinterpret_cast<T*>(dsm);                   // [KB][DP]
+  T* Vs = Ks + KB * DP;                                 // [KB][DP]
+  float* qs = reinterpret_cast<float*>(Vs + KB * DP);   // [D] rotated, scaled q
+  float* kn = qs + D;                                    // [D] new key (rounded to T)
+  float* vn = kn + D;                                    // [D] new value
+  float* ps = vn + D;                                    // [KB]
+  float* red = ps + KB;                                  // [2*128] partials / reductions
+  float* misc = red + 2 * 128;                           // [8]
+
+  const int tid = threadIdx.x;
+  const int t = blockIdx.x / H, h = blockIdx.x % H;
+  const int group = H / Hkv, hk = h / group;
+  const int pos = tok_pos[t], seq = tok_seq[t];
+  const int half = D / 2;
+  const T* row = qkv + (size_t)t * ld;
+  const float* cr = cos_tab + (size_t)pos * half;
+  const float* sr = sin_tab + (size_t)pos * half;
+  T* kdst = kc + (((size_t)seq * Hkv + hk) * max_ctx + pos) * D;
+  T* vdst = vc + (((size_t)seq * Hkv + hk) * max_ctx + pos) * D;
+  for (int i = tid; i < half; i += NT) {
+    const float c = cr[i], sn = sr[i];
+    const float q1 = to_f32(row[h * D + i]), q2 = to_f32(row[h * D + i + half]);
+    // q is rounded to T exactly as the unfused path stores it before attention reads it back
+    qs[i] = to_f32(from_f32<T>(q1 * c - q2 * sn)) * scale_log2;
+    qs[i + half] = to_f32(from_f32<T>(q2 * c + q1 * sn)) * scale_log2;
+    const float k1 = to_f32(row[(H + hk) * D + i]), k2 = to_f32(row[(H + hk) * D + i + half]);
+    const T r1 = from_f32<T>(k1 * c - k2 * sn), r2 = from_f32<T>(k2 * c + k1 * sn);
+    kn[i] = to_f32(r1);
+    kn[i + half] = to_f32(r2);
+    if (h % group == 0) {
+      kdst[i] = r1;
+      kdst[i + half] = r2;
+    }
+  }
+  for (int i = tid; i < D; i += NT) {
+    const T v = row[(H + Hkv + hk) * D + i];
+    vn[i] = to_f32(v);
+    if (h % group == 0) vdst[i] = v;
+  }
+  __syncthreads();
+
+  const T* kbase = kc + ((size_t)seq * Hkv + hk) * max_ctx * D;
+  const T* vbase = vc + ((size_t)seq * Hkv + hk) * max_ctx * D;
+  // the new key first: its score seeds the running max
+  float s_new = 0.f;
+  {
+    float part = 0.f;
+    for (int i = tid; i < D; i += NT) part += qs[i] * kn[i];
+    part = warp_sum(part);
+    if ((tid & 31) == 0) red[tid >> 5] = part;
+    __syncthreads();
+    s_new = red[0] + red[1] + red[2] + red[3];
+    __syncthreads();
+  }
+  float m = s_new, l = 1.f;
+  const int dd = tid % D, kp = tid / D;   // P.V: dim dd over key partition kp
+  float acc = kp == 0 ? vn[dd] : 0.f;     // p_new = exp2(s_new - m) = 1
+  const int n_cached = pos;
+  for (int k0 = 0; k0 < n_cached; k0 += KB) {
+    const int nk = min(KB, n_cached - k0);
+    for (int e = tid; e < nk * CH; e += NT) {
+      const int r = e / CH, c = e % CH;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(Ks + r * DP + c * VEC))),
+                   "l"(kbase + (size_t)(k0 + r) * D + c * VEC) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(Vs + r * DP + c * VEC))),
+                   "l"(vbase + (size_t)(k0 + r) * D + c * VEC) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    // scores: thread = key (KB <= 128 threads)
+    float sc = -INFINITY;
+    if (tid < nk) {
+      const T* kr = Ks + tid * DP;
+      float dot = 0.f;
+#pragma unroll
+      for (int i = 0; i < D; i += 8) {
+        float f[8];
+        Vec8<T>::load(kr + i, f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dot = fmaf(qs[i + e], f[e], dot);
+      }
+      sc = dot;
+    }
+    float bm = warp_max(sc);
+    if ((tid & 31) == 0) red[tid >> 5] = bm;
+    __syncthreads();
+    bm = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+    const float m_new = fmaxf(m, bm);
+    const float corr = exp2f(m - m_new);
+    const float p = tid < nk ? exp2f(sc - m_new) : 0.f;
+    if (tid < KB) ps[tid] = p;
+    float bs = warp_sum(p);
+    __syncthreads();   // ps visible; red[0..3] consumed
+    if ((tid & 31) == 0) red[4 + (tid >> 5)] = bs;
+    // P.V over this block
+    float a = 0.f;
+    for (int j = kp; j < nk; j += KP) a = fmaf(ps[j], to_f32(Vs[j * DP + dd]), a);
+    __syncthreads();
+    l = l * corr + (red[4] + red[5] + red[6] + red[7]);
+    acc = acc * corr + a;
+    m = m_new;
+    __syncthreads();   // Ks/Vs/ps reused by the next block
+  }
+  if (KP > 1) {
+    red[tid] = acc;
+    __syncthreads();
+    if (tid < D) {
+      float o = 0.f;
+      for (int q = 0; q < KP; ++q) o += red[q * D + tid];
+      out[(size_t)t * ldo + h * D + tid] = from_f32<T>(o / l);
+    }
+  } else {
+    out[(size_t)t * ldo + h * D + tid] = from_f32<T>(acc / l);
+  }
+}
+
 // ------------------------------------------------------------------ SiLU * mul (blocked gate/up)
 template <typename T>
 __global__ void silu_mul_kernel(T* __restrict__ out, int ldo, const T* __restrict__ gu, int ld_gu,
@@ -464,4 +613,49 @@ extern "C" int slx_gemm_f32(const void* A, int lda, const void* W, void* C, int 
   return launch_ex(gemm_f32_kernel, grid, dim3(256), 0, (cudaStream_t)stream, 1u,
                    (const float*)A, lda, (const bf16*)W, (float*)C, ldc,
                    epilogue == SLX_EPI_RESIDUAL ? (const float*)R : nullptr, ldr, M, N, K);
+}
+
+template <typename T, int D>
+static int launch_rope_attn(void* out, int ldo, const void* qkv, int ld_qkv, int n_tok, int heads,
+                            int kv_heads, const int32_t* tok_pos, const int32_t* tok_seq,
+                            const float* cos_tab, const float* sin_tab, void* k_cache,
+                            void* v_cache, int max_ctx, float scale, cudaStream_t s) {
+  auto k = rope_attn_decode_kernel<T, D>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dec_smem<T, D>()) !=
+        cudaSuccess)
+      return SLX_ERR_CUDA;
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    configured = true;
+  }
+  return launch_ex(k, dim3((unsigned)n_tok * heads), dim3(128), dec_smem<T, D>(), s, 1u, (T*)out,
+                   ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab,
+                   (T*)k_cache, (T*)v_cache, max_ctx, scale);
+}
+
+extern "C" int slx_rope_attention_decode(int dtype, void* out, int ldo, const void* qkv,
+                                         int ld_qkv, int n_tok, int heads, int kv_heads,
+                                         int head_dim, const int32_t* tok_pos,
+                                         const int32_t* tok_seq, const float* cos_tab,
+                                         const float* sin_tab, int max_pos, void* k_cache,
+                                         void* v_cache, int max_ctx, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && heads > 0 && kv_heads > 0 && heads % kv_heads == 0 &&
+                ld_qkv >= (heads + 2 * kv_heads) * head_dim && ldo >= heads * head_dim && out &&
+                qkv && tok_pos && tok_seq && cos_tab && sin_tab && k_cache && v_cache &&
+                max_pos > 0 && max_ctx > 0);
+  SLX_CHECK_ARG(ldo % 8 == 0 && ld_qkv % 8 == 0);
+  SLX_CHECK_ALIGN(k_cache, 16);
+  SLX_CHECK_ALIGN(v_cache, 16);
+  if (head_dim != 64 && head_dim != 128) return SLX_ERR_UNSUPPORTED;
+  if (n_tok == 0) return SLX_OK;
+  const float scale = 1.4426950408889634f / sqrtf((float)head_dim);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == SLX_DT_BF16)
+    return head_dim == 64 ? launch_rope_attn<bf16, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, s)
+                          : launch_rope_attn<bf16, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, s);
+  if (dtype == SLX_DT_F32)
+    return head_dim == 64 ? launch_rope_attn<float, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, s)
+                          : launch_rope_attn<float, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, s);
+  return SLX_ERR_INVALID;
 }

@@ -51,7 +51,7 @@ class DecodeGraph:
         self.kernels_per_step = 0
 
     def _step(self):
-        self.logits = self.m.forward(self.tok, self.pos, self.seq, self.slot)
+        self.logits = self.m.forward(self.tok, self.pos, self.seq, self.slot, decode=True)
         ops.argmax(self.next_tok, self.logits)
 
     def capture(self, warmup: int = 2):

@@ -273,8 +273,10 @@ class MultiLoraModel:
         ops.lora_apply(y, x, d_in if d_in is not None else x.shape[1], self.pool.rank,
                        self.pool.scale, self.pool.max_rank, ops.make_targets(specs), self.lora_ws)
 
-    def forward(self, tokens, pos, seq, slot, logit_rows=None) -> torch.Tensor:
+    def forward(self, tokens, pos, seq, slot, logit_rows=None, decode: bool = False) -> torch.Tensor:
         """Token-major mixed batch.  tokens/pos/seq/slot: device int32 [T].
+        ``decode``: every token is the next position of its own sequence, so RoPE, the KV
+        append and attention run as one fused kernel per layer.
         Returns logits (fp32) for ``logit_rows`` (device int64) or for every token."""
         cfg, w, dt = self.cfg, self.w, self.dtype
         T = tokens.numel()
@@ -298,10 +300,14 @@ class MultiLoraModel:
             ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
             self._gemm(h, w[p + "w_qkv"], qkv)
             self._lora(qkv, h, l, ("q", "k", "v"), qkv_cols)
-            ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
-                              self.sin, self.k_cache[l], self.v_cache[l])
-            ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
-                          self.k_cache[l], self.v_cache[l])
+            if decode:
+                ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos,
+                                          seq, self.cos, self.sin, self.k_cache[l], self.v_cache[l])
+            else:
+                ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
+                                  self.sin, self.k_cache[l], self.v_cache[l])
+                ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
+                              self.k_cache[l], self.v_cache[l])
             self._gemm(attn, w[p + "wo"], x, residual=x)
             self._lora(x, attn, l, ("o",), {"o": (0, d, d)})
             ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
@@ -351,7 +357,8 @@ class MultiLoraModel:
             self.seq_len[s] += 1
         dev = self.device
         i32 = lambda v: torch.tensor(v, dtype=torch.int32, device=dev)  # noqa: E731
-        return self.forward(i32(list(tokens)), i32(pos), i32(list(seqs)), i32(list(adapter_slots)))
+        return self.forward(i32(list(tokens)), i32(pos), i32(list(seqs)), i32(list(adapter_slots)),
+                            decode=len(set(seqs)) == len(seqs))
 
     def argmax(self, logits: torch.Tensor) -> torch.Tensor:
         out = torch.empty(logits.shape[0], dtype=torch.int32, device=logits.device)

@@ -277,6 +277,18 @@ def attention(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, k_cache, v_
     return out
 
 
+@_op("attention", 1)
+def rope_attention_decode(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos, sin,
+                          k_cache, v_cache):
+    """Decode-step RoPE + KV append + attention in one kernel (each token = next position of
+    its own sequence)."""
+    check(_lib.load().slx_rope_attention_decode(
+        _dt(out), _ptr(out), _ld(out), _ptr(qkv), _ld(qkv), qkv.shape[0], heads, kv_heads, head_dim,
+        _ptr(tok_pos), _ptr(tok_seq), _ptr(cos), _ptr(sin), cos.shape[0], _ptr(k_cache),
+        _ptr(v_cache), k_cache.shape[2], _stream()), "slx_rope_attention_decode")
+    return out
+
+
 @_op("silu_mul", 1)
 def silu_mul_blocked(out, gu, ffn: int):
     check(_lib.load().slx_silu_mul_blocked(_dt(out), _ptr(out), _ld(out), _ptr(gu), _ld(gu),

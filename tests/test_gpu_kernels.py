@@ -250,3 +250,39 @@ def test_rope_kv_attention_match_oracle(dtype, H, Hkv, D):
     tol = 2e-5 if dtype == torch.float32 else 3e-2
     np.testing.assert_allclose(out.float().cpu().numpy(), ref.reshape(T, -1), rtol=tol, atol=tol)
     np.testing.assert_allclose(kc[1, :, :13].float().cpu().numpy().transpose(1, 0, 2), k[1:14], rtol=tol, atol=tol)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("H,Hkv,D", [(4, 4, 64), (32, 32, 128), (8, 2, 128)])
+@pytest.mark.parametrize("ctx", [0, 5, 128, 300])
+def test_rope_attention_decode_fused(dtype, H, Hkv, D, ctx):
+    """Fused decode kernel == rope_kv_write + attention (and the oracle), incl. the KV append."""
+    rng = np.random.default_rng(ctx + D)
+    B, max_ctx = 3, 320
+    cos, sin = orc.rope_table(max_ctx, D, 10000.0)
+    cos_d, sin_d = torch.from_numpy(cos).to(DEV), torch.from_numpy(sin).to(DEV)
+    kc = torch.from_numpy(rng.standard_normal((B, Hkv, max_ctx, D)).astype(np.float32)).to(DEV, dtype)
+    vc = torch.from_numpy(rng.standard_normal((B, Hkv, max_ctx, D)).astype(np.float32)).to(DEV, dtype)
+    qkv = torch.from_numpy(rng.standard_normal((B, (H + 2 * Hkv) * D)).astype(np.float32)).to(DEV, dtype)
+    pos = torch.full((B,), ctx, dtype=torch.int32, device=DEV)
+    seq = torch.arange(B, dtype=torch.int32, device=DEV)
+    kc2, vc2, qkv2 = kc.clone(), vc.clone(), qkv.clone()
+    out_f = torch.empty(B, H * D, dtype=dtype, device=DEV)
+    ops.rope_attention_decode(out_f, qkv, H, Hkv, D, pos, seq, cos_d, sin_d, kc, vc)
+    out_u = torch.empty(B, H * D, dtype=dtype, device=DEV)
+    ops.rope_kv_write(qkv2, H, Hkv, D, pos, seq, cos_d, sin_d, kc2, vc2)
+    ops.attention(out_u, qkv2, H, Hkv, D, pos, seq, kc2, vc2)
+    tol = 2e-5 if dtype == torch.float32 else 2e-2
+    torch.testing.assert_close(out_f.float(), out_u.float(), rtol=tol, atol=tol)
+    assert torch.equal(kc[:, :, :ctx + 1], kc2[:, :, :ctx + 1])   # identical KV append
+    assert torch.equal(vc[:, :, :ctx + 1], vc2[:, :, :ctx + 1])
+    # oracle: rotate q/k in fp32 from the (dtype-rounded) inputs
+    q_in = qkv.float().cpu().numpy() if dtype == torch.float32 else qkv2.float().cpu().numpy()
+    kk = kc2[:, :, :ctx + 1].float().cpu().numpy()
+    vv = vc2[:, :, :ctx + 1].float().cpu().numpy()
+    for b in range(B):
+        q = q_in[b, :H * D].reshape(1, H, D)
+        if dtype == torch.float32:
+            q = orc.apply_rope(q, np.array([ctx]), cos, sin)
+        ref = orc.attention(q, kk[b].transpose(1, 0, 2), vv[b].transpose(1, 0, 2), np.array([ctx]))
+        np.testing.assert_allclose(out_f[b].float().cpu().numpy(), ref.reshape(-1), rtol=tol * 5, atol=tol * 5)
