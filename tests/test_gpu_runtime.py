@@ -1,0 +1,96 @@
+"""GPU: the serving runtime (batcher -> merged prefill -> merged decode), the artifact
+pre-loader and the calibration bridge, end to end on the tiny config."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2505_14468_b200.batching import max_batch_size, predict_ttft
+from paper_2505_14468_b200.calibrate import profile_function_spec
+from paper_2505_14468_b200.config import TINY, TINY_LORA, init_adapter, init_backbone
+from paper_2505_14468_b200.model import MultiLoraModel
+from paper_2505_14468_b200.preload import HostArtifactStore, NcclComm, Preloader
+from paper_2505_14468_b200.runtime import ServingRuntime
+from paper_2505_14468_b200.spec import ArtifactKind, ArtifactSpec, FunctionSpec
+
+pytestmark = pytest.mark.gpu
+
+
+def _model(golden, dtype=torch.float32, max_seqs=16):
+    seed = int(golden["seed"])
+    w = init_backbone(TINY, seed)
+    ads = [init_adapter(TINY, TINY_LORA, seed, a) for a in range(4)]
+    m = MultiLoraModel(TINY, dtype=dtype, max_seqs=max_seqs, max_ctx=128, n_slots=8, max_rank=16,
+                       max_tokens=2048)
+    m.load_backbone(w)
+    return m, w, ads
+
+
+def _prompts(golden):
+    ip = golden["prompt_indptr"]
+    return [list(map(int, golden["prompt_flat"][ip[i]:ip[i + 1]])) for i in range(len(ip) - 1)]
+
+
+def _spec(fid, t0=5.0, alpha=1.0):
+    arts = (ArtifactSpec(ArtifactKind.ADAPTER_MODEL, 10, 1.0, 1.0),)
+    return FunctionSpec(fid, arts, 5 * t0, t0, alpha, 1.0, 0, 0.0, backbone_id="tiny")
+
+
+def test_preloader_h2d_then_runtime_serves_golden_tokens(golden):
+    """Adapters enter HBM through the pinned-host pre-loader; four LoRA functions are served
+    through batcher rounds as merged mixed-adapter prefill/decode; fp32 greedy tokens are
+    bit-exact with the transformers golden."""
+    m, w, ads = _model(golden)
+    store = HostArtifactStore(64 << 20)
+    pre = Preloader(store, m.device, chunk_bytes=1 << 20)
+    for a, ad in enumerate(ads):
+        store.put(f"adapter{a}", m.pool.pack(ad, TINY_LORA.rank))
+    for a in range(4):
+        dev, ev = pre.load(f"adapter{a}")
+        ev.synchronize()
+        m.pool.install(a, dev.view(torch.bfloat16), TINY_LORA)
+    assert pre.timed_load_ms("adapter0") > 0
+    funcs = {f"fn{a}": (_spec(f"fn{a}"), a) for a in range(4)}
+    rt = ServingRuntime(m, funcs)
+    prompts = _prompts(golden)
+    ids = list(map(int, golden["adapter_ids"]))
+    n_new = int(golden["n_new"])
+    for i, (p, a) in enumerate(zip(prompts, ids)):
+        rt.submit(i, f"fn{a}", p, n_new)
+    done = rt.run_until_idle()
+    assert len(done) == len(prompts)
+    toks = np.stack([np.asarray(sorted(done, key=lambda r: r.request_id)[i].generated[:n_new])
+                     for i in range(len(prompts))])
+    assert np.array_equal(toks, golden["tokens"])
+    assert all(r.first_token_ms is not None and r.done_ms >= r.first_token_ms for r in done)
+    store.close()
+
+
+def test_nccl_broadcast_world1_roundtrip():
+    """The pre-loader's own NCCL communicator (world 1 on the single-GPU box): one host read,
+    pipelined H2D + broadcast, bytes land intact."""
+    store = HostArtifactStore(8 << 20)
+    data = np.random.default_rng(0).integers(0, 255, size=5_000_000, dtype=np.uint8)
+    store.put("blob", data)
+    pre = Preloader(store, torch.device("cuda", 0), chunk_bytes=1 << 20)
+    comm = NcclComm(0, 1)
+    out = pre.load_broadcast("blob", 0, comm)
+    pre.wait()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), data)
+    comm.close()
+    store.close()
+
+
+def test_calibration_feeds_the_batcher(golden):
+    m, w, ads = _model(golden, dtype=torch.bfloat16)
+    m.pool.load(0, ads[0], TINY_LORA)
+    spec, raw = profile_function_spec(m, "tiny-chat", 0, backbone_id="tiny", prompt_len=24,
+                                      max_new_tokens=8, batch_sizes=(1, 2, 4, 8))
+    assert spec.prefill_base_ms > 0 and spec.prefill_marginal_ms >= 0
+    assert spec.decode_ms_per_token > 0
+    assert spec.kv_cache_bytes_per_request == TINY.kv_bytes_per_token() * 32
+    assert spec.slo_ttft_ms == pytest.approx(5 * spec.prefill_base_ms)
+    assert predict_ttft(spec, 1) == spec.prefill_base_ms
+    assert max_batch_size(spec) >= 1
+    assert len(raw["prefill_ms"]) == 4

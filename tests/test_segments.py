@@ -1,0 +1,48 @@
+"""CPU: FlushDecisions -> adapter-segmented mixed batches."""
+
+import numpy as np
+
+from paper_2505_14468_b200.batching import FlushDecision
+from paper_2505_14468_b200.segments import Request, build_decode, build_prefill, group_by_gpu
+
+
+def _reqs():
+    rs = [Request(i, f"f{i % 3}", list(range(10 * i + 1, 10 * i + 1 + (i % 4) + 1)), 4) for i in range(7)]
+    for i, r in enumerate(rs):
+        r.seq = i
+        r.adapter_slot = [2, -1, 0][i % 3]
+    return rs
+
+
+def test_prefill_segments_grouped_by_adapter():
+    rs = _reqs()
+    seq_len = [0] * 8
+    seq_len[3] = 5          # a continuing sequence starts at its cached length
+    b = build_prefill(rs, seq_len)
+    assert b.n_tokens == sum(len(r.prompt) for r in rs)
+    assert list(b.seg_slot) == sorted(b.seg_slot.tolist())     # grouped by adapter slot
+    for s, r in enumerate(b.requests):
+        lo, hi = b.seg_indptr[s], b.seg_indptr[s + 1]
+        assert b.tokens[lo:hi].tolist() == r.prompt
+        assert (b.seq[lo:hi] == r.seq).all() and (b.slot[lo:hi] == r.adapter_slot).all()
+        assert b.pos[lo:hi].tolist() == list(range(seq_len[r.seq], seq_len[r.seq] + hi - lo))
+        assert b.logit_rows[s] == hi - 1
+
+
+def test_decode_one_token_per_sequence():
+    rs = _reqs()
+    for r in rs:
+        r.generated = [r.request_id + 100]
+    seq_len = list(range(8))
+    b = build_decode(rs, seq_len)
+    assert b.tokens.tolist() == [r.request_id + 100 for r in rs]
+    assert b.pos.tolist() == [seq_len[r.seq] for r in rs]
+    assert b.slot.tolist() == [r.adapter_slot for r in rs]
+    assert b.seg_indptr.tolist() == list(range(len(rs) + 1))
+
+
+def test_group_by_gpu():
+    ds = [FlushDecision("a", "g0", (1,), "fill"), FlushDecision("b", "g1", (2,), "expire"),
+          FlushDecision("c", "g0", (3, 4), "margin", 1.0)]
+    g = group_by_gpu(ds)
+    assert [d.function_id for d in g["g0"]] == ["a", "c"] and len(g["g1"]) == 1
