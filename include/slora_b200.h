@@ -79,13 +79,20 @@ enum {
                          TMA box of the GEMM is one contiguous 16 KB burst (slx_pack_weight) */
 };
 SLX_API size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue);
+/* Side output: with C2 != NULL, columns [n_main, N) (e.g. the stacked LoRA A rows appended
+ * to a projection's W: the decode shrink) are written in fp32 to C2 [M, ldc2] and get no
+ * residual; columns [0, n_main) go to C/R as usual (n_main % 16 == 0; not with SiLU). */
 SLX_API int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
-                  void* stream);
+                  int n_main, void* C2, int ldc2, void* stream);
 /* Pack a row-major bf16 W[N, K] (row stride ld) into the SLX_W_TILED layout (device kernel).
  * dst must hold slx_packed_weight_elems(N, K) elements. */
 SLX_API size_t slx_packed_weight_elems(int N, int K);
 SLX_API int slx_pack_weight(void* dst, const void* src, int N, int K, int ld, void* stream);
+/* (Re)write rows [row0, row0 + n_rows) of a packed SLX_W_TILED matrix with K columns from a
+ * row-major src [n_rows, K] (row stride ld); src == NULL writes zeros (slot eviction). */
+SLX_API int slx_pack_weight_rows(void* dst, const void* src, int n_rows, int K, int ld, int row0,
+                  void* stream);
 /* fp32-parity GEMM (CUDA cores): A fp32 [M,K], W bf16 [N,K], C/R fp32.  Epilogue NONE or
  * RESIDUAL.  K % 8 == 0. */
 SLX_API int slx_gemm_f32(const void* A, int lda, const void* W, void* C, int ldc,
@@ -121,6 +128,13 @@ SLX_API int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ldx, 
                    const int32_t* slot_rank, const float* slot_scale, int n_slots, int max_rank,
                    int n_targets, const slx_lora_target* targets,
                    void* ws, size_t ws_bytes, void* stream);
+/* Decode expand when the shrink ran inside the projection GEMM (slx_gemm_bf16 side output):
+ * v_all [n_tok, ldv] fp32 holds, for target i, column v_col_off[i] + slot*max_rank + j =
+ * x_t . A_slot[j]; adds scale * v . B_slot^T into y over the plan in ws (a_ptrs unused). */
+SLX_API int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, int ldv, int n_tok,
+                  const int32_t* slot_rank, const float* slot_scale, int n_slots, int max_rank,
+                  int n_targets, const slx_lora_target* targets, const int* v_col_off,
+                  void* ws, size_t ws_bytes, void* stream);
 /* Convenience: plan_tokens + apply (BGMV) and plan_segments + apply (SGMV). */
 SLX_API int slx_lora_bgmv(int dtype, void* y, int ldy, const void* x, int ldx, const int32_t* tok_slot,
                   int n_tok, int d_in, const int32_t* slot_rank, const float* slot_scale,

@@ -46,7 +46,10 @@ SIGNATURES = {
     "slx_abi_version": (_i, []),
     "slx_device_sm_count": (_i, [ctypes.POINTER(_i)]),
     "slx_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
-    "slx_gemm_bf16": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _p]),
+    "slx_gemm_bf16": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p]),
+    "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),
+    "slx_lora_expand": (_i, [_i, _p, _i, _p, _i, _i, _p, _p, _i, _i, _i,
+                             ctypes.POINTER(LoraTarget), ctypes.POINTER(_i), _p, _sz, _p]),
     "slx_packed_weight_elems": (_sz, [_i, _i]),
     "slx_pack_weight": (_i, [_p, _p, _i, _i, _i, _p]),
     "slx_gemm_f32": (_i, [_p, _i, _p, _p, _i, _p, _i, _i, _i, _i, _i, _p]),

@@ -50,6 +50,9 @@ struct GemmArgs {
   const void* R;
   int ldr;
   int w_tiled;   // W packed as [N/128][kblocks][128][64] (SLX_W_TILED)
+  int n_main;    // columns >= n_main go to the fp32 side output C2 (LoRA shrink rows)
+  float* C2;
+  int ldc2;
 };
 
 template <typename OutT>
@@ -69,6 +72,33 @@ __device__ __forceinline__ void store16(OutT* row, int n0, int n_lim, const floa
     for (int j = 0; j < 16; ++j)
       if (n0 + j < n_lim) store_out(row + n0 + j, v[j]);
   }
+}
+
+// 16 output columns [n, n+16) of row m: main columns get the residual and go to C, side
+// columns (n >= n_main, LoRA shrink rows appended to W) go to the fp32 side output C2.
+template <int EPI, typename OutT>
+__device__ __forceinline__ void store_cols(const GemmArgs& g, OutT* C, const OutT* R, int m, int n,
+                                           int n_out, float* v) {
+  if (g.C2 != nullptr && n >= g.n_main) {
+    float* row = g.C2 + (size_t)m * g.ldc2 + (n - g.n_main);
+    if (n + 16 <= g.N) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        reinterpret_cast<float4*>(row)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (n + j < g.N) row[j] = v[j];
+    }
+    return;
+  }
+  const int lim = g.C2 != nullptr ? g.n_main : n_out;
+  if (EPI == SLX_EPI_RESIDUAL) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (n + j < lim) v[j] += to_f32(R[(size_t)m * g.ldr + n + j]);
+  }
+  store16(C + (size_t)m * g.ldc, n, lim, v);
 }
 
 // TMA coordinates of the 128-row weight block starting at row0 (multiple of 128), k-block kb.
@@ -202,14 +232,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
           float v[16];
           tc::tmem_ld16(t_row + c0, v);
           const int n = n0 + c0;
-          if (m < g.M) {
-            if (EPI == SLX_EPI_RESIDUAL) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (n + j < g.N) v[j] += to_f32(R[(size_t)m * g.ldr + n + j]);
-            }
-            store16(C + (size_t)m * g.ldc, n, n_out, v);
-          }
+          if (m < g.M) store_cols<EPI>(g, C, R, m, n, n_out, v);
         }
       }
     }
@@ -266,13 +289,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
           for (int j = 0; j < 16; ++j) v[j] = silu_f(v[j]) * u[j];
           store16(C + (size_t)m * g.ldc, tile * (TC_BN / 2) + f0, n_out, v);
         } else {
-          const int n = n0 + f0;
-          if (EPI == SLX_EPI_RESIDUAL) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (n + j < g.N) v[j] += to_f32(R[(size_t)m * g.ldr + n + j]);
-          }
-          store16(C + (size_t)m * g.ldc, n, n_out, v);
+          store_cols<EPI>(g, C, R, m, n0 + f0, n_out, v);
         }
       }
     }
@@ -452,7 +469,7 @@ extern "C" size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
 
 extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                              const void* R, int ldr, int M, int N, int K, int epilogue,
-                             int w_layout, void* stream) {
+                             int w_layout, int n_main, void* C2, int ldc2, void* stream) {
   SLX_CHECK_ARG(w_layout == SLX_W_ROWMAJOR || w_layout == SLX_W_TILED);
   SLX_CHECK_ARG(A && W && C && M >= 0 && N > 0 && K > 0 && lda >= K && K % 8 == 0 &&
                 lda % 8 == 0 && ldc % 8 == 0);
@@ -465,9 +482,16 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   if (epilogue == SLX_EPI_SILU_MUL) {
     SLX_CHECK_ARG(N % 256 == 0 && ldc >= N / 2);
   } else {
-    SLX_CHECK_ARG(N % 16 == 0 && ldc >= N);
+    SLX_CHECK_ARG(N % 16 == 0 && (C2 != nullptr || ldc >= N));
   }
-  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= N && ldr % 8 == 0);
+  if (C2 != nullptr) {
+    SLX_CHECK_ARG(epilogue != SLX_EPI_SILU_MUL && n_main > 0 && n_main < N && n_main % 16 == 0 &&
+                  ldc2 >= N - n_main && ldc2 % 4 == 0 && ldc >= n_main);
+    SLX_CHECK_ALIGN(C2, 16);
+  } else {
+    n_main = N;
+  }
+  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= n_main && ldr % 8 == 0);
   if (M == 0) return SLX_OK;
   GemmPlan p = plan_gemm(M, N, K);
   if (env_int("SLX_GEMM_DEBUG", 0))
@@ -479,6 +503,9 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   a.n_tiles = p.n_tiles;
   a.C = C; a.ldc = ldc; a.R = R; a.ldr = ldr;
   a.w_tiled = w_layout == SLX_W_TILED;
+  a.n_main = n_main;
+  a.C2 = (float*)C2;
+  a.ldc2 = ldc2;
   // tiled W: a [n_blocks * kblocks * 128, 64] matrix of contiguous 16 KB boxes
   const int w_rows = a.w_tiled ? ceil_div(N, 128) * p.kblocks * 128 : N;
   const int w_cols = a.w_tiled ? TC_BK : K;
@@ -511,6 +538,24 @@ __global__ void pack_weight_kernel(bf16* __restrict__ dst, const bf16* __restric
   if (n < N && k < K) v = *reinterpret_cast<const uint4*>(src + (size_t)n * ld + k);  // K % 8 == 0
   *reinterpret_cast<uint4*>(dst + row * TC_BK + c8 * 8) = v;
 }
+
+// Write rows [row0, row0 + n) of an already packed (SLX_W_TILED) matrix from row-major src.
+__global__ void pack_rows_kernel(bf16* __restrict__ dst, const bf16* __restrict__ src, int n,
+                                 int K, int ld, int row0, int kblocks) {
+  pdl_trigger();
+  pdl_wait();
+  const size_t chunk = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t total = (size_t)n * kblocks * 8;
+  if (chunk >= total) return;
+  const int c8 = (int)(chunk % 8);
+  const int kb = (int)((chunk / 8) % kblocks);
+  const int i = (int)(chunk / 8 / kblocks);
+  const int row = row0 + i, k = kb * TC_BK + c8 * 8;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (src != nullptr && k < K) v = *reinterpret_cast<const uint4*>(src + (size_t)i * ld + k);
+  const size_t prow = ((size_t)(row >> 7) * kblocks + kb) * 128 + (row & 127);
+  *reinterpret_cast<uint4*>(dst + prow * TC_BK + c8 * 8) = v;
+}
 }  // namespace slx
 
 extern "C" size_t slx_packed_weight_elems(int N, int K) {
@@ -526,4 +571,16 @@ extern "C" int slx_pack_weight(void* dst, const void* src, int N, int K, int ld,
   const size_t total = (size_t)ceil_div(N, 128) * kb * 128 * 8;
   return launch_ex(pack_weight_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0,
                    (cudaStream_t)stream, 1u, (bf16*)dst, (const bf16*)src, N, K, ld, kb);
+}
+
+extern "C" int slx_pack_weight_rows(void* dst, const void* src, int n_rows, int K, int ld,
+                                    int row0, void* stream) {
+  SLX_CHECK_ARG(dst && n_rows > 0 && K > 0 && K % 8 == 0 && row0 >= 0 && (!src || ld >= K) &&
+                ld % 8 == 0);
+  SLX_CHECK_ALIGN(dst, 16);
+  if (src) SLX_CHECK_ALIGN(src, 16);
+  const int kb = ceil_div(K, TC_BK);
+  const size_t total = (size_t)n_rows * kb * 8;
+  return launch_ex(pack_rows_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0,
+                   (cudaStream_t)stream, 1u, (bf16*)dst, (const bf16*)src, n_rows, K, ld, row0, kb);
 }

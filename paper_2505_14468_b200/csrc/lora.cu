@@ -458,6 +458,106 @@ lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, 
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+
+// ---------------------------------------------------------------- decode expand (shrink in GEMM)
+// The decode shrink runs inside the projection GEMM (stacked A rows of every slot appended to
+// W, fp32 side output v_all); this kernel is the expand: CTA (tile, target, n-chunk) stages
+// the tile adapter's B rows of its n-chunk and the tokens' y slices with one burst of
+// cp.async, then y[t, col(n)] += scale * sum_j v_all[t, off + slot*max_rank + j] * B[n, j].
+constexpr int EX_THREADS = 256;
+constexpr int EX_CHUNK = 512;   // output features per CTA
+
+struct ExpandArgs {
+  int v_off[SLX_LORA_MAX_TARGETS];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(EX_THREADS)
+lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, int ldv,
+                     const int32_t* __restrict__ slot_rank, const float* __restrict__ slot_scale,
+                     int max_rank, TargetArgs ta, ExpandArgs ea, LoraWs ws) {
+  extern __shared__ __align__(16) uint8_t esm[];
+  pdl_trigger();
+  pdl_wait();
+  const int tile_id = blockIdx.x;
+  if (tile_id >= *ws.n_tiles) return;
+  const LoraTile tile = ws.tiles[tile_id];
+  const int tgt = blockIdx.y;
+  const int d_out = ta.d_out[tgt];
+  const int n_lo = blockIdx.z * EX_CHUNK;
+  if (n_lo >= d_out) return;
+  const int nn = min(EX_CHUNK, d_out - n_lo);
+  const int cnt = tile.count;
+  const int rank = min(slot_rank[tile.slot], max_rank);
+  const float scale = slot_scale[tile.slot];
+  const bf16* B = reinterpret_cast<const bf16*>(ta.b_ptrs[tgt][tile.slot]);
+  const int cb = ta.col_blk[tgt], cstr = ta.col_stride[tgt], co = ta.col_off[tgt];
+  const int col_lo = co + (n_lo / cb) * cstr + (n_lo % cb);
+  const bool y_contig = (n_lo / cb) == ((n_lo + nn - 1) / cb) && (col_lo % 8) == 0 &&
+                        (ldy % 8) == 0 && (nn % 8) == 0;
+  // smem: bs [EX_CHUNK][max_rank] bf16 | ys [TT][EX_CHUNK] T | vs [TT][max_rank] f32 | toks
+  bf16* bs = reinterpret_cast<bf16*>(esm);
+  T* ys = reinterpret_cast<T*>(bs + (size_t)EX_CHUNK * max_rank);
+  float* vs = reinterpret_cast<float*>(ys + (size_t)LORA_TT * EX_CHUNK);
+  int* toks = reinterpret_cast<int*>(vs + LORA_TT * max_rank);
+  if (threadIdx.x < LORA_TT) toks[threadIdx.x] = threadIdx.x < cnt ? ws.perm[tile.start + threadIdx.x] : 0;
+  __syncthreads();
+  const int bchunks = nn * rank / 8;   // rows n_lo..n_lo+nn of B are contiguous
+  for (int e = threadIdx.x; e < bchunks; e += EX_THREADS) {
+    const int flat = e * 8;
+    cp_async16(bs + (size_t)(flat / rank) * max_rank + flat % rank, B + (size_t)n_lo * rank + flat);
+  }
+  constexpr int XV = 16 / sizeof(T);
+  if (y_contig) {
+    const int ych = nn / XV;
+    for (int e = threadIdx.x; e < cnt * ych; e += EX_THREADS) {
+      const int i = e / ych, c = e % ych;
+      cp_async16(ys + (size_t)i * EX_CHUNK + c * XV, y + (size_t)toks[i] * ldy + col_lo + c * XV);
+    }
+  }
+  const int voff = ea.v_off[tgt] + tile.slot * max_rank;
+  for (int e = threadIdx.x; e < cnt * max_rank; e += EX_THREADS) {
+    const int i = e / max_rank, j = e % max_rank;
+    vs[e] = j < rank ? v[(size_t)toks[i] * ldv + voff + j] * scale : 0.f;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int R8 = (rank + 7) & ~7;
+  const int ngrp = (nn + 7) / 8;
+  for (int e = threadIdx.x; e < cnt * ngrp; e += EX_THREADS) {
+    const int i = e / ngrp, n0 = (e % ngrp) * 8;
+    const float* vr = vs + i * max_rank;
+    float d[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int j = 0; j < R8; j += 8) {
+      float vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) vv[u] = vr[j + u];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        if (n0 + r >= nn) break;
+        float b[8];
+        Vec8<bf16>::load(bs + (size_t)(n0 + r) * max_rank + j, b);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d[r] = fmaf(vv[u], b[u], d[r]);
+      }
+    }
+    T* yr = y + (size_t)toks[i] * ldy;
+    if (y_contig) {
+      float yv[8];
+      Vec8<T>::load(ys + (size_t)i * EX_CHUNK + n0, yv);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) yv[r] += d[r];
+      Vec8<T>::store(yr + col_lo + n0, yv);
+    } else {
+      for (int r = 0; r < 8 && n0 + r < nn; ++r) {
+        const int n = n_lo + n0 + r;
+        const int col = co + (n / cb) * cstr + (n % cb);
+        yr[col] = from_f32<T>(to_f32(yr[col]) + d[r]);
+      }
+    }
+  }
+}
+
 }  // namespace slx
 
 using namespace slx;
@@ -606,4 +706,52 @@ extern "C" int slx_lora_sgmv(int dtype, void* y, int ldy, const void* x, int ldx
   if (st) return st;
   return slx_lora_apply(dtype, y, ldy, x, ldx, n_tok, d_in, slot_rank, slot_scale, n_slots,
                         max_rank, n_targets, targets, ws, ws_bytes, stream);
+}
+
+extern "C" int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, int ldv, int n_tok,
+                               const int32_t* slot_rank, const float* slot_scale, int n_slots,
+                               int max_rank, int n_targets, const slx_lora_target* targets,
+                               const int* v_col_off, void* ws, size_t ws_bytes, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && n_slots > 0 && max_rank > 0 && max_rank <= LORA_MAX_RANK &&
+                max_rank % 8 == 0 && n_targets >= 1 && n_targets <= SLX_LORA_MAX_TARGETS &&
+                targets && v_col_off && slot_rank && slot_scale && y && v_all && ldv > 0);
+  TargetArgs ta;
+  ExpandArgs ea;
+  int max_dout = 0;
+  for (int i = 0; i < n_targets; ++i) {
+    const slx_lora_target& t = targets[i];
+    SLX_CHECK_ARG(t.b_ptrs && t.d_out > 0 && t.d_out % 8 == 0 && t.y_col_block > 0 &&
+                  t.y_col_stride >= t.y_col_block && v_col_off[i] >= 0 &&
+                  v_col_off[i] + n_slots * max_rank <= ldv);
+    ta.a_ptrs[i] = t.a_ptrs;
+    ta.b_ptrs[i] = t.b_ptrs;
+    ta.d_out[i] = t.d_out;
+    ta.col_off[i] = t.y_col_offset;
+    ta.col_blk[i] = t.y_col_block;
+    ta.col_stride[i] = t.y_col_stride;
+    ea.v_off[i] = v_col_off[i];
+    max_dout = t.d_out > max_dout ? t.d_out : max_dout;
+  }
+  LoraWs w;
+  int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
+  if (st) return st;
+  if (n_tok == 0) return SLX_OK;
+  const size_t tsz = dtype == SLX_DT_BF16 ? 2 : 4;
+  const size_t smem = (size_t)EX_CHUNK * max_rank * 2 + (size_t)LORA_TT * EX_CHUNK * tsz +
+                      (size_t)LORA_TT * max_rank * 4 + LORA_TT * 4;
+  dim3 grid((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)ceil_div(max_dout, EX_CHUNK));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == SLX_DT_BF16) {
+    auto k = lora_expand_v_kernel<bf16>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return launch_ex(k, grid, dim3(EX_THREADS), smem, s, 1u, (bf16*)y, ldy, (const float*)v_all, ldv,
+                     slot_rank, slot_scale, max_rank, ta, ea, w);
+  }
+  if (dtype == SLX_DT_F32) {
+    auto k = lora_expand_v_kernel<float>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return launch_ex(k, grid, dim3(EX_THREADS), smem, s, 1u, (float*)y, ldy, (const float*)v_all, ldv,
+                     slot_rank, slot_scale, max_rank, ta, ea, w);
+  }
+  return SLX_ERR_INVALID;
 }

@@ -64,6 +64,8 @@ class AdapterPool:
         self.scale = torch.zeros(n_slots, dtype=torch.float32, device=self.device)
         self.blobs: list[torch.Tensor | None] = [None] * n_slots
         self.configs: list[LoraConfig | None] = [None] * n_slots
+        self.on_install = None   # model hooks (stacked-A rows of the projection GEMMs)
+        self.on_evict = None
 
     def blob_layout(self, rank: int):
         """[(layer, target, a_off, b_off, d_in, d_out)] in elements, and total elements."""
@@ -107,6 +109,8 @@ class AdapterPool:
         self.scale[slot] = lora.scale
         self.blobs[slot] = blob
         self.configs[slot] = lora
+        if self.on_install is not None:
+            self.on_install(slot, blob, lora)
 
     def load(self, slot: int, weights: dict, lora: LoraConfig) -> None:
         blob = self.pack(weights, lora.rank)
@@ -127,6 +131,8 @@ class AdapterPool:
         self.install(slot, blob, lora)
 
     def evict(self, slot: int) -> None:
+        if self.on_evict is not None:
+            self.on_evict(slot)
         self.a_ptr[:, :, slot] = 0
         self.b_ptr[:, :, slot] = 0
         self.rank[slot] = 0
@@ -165,6 +171,19 @@ class MultiLoraModel:
         self.seq_len = [0] * max_seqs
         self.free_seqs = list(range(max_seqs))[::-1]
         self.w: dict[str, torch.Tensor] = {}
+        # decode shrink inside the projection GEMMs (bf16): stacked A rows of every slot are
+        # appended to the packed q/k/v and o weights; the GEMM writes v_all in fp32 as a side
+        # output and slx_lora_expand finishes the LoRA term.  Per group: targets, row layout.
+        self.stack = {}
+        if dtype == torch.bfloat16:
+            qkv_t = tuple(t for t in ("q", "k", "v") if t in self.targets)
+            if qkv_t:
+                self.stack["w_qkv"] = qkv_t
+            if "o" in self.targets:
+                self.stack["wo"] = ("o",)
+        self.use_stacked_decode = bool(self.stack)
+        self.pool.on_install = self._stack_install
+        self.pool.on_evict = self._stack_evict
 
     # ------------------------------------------------------------------ weights
     def load_backbone(self, weights: dict) -> None:
@@ -187,6 +206,7 @@ class MultiLoraModel:
             w[p + "w_down"] = down.to(dev)
         self.w = w
         self._pack()
+        self._restack()
 
     def _block_gate_up(self, gate: torch.Tensor, up: torch.Tensor) -> torch.Tensor:
         """[gate rows 128 | up rows 128] blocks, zero-padded to ffn_pad (SLX_EPI_SILU_MUL)."""
@@ -220,10 +240,11 @@ class MultiLoraModel:
             w[p + "w_down"] = down
             if self.dtype == torch.bfloat16:   # pack layer by layer to bound peak memory
                 for k in self.PROJ:
-                    w[p + k] = ops.pack_weight(w[p + k])
+                    w[p + k] = ops.pack_weight(w[p + k], self._extra_rows(k))
         if self.dtype == torch.bfloat16:
             w["lm_head"] = ops.pack_weight(w["lm_head"])
         self.w = w
+        self._restack()
 
     PROJ = ("w_qkv", "wo", "w_gu", "w_down")
 
@@ -233,8 +254,49 @@ class MultiLoraModel:
             return
         for k in list(self.w):
             if k == "lm_head" or k.split(".")[-1] in self.PROJ:
-                self.w[k] = ops.pack_weight(self.w[k])
+                self.w[k] = ops.pack_weight(self.w[k], self._extra_rows(k.split(".")[-1]))
         torch.cuda.synchronize(self.device)
+
+    def _extra_rows(self, proj: str) -> int:
+        targets = self.stack.get(proj, ())
+        return len(targets) * self.pool.n_slots * self.pool.max_rank
+
+    def _stack_rows(self, proj: str, t: str, slot: int) -> int:
+        return (self.stack[proj].index(t) * self.pool.n_slots + slot) * self.pool.max_rank
+
+    def _stack_install(self, slot: int, blob: torch.Tensor, lora) -> None:
+        if not self.stack or not self.w:
+            return
+        layout, _ = self.pool.blob_layout(lora.rank)
+        R = self.pool.max_rank
+        for l, t, ao, _bo, di, _do in layout:
+            for proj, ts in self.stack.items():
+                if t not in ts:
+                    continue
+                pw = self.w[f"layers.{l}.{proj}"]
+                row0 = pw.n + self._stack_rows(proj, t, slot)
+                if t in lora.targets:
+                    a = blob[ao:ao + lora.rank * di].view(lora.rank, di)
+                    ops.pack_rows(pw, a, lora.rank, row0)
+                    if lora.rank < R:
+                        ops.pack_rows(pw, None, R - lora.rank, row0 + lora.rank)
+                else:
+                    ops.pack_rows(pw, None, R, row0)
+
+    def _restack(self) -> None:
+        """(Re)write the stacked A rows of every resident adapter (backbone loaded later)."""
+        for slot, blob in enumerate(self.pool.blobs):
+            if blob is not None:
+                self._stack_install(slot, blob, self.pool.configs[slot])
+
+    def _stack_evict(self, slot: int) -> None:
+        if not self.stack or not self.w:
+            return
+        for l in range(self.cfg.layers):
+            for proj, ts in self.stack.items():
+                pw = self.w[f"layers.{l}.{proj}"]
+                for t in ts:
+                    ops.pack_rows(pw, None, self.pool.max_rank, pw.n + self._stack_rows(proj, t, slot))
 
     def backbone_bytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in self.w.values())
@@ -273,6 +335,17 @@ class MultiLoraModel:
         ops.lora_apply(y, x, d_in if d_in is not None else x.shape[1], self.pool.rank,
                        self.pool.scale, self.pool.max_rank, ops.make_targets(specs), self.lora_ws)
 
+    def _expand(self, y, v_all, layer: int, proj: str, cols) -> None:
+        specs, offs = [], []
+        for t in self.stack[proj]:
+            i = self.targets.index(t)
+            off, blk, stride = cols[t]
+            specs.append((self.pool.a_ptr[layer, i], self.pool.b_ptr[layer, i],
+                          self.cfg.target_dims(t)[1], off, blk, stride))
+            offs.append(self._stack_rows(proj, t, 0))
+        ops.lora_expand(y, v_all, self.pool.rank, self.pool.scale, self.pool.max_rank,
+                        ops.make_targets(specs), offs, self.lora_ws)
+
     def forward(self, tokens, pos, seq, slot, logit_rows=None, decode: bool = False) -> torch.Tensor:
         """Token-major mixed batch.  tokens/pos/seq/slot: device int32 [T].
         ``decode``: every token is the next position of its own sequence, so RoPE, the KV
@@ -291,6 +364,12 @@ class MultiLoraModel:
         mlp = torch.empty((T, self.ffn_pad), dtype=dt, device=dev)
         fused_silu = dt == torch.bfloat16 and not ({"gate", "up"} & set(self.targets))
         gu = None if fused_silu else torch.empty((T, 2 * self.ffn_pad), dtype=dt, device=dev)
+        stacked = self.use_stacked_decode and T <= 128 and bool(self.stack)
+        if stacked:
+            v_qkv = (torch.empty((T, self._extra_rows("w_qkv")), dtype=torch.float32, device=dev)
+                     if "w_qkv" in self.stack else None)
+            v_o = (torch.empty((T, self._extra_rows("wo")), dtype=torch.float32, device=dev)
+                   if "wo" in self.stack else None)
         ops.embedding(x, w["embed"], tokens)
         if self.targets:
             ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
@@ -298,8 +377,12 @@ class MultiLoraModel:
         for l in range(cfg.layers):
             p = f"layers.{l}."
             ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
-            self._gemm(h, w[p + "w_qkv"], qkv)
-            self._lora(qkv, h, l, ("q", "k", "v"), qkv_cols)
+            if stacked and "w_qkv" in self.stack:
+                ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv)
+                self._expand(qkv, v_qkv, l, "w_qkv", qkv_cols)
+            else:
+                self._gemm(h, w[p + "w_qkv"], qkv)
+                self._lora(qkv, h, l, ("q", "k", "v"), qkv_cols)
             if decode:
                 ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos,
                                           seq, self.cos, self.sin, self.k_cache[l], self.v_cache[l])
@@ -308,8 +391,12 @@ class MultiLoraModel:
                                   self.sin, self.k_cache[l], self.v_cache[l])
                 ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
                               self.k_cache[l], self.v_cache[l])
-            self._gemm(attn, w[p + "wo"], x, residual=x)
-            self._lora(x, attn, l, ("o",), {"o": (0, d, d)})
+            if stacked and "wo" in self.stack:
+                ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o)
+                self._expand(x, v_o, l, "wo", {"o": (0, d, d)})
+            else:
+                self._gemm(attn, w[p + "wo"], x, residual=x)
+                self._lora(x, attn, l, ("o",), {"o": (0, d, d)})
             ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
             if fused_silu:
                 self._gemm(h, w[p + "w_gu"], mlp, silu=True)

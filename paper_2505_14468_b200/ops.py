@@ -113,10 +113,11 @@ class Workspace:
 # ---------------------------------------------------------------------------------- K1
 class PackedWeight:
     """bf16 W[N, K] packed in the SLX_W_TILED layout ([N/128][K/64][128][64], zero-padded):
-    every TMA box the GEMM loads is one contiguous 16 KB HBM burst."""
+    every TMA box the GEMM loads is one contiguous 16 KB HBM burst.  ``n_extra`` rows after
+    the first ``n`` hold the stacked LoRA A of every adapter slot (decode shrink rows)."""
 
-    def __init__(self, data: torch.Tensor, n: int, k: int):
-        self.data, self.n, self.k = data, n, k
+    def __init__(self, data: torch.Tensor, n: int, k: int, n_extra: int = 0):
+        self.data, self.n, self.k, self.n_extra = data, n, k, n_extra
         self.shape = (n, k)
         self.dtype = torch.bfloat16
 
@@ -128,28 +129,54 @@ class PackedWeight:
 
 
 @_op("pack", 1)
-def pack_weight(w: torch.Tensor) -> PackedWeight:
+def pack_weight(w: torch.Tensor, extra_rows: int = 0) -> PackedWeight:
     if w.dtype != torch.bfloat16 or w.dim() != 2 or w.stride(1) != 1:
         raise ValueError("pack_weight: bf16 row-major [N, K] expected")
     N, K = w.shape
     lib = _lib.load()
+    if extra_rows:
+        if N % 128:
+            raise ValueError("pack_weight: stacked rows need N % 128 == 0")
+        out = torch.zeros(lib.slx_packed_weight_elems(N + extra_rows, K), dtype=torch.bfloat16,
+                          device=w.device)
+        check(lib.slx_pack_weight_rows(_ptr(out), _ptr(w), N, K, w.stride(0), 0, _stream()),
+              "slx_pack_weight_rows")
+        return PackedWeight(out, N, K, extra_rows)
     out = torch.empty(lib.slx_packed_weight_elems(N, K), dtype=torch.bfloat16, device=w.device)
     check(lib.slx_pack_weight(_ptr(out), _ptr(w), N, K, w.stride(0), _stream()), "slx_pack_weight")
     return PackedWeight(out, N, K)
 
 
+@_op("pack", 1)
+def pack_rows(pw: PackedWeight, src: torch.Tensor | None, n_rows: int, row0: int) -> None:
+    """(Re)write rows [row0, row0+n_rows) of a packed weight from row-major bf16 src (None =
+    zeros)."""
+    if src is not None and (src.dtype != torch.bfloat16 or src.stride(-1) != 1):
+        raise ValueError("pack_rows: bf16 row-major src expected")
+    ld = src.stride(0) if src is not None and src.dim() == 2 else pw.k
+    check(_lib.load().slx_pack_weight_rows(_ptr(pw.data), _ptr(src), n_rows, pw.k, ld, row0,
+                                           _stream()), "slx_pack_weight_rows")
+
+
 @_op("gemm", 1)
 def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
          epilogue: int = EPI_NONE, residual: torch.Tensor | None = None,
-         out_dtype: torch.dtype | None = None, ws=None) -> torch.Tensor:
+         out_dtype: torch.dtype | None = None, ws=None, side: torch.Tensor | None = None
+         ) -> torch.Tensor:
     """bf16 tcgen05 GEMM: out = a @ w.T (+ residual | silu*mul of blocked gate/up).
-    ``w`` is a row-major bf16 [N, K] tensor or a :class:`PackedWeight`."""
+    ``w`` is a row-major bf16 [N, K] tensor or a :class:`PackedWeight`; with ``side`` (fp32
+    [M, n_extra]) the packed weight's stacked extra rows are computed too (LoRA shrink)."""
     if a.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
         raise ValueError("gemm: a and w must be bf16")
     M, K = a.shape
     N, Kw = w.shape
+    n_main, n_tot = N, N
     if isinstance(w, PackedWeight):
         layout, wt = W_TILED, w.data
+        if side is not None:
+            if side.dtype != torch.float32 or side.shape[0] != M or side.shape[1] < w.n_extra:
+                raise ValueError("gemm: side output must be fp32 [M, n_extra]")
+            n_tot = N + w.n_extra
     else:
         if not w.is_contiguous():
             raise ValueError("gemm: w must be contiguous [N, K]")
@@ -163,7 +190,9 @@ def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
         raise ValueError("gemm: residual must have the output dtype")
     check(_lib.load().slx_gemm_bf16(_ptr(a), _ld(a), _ptr(wt), _ptr(out), _ld(out), _dt(out),
                                     _ptr(residual), _ld(residual) if residual is not None else 0,
-                                    M, N, K, epilogue, layout, _stream()), "slx_gemm_bf16")
+                                    M, n_tot, K, epilogue, layout, n_main,
+                                    _ptr(side) if n_tot > n_main else None,
+                                    _ld(side) if n_tot > n_main else 0, _stream()), "slx_gemm_bf16")
     return out
 
 
@@ -242,6 +271,17 @@ def lora_sgmv(y, x, seg_indptr, seg_slot, slot_rank, slot_scale, max_rank, targe
                                     _ptr(slot_rank), _ptr(slot_scale), slot_rank.numel(),
                                     max_rank, len(targets), targets, _ptr(ws), ws.numel(),
                                     _stream()), "slx_lora_sgmv")
+
+
+@_op("lora", 1)
+def lora_expand(y: torch.Tensor, v_all: torch.Tensor, slot_rank, slot_scale, max_rank: int,
+                targets, v_col_off, ws: torch.Tensor) -> None:
+    """Decode expand after the GEMM-side shrink: y[t, col(n)] += scale * v . B_slot^T."""
+    offs = (ctypes.c_int * len(v_col_off))(*v_col_off)
+    check(_lib.load().slx_lora_expand(_dt(y), _ptr(y), _ld(y), _ptr(v_all), _ld(v_all), y.shape[0],
+                                      _ptr(slot_rank), _ptr(slot_scale), slot_rank.numel(), max_rank,
+                                      len(targets), targets, offs, _ptr(ws), ws.numel(), _stream()),
+          "slx_lora_expand")
 
 
 # ---------------------------------------------------------------------------------- K4

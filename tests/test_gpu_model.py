@@ -101,3 +101,43 @@ def test_bf16_all_linear_targets_logits(golden):
     ref = orc.prefill(prompts[:6], ids)
     seqs, got = m.prefill(prompts[:6], ids)
     np.testing.assert_allclose(got.cpu().numpy(), ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
+def test_bf16_stacked_decode_shrink_matches_sgmv_path(golden):
+    """Decode LoRA with the shrink inside the projection GEMM (stacked A rows, fp32 side
+    output) + expand kernel == the shrink/expand kernel path == the oracle; mixed ranks."""
+    cfg = TINY
+    seed = int(golden["seed"])
+    w = init_backbone(cfg, seed)
+    loras = [LoraConfig(8, 16.0), LoraConfig(16, 8.0), LoraConfig(8, 16.0), LoraConfig(16, 32.0)]
+    ads = [init_adapter(cfg, lo, seed, a) for a, lo in enumerate(loras)]
+    m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=8, max_ctx=64, n_slots=6, max_rank=16,
+                       max_tokens=512)
+    m.load_backbone(w)
+    for a, (ad, lo) in enumerate(zip(ads, loras)):
+        m.pool.load(a, ad, lo)
+    prompts = [[5, 9, 200, 31], [7, 7, 7], [100, 2, 3, 4, 5], [9]]
+    ids = [0, 1, 3, 2]
+    seqs, _ = m.prefill(prompts, ids)
+    toks = [11, 12, 13, 14]
+    got = {}
+    for stacked in (True, False):
+        m.use_stacked_decode = stacked
+        for s_ in seqs:
+            m.seq_len[s_] = len(prompts[seqs.index(s_)])
+        got[stacked] = m.decode(seqs, toks, ids).cpu().numpy()
+    np.testing.assert_allclose(got[True], got[False], rtol=1e-2, atol=1e-2)
+    orc = OracleModel(cfg, w, ads, [lo.scale for lo in loras], loras[0].targets)
+    orc.prefill(prompts, ids)
+    ref = orc.decode(list(range(4)), toks, ids)
+    np.testing.assert_allclose(got[True], ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+    # eviction zeroes the stacked rows: slot 1 then behaves like the bare backbone
+    m.use_stacked_decode = True
+    m.pool.evict(1)
+    for s_ in seqs:
+        m.seq_len[s_] = len(prompts[seqs.index(s_)])
+    ev = m.decode(seqs, toks, [0, -1, 3, 2]).cpu().numpy()
+    for s_ in seqs:
+        m.seq_len[s_] = len(prompts[seqs.index(s_)])
+    ev2 = m.decode(seqs, toks, [0, 1, 3, 2]).cpu().numpy()   # slot 1 evicted: rank 0
+    np.testing.assert_allclose(ev[1], ev2[1], rtol=1e-2, atol=1e-2)
