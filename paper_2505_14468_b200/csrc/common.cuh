@@ -103,9 +103,11 @@ namespace slx {
 
 // Programmatic dependent launch: every kernel of the library calls pdl_wait() before it
 // touches global memory produced or consumed by earlier kernels on the stream, and
-// pdl_trigger() once its own CTAs are resident, so the next kernel's prologue (barrier
-// init, TMEM alloc, weight prefetch) overlaps this kernel's tail.  Both are no-ops when the
-// kernel was launched without the attribute.
+// pdl_trigger() only AFTER its own pdl_wait(), so the next kernel's prologue (barrier init,
+// TMEM alloc, weight prefetch) overlaps this kernel's body.  Invariant this buys: when a
+// kernel of the library starts, every library kernel two or more launches back on the
+// stream has completed, so data they produced (e.g. the step's LoRA plan) may be read
+// before this kernel's own pdl_wait().  Both are no-ops without the launch attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

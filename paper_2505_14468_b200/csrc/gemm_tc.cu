@@ -151,7 +151,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem_base = *tmem_slot;
-  pdl_trigger();
+  if (!(warp == 0 && lane == 0)) {
+    pdl_wait();
+    pdl_trigger();
+  }
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer
@@ -171,6 +174,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       load_w(smem + i * stage_bytes, &full[i], kb_lo + i);
     }
     pdl_wait();
+    pdl_trigger();
     for (int i = 0; i < npre; ++i)
       tc::tma_load_2d(smem + i * stage_bytes, &tmap_x, &full[i], (kb_lo + i) * TC_BK, m0, pol_x);
     for (int i = npre; i < n_kb; ++i) {
@@ -202,7 +206,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   }
 
   // ---------------- epilogue: all 4 warps; warp w owns TMEM lanes (token rows) [32w, 32w+32)
-  pdl_wait();
   tc::mbar_wait(accum, 0);
   __syncwarp();
   tc::fence_after_sync();
@@ -521,8 +524,8 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
 namespace slx {
 __global__ void pack_weight_kernel(bf16* __restrict__ dst, const bf16* __restrict__ src, int N,
                                    int K, int ld, int kblocks) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   // one thread per 16-byte chunk of the packed tensor
   const size_t chunk = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t total = (size_t)ceil_div(N, 128) * kblocks * 128 * 8;
@@ -542,8 +545,8 @@ __global__ void pack_weight_kernel(bf16* __restrict__ dst, const bf16* __restric
 // Write rows [row0, row0 + n) of an already packed (SLX_W_TILED) matrix from row-major src.
 __global__ void pack_rows_kernel(bf16* __restrict__ dst, const bf16* __restrict__ src, int n,
                                  int K, int ld, int row0, int kblocks) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const size_t chunk = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t total = (size_t)n * kblocks * 8;
   if (chunk >= total) return;

@@ -90,8 +90,8 @@ __device__ void emit_tiles(const int* g_slot, const int* g_start, const int* g_c
 
 __global__ void __launch_bounds__(PLAN_THREADS)
 plan_tokens_kernel(const int32_t* __restrict__ tok_slot, int n_tok, int n_slots, LoraWs ws) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   __shared__ int cnt[PLAN_MAX_GROUPS];
   __shared__ int start[PLAN_MAX_GROUPS];
   __shared__ int slot_id[PLAN_MAX_GROUPS];
@@ -130,8 +130,8 @@ plan_tokens_kernel(const int32_t* __restrict__ tok_slot, int n_tok, int n_slots,
 __global__ void __launch_bounds__(PLAN_THREADS)
 plan_segments_kernel(const int32_t* __restrict__ seg_indptr, const int32_t* __restrict__ seg_slot,
                      int n_seg, int n_tok, int n_slots, LoraWs ws) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   __shared__ int cnt[PLAN_MAX_GROUPS];
   __shared__ int start[PLAN_MAX_GROUPS];
   __shared__ int slot_id[PLAN_MAX_GROUPS];
@@ -163,8 +163,8 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 lora_shrink_kernel(const T* __restrict__ x, int ldx, int n_tok, int d_in, int ks,
                    const int32_t* __restrict__ slot_rank, int max_rank, TargetArgs ta, LoraWs ws) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const int tile_id = blockIdx.x;
   if (tile_id >= *ws.n_tiles) return;
   const LoraTile tile = ws.tiles[tile_id];
@@ -257,8 +257,8 @@ __global__ void __launch_bounds__(256)
 lora_expand_kernel(T* __restrict__ y, int ldy, int n_tok, int ks, int n_split,
                    const int32_t* __restrict__ slot_rank, const float* __restrict__ slot_scale,
                    int max_rank, TargetArgs ta, LoraWs ws) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const int tile_id = blockIdx.x;
   if (tile_id >= *ws.n_tiles) return;
   const LoraTile tile = ws.tiles[tile_id];
@@ -321,8 +321,8 @@ lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, 
                   int ks, int kc, int ns, const int32_t* __restrict__ slot_rank,
                   const float* __restrict__ slot_scale, int max_rank, TargetArgs ta, LoraWs ws) {
   extern __shared__ __align__(16) uint8_t fsm[];
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const int q = (int)tc::cluster_ctarank();
   const int tile_id = blockIdx.x / ks;
   const int tgt = blockIdx.y;
@@ -477,15 +477,19 @@ lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, in
                      const int32_t* __restrict__ slot_rank, const float* __restrict__ slot_scale,
                      int max_rank, TargetArgs ta, ExpandArgs ea, LoraWs ws) {
   extern __shared__ __align__(16) uint8_t esm[];
-  pdl_trigger();
-  pdl_wait();
+  // The plan (kernel at the start of the step) and the adapter pool (static) are >= 2
+  // launches back: read them and start streaming B before waiting on the shrink GEMM.
   const int tile_id = blockIdx.x;
-  if (tile_id >= *ws.n_tiles) return;
-  const LoraTile tile = ws.tiles[tile_id];
+  const bool live = tile_id < *ws.n_tiles;
   const int tgt = blockIdx.y;
   const int d_out = ta.d_out[tgt];
   const int n_lo = blockIdx.z * EX_CHUNK;
-  if (n_lo >= d_out) return;
+  if (!live || n_lo >= d_out) {
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
+  const LoraTile tile = ws.tiles[tile_id];
   const int nn = min(EX_CHUNK, d_out - n_lo);
   const int cnt = tile.count;
   const int rank = min(slot_rank[tile.slot], max_rank);
@@ -501,12 +505,14 @@ lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, in
   float* vs = reinterpret_cast<float*>(ys + (size_t)LORA_TT * EX_CHUNK);
   int* toks = reinterpret_cast<int*>(vs + LORA_TT * max_rank);
   if (threadIdx.x < LORA_TT) toks[threadIdx.x] = threadIdx.x < cnt ? ws.perm[tile.start + threadIdx.x] : 0;
-  __syncthreads();
   const int bchunks = nn * rank / 8;   // rows n_lo..n_lo+nn of B are contiguous
   for (int e = threadIdx.x; e < bchunks; e += EX_THREADS) {
     const int flat = e * 8;
     cp_async16(bs + (size_t)(flat / rank) * max_rank + flat % rank, B + (size_t)n_lo * rank + flat);
   }
+  pdl_wait();       // v_all and y come from the GEMM just before us
+  pdl_trigger();
+  __syncthreads();  // toks visible
   constexpr int XV = 16 / sizeof(T);
   if (y_contig) {
     const int ych = nn / XV;

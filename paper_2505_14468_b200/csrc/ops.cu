@@ -12,8 +12,8 @@ namespace slx {
 template <typename T>
 __global__ void embedding_kernel(T* __restrict__ out, const bf16* __restrict__ table,
                                  const int32_t* __restrict__ tokens, int d, int vocab) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   int tok = tokens[t];
   tok = tok < 0 ? 0 : (tok >= vocab ? vocab - 1 : tok);
@@ -31,8 +31,8 @@ __global__ void embedding_kernel(T* __restrict__ out, const bf16* __restrict__ t
 template <typename T>
 __global__ void rmsnorm_kernel(T* __restrict__ out, int ldo, const T* __restrict__ x, int ldx,
                                const bf16* __restrict__ w, int d, float eps) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   const T* xr = x + (size_t)t * ldx;
   float ss = 0.f;
@@ -72,8 +72,8 @@ __global__ void rope_kv_kernel(T* __restrict__ qkv, int ld, int H, int Hkv, int 
                                const int32_t* __restrict__ tok_seq,
                                const float* __restrict__ cos_tab, const float* __restrict__ sin_tab,
                                T* __restrict__ kc, T* __restrict__ vc, int max_ctx) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.x;
   const int pos = tok_pos[t];
   const int seq = tok_seq[t];
@@ -139,8 +139,8 @@ __global__ void __launch_bounds__(ATT_WARPS * 32)
 attention_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv, int ld, int H, int Hkv,
                  const int32_t* __restrict__ tok_pos, const int32_t* __restrict__ tok_seq,
                  const T* __restrict__ kc, const T* __restrict__ vc, int max_ctx, float scale_log2) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   constexpr int PL = D / 32;   // output dims per lane
   __shared__ float qs[D];
   __shared__ float m_s[ATT_WARPS], l_s[ATT_WARPS];
@@ -253,8 +253,8 @@ rope_attn_decode_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv,
                         const int32_t* __restrict__ tok_seq, const float* __restrict__ cos_tab,
                         const float* __restrict__ sin_tab, T* __restrict__ kc, T* __restrict__ vc,
                         int max_ctx, float scale_log2) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   constexpr int KB = DecCfg<T>::KB;
   constexpr int VEC = 16 / sizeof(T);
   constexpr int DP = D + VEC;          // padded smem row
@@ -384,8 +384,8 @@ rope_attn_decode_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv,
 template <typename T>
 __global__ void silu_mul_kernel(T* __restrict__ out, int ldo, const T* __restrict__ gu, int ld_gu,
                                 int ffn) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const int t = blockIdx.y;
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (i >= ffn) return;
@@ -402,8 +402,8 @@ __global__ void silu_mul_kernel(T* __restrict__ out, int ldo, const T* __restric
 // ------------------------------------------------------------------ argmax
 template <typename T>
 __global__ void argmax_kernel(int32_t* __restrict__ out, const T* __restrict__ x, int ld, int n) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   const T* row = x + (size_t)blockIdx.x * ld;
   float best = -FLT_MAX;
   int bi = 0x7fffffff;
@@ -436,8 +436,8 @@ __global__ void __launch_bounds__(256)
 gemm_f32_kernel(const float* __restrict__ A, int lda, const bf16* __restrict__ W,
                 float* __restrict__ C, int ldc, const float* __restrict__ R, int ldr,
                 int M, int N, int K) {
-  pdl_trigger();
   pdl_wait();
+  pdl_trigger();
   __shared__ float As[SG_BK][SG_BM + 4];
   __shared__ float Ws[SG_BK][SG_BN + 4];
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
