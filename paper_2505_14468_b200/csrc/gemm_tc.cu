@@ -33,7 +33,7 @@ namespace slx {
 
 constexpr int TC_THREADS = 128;
 constexpr int TC_BK = 64;       // 64 bf16 = one 128-byte swizzle row
-constexpr int TC_BN = 256;      // weight rows per tile (MMA N)
+constexpr int TC_BN_MAX = 256;  // weight rows per tile (MMA N): 256 or 128
 constexpr int TC_MAX_STAGES = 8;
 constexpr int W_BLOCK_BYTES = 128 * TC_BK * 2;   // 16 KB: one 128-row weight box
 constexpr int TC_MAX_CLUSTER = 8;
@@ -112,14 +112,15 @@ __device__ __forceinline__ void w_coord(const GemmArgs& g, int row0, int kb, int
   }
 }
 
-template <int EPI, typename OutT>
+template <int EPI, typename OutT, int TC_BN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                GemmArgs g) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int x_bytes = g.bm * TC_BK * 2;
-  const int stage_bytes = x_bytes + 2 * W_BLOCK_BYTES;
+  constexpr int WB = TC_BN / 128;   // 128-row weight boxes per stage
+  const int stage_bytes = x_bytes + WB * W_BLOCK_BYTES;
   uint64_t* full = (uint64_t*)(smem + g.stages * stage_bytes);
   uint64_t* empty = full + TC_MAX_STAGES;
   uint64_t* accum = empty + TC_MAX_STAGES;
@@ -161,7 +162,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     const uint64_t pol_w = tc::policy_evict_first();  // weights: streamed once
     const uint64_t pol_x = tc::policy_evict_last();   // activations: re-read by every tile
     auto load_w = [&](uint8_t* st, uint64_t* bar, int kb) {
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < WB; ++b) {
         int c0, c1;
         w_coord(g, n0 + b * 128, kb, c0, c1);
         tc::tma_load_2d(st + x_bytes + b * W_BLOCK_BYTES, &tmap_w, bar, c0, c1, pol_w);
@@ -244,6 +245,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     // smem as red[row][col] (row stride RED_LD floats, padded against bank conflicts), then
     // reduce a 1/S slice of the columns across the cluster with 16-byte DSMEM loads.
     constexpr int RED_LD = TC_BN + 4;
+    static_assert(EPI != SLX_EPI_SILU_MUL || TC_BN == 256, "SiLU pairs need 256-wide tiles");
     float* red = reinterpret_cast<float*>(smem);
     if (warp_live) {
       for (int c0 = 0; c0 < TC_BN; c0 += 16) {
@@ -352,7 +354,7 @@ static void configure_kernel(const void* k) {
 }
 
 struct GemmPlan {
-  int bm, stages, kblocks, splits, n_tiles, m_tiles;
+  int bn, bm, stages, kblocks, splits, n_tiles, m_tiles;
   size_t smem;
 };
 
@@ -365,7 +367,7 @@ static int max_active_clusters(size_t smem, int cluster) {
   static int n_cache = 0;
   for (int i = 0; i < n_cache; ++i)
     if (cache[i].smem == smem && cache[i].cluster == cluster) return cache[i].value;
-  auto k = gemm_tc_kernel<SLX_EPI_NONE, bf16>;
+  auto k = gemm_tc_kernel<SLX_EPI_NONE, bf16, 256>;
   configure_kernel((const void*)k);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cluster * 64);
@@ -390,57 +392,66 @@ static int max_active_clusters(size_t smem, int cluster) {
 // Few tiles (decode): pick CTAs/SM (1 or 2) and the cluster split S that cover the most SMs
 // in ONE wave (cudaOccupancyMaxActiveClusters), every split keeping >= 4 k-blocks and its
 // partial tile fitting the pipeline smem.  SLX_GEMM_{CTAS,SPLITS,STAGES} override (tuning).
-static GemmPlan plan_gemm(int M, int N, int K) {
+static GemmPlan plan_gemm(int M, int N, int K, bool silu) {
   GemmPlan p{};
   p.kblocks = ceil_div(K, TC_BK);
-  p.n_tiles = ceil_div(N, TC_BN);
   p.m_tiles = ceil_div(M, 128);
   p.bm = M >= 128 ? 128 : ((M + 15) / 16) * 16;
-  const size_t stage = (size_t)p.bm * TC_BK * 2 + 2 * W_BLOCK_BYTES;
-  const size_t red = (size_t)(TC_BN + 4) * p.bm * 4;
   const int sms = sm_count();
-  const int tiles = p.n_tiles * p.m_tiles;
   const int e_ctas = env_int("SLX_GEMM_CTAS", 0), e_s = env_int("SLX_GEMM_SPLITS", 0);
-  const int e_st = env_int("SLX_GEMM_STAGES", 0);
+  const int e_st = env_int("SLX_GEMM_STAGES", 0), e_bn = env_int("SLX_GEMM_BN", 0);
   double best = -1.0;
-  for (int ctas = 1; ctas <= 2; ++ctas) {
-    if (e_ctas && ctas != e_ctas) continue;
-    const size_t budget = ctas == 2 ? 112 * 1024 - 1024 - BAR_BYTES : 225 * 1024 - 1024 - BAR_BYTES;
-    int st = (int)(budget / stage);
-    st = st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
-    if (e_st >= 2 && e_st < st) st = e_st;
-    if (st < 2) continue;
-    const size_t smem = (size_t)st * stage + BAR_BYTES + 1024;
-    for (int s = 1; s <= TC_MAX_CLUSTER; ++s) {
-      if (e_s && s != e_s) continue;
-      if (s > 1 && (p.m_tiles > 1 || (size_t)st * stage < red)) continue;
-      if (!e_s && s > 1 && ceil_div(p.kblocks, s) < 4) continue;
-      if ((s - 1) * ceil_div(p.kblocks, s) >= p.kblocks && s > 1) continue;   // no empty split
-      const int ctas_total = tiles * s;
-      if (!e_s && ctas_total > ctas * sms) continue;                            // one wave
-      if (s > 1 && !e_s && tiles > max_active_clusters(smem, s)) continue;
-      const int covered = ctas_total < sms ? ctas_total : sms;
-      const double score = covered * 1000.0 + st * 10.0 - ctas;   // SMs covered, then depth
-      if (score > best) {
-        best = score;
-        p.stages = st; p.splits = s; p.smem = smem;
+  for (int bn = 256; bn >= 128; bn -= 128) {
+    if (silu && bn != 256) continue;
+    if (e_bn && bn != e_bn) continue;
+    const int n_tiles = ceil_div(N, bn);
+    const int tiles = n_tiles * p.m_tiles;
+    const size_t stage = (size_t)p.bm * TC_BK * 2 + (size_t)(bn / 128) * W_BLOCK_BYTES;
+    const size_t red = (size_t)(bn + 4) * p.bm * 4;
+    for (int ctas = 1; ctas <= 2; ++ctas) {
+      if (e_ctas && ctas != e_ctas) continue;
+      const size_t budget = ctas == 2 ? 112 * 1024 - 1024 - BAR_BYTES : 225 * 1024 - 1024 - BAR_BYTES;
+      int st = (int)(budget / stage);
+      st = st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
+      if (e_st >= 2 && e_st < st) st = e_st;
+      if (st < 2) continue;
+      const size_t smem = (size_t)st * stage + BAR_BYTES + 1024;
+      for (int s = 1; s <= TC_MAX_CLUSTER; ++s) {
+        if (e_s && s != e_s) continue;
+        if (s > 1 && (p.m_tiles > 1 || (size_t)st * stage < red)) continue;
+        if (!e_s && s > 1 && ceil_div(p.kblocks, s) < 4) continue;
+        if ((s - 1) * ceil_div(p.kblocks, s) >= p.kblocks && s > 1) continue;   // no empty split
+        const int ctas_total = tiles * s;
+        if (!e_s && ctas_total > ctas * sms) continue;                            // one wave
+        if (s > 1 && !e_s && tiles > max_active_clusters(smem, s)) continue;
+        const int covered = ctas_total < sms ? ctas_total : sms;
+        // SMs covered; then wider tiles (fewer MMAs per weight byte), deeper pipelines,
+        // fewer splits (less reduction), one CTA per SM
+        const double score = covered * 1000.0 + (bn == 256 ? 50.0 : 0.0) + st * 10.0 - s - ctas;
+        if (score > best) {
+          best = score;
+          p.bn = bn; p.n_tiles = n_tiles; p.stages = st; p.splits = s; p.smem = smem;
+        }
       }
     }
   }
   if (best < 0) {   // many tiles (prefill) or overrides that cannot apply: one CTA/SM, no split
+    p.bn = (e_bn == 128 && !silu) ? 128 : 256;
+    p.n_tiles = ceil_div(N, p.bn);
     p.splits = 1;
+    const size_t stage = (size_t)p.bm * TC_BK * 2 + (size_t)(p.bn / 128) * W_BLOCK_BYTES;
     int st = (int)((225 * 1024 - 1024 - BAR_BYTES) / stage);
     p.stages = st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
-    if (p.stages > 4 && tiles >= sms) p.stages = 4;
+    if (p.stages > 4 && p.n_tiles * p.m_tiles >= sms) p.stages = 4;
     p.smem = (size_t)p.stages * stage + BAR_BYTES + 1024;
   }
   return p;
 }
 
-template <int EPI, typename OutT>
+template <int EPI, typename OutT, int BN>
 static int launch_tc(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& a, dim3 grid,
                      size_t smem, unsigned cluster, cudaStream_t s) {
-  auto k = gemm_tc_kernel<EPI, OutT>;
+  auto k = gemm_tc_kernel<EPI, OutT, BN>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     configure_kernel((const void*)k);
@@ -449,16 +460,22 @@ static int launch_tc(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArg
   return launch_ex(k, grid, dim3(TC_THREADS), smem, s, cluster, mx, mw, a);
 }
 
-static int dispatch_tc(int epi, int c_dtype, const CUtensorMap& mx, const CUtensorMap& mw,
+template <typename OutT, int BN>
+static int dispatch_epi(int epi, const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& a,
+                        dim3 grid, size_t smem, unsigned cl, cudaStream_t s) {
+  if (epi == SLX_EPI_NONE) return launch_tc<SLX_EPI_NONE, OutT, BN>(mx, mw, a, grid, smem, cl, s);
+  if (epi == SLX_EPI_RESIDUAL) return launch_tc<SLX_EPI_RESIDUAL, OutT, BN>(mx, mw, a, grid, smem, cl, s);
+  if (BN == 256) return launch_tc<SLX_EPI_SILU_MUL, OutT, 256>(mx, mw, a, grid, smem, cl, s);
+  return SLX_ERR_UNSUPPORTED;
+}
+
+static int dispatch_tc(int epi, int c_dtype, int bn, const CUtensorMap& mx, const CUtensorMap& mw,
                        const GemmArgs& a, dim3 grid, size_t smem, unsigned cl, cudaStream_t s) {
-  if (c_dtype == SLX_DT_BF16) {
-    if (epi == SLX_EPI_NONE) return launch_tc<SLX_EPI_NONE, bf16>(mx, mw, a, grid, smem, cl, s);
-    if (epi == SLX_EPI_RESIDUAL) return launch_tc<SLX_EPI_RESIDUAL, bf16>(mx, mw, a, grid, smem, cl, s);
-    return launch_tc<SLX_EPI_SILU_MUL, bf16>(mx, mw, a, grid, smem, cl, s);
-  }
-  if (epi == SLX_EPI_NONE) return launch_tc<SLX_EPI_NONE, float>(mx, mw, a, grid, smem, cl, s);
-  if (epi == SLX_EPI_RESIDUAL) return launch_tc<SLX_EPI_RESIDUAL, float>(mx, mw, a, grid, smem, cl, s);
-  return launch_tc<SLX_EPI_SILU_MUL, float>(mx, mw, a, grid, smem, cl, s);
+  if (c_dtype == SLX_DT_BF16)
+    return bn == 256 ? dispatch_epi<bf16, 256>(epi, mx, mw, a, grid, smem, cl, s)
+                     : dispatch_epi<bf16, 128>(epi, mx, mw, a, grid, smem, cl, s);
+  return bn == 256 ? dispatch_epi<float, 256>(epi, mx, mw, a, grid, smem, cl, s)
+                   : dispatch_epi<float, 128>(epi, mx, mw, a, grid, smem, cl, s);
 }
 
 }  // namespace slx
@@ -496,10 +513,10 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   }
   if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= n_main && ldr % 8 == 0);
   if (M == 0) return SLX_OK;
-  GemmPlan p = plan_gemm(M, N, K);
+  GemmPlan p = plan_gemm(M, N, K, epilogue == SLX_EPI_SILU_MUL);
   if (env_int("SLX_GEMM_DEBUG", 0))
-    fprintf(stderr, "[slx_gemm] M=%d N=%d K=%d epi=%d bm=%d stages=%d splits=%d tiles=%dx%d smem=%zu\n",
-            M, N, K, epilogue, p.bm, p.stages, p.splits, p.n_tiles, p.m_tiles, p.smem);
+    fprintf(stderr, "[slx_gemm] M=%d N=%d K=%d epi=%d bn=%d bm=%d stages=%d splits=%d tiles=%dx%d smem=%zu\n",
+            M, N, K, epilogue, p.bn, p.bm, p.stages, p.splits, p.n_tiles, p.m_tiles, p.smem);
   GemmArgs a{};
   a.M = M; a.N = N; a.K = K;
   a.bm = p.bm; a.stages = p.stages; a.kblocks = p.kblocks; a.splits = p.splits;
@@ -516,7 +533,7 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   if (!make_tmap(&mx, A, M, K, lda, p.bm) || !make_tmap(&mw, W, w_rows, w_cols, w_cols, 128))
     return SLX_ERR_CUDA;
   dim3 grid((unsigned)(p.n_tiles * p.splits), (unsigned)p.m_tiles);
-  return dispatch_tc(epilogue, c_dtype, mx, mw, a, grid, p.smem, (unsigned)p.splits,
+  return dispatch_tc(epilogue, c_dtype, p.bn, mx, mw, a, grid, p.smem, (unsigned)p.splits,
                      (cudaStream_t)stream);
 }
 

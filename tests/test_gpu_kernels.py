@@ -40,8 +40,9 @@ def test_gemm_matches_torch_fp32(M, N, K, tiled):
 
 
 @pytest.mark.parametrize("M", [1, 64, 100])
+@pytest.mark.parametrize("bn", [256, 128])
 @pytest.mark.parametrize("ctas,splits", [(1, 1), (2, 8), (1, 3), (1, 6), (2, 2), (1, 5)])
-def test_gemm_decode_tilings(M, ctas, splits, monkeypatch):
+def test_gemm_decode_tilings(M, bn, ctas, splits, monkeypatch):
     """Every cluster split-K tiling the planner can pick gives the same result."""
     N, K = 3072, 4096
     a = bf(torch.randn(M, K, device=DEV))
@@ -49,6 +50,7 @@ def test_gemm_decode_tilings(M, ctas, splits, monkeypatch):
     ref = a.float() @ w.float().T
     monkeypatch.setenv("SLX_GEMM_CTAS", str(ctas))
     monkeypatch.setenv("SLX_GEMM_SPLITS", str(splits))
+    monkeypatch.setenv("SLX_GEMM_BN", str(bn))
     out = ops.gemm(a, ops.pack_weight(w), out_dtype=torch.float32)
     torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
     # SiLU and residual epilogues through the same split-K reduction
@@ -56,6 +58,7 @@ def test_gemm_decode_tilings(M, ctas, splits, monkeypatch):
     o2 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_RESIDUAL, residual=r, out_dtype=torch.float32)
     torch.testing.assert_close(o2, ref + r, rtol=1e-4, atol=1e-3)
     g_, u_ = ref.view(M, N // 256, 2, 128)[:, :, 0], ref.view(M, N // 256, 2, 128)[:, :, 1]
+    monkeypatch.setenv("SLX_GEMM_BN", "256")   # SiLU pairs always use 256-wide tiles
     o3 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_SILU_MUL, out_dtype=torch.float32)
     torch.testing.assert_close(o3, (g_ * torch.sigmoid(g_) * u_).reshape(M, N // 2), rtol=1e-3, atol=1e-3)
 
@@ -286,3 +289,21 @@ def test_rope_attention_decode_fused(dtype, H, Hkv, D, ctx):
             q = orc.apply_rope(q, np.array([ctx]), cos, sin)
         ref = orc.attention(q, kk[b].transpose(1, 0, 2), vv[b].transpose(1, 0, 2), np.array([ctx]))
         np.testing.assert_allclose(out_f[b].float().cpu().numpy(), ref.reshape(-1), rtol=tol * 5, atol=tol * 5)
+
+
+@pytest.mark.parametrize("M", [1, 64, 300])
+def test_gemm_lora_side_output(M):
+    """Stacked extra rows of a packed weight land, in fp32, in the side output; the main
+    columns keep the residual epilogue."""
+    N, E, K = 512, 384, 4096
+    a = bf(torch.randn(M, K, device=DEV))
+    w = bf(torch.randn(N, K, device=DEV) * 0.05)
+    ext = bf(torch.randn(E, K, device=DEV) * 0.05)
+    pw = ops.pack_weight(w, extra_rows=E)
+    ops.pack_rows(pw, ext, E, N)
+    x = bf(torch.randn(M, N, device=DEV))
+    ref_main = a.float() @ w.float().T + x.float()
+    side = torch.empty(M, E, device=DEV)
+    ops.gemm(a, pw, x, epilogue=EPI_RESIDUAL, residual=x, side=side)
+    torch.testing.assert_close(x.float(), ref_main, rtol=1e-2, atol=2e-2)
+    torch.testing.assert_close(side, a.float() @ ext.float().T, rtol=1e-4, atol=1e-3)
