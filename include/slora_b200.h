@@ -173,6 +173,14 @@ SLX_API int slx_rope_attention_decode(int dtype, void* out, int ldo, const void*
                   int n_tok, int heads, int kv_heads, int head_dim, const int32_t* tok_pos,
                   const int32_t* tok_seq, const float* cos_tab, const float* sin_tab, int max_pos,
                   void* k_cache, void* v_cache, int max_ctx, void* stream);
+/* Prefill (tensor cores, mma.sync flash attention, head_dim 128, bf16): `tiles` is a device
+ * array of n_tiles {int tok0, nq, seq, pos0} (<= 64 queries of one segment each, size
+ * slx_flash_prefill_tile_bytes()); query t of a tile attends cache positions 0..pos0+t of
+ * its sequence (k/v already appended by slx_rope_kv_write, q rotated in qkv). */
+SLX_API size_t slx_flash_prefill_tile_bytes(void);
+SLX_API int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld_qkv, int heads,
+                  int kv_heads, int head_dim, const void* tiles, int n_tiles, const void* k_cache,
+                  const void* v_cache, int max_ctx, void* stream);
 /* gu [n_tok, 2*ffn] in the blocked layout of SLX_EPI_SILU_MUL -> out [n_tok, ffn]. */
 SLX_API int slx_silu_mul_blocked(int dtype, void* out, int ldo, const void* gu, int ld_gu, int n_tok,
                          int ffn, void* stream);

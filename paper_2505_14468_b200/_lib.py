@@ -68,6 +68,8 @@ SIGNATURES = {
     "slx_attention": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p]),
     "slx_rope_attention_decode": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p,
                                        _i, _p]),
+    "slx_flash_prefill_tile_bytes": (_sz, []),
+    "slx_attention_prefill": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _i, _p, _p, _i, _p]),
     "slx_silu_mul_blocked": (_i, [_i, _p, _i, _p, _i, _i, _i, _p]),
     "slx_argmax": (_i, [_i, _p, _p, _i, _i, _i, _p]),
     "slx_host_register": (_i, [_p, _sz]),

@@ -43,7 +43,8 @@ def measure_prefill_ms(model, adapter_slot: int, b: int, prompt_len: int, seed: 
     seq = torch.from_numpy(np.repeat(np.arange(b, dtype=np.int32), prompt_len)).to(dev)
     slot = torch.full((T,), adapter_slot, dtype=torch.int32, device=dev)
     last = torch.from_numpy((np.arange(b) + 1) * prompt_len - 1).to(dev)
-    return _time_ms(lambda: model.forward(toks, pos, seq, slot, last))
+    segs = [(i * prompt_len, prompt_len, i, 0) for i in range(b)]
+    return _time_ms(lambda: model.forward(toks, pos, seq, slot, last, segments=segs))
 
 
 def measure_decode_ms(model, adapter_slot: int, b: int, ctx: int) -> float:

@@ -346,7 +346,19 @@ class MultiLoraModel:
         ops.lora_expand(y, v_all, self.pool.rank, self.pool.scale, self.pool.max_rank,
                         ops.make_targets(specs), offs, self.lora_ws)
 
-    def forward(self, tokens, pos, seq, slot, logit_rows=None, decode: bool = False) -> torch.Tensor:
+    @staticmethod
+    def segments_of(pos, seq) -> list:
+        """Host (tok0, n, seq, pos0) runs of consecutive positions of one sequence."""
+        pos, seq = np.asarray(pos), np.asarray(seq)
+        out, start = [], 0
+        for i in range(1, len(pos) + 1):
+            if i == len(pos) or seq[i] != seq[start] or pos[i] != pos[i - 1] + 1:
+                out.append((start, i - start, int(seq[start]), int(pos[start])))
+                start = i
+        return out
+
+    def forward(self, tokens, pos, seq, slot, logit_rows=None, decode: bool = False,
+                segments=None) -> torch.Tensor:
         """Token-major mixed batch.  tokens/pos/seq/slot: device int32 [T].
         ``decode``: every token is the next position of its own sequence, so RoPE, the KV
         append and attention run as one fused kernel per layer.
@@ -370,6 +382,10 @@ class MultiLoraModel:
                      if "w_qkv" in self.stack else None)
             v_o = (torch.empty((T, self._extra_rows("wo")), dtype=torch.float32, device=dev)
                    if "wo" in self.stack else None)
+        flash = (segments is not None and not decode and dt == torch.bfloat16
+                 and cfg.head_dim == 128)
+        if flash:
+            tiles = ops.prefill_tiles(segments, dev)
         ops.embedding(x, w["embed"], tokens)
         if self.targets:
             ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
@@ -389,8 +405,12 @@ class MultiLoraModel:
             else:
                 ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
                                   self.sin, self.k_cache[l], self.v_cache[l])
-                ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
-                              self.k_cache[l], self.v_cache[l])
+                if flash:
+                    ops.attention_prefill(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, tiles,
+                                          self.k_cache[l], self.v_cache[l])
+                else:
+                    ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
+                                  self.k_cache[l], self.v_cache[l])
             if stacked and "wo" in self.stack:
                 ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o)
                 self._expand(x, v_o, l, "wo", {"o": (0, d, d)})
@@ -432,7 +452,8 @@ class MultiLoraModel:
         dev = self.device
         i32 = lambda v: torch.tensor(v, dtype=torch.int32, device=dev)  # noqa: E731
         logits = self.forward(i32(toks), i32(pos), i32(sq), i32(sl),
-                              torch.tensor(last, dtype=torch.int64, device=dev))
+                              torch.tensor(last, dtype=torch.int64, device=dev),
+                              segments=self.segments_of(pos, sq))
         return seqs, logits
 
     def decode(self, seqs, tokens, adapter_slots) -> torch.Tensor:

@@ -329,6 +329,25 @@ def rope_attention_decode(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq,
     return out
 
 
+def prefill_tiles(segments, device, bq: int = 64) -> torch.Tensor:
+    """[(tok0, n, seq, pos0)] segments -> int32 [n_tiles, 4] tile table of <= bq queries."""
+    rows = []
+    for tok0, n, seq, pos0 in segments:
+        for q in range(0, n, bq):
+            rows.append((tok0 + q, min(bq, n - q), seq, pos0 + q))
+    return torch.tensor(rows, dtype=torch.int32).reshape(-1, 4).to(device)
+
+
+@_op("attention", 1)
+def attention_prefill(out, qkv, heads, kv_heads, head_dim, tiles, k_cache, v_cache):
+    """Tensor-core causal flash attention for prefill segments (tiles from prefill_tiles)."""
+    check(_lib.load().slx_attention_prefill(_ptr(out), _ld(out), _ptr(qkv), _ld(qkv), heads,
+                                            kv_heads, head_dim, _ptr(tiles), tiles.shape[0],
+                                            _ptr(k_cache), _ptr(v_cache), k_cache.shape[2],
+                                            _stream()), "slx_attention_prefill")
+    return out
+
+
 @_op("silu_mul", 1)
 def silu_mul_blocked(out, gu, ffn: int):
     check(_lib.load().slx_silu_mul_blocked(_dt(out), _ptr(out), _ld(out), _ptr(gu), _ld(gu),

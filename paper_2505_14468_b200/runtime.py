@@ -62,7 +62,8 @@ class ServingRuntime:
             batch = build_prefill(flushed, self.m.seq_len)
             logits = self.m.forward(self._i32(batch.tokens), self._i32(batch.pos),
                                     self._i32(batch.seq), self._i32(batch.slot),
-                                    torch.from_numpy(batch.logit_rows).to(self.m.device))
+                                    torch.from_numpy(batch.logit_rows).to(self.m.device),
+                                    segments=self.m.segments_of(batch.pos, batch.seq))
             for r in batch.requests:
                 self.m.seq_len[r.seq] += len(r.prompt)
             nxt = self.m.argmax(logits).cpu().tolist()

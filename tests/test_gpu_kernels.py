@@ -307,3 +307,33 @@ def test_gemm_lora_side_output(M):
     ops.gemm(a, pw, x, epilogue=EPI_RESIDUAL, residual=x, side=side)
     torch.testing.assert_close(x.float(), ref_main, rtol=1e-2, atol=2e-2)
     torch.testing.assert_close(side, a.float() @ ext.float().T, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("H,Hkv", [(4, 4), (8, 2)])
+@pytest.mark.parametrize("segs", [[(0, 1, 0, 0)], [(0, 70, 0, 0), (70, 64, 1, 0), (134, 5, 2, 30)],
+                                  [(0, 200, 0, 100), (200, 129, 1, 0)]])
+def test_flash_prefill_matches_oracle(H, Hkv, segs):
+    """Tensor-core prefill attention over ragged segments with cached prefixes (pos0 > 0)."""
+    D, max_ctx = 128, 320
+    rng = np.random.default_rng(H + len(segs))
+    T = sum(n for _, n, _, _ in segs)
+    n_seq = max(s for _, _, s, _ in segs) + 1
+    kc = torch.from_numpy(rng.standard_normal((n_seq, Hkv, max_ctx, D)).astype(np.float32)).to(DEV, torch.bfloat16)
+    vc = torch.from_numpy(rng.standard_normal((n_seq, Hkv, max_ctx, D)).astype(np.float32)).to(DEV, torch.bfloat16)
+    qkv = torch.from_numpy(rng.standard_normal((T, (H + 2 * Hkv) * D)).astype(np.float32)).to(DEV, torch.bfloat16)
+    out = torch.empty(T, H * D, dtype=torch.bfloat16, device=DEV)
+    tiles = ops.prefill_tiles(segs, DEV)
+    ops.attention_prefill(out, qkv, H, Hkv, D, tiles, kc, vc)
+    # generic attention kernel over the same (already rotated) q and pool
+    pos = np.concatenate([np.arange(p0, p0 + n) for _, n, _, p0 in segs]).astype(np.int32)
+    seq = np.concatenate([[s] * n for _, n, s, _ in segs]).astype(np.int32)
+    ref_k = torch.empty_like(out)
+    ops.attention(ref_k, qkv, H, Hkv, D, torch.from_numpy(pos).to(DEV), torch.from_numpy(seq).to(DEV), kc, vc)
+    torch.testing.assert_close(out.float(), ref_k.float(), rtol=2e-2, atol=2e-2)
+    q = qkv.float().cpu().numpy()[:, :H * D].reshape(T, H, D)
+    kk, vv = kc.float().cpu().numpy(), vc.float().cpu().numpy()
+    for tok0, n, s_, p0 in segs:
+        ref = orc.attention(q[tok0:tok0 + n], kk[s_].transpose(1, 0, 2)[:p0 + n],
+                            vv[s_].transpose(1, 0, 2)[:p0 + n], np.arange(p0, p0 + n))
+        np.testing.assert_allclose(out[tok0:tok0 + n].float().cpu().numpy(), ref.reshape(n, -1),
+                                   rtol=3e-2, atol=3e-2)

@@ -34,11 +34,11 @@ def timeit(fn, iters=15):
 
 def main():
     M = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-    shapes = [("qkv", 12288, 4096, EPI_NONE), ("o", 4096, 4096, EPI_RESIDUAL),
+    shapes = [("qkv", 13824, 4096, EPI_NONE), ("o", 4608, 4096, EPI_RESIDUAL),
               ("gate_up", 22016, 4096, EPI_SILU_MUL), ("down", 4096, 11008, EPI_RESIDUAL),
               ("lm_head", 32000, 4096, EPI_NONE)]
     best = {}
-    for k in ("SLX_GEMM_CTAS", "SLX_GEMM_SPLITS"):
+    for k in ("SLX_GEMM_CTAS", "SLX_GEMM_SPLITS", "SLX_GEMM_BN"):
         os.environ.pop(k, None)
     for name, N, K, epi in shapes:   # planner's own choice first
         a = torch.randn(M, K, device=DEV).to(torch.bfloat16)
@@ -56,9 +56,11 @@ def main():
         r = torch.randn(M, N, device=DEV).to(torch.bfloat16) if epi == EPI_RESIDUAL else None
         ref = None
         byts = N * K * 2
-        for ctas, splits in itertools.product([1, 2], [1, 2, 3, 4, 5, 6, 8]):
-            nsub = 0
-            os.environ.update(SLX_GEMM_CTAS=str(ctas), SLX_GEMM_SPLITS=str(splits))
+        for bn, ctas, splits in itertools.product([256, 128], [1, 2], [1, 2, 3, 4, 5, 6, 8]):
+            if epi == EPI_SILU_MUL and bn == 128:
+                continue
+            os.environ.update(SLX_GEMM_CTAS=str(ctas), SLX_GEMM_SPLITS=str(splits),
+                              SLX_GEMM_BN=str(bn))
             try:
                 ms = timeit(lambda: ops.gemm(a, w, c, epilogue=epi, residual=r))
             except Exception as e:  # noqa: BLE001
@@ -70,7 +72,7 @@ def main():
                 ref = out.clone()
             ok = torch.allclose(out, ref, rtol=2e-2, atol=2e-2)
             gbs = byts / ms / 1e6
-            rec = {"gemm": name, "ctas": ctas, "splits": splits,
+            rec = {"gemm": name, "bn": bn, "ctas": ctas, "splits": splits,
                    "us": round(ms * 1000, 2), "GB/s": round(gbs, 1), "ok": ok}
             print(json.dumps(rec), flush=True)
             if ok and (name not in best or gbs > best[name]["GB/s"]):
