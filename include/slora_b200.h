@@ -85,6 +85,17 @@ SLX_API size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 SLX_API int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
                   int n_main, void* C2, int ldc2, void* stream);
+/* Grouped GEMM (SGMV on tcgen05): CTA tile i = gtiles[i] = {group, m0, m_rows, n0} computes
+ * C[m0:m0+m_rows, n0:n0+256] = alpha[group] * A[m0.., :K] . W_group[n0.., :]^T (+ R), where
+ * W_group is row-major [w_rows, w_cols] (row stride w_ld) and columns >= w_cols read as 0.
+ * Up to 16 groups per call; host arrays w_ptrs/w_rows/w_cols/w_ld/alpha; gtiles on device
+ * (slx_gemm_group_tile_bytes() each).  Prefill LoRA: shrink with W = A_adapter (alpha =
+ * scale), expand with A = v and W = B_adapter (residual in place). */
+SLX_API size_t slx_gemm_group_tile_bytes(void);
+SLX_API int slx_gemm_grouped_bf16(const void* A, int lda, int M, int K, int n_groups,
+                  const uint64_t* w_ptrs, const int* w_rows, const int* w_cols, const int* w_ld,
+                  const float* alpha, void* C, int ldc, int c_dtype, const void* R, int ldr, int N,
+                  int epilogue, const void* gtiles, int n_gtiles, void* stream);
 /* Pack a row-major bf16 W[N, K] (row stride ld) into the SLX_W_TILED layout (device kernel).
  * dst must hold slx_packed_weight_elems(N, K) elements. */
 SLX_API size_t slx_packed_weight_elems(int N, int K);

@@ -48,6 +48,9 @@ SIGNATURES = {
     "slx_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "slx_gemm_bf16": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),
+    "slx_gemm_group_tile_bytes": (_sz, []),
+    "slx_gemm_grouped_bf16": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p, _i, _i,
+                                   _i, _p, _i, _p]),
     "slx_lora_expand": (_i, [_i, _p, _i, _p, _i, _i, _p, _p, _i, _i, _i,
                              ctypes.POINTER(LoraTarget), ctypes.POINTER(_i), _p, _sz, _p]),
     "slx_packed_weight_elems": (_sz, [_i, _i]),

@@ -38,6 +38,17 @@ constexpr int TC_MAX_STAGES = 8;
 constexpr int W_BLOCK_BYTES = 128 * TC_BK * 2;   // 16 KB: one 128-row weight box
 constexpr int TC_MAX_CLUSTER = 8;
 
+// Grouped mode (SGMV on the tensor cores): CTA x-index -> one GroupTile; each group (adapter
+// segment) has its own row-major W tensor map and alpha (the LoRA scale).
+constexpr int TC_MAX_GROUPS = 16;
+struct GroupTile {
+  int group, m0, m_rows, n0;
+};
+struct GroupMaps {
+  CUtensorMap w[TC_MAX_GROUPS];
+  float alpha[TC_MAX_GROUPS];
+};
+
 struct GemmArgs {
   int M, N, K;
   int bm;        // activation rows per tile actually loaded (<= 128, multiple of 16)
@@ -53,6 +64,7 @@ struct GemmArgs {
   int n_main;    // columns >= n_main go to the fp32 side output C2 (LoRA shrink rows)
   float* C2;
   int ldc2;
+  const GroupTile* gtiles;   // grouped mode only
 };
 
 template <typename OutT>
@@ -78,7 +90,11 @@ __device__ __forceinline__ void store16(OutT* row, int n0, int n_lim, const floa
 // columns (n >= n_main, LoRA shrink rows appended to W) go to the fp32 side output C2.
 template <int EPI, typename OutT>
 __device__ __forceinline__ void store_cols(const GemmArgs& g, OutT* C, const OutT* R, int m, int n,
-                                           int n_out, float* v) {
+                                           int n_out, float* v, float alpha = 1.f) {
+  if (alpha != 1.f) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] *= alpha;
+  }
   if (g.C2 != nullptr && n >= g.n_main) {
     float* row = g.C2 + (size_t)m * g.ldc2 + (n - g.n_main);
     if (n + 16 <= g.N) {
@@ -112,10 +128,10 @@ __device__ __forceinline__ void w_coord(const GemmArgs& g, int row0, int kb, int
   }
 }
 
-template <int EPI, typename OutT, int TC_BN>
+template <int EPI, typename OutT, int TC_BN, bool GROUPED>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-               GemmArgs g) {
+               GemmArgs g, const __grid_constant__ GroupMaps gm) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int x_bytes = g.bm * TC_BK * 2;
@@ -134,12 +150,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   const int kb_lo = split * kb_per;
   const int kb_hi = min(g.kblocks, kb_lo + kb_per);
   const int n_kb = max(0, kb_hi - kb_lo);
-  const int m0 = blockIdx.y * 128;
-  const int n0 = tile * TC_BN;
+  // grouped mode: the tile table comes from the host stream; read it after the PDL wait
+  if (GROUPED) pdl_wait();
+  const GroupTile gt = GROUPED ? g.gtiles[blockIdx.x] : GroupTile{0, 0, 0, 0};
+  const int m0 = GROUPED ? gt.m0 : blockIdx.y * 128;
+  const int n0 = GROUPED ? gt.n0 : tile * TC_BN;
+  const int m_lim = GROUPED ? gt.m0 + gt.m_rows : g.M;
+  const float alpha = GROUPED ? gm.alpha[gt.group] : 1.f;
+  const CUtensorMap* wmap = GROUPED ? &gm.w[gt.group] : &tmap_w;
 
   if (threadIdx.x == 0) {
     tc::tma_prefetch_desc(&tmap_x);
-    tc::tma_prefetch_desc(&tmap_w);
+    tc::tma_prefetch_desc(wmap);
     for (int s = 0; s < g.stages; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -165,7 +187,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       for (int b = 0; b < WB; ++b) {
         int c0, c1;
         w_coord(g, n0 + b * 128, kb, c0, c1);
-        tc::tma_load_2d(st + x_bytes + b * W_BLOCK_BYTES, &tmap_w, bar, c0, c1, pol_w);
+        tc::tma_load_2d(st + x_bytes + b * W_BLOCK_BYTES, wmap, bar, c0, c1, pol_w);
       }
     };
     const int npre = min(n_kb, g.stages);
@@ -212,7 +234,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   tc::fence_after_sync();
   const int r = warp * 32 + lane;
   const int m = m0 + r;
-  const bool warp_live = m0 + warp * 32 < g.M && warp * 32 < g.bm;   // warp-uniform
+  const bool warp_live = m0 + warp * 32 < m_lim && warp * 32 < g.bm;   // warp-uniform
   const uint32_t t_row = tmem_base + ((uint32_t)(warp * 32) << 16);
   OutT* C = reinterpret_cast<OutT*>(g.C);
   const OutT* R = reinterpret_cast<const OutT*>(g.R);
@@ -225,7 +247,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
           float gv[16], uv[16];
           tc::tmem_ld16(t_row + c0, gv);
           tc::tmem_ld16(t_row + TC_BN / 2 + c0, uv);
-          if (m < g.M) {
+          if (m < m_lim) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) gv[j] = silu_f(gv[j]) * uv[j];
             store16(C + (size_t)m * g.ldc, tile * (TC_BN / 2) + c0, n_out, gv);
@@ -236,7 +258,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
           float v[16];
           tc::tmem_ld16(t_row + c0, v);
           const int n = n0 + c0;
-          if (m < g.M) store_cols<EPI>(g, C, R, m, n, n_out, v);
+          if (m < m_lim) store_cols<EPI>(g, C, R, m, n, n_out, v, alpha);
         }
       }
     }
@@ -283,7 +305,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
         }
       }
     };
-    if (warp_live && m < g.M && r < g.bm) {
+    if (warp_live && m < m_lim && r < g.bm) {
       for (int f0 = f_lo; f0 < f_hi; f0 += 16) {
         float v[16];
         reduce16(f0, v);
@@ -367,7 +389,7 @@ static int max_active_clusters(size_t smem, int cluster) {
   static int n_cache = 0;
   for (int i = 0; i < n_cache; ++i)
     if (cache[i].smem == smem && cache[i].cluster == cluster) return cache[i].value;
-  auto k = gemm_tc_kernel<SLX_EPI_NONE, bf16, 256>;
+  auto k = gemm_tc_kernel<SLX_EPI_NONE, bf16, 256, false>;
   configure_kernel((const void*)k);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)cluster * 64);
@@ -448,16 +470,22 @@ static GemmPlan plan_gemm(int M, int N, int K, bool silu) {
   return p;
 }
 
-template <int EPI, typename OutT, int BN>
+static const GroupMaps& no_groups() {
+  static GroupMaps gm{};
+  return gm;
+}
+
+template <int EPI, typename OutT, int BN, bool GROUPED = false>
 static int launch_tc(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& a, dim3 grid,
-                     size_t smem, unsigned cluster, cudaStream_t s) {
-  auto k = gemm_tc_kernel<EPI, OutT, BN>;
+                     size_t smem, unsigned cluster, cudaStream_t s,
+                     const GroupMaps& gm = no_groups()) {
+  auto k = gemm_tc_kernel<EPI, OutT, BN, GROUPED>;
   static bool configured = false;  // per instantiation
   if (!configured) {
     configure_kernel((const void*)k);
     configured = true;
   }
-  return launch_ex(k, grid, dim3(TC_THREADS), smem, s, cluster, mx, mw, a);
+  return launch_ex(k, grid, dim3(TC_THREADS), smem, s, cluster, mx, mw, a, gm);
 }
 
 template <typename OutT, int BN>
@@ -603,4 +631,52 @@ extern "C" int slx_pack_weight_rows(void* dst, const void* src, int n_rows, int 
   const size_t total = (size_t)n_rows * kb * 8;
   return launch_ex(pack_rows_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0,
                    (cudaStream_t)stream, 1u, (bf16*)dst, (const bf16*)src, n_rows, K, ld, row0, kb);
+}
+
+// ------------------------------------------------------------------ grouped GEMM (SGMV)
+extern "C" size_t slx_gemm_group_tile_bytes(void) { return sizeof(GroupTile); }
+
+extern "C" int slx_gemm_grouped_bf16(const void* A, int lda, int M, int K, int n_groups,
+                                     const uint64_t* w_ptrs, const int* w_rows, const int* w_cols,
+                                     const int* w_ld, const float* alpha, void* C, int ldc, int c_dtype,
+                                     const void* R, int ldr, int N, int epilogue,
+                                     const void* gtiles, int n_gtiles, void* stream) {
+  SLX_CHECK_ARG(A && C && w_ptrs && w_rows && w_cols && w_ld && alpha && gtiles && M > 0 && K > 0 &&
+                K % 8 == 0 && lda >= K && lda % 8 == 0 && ldc % 8 == 0 && N > 0 &&
+                n_groups >= 1 && n_groups <= TC_MAX_GROUPS && n_gtiles >= 0);
+  SLX_CHECK_ARG(epilogue == SLX_EPI_NONE || epilogue == SLX_EPI_RESIDUAL);
+  SLX_CHECK_ARG(c_dtype == SLX_DT_BF16 || c_dtype == SLX_DT_F32);
+  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr % 8 == 0);
+  SLX_CHECK_ALIGN(A, 16);
+  SLX_CHECK_ALIGN(C, 16);
+  if (n_gtiles == 0) return SLX_OK;
+  GroupMaps gm{};
+  for (int i = 0; i < n_groups; ++i) {
+    // per-group K extent: columns >= w_cols[i] (e.g. beyond an adapter's rank) read as zeros
+    SLX_CHECK_ARG(w_ptrs[i] != 0 && w_rows[i] > 0 && w_cols[i] > 0 && w_cols[i] <= K &&
+                  w_ld[i] >= w_cols[i] && w_ld[i] % 8 == 0);
+    if (!make_tmap(&gm.w[i], (const void*)w_ptrs[i], w_rows[i], w_cols[i], w_ld[i], 128))
+      return SLX_ERR_CUDA;
+    gm.alpha[i] = alpha[i];
+  }
+  GemmArgs a{};
+  a.M = M; a.N = N; a.K = K;
+  a.bm = 128; a.kblocks = ceil_div(K, TC_BK); a.splits = 1; a.n_tiles = 1;
+  const size_t stage = (size_t)128 * TC_BK * 2 + 2 * W_BLOCK_BYTES;
+  a.stages = a.kblocks < 4 ? (a.kblocks < 2 ? 2 : a.kblocks) : 4;
+  const size_t smem = (size_t)a.stages * stage + BAR_BYTES + 1024;
+  a.C = C; a.ldc = ldc; a.R = R; a.ldr = ldr; a.w_tiled = 0; a.n_main = N;
+  a.gtiles = (const GroupTile*)gtiles;
+  CUtensorMap mx;
+  if (!make_tmap(&mx, A, M, K, lda, 128)) return SLX_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((unsigned)n_gtiles, 1);
+  if (c_dtype == SLX_DT_BF16) {
+    if (epilogue == SLX_EPI_NONE)
+      return launch_tc<SLX_EPI_NONE, bf16, 256, true>(mx, mx, a, grid, smem, 1u, s, gm);
+    return launch_tc<SLX_EPI_RESIDUAL, bf16, 256, true>(mx, mx, a, grid, smem, 1u, s, gm);
+  }
+  if (epilogue == SLX_EPI_NONE)
+    return launch_tc<SLX_EPI_NONE, float, 256, true>(mx, mx, a, grid, smem, 1u, s, gm);
+  return launch_tc<SLX_EPI_RESIDUAL, float, 256, true>(mx, mx, a, grid, smem, 1u, s, gm);
 }

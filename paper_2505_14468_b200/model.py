@@ -182,6 +182,7 @@ class MultiLoraModel:
             if "o" in self.targets:
                 self.stack["wo"] = ("o",)
         self.use_stacked_decode = bool(self.stack)
+        self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
         self.pool.on_install = self._stack_install
         self.pool.on_evict = self._stack_evict
 
@@ -335,6 +336,66 @@ class MultiLoraModel:
         ops.lora_apply(y, x, d_in if d_in is not None else x.shape[1], self.pool.rank,
                        self.pool.scale, self.pool.max_rank, ops.make_targets(specs), self.lora_ws)
 
+    def _sgmv_plan(self, segments, slot_host):
+        """Grouped-GEMM tile tables for the prefill LoRA (SGMV on tcgen05): adapter groups of
+        the batch (<= 16 per launch) and, per launch, shrink tiles and expand tiles per d_out."""
+        by_slot: dict = {}
+        for tok0, n, _seq, _p0 in segments:
+            a = int(slot_host[tok0])
+            if a >= 0 and self.pool.configs[a] is not None:
+                by_slot.setdefault(a, []).append((tok0, n))
+        slots = sorted(by_slot)
+        launches = []
+        for c in range(0, len(slots), ops.GROUP_MAX):
+            chunk = slots[c:c + ops.GROUP_MAX]
+            shrink, expand = [], {}
+            for gi, a in enumerate(chunk):
+                for tok0, n in by_slot[a]:
+                    for m0 in range(tok0, tok0 + n, 128):
+                        shrink.append((gi, m0, min(128, tok0 + n - m0), 0))
+            launches.append((chunk, shrink, by_slot))
+        return launches
+
+    def _sgmv_tc(self, y, x, layer: int, names, cols, plan, v_buf) -> bool:
+        """Prefill LoRA for contiguous targets via two grouped tcgen05 GEMMs per target:
+        v = scale * x A^T (shrink, bf16 [T, 64]) then y[:, off:] += v B^T (expand)."""
+        idx = [i for i, t in enumerate(self.targets) if t in names]
+        if not idx:
+            return True
+        R = 64
+        for i in idx:
+            t = self.targets[i]
+            off, blk, _stride = cols[t]
+            di, do = self.cfg.target_dims(t)
+            if blk != do or self.pool.max_rank > R:
+                return False
+        for chunk, shrink, by_slot in plan:
+            sh_tiles = torch.tensor(shrink, dtype=torch.int32).reshape(-1, 4).to(self.device)
+            for i in idx:
+                t = self.targets[i]
+                off, _blk, _stride = cols[t]
+                di, do = self.cfg.target_dims(t)
+                ga, gb = [], []
+                for a in chunk:
+                    lo = self.pool.configs[a]
+                    layout, _ = self.pool.blob_layout(lo.rank)
+                    base = self.pool.blobs[a].data_ptr()
+                    ent = next(e for e in layout if e[0] == layer and e[1] == t)
+                    _l, _t, ao, bo, _di, _do = ent
+                    ga.append((base + 2 * ao, lo.rank, di, di, lo.scale))
+                    gb.append((base + 2 * bo, do, lo.rank, lo.rank, 1.0))
+                ex = []
+                for gi, a in enumerate(chunk):
+                    for tok0, n in by_slot[a]:
+                        for m0 in range(tok0, tok0 + n, 128):
+                            for n0 in range(0, do, 256):
+                                ex.append((gi, m0, min(128, tok0 + n - m0), n0))
+                ex_tiles = torch.tensor(ex, dtype=torch.int32).reshape(-1, 4).to(self.device)
+                ops.gemm_grouped(x, di, ga, sh_tiles, v_buf, R)
+                yv = y[:, off:off + do]
+                ops.gemm_grouped(v_buf, R, gb, ex_tiles, yv, do, residual=yv)
+        return True
+
     def _expand(self, y, v_all, layer: int, proj: str, cols) -> None:
         specs, offs = [], []
         for t in self.stack[proj]:
@@ -386,6 +447,11 @@ class MultiLoraModel:
                  and cfg.head_dim == 128)
         if flash:
             tiles = ops.prefill_tiles(segments, dev)
+        sgmv_plan = None
+        if (segments is not None and not decode and dt == torch.bfloat16 and self.targets
+                and self.use_tc_sgmv and not (self.use_stacked_decode and T <= 128)):
+            sgmv_plan = self._sgmv_plan(segments, slot.cpu().numpy())
+            v_buf = torch.empty((T, 64), dtype=dt, device=dev)
         ops.embedding(x, w["embed"], tokens)
         if self.targets:
             ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
@@ -398,7 +464,9 @@ class MultiLoraModel:
                 self._expand(qkv, v_qkv, l, "w_qkv", qkv_cols)
             else:
                 self._gemm(h, w[p + "w_qkv"], qkv)
-                self._lora(qkv, h, l, ("q", "k", "v"), qkv_cols)
+                if not (sgmv_plan is not None and
+                        self._sgmv_tc(qkv, h, l, ("q", "k", "v"), qkv_cols, sgmv_plan, v_buf)):
+                    self._lora(qkv, h, l, ("q", "k", "v"), qkv_cols)
             if decode:
                 ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos,
                                           seq, self.cos, self.sin, self.k_cache[l], self.v_cache[l])
@@ -416,7 +484,9 @@ class MultiLoraModel:
                 self._expand(x, v_o, l, "wo", {"o": (0, d, d)})
             else:
                 self._gemm(attn, w[p + "wo"], x, residual=x)
-                self._lora(x, attn, l, ("o",), {"o": (0, d, d)})
+                if not (sgmv_plan is not None and
+                        self._sgmv_tc(x, attn, l, ("o",), {"o": (0, d, d)}, sgmv_plan, v_buf)):
+                    self._lora(x, attn, l, ("o",), {"o": (0, d, d)})
             ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
             if fused_silu:
                 self._gemm(h, w[p + "w_gu"], mlp, silu=True)

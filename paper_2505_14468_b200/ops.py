@@ -284,6 +284,28 @@ def lora_expand(y: torch.Tensor, v_all: torch.Tensor, slot_rank, slot_scale, max
           "slx_lora_expand")
 
 
+GROUP_MAX = 16
+
+
+@_op("lora", 1)
+def gemm_grouped(a: torch.Tensor, k: int, groups, gtiles: torch.Tensor, out: torch.Tensor, n: int,
+                 residual: torch.Tensor | None = None) -> torch.Tensor:
+    """Grouped tcgen05 GEMM.  groups: [(w_ptr, w_rows, w_cols, w_ld, alpha)] (<= 16);
+    gtiles: device int32 [n_tiles, 4] of (group, m0, m_rows, n0)."""
+    g = list(groups)
+    if not 1 <= len(g) <= GROUP_MAX:
+        raise ValueError("gemm_grouped: 1..16 groups per call")
+    arr = lambda t, vals: (t * len(vals))(*vals)  # noqa: E731
+    epi = EPI_RESIDUAL if residual is not None else EPI_NONE
+    check(_lib.load().slx_gemm_grouped_bf16(
+        _ptr(a), _ld(a), a.shape[0], k, len(g), arr(ctypes.c_uint64, [x[0] for x in g]),
+        arr(ctypes.c_int, [x[1] for x in g]), arr(ctypes.c_int, [x[2] for x in g]),
+        arr(ctypes.c_int, [x[3] for x in g]), arr(ctypes.c_float, [x[4] for x in g]),
+        _ptr(out), _ld(out), _dt(out), _ptr(residual), _ld(residual) if residual is not None else 0,
+        n, epi, _ptr(gtiles), gtiles.shape[0], _stream()), "slx_gemm_grouped_bf16")
+    return out
+
+
 # ---------------------------------------------------------------------------------- K4
 @_op("embedding", 1)
 def embedding(out, table, tokens):

@@ -141,3 +141,31 @@ def test_bf16_stacked_decode_shrink_matches_sgmv_path(golden):
         m.seq_len[s_] = len(prompts[seqs.index(s_)])
     ev2 = m.decode(seqs, toks, [0, 1, 3, 2]).cpu().numpy()   # slot 1 evicted: rank 0
     np.testing.assert_allclose(ev[1], ev2[1], rtol=1e-2, atol=1e-2)
+
+
+def test_bf16_prefill_tc_path_matches_oracle():
+    """Prefill with the tensor-core paths (flash attention, SGMV as grouped tcgen05 GEMMs) on a
+    head_dim-128 GQA model with mixed adapter ranks {8,16,64} == SIMT paths == oracle."""
+    from paper_2505_14468_b200.config import BackboneConfig
+    cfg = BackboneConfig("small128", hidden=512, layers=2, heads=4, kv_heads=2, head_dim=128,
+                         ffn=1024, vocab=1000)
+    w = init_backbone(cfg, 3)
+    loras = [LoraConfig(8, 16.0), LoraConfig(64, 32.0), LoraConfig(16, 16.0)]
+    ads = [init_adapter(cfg, lo, 3, a) for a, lo in enumerate(loras)]
+    rng = np.random.default_rng(5)
+    prompts = [list(map(int, rng.integers(1, cfg.vocab, size=L))) for L in (300, 7, 129, 64, 1)]
+    ids = [1, 0, 2, 1, -1]
+    out = {}
+    for tc in (True, False):
+        m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=8, max_ctx=512, n_slots=4,
+                           max_rank=64, max_tokens=1024)
+        m.use_tc_sgmv = tc
+        m.load_backbone(w)
+        for a, (ad, lo) in enumerate(zip(ads, loras)):
+            m.pool.load(a, ad, lo)
+        _, lg = m.prefill(prompts, ids)
+        out[tc] = lg.cpu().numpy()
+    np.testing.assert_allclose(out[True], out[False], rtol=2e-2, atol=2e-2)
+    orc = OracleModel(cfg, w, ads, [lo.scale for lo in loras], loras[0].targets)
+    ref = orc.prefill(prompts, ids)
+    np.testing.assert_allclose(out[True], ref, rtol=BF16_RTOL, atol=BF16_ATOL)
