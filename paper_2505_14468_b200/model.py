@@ -64,6 +64,7 @@ class AdapterPool:
         self.scale = torch.zeros(n_slots, dtype=torch.float32, device=self.device)
         self.blobs: list[torch.Tensor | None] = [None] * n_slots
         self.configs: list[LoraConfig | None] = [None] * n_slots
+        self._off_cache: dict = {}
         self.on_install = None   # model hooks (stacked-A rows of the projection GEMMs)
         self.on_evict = None
 
@@ -76,6 +77,15 @@ class AdapterPool:
                 out.append((l, t, off, off + rank * di, di, do))
                 off += rank * (di + do)
         return out, off
+
+    def offsets(self, rank: int, layer: int, target: str) -> tuple[int, int]:
+        """Element offsets of A and B of (layer, target) inside a rank-``rank`` blob."""
+        key = (rank, layer, target)
+        if key not in self._off_cache:
+            layout, _ = self.blob_layout(rank)
+            for l, t, ao, bo, _di, _do in layout:
+                self._off_cache[(rank, l, t)] = (ao, bo)
+        return self._off_cache[key]
 
     def pack(self, weights: dict, rank: int) -> torch.Tensor:
         """Host-side packing of an adapter dict (``layers.{l}.{t}.A/B``) into a blob (CPU bf16)."""
@@ -337,23 +347,29 @@ class MultiLoraModel:
                        self.pool.scale, self.pool.max_rank, ops.make_targets(specs), self.lora_ws)
 
     def _sgmv_plan(self, segments, slot_host):
-        """Grouped-GEMM tile tables for the prefill LoRA (SGMV on tcgen05): adapter groups of
-        the batch (<= 16 per launch) and, per launch, shrink tiles and expand tiles per d_out."""
+        """Grouped-GEMM tile tables for the prefill LoRA (SGMV on tcgen05), built once per
+        forward: per launch (<= 16 adapter groups) the shrink tiles and, per distinct d_out,
+        the expand tiles, uploaded to the device in one copy each."""
         by_slot: dict = {}
         for tok0, n, _seq, _p0 in segments:
             a = int(slot_host[tok0])
             if a >= 0 and self.pool.configs[a] is not None:
                 by_slot.setdefault(a, []).append((tok0, n))
         slots = sorted(by_slot)
+        douts = sorted({self.cfg.target_dims(t)[1] for t in self.targets})
         launches = []
         for c in range(0, len(slots), ops.GROUP_MAX):
             chunk = slots[c:c + ops.GROUP_MAX]
-            shrink, expand = [], {}
+            shrink, expand = [], {do: [] for do in douts}
             for gi, a in enumerate(chunk):
                 for tok0, n in by_slot[a]:
                     for m0 in range(tok0, tok0 + n, 128):
-                        shrink.append((gi, m0, min(128, tok0 + n - m0), 0))
-            launches.append((chunk, shrink, by_slot))
+                        mr = min(128, tok0 + n - m0)
+                        shrink.append((gi, m0, mr, 0))
+                        for do in douts:
+                            expand[do] += [(gi, m0, mr, n0) for n0 in range(0, do, 256)]
+            dev = lambda rows: torch.tensor(rows, dtype=torch.int32).reshape(-1, 4).to(self.device)  # noqa: E731
+            launches.append((chunk, dev(shrink), {do: dev(v) for do, v in expand.items()}))
         return launches
 
     def _sgmv_tc(self, y, x, layer: int, names, cols, plan, v_buf) -> bool:
@@ -365,12 +381,10 @@ class MultiLoraModel:
         R = 64
         for i in idx:
             t = self.targets[i]
-            off, blk, _stride = cols[t]
-            di, do = self.cfg.target_dims(t)
-            if blk != do or self.pool.max_rank > R:
+            _off, blk, _stride = cols[t]
+            if blk != self.cfg.target_dims(t)[1] or self.pool.max_rank > R:
                 return False
-        for chunk, shrink, by_slot in plan:
-            sh_tiles = torch.tensor(shrink, dtype=torch.int32).reshape(-1, 4).to(self.device)
+        for chunk, sh_tiles, ex_tiles in plan:
             for i in idx:
                 t = self.targets[i]
                 off, _blk, _stride = cols[t]
@@ -378,22 +392,13 @@ class MultiLoraModel:
                 ga, gb = [], []
                 for a in chunk:
                     lo = self.pool.configs[a]
-                    layout, _ = self.pool.blob_layout(lo.rank)
+                    ao, bo = self.pool.offsets(lo.rank, layer, t)
                     base = self.pool.blobs[a].data_ptr()
-                    ent = next(e for e in layout if e[0] == layer and e[1] == t)
-                    _l, _t, ao, bo, _di, _do = ent
                     ga.append((base + 2 * ao, lo.rank, di, di, lo.scale))
                     gb.append((base + 2 * bo, do, lo.rank, lo.rank, 1.0))
-                ex = []
-                for gi, a in enumerate(chunk):
-                    for tok0, n in by_slot[a]:
-                        for m0 in range(tok0, tok0 + n, 128):
-                            for n0 in range(0, do, 256):
-                                ex.append((gi, m0, min(128, tok0 + n - m0), n0))
-                ex_tiles = torch.tensor(ex, dtype=torch.int32).reshape(-1, 4).to(self.device)
                 ops.gemm_grouped(x, di, ga, sh_tiles, v_buf, R)
                 yv = y[:, off:off + do]
-                ops.gemm_grouped(v_buf, R, gb, ex_tiles, yv, do, residual=yv)
+                ops.gemm_grouped(v_buf, R, gb, ex_tiles[do], yv, do, residual=yv)
         return True
 
     def _expand(self, y, v_all, layer: int, proj: str, cols) -> None:
