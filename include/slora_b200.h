@@ -68,7 +68,7 @@ SLX_API int slx_device_sm_count(int* out);
  * engine.py:832 prefill_work_ms, engine.py:888,909 decode gap) for the q/k/v/o,
  * gate/up/down and lm_head projections.
  * C[M,N] = A[M,K] · W[N,K]^T (+ epilogue), bf16 in, fp32 accumulate in TMEM (tcgen05),
- * C dtype c_dtype (bf16 or fp32).  N % 16 == 0 (SiLU: N % 256 == 0), K % 8 == 0,
+ * C dtype c_dtype (bf16 or fp32).  Any N (SiLU: N % 256 == 0), K % 8 == 0,
  * lda/ldc/ldr % 8 == 0.  M <= 128 (decode) runs the swap-AB kernel whose K split is reduced
  * across a thread-block cluster in distributed shared memory (no workspace: the
  * workspace query returns 0 and is kept for ABI stability).

@@ -530,7 +530,7 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   if (epilogue == SLX_EPI_SILU_MUL) {
     SLX_CHECK_ARG(N % 256 == 0 && ldc >= N / 2);
   } else {
-    SLX_CHECK_ARG(N % 16 == 0 && (C2 != nullptr || ldc >= N));
+    SLX_CHECK_ARG(C2 != nullptr || ldc >= N);   // any N: the epilogue masks columns >= N
   }
   if (C2 != nullptr) {
     SLX_CHECK_ARG(epilogue != SLX_EPI_SILU_MUL && n_main > 0 && n_main < N && n_main % 16 == 0 &&
