@@ -69,9 +69,10 @@ SLX_API int slx_device_sm_count(int* out);
  * gate/up/down and lm_head projections.
  * C[M,N] = A[M,K] · W[N,K]^T (+ epilogue), bf16 in, fp32 accumulate in TMEM (tcgen05),
  * C dtype c_dtype (bf16 or fp32).  Any N (SiLU: N % 256 == 0), K % 8 == 0,
- * lda/ldc/ldr % 8 == 0.  M <= 128 (decode) runs the swap-AB kernel whose K split is reduced
- * across a thread-block cluster in distributed shared memory (no workspace: the
- * workspace query returns 0 and is kept for ABI stability).
+ * lda/ldc/ldr % 8 == 0.  For few output tiles (decode) the K range is split over CTAs and
+ * reduced either across a thread-block cluster in distributed shared memory or, when that
+ * covers more SMs, through fp32 partial tiles in `ws` (zero-initialised once, left zeroed;
+ * slx_gemm_workspace_bytes; pass NULL to disable).  Both reductions are deterministic.
  */
 enum {
   SLX_W_ROWMAJOR = 0, /* W[N, K] row-major (nn.Linear) */
@@ -84,7 +85,7 @@ SLX_API size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue);
  * residual; columns [0, n_main) go to C/R as usual (n_main % 16 == 0; not with SiLU). */
 SLX_API int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
-                  int n_main, void* C2, int ldc2, void* stream);
+                  int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes, void* stream);
 /* Grouped GEMM (SGMV on tcgen05): CTA tile i = gtiles[i] = {group, m0, m_rows, n0} computes
  * C[m0:m0+m_rows, n0:n0+256] = alpha[group] * A[m0.., :K] . W_group[n0.., :]^T (+ R), where
  * W_group is row-major [w_rows, w_cols] (row stride w_ld) and columns >= w_cols read as 0.

@@ -65,6 +65,9 @@ struct GemmArgs {
   float* C2;
   int ldc2;
   const GroupTile* gtiles;   // grouped mode only
+  int gsplit;                // split-K reduced through global partial tiles (no cluster)
+  float* ws_part;            // [tiles][S][bm][BN] fp32 partials
+  int* ws_cnt;               // [tiles] arrival counters (zero; self-cleaning)
 };
 
 template <typename OutT>
@@ -262,6 +265,65 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
         }
       }
     }
+  } else if (g.gsplit) {
+    // split-K through global memory (no cluster placement constraints): every split CTA
+    // writes its fp32 partial tile with 16-byte stores; the last to arrive (tile counter)
+    // sums the S partials in split order (deterministic) and runs the epilogue.
+    __shared__ int sh_last;
+    float* part = g.ws_part + (size_t)tile * S * g.bm * TC_BN;
+    if (warp_live) {
+      for (int c0 = 0; c0 < TC_BN; c0 += 16) {
+        float v[16];
+        tc::tmem_ld16(t_row + c0, v);
+        if (r < g.bm) {
+          float4* dst = reinterpret_cast<float4*>(part + ((size_t)split * g.bm + r) * TC_BN + c0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) sh_last = atomicAdd(&g.ws_cnt[tile], 1) == S - 1;
+    __syncthreads();
+    if (sh_last) {
+      __threadfence();
+      auto sum16 = [&](int col0, float* out) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) out[j] = 0.f;
+#pragma unroll
+        for (int sp = 0; sp < TC_MAX_CLUSTER; ++sp) {   // fixed order: deterministic
+          if (sp < S) {
+            const float4* src = reinterpret_cast<const float4*>(part + ((size_t)sp * g.bm + r) * TC_BN + col0);
+            float4 q[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) q[u] = __ldcg(src + u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              out[4 * u] += q[u].x; out[4 * u + 1] += q[u].y;
+              out[4 * u + 2] += q[u].z; out[4 * u + 3] += q[u].w;
+            }
+          }
+        }
+      };
+      const int feats = EPI == SLX_EPI_SILU_MUL ? TC_BN / 2 : TC_BN;
+      if (warp_live && m < m_lim && r < g.bm) {
+        for (int f0 = 0; f0 < feats; f0 += 16) {
+          float v[16];
+          sum16(f0, v);
+          if (EPI == SLX_EPI_SILU_MUL) {
+            float u[16];
+            sum16(f0 + TC_BN / 2, u);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = silu_f(v[j]) * u[j];
+            store16(C + (size_t)m * g.ldc, tile * (TC_BN / 2) + f0, n_out, v);
+          } else {
+            store_cols<EPI>(g, C, R, m, n0 + f0, n_out, v);
+          }
+        }
+      }
+      if (threadIdx.x == 0) g.ws_cnt[tile] = 0;   // ready for the next launch / graph replay
+    }
   } else {
     // split-K over the cluster: stage this CTA's partial tile (rows < bm) in its idle pipeline
     // smem as red[row][col] (row stride RED_LD floats, padded against bank conflicts), then
@@ -377,8 +439,15 @@ static void configure_kernel(const void* k) {
 
 struct GemmPlan {
   int bn, bm, stages, kblocks, splits, n_tiles, m_tiles;
+  int gsplit;
   size_t smem;
 };
+
+static constexpr size_t GS_CNT_BYTES = 64 * 1024;   // fixed counter region at the head of ws
+
+static size_t gsplit_ws_bytes(const GemmPlan& p) {
+  return GS_CNT_BYTES + (size_t)p.n_tiles * p.m_tiles * p.splits * p.bm * p.bn * 4;
+}
 
 static constexpr size_t BAR_BYTES = 2 * TC_MAX_STAGES * 8 + 8 + 16;
 
@@ -414,7 +483,7 @@ static int max_active_clusters(size_t smem, int cluster) {
 // Few tiles (decode): pick CTAs/SM (1 or 2) and the cluster split S that cover the most SMs
 // in ONE wave (cudaOccupancyMaxActiveClusters), every split keeping >= 4 k-blocks and its
 // partial tile fitting the pipeline smem.  SLX_GEMM_{CTAS,SPLITS,STAGES} override (tuning).
-static GemmPlan plan_gemm(int M, int N, int K, bool silu) {
+static GemmPlan plan_gemm(int M, int N, int K, bool silu, size_t ws_bytes) {
   GemmPlan p{};
   p.kblocks = ceil_div(K, TC_BK);
   p.m_tiles = ceil_div(M, 128);
@@ -422,6 +491,7 @@ static GemmPlan plan_gemm(int M, int N, int K, bool silu) {
   const int sms = sm_count();
   const int e_ctas = env_int("SLX_GEMM_CTAS", 0), e_s = env_int("SLX_GEMM_SPLITS", 0);
   const int e_st = env_int("SLX_GEMM_STAGES", 0), e_bn = env_int("SLX_GEMM_BN", 0);
+  const int e_gs = env_int("SLX_GEMM_GSPLIT", -1);
   double best = -1.0;
   for (int bn = 256; bn >= 128; bn -= 128) {
     if (silu && bn != 256) continue;
@@ -438,26 +508,39 @@ static GemmPlan plan_gemm(int M, int N, int K, bool silu) {
       if (e_st >= 2 && e_st < st) st = e_st;
       if (st < 2) continue;
       const size_t smem = (size_t)st * stage + BAR_BYTES + 1024;
-      for (int s = 1; s <= TC_MAX_CLUSTER; ++s) {
-        if (e_s && s != e_s) continue;
-        if (s > 1 && (p.m_tiles > 1 || (size_t)st * stage < red)) continue;
-        if (!e_s && s > 1 && ceil_div(p.kblocks, s) < 4) continue;
-        if ((s - 1) * ceil_div(p.kblocks, s) >= p.kblocks && s > 1) continue;   // no empty split
-        const int ctas_total = tiles * s;
-        if (!e_s && ctas_total > ctas * sms) continue;                            // one wave
-        if (s > 1 && !e_s && tiles > max_active_clusters(smem, s)) continue;
-        const int covered = ctas_total < sms ? ctas_total : sms;
-        // SMs covered; then wider tiles (fewer MMAs per weight byte), deeper pipelines,
-        // fewer splits (less reduction), one CTA per SM
-        const double score = covered * 1000.0 + (bn == 256 ? 50.0 : 0.0) + st * 10.0 - s - ctas;
-        if (score > best) {
-          best = score;
-          p.bn = bn; p.n_tiles = n_tiles; p.stages = st; p.splits = s; p.smem = smem;
+      for (int gs = 0; gs <= 1; ++gs) {
+        if (e_gs >= 0 && gs != e_gs) continue;
+        for (int s = 1; s <= TC_MAX_CLUSTER; ++s) {
+          if (gs && s == 1) continue;
+          if (e_s && s != e_s) continue;
+          if (s > 1 && p.m_tiles > 1) continue;
+          if (s > 1 && !gs && (size_t)st * stage < red) continue;
+          if (!e_s && s > 1 && ceil_div(p.kblocks, s) < 4) continue;
+          if ((s - 1) * ceil_div(p.kblocks, s) >= p.kblocks && s > 1) continue;   // no empty split
+          const int ctas_total = tiles * s;
+          if (!e_s && ctas_total > ctas * sms) continue;                            // one wave
+          if (s > 1 && !gs && !e_s && tiles > max_active_clusters(smem, s)) continue;
+          if (gs) {
+            GemmPlan q = p;
+            q.bn = bn; q.n_tiles = n_tiles; q.splits = s;
+            if (gsplit_ws_bytes(q) > ws_bytes) continue;
+          }
+          const int covered = ctas_total < sms ? ctas_total : sms;
+          // SMs covered; then wider tiles (fewer MMAs per weight byte), deeper pipelines,
+          // fewer splits (less reduction), one CTA per SM, cluster reduction over global
+          const double score = covered * 1000.0 + (bn == 256 ? 50.0 : 0.0) + st * 10.0 - s -
+                               ctas - 5.0 * gs;
+          if (score > best) {
+            best = score;
+            p.bn = bn; p.n_tiles = n_tiles; p.stages = st; p.splits = s; p.smem = smem;
+            p.gsplit = gs;
+          }
         }
       }
     }
   }
   if (best < 0) {   // many tiles (prefill) or overrides that cannot apply: one CTA/SM, no split
+    p.gsplit = 0;
     p.bn = (e_bn == 128 && !silu) ? 128 : 256;
     p.n_tiles = ceil_div(N, p.bn);
     p.splits = 1;
@@ -511,13 +594,16 @@ static int dispatch_tc(int epi, int c_dtype, int bn, const CUtensorMap& mx, cons
 using namespace slx;
 
 extern "C" size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
-  (void)M; (void)N; (void)K; (void)epilogue;
-  return 0;  // split-K partials live in cluster shared memory
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  // the largest global-split plan any shape can get: one wave of 2 CTAs/SM x 128 x 256 fp32
+  (void)epilogue;
+  return GS_CNT_BYTES + (size_t)2 * sm_count() * 128 * 256 * 4;
 }
 
 extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                              const void* R, int ldr, int M, int N, int K, int epilogue,
-                             int w_layout, int n_main, void* C2, int ldc2, void* stream) {
+                             int w_layout, int n_main, void* C2, int ldc2, void* ws,
+                             size_t ws_bytes, void* stream) {
   SLX_CHECK_ARG(w_layout == SLX_W_ROWMAJOR || w_layout == SLX_W_TILED);
   SLX_CHECK_ARG(A && W && C && M >= 0 && N > 0 && K > 0 && lda >= K && K % 8 == 0 &&
                 lda % 8 == 0 && ldc % 8 == 0);
@@ -541,10 +627,12 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   }
   if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= n_main && ldr % 8 == 0);
   if (M == 0) return SLX_OK;
-  GemmPlan p = plan_gemm(M, N, K, epilogue == SLX_EPI_SILU_MUL);
+  if (ws) SLX_CHECK_ALIGN(ws, 256);
+  GemmPlan p = plan_gemm(M, N, K, epilogue == SLX_EPI_SILU_MUL, ws ? ws_bytes : 0);
   if (env_int("SLX_GEMM_DEBUG", 0))
-    fprintf(stderr, "[slx_gemm] M=%d N=%d K=%d epi=%d bn=%d bm=%d stages=%d splits=%d tiles=%dx%d smem=%zu\n",
-            M, N, K, epilogue, p.bn, p.bm, p.stages, p.splits, p.n_tiles, p.m_tiles, p.smem);
+    fprintf(stderr, "[slx_gemm] M=%d N=%d K=%d epi=%d bn=%d bm=%d stages=%d splits=%d%s tiles=%dx%d smem=%zu\n",
+            M, N, K, epilogue, p.bn, p.bm, p.stages, p.splits, p.gsplit ? "(global)" : "",
+            p.n_tiles, p.m_tiles, p.smem);
   GemmArgs a{};
   a.M = M; a.N = N; a.K = K;
   a.bm = p.bm; a.stages = p.stages; a.kblocks = p.kblocks; a.splits = p.splits;
@@ -554,6 +642,11 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   a.n_main = n_main;
   a.C2 = (float*)C2;
   a.ldc2 = ldc2;
+  a.gsplit = p.gsplit;
+  if (p.gsplit) {
+    a.ws_cnt = (int*)ws;
+    a.ws_part = (float*)((char*)ws + GS_CNT_BYTES);
+  }
   // tiled W: a [n_blocks * kblocks * 128, 64] matrix of contiguous 16 KB boxes
   const int w_rows = a.w_tiled ? ceil_div(N, 128) * p.kblocks * 128 : N;
   const int w_cols = a.w_tiled ? TC_BK : K;
@@ -561,8 +654,8 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   if (!make_tmap(&mx, A, M, K, lda, p.bm) || !make_tmap(&mw, W, w_rows, w_cols, w_cols, 128))
     return SLX_ERR_CUDA;
   dim3 grid((unsigned)(p.n_tiles * p.splits), (unsigned)p.m_tiles);
-  return dispatch_tc(epilogue, c_dtype, p.bn, mx, mw, a, grid, p.smem, (unsigned)p.splits,
-                     (cudaStream_t)stream);
+  return dispatch_tc(epilogue, c_dtype, p.bn, mx, mw, a, grid, p.smem,
+                     p.gsplit ? 1u : (unsigned)p.splits, (cudaStream_t)stream);
 }
 
 // ------------------------------------------------------------------ weight packing

@@ -110,6 +110,18 @@ class Workspace:
         return self.buf
 
 
+_DEFAULT_WS: dict = {}
+
+
+def default_workspace(device) -> "Workspace":
+    """Per-device zeroed GEMM workspace (split-K partials + self-cleaning counters), sized
+    once so it never grows during CUDA graph capture.  One stream at a time may use it."""
+    d = torch.device(device)
+    if d not in _DEFAULT_WS:
+        _DEFAULT_WS[d] = Workspace(d, 48 << 20)
+    return _DEFAULT_WS[d]
+
+
 # ---------------------------------------------------------------------------------- K1
 class PackedWeight:
     """bf16 W[N, K] packed in the SLX_W_TILED layout ([N/128][K/64][128][64], zero-padded):
@@ -188,11 +200,14 @@ def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
         out = torch.empty((M, n_out), dtype=out_dtype or torch.bfloat16, device=a.device)
     if residual is not None and residual.dtype != out.dtype:
         raise ValueError("gemm: residual must have the output dtype")
+    wsb = (ws if ws is not None else default_workspace(a.device)).get(
+        _lib.load().slx_gemm_workspace_bytes(M, n_tot, K, epilogue))
     check(_lib.load().slx_gemm_bf16(_ptr(a), _ld(a), _ptr(wt), _ptr(out), _ld(out), _dt(out),
                                     _ptr(residual), _ld(residual) if residual is not None else 0,
                                     M, n_tot, K, epilogue, layout, n_main,
                                     _ptr(side) if n_tot > n_main else None,
-                                    _ld(side) if n_tot > n_main else 0, _stream()), "slx_gemm_bf16")
+                                    _ld(side) if n_tot > n_main else 0, _ptr(wsb), wsb.numel(),
+                                    _stream()), "slx_gemm_bf16")
     return out
 
 

@@ -45,7 +45,7 @@ def test_argument_validation_without_device():
     lib = _lib.load()
     null = None
     # null operands / bad shapes are rejected before any CUDA call
-    assert lib.slx_gemm_bf16(null, 64, null, null, 64, 0, null, 0, 1, 128, 64, 0, 0, 0, null, 0, null) == -1
+    assert lib.slx_gemm_bf16(null, 64, null, null, 64, 0, null, 0, 1, 128, 64, 0, 0, 0, null, 0, null, 0, null) == -1
     assert lib.slx_pack_weight(null, null, 128, 64, 64, null) == -1
     assert lib.slx_packed_weight_elems(130, 70) == 256 * 128
     assert lib.slx_rmsnorm(0, null, 8, null, 8, null, 1, 7, 1e-5, null) == -1
@@ -53,6 +53,7 @@ def test_argument_validation_without_device():
     assert lib.slx_attention(0, null, 128, null, 384, 1, 1, 1, 128, null, null, null, null, 8, null) == -1
     assert lib.slx_lora_workspace_bytes(64, 32, 16, 3) > 0
     assert lib.slx_gemm_workspace_bytes(0, 128, 64, 0) == 0
+    assert lib.slx_gemm_workspace_bytes(64, 4096, 4096, 1) > 64 * 1024
     # misaligned pointer
     buf = (ctypes.c_char * 64)()
     addr = ctypes.addressof(buf) | 1

@@ -41,8 +41,9 @@ def test_gemm_matches_torch_fp32(M, N, K, tiled):
 
 @pytest.mark.parametrize("M", [1, 64, 100])
 @pytest.mark.parametrize("bn", [256, 128])
+@pytest.mark.parametrize("gsplit", [0, 1])
 @pytest.mark.parametrize("ctas,splits", [(1, 1), (2, 8), (1, 3), (1, 6), (2, 2), (1, 5)])
-def test_gemm_decode_tilings(M, bn, ctas, splits, monkeypatch):
+def test_gemm_decode_tilings(M, bn, gsplit, ctas, splits, monkeypatch):
     """Every cluster split-K tiling the planner can pick gives the same result."""
     N, K = 3072, 4096
     a = bf(torch.randn(M, K, device=DEV))
@@ -51,6 +52,7 @@ def test_gemm_decode_tilings(M, bn, ctas, splits, monkeypatch):
     monkeypatch.setenv("SLX_GEMM_CTAS", str(ctas))
     monkeypatch.setenv("SLX_GEMM_SPLITS", str(splits))
     monkeypatch.setenv("SLX_GEMM_BN", str(bn))
+    monkeypatch.setenv("SLX_GEMM_GSPLIT", str(gsplit))
     out = ops.gemm(a, ops.pack_weight(w), out_dtype=torch.float32)
     torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
     # SiLU and residual epilogues through the same split-K reduction
