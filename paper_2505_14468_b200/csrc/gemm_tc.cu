@@ -269,7 +269,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     // split-K through global memory (no cluster placement constraints): every split CTA
     // writes its fp32 partial tile with 16-byte stores; the last to arrive (tile counter)
     // sums the S partials in split order (deterministic) and runs the epilogue.
-    __shared__ int sh_last;
+    int& sh_last = *reinterpret_cast<int*>(tmem_slot + 1);   // dynamic smem: no static smem
     float* part = g.ws_part + (size_t)tile * S * g.bm * TC_BN;
     if (warp_live) {
       for (int c0 = 0; c0 < TC_BN; c0 += 16) {
@@ -432,7 +432,10 @@ static int env_int(const char* name, int dflt) {
 }
 
 static void configure_kernel(const void* k) {
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, k);   // the opt-in limit counts static + dynamic shared memory
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(227 * 1024 - fa.sharedSizeBytes));
   // without this the driver may pick an L1-heavy carveout that fits fewer CTAs per SM
   cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
