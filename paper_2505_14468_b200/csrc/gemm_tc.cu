@@ -504,7 +504,9 @@ static GemmPlan plan_gemm(int M, int N, int K, bool silu, size_t ws_bytes) {
     const size_t stage = (size_t)p.bm * TC_BK * 2 + (size_t)(bn / 128) * W_BLOCK_BYTES;
     const size_t red = (size_t)(bn + 4) * p.bm * 4;
     for (int ctas = 1; ctas <= 2; ++ctas) {
-      if (e_ctas && ctas != e_ctas) continue;
+      // measured (tools/gemm_sweep.py): one CTA per SM with a deep pipeline beats two CTAs
+      // with shallow ones; 2 CTAs/SM only on request
+      if (e_ctas ? ctas != e_ctas : ctas != 1) continue;
       const size_t budget = ctas == 2 ? 112 * 1024 - 1024 - BAR_BYTES : 225 * 1024 - 1024 - BAR_BYTES;
       int st = (int)(budget / stage);
       st = st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
