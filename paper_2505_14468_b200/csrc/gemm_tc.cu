@@ -267,10 +267,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     }
   } else if (g.gsplit) {
     // split-K through global memory (no cluster placement constraints): every split CTA
-    // writes its fp32 partial tile with 16-byte stores; the last to arrive (tile counter)
-    // sums the S partials in split order (deterministic) and runs the epilogue.
-    int& sh_last = *reinterpret_cast<int*>(tmem_slot + 1);   // dynamic smem: no static smem
+    // writes its fp32 partial tile with 16-byte stores, the S CTAs of the tile rendezvous on
+    // an arrival counter (the plan is one wave at <= 1 CTA per SM, so all S are resident),
+    // and each reduces a 1/S column slice in split order (deterministic).  A departure
+    // counter lets the last CTA out reset both counters for the next launch / graph replay.
     float* part = g.ws_part + (size_t)tile * S * g.bm * TC_BN;
+    int* arrive = g.ws_cnt + 2 * tile;
+    int* depart = arrive + 1;
     if (warp_live) {
       for (int c0 = 0; c0 < TC_BN; c0 += 16) {
         float v[16];
@@ -284,45 +287,53 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) sh_last = atomicAdd(&g.ws_cnt[tile], 1) == S - 1;
+    if (threadIdx.x == 0) {
+      atomicAdd(arrive, 1);
+      while (atomicAdd(arrive, 0) < S) __nanosleep(64);
+    }
     __syncthreads();
-    if (sh_last) {
-      __threadfence();
-      auto sum16 = [&](int col0, float* out) {
+    __threadfence();
+    auto sum16 = [&](int col0, float* out) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) out[j] = 0.f;
+      for (int j = 0; j < 16; ++j) out[j] = 0.f;
 #pragma unroll
-        for (int sp = 0; sp < TC_MAX_CLUSTER; ++sp) {   // fixed order: deterministic
-          if (sp < S) {
-            const float4* src = reinterpret_cast<const float4*>(part + ((size_t)sp * g.bm + r) * TC_BN + col0);
-            float4 q[4];
+      for (int sp = 0; sp < TC_MAX_CLUSTER; ++sp) {   // fixed order: deterministic
+        if (sp < S) {
+          const float4* src = reinterpret_cast<const float4*>(part + ((size_t)sp * g.bm + r) * TC_BN + col0);
+          float4 q[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) q[u] = __ldcg(src + u);
+          for (int u = 0; u < 4; ++u) q[u] = __ldcg(src + u);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              out[4 * u] += q[u].x; out[4 * u + 1] += q[u].y;
-              out[4 * u + 2] += q[u].z; out[4 * u + 3] += q[u].w;
-            }
-          }
-        }
-      };
-      const int feats = EPI == SLX_EPI_SILU_MUL ? TC_BN / 2 : TC_BN;
-      if (warp_live && m < m_lim && r < g.bm) {
-        for (int f0 = 0; f0 < feats; f0 += 16) {
-          float v[16];
-          sum16(f0, v);
-          if (EPI == SLX_EPI_SILU_MUL) {
-            float u[16];
-            sum16(f0 + TC_BN / 2, u);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = silu_f(v[j]) * u[j];
-            store16(C + (size_t)m * g.ldc, tile * (TC_BN / 2) + f0, n_out, v);
-          } else {
-            store_cols<EPI>(g, C, R, m, n0 + f0, n_out, v);
+          for (int u = 0; u < 4; ++u) {
+            out[4 * u] += q[u].x; out[4 * u + 1] += q[u].y;
+            out[4 * u + 2] += q[u].z; out[4 * u + 3] += q[u].w;
           }
         }
       }
-      if (threadIdx.x == 0) g.ws_cnt[tile] = 0;   // ready for the next launch / graph replay
+    };
+    const int feats = EPI == SLX_EPI_SILU_MUL ? TC_BN / 2 : TC_BN;
+    const int fw = ((feats + S - 1) / S + 15) / 16 * 16;
+    const int f_lo = min(feats, split * fw), f_hi = min(feats, f_lo + fw);
+    if (warp_live && m < m_lim && r < g.bm) {
+      for (int f0 = f_lo; f0 < f_hi; f0 += 16) {
+        float v[16];
+        sum16(f0, v);
+        if (EPI == SLX_EPI_SILU_MUL) {
+          float u[16];
+          sum16(f0 + TC_BN / 2, u);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = silu_f(v[j]) * u[j];
+          store16(C + (size_t)m * g.ldc, tile * (TC_BN / 2) + f0, n_out, v);
+        } else {
+          store_cols<EPI>(g, C, R, m, n0 + f0, n_out, v);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(depart, 1) == S - 1) {
+      *arrive = 0;   // every split passed the rendezvous and finished reading the partials
+      *depart = 0;
+      __threadfence();
     }
   } else {
     // split-K over the cluster: stage this CTA's partial tile (rows < bm) in its idle pipeline
@@ -447,6 +458,7 @@ struct GemmPlan {
 };
 
 static constexpr size_t GS_CNT_BYTES = 64 * 1024;   // fixed counter region at the head of ws
+// (2 ints per tile: <= 8192 tiles)
 
 static size_t gsplit_ws_bytes(const GemmPlan& p) {
   return GS_CNT_BYTES + (size_t)p.n_tiles * p.m_tiles * p.splits * p.bm * p.bn * 4;
@@ -649,7 +661,7 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   a.ldc2 = ldc2;
   a.gsplit = p.gsplit;
   if (p.gsplit) {
-    a.ws_cnt = (int*)ws;
+    a.ws_cnt = (int*)ws;   // [tiles][2]: arrival, departure
     a.ws_part = (float*)((char*)ws + GS_CNT_BYTES);
   }
   // tiled W: a [n_blocks * kblocks * 128, 64] matrix of contiguous 16 KB boxes
