@@ -86,6 +86,11 @@ SLX_API size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 SLX_API int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
                   int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes, void* stream);
+/* Debug only: following slx_gemm_bf16 launches write 16 u64 globaltimer slots per CTA into
+ * the device buffer `buf` (phase timeline: entry, prologue, past PDL wait, first stage landed,
+ * last MMA issued, accumulator ready, split-K reduction start, exit, reduction end, segment
+ * accumulators ready; unused slots stay as they were).  NULL disables. */
+SLX_API int slx_debug_gemm_trace(void* buf);
 /* Grouped GEMM (SGMV on tcgen05): CTA tile i = gtiles[i] = {group, m0, m_rows, n0} computes
  * C[m0:m0+m_rows, n0:n0+256] = alpha[group] * A[m0.., :K] . W_group[n0.., :]^T (+ R), where
  * W_group is row-major [w_rows, w_cols] (row stride w_ld) and columns >= w_cols read as 0.

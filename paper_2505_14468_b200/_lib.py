@@ -48,6 +48,7 @@ SIGNATURES = {
     "slx_gemm_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "slx_gemm_bf16": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p, _sz,
                            _p]),
+    "slx_debug_gemm_trace": (_i, [_p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),
     "slx_gemm_group_tile_bytes": (_sz, []),
     "slx_gemm_grouped_bf16": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p, _i, _i,

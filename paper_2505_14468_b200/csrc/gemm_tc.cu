@@ -27,6 +27,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "gemm_host.h"
 #include "tc_ptx.cuh"
 
 namespace slx {
@@ -68,13 +69,23 @@ struct GemmArgs {
   int gsplit;                // split-K reduced through global partial tiles (no cluster)
   float* ws_part;            // [tiles][S][bm][BN] fp32 partials
   int* ws_cnt;               // [tiles] arrival counters (zero; self-cleaning)
+  unsigned long long* trace; // debug (slx_debug_gemm_trace): 8 globaltimer stamps per CTA
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+  return t;
+}
+#define SLX_TR(i) \
+  if (g.trace) g.trace[(size_t)(blockIdx.y * gridDim.x + blockIdx.x) * 16 + (i)] = gtimer()
 
 template <typename OutT>
 __device__ __forceinline__ void store_out(OutT* p, float v) {
   *p = from_f32<OutT>(v);
 }
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + expf(-g)); }
+// fast-math SiLU: no IEEE-division slow path (whose per-element branch serialises the epilogue)
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // 16 consecutive outputs of one row: vector stores for bf16 when the run is in bounds.
 template <typename OutT>
@@ -146,6 +157,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   uint32_t* tmem_slot = (uint32_t*)(accum + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) SLX_TR(0);
   const int S = g.splits;
   const int tile = blockIdx.x / S;
   const int split = blockIdx.x % S;   // == cluster rank (cluster dims (S,1,1))
@@ -177,6 +189,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) SLX_TR(1);
   if (!(warp == 0 && lane == 0)) {
     pdl_wait();
     pdl_trigger();
@@ -201,6 +214,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     }
     pdl_wait();
     pdl_trigger();
+    SLX_TR(2);
     for (int i = 0; i < npre; ++i)
       tc::tma_load_2d(smem + i * stage_bytes, &tmap_x, &full[i], (kb_lo + i) * TC_BK, m0, pol_x);
     for (int i = npre; i < n_kb; ++i) {
@@ -220,6 +234,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       const int s = i % g.stages;
       tc::mbar_wait(&full[s], (i / g.stages) & 1);
       tc::fence_after_sync();
+      if (i == 0) SLX_TR(3);
       const uint32_t st = tc::smem_u32(smem + s * stage_bytes);
 #pragma unroll
       for (int ks = 0; ks < TC_BK / 16; ++ks)
@@ -229,12 +244,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       tc::mma_commit(&empty[s]);
     }
     tc::mma_commit(accum);
+    SLX_TR(4);
   }
 
   // ---------------- epilogue: all 4 warps; warp w owns TMEM lanes (token rows) [32w, 32w+32)
   tc::mbar_wait(accum, 0);
   __syncwarp();
   tc::fence_after_sync();
+  if (threadIdx.x == 0) SLX_TR(5);
   const int r = warp * 32 + lane;
   const int m = m0 + r;
   const bool warp_live = m0 + warp * 32 < m_lim && warp * 32 < g.bm;   // warp-uniform
@@ -293,6 +310,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     }
     __syncthreads();
     __threadfence();
+    if (threadIdx.x == 0) SLX_TR(6);
     auto sum16 = [&](int col0, float* out) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) out[j] = 0.f;
@@ -354,6 +372,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       }
     }
     tc::cluster_sync();
+    if (threadIdx.x == 0) SLX_TR(6);
     const uint32_t red_base = tc::smem_u32(red);
     // this CTA's slice: output features [f_lo, f_hi) of the tile (SiLU: 128 features)
     const int feats = EPI == SLX_EPI_SILU_MUL ? TC_BN / 2 : TC_BN;
@@ -398,6 +417,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
 
   tc::fence_before_sync();
   __syncthreads();
+  if (threadIdx.x == 0) SLX_TR(7);
   if (warp == 1) {
     tc::fence_after_sync();
     tc::tmem_dealloc(tmem_base, TC_BN);
@@ -425,7 +445,7 @@ static EncodeTiledFn encode_fn() {
 }
 
 // K-major bf16 matrix [rows, cols] with row stride ld (elements); box = box_rows x 64.
-static bool make_tmap(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int box_rows) {
+bool make_tmap(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int box_rows) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -437,12 +457,12 @@ static bool make_tmap(CUtensorMap* map, const void* ptr, int rows, int cols, int
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int env_int(const char* name, int dflt) {
+int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return (e && *e) ? atoi(e) : dflt;
 }
 
-static void configure_kernel(const void* k) {
+void configure_kernel(const void* k) {
   cudaFuncAttributes fa{};
   cudaFuncGetAttributes(&fa, k);   // the opt-in limit counts static + dynamic shared memory
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -457,8 +477,8 @@ struct GemmPlan {
   size_t smem;
 };
 
-static constexpr size_t GS_CNT_BYTES = 64 * 1024;   // fixed counter region at the head of ws
-// (2 ints per tile: <= 8192 tiles)
+static constexpr size_t GS_CNT_BYTES = 64 * 1024;   // counter region at the head of ws:
+// [0, 32K) gemm_sk (monotonic), [32K, 64K) this path (self-cleaning); 2 ints per tile
 
 static size_t gsplit_ws_bytes(const GemmPlan& p) {
   return GS_CNT_BYTES + (size_t)p.n_tiles * p.m_tiles * p.splits * p.bm * p.bn * 4;
@@ -610,11 +630,22 @@ static int dispatch_tc(int epi, int c_dtype, int bn, const CUtensorMap& mx, cons
 
 using namespace slx;
 
+static unsigned long long* g_trace = nullptr;
+// Debug: every following slx_gemm_bf16 launch records 8 globaltimer stamps per CTA into buf
+// ([grid CTAs][8] u64: entry, prologue done, producer past PDL wait, first stage landed, last MMA
+// issued, accumulator ready, split-K rendezvous passed, exit).  NULL turns it off.
+extern "C" int slx_debug_gemm_trace(void* buf) {
+  g_trace = (unsigned long long*)buf;
+  return SLX_OK;
+}
+
 extern "C" size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   // the largest global-split plan any shape can get: one wave of 2 CTAs/SM x 128 x 256 fp32
   (void)epilogue;
-  return GS_CNT_BYTES + (size_t)2 * sm_count() * 128 * 256 * 4;
+  const size_t gs = GS_CNT_BYTES + (size_t)2 * sm_count() * 128 * 256 * 4;
+  const size_t sk = gemm_sk_workspace_bytes(M, N, K);
+  return sk > gs ? sk : gs;
 }
 
 extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
@@ -645,6 +676,12 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= n_main && ldr % 8 == 0);
   if (M == 0) return SLX_OK;
   if (ws) SLX_CHECK_ALIGN(ws, 256);
+  if (w_layout == SLX_W_TILED) {   // decode: stream-K kernel (gemm_sk.cu) when it applies
+    SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
+              ws, ws ? ws_bytes : 0, stream, g_trace};
+    const int st = gemm_sk_launch(sc);
+    if (st != SLX_ERR_UNSUPPORTED) return st;
+  }
   GemmPlan p = plan_gemm(M, N, K, epilogue == SLX_EPI_SILU_MUL, ws ? ws_bytes : 0);
   if (env_int("SLX_GEMM_DEBUG", 0))
     fprintf(stderr, "[slx_gemm] M=%d N=%d K=%d epi=%d bn=%d bm=%d stages=%d splits=%d%s tiles=%dx%d smem=%zu\n",
@@ -660,8 +697,9 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   a.C2 = (float*)C2;
   a.ldc2 = ldc2;
   a.gsplit = p.gsplit;
+  a.trace = g_trace;
   if (p.gsplit) {
-    a.ws_cnt = (int*)ws;   // [tiles][2]: arrival, departure
+    a.ws_cnt = (int*)((char*)ws + 32768);   // [tiles][2]: arrival, departure ([0,32K): gemm_sk)
     a.ws_part = (float*)((char*)ws + GS_CNT_BYTES);
   }
   // tiled W: a [n_blocks * kblocks * 128, 64] matrix of contiguous 16 KB boxes

@@ -49,6 +49,7 @@ def test_gemm_decode_tilings(M, bn, gsplit, ctas, splits, monkeypatch):
     a = bf(torch.randn(M, K, device=DEV))
     w = bf(torch.randn(N, K, device=DEV) * 0.05)
     ref = a.float() @ w.float().T
+    monkeypatch.setenv("SLX_GEMM_SK", "0")   # the cluster / global split-K tilings (M > 64 path)
     monkeypatch.setenv("SLX_GEMM_CTAS", str(ctas))
     monkeypatch.setenv("SLX_GEMM_SPLITS", str(splits))
     monkeypatch.setenv("SLX_GEMM_BN", str(bn))
@@ -63,6 +64,45 @@ def test_gemm_decode_tilings(M, bn, gsplit, ctas, splits, monkeypatch):
     monkeypatch.setenv("SLX_GEMM_BN", "256")   # SiLU pairs always use 256-wide tiles
     o3 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_SILU_MUL, out_dtype=torch.float32)
     torch.testing.assert_close(o3, (g_ * torch.sigmoid(g_) * u_).reshape(M, N // 2), rtol=1e-3, atol=1e-3)
+
+
+@pytest.mark.parametrize("M", [1, 17, 64])
+@pytest.mark.parametrize("N,K", [(3072, 4096), (4608, 4096), (1000, 11008), (32000, 1024)])
+@pytest.mark.parametrize("ctas,min_units", [(0, 4), (37, 4), (5, 4), (1, 1), (0, 1)])
+def test_gemm_stream_k(M, N, K, ctas, min_units, monkeypatch):
+    """Stream-K decode GEMM (M <= 64): every range split (whole tiles, tail/head pieces, up to
+    dozens of pieces per tile) gives the fp32 result; epilogues residual / SiLU / side output."""
+    monkeypatch.setenv("SLX_SK_CTAS", str(ctas))
+    monkeypatch.setenv("SLX_SK_MIN_UNITS", str(min_units))
+    g = torch.Generator(device=DEV).manual_seed(M + N + K + ctas)
+    a = bf(torch.randn(M, K, device=DEV, generator=g))
+    w = bf(torch.randn(N, K, device=DEV, generator=g) * 0.05)
+    ref = a.float() @ w.float().T
+    pw = ops.pack_weight(w)
+    out = ops.gemm(a, pw, out_dtype=torch.float32)
+    torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
+    again = ops.gemm(a, pw, out_dtype=torch.float32)   # counters re-armed, same split order
+    assert torch.equal(out, again)
+    r = bf(torch.randn(M, N, device=DEV, generator=g))
+    o2 = ops.gemm(a, pw, epilogue=EPI_RESIDUAL, residual=r)
+    torch.testing.assert_close(o2.float(), ref + r.float(), rtol=1e-2, atol=2e-2)
+    if N % 256 == 0:
+        g_, u_ = ref.view(M, N // 256, 2, 128)[:, :, 0], ref.view(M, N // 256, 2, 128)[:, :, 1]
+        o3 = ops.gemm(a, pw, epilogue=EPI_SILU_MUL, out_dtype=torch.float32)
+        torch.testing.assert_close(o3, (g_ * torch.sigmoid(g_) * u_).reshape(M, N // 2), rtol=1e-3,
+                                   atol=1e-3)
+    # stacked extra rows -> fp32 side output (decode LoRA shrink), main columns + residual
+    if N % 128:
+        return
+    E = 512
+    ext = bf(torch.randn(E, K, device=DEV, generator=g) * 0.05)
+    pw2 = ops.pack_weight(w, extra_rows=E)
+    ops.pack_rows(pw2, ext, E, N)
+    x = r.clone()
+    side = torch.empty(M, E, device=DEV)
+    ops.gemm(a, pw2, x, epilogue=EPI_RESIDUAL, residual=x, side=side)
+    torch.testing.assert_close(x.float(), ref + r.float(), rtol=1e-2, atol=2e-2)
+    torch.testing.assert_close(side, a.float() @ ext.float().T, rtol=1e-4, atol=1e-3)
 
 
 @pytest.mark.parametrize("M", [3, 64, 200])
