@@ -152,6 +152,26 @@ SLX_API int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, int 
                   const int32_t* slot_rank, const float* slot_scale, int n_slots, int max_rank,
                   int n_targets, const slx_lora_target* targets, const int* v_col_off,
                   void* ws, size_t ws_bytes, void* stream);
+/* Fused decode expand: a consumer kernel adds the LoRA term of the projection it reads while
+ * loading it, instead of a separate expand launch + read-modify-write of y.  For output
+ * column n of target i of token t (slot s = tok_slot[t] >= 0, rank r = slot_rank[s]):
+ *   delta = sum_{j < r} (v[t, v_col_off[i] + s * max_rank + j] * slot_scale[s]) * B_s[n, j]
+ * (sequential fmaf in j: bit-identical to slx_lora_expand).  The target's outputs are the row
+ * columns [y_col_off[i], y_col_off[i] + d_out[i]).  b_ptrs[i]: device uint64 [n_slots] table of
+ * B_s [d_out, r] (bf16; 0 = adapter does not target it). */
+typedef struct slx_lora_delta {
+  const float* v;            /* fp32 [n_tok, ldv]: the GEMM side output (stacked shrink) */
+  int ldv;
+  const int32_t* tok_slot;   /* [n_tok], -1 = no adapter */
+  const int32_t* slot_rank;  /* [n_slots] */
+  const float* slot_scale;   /* [n_slots] */
+  int max_rank;
+  int n_targets;             /* 0 .. SLX_LORA_MAX_TARGETS */
+  const uint64_t* b_ptrs[SLX_LORA_MAX_TARGETS];
+  int v_col_off[SLX_LORA_MAX_TARGETS];
+  int y_col_off[SLX_LORA_MAX_TARGETS];
+  int d_out[SLX_LORA_MAX_TARGETS];
+} slx_lora_delta;
 /* Convenience: plan_tokens + apply (BGMV) and plan_segments + apply (SGMV). */
 SLX_API int slx_lora_bgmv(int dtype, void* y, int ldy, const void* x, int ldx, const int32_t* tok_slot,
                   int n_tok, int d_in, const int32_t* slot_rank, const float* slot_scale,
@@ -171,6 +191,10 @@ SLX_API int slx_embedding(int dtype, void* out, const void* table, const int32_t
                   int n_tok, int d, int vocab, void* stream);
 SLX_API int slx_rmsnorm(int dtype, void* out, int ldo, const void* x, int ldx, const void* w,
                 int n_tok, int d, float eps, void* stream);
+/* Residual-stream LoRA add + RMSNorm: x[t, :] += delta (slx_lora_delta over the row, rounded
+ * to the activation dtype and written back to x), then out = rmsnorm(x) (lora may be NULL). */
+SLX_API int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx, const void* w,
+                int n_tok, int d, float eps, const slx_lora_delta* lora, void* stream);
 /* qkv [n_tok, (H + 2 Hkv) D]: rotate q,k in place (rotate-half, cos/sin tables fp32
  * [max_pos, D/2]) and write k, v at (tok_seq[t], tok_pos[t]) of the caches. */
 SLX_API int slx_rope_kv_write(int dtype, void* qkv, int ld_qkv, int n_tok, int heads, int kv_heads,
@@ -190,6 +214,14 @@ SLX_API int slx_rope_attention_decode(int dtype, void* out, int ldo, const void*
                   int n_tok, int heads, int kv_heads, int head_dim, const int32_t* tok_pos,
                   const int32_t* tok_seq, const float* cos_tab, const float* sin_tab, int max_pos,
                   void* k_cache, void* v_cache, int max_ctx, void* stream);
+/* Same, with the q/k/v LoRA expand fused in: the row values of q (head h), k and v (kv head)
+ * get the slx_lora_delta of their qkv-row columns added before RoPE / the KV append (lora may
+ * be NULL).  qkv itself is not modified. */
+SLX_API int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, const void* qkv,
+                  int ld_qkv, int n_tok, int heads, int kv_heads, int head_dim,
+                  const int32_t* tok_pos, const int32_t* tok_seq, const float* cos_tab,
+                  const float* sin_tab, int max_pos, void* k_cache, void* v_cache, int max_ctx,
+                  const slx_lora_delta* lora, void* stream);
 /* Prefill (tensor cores, mma.sync flash attention, head_dim 128, bf16): `tiles` is a device
  * array of n_tiles {int tok0, nq, seq, pos0} (<= 64 queries of one segment each, size
  * slx_flash_prefill_tile_bytes()); query t of a tile attends cache positions 0..pos0+t of

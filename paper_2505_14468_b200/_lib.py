@@ -40,6 +40,13 @@ class LoraTarget(ctypes.Structure):
                 ("y_col_block", _i), ("y_col_stride", _i)]
 
 
+class LoraDelta(ctypes.Structure):
+    """slx_lora_delta: fused decode expand in a consumer kernel."""
+    _fields_ = [("v", _p), ("ldv", _i), ("tok_slot", _p), ("slot_rank", _p), ("slot_scale", _p),
+                ("max_rank", _i), ("n_targets", _i), ("b_ptrs", _p * 4), ("v_col_off", _i * 4),
+                ("y_col_off", _i * 4), ("d_out", _i * 4)]
+
+
 # name -> (restype, argtypes): every symbol declared in include/slora_b200.h
 SIGNATURES = {
     "slx_status_string": (ctypes.c_char_p, [_i]),
@@ -69,10 +76,13 @@ SIGNATURES = {
                            ctypes.POINTER(LoraTarget), _p, _sz, _p]),
     "slx_embedding": (_i, [_i, _p, _p, _p, _i, _i, _i, _p]),
     "slx_rmsnorm": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _f, _p]),
+    "slx_rmsnorm_lora": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _f, ctypes.POINTER(LoraDelta), _p]),
     "slx_rope_kv_write": (_i, [_i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p, _i, _p]),
     "slx_attention": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p]),
     "slx_rope_attention_decode": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p,
                                        _i, _p]),
+    "slx_rope_attention_decode_lora": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i,
+                                            _p, _p, _i, ctypes.POINTER(LoraDelta), _p]),
     "slx_flash_prefill_tile_bytes": (_sz, []),
     "slx_attention_prefill": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _i, _p, _p, _i, _p]),
     "slx_silu_mul_blocked": (_i, [_i, _p, _i, _p, _i, _i, _i, _p]),

@@ -98,6 +98,154 @@ int sm_count();
 
 }  // namespace slx
 
+// ---------------------------------------------------------------- fused LoRA expand (slx_lora_delta)
+namespace slx {
+struct DeltaArgs {
+  const float* v;
+  int ldv;
+  const int32_t* tok_slot;
+  const int32_t* slot_rank;
+  const float* slot_scale;
+  int max_rank, n_targets;
+  const uint64_t* b_ptrs[SLX_LORA_MAX_TARGETS];
+  int v_col_off[SLX_LORA_MAX_TARGETS], y_col_off[SLX_LORA_MAX_TARGETS], d_out[SLX_LORA_MAX_TARGETS];
+};
+inline DeltaArgs delta_args(const slx_lora_delta* d) {
+  DeltaArgs a{};
+  if (d == nullptr) return a;
+  a.v = d->v; a.ldv = d->ldv; a.tok_slot = d->tok_slot; a.slot_rank = d->slot_rank;
+  a.slot_scale = d->slot_scale; a.max_rank = d->max_rank; a.n_targets = d->n_targets;
+  for (int i = 0; i < SLX_LORA_MAX_TARGETS; ++i) {
+    a.b_ptrs[i] = i < d->n_targets ? d->b_ptrs[i] : nullptr;
+    a.v_col_off[i] = d->v_col_off[i]; a.y_col_off[i] = d->y_col_off[i]; a.d_out[i] = d->d_out[i];
+  }
+  return a;
+}
+inline bool delta_valid(const slx_lora_delta* d) {
+  if (d == nullptr) return true;
+  if (d->n_targets < 0 || d->n_targets > SLX_LORA_MAX_TARGETS) return false;
+  if (d->n_targets == 0) return true;
+  if (!d->v || !d->tok_slot || !d->slot_rank || !d->slot_scale || d->max_rank <= 0 || d->ldv <= 0)
+    return false;
+  // 16-byte v / B vectors: ldv, offsets, max_rank multiples of 4 / 8; v 16-byte aligned
+  if (d->ldv % 4 || d->max_rank % 8 || (reinterpret_cast<uintptr_t>(d->v) & 15)) return false;
+  for (int i = 0; i < d->n_targets; ++i)
+    if (!d->b_ptrs[i] || d->d_out[i] <= 0 || d->y_col_off[i] < 0 || d->v_col_off[i] < 0 ||
+        d->v_col_off[i] % 4)
+      return false;
+  return true;
+}
+// Per-token view: slot, rank, scale resolved once.
+struct DeltaTok {
+  int slot, rank;
+  float scale;
+  const float* vrow;
+};
+__device__ __forceinline__ DeltaTok delta_tok(const DeltaArgs& d, int t) {
+  DeltaTok k{-1, 0, 0.f, nullptr};
+  if (d.n_targets == 0) return k;
+  k.slot = d.tok_slot[t];
+  if (k.slot >= 0) {
+    k.rank = min(d.slot_rank[k.slot], d.max_rank);
+    k.scale = d.slot_scale[k.slot];
+    k.vrow = d.v + (size_t)t * d.ldv;
+  }
+  return k;
+}
+// LoRA delta of row column `col` (0 when no target covers it / no adapter).
+__device__ __forceinline__ float delta_dot(const DeltaTok& k, const uint64_t* b_tab, int v_off, int n,
+                                           int max_rank) {
+  const bf16* B = reinterpret_cast<const bf16*>(b_tab[k.slot]);
+  if (B == nullptr) return 0.f;
+  const float* vr = k.vrow + v_off + k.slot * max_rank;
+  const bf16* br = B + (size_t)n * k.rank;   // rank % 8 == 0 (pool invariant): 16 B rows
+  float acc = 0.f;
+  for (int j = 0; j < k.rank; j += 8) {
+    float b[8];
+    Vec8<bf16>::load(br + j, b);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = fmaf(vr[j + u] * k.scale, b[u], acc);
+  }
+  return acc;
+}
+// Register-resident fast path (rank <= 8 * RV): the B row of output column `col` is fetched
+// before the PDL wait (adapters are static); after it, the CTA stages scale * v of every target
+// once in shared memory (delta_stage_v) and each thread finishes its columns from there.
+template <int RV>
+struct DeltaRow {
+  uint4 b[RV];
+  int ti;   // target index (-1: no delta)
+};
+template <int RV>
+__device__ __forceinline__ void delta_prefetch(const DeltaArgs& d, const DeltaTok& k, int col,
+                                               DeltaRow<RV>& r) {
+  r.ti = -1;
+  if (k.slot < 0 || k.rank == 0) return;
+#pragma unroll
+  for (int i = 0; i < SLX_LORA_MAX_TARGETS; ++i) {
+    const int n = col - d.y_col_off[i];
+    if (r.ti < 0 && i < d.n_targets && n >= 0 && n < d.d_out[i]) {
+      const bf16* B = reinterpret_cast<const bf16*>(__ldg(&d.b_ptrs[i][k.slot]));
+      if (B != nullptr) {
+        r.ti = i;
+        const uint4* src = reinterpret_cast<const uint4*>(B + (size_t)n * k.rank);
+#pragma unroll
+        for (int j = 0; j < RV; ++j) r.b[j] = j * 8 < k.rank ? __ldg(src + j) : make_uint4(0, 0, 0, 0);
+      }
+    }
+  }
+}
+constexpr int DELTA_VS = SLX_LORA_MAX_TARGETS * 64;   // staged floats (rank <= 64)
+// vs[i * 64 + j] = v[t, v_col_off[i] + slot * max_rank + j] * scale  (j < rank), cooperative.
+__device__ __forceinline__ void delta_stage_v(const DeltaArgs& d, const DeltaTok& k, float* vs,
+                                              int tid, int nthreads) {
+  if (k.slot < 0 || k.rank == 0) return;
+  for (int e = tid; e < d.n_targets * 64; e += nthreads) {
+    const int i = e >> 6, j = e & 63;
+    int off = 0;
+#pragma unroll
+    for (int q = 0; q < SLX_LORA_MAX_TARGETS; ++q)
+      if (q == i) off = d.v_col_off[q];
+    if (j < k.rank) vs[e] = k.vrow[off + k.slot * d.max_rank + j] * k.scale;
+  }
+}
+// delta = sum_j vs[j] * B[j], sequential fmaf (bit-identical to delta_col)
+template <int RV>
+__device__ __forceinline__ float delta_finish(const DeltaTok& k, const DeltaRow<RV>& r, const float* vs) {
+  if (r.ti < 0) return 0.f;
+  const float* v = vs + r.ti * 64;
+  float acc = 0.f;
+#pragma unroll
+  for (int j = 0; j < RV; ++j) {
+    if (j * 8 < k.rank) {
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&r.b[j]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __bfloat1622float2(h2[u]);
+        acc = fmaf(v[8 * j + 2 * u], f.x, acc);
+        acc = fmaf(v[8 * j + 2 * u + 1], f.y, acc);
+      }
+    }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ float delta_col(const DeltaArgs& d, const DeltaTok& k, int col) {
+  if (k.slot < 0 || k.rank == 0) return 0.f;
+  float res = 0.f;
+  bool hit = false;
+#pragma unroll
+  for (int i = 0; i < SLX_LORA_MAX_TARGETS; ++i) {   // static indices: params stay in the cbank
+    const int n = col - d.y_col_off[i];
+    if (!hit && i < d.n_targets && n >= 0 && n < d.d_out[i]) {
+      hit = true;
+      res = delta_dot(k, d.b_ptrs[i], d.v_col_off[i], n, d.max_rank);
+    }
+  }
+  return res;
+}
+}  // namespace slx
+
 // ---------------------------------------------------------------- launch plumbing (PDL + clusters)
 namespace slx {
 

@@ -48,6 +48,7 @@ constexpr size_t SK_BAR_BYTES = (2 * SK_MAX_STAGES + 4) * 8 + 16 + 4 * SK_MAX_SE
 
 struct SkArgs {
   int M, N, bm, stages, kblocks, n_tiles, G, pmax;
+  int cs;        // > 1: cluster mode, G = n_tiles * cs, tile t's pieces are cluster t (DSMEM)
   int U;         // n_tiles * kblocks MMA units (one 64-wide k-block of one 256-row tile);
                  // U * G < 2^31 (planner), so all unit arithmetic is 32-bit
   void* C;
@@ -246,6 +247,97 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       SK_TR(4);
     }
     __syncwarp();
+  } else if (g.cs > 1) {
+    // ------------------------------------------- epilogue, cluster mode (warps 2-5)
+    // This CTA holds piece `rank` of tile c / cs (exactly one segment).  Pieces are staged in
+    // each CTA's own (now idle) pipeline smem as [chunk][row][16] fp32 and reduced through
+    // DSMEM: CTA `rank` sums a 1/cs slice of the tile over the cs peers in rank order.
+    const int q = warp & 3, r = q * 32 + lane, et = threadIdx.x - 64;
+    const bool qlive = q * 32 < g.bm;
+    const bool silu = EPI == SLX_EPI_SILU_MUL;
+    const int cs = g.cs, rank = c % cs, tile = c / cs;
+    const int n_out = silu ? g.N / 2 : g.N;
+    float* stg = reinterpret_cast<float*>(smem);
+    tc::mbar_wait(&tfull[0], 0);
+    if (et == 0) SK_TR(9);
+    __syncwarp();
+    tc::fence_after_sync();
+    if (qlive) {
+      const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16);
+      for (int ch = 0; ch < 16; ch += 2) {
+        float v0[16], v1[16];
+        tc::tmem_ld16x2(tacc + ch * 16, tacc + ch * 16 + 16, v0, v1);
+        if (r < g.bm) {
+          float4* p0 = reinterpret_cast<float4*>(stg + ((size_t)ch * g.bm + r) * 16);
+          float4* p1 = reinterpret_cast<float4*>(stg + ((size_t)(ch + 1) * g.bm + r) * 16);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            p0[e] = make_float4(v0[4 * e], v0[4 * e + 1], v0[4 * e + 2], v0[4 * e + 3]);
+            p1[e] = make_float4(v1[4 * e], v1[4 * e + 1], v1[4 * e + 2], v1[4 * e + 3]);
+          }
+        }
+      }
+    }
+    tc::fence_before_sync();
+    tc::cluster_sync();   // #1: every piece of the tile staged
+    if (et == 0) SK_TR(6);
+    const uint32_t stg_s = tc::smem_u32(stg);
+    const int nfc = silu ? 8 : 16;
+    const int items = nfc * g.bm;
+    const int it_lo = rank * items / cs, it_hi = (rank + 1) * items / cs;
+    for (int it = it_lo + et; it < it_hi; it += 128) {
+      const int ch = it / g.bm, m = it % g.bm;
+      const int n = tile * SK_BN + ch * 16;
+      float res[16];
+      if (EPI == SLX_EPI_RESIDUAL && m < g.M && n < g.N)
+        sk_load_res<OutT>(g, m, n, g.C2 != nullptr ? g.n_main : g.N, res);
+      const uint32_t oa = stg_s + (uint32_t)(((ch * g.bm + m) * 16) * 4);
+      const uint32_t ob = stg_s + (uint32_t)((((ch + 8) * g.bm + m) * 16) * 4);
+      float a[16], b[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) a[e] = b[e] = 0.f;
+      constexpr int PB = EPI == SLX_EPI_SILU_MUL ? 4 : 8;   // register budget
+      for (int p0 = 0; p0 < cs; p0 += PB) {
+        float4 qa[PB][4], qb[silu ? PB : 1][4];
+#pragma unroll
+        for (int bi = 0; bi < PB; ++bi) {
+          if (p0 + bi < cs) {
+            const uint32_t ra = tc::mapa(oa, (uint32_t)(p0 + bi));
+#pragma unroll
+            for (int e = 0; e < 4; ++e) qa[bi][e] = tc::ld_dsmem4(ra + e * 16);
+            if (silu) {
+              const uint32_t rb = tc::mapa(ob, (uint32_t)(p0 + bi));
+#pragma unroll
+              for (int e = 0; e < 4; ++e) qb[silu ? bi : 0][e] = tc::ld_dsmem4(rb + e * 16);
+            }
+          }
+        }
+#pragma unroll
+        for (int bi = 0; bi < PB; ++bi) {   // fixed rank order: deterministic
+          if (p0 + bi < cs) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              a[4 * e] += qa[bi][e].x; a[4 * e + 1] += qa[bi][e].y;
+              a[4 * e + 2] += qa[bi][e].z; a[4 * e + 3] += qa[bi][e].w;
+              if (silu) {
+                const float4 t = qb[silu ? bi : 0][e];
+                b[4 * e] += t.x; b[4 * e + 1] += t.y; b[4 * e + 2] += t.z; b[4 * e + 3] += t.w;
+              }
+            }
+          }
+        }
+      }
+      if (m >= g.M) continue;
+      if (silu) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) a[e] = sk_silu(a[e]) * b[e];
+        sk_store16(reinterpret_cast<OutT*>(g.C) + (size_t)m * g.ldc, tile * 128 + ch * 16, n_out, a);
+      } else if (n < g.N) {
+        sk_finish<EPI, OutT>(g, m, n, a, res);
+      }
+    }
+    if (et == 0) SK_TR(8);
+    tc::cluster_sync();   // #2: keep our smem alive until every peer has read it
   } else {
     // -------------------------------------------------------------- epilogue (warps 2-5)
     const int q = warp & 3;              // TMEM lane quadrant this warp may access
@@ -432,6 +524,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     if (et == 0) SK_TR(8);
   }
 
+  if (warp < 2 && g.cs > 1) {   // producer / MMA warps join the epilogue's cluster barriers
+    tc::cluster_sync();
+    tc::cluster_sync();
+  }
   tc::fence_before_sync();
   __syncthreads();
   if (threadIdx.x == 0) SK_TR(7);
@@ -442,10 +538,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
 }
 
 struct SkPlan {
-  int bm, stages, kblocks, n_tiles, G, pmax;
+  int bm, stages, kblocks, n_tiles, G, pmax, cs;
   long long U;
   size_t smem, ws;
 };
+
+int sk_max_clusters(size_t smem, int cluster);
 
 bool sk_plan(int M, int N, int K, SkPlan* p) {
   if (M <= 0 || M > SK_MAX_M) return false;
@@ -478,6 +576,7 @@ bool sk_plan(int M, int N, int K, SkPlan* p) {
     if (e_g < G) G = e_g;
   }
   p->G = (int)G;
+  p->cs = 1;
   const long long upc = (p->U + G - 1) / G;
   if ((upc - 1) / p->kblocks + 2 > SK_MAX_SEGS) return false;
   int pmax = 1;
@@ -495,6 +594,16 @@ bool sk_plan(int M, int N, int K, SkPlan* p) {
   p->stages = st;
   p->smem = (size_t)st * stage + SK_BAR_BYTES + 1024;
   p->ws = SK_PART_OFF + (size_t)p->n_tiles * pmax * p->bm * SK_BN * 4;
+  // Uniform split (every CTA one piece, tile t = CTAs [t*s, t*s+s)): reduce through DSMEM in a
+  // cluster of s when all n_tiles clusters are co-resident and the staged piece fits the
+  // pipeline smem.
+  const int s_split = p->G / p->n_tiles;
+  if (env_int("SLX_SK_CLUSTER", 1) && s_split >= 2 && s_split <= 8 &&
+      p->G == p->n_tiles * s_split && (size_t)p->bm * SK_BN * 4 <= (size_t)st * stage &&
+      sk_max_clusters(p->smem, s_split) >= p->n_tiles) {
+    p->cs = s_split;
+    p->ws = SK_PART_OFF;
+  }
   return true;
 }
 
@@ -507,7 +616,36 @@ int sk_launch_t(const CUtensorMap& mx, const CUtensorMap& mw, const SkArgs& a, c
     configure_kernel((const void*)k);
     configured = true;
   }
-  return launch_ex(k, dim3((unsigned)p.G), dim3(SK_THREADS), p.smem, s, 1u, mx, mw, a);
+  return launch_ex(k, dim3((unsigned)p.G), dim3(SK_THREADS), p.smem, s, (unsigned)p.cs, mx, mw, a);
+}
+
+// Max co-resident clusters of `cluster` CTAs with `smem` bytes each (cached per device shape).
+int sk_max_clusters(size_t smem, int cluster) {
+  struct Key { size_t smem; int cluster, value; };
+  static Key cache[32];
+  static int n_cache = 0;
+  for (int i = 0; i < n_cache; ++i)
+    if (cache[i].smem == smem && cache[i].cluster == cluster) return cache[i].value;
+  auto k = gemm_sk_kernel<SLX_EPI_NONE, bf16>;
+  configure_kernel((const void*)k);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)cluster * 64);
+  cfg.blockDim = dim3(SK_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = (unsigned)cluster;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    n = 0;
+  }
+  if (n_cache < 32) cache[n_cache++] = Key{smem, cluster, n};
+  return n;
 }
 
 }  // namespace
@@ -522,11 +660,11 @@ int gemm_sk_launch(const SkCall& c) {
   SkPlan p{};
   if (!sk_plan(c.M, c.N, c.K, &p) || p.ws > c.ws_bytes) return SLX_ERR_UNSUPPORTED;
   if (env_int("SLX_GEMM_DEBUG", 0))
-    fprintf(stderr, "[slx_gemm_sk] M=%d N=%d K=%d epi=%d bm=%d stages=%d G=%d tiles=%d kb=%d pmax=%d\n",
-            c.M, c.N, c.K, c.epilogue, p.bm, p.stages, p.G, p.n_tiles, p.kblocks, p.pmax);
+    fprintf(stderr, "[slx_gemm_sk] M=%d N=%d K=%d epi=%d bm=%d stages=%d G=%d tiles=%d kb=%d pmax=%d cluster=%d\n",
+            c.M, c.N, c.K, c.epilogue, p.bm, p.stages, p.G, p.n_tiles, p.kblocks, p.pmax, p.cs);
   SkArgs a{};
   a.M = c.M; a.N = c.N; a.bm = p.bm; a.stages = p.stages; a.kblocks = p.kblocks;
-  a.n_tiles = p.n_tiles; a.G = p.G; a.pmax = p.pmax; a.U = (int)p.U;
+  a.n_tiles = p.n_tiles; a.G = p.G; a.pmax = p.pmax; a.U = (int)p.U; a.cs = p.cs;
   a.C = c.C; a.ldc = c.ldc; a.R = c.R; a.ldr = c.ldr;
   a.n_main = c.C2 != nullptr ? c.n_main : c.N;
   a.C2 = (float*)c.C2; a.ldc2 = c.ldc2;

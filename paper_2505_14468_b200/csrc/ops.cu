@@ -64,6 +64,70 @@ __global__ void rmsnorm_kernel(T* __restrict__ out, int ldo, const T* __restrict
   }
 }
 
+// x[t] += LoRA delta (rounded to T, written back), then out = rmsnorm(x).  The o-projection
+// expand of the decode step fused into the post-attention norm (slx_rmsnorm_lora).
+template <typename T>
+__global__ void __launch_bounds__(512) rmsnorm_lora_kernel(T* __restrict__ out, int ldo, T* __restrict__ x, int ldx,
+                                    const bf16* __restrict__ w, int d, float eps, DeltaArgs lora) {
+  const int t = blockIdx.x;   // the slot table / adapter pool are >= 2 launches old (PDL)
+  T* xr = x + (size_t)t * ldx;
+  const DeltaTok dt = delta_tok(lora, t);
+  float ss = 0.f;
+  const int i0 = threadIdx.x * 8;
+  if (d == (int)blockDim.x * 8 && dt.slot >= 0 && dt.rank <= 16) {
+    // one 8-column group per thread: B rows fetched in registers before the PDL wait
+    DeltaRow<2> dr[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) delta_prefetch<2>(lora, dt, i0 + j, dr[j]);
+    pdl_wait();
+    pdl_trigger();
+    __shared__ float vs[DELTA_VS];
+    float f[8];
+    Vec8<T>::load(xr + i0, f);
+    delta_stage_v(lora, dt, vs, threadIdx.x, blockDim.x);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + delta_finish<2>(dt, dr[j], vs)));
+    Vec8<T>::store(xr + i0, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+  } else {
+    pdl_wait();
+    pdl_trigger();
+    for (int i = i0; i < d; i += blockDim.x * 8) {
+      float f[8];
+      Vec8<T>::load(xr + i, f);
+      if (dt.slot >= 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + delta_col(lora, dt, i + j)));
+        Vec8<T>::store(xr + i, f);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+    }
+  }
+  __shared__ float red[32];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();   // also orders this CTA's x write-back before the re-read below
+  const float inv = 1.0f / sqrtf(red[0] / (float)d + eps);
+  T* orow = out + (size_t)t * ldo;
+  for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+    float f[8], g[8];
+    Vec8<T>::load(xr + i, f);
+    Vec8<bf16>::load(w + i, g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = (f[j] * inv) * g[j];
+    Vec8<T>::store(orow + i, f);
+  }
+}
+
 // ------------------------------------------------------------------ RoPE + KV write
 // One CTA per token; thread i handles rotation pair (i, i + D/2) of every head.
 template <typename T>
@@ -243,7 +307,7 @@ template <> struct DecCfg<float> { static constexpr int KB = 64; };
 template <typename T, int D>
 constexpr size_t dec_smem() {
   return (size_t)2 * DecCfg<T>::KB * (D + 16 / sizeof(T)) * sizeof(T) +
-         (size_t)(3 * D + DecCfg<T>::KB + 2 * 128 + 8) * 4;
+         (size_t)(3 * D + DecCfg<T>::KB + 2 * 128 + 8 + 3 * D + DELTA_VS) * 4;
 }
 
 template <typename T, int D>
@@ -252,15 +316,14 @@ rope_attn_decode_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv,
                         int Hkv, const int32_t* __restrict__ tok_pos,
                         const int32_t* __restrict__ tok_seq, const float* __restrict__ cos_tab,
                         const float* __restrict__ sin_tab, T* __restrict__ kc, T* __restrict__ vc,
-                        int max_ctx, float scale_log2) {
-  pdl_wait();
-  pdl_trigger();
+                        int max_ctx, float scale_log2, DeltaArgs lora) {
   constexpr int KB = DecCfg<T>::KB;
   constexpr int VEC = 16 / sizeof(T);
   constexpr int DP = D + VEC;          // padded smem row
   constexpr int CH = D / VEC;          // 16-byte chunks per row
   constexpr int NT = 128;
   constexpr int KP = NT / D;           // key partitions in P.V (1 for D=128, 2 for D=64)
+  constexpr int PER = (3 * D + NT - 1) / NT;   // q/k/v row columns per thread
   extern __shared__ __align__(16) uint8_t dsm[];
   T* Ks = reinterpret_cast<T*>(dsm);                   // [KB][DP]
   T* Vs = Ks + KB * DP;                                 // [KB][DP]
@@ -270,24 +333,80 @@ rope_attn_decode_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv,
   float* ps = vn + D;                                    // [KB]
   float* red = ps + KB;                                  // [2*128] partials / reductions
   float* misc = red + 2 * 128;                           // [8]
+  float* raw = misc + 8;                                 // [3][D] q, k, v row (+ LoRA delta)
+  float* vs = raw + 3 * D;                               // [DELTA_VS] scale * LoRA v
 
   const int tid = threadIdx.x;
   const int t = blockIdx.x / H, h = blockIdx.x % H;
   const int group = H / Hkv, hk = h / group;
+  // step inputs (token positions / sequences / adapter slots), the adapter pool and the cached
+  // keys and values before `pos` were all written two or more launches back (PDL invariant,
+  // common.cuh): fetch them before waiting on the projection GEMM.
   const int pos = tok_pos[t], seq = tok_seq[t];
+  const DeltaTok dt = delta_tok(lora, t);
+  const T* kbase = kc + ((size_t)seq * Hkv + hk) * max_ctx * D;
+  const T* vbase = vc + ((size_t)seq * Hkv + hk) * max_ctx * D;
+  auto load_block = [&](int k0, int nk) {
+    for (int e = tid; e < nk * CH; e += NT) {
+      const int r = e / CH, c = e % CH;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(Ks + r * DP + c * VEC))),
+                   "l"(kbase + (size_t)(k0 + r) * D + c * VEC) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(Vs + r * DP + c * VEC))),
+                   "l"(vbase + (size_t)(k0 + r) * D + c * VEC) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const int n_cached = pos;
+  if (n_cached > 0) load_block(0, min(KB, n_cached));
+  const bool fast = dt.slot >= 0 && dt.rank <= 16;
+  DeltaRow<2> dr[PER];
+  auto col_of = [&](int i) {
+    const int part = i / D, e = i - part * D;
+    return (part == 0 ? h : (part == 1 ? H + hk : H + Hkv + hk)) * D + e;
+  };
+  if (fast) {
+#pragma unroll
+    for (int p = 0; p < PER; ++p)
+      if (tid + p * NT < 3 * D) delta_prefetch<2>(lora, dt, col_of(tid + p * NT), dr[p]);
+  }
+  pdl_wait();
+  pdl_trigger();
+
   const int half = D / 2;
   const T* row = qkv + (size_t)t * ld;
   const float* cr = cos_tab + (size_t)pos * half;
   const float* sr = sin_tab + (size_t)pos * half;
   T* kdst = kc + (((size_t)seq * Hkv + hk) * max_ctx + pos) * D;
   T* vdst = vc + (((size_t)seq * Hkv + hk) * max_ctx + pos) * D;
+  // the projection outputs of this head, with the fused LoRA expand added and rounded to T
+  // exactly as slx_lora_expand would have stored them in qkv
+  float rv[PER];
+#pragma unroll
+  for (int p = 0; p < PER; ++p) rv[p] = tid + p * NT < 3 * D ? to_f32(row[col_of(tid + p * NT)]) : 0.f;
+  if (fast) {
+    delta_stage_v(lora, dt, vs, tid, NT);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int i = tid + p * NT;
+    if (i < 3 * D) {
+      float v = rv[p];
+      if (dt.slot >= 0)
+        v = to_f32(from_f32<T>(v + (fast ? delta_finish<2>(dt, dr[p], vs) : delta_col(lora, dt, col_of(i)))));
+      raw[i] = v;
+    }
+  }
+  __syncthreads();
   for (int i = tid; i < half; i += NT) {
     const float c = cr[i], sn = sr[i];
-    const float q1 = to_f32(row[h * D + i]), q2 = to_f32(row[h * D + i + half]);
+    const float q1 = raw[i], q2 = raw[i + half];
     // q is rounded to T exactly as the unfused path stores it before attention reads it back
     qs[i] = to_f32(from_f32<T>(q1 * c - q2 * sn)) * scale_log2;
     qs[i + half] = to_f32(from_f32<T>(q2 * c + q1 * sn)) * scale_log2;
-    const float k1 = to_f32(row[(H + hk) * D + i]), k2 = to_f32(row[(H + hk) * D + i + half]);
+    const float k1 = raw[D + i], k2 = raw[D + i + half];
     const T r1 = from_f32<T>(k1 * c - k2 * sn), r2 = from_f32<T>(k2 * c + k1 * sn);
     kn[i] = to_f32(r1);
     kn[i + half] = to_f32(r2);
@@ -297,14 +416,12 @@ rope_attn_decode_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv,
     }
   }
   for (int i = tid; i < D; i += NT) {
-    const T v = row[(H + Hkv + hk) * D + i];
+    const T v = from_f32<T>(raw[2 * D + i]);
     vn[i] = to_f32(v);
     if (h % group == 0) vdst[i] = v;
   }
   __syncthreads();
 
-  const T* kbase = kc + ((size_t)seq * Hkv + hk) * max_ctx * D;
-  const T* vbase = vc + ((size_t)seq * Hkv + hk) * max_ctx * D;
   // the new key first: its score seeds the running max
   float s_new = 0.f;
   {
@@ -319,19 +436,10 @@ rope_attn_decode_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv,
   float m = s_new, l = 1.f;
   const int dd = tid % D, kp = tid / D;   // P.V: dim dd over key partition kp
   float acc = kp == 0 ? vn[dd] : 0.f;     // p_new = exp2(s_new - m) = 1
-  const int n_cached = pos;
   for (int k0 = 0; k0 < n_cached; k0 += KB) {
     const int nk = min(KB, n_cached - k0);
-    for (int e = tid; e < nk * CH; e += NT) {
-      const int r = e / CH, c = e % CH;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                       static_cast<uint32_t>(__cvta_generic_to_shared(Ks + r * DP + c * VEC))),
-                   "l"(kbase + (size_t)(k0 + r) * D + c * VEC) : "memory");
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                       static_cast<uint32_t>(__cvta_generic_to_shared(Vs + r * DP + c * VEC))),
-                   "l"(vbase + (size_t)(k0 + r) * D + c * VEC) : "memory");
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    if (k0 > 0) load_block(k0, nk);   // block 0 was issued before the PDL wait
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     // scores: thread = key (KB <= 128 threads)
     float sc = -INFINITY;
@@ -536,6 +644,22 @@ extern "C" int slx_rmsnorm(int dtype, void* out, int ldo, const void* x, int ldx
   return st;
 }
 
+extern "C" int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx, const void* w,
+                                int n_tok, int d, float eps, const slx_lora_delta* lora,
+                                void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && d > 0 && d % 8 == 0 && ldo % 8 == 0 && ldx % 8 == 0 && ldo >= d &&
+                ldx >= d && out && x && w && delta_valid(lora));
+  SLX_CHECK_ALIGN(out, 16);
+  SLX_CHECK_ALIGN(x, 16);
+  SLX_CHECK_ALIGN(w, 16);
+  if (n_tok == 0) return SLX_OK;
+  const DeltaArgs la = delta_args(lora);
+  int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
+  int st = SLX_OK;
+  DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_kernel<T>, dim3(n_tok), dim3(threads), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la));
+  return st;
+}
+
 extern "C" int slx_rope_kv_write(int dtype, void* qkv, int ld_qkv, int n_tok, int heads,
                                  int kv_heads, int head_dim, const int32_t* tok_pos,
                                  const int32_t* tok_seq, const float* cos_tab,
@@ -619,7 +743,8 @@ template <typename T, int D>
 static int launch_rope_attn(void* out, int ldo, const void* qkv, int ld_qkv, int n_tok, int heads,
                             int kv_heads, const int32_t* tok_pos, const int32_t* tok_seq,
                             const float* cos_tab, const float* sin_tab, void* k_cache,
-                            void* v_cache, int max_ctx, float scale, cudaStream_t s) {
+                            void* v_cache, int max_ctx, float scale, const DeltaArgs& lora,
+                            cudaStream_t s) {
   auto k = rope_attn_decode_kernel<T, D>;
   static bool configured = false;
   if (!configured) {
@@ -631,7 +756,35 @@ static int launch_rope_attn(void* out, int ldo, const void* qkv, int ld_qkv, int
   }
   return launch_ex(k, dim3((unsigned)n_tok * heads), dim3(128), dec_smem<T, D>(), s, 1u, (T*)out,
                    ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab,
-                   (T*)k_cache, (T*)v_cache, max_ctx, scale);
+                   (T*)k_cache, (T*)v_cache, max_ctx, scale, lora);
+}
+
+extern "C" int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, const void* qkv,
+                                              int ld_qkv, int n_tok, int heads, int kv_heads,
+                                              int head_dim, const int32_t* tok_pos,
+                                              const int32_t* tok_seq, const float* cos_tab,
+                                              const float* sin_tab, int max_pos, void* k_cache,
+                                              void* v_cache, int max_ctx,
+                                              const slx_lora_delta* lora, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && heads > 0 && kv_heads > 0 && heads % kv_heads == 0 &&
+                ld_qkv >= (heads + 2 * kv_heads) * head_dim && ldo >= heads * head_dim && out &&
+                qkv && tok_pos && tok_seq && cos_tab && sin_tab && k_cache && v_cache &&
+                max_pos > 0 && max_ctx > 0);
+  SLX_CHECK_ARG(ldo % 8 == 0 && ld_qkv % 8 == 0 && delta_valid(lora));
+  SLX_CHECK_ALIGN(k_cache, 16);
+  SLX_CHECK_ALIGN(v_cache, 16);
+  if (head_dim != 64 && head_dim != 128) return SLX_ERR_UNSUPPORTED;
+  if (n_tok == 0) return SLX_OK;
+  const float scale = 1.4426950408889634f / sqrtf((float)head_dim);
+  const DeltaArgs la = delta_args(lora);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == SLX_DT_BF16)
+    return head_dim == 64 ? launch_rope_attn<bf16, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, s)
+                          : launch_rope_attn<bf16, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, s);
+  if (dtype == SLX_DT_F32)
+    return head_dim == 64 ? launch_rope_attn<float, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, s)
+                          : launch_rope_attn<float, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, s);
+  return SLX_ERR_INVALID;
 }
 
 extern "C" int slx_rope_attention_decode(int dtype, void* out, int ldo, const void* qkv,
@@ -640,22 +793,7 @@ extern "C" int slx_rope_attention_decode(int dtype, void* out, int ldo, const vo
                                          const int32_t* tok_seq, const float* cos_tab,
                                          const float* sin_tab, int max_pos, void* k_cache,
                                          void* v_cache, int max_ctx, void* stream) {
-  SLX_CHECK_ARG(n_tok >= 0 && heads > 0 && kv_heads > 0 && heads % kv_heads == 0 &&
-                ld_qkv >= (heads + 2 * kv_heads) * head_dim && ldo >= heads * head_dim && out &&
-                qkv && tok_pos && tok_seq && cos_tab && sin_tab && k_cache && v_cache &&
-                max_pos > 0 && max_ctx > 0);
-  SLX_CHECK_ARG(ldo % 8 == 0 && ld_qkv % 8 == 0);
-  SLX_CHECK_ALIGN(k_cache, 16);
-  SLX_CHECK_ALIGN(v_cache, 16);
-  if (head_dim != 64 && head_dim != 128) return SLX_ERR_UNSUPPORTED;
-  if (n_tok == 0) return SLX_OK;
-  const float scale = 1.4426950408889634f / sqrtf((float)head_dim);
-  cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == SLX_DT_BF16)
-    return head_dim == 64 ? launch_rope_attn<bf16, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, s)
-                          : launch_rope_attn<bf16, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, s);
-  if (dtype == SLX_DT_F32)
-    return head_dim == 64 ? launch_rope_attn<float, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, s)
-                          : launch_rope_attn<float, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, s);
-  return SLX_ERR_INVALID;
+  return slx_rope_attention_decode_lora(dtype, out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads,
+                                        head_dim, tok_pos, tok_seq, cos_tab, sin_tab, max_pos,
+                                        k_cache, v_cache, max_ctx, nullptr, stream);
 }

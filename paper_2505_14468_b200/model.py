@@ -192,6 +192,8 @@ class MultiLoraModel:
             if "o" in self.targets:
                 self.stack["wo"] = ("o",)
         self.use_stacked_decode = bool(self.stack)
+        # decode: q/k/v expand fused into the attention kernel, o expand into the post-norm
+        self.fuse_expand = True
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
         self.pool.on_install = self._stack_install
         self.pool.on_evict = self._stack_evict
@@ -412,6 +414,15 @@ class MultiLoraModel:
         ops.lora_expand(y, v_all, self.pool.rank, self.pool.scale, self.pool.max_rank,
                         ops.make_targets(specs), offs, self.lora_ws)
 
+    def _delta(self, layer: int, proj: str, v_all, slot, cols):
+        """slx_lora_delta of the stacked targets of ``proj`` (fused decode expand)."""
+        tg = []
+        for t in self.stack[proj]:
+            i = self.targets.index(t)
+            tg.append((self.pool.b_ptr[layer, i], self._stack_rows(proj, t, 0), cols[t][0],
+                       self.cfg.target_dims(t)[1]))
+        return ops.make_delta(v_all, slot, self.pool.rank, self.pool.scale, self.pool.max_rank, tg)
+
     @staticmethod
     def segments_of(pos, seq) -> list:
         """Host (tok0, n, seq, pos0) runs of consecutive positions of one sequence."""
@@ -464,9 +475,13 @@ class MultiLoraModel:
         for l in range(cfg.layers):
             p = f"layers.{l}."
             ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
+            d_qkv = None
             if stacked and "w_qkv" in self.stack:
                 ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv)
-                self._expand(qkv, v_qkv, l, "w_qkv", qkv_cols)
+                if decode and self.fuse_expand:
+                    d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
+                else:
+                    self._expand(qkv, v_qkv, l, "w_qkv", qkv_cols)
             else:
                 self._gemm(h, w[p + "w_qkv"], qkv)
                 if not (sgmv_plan is not None and
@@ -474,7 +489,8 @@ class MultiLoraModel:
                     self._lora(qkv, h, l, ("q", "k", "v"), qkv_cols)
             if decode:
                 ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos,
-                                          seq, self.cos, self.sin, self.k_cache[l], self.v_cache[l])
+                                          seq, self.cos, self.sin, self.k_cache[l], self.v_cache[l],
+                                          lora=d_qkv)
             else:
                 ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
                                   self.sin, self.k_cache[l], self.v_cache[l])
@@ -484,15 +500,22 @@ class MultiLoraModel:
                 else:
                     ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
                                   self.k_cache[l], self.v_cache[l])
+            d_o = None
             if stacked and "wo" in self.stack:
                 ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o)
-                self._expand(x, v_o, l, "wo", {"o": (0, d, d)})
+                if decode and self.fuse_expand:
+                    d_o = self._delta(l, "wo", v_o, slot, {"o": (0, d, d)})
+                else:
+                    self._expand(x, v_o, l, "wo", {"o": (0, d, d)})
             else:
                 self._gemm(attn, w[p + "wo"], x, residual=x)
                 if not (sgmv_plan is not None and
                         self._sgmv_tc(x, attn, l, ("o",), {"o": (0, d, d)}, sgmv_plan, v_buf)):
                     self._lora(x, attn, l, ("o",), {"o": (0, d, d)})
-            ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
+            if d_o is not None:
+                ops.rmsnorm_lora(h, x, w[p + "post_norm"], cfg.rms_eps, d_o)
+            else:
+                ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
             if fused_silu:
                 self._gemm(h, w[p + "w_gu"], mlp, silu=True)
             else:

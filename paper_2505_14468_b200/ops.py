@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import (DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED,
-                   LoraTarget, check)
+                   LoraDelta, LoraTarget, check)
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
 
@@ -336,6 +336,31 @@ def rmsnorm(out, x, w, eps: float):
     return out
 
 
+def make_delta(v_all: torch.Tensor, tok_slot, slot_rank, slot_scale, max_rank: int, targets):
+    """slx_lora_delta for a fused decode expand.  targets: [(b_ptr_table, v_col_off, y_col_off,
+    d_out)] (<= 4); v_all: the fp32 GEMM side output [n_tok, ldv]."""
+    targets = list(targets)
+    if not 1 <= len(targets) <= 4 or v_all.dtype != torch.float32:
+        raise ValueError("make_delta: 1..4 targets and an fp32 v_all")
+    d = LoraDelta()
+    d.v, d.ldv = v_all.data_ptr(), _ld(v_all)
+    d.tok_slot, d.slot_rank, d.slot_scale = tok_slot.data_ptr(), slot_rank.data_ptr(), slot_scale.data_ptr()
+    d.max_rank, d.n_targets = max_rank, len(targets)
+    for i, (b, voff, yoff, dout) in enumerate(targets):
+        d.b_ptrs[i], d.v_col_off[i], d.y_col_off[i], d.d_out[i] = b.data_ptr(), voff, yoff, dout
+    return d
+
+
+@_op("rmsnorm", 1)
+def rmsnorm_lora(out, x, w, eps: float, delta):
+    """x += LoRA delta (fused o-projection expand, written back), out = rmsnorm(x)."""
+    check(_lib.load().slx_rmsnorm_lora(_dt(out), _ptr(out), _ld(out), _ptr(x), _ld(x), _ptr(w),
+                                       x.shape[0], w.numel(), float(eps),
+                                       None if delta is None else ctypes.byref(delta), _stream()),
+          "slx_rmsnorm_lora")
+    return out
+
+
 @_op("rope_kv", 1)
 def rope_kv_write(qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos, sin, k_cache, v_cache):
     check(_lib.load().slx_rope_kv_write(_dt(qkv), _ptr(qkv), _ld(qkv), qkv.shape[0], heads,
@@ -356,13 +381,14 @@ def attention(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, k_cache, v_
 
 @_op("attention", 1)
 def rope_attention_decode(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos, sin,
-                          k_cache, v_cache):
+                          k_cache, v_cache, lora=None):
     """Decode-step RoPE + KV append + attention in one kernel (each token = next position of
-    its own sequence)."""
-    check(_lib.load().slx_rope_attention_decode(
+    its own sequence); ``lora`` (make_delta) fuses the q/k/v LoRA expand."""
+    check(_lib.load().slx_rope_attention_decode_lora(
         _dt(out), _ptr(out), _ld(out), _ptr(qkv), _ld(qkv), qkv.shape[0], heads, kv_heads, head_dim,
         _ptr(tok_pos), _ptr(tok_seq), _ptr(cos), _ptr(sin), cos.shape[0], _ptr(k_cache),
-        _ptr(v_cache), k_cache.shape[2], _stream()), "slx_rope_attention_decode")
+        _ptr(v_cache), k_cache.shape[2], None if lora is None else ctypes.byref(lora), _stream()),
+        "slx_rope_attention_decode")
     return out
 
 

@@ -68,10 +68,13 @@ def test_gemm_decode_tilings(M, bn, gsplit, ctas, splits, monkeypatch):
 
 @pytest.mark.parametrize("M", [1, 17, 64])
 @pytest.mark.parametrize("N,K", [(3072, 4096), (4608, 4096), (1000, 11008), (32000, 1024)])
-@pytest.mark.parametrize("ctas,min_units", [(0, 4), (37, 4), (5, 4), (1, 1), (0, 1)])
-def test_gemm_stream_k(M, N, K, ctas, min_units, monkeypatch):
+@pytest.mark.parametrize("ctas,min_units,cluster", [(0, 4, 1), (0, 4, 0), (37, 4, 1), (5, 4, 1),
+                                                     (1, 1, 1), (0, 1, 1)])
+def test_gemm_stream_k(M, N, K, ctas, min_units, cluster, monkeypatch):
     """Stream-K decode GEMM (M <= 64): every range split (whole tiles, tail/head pieces, up to
-    dozens of pieces per tile) gives the fp32 result; epilogues residual / SiLU / side output."""
+    dozens of pieces per tile; uniform splits reduced in DSMEM clusters or through global
+    memory) gives the fp32 result; epilogues residual / SiLU / side output."""
+    monkeypatch.setenv("SLX_SK_CLUSTER", str(cluster))
     monkeypatch.setenv("SLX_SK_CTAS", str(ctas))
     monkeypatch.setenv("SLX_SK_MIN_UNITS", str(min_units))
     g = torch.Generator(device=DEV).manual_seed(M + N + K + ctas)

@@ -121,11 +121,15 @@ def test_bf16_stacked_decode_shrink_matches_sgmv_path(golden):
     seqs, _ = m.prefill(prompts, ids)
     toks = [11, 12, 13, 14]
     got = {}
-    for stacked in (True, False):
-        m.use_stacked_decode = stacked
+    for stacked, fuse in ((True, True), (True, False), (False, False)):
+        m.use_stacked_decode, m.fuse_expand = stacked, fuse
         for s_ in seqs:
             m.seq_len[s_] = len(prompts[seqs.index(s_)])
-        got[stacked] = m.decode(seqs, toks, ids).cpu().numpy()
+        got[(stacked, fuse)] = m.decode(seqs, toks, ids).cpu().numpy()
+    m.fuse_expand = True
+    # the expand fused into attention / post-norm rounds exactly like the expand kernel
+    np.testing.assert_array_equal(got[(True, True)], got[(True, False)])
+    got[True], got[False] = got[(True, True)], got[(False, False)]
     np.testing.assert_allclose(got[True], got[False], rtol=1e-2, atol=1e-2)
     orc = OracleModel(cfg, w, ads, [lo.scale for lo in loras], loras[0].targets)
     orc.prefill(prompts, ids)
