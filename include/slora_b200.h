@@ -86,6 +86,19 @@ SLX_API size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 SLX_API int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
                   int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes, void* stream);
+/* L2 prefetch hint: up to two device regions the NEXT kernel on the stream streams first.  A
+ * kernel that takes one issues cp.async.bulk.prefetch.L2 of them (split over its CTAs) as soon
+ * as its own HBM stream has been issued, so HBM stays busy across the kernel boundary (its
+ * epilogue, the next launch and the next prologue) and the next kernel starts from L2. */
+typedef struct slx_l2_prefetch {
+  const void* ptr[2];
+  size_t bytes[2];
+} slx_l2_prefetch;
+/* slx_gemm_bf16 + an L2 prefetch hint for the next kernel (pf may be NULL). */
+SLX_API int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
+                  const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
+                  int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes,
+                  const slx_l2_prefetch* pf, void* stream);
 /* Debug only: following slx_gemm_bf16 launches write 16 u64 globaltimer slots per CTA into
  * the device buffer `buf` (phase timeline: entry, prologue, past PDL wait, first stage landed,
  * last MMA issued, accumulator ready, split-K reduction start, exit, reduction end, segment
@@ -222,6 +235,12 @@ SLX_API int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, const 
                   const int32_t* tok_pos, const int32_t* tok_seq, const float* cos_tab,
                   const float* sin_tab, int max_pos, void* k_cache, void* v_cache, int max_ctx,
                   const slx_lora_delta* lora, void* stream);
+/* Same + L2 prefetch hint for the next kernel (issued by the last wave of CTAs; pf may be NULL). */
+SLX_API int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const void* qkv,
+                  int ld_qkv, int n_tok, int heads, int kv_heads, int head_dim,
+                  const int32_t* tok_pos, const int32_t* tok_seq, const float* cos_tab,
+                  const float* sin_tab, int max_pos, void* k_cache, void* v_cache, int max_ctx,
+                  const slx_lora_delta* lora, const slx_l2_prefetch* pf, void* stream);
 /* Prefill (tensor cores, mma.sync flash attention, head_dim 128, bf16): `tiles` is a device
  * array of n_tiles {int tok0, nq, seq, pos0} (<= 64 queries of one segment each, size
  * slx_flash_prefill_tile_bytes()); query t of a tile attends cache positions 0..pos0+t of

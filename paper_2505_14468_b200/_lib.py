@@ -47,6 +47,11 @@ class LoraDelta(ctypes.Structure):
                 ("y_col_off", _i * 4), ("d_out", _i * 4)]
 
 
+class L2Prefetch(ctypes.Structure):
+    """slx_l2_prefetch: the next kernel's first bytes (two regions)."""
+    _fields_ = [("ptr", _p * 2), ("bytes", _sz * 2)]
+
+
 # name -> (restype, argtypes): every symbol declared in include/slora_b200.h
 SIGNATURES = {
     "slx_status_string": (ctypes.c_char_p, [_i]),
@@ -56,6 +61,8 @@ SIGNATURES = {
     "slx_gemm_bf16": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p, _sz,
                            _p]),
     "slx_debug_gemm_trace": (_i, [_p]),
+    "slx_gemm_bf16_pf": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p,
+                              _sz, ctypes.POINTER(L2Prefetch), _p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),
     "slx_gemm_group_tile_bytes": (_sz, []),
     "slx_gemm_grouped_bf16": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p, _i, _i,
@@ -83,6 +90,9 @@ SIGNATURES = {
                                        _i, _p]),
     "slx_rope_attention_decode_lora": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i,
                                             _p, _p, _i, ctypes.POINTER(LoraDelta), _p]),
+    "slx_rope_attention_decode_pf": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i,
+                                          _p, _p, _i, ctypes.POINTER(LoraDelta),
+                                          ctypes.POINTER(L2Prefetch), _p]),
     "slx_flash_prefill_tile_bytes": (_sz, []),
     "slx_attention_prefill": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _i, _p, _p, _i, _p]),
     "slx_silu_mul_blocked": (_i, [_i, _p, _i, _p, _i, _i, _i, _p]),

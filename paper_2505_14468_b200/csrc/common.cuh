@@ -246,6 +246,39 @@ __device__ __forceinline__ float delta_col(const DeltaArgs& d, const DeltaTok& k
 }
 }  // namespace slx
 
+// ---------------------------------------------------------------- L2 prefetch (slx_l2_prefetch)
+namespace slx {
+struct PfArgs {
+  const char* ptr[2];
+  unsigned long long bytes[2];
+};
+inline PfArgs pf_args(const slx_l2_prefetch* p) {
+  PfArgs a{};
+  if (p == nullptr) return a;
+  for (int i = 0; i < 2; ++i) {
+    a.ptr[i] = static_cast<const char*>(p->ptr[i]);
+    a.bytes[i] = p->ptr[i] ? (p->bytes[i] & ~15ull) : 0;
+  }
+  return a;
+}
+// Part `part` of `parts` of both regions, as bulk L2 prefetches of <= 64 KB (one thread).
+__device__ __forceinline__ void l2_prefetch_part(const PfArgs& pf, int part, int parts) {
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const unsigned long long n = pf.bytes[r];
+    if (n == 0) continue;
+    const unsigned long long per = ((n + parts - 1) / parts + 15) & ~15ull;
+    unsigned long long lo = per * part, hi = lo + per;
+    hi = hi > n ? n : hi;
+    for (unsigned long long o = lo; o < hi; o += 65536) {
+      const unsigned sz = (unsigned)((hi - o) < 65536 ? (hi - o) : 65536);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf.ptr[r] + o), "r"(sz)
+                   : "memory");
+    }
+  }
+}
+}  // namespace slx
+
 // ---------------------------------------------------------------- launch plumbing (PDL + clusters)
 namespace slx {
 

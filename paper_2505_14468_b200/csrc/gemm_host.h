@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <stddef.h>
 
+#include "../../include/slora_b200.h"
+
 namespace slx {
 // K-major bf16 matrix [rows, cols] with row stride ld (elements); TMA box = box_rows x 64,
 // SWIZZLE_128B (the tcgen05 smem descriptor layout).
@@ -18,6 +20,7 @@ struct SkCall {
   const void* A; int lda; const void* W; void* C; int ldc; int c_dtype;
   const void* R; int ldr; int M, N, K, epilogue, n_main; void* C2; int ldc2;
   void* ws; size_t ws_bytes; void* stream; unsigned long long* trace;
+  const slx_l2_prefetch* pf;
 };
 int gemm_sk_launch(const SkCall& c);
 size_t gemm_sk_workspace_bytes(int M, int N, int K);

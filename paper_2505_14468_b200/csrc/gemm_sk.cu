@@ -61,6 +61,7 @@ struct SkArgs {
   float* part;   // [n_tiles][pmax][16 chunks][bm][16] fp32 pieces
   uint32_t* cnt; // [n_tiles][2]: arrivals, departures (monotonic; A == D between launches)
   unsigned long long* trace;
+  PfArgs pf;     // L2 prefetch of the next kernel's first bytes, after our last TMA issue
 };
 
 __device__ __forceinline__ unsigned long long sk_timer() {
@@ -210,6 +211,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
         load_w(i, st, &full[s]);
         load_x(i, st, &full[s]);
       }
+      l2_prefetch_part(g.pf, c, g.G);   // keep HBM busy across the kernel boundary
     }
     __syncwarp();   // reconverge before the CTA-wide barrier at the end
   } else if (warp == 1) {
@@ -671,6 +673,7 @@ int gemm_sk_launch(const SkCall& c) {
   a.cnt = (uint32_t*)c.ws;
   a.part = (float*)((char*)c.ws + SK_PART_OFF);
   a.trace = c.trace;
+  a.pf = pf_args(c.pf);
   CUtensorMap mx, mw;
   const int w_rows = ceil_div(c.N, 128) * p.kblocks * 128;
   if (!make_tmap(&mx, c.A, c.M, c.K, c.lda, p.bm) || !make_tmap(&mw, c.W, w_rows, SK_BK, SK_BK, 128))

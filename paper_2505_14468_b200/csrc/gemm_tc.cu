@@ -652,6 +652,15 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
                              const void* R, int ldr, int M, int N, int K, int epilogue,
                              int w_layout, int n_main, void* C2, int ldc2, void* ws,
                              size_t ws_bytes, void* stream) {
+  return slx_gemm_bf16_pf(A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, w_layout, n_main,
+                          C2, ldc2, ws, ws_bytes, nullptr, stream);
+}
+
+extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, int ldc,
+                                int c_dtype, const void* R, int ldr, int M, int N, int K,
+                                int epilogue, int w_layout, int n_main, void* C2, int ldc2,
+                                void* ws, size_t ws_bytes, const slx_l2_prefetch* pf,
+                                void* stream) {
   SLX_CHECK_ARG(w_layout == SLX_W_ROWMAJOR || w_layout == SLX_W_TILED);
   SLX_CHECK_ARG(A && W && C && M >= 0 && N > 0 && K > 0 && lda >= K && K % 8 == 0 &&
                 lda % 8 == 0 && ldc % 8 == 0);
@@ -678,7 +687,7 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
   if (ws) SLX_CHECK_ALIGN(ws, 256);
   if (w_layout == SLX_W_TILED) {   // decode: stream-K kernel (gemm_sk.cu) when it applies
     SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
-              ws, ws ? ws_bytes : 0, stream, g_trace};
+              ws, ws ? ws_bytes : 0, stream, g_trace, pf};
     const int st = gemm_sk_launch(sc);
     if (st != SLX_ERR_UNSUPPORTED) return st;
   }

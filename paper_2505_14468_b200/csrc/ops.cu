@@ -3,10 +3,22 @@
 // All templated on the activation type (bf16 throughput mode / fp32 parity mode); weights
 // are always bf16 and accumulation is always fp32.
 #include <float.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
 namespace slx {
+
+int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int n_tok, int heads,
+                            int head_dim, const int32_t* tok_pos, const int32_t* tok_seq,
+                            const float* cos_tab, const float* sin_tab, void* k_cache,
+                            void* v_cache, int max_ctx, float scale_log2, const DeltaArgs& lora,
+                            const PfArgs& pf, cudaStream_t stream);   // attn_decode.cu
+
+static bool attn_pipe_enabled() {   // SLX_ATTN_PIPE=0: the per-(token, head) kernel (A/B tests)
+  const char* e = getenv("SLX_ATTN_PIPE");
+  return !(e && e[0] == '0');
+}
 
 // ------------------------------------------------------------------ embedding
 template <typename T>
@@ -316,7 +328,7 @@ rope_attn_decode_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv,
                         int Hkv, const int32_t* __restrict__ tok_pos,
                         const int32_t* __restrict__ tok_seq, const float* __restrict__ cos_tab,
                         const float* __restrict__ sin_tab, T* __restrict__ kc, T* __restrict__ vc,
-                        int max_ctx, float scale_log2, DeltaArgs lora) {
+                        int max_ctx, float scale_log2, DeltaArgs lora, PfArgs pf, int pf_from) {
   constexpr int KB = DecCfg<T>::KB;
   constexpr int VEC = 16 / sizeof(T);
   constexpr int DP = D + VEC;          // padded smem row
@@ -360,6 +372,9 @@ rope_attn_decode_kernel(T* __restrict__ out, int ldo, const T* __restrict__ qkv,
   };
   const int n_cached = pos;
   if (n_cached > 0) load_block(0, min(KB, n_cached));
+  // the last wave prefetches the next kernel's first bytes into L2 (HBM busy across the boundary)
+  if (tid == 0 && (int)blockIdx.x >= pf_from)
+    l2_prefetch_part(pf, blockIdx.x - pf_from, gridDim.x - pf_from);
   const bool fast = dt.slot >= 0 && dt.rank <= 16;
   DeltaRow<2> dr[PER];
   auto col_of = [&](int i) {
@@ -744,7 +759,7 @@ static int launch_rope_attn(void* out, int ldo, const void* qkv, int ld_qkv, int
                             int kv_heads, const int32_t* tok_pos, const int32_t* tok_seq,
                             const float* cos_tab, const float* sin_tab, void* k_cache,
                             void* v_cache, int max_ctx, float scale, const DeltaArgs& lora,
-                            cudaStream_t s) {
+                            const PfArgs& pf, cudaStream_t s) {
   auto k = rope_attn_decode_kernel<T, D>;
   static bool configured = false;
   if (!configured) {
@@ -756,7 +771,8 @@ static int launch_rope_attn(void* out, int ldo, const void* qkv, int ld_qkv, int
   }
   return launch_ex(k, dim3((unsigned)n_tok * heads), dim3(128), dec_smem<T, D>(), s, 1u, (T*)out,
                    ldo, (const T*)qkv, ld_qkv, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab,
-                   (T*)k_cache, (T*)v_cache, max_ctx, scale, lora);
+                   (T*)k_cache, (T*)v_cache, max_ctx, scale, lora, pf,
+                   max(0, n_tok * heads - 3 * sm_count()));
 }
 
 extern "C" int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, const void* qkv,
@@ -766,6 +782,19 @@ extern "C" int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, con
                                               const float* sin_tab, int max_pos, void* k_cache,
                                               void* v_cache, int max_ctx,
                                               const slx_lora_delta* lora, void* stream) {
+  return slx_rope_attention_decode_pf(dtype, out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads,
+                                      head_dim, tok_pos, tok_seq, cos_tab, sin_tab, max_pos,
+                                      k_cache, v_cache, max_ctx, lora, nullptr, stream);
+}
+
+extern "C" int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const void* qkv,
+                                            int ld_qkv, int n_tok, int heads, int kv_heads,
+                                            int head_dim, const int32_t* tok_pos,
+                                            const int32_t* tok_seq, const float* cos_tab,
+                                            const float* sin_tab, int max_pos, void* k_cache,
+                                            void* v_cache, int max_ctx,
+                                            const slx_lora_delta* lora, const slx_l2_prefetch* pf,
+                                            void* stream) {
   SLX_CHECK_ARG(n_tok >= 0 && heads > 0 && kv_heads > 0 && heads % kv_heads == 0 &&
                 ld_qkv >= (heads + 2 * kv_heads) * head_dim && ldo >= heads * head_dim && out &&
                 qkv && tok_pos && tok_seq && cos_tab && sin_tab && k_cache && v_cache &&
@@ -777,13 +806,18 @@ extern "C" int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, con
   if (n_tok == 0) return SLX_OK;
   const float scale = 1.4426950408889634f / sqrtf((float)head_dim);
   const DeltaArgs la = delta_args(lora);
+  const PfArgs pa = pf_args(pf);
   cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == SLX_DT_BF16 && heads == kv_heads && attn_pipe_enabled() && ld_qkv % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(qkv) & 15) == 0)
+    return attn_decode_pipe_launch(out, ldo, qkv, ld_qkv, n_tok, heads, head_dim, tok_pos, tok_seq,
+                                   cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s);
   if (dtype == SLX_DT_BF16)
-    return head_dim == 64 ? launch_rope_attn<bf16, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, s)
-                          : launch_rope_attn<bf16, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, s);
+    return head_dim == 64 ? launch_rope_attn<bf16, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s)
+                          : launch_rope_attn<bf16, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s);
   if (dtype == SLX_DT_F32)
-    return head_dim == 64 ? launch_rope_attn<float, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, s)
-                          : launch_rope_attn<float, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, s);
+    return head_dim == 64 ? launch_rope_attn<float, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s)
+                          : launch_rope_attn<float, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s);
   return SLX_ERR_INVALID;
 }
 

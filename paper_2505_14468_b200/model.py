@@ -16,6 +16,7 @@ Two activation modes share the same packed bf16 weights:
 from __future__ import annotations
 
 import math
+import os
 
 import numpy as np
 import torch
@@ -194,6 +195,9 @@ class MultiLoraModel:
         self.use_stacked_decode = bool(self.stack)
         # decode: q/k/v expand fused into the attention kernel, o expand into the post-norm
         self.fuse_expand = True
+        # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off)
+        self.l2_prefetch_mb = float(os.environ.get("SLX_L2_PF_MB", "32"))
+        self._pf_cache: dict = {}
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
         self.pool.on_install = self._stack_install
         self.pool.on_evict = self._stack_evict
@@ -327,10 +331,11 @@ class MultiLoraModel:
         self.free_seqs.append(s)
 
     # ------------------------------------------------------------------ forward
-    def _gemm(self, a, w, out=None, residual=None, silu=False, out_dtype=None):
+    def _gemm(self, a, w, out=None, residual=None, silu=False, out_dtype=None, prefetch=None):
         if self.dtype == torch.bfloat16:
             epi = EPI_SILU_MUL if silu else (EPI_RESIDUAL if residual is not None else 0)
-            return ops.gemm(a, w, out, epilogue=epi, residual=residual, out_dtype=out_dtype)
+            return ops.gemm(a, w, out, epilogue=epi, residual=residual, out_dtype=out_dtype,
+                            prefetch=prefetch)
         assert not silu
         return ops.gemm_f32(a, w, out, residual=residual)
 
@@ -414,6 +419,15 @@ class MultiLoraModel:
         ops.lora_expand(y, v_all, self.pool.rank, self.pool.scale, self.pool.max_rank,
                         ops.make_targets(specs), offs, self.lora_ws)
 
+    def _pf(self, key, *tensors):
+        """Cached slx_l2_prefetch of the first l2_prefetch_mb MB (split over the tensors)."""
+        if self.l2_prefetch_mb <= 0:
+            return None
+        if key not in self._pf_cache:
+            n = int(self.l2_prefetch_mb * (1 << 20)) // len(tensors)
+            self._pf_cache[key] = ops.l2_prefetch(*[(getattr(t, "data", t), n) for t in tensors])
+        return self._pf_cache[key]
+
     def _delta(self, layer: int, proj: str, v_all, slot, cols):
         """slx_lora_delta of the stacked targets of ``proj`` (fused decode expand)."""
         tg = []
@@ -476,8 +490,15 @@ class MultiLoraModel:
             p = f"layers.{l}."
             ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
             d_qkv = None
+            pfd = decode and dt == torch.bfloat16
+            nxt = f"layers.{l + 1}.w_qkv" if l + 1 < cfg.layers else "lm_head"
+            pf_qkv = self._pf(("kv", l), self.k_cache[l], self.v_cache[l]) if pfd else None
+            pf_att = self._pf(p + "wo", w[p + "wo"]) if pfd else None
+            pf_o = self._pf(p + "w_gu", w[p + "w_gu"]) if pfd else None
+            pf_gu = self._pf(p + "w_down", w[p + "w_down"]) if pfd else None
+            pf_dn = self._pf(nxt, w[nxt]) if pfd else None
             if stacked and "w_qkv" in self.stack:
-                ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv)
+                ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv, prefetch=pf_qkv)
                 if decode and self.fuse_expand:
                     d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
                 else:
@@ -490,7 +511,7 @@ class MultiLoraModel:
             if decode:
                 ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos,
                                           seq, self.cos, self.sin, self.k_cache[l], self.v_cache[l],
-                                          lora=d_qkv)
+                                          lora=d_qkv, prefetch=pf_att)
             else:
                 ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
                                   self.sin, self.k_cache[l], self.v_cache[l])
@@ -502,7 +523,8 @@ class MultiLoraModel:
                                   self.k_cache[l], self.v_cache[l])
             d_o = None
             if stacked and "wo" in self.stack:
-                ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o)
+                ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o,
+                         prefetch=pf_o)
                 if decode and self.fuse_expand:
                     d_o = self._delta(l, "wo", v_o, slot, {"o": (0, d, d)})
                 else:
@@ -517,12 +539,12 @@ class MultiLoraModel:
             else:
                 ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
             if fused_silu:
-                self._gemm(h, w[p + "w_gu"], mlp, silu=True)
+                self._gemm(h, w[p + "w_gu"], mlp, silu=True, prefetch=pf_gu)
             else:
                 self._gemm(h, w[p + "w_gu"], gu)
                 self._lora(gu, h, l, ("gate", "up"), {"gate": (0, 128, 256), "up": (128, 128, 256)})
                 ops.silu_mul_blocked(mlp, gu, self.ffn_pad)
-            self._gemm(mlp, w[p + "w_down"], x, residual=x)
+            self._gemm(mlp, w[p + "w_down"], x, residual=x, prefetch=pf_dn)
             self._lora(x, mlp, l, ("down",), {"down": (0, d, d)}, d_in=cfg.ffn)
         rows = x if logit_rows is None else x.index_select(0, logit_rows)
         hn = torch.empty_like(rows)

@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import (DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED,
-                   LoraDelta, LoraTarget, check)
+                   L2Prefetch, LoraDelta, LoraTarget, check)
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
 
@@ -170,14 +170,29 @@ def pack_rows(pw: PackedWeight, src: torch.Tensor | None, n_rows: int, row0: int
                                            _stream()), "slx_pack_weight_rows")
 
 
+def l2_prefetch(*regions) -> L2Prefetch | None:
+    """slx_l2_prefetch of up to two (tensor, nbytes) regions the next kernel streams first."""
+    regions = [r for r in regions if r is not None and r[1] > 0]
+    if not regions:
+        return None
+    if len(regions) > 2:
+        raise ValueError("l2_prefetch: at most two regions")
+    pf = L2Prefetch()
+    for i, (t, n) in enumerate(regions):
+        pf.ptr[i] = t.data_ptr()
+        pf.bytes[i] = min(int(n), t.numel() * t.element_size())
+    return pf
+
+
 @_op("gemm", 1)
 def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
          epilogue: int = EPI_NONE, residual: torch.Tensor | None = None,
-         out_dtype: torch.dtype | None = None, ws=None, side: torch.Tensor | None = None
-         ) -> torch.Tensor:
+         out_dtype: torch.dtype | None = None, ws=None, side: torch.Tensor | None = None,
+         prefetch: L2Prefetch | None = None) -> torch.Tensor:
     """bf16 tcgen05 GEMM: out = a @ w.T (+ residual | silu*mul of blocked gate/up).
     ``w`` is a row-major bf16 [N, K] tensor or a :class:`PackedWeight`; with ``side`` (fp32
-    [M, n_extra]) the packed weight's stacked extra rows are computed too (LoRA shrink)."""
+    [M, n_extra]) the packed weight's stacked extra rows are computed too (LoRA shrink);
+    ``prefetch`` (l2_prefetch) names the next kernel's first bytes."""
     if a.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
         raise ValueError("gemm: a and w must be bf16")
     M, K = a.shape
@@ -202,12 +217,13 @@ def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
         raise ValueError("gemm: residual must have the output dtype")
     wsb = (ws if ws is not None else default_workspace(a.device)).get(
         _lib.load().slx_gemm_workspace_bytes(M, n_tot, K, epilogue))
-    check(_lib.load().slx_gemm_bf16(_ptr(a), _ld(a), _ptr(wt), _ptr(out), _ld(out), _dt(out),
-                                    _ptr(residual), _ld(residual) if residual is not None else 0,
-                                    M, n_tot, K, epilogue, layout, n_main,
-                                    _ptr(side) if n_tot > n_main else None,
-                                    _ld(side) if n_tot > n_main else 0, _ptr(wsb), wsb.numel(),
-                                    _stream()), "slx_gemm_bf16")
+    check(_lib.load().slx_gemm_bf16_pf(_ptr(a), _ld(a), _ptr(wt), _ptr(out), _ld(out), _dt(out),
+                                       _ptr(residual), _ld(residual) if residual is not None else 0,
+                                       M, n_tot, K, epilogue, layout, n_main,
+                                       _ptr(side) if n_tot > n_main else None,
+                                       _ld(side) if n_tot > n_main else 0, _ptr(wsb), wsb.numel(),
+                                       None if prefetch is None else ctypes.byref(prefetch),
+                                       _stream()), "slx_gemm_bf16")
     return out
 
 
@@ -381,13 +397,15 @@ def attention(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, k_cache, v_
 
 @_op("attention", 1)
 def rope_attention_decode(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos, sin,
-                          k_cache, v_cache, lora=None):
+                          k_cache, v_cache, lora=None, prefetch=None):
     """Decode-step RoPE + KV append + attention in one kernel (each token = next position of
-    its own sequence); ``lora`` (make_delta) fuses the q/k/v LoRA expand."""
-    check(_lib.load().slx_rope_attention_decode_lora(
+    its own sequence); ``lora`` (make_delta) fuses the q/k/v LoRA expand, ``prefetch``
+    (l2_prefetch) names the next kernel's first bytes."""
+    check(_lib.load().slx_rope_attention_decode_pf(
         _dt(out), _ptr(out), _ld(out), _ptr(qkv), _ld(qkv), qkv.shape[0], heads, kv_heads, head_dim,
         _ptr(tok_pos), _ptr(tok_seq), _ptr(cos), _ptr(sin), cos.shape[0], _ptr(k_cache),
-        _ptr(v_cache), k_cache.shape[2], None if lora is None else ctypes.byref(lora), _stream()),
+        _ptr(v_cache), k_cache.shape[2], None if lora is None else ctypes.byref(lora),
+        None if prefetch is None else ctypes.byref(prefetch), _stream()),
         "slx_rope_attention_decode")
     return out
 

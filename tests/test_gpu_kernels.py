@@ -336,6 +336,44 @@ def test_rope_attention_decode_fused(dtype, H, Hkv, D, ctx):
         np.testing.assert_allclose(out_f[b].float().cpu().numpy(), ref.reshape(-1), rtol=tol * 5, atol=tol * 5)
 
 
+@pytest.mark.parametrize("ctx", [0, 1, 127, 128, 129, 300])
+@pytest.mark.parametrize("B,H,D,rank", [(24, 32, 128, 16), (5, 4, 64, 8), (7, 8, 128, 64)])
+def test_attention_decode_pipe_lora(B, H, D, rank, ctx, monkeypatch):
+    """Persistent TMA-pipelined decode attention (several items per CTA, multi-block contexts)
+    with the fused q/k/v LoRA delta == the per-(token, head) kernel; ranks staged (<= 16) and
+    not staged (64); tokens without an adapter; identical KV append."""
+    rng = np.random.default_rng(ctx + B + rank)
+    max_ctx, n_slots = 320, 3
+    cos, sin = orc.rope_table(max_ctx, D, 10000.0)
+    cos_d, sin_d = torch.from_numpy(cos).to(DEV), torch.from_numpy(sin).to(DEV)
+    kc = bf(torch.from_numpy(rng.standard_normal((B, H, max_ctx, D)).astype(np.float32)).to(DEV))
+    vc = bf(torch.from_numpy(rng.standard_normal((B, H, max_ctx, D)).astype(np.float32)).to(DEV))
+    qkv = bf(torch.from_numpy(rng.standard_normal((B, 3 * H * D)).astype(np.float32)).to(DEV))
+    pos = torch.full((B,), ctx, dtype=torch.int32, device=DEV)
+    seq = torch.from_numpy(rng.permutation(B).astype(np.int32)).to(DEV)
+    slot = torch.from_numpy(rng.integers(-1, n_slots, size=B).astype(np.int32)).to(DEV)
+    ranks = torch.full((n_slots,), rank, dtype=torch.int32, device=DEV)
+    scales = torch.tensor([0.5, 2.0, 1.0], device=DEV)
+    v_all = torch.randn(B, 3 * n_slots * rank, device=DEV)
+    Bs = [bf(torch.randn(n_slots, H * D, rank, device=DEV) * 0.1) for _ in range(3)]
+    tabs = [torch.tensor([b[s].data_ptr() for s in range(n_slots)], dtype=torch.int64, device=DEV)
+            for b in Bs]
+    delta = ops.make_delta(v_all, slot, ranks, scales, rank,
+                           [(tabs[i], i * n_slots * rank, i * H * D, H * D) for i in range(3)])
+    out = {}
+    caches = {}
+    for pipe in ("1", "0"):
+        monkeypatch.setenv("SLX_ATTN_PIPE", pipe)
+        k2, v2 = kc.clone(), vc.clone()
+        o = torch.empty(B, H * D, dtype=torch.bfloat16, device=DEV)
+        ops.rope_attention_decode(o, qkv, H, H, D, pos, seq, cos_d, sin_d, k2, v2, lora=delta)
+        out[pipe], caches[pipe] = o, (k2, v2)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out["1"].float(), out["0"].float(), rtol=2e-2, atol=2e-2)
+    assert torch.equal(caches["1"][0], caches["0"][0])   # appended k (LoRA + RoPE) identical
+    assert torch.equal(caches["1"][1], caches["0"][1])
+
+
 @pytest.mark.parametrize("M", [1, 64, 300])
 def test_gemm_lora_side_output(M):
     """Stacked extra rows of a packed weight land, in fp32, in the side output; the main

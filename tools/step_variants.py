@@ -50,6 +50,11 @@ def timed(slot_list, stacked=True, fuse=True):
 
 
 none = [-1] * bench.BATCH
+for mb in [float(x) for x in os.environ.get("PF_SWEEP", "").split(",") if x]:
+    m.l2_prefetch_mb, m._pf_cache = mb, {}
+    ms, k = timed(slots.tolist(), True, True)
+    print(f"lora fused, L2 prefetch {mb:5.1f} MB            {ms:7.3f} ms/step  {bench.BATCH / ms * 1000:9.0f} tok/s", flush=True)
+m.l2_prefetch_mb, m._pf_cache = float(os.environ.get("SLX_L2_PF_MB", "32")), {}
 for name, args in [("lora fused", (slots.tolist(), True, True)),
                    ("lora expand kernels", (slots.tolist(), True, False)),
                    ("lora shrink/expand kernels (no stacking)", (slots.tolist(), False, False)),
