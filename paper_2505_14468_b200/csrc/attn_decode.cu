@@ -3,34 +3,40 @@
 // One work item = (token t, head h): the token is the NEXT position `pos` of its own sequence.
 // Per layer of the 7B decode step the kernel streams 64 tok x 32 heads x 128 cached keys x
 // (K + V) = 134 MB of KV cache, so it is HBM-bound and the design goal is to keep every SM's
-// copy engine busy.  Two persistent CTAs per SM, each with
-//   * one producer thread issuing 1-D bulk copies (TMA) of whole K and V blocks (one contiguous
-//     run each in the [seq][head][max_ctx][D] pool) into a 2-stage smem ring, and of the item's
-//     "header" (its q/k/v row slices, the cos/sin rows of pos, and the LoRA B rows and v vector
-//     of the fused q/k/v expand) into a 2-slot ring — item 0's KV is requested before the PDL
-//     wait, and after its last item the producer prefetches the next kernel's first bytes into L2;
-//   * eight consumer warps: fused LoRA delta (bit-identical to slx_lora_expand), RoPE, append
-//     k/v at pos, then online softmax over the ring's blocks.  Four threads share a key, each
-//     reading its quarter of the K row in a per-key rotated chunk order, so the unpadded TMA
-//     layout is bank-conflict free.
-// The two CTAs of an SM overlap one item's consumer latency chain with the other's copies.
+// copy engine busy (the copy ring alone streams at ~7 TB/s, SLX_ATTN_DBG_STREAM=1).  One
+// persistent CTA per SM:
+//   * a producer warp: its 32 lanes resolve the metadata of 32 items at a time (position,
+//     sequence, adapter slot / rank / scale, LoRA B rows), then lane 0 issues 1-D bulk copies
+//     (TMA) of whole K and V blocks (one contiguous run each in the [seq][head][max_ctx][D]
+//     pool) into a 4-stage ring and of each item's header (q/k/v row slices, cos/sin of pos,
+//     LoRA v) into a 4-slot ring; item 0's KV is requested before the PDL wait, and after the
+//     last item the producer prefetches the next kernel's first bytes into L2;
+//   * two consumer groups of 4 warps taking alternate items, so one group's latency chain
+//     (fused LoRA delta — bit-identical to slx_lora_expand —, RoPE, k/v append, barriers)
+//     overlaps the other's attention.  Within a group each warp runs its own online softmax
+//     over its keys of every block (no CTA barrier per block); two lanes share a key, reading
+//     K in a per-key rotated chunk order, so the unpadded TMA layout is bank-conflict free.
 // ops.cu's one-CTA-per-(token, head) kernel stays for fp32 / GQA.
 //
 // Reference: the decode gap the simulator models as decode_ms_per_token x M
 // (/root/reference/pkg/src/slorasim/engine.py:888,909).
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
 namespace slx {
 namespace {
 
-constexpr int AD_CONS = 256;               // consumer threads (8 warps)
-constexpr int AD_THREADS = AD_CONS + 32;   // + producer warp
-constexpr int AD_RMAX = 16;                // LoRA rank staged by TMA (larger ranks: global loads)
-constexpr int AD_STAGES = 2;
-
-template <int D> struct AdCfg { static constexpr int KB = 64; };     // keys per block
-template <> struct AdCfg<64> { static constexpr int KB = 128; };
+constexpr int AD_GW = 4;                      // warps per consumer group
+constexpr int AD_GROUPS = 2;
+constexpr int AD_GT = AD_GW * 32;             // threads per group
+constexpr int AD_CONS = AD_GROUPS * AD_GT;    // consumer threads
+constexpr int AD_THREADS = AD_CONS + 32;      // + producer warp
+constexpr int AD_STAGES = 4;                  // KV ring
+constexpr int AD_HSLOTS = 4;                  // header ring (2 per group)
+constexpr int AD_VMAX = 64;                   // LoRA rank staged in the header (v)
+constexpr int AD_BST = 16;                    // LoRA rank whose B rows are staged by TMA
 
 struct AdArgs {
   bf16* out;
@@ -48,60 +54,81 @@ struct AdArgs {
   float scale_log2;
   DeltaArgs lora;
   PfArgs pf;
+  int pf_early;   // SLX_ATTN_PF_EARLY=1: prefetch at kernel start instead of after the last item
+  int dbg_stream; // SLX_ATTN_DBG_STREAM=1 (debug): consumers only drain the rings (copy roofline)
 };
 
-// Header (one per item, 2-slot ring).
+struct ItemMeta {
+  const bf16* b[3];   // B rows of the three parts' column ranges
+  int voff[3];        // v column of the slot block per part
+  int ti[3];
+  int t, h, pos, seq, slot, rank, valid;
+  float scale;
+};
+
+// Header (one per item, 4-slot ring).
 template <int D>
 struct __align__(16) AdHeader {
   bf16 row[3][D];                // q (head h), k, v of the token
-  bf16 b[3][D * AD_RMAX];        // B rows [D][rank] of the three column ranges (rank <= AD_RMAX)
-  float v[3][AD_RMAX];           // LoRA shrink output of the three targets
   float cs[D];                   // cos[D/2], sin[D/2] of pos
-  int ti[3];                     // target index per part (-1: none)
-  int rank, staged, pos, seq, slot;
+  float v[3][AD_VMAX];           // LoRA shrink output of the three targets (rank <= AD_VMAX)
+  bf16 bs[3][D * AD_BST];        // B rows [D][rank] staged by TMA (rank <= AD_BST)
+  const bf16* b[3];              // B rows [D][rank] of the three column ranges (nullptr: none)
+  int bstaged;
+  int kv_base;                   // ring counter of the item's first KV block
+  int rank, pos, seq, slot;
   float lscale;
-  int pad;
 };
 
+// Per-group scratch.
 template <int D>
-constexpr size_t ad_stage_bytes() { return (size_t)2 * AdCfg<D>::KB * D * 2; }
+struct __align__(16) AdScratch {
+  float raw[3][D];
+  float kn[D], vn[D];
+  float pv[AD_GW][D];
+  float red[2 * AD_GW];
+  float sv[3][AD_VMAX];          // scale * LoRA v
+  bf16 qb[D];
+};
 
-template <int D>
+template <int D, int KB>
+constexpr size_t ad_stage_bytes() { return (size_t)2 * KB * D * 2; }
+
+template <int D, int KB>
 constexpr size_t ad_smem() {
-  return 1024 + (size_t)AD_STAGES * ad_stage_bytes<D>() + 2 * sizeof(AdHeader<D>) +
-         (size_t)(D * 2 + 2 * D * 4 + AdCfg<D>::KB * 4 + 64 * 4 + 8 * D * 4 + 3 * D * 4) +
-         (size_t)(2 * AD_STAGES + 4) * 8;
+  return 1024 + (size_t)AD_STAGES * ad_stage_bytes<D, KB>() + AD_HSLOTS * sizeof(AdHeader<D>) +
+         AD_GROUPS * sizeof(AdScratch<D>) + 32 * sizeof(ItemMeta) +
+         (size_t)(2 * AD_STAGES + 2 * AD_HSLOTS) * 8;
 }
 
-__device__ __forceinline__ void cons_sync() { tc::named_bar_sync(1, AD_CONS); }
+__device__ __forceinline__ void group_sync(int g) { tc::named_bar_sync(1 + g, AD_GT); }
 
-template <int D>
-__global__ void __launch_bounds__(AD_THREADS, 2) attn_decode_pipe_kernel(AdArgs a) {
+// Two packed bf16 (low half = element 0) -> fp32 pair: bf16 is the top half of an fp32.
+__device__ __forceinline__ float2 bf2_unpack(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+
+template <int D, int KB>
+__global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs a) {
   constexpr int HALF = D / 2;
-  constexpr int KB = AdCfg<D>::KB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  AdHeader<D>* hdr = reinterpret_cast<AdHeader<D>*>(ring + (size_t)AD_STAGES * ad_stage_bytes<D>());
-  bf16* qb = reinterpret_cast<bf16*>(hdr + 2);           // [D] rotated q (bf16)
-  float* kn = reinterpret_cast<float*>(qb + D);          // [D] new key
-  float* vn = kn + D;                                    // [D] new value
-  float* ps = vn + D;                                    // [KB] probabilities
-  float* red = ps + KB;                                  // [64]
-  float* pv = red + 64;                                  // [8 warps][D] P.V partials
-  float* raw = pv + 8 * D;                               // [3][D]
-  uint64_t* kv_full = reinterpret_cast<uint64_t*>(raw + 3 * D);
+  AdHeader<D>* hdr = reinterpret_cast<AdHeader<D>*>(ring + (size_t)AD_STAGES * ad_stage_bytes<D, KB>());
+  AdScratch<D>* scr = reinterpret_cast<AdScratch<D>*>(hdr + AD_HSLOTS);
+  ItemMeta* meta = reinterpret_cast<ItemMeta*>(scr + AD_GROUPS);
+  uint64_t* kv_full = reinterpret_cast<uint64_t*>(meta + 32);
   uint64_t* kv_empty = kv_full + AD_STAGES;
   uint64_t* h_full = kv_empty + AD_STAGES;
-  uint64_t* h_empty = h_full + 2;
+  uint64_t* h_empty = h_full + AD_HSLOTS;
 
   const int tid = threadIdx.x;
   const int n_items = a.n_tok * a.H;
   if (tid == 0) {
     for (int s = 0; s < AD_STAGES; ++s) {
       tc::mbar_init(&kv_full[s], 1);
-      tc::mbar_init(&kv_empty[s], AD_CONS / 32);   // one arrival per consumer warp
+      tc::mbar_init(&kv_empty[s], AD_GW);   // one arrival per warp of the consuming group
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < AD_HSLOTS; ++i) {
       tc::mbar_init(&h_full[i], 1);
       tc::mbar_init(&h_empty[i], 1);
     }
@@ -110,201 +137,261 @@ __global__ void __launch_bounds__(AD_THREADS, 2) attn_decode_pipe_kernel(AdArgs 
   __syncthreads();
 
   if (tid >= AD_CONS) {
-    // ================================================================ producer (one thread)
-    if (tid == AD_CONS) {
-      const uint64_t pol_kv = tc::policy_evict_first();    // cache rows are read once
-      const uint64_t pol_h = tc::policy_evict_normal();
-      int kv_it = 0;
-      auto issue_kv = [&](int seq, int h, int blk, int pos) {
-        const int s = kv_it % AD_STAGES;
-        tc::mbar_wait(&kv_empty[s], ((kv_it / AD_STAGES) & 1) ^ 1);
-        const int nk = min(KB, pos - blk * KB);
-        const uint32_t bytes = (uint32_t)nk * D * 2;
-        const size_t off = (((size_t)seq * a.H + h) * a.max_ctx + (size_t)blk * KB) * D;
-        uint8_t* st = ring + (size_t)s * ad_stage_bytes<D>();
-        tc::mbar_arrive_expect_tx(&kv_full[s], 2 * bytes);
-        tc::bulk_g2s(st, a.kc + off, bytes, &kv_full[s], pol_kv);
-        tc::bulk_g2s(st + KB * D * 2, a.vc + off, bytes, &kv_full[s], pol_kv);
-        ++kv_it;
-      };
-      // item 0's cached keys were written >= 2 launches back: start before the PDL wait
-      int n_pre = 0;
-      if ((int)blockIdx.x < n_items) {
-        const int t0 = blockIdx.x / a.H, h0 = blockIdx.x % a.H;
-        const int pos0 = a.tok_pos[t0], seq0 = a.tok_seq[t0];
-        n_pre = min((pos0 + KB - 1) / KB, AD_STAGES);
-        for (int b = 0; b < n_pre; ++b) issue_kv(seq0, h0, b, pos0);
-      }
-      pdl_wait();
-      pdl_trigger();
-      int j = 0;
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++j) {
-        const int t = w / a.H, h = w % a.H;
-        const int pos = a.tok_pos[t], seq = a.tok_seq[t];
-        const int hb = j & 1;
-        // LoRA: slot / rank / target of each part; B rows and v staged when rank <= AD_RMAX
-        const DeltaTok dt = delta_tok(a.lora, t);
-        int ti[3] = {-1, -1, -1};
-        const bf16* bsrc[3] = {nullptr, nullptr, nullptr};
-        const float* vsrc[3] = {nullptr, nullptr, nullptr};
-        if (dt.slot >= 0 && dt.rank > 0) {
+    // ================================================================ producer warp
+    const int pl = tid - AD_CONS;
+    const uint64_t pol_kv = tc::policy_evict_first();    // cache rows are read once
+    const uint64_t pol_h = tc::policy_evict_normal();
+    int kv_it = 0, j = 0, n_pre = 0;
+    auto issue_kv = [&](int seq, int h, int blk, int pos) {
+      const int s = kv_it % AD_STAGES;
+      tc::mbar_wait(&kv_empty[s], ((kv_it / AD_STAGES) & 1) ^ 1);
+      const int nk = min(KB, pos - blk * KB);
+      const uint32_t bytes = (uint32_t)nk * D * 2;
+      const size_t off = (((size_t)seq * a.H + h) * a.max_ctx + (size_t)blk * KB) * D;
+      uint8_t* st = ring + (size_t)s * ad_stage_bytes<D, KB>();
+      tc::mbar_arrive_expect_tx(&kv_full[s], 2 * bytes);
+      tc::bulk_g2s(st, a.kc + off, bytes, &kv_full[s], pol_kv);
+      tc::bulk_g2s(st + KB * D * 2, a.vc + off, bytes, &kv_full[s], pol_kv);
+      ++kv_it;
+    };
+    bool waited = false;
+    for (int w0 = blockIdx.x; w0 < n_items; w0 += 32 * gridDim.x) {
+      // ---- metadata of items w0 + i * gridDim.x, lane i (inputs / adapter pool: >= 2 launches old)
+      {
+        const int w = w0 + pl * (int)gridDim.x;
+        ItemMeta mt{};
+        mt.valid = w < n_items;
+        mt.ti[0] = mt.ti[1] = mt.ti[2] = -1;
+        if (mt.valid) {
+          const int t = w / a.H, h = w % a.H;
+          mt.t = t; mt.h = h;
+          mt.pos = a.tok_pos[t];
+          mt.seq = a.tok_seq[t];
+          const DeltaTok dt = delta_tok(a.lora, t);
+          mt.slot = dt.slot; mt.rank = dt.rank; mt.scale = dt.scale;
+          if (dt.slot >= 0 && dt.rank > 0) {
 #pragma unroll
-          for (int p = 0; p < 3; ++p) {
-            const int col = (p == 0 ? h : (p == 1 ? a.H + h : 2 * a.H + h)) * D;
+            for (int p = 0; p < 3; ++p) {
+              const int col = (p == 0 ? h : (p == 1 ? a.H + h : 2 * a.H + h)) * D;
 #pragma unroll
-            for (int i = 0; i < SLX_LORA_MAX_TARGETS; ++i) {
-              const int n = col - a.lora.y_col_off[i];
-              if (ti[p] < 0 && i < a.lora.n_targets && n >= 0 && n + D <= a.lora.d_out[i]) {
-                const bf16* B = reinterpret_cast<const bf16*>(a.lora.b_ptrs[i][dt.slot]);
-                if (B != nullptr) {
-                  ti[p] = i;
-                  bsrc[p] = B + (size_t)n * dt.rank;
-                  vsrc[p] = dt.vrow + a.lora.v_col_off[i] + dt.slot * a.lora.max_rank;
+              for (int i = 0; i < SLX_LORA_MAX_TARGETS; ++i) {
+                const int n = col - a.lora.y_col_off[i];
+                if (mt.ti[p] < 0 && i < a.lora.n_targets && n >= 0 && n + D <= a.lora.d_out[i]) {
+                  const bf16* B = reinterpret_cast<const bf16*>(a.lora.b_ptrs[i][dt.slot]);
+                  if (B != nullptr) {
+                    mt.ti[p] = i;
+                    mt.b[p] = B + (size_t)n * dt.rank;
+                    mt.voff[p] = a.lora.v_col_off[i] + dt.slot * a.lora.max_rank;
+                  }
                 }
               }
             }
           }
         }
-        const int staged = dt.rank <= AD_RMAX ? 1 : 0;
-        uint32_t bytes = 3 * D * 2 + D * 4;
-        for (int p = 0; p < 3; ++p)
-          if (ti[p] >= 0 && staged) bytes += (uint32_t)(D * dt.rank * 2 + dt.rank * 4);
-        tc::mbar_wait(&h_empty[hb], ((j >> 1) & 1) ^ 1);
-        AdHeader<D>* hd = hdr + hb;
-        hd->ti[0] = ti[0]; hd->ti[1] = ti[1]; hd->ti[2] = ti[2];
-        hd->rank = dt.rank; hd->staged = staged; hd->pos = pos; hd->seq = seq;
-        hd->slot = dt.slot; hd->lscale = dt.scale;
-        tc::mbar_arrive_expect_tx(&h_full[hb], bytes);   // releases the plain stores above too
-        const bf16* rowp = a.qkv + (size_t)t * a.ld;
-        tc::bulk_g2s(hd->row[0], rowp + (size_t)h * D, D * 2, &h_full[hb], pol_h);
-        tc::bulk_g2s(hd->row[1], rowp + (size_t)(a.H + h) * D, D * 2, &h_full[hb], pol_h);
-        tc::bulk_g2s(hd->row[2], rowp + (size_t)(2 * a.H + h) * D, D * 2, &h_full[hb], pol_h);
-        tc::bulk_g2s(hd->cs, a.cos_tab + (size_t)pos * HALF, HALF * 4, &h_full[hb], pol_h);
-        tc::bulk_g2s(hd->cs + HALF, a.sin_tab + (size_t)pos * HALF, HALF * 4, &h_full[hb], pol_h);
-        if (staged) {
-          for (int p = 0; p < 3; ++p) {
-            if (ti[p] < 0) continue;
-            tc::bulk_g2s(hd->b[p], bsrc[p], (uint32_t)(D * dt.rank * 2), &h_full[hb], pol_h);
-            tc::bulk_g2s(hd->v[p], vsrc[p], (uint32_t)(dt.rank * 4), &h_full[hb], pol_h);
-          }
-        }
-        for (int b = (j == 0 ? n_pre : 0); b < (pos + KB - 1) / KB; ++b) issue_kv(seq, h, b, pos);
+        meta[pl] = mt;
       }
-      l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);   // next kernel's first bytes
-    } else {
+      __syncwarp();
+      if (pl == 0) {
+        const int nloc = min(32, (n_items - w0 + (int)gridDim.x - 1) / (int)gridDim.x);
+        if (!waited) {
+          // item 0's cached keys were written >= 2 launches back: start before the PDL wait
+          n_pre = min((meta[0].pos + KB - 1) / KB, AD_STAGES);
+          for (int b = 0; b < n_pre; ++b) issue_kv(meta[0].seq, meta[0].h, b, meta[0].pos);
+          if (a.pf_early) l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);
+          pdl_wait();
+          pdl_trigger();
+        }
+        for (int i = 0; i < nloc; ++i, ++j) {
+          const ItemMeta& mt = meta[i];
+          const int hs = j % AD_HSLOTS;
+          const bool stage_v = mt.rank <= AD_VMAX;
+          const bool stage_b = mt.rank <= AD_BST;
+          uint32_t bytes = 3 * D * 2 + D * 4;
+          for (int p = 0; p < 3; ++p)
+            if (mt.ti[p] >= 0 && stage_v)
+              bytes += (uint32_t)(mt.rank * 4) + (stage_b ? (uint32_t)(D * mt.rank * 2) : 0u);
+          tc::mbar_wait(&h_empty[hs], ((j / AD_HSLOTS) & 1) ^ 1);
+          AdHeader<D>* hd = hdr + hs;
+          for (int p = 0; p < 3; ++p) hd->b[p] = (stage_v && mt.ti[p] >= 0) ? mt.b[p] : nullptr;
+          hd->kv_base = j == 0 ? 0 : kv_it;   // item 0's first blocks went out before the wait
+          hd->bstaged = stage_b ? 1 : 0;
+          hd->rank = mt.rank; hd->pos = mt.pos; hd->seq = mt.seq;
+          hd->slot = mt.slot; hd->lscale = mt.scale;
+          tc::mbar_arrive_expect_tx(&h_full[hs], bytes);   // releases the plain stores above too
+          const bf16* rowp = a.qkv + (size_t)mt.t * a.ld;
+          tc::bulk_g2s(hd->row[0], rowp + (size_t)mt.h * D, D * 2, &h_full[hs], pol_h);
+          tc::bulk_g2s(hd->row[1], rowp + (size_t)(a.H + mt.h) * D, D * 2, &h_full[hs], pol_h);
+          tc::bulk_g2s(hd->row[2], rowp + (size_t)(2 * a.H + mt.h) * D, D * 2, &h_full[hs], pol_h);
+          tc::bulk_g2s(hd->cs, a.cos_tab + (size_t)mt.pos * HALF, HALF * 4, &h_full[hs], pol_h);
+          tc::bulk_g2s(hd->cs + HALF, a.sin_tab + (size_t)mt.pos * HALF, HALF * 4, &h_full[hs], pol_h);
+          if (stage_v) {
+            const float* vrow = a.lora.v + (size_t)mt.t * a.lora.ldv;
+            for (int p = 0; p < 3; ++p)
+              if (mt.ti[p] >= 0) {
+                tc::bulk_g2s(hd->v[p], vrow + mt.voff[p], (uint32_t)(mt.rank * 4), &h_full[hs], pol_h);
+                if (stage_b)
+                  tc::bulk_g2s(hd->bs[p], mt.b[p], (uint32_t)(D * mt.rank * 2), &h_full[hs], pol_h);
+              }
+          }
+          for (int b = (j == 0 ? n_pre : 0); b < (mt.pos + KB - 1) / KB; ++b) issue_kv(mt.seq, mt.h, b, mt.pos);
+        }
+      } else if (!waited) {
+        pdl_wait();
+        pdl_trigger();
+      }
+      waited = true;
+      __syncwarp();
+    }
+    if (!waited) {   // no items for this CTA
       pdl_wait();
       pdl_trigger();
     }
+    if (pl == 0 && !a.pf_early) l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);
     __syncwarp();
     return;
   }
 
-  // ================================================================== consumers (8 warps)
-  // Each warp runs its own online softmax over its slice of every block (KB / 8 keys), so a
-  // block needs no CTA-wide barrier: the warp releases the stage (kv_empty counts 8 arrivals)
-  // and the 8 partial (max, sum, acc) states are merged once per item.
+  // ================================================================== consumer groups
+  // Group g takes items g, g + 2, ...  Each of its 4 warps runs its own online softmax over
+  // KB / 4 keys of every block; the 4 (max, sum, acc) states are merged once per item.
   pdl_wait();
   pdl_trigger();
-  const int warp = tid >> 5, lane = tid & 31;
-  constexpr int KPW = KB / 8;            // keys per warp per block
-  constexpr int LPK = 32 / KPW;          // lanes per key in the scores (4 | 2)
-  constexpr int CPL = D / LPK / 8;       // 16-byte chunks per lane (4)
+  const int g = tid / AD_GT, gt = tid % AD_GT;
+  const int gw = gt >> 5, lane = tid & 31;
+  AdScratch<D>& sc_ = scr[g];
+  constexpr int KPW = KB / AD_GW;        // keys per warp per block
+  constexpr int LPK = 32 / KPW;          // lanes per key in the scores
+  constexpr int CPL = D / LPK / 8;       // 16-byte chunks per lane
   constexpr int DPL = D / 32;            // output dims per lane in P.V (4 | 2)
   const int wkey = lane / LPK, lq = lane % LPK;
-  int kv_it = 0, j = 0;
-  for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++j) {
+  for (int j = g; (int)blockIdx.x + j * (int)gridDim.x < n_items; j += AD_GROUPS) {
+    const int w = blockIdx.x + j * (int)gridDim.x;
     const int t = w / a.H, h = w % a.H;
-    const int hb = j & 1;
-    tc::mbar_wait(&h_full[hb], (j >> 1) & 1);
-    const AdHeader<D>* hd = hdr + hb;
+    const int hs = j % AD_HSLOTS;
+    tc::mbar_wait(&h_full[hs], (j / AD_HSLOTS) & 1);
+    const AdHeader<D>* hd = hdr + hs;
     const int pos = hd->pos, seq = hd->seq, rank = hd->rank;
+    const int nb = (pos + KB - 1) / KB;
+    const int kv0 = hd->kv_base;
+    if (a.dbg_stream) {   // copy-engine roofline: drain the header and the KV blocks only
+      group_sync(g);
+      if (gt == 0) tc::mbar_arrive(&h_empty[hs]);
+      for (int b = 0; b < nb; ++b) {
+        const int it = kv0 + b;
+        tc::mbar_wait(&kv_full[it % AD_STAGES], (it / AD_STAGES) & 1);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&kv_empty[it % AD_STAGES]);
+      }
+      continue;
+    }
     // ---- q/k/v of this head with the fused LoRA expand (sequential fmaf: as slx_lora_expand)
-    for (int i = tid; i < 3 * D; i += AD_CONS) {
+    const bool lora_v = hd->b[0] != nullptr || hd->b[1] != nullptr || hd->b[2] != nullptr;
+    if (lora_v) {   // scale * v once per item
+      const float sc = hd->lscale;
+      for (int i = gt; i < 3 * AD_VMAX; i += AD_GT) {
+        const int p = i / AD_VMAX, jj = i - p * AD_VMAX;
+        if (jj < rank) sc_.sv[p][jj] = hd->v[p][jj] * sc;
+      }
+      group_sync(g);
+    }
+    for (int i = gt; i < 3 * D; i += AD_GT) {
       const int p = i / D, e = i - p * D;
       float v = __bfloat162float(hd->row[p][e]);
-      if (hd->ti[p] >= 0) {
+      const bf16* bp = hd->b[p];
+      if (bp != nullptr) {
+        const bf16* br = (hd->bstaged ? hd->bs[p] : bp) + (size_t)e * rank;
+        const float* vv = sc_.sv[p];
         float acc = 0.f;
-        if (hd->staged) {
-          const bf16* br = hd->b[p] + (size_t)e * rank;
-          const float* vv = hd->v[p];
-          const float sc = hd->lscale;
-          for (int jj = 0; jj < rank; jj += 8) {
-            float bf[8];
-            Vec8<bf16>::load(br + jj, bf);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) acc = fmaf(vv[jj + u] * sc, bf[u], acc);
-          }
-        } else {
-          const int col = (p == 0 ? h : (p == 1 ? a.H + h : 2 * a.H + h)) * D + e;
-          acc = delta_col(a.lora, delta_tok(a.lora, t), col);
+        for (int jj = 0; jj < rank; jj += 8) {
+          const uint4 u = *reinterpret_cast<const uint4*>(br + jj);
+          const float4 v0 = *reinterpret_cast<const float4*>(vv + jj);
+          const float4 v1 = *reinterpret_cast<const float4*>(vv + jj + 4);
+          const float2 b0 = bf2_unpack(u.x), b1 = bf2_unpack(u.y), b2 = bf2_unpack(u.z), b3 = bf2_unpack(u.w);
+          acc = fmaf(v0.x, b0.x, acc); acc = fmaf(v0.y, b0.y, acc);
+          acc = fmaf(v0.z, b1.x, acc); acc = fmaf(v0.w, b1.y, acc);
+          acc = fmaf(v1.x, b2.x, acc); acc = fmaf(v1.y, b2.y, acc);
+          acc = fmaf(v1.z, b3.x, acc); acc = fmaf(v1.w, b3.y, acc);
         }
         v = __bfloat162float(__float2bfloat16_rn(v + acc));
+      } else if (hd->slot >= 0 && rank > AD_VMAX) {
+        const int col = (p == 0 ? h : (p == 1 ? a.H + h : 2 * a.H + h)) * D + e;
+        v = __bfloat162float(__float2bfloat16_rn(v + delta_col(a.lora, delta_tok(a.lora, t), col)));
       }
-      raw[i] = v;
+      sc_.raw[p][e] = v;
     }
-    cons_sync();
+    group_sync(g);
     // ---- RoPE (rotate-half), new key / value appended at pos
     {
       bf16* kdst = a.kc + (((size_t)seq * a.H + h) * a.max_ctx + pos) * D;
       bf16* vdst = a.vc + (((size_t)seq * a.H + h) * a.max_ctx + pos) * D;
-      for (int i = tid; i < HALF; i += AD_CONS) {
+      for (int i = gt; i < HALF; i += AD_GT) {
         const float c = hd->cs[i], sn = hd->cs[HALF + i];
-        const float q1 = raw[i], q2 = raw[i + HALF];
-        qb[i] = __float2bfloat16_rn(q1 * c - q2 * sn);
-        qb[i + HALF] = __float2bfloat16_rn(q2 * c + q1 * sn);
-        const float k1 = raw[D + i], k2 = raw[D + i + HALF];
+        const float q1 = sc_.raw[0][i], q2 = sc_.raw[0][i + HALF];
+        sc_.qb[i] = __float2bfloat16_rn(q1 * c - q2 * sn);
+        sc_.qb[i + HALF] = __float2bfloat16_rn(q2 * c + q1 * sn);
+        const float k1 = sc_.raw[1][i], k2 = sc_.raw[1][i + HALF];
         const bf16 r1 = __float2bfloat16_rn(k1 * c - k2 * sn), r2 = __float2bfloat16_rn(k2 * c + k1 * sn);
-        kn[i] = __bfloat162float(r1);
-        kn[i + HALF] = __bfloat162float(r2);
+        sc_.kn[i] = __bfloat162float(r1);
+        sc_.kn[i + HALF] = __bfloat162float(r2);
         kdst[i] = r1;
         kdst[i + HALF] = r2;
       }
-      for (int i = tid; i < D; i += AD_CONS) {
-        const bf16 v = __float2bfloat16_rn(raw[2 * D + i]);
-        vn[i] = __bfloat162float(v);
+      for (int i = gt; i < D; i += AD_GT) {
+        const bf16 v = __float2bfloat16_rn(sc_.raw[2][i]);
+        sc_.vn[i] = __bfloat162float(v);
         vdst[i] = v;
       }
     }
-    cons_sync();
-    if (tid == 0) tc::mbar_arrive(&h_empty[hb]);   // header consumed (pos/seq/cs read above)
-    // q slice of this lane (rotation applied per key below) and the new key's score
+    group_sync(g);
+    if (gt == 0) tc::mbar_arrive(&h_empty[hs]);   // header consumed
+    // the new key's score (every warp, redundantly) and per-warp softmax state
     float s_new;
     {
       float part = 0.f;
 #pragma unroll
       for (int e = 0; e < DPL; ++e)
-        part += __bfloat162float(qb[lane * DPL + e]) * kn[lane * DPL + e];
+        part += __bfloat162float(sc_.qb[lane * DPL + e]) * sc_.kn[lane * DPL + e];
       s_new = warp_sum(part) * a.scale_log2;
     }
-    // per-warp online softmax state; warp 0 owns the new key's term
-    float m = warp == 0 ? s_new : -INFINITY, l = warp == 0 ? 1.f : 0.f;
-    float acc[DPL];
+    float m = gw == 0 ? s_new : -INFINITY, l = gw == 0 ? 1.f : 0.f;
+    // P.V accumulators (packed fp32 pairs: FFMA2), dims [lane*DPL, lane*DPL + DPL)
+    float2 acc2[DPL / 2];
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) acc[e] = warp == 0 ? vn[lane * DPL + e] : 0.f;
-    const int nb = (pos + KB - 1) / KB;
-    for (int b = 0; b < nb; ++b, ++kv_it) {
-      const int s = kv_it % AD_STAGES;
+    for (int e = 0; e < DPL / 2; ++e)
+      acc2[e] = gw == 0 ? make_float2(sc_.vn[lane * DPL + 2 * e], sc_.vn[lane * DPL + 2 * e + 1])
+                        : make_float2(0.f, 0.f);
+    const int key = gw * KPW + wkey;
+    // this lane's q slice in its key-rotated chunk order (the key index of the lane is the same
+    // in every block), unpacked to fp32 pairs once per item
+    float2 q2[CPL][4];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int cc = (c + key) & (CPL - 1);
+      const uint4 u = *reinterpret_cast<const uint4*>(sc_.qb + lq * (D / LPK) + cc * 8);
+      q2[c][0] = bf2_unpack(u.x); q2[c][1] = bf2_unpack(u.y);
+      q2[c][2] = bf2_unpack(u.z); q2[c][3] = bf2_unpack(u.w);
+    }
+    for (int b = 0; b < nb; ++b) {
+      const int it = kv0 + b, s = it % AD_STAGES;
       const int nk = min(KB, pos - b * KB);
-      tc::mbar_wait(&kv_full[s], (kv_it / AD_STAGES) & 1);
-      const bf16* Ks = reinterpret_cast<const bf16*>(ring + (size_t)s * ad_stage_bytes<D>());
+      tc::mbar_wait(&kv_full[s], (it / AD_STAGES) & 1);
+      const bf16* Ks = reinterpret_cast<const bf16*>(ring + (size_t)s * ad_stage_bytes<D, KB>());
       const bf16* Vs = Ks + KB * D;
-      const int key = warp * KPW + wkey;
-      // scores: LPK lanes per key, each a D/LPK slice read in a key-rotated chunk order
+      // scores: LPK lanes per key, each a D/LPK slice read in the key-rotated chunk order
       float sc = 0.f;
       if (key < nk) {
         const bf16* kr = Ks + (size_t)key * D + lq * (D / LPK);
-        const bf16* qh = qb + lq * (D / LPK);
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};   // independent chains (latency)
+        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const int cc = (c + key) & (CPL - 1);
-          float kf[8], qf[8];
-          Vec8<bf16>::load(kr + cc * 8, kf);
-          Vec8<bf16>::load(qh + cc * 8, qf);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) s4[e & 3] = fmaf(qf[e], kf[e], s4[e & 3]);
+          const uint4 u = *reinterpret_cast<const uint4*>(kr + cc * 8);
+          s0 = __ffma2_rn(q2[c][0], bf2_unpack(u.x), s0);
+          s1 = __ffma2_rn(q2[c][1], bf2_unpack(u.y), s1);
+          s0 = __ffma2_rn(q2[c][2], bf2_unpack(u.z), s0);
+          s1 = __ffma2_rn(q2[c][3], bf2_unpack(u.w), s1);
         }
-        sc = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        sc = (s0.x + s0.y) + (s1.x + s1.y);
       }
 #pragma unroll
       for (int o = 1; o < LPK; o <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
@@ -313,54 +400,57 @@ __global__ void __launch_bounds__(AD_THREADS, 2) attn_decode_pipe_kernel(AdArgs 
       const float corr = m_new == -INFINITY ? 1.f : exp2f(m - m_new);
       const float p = key < nk ? exp2f(sc - m_new) : 0.f;
       l = l * corr + warp_sum(lq == 0 ? p : 0.f);
+      const float2 corr2 = make_float2(corr, corr);
 #pragma unroll
-      for (int e = 0; e < DPL; ++e) acc[e] *= corr;
-      // P.V over the warp's keys: lane owns dims [lane*DPL, lane*DPL + DPL)
+      for (int e = 0; e < DPL / 2; ++e) acc2[e] = __fmul2_rn(acc2[e], corr2);
+      // P.V over the warp's keys
 #pragma unroll
       for (int kk = 0; kk < KPW; ++kk) {
         const float pk = __shfl_sync(0xffffffffu, p, kk * LPK);
-        if (warp * KPW + kk < nk) {
-          float vf[DPL];
+        if (gw * KPW + kk < nk) {
+          const float2 p2 = make_float2(pk, pk);
+          const bf16* vr = Vs + (size_t)(gw * KPW + kk) * D + lane * DPL;
           if (DPL == 4) {
-            const uint2 u = *reinterpret_cast<const uint2*>(Vs + (size_t)(warp * KPW + kk) * D + lane * 4);
-            const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-            const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-            vf[0] = f0.x; vf[1] = f0.y; vf[2 % DPL] = f1.x; vf[3 % DPL] = f1.y;
+            const uint2 u = *reinterpret_cast<const uint2*>(vr);
+            acc2[0] = __ffma2_rn(p2, bf2_unpack(u.x), acc2[0]);
+            acc2[(DPL / 2) - 1] = __ffma2_rn(p2, bf2_unpack(u.y), acc2[(DPL / 2) - 1]);
           } else {
-            const float2 f0 = __bfloat1622float2(
-                *reinterpret_cast<const __nv_bfloat162*>(Vs + (size_t)(warp * KPW + kk) * D + lane * 2));
-            vf[0] = f0.x; vf[1 % DPL] = f0.y;
+            acc2[0] = __ffma2_rn(p2, bf2_unpack(*reinterpret_cast<const uint32_t*>(vr)), acc2[0]);
           }
-#pragma unroll
-          for (int e = 0; e < DPL; ++e) acc[e] = fmaf(pk, vf[e], acc[e]);
         }
       }
       m = m_new;
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&kv_empty[s]);   // this warp is done with the stage
     }
-    // ---- merge the 8 warp states (fixed order) and write the head's output
+    float acc[DPL];
+#pragma unroll
+    for (int e = 0; e < DPL / 2; ++e) {
+      acc[2 * e] = acc2[e].x;
+      acc[2 * e + 1] = acc2[e].y;
+    }
+    // ---- merge the group's warp states (fixed order) and write the head's output
     if (lane == 0) {
-      red[warp] = m;
-      red[8 + warp] = l;
+      sc_.red[gw] = m;
+      sc_.red[AD_GW + gw] = l;
     }
 #pragma unroll
-    for (int e = 0; e < DPL; ++e) pv[warp * D + lane * DPL + e] = acc[e];
-    cons_sync();
-    if (tid < D) {
-      float mx = red[0];
+    for (int e = 0; e < DPL; ++e) sc_.pv[gw][lane * DPL + e] = acc[e];
+    group_sync(g);
+    if (gt < D) {
+      float mx = sc_.red[0];
 #pragma unroll
-      for (int q = 1; q < 8; ++q) mx = fmaxf(mx, red[q]);
+      for (int q = 1; q < AD_GW; ++q) mx = fmaxf(mx, sc_.red[q]);
       float o = 0.f, ls = 0.f;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float f = red[q] == -INFINITY ? 0.f : exp2f(red[q] - mx);
-        o = fmaf(pv[q * D + tid], f, o);
-        ls = fmaf(red[8 + q], f, ls);
+      for (int q = 0; q < AD_GW; ++q) {
+        const float f = sc_.red[q] == -INFINITY ? 0.f : exp2f(sc_.red[q] - mx);
+        o = fmaf(sc_.pv[q][gt], f, o);
+        ls = fmaf(sc_.red[AD_GW + q], f, ls);
       }
-      a.out[(size_t)t * a.ldo + (size_t)h * D + tid] = __float2bfloat16_rn(o / ls);
+      a.out[(size_t)t * a.ldo + (size_t)h * D + gt] = __float2bfloat16_rn(o / ls);
     }
-    cons_sync();   // red / pv / qb / kn / vn / raw reused by the next item
+    group_sync(g);   // scratch reused by the group's next item
   }
 }
 
@@ -377,8 +467,12 @@ int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int
   a.n_tok = n_tok; a.H = heads; a.tok_pos = tok_pos; a.tok_seq = tok_seq;
   a.cos_tab = cos_tab; a.sin_tab = sin_tab; a.kc = (bf16*)k_cache; a.vc = (bf16*)v_cache;
   a.max_ctx = max_ctx; a.scale_log2 = scale_log2; a.lora = lora; a.pf = pf;
+  const char* e = getenv("SLX_ATTN_PF_EARLY");
+  a.pf_early = (e && e[0] == '1') ? 1 : 0;
+  const char* ed = getenv("SLX_ATTN_DBG_STREAM");
+  a.dbg_stream = (ed && ed[0] == '1') ? 1 : 0;
   const int items = n_tok * heads;
-  const int grid = items < 2 * sm_count() ? items : 2 * sm_count();
+  const int grid = items < sm_count() ? items : sm_count();
   auto go = [&](auto kernel, size_t smem) -> int {
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
@@ -386,8 +480,8 @@ int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return launch_ex(kernel, dim3((unsigned)grid), dim3(AD_THREADS), smem, stream, 1u, a);
   };
-  if (head_dim == 128) return go(attn_decode_pipe_kernel<128>, ad_smem<128>());
-  if (head_dim == 64) return go(attn_decode_pipe_kernel<64>, ad_smem<64>());
+  if (head_dim == 128) return go(attn_decode_pipe_kernel<128, 64>, ad_smem<128, 64>());
+  if (head_dim == 64) return go(attn_decode_pipe_kernel<64, 128>, ad_smem<64, 128>());
   return SLX_ERR_UNSUPPORTED;
 }
 

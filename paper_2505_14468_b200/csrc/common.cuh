@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <utility>
 
@@ -251,10 +252,13 @@ namespace slx {
 struct PfArgs {
   const char* ptr[2];
   unsigned long long bytes[2];
+  int evict_last;   // SLX_PF_EVICT_LAST (debug / tuning): prefetch with an evict_last policy
 };
 inline PfArgs pf_args(const slx_l2_prefetch* p) {
   PfArgs a{};
   if (p == nullptr) return a;
+  const char* e = getenv("SLX_PF_EVICT_LAST");
+  a.evict_last = (e && e[0] == '1') ? 1 : 0;
   for (int i = 0; i < 2; ++i) {
     a.ptr[i] = static_cast<const char*>(p->ptr[i]);
     a.bytes[i] = p->ptr[i] ? (p->bytes[i] & ~15ull) : 0;
@@ -270,9 +274,15 @@ __device__ __forceinline__ void l2_prefetch_part(const PfArgs& pf, int part, int
     const unsigned long long per = ((n + parts - 1) / parts + 15) & ~15ull;
     unsigned long long lo = per * part, hi = lo + per;
     hi = hi > n ? n : hi;
+    uint64_t pol;   // evict_last: keep the prefetched lines until the next kernel streams them
+    if (pf.evict_last)
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     for (unsigned long long o = lo; o < hi; o += 65536) {
       const unsigned sz = (unsigned)((hi - o) < 65536 ? (hi - o) : 65536);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf.ptr[r] + o), "r"(sz)
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(pf.ptr[r] + o),
+                   "r"(sz), "l"(pol)
                    : "memory");
     }
   }

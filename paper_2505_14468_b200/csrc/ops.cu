@@ -140,6 +140,76 @@ __global__ void __launch_bounds__(512) rmsnorm_lora_kernel(T* __restrict__ out, 
   }
 }
 
+// Cluster variant: one 8-CTA cluster per token, each CTA d/8 columns (8 per thread), the
+// sum of squares reduced over the cluster through DSMEM in a fixed rank order.  Spreads the
+// o-projection B rows (d x rank per token) over 8 SMs instead of one.
+constexpr int RNL_CL = 8;
+template <typename T>
+__global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict__ out, int ldo,
+                                                                   T* __restrict__ x, int ldx,
+                                                                   const bf16* __restrict__ w,
+                                                                   int d, float eps, DeltaArgs lora) {
+  __shared__ float vs[DELTA_VS];
+  __shared__ float red[8];
+  const int t = blockIdx.x / RNL_CL, cr = blockIdx.x % RNL_CL;
+  const int i0 = cr * (d / RNL_CL) + threadIdx.x * 8;
+  T* xr = x + (size_t)t * ldx;
+  const DeltaTok dt = delta_tok(lora, t);   // slot tables / adapter pool: >= 2 launches old
+  const bool fast = dt.slot >= 0 && dt.rank <= 16;
+  DeltaRow<2> dr[8];
+  if (fast) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) delta_prefetch<2>(lora, dt, i0 + j, dr[j]);
+  }
+  pdl_wait();
+  pdl_trigger();
+  float f[8];
+  Vec8<T>::load(xr + i0, f);
+  if (fast) {
+    delta_stage_v(lora, dt, vs, threadIdx.x, blockDim.x);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + delta_finish<2>(dt, dr[j], vs)));
+    Vec8<T>::store(xr + i0, f);
+  } else if (dt.slot >= 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + delta_col(lora, dt, i0 + j)));
+    Vec8<T>::store(xr + i0, f);
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float c = 0.f;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) c += red[q];
+    red[4] = c;   // this CTA's partial
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  float tot = 0.f;
+  {
+    const uint32_t a_local = static_cast<uint32_t>(__cvta_generic_to_shared(&red[4]));
+#pragma unroll
+    for (int r = 0; r < RNL_CL; ++r) {   // fixed rank order: deterministic
+      uint32_t ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a_local), "r"(r));
+      float v;
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+      tot += v;
+    }
+  }
+  const float inv = 1.0f / sqrtf(tot / (float)d + eps);
+  float g[8];
+  Vec8<bf16>::load(w + i0, g);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) f[j] = (f[j] * inv) * g[j];
+  Vec8<T>::store(out + (size_t)t * ldo + i0, f);
+  // keep red[4] alive until every peer has read it
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ RoPE + KV write
 // One CTA per token; thread i handles rotation pair (i, i + D/2) of every head.
 template <typename T>
@@ -669,8 +739,14 @@ extern "C" int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx,
   SLX_CHECK_ALIGN(w, 16);
   if (n_tok == 0) return SLX_OK;
   const DeltaArgs la = delta_args(lora);
-  int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
   int st = SLX_OK;
+  const char* e = getenv("SLX_RMSNORM_CLUSTER");
+  if (d % (RNL_CL * 8 * 32) == 0 && d / (RNL_CL * 8) <= 128 && !(e && e[0] == '0')) {
+    const int thr = d / (RNL_CL * 8);
+    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la));
+    return st;
+  }
+  int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
   DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_kernel<T>, dim3(n_tok), dim3(threads), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la));
   return st;
 }

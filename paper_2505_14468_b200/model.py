@@ -196,7 +196,7 @@ class MultiLoraModel:
         # decode: q/k/v expand fused into the attention kernel, o expand into the post-norm
         self.fuse_expand = True
         # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off)
-        self.l2_prefetch_mb = float(os.environ.get("SLX_L2_PF_MB", "32"))
+        self.l2_prefetch_mb = float(os.environ.get("SLX_L2_PF_MB", "16"))
         self._pf_cache: dict = {}
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
         self.pool.on_install = self._stack_install
@@ -426,6 +426,15 @@ class MultiLoraModel:
         if key not in self._pf_cache:
             n = int(self.l2_prefetch_mb * (1 << 20)) // len(tensors)
             self._pf_cache[key] = ops.l2_prefetch(*[(getattr(t, "data", t), n) for t in tensors])
+        return self._pf_cache[key]
+
+    def _pf_all(self, key, t):
+        """slx_l2_prefetch of a whole (packed) weight (spread over a long kernel)."""
+        if self.l2_prefetch_mb <= 0:
+            return None
+        if key not in self._pf_cache:
+            d = getattr(t, "data", t)
+            self._pf_cache[key] = ops.l2_prefetch((d, d.numel() * d.element_size()))
         return self._pf_cache[key]
 
     def _delta(self, layer: int, proj: str, v_all, slot, cols):

@@ -374,6 +374,44 @@ def test_attention_decode_pipe_lora(B, H, D, rank, ctx, monkeypatch):
     assert torch.equal(caches["1"][1], caches["0"][1])
 
 
+@pytest.mark.parametrize("d,rank", [(4096, 16), (4096, 64), (5120, 8), (8192, 16)])
+def test_rmsnorm_lora_cluster(d, rank, monkeypatch):
+    """Residual LoRA add + RMSNorm: the 8-CTA cluster kernel == the one-CTA-per-token kernel
+    (identical x write-back; normalised output to fp32 reduction-order rounding), tokens
+    without an adapter untouched."""
+    T, n_slots = 37, 4
+    g = torch.Generator(device=DEV).manual_seed(d + rank)
+    x0 = bf(torch.randn(T, d, device=DEV, generator=g))
+    w = bf(torch.rand(d, device=DEV, generator=g) + 0.5)
+    slot = torch.randint(-1, n_slots, (T,), device=DEV, generator=g, dtype=torch.int32)
+    ranks = torch.full((n_slots,), rank, dtype=torch.int32, device=DEV)
+    scales = torch.tensor([0.5, 1.0, 2.0, 4.0], device=DEV)
+    v_all = torch.randn(T, n_slots * rank, device=DEV, generator=g)
+    Bw = bf(torch.randn(n_slots, d, rank, device=DEV, generator=g) * 0.1)
+    tab = torch.tensor([Bw[s].data_ptr() for s in range(n_slots)], dtype=torch.int64, device=DEV)
+    delta = ops.make_delta(v_all, slot, ranks, scales, rank, [(tab, 0, 0, d)])
+    res = {}
+    for cl in ("1", "0"):
+        monkeypatch.setenv("SLX_RMSNORM_CLUSTER", cl)
+        x = x0.clone()
+        h = torch.empty_like(x)
+        ops.rmsnorm_lora(h, x, w, 1e-5, delta)
+        res[cl] = (x, h)
+    torch.cuda.synchronize()
+    assert torch.equal(res["1"][0], res["0"][0])
+    torch.testing.assert_close(res["1"][1].float(), res["0"][1].float(), rtol=8e-3, atol=8e-3)
+    none = (slot < 0).nonzero().flatten()
+    assert torch.equal(res["1"][0][none], x0[none])
+    # reference: fp32 delta, bf16 round, fp32 rmsnorm
+    sl = slot.clamp(min=0).long()
+    dl = torch.einsum("tr,tdr->td", v_all.view(T, n_slots, rank)[torch.arange(T), sl] * scales[sl][:, None],
+                      Bw[sl].float())
+    xr = torch.where(slot[:, None] >= 0, (x0.float() + dl).bfloat16().float(), x0.float())
+    torch.testing.assert_close(res["1"][0].float(), xr, rtol=1e-2, atol=1e-2)
+    hr = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + 1e-5) * w.float()
+    torch.testing.assert_close(res["1"][1].float(), hr, rtol=2e-2, atol=2e-2)
+
+
 @pytest.mark.parametrize("M", [1, 64, 300])
 def test_gemm_lora_side_output(M):
     """Stacked extra rows of a packed weight land, in fp32, in the side output; the main

@@ -63,6 +63,8 @@ def run(pipe, lora):
     return {"pipe": pipe, "lora": lora, "ctx": CTX, "us": round(us, 2), "GB/s": round(kv_bytes / us / 1e3, 1)}
 
 
-for pipe in ("1", "0"):
+for pipe in (("1",) if os.environ.get("SLX_ATTN_DBG_STREAM") else ("1", "0")):
     for lora in (False, True):
-        print(json.dumps(run(pipe, lora)), flush=True)
+        r = run(pipe, lora)
+        r["kb"] = os.environ.get("SLX_ATTN_KB", "64")
+        print(json.dumps(r), flush=True)

@@ -50,10 +50,41 @@ def timed(slot_list, stacked=True, fuse=True):
 
 
 none = [-1] * bench.BATCH
-for mb in [float(x) for x in os.environ.get("PF_SWEEP", "").split(",") if x]:
-    m.l2_prefetch_mb, m._pf_cache = mb, {}
-    ms, k = timed(slots.tolist(), True, True)
-    print(f"lora fused, L2 prefetch {mb:5.1f} MB            {ms:7.3f} ms/step  {bench.BATCH / ms * 1000:9.0f} tok/s", flush=True)
+# prefetch configurations, interleaved over rounds (box-to-box variance is larger than the effects)
+cfgs = []
+for spec in [x for x in os.environ.get("PF_SWEEP", "").split(";") if x]:
+    mb, early, last, wo_all = spec.split(",")
+    cfgs.append((float(mb), early, last, wo_all == "1"))
+if cfgs:
+    graphs = []
+    for mb, early, last, wo_all in cfgs:
+        os.environ["SLX_ATTN_PF_EARLY"], os.environ["SLX_PF_EVICT_LAST"] = early, last
+        m.l2_prefetch_mb, m._pf_cache = mb, {}
+        if not wo_all:
+            m._pf_all = lambda key, t: m._pf(key, t)
+        else:
+            m.__dict__.pop("_pf_all", None)
+        m.use_stacked_decode, m.fuse_expand = True, True
+        dg = DecodeGraph(m, seqs, slots.tolist(), fixed_pos=bench.CTX)
+        dg.capture()
+        graphs.append(((mb, early, last, wo_all), dg))
+    res = {c: [] for c, _ in graphs}
+    for _ in range(3):
+        for c, dg in graphs:
+            for _ in range(3):
+                dg.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(steps):
+                dg.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            res[c].append(e0.elapsed_time(e1) / steps)
+    for c, v in res.items():
+        print(f"prefetch mb={c[0]:5.1f} attn_early={c[1]} evict_last={c[2]} wo_all={c[3]}: "
+              f"{min(v):7.3f} ms/step  {bench.BATCH / min(v) * 1000:9.0f} tok/s", flush=True)
+    sys.exit(0)
 m.l2_prefetch_mb, m._pf_cache = float(os.environ.get("SLX_L2_PF_MB", "32")), {}
 for name, args in [("lora fused", (slots.tolist(), True, True)),
                    ("lora expand kernels", (slots.tolist(), True, False)),
