@@ -99,6 +99,16 @@ SLX_API int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, int
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
                   int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes,
                   const slx_l2_prefetch* pf, void* stream);
+/* Decode split-K handed to the consumer: W tiled, M <= 64; the N columns are cut in 256-wide
+ * tiles and the K range of each tile in `splits` equal pieces, one CTA per piece; every piece
+ * is written in fp32 to `part` with no reduction and no epilogue, so the kernel has no tail.
+ * Layout (the consumer's contract, e.g. slx_rmsnorm_fused): with bm = M rounded up to 16,
+ *   part[((tile * splits + piece) * bm * 256) + ((col % 256) / 16 * bm + m) * 16 + col % 16]
+ * and C[m, col] = sum over piece (in order) of the pieces.  part_bytes >= slx_gemm_splitk_bytes. */
+SLX_API size_t slx_gemm_splitk_bytes(int M, int N, int splits);
+SLX_API int slx_gemm_bf16_splitk(const void* A, int lda, const void* W, int M, int N, int K,
+                  int splits, float* part, size_t part_bytes, const slx_l2_prefetch* pf,
+                  void* stream);
 /* Debug only: following slx_gemm_bf16 launches write 16 u64 globaltimer slots per CTA into
  * the device buffer `buf` (phase timeline: entry, prologue, past PDL wait, first stage landed,
  * last MMA issued, accumulator ready, split-K reduction start, exit, reduction end, segment
@@ -204,10 +214,25 @@ SLX_API int slx_embedding(int dtype, void* out, const void* table, const int32_t
                   int n_tok, int d, int vocab, void* stream);
 SLX_API int slx_rmsnorm(int dtype, void* out, int ldo, const void* x, int ldx, const void* w,
                 int n_tok, int d, float eps, void* stream);
+/* Split-K pieces of a projection (slx_gemm_bf16_splitk layout) consumed by the next kernel:
+ * columns [0, n_main) are the projection output, columns >= n_main its stacked LoRA shrink rows. */
+typedef struct slx_splitk_in {
+  const float* part;
+  int splits;
+  int bm;       /* token rows per piece (M rounded up to 16) */
+  int n_main;
+} slx_splitk_in;
 /* Residual-stream LoRA add + RMSNorm: x[t, :] += delta (slx_lora_delta over the row, rounded
  * to the activation dtype and written back to x), then out = rmsnorm(x) (lora may be NULL). */
 SLX_API int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx, const void* w,
                 int n_tok, int d, float eps, const slx_lora_delta* lora, void* stream);
+/* The residual epilogue of a split-K projection fused in front: x[t, :] = round(x + sum of the
+ * pieces) (what slx_gemm_bf16's residual epilogue would have stored), then the LoRA add (its v
+ * taken from the pieces' columns >= n_main when lora->v is NULL) and the RMSNorm, as
+ * slx_rmsnorm_lora.  d % 2048 == 0 (8-CTA cluster per token). */
+SLX_API int slx_rmsnorm_fused(int dtype, void* out, int ldo, void* x, int ldx, const void* w,
+                int n_tok, int d, float eps, const slx_splitk_in* sk, const slx_lora_delta* lora,
+                void* stream);
 /* qkv [n_tok, (H + 2 Hkv) D]: rotate q,k in place (rotate-half, cos/sin tables fp32
  * [max_pos, D/2]) and write k, v at (tok_seq[t], tok_pos[t]) of the caches. */
 SLX_API int slx_rope_kv_write(int dtype, void* qkv, int ld_qkv, int n_tok, int heads, int kv_heads,

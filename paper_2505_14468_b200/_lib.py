@@ -47,6 +47,11 @@ class LoraDelta(ctypes.Structure):
                 ("y_col_off", _i * 4), ("d_out", _i * 4)]
 
 
+class SplitKIn(ctypes.Structure):
+    """slx_splitk_in: split-K pieces of a projection for the consuming kernel."""
+    _fields_ = [("part", _p), ("splits", _i), ("bm", _i), ("n_main", _i)]
+
+
 class L2Prefetch(ctypes.Structure):
     """slx_l2_prefetch: the next kernel's first bytes (two regions)."""
     _fields_ = [("ptr", _p * 2), ("bytes", _sz * 2)]
@@ -61,6 +66,8 @@ SIGNATURES = {
     "slx_gemm_bf16": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p, _sz,
                            _p]),
     "slx_debug_gemm_trace": (_i, [_p]),
+    "slx_gemm_splitk_bytes": (_sz, [_i, _i, _i]),
+    "slx_gemm_bf16_splitk": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _sz, ctypes.POINTER(L2Prefetch), _p]),
     "slx_gemm_bf16_pf": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p,
                               _sz, ctypes.POINTER(L2Prefetch), _p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),
@@ -84,6 +91,8 @@ SIGNATURES = {
     "slx_embedding": (_i, [_i, _p, _p, _p, _i, _i, _i, _p]),
     "slx_rmsnorm": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _f, _p]),
     "slx_rmsnorm_lora": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _f, ctypes.POINTER(LoraDelta), _p]),
+    "slx_rmsnorm_fused": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _f, ctypes.POINTER(SplitKIn),
+                               ctypes.POINTER(LoraDelta), _p]),
     "slx_rope_kv_write": (_i, [_i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p, _i, _p]),
     "slx_attention": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p]),
     "slx_rope_attention_decode": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p,

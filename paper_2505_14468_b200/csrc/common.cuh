@@ -122,11 +122,11 @@ inline DeltaArgs delta_args(const slx_lora_delta* d) {
   }
   return a;
 }
-inline bool delta_valid(const slx_lora_delta* d) {
+inline bool delta_valid(const slx_lora_delta* d, bool v_optional = false) {
   if (d == nullptr) return true;
   if (d->n_targets < 0 || d->n_targets > SLX_LORA_MAX_TARGETS) return false;
   if (d->n_targets == 0) return true;
-  if (!d->v || !d->tok_slot || !d->slot_rank || !d->slot_scale || d->max_rank <= 0 || d->ldv <= 0)
+  if ((!d->v && !v_optional) || !d->tok_slot || !d->slot_rank || !d->slot_scale || d->max_rank <= 0 || (d->v && d->ldv <= 0))
     return false;
   // 16-byte v / B vectors: ldv, offsets, max_rank multiples of 4 / 8; v 16-byte aligned
   if (d->ldv % 4 || d->max_rank % 8 || (reinterpret_cast<uintptr_t>(d->v) & 15)) return false;
@@ -149,7 +149,7 @@ __device__ __forceinline__ DeltaTok delta_tok(const DeltaArgs& d, int t) {
   if (k.slot >= 0) {
     k.rank = min(d.slot_rank[k.slot], d.max_rank);
     k.scale = d.slot_scale[k.slot];
-    k.vrow = d.v + (size_t)t * d.ldv;
+    k.vrow = d.v ? d.v + (size_t)t * d.ldv : nullptr;
   }
   return k;
 }
@@ -286,6 +286,50 @@ __device__ __forceinline__ void l2_prefetch_part(const PfArgs& pf, int part, int
                    : "memory");
     }
   }
+}
+}  // namespace slx
+
+// ---------------------------------------------------------------- split-K pieces (slx_splitk_in)
+namespace slx {
+struct SplitArgs {
+  const float* part;
+  int splits, bm, n_main;
+};
+inline SplitArgs split_args(const slx_splitk_in* s) {
+  SplitArgs a{};
+  if (s) { a.part = s->part; a.splits = s->splits; a.bm = s->bm; a.n_main = s->n_main; }
+  return a;
+}
+// sum over the pieces (in order) of columns [col, col + 8) of row m (col % 8 == 0)
+__device__ __forceinline__ void split_sum8(const SplitArgs& sa, int m, int col, float* out) {
+  const size_t piece = (size_t)sa.bm * 256;
+  const float* p = sa.part + (size_t)(col >> 8) * sa.splits * piece +
+                   ((size_t)((col & 255) >> 4) * sa.bm + m) * 16 + (col & 15);
+  float4 q[16][2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i < sa.splits) {
+      q[i][0] = __ldcg(reinterpret_cast<const float4*>(p + i * piece));
+      q[i][1] = __ldcg(reinterpret_cast<const float4*>(p + i * piece) + 1);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) out[e] = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    if (i < sa.splits) {
+      out[0] += q[i][0].x; out[1] += q[i][0].y; out[2] += q[i][0].z; out[3] += q[i][0].w;
+      out[4] += q[i][1].x; out[5] += q[i][1].y; out[6] += q[i][1].z; out[7] += q[i][1].w;
+    }
+  }
+}
+__device__ __forceinline__ float split_sum1(const SplitArgs& sa, int m, int col) {
+  const size_t piece = (size_t)sa.bm * 256;
+  const float* p = sa.part + (size_t)(col >> 8) * sa.splits * piece +
+                   ((size_t)((col & 255) >> 4) * sa.bm + m) * 16 + (col & 15);
+  float s = 0.f;
+  for (int i = 0; i < sa.splits; ++i) s += __ldcg(p + i * piece);
+  return s;
 }
 }  // namespace slx
 

@@ -21,7 +21,11 @@ struct SkCall {
   const void* R; int ldr; int M, N, K, epilogue, n_main; void* C2; int ldc2;
   void* ws; size_t ws_bytes; void* stream; unsigned long long* trace;
   const slx_l2_prefetch* pf;
+  float* part_out;    // slx_gemm_bf16_splitk: pieces out (no epilogue), `splits` per tile
+  int splits;
+  size_t part_bytes;
 };
 int gemm_sk_launch(const SkCall& c);
 size_t gemm_sk_workspace_bytes(int M, int N, int K);
+size_t gemm_sk_splitk_bytes(int M, int N, int splits);
 }  // namespace slx

@@ -62,6 +62,7 @@ struct SkArgs {
   uint32_t* cnt; // [n_tiles][2]: arrivals, departures (monotonic; A == D between launches)
   unsigned long long* trace;
   PfArgs pf;     // L2 prefetch of the next kernel's first bytes, after our last TMA issue
+  int part_only; // slx_gemm_bf16_splitk: every piece written to `part`, reduced by the consumer
 };
 
 __device__ __forceinline__ unsigned long long sk_timer() {
@@ -359,7 +360,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
         const int tile = u / kb, k0 = u - tile * kb;
         const int k1 = min(kb, k0 + (hi - u));
         u += k1 - k0;
-        if (!(k0 == 0 && k1 == kb)) base[j] = tc::ld_relaxed_gpu(&g.cnt[2 * tile + 1]);
+        if (!(k0 == 0 && k1 == kb) && !g.part_only) base[j] = tc::ld_relaxed_gpu(&g.cnt[2 * tile + 1]);
       }
     }
 
@@ -376,7 +377,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       tc::fence_after_sync();
       if (j == 0 && et == 0) SK_TR(5);
       const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * SK_BN);
-      const bool whole = k0 == 0 && k1 == kb;
+      const bool whole = k0 == 0 && k1 == kb && !g.part_only;
       if (whole) {
         if (qlive) {
           const int m = r;
@@ -432,11 +433,14 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       if (et == 0) {
         tc::mbar_arrive(&tempty[acc]);
         // release at gpu scope after the CTA barrier publishes every thread's piece stores
-        if (!whole) tc::red_release_gpu_add(&g.cnt[2 * tile], 1u);
+        if (!whole && !g.part_only) tc::red_release_gpu_add(&g.cnt[2 * tile], 1u);
       }
     }
 
     // phase 2: wait for every split tile held, then reduce this CTA's slice of each
+    if (g.part_only) {   // the consumer reduces the pieces (no rendezvous, no tail)
+      if (et == 0) SK_TR(8);
+    } else {
     if (et == 0) {
       SK_TR(6);
       int jj = 0;
@@ -524,6 +528,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       if (et == 0) atomicAdd(&g.cnt[2 * tile + 1], 1);
     }
     if (et == 0) SK_TR(8);
+    }
   }
 
   if (warp < 2 && g.cs > 1) {   // producer / MMA warps join the epilogue's cluster barriers
@@ -652,15 +657,30 @@ int sk_max_clusters(size_t smem, int cluster) {
 
 }  // namespace
 
+size_t gemm_sk_splitk_bytes(int M, int N, int splits) {
+  if (M <= 0 || M > SK_MAX_M || N <= 0 || splits < 1) return 0;
+  return (size_t)ceil_div(N, SK_BN) * splits * ((M + 15) / 16 * 16) * SK_BN * 4;
+}
+
 size_t gemm_sk_workspace_bytes(int M, int N, int K) {
   SkPlan p{};
   return sk_plan(M, N, K, &p) ? p.ws : 0;
 }
 
 int gemm_sk_launch(const SkCall& c) {
-  if (env_int("SLX_GEMM_SK", 1) == 0 || c.ws == nullptr) return SLX_ERR_UNSUPPORTED;
   SkPlan p{};
-  if (!sk_plan(c.M, c.N, c.K, &p) || p.ws > c.ws_bytes) return SLX_ERR_UNSUPPORTED;
+  if (c.part_out != nullptr) {
+    // split-K pieces for the consumer: G = n_tiles * splits, every CTA exactly one piece
+    if (!sk_plan(c.M, c.N, c.K, &p)) return SLX_ERR_UNSUPPORTED;
+    if (c.splits < 1 || c.splits > 16 || p.kblocks / c.splits < 1) return SLX_ERR_INVALID;
+    p.G = p.n_tiles * c.splits;
+    p.pmax = c.splits;
+    p.cs = 1;
+    if ((size_t)p.n_tiles * c.splits * p.bm * SK_BN * 4 > c.part_bytes) return SLX_ERR_WORKSPACE;
+  } else {
+    if (env_int("SLX_GEMM_SK", 1) == 0 || c.ws == nullptr) return SLX_ERR_UNSUPPORTED;
+    if (!sk_plan(c.M, c.N, c.K, &p) || p.ws > c.ws_bytes) return SLX_ERR_UNSUPPORTED;
+  }
   if (env_int("SLX_GEMM_DEBUG", 0))
     fprintf(stderr, "[slx_gemm_sk] M=%d N=%d K=%d epi=%d bm=%d stages=%d G=%d tiles=%d kb=%d pmax=%d cluster=%d\n",
             c.M, c.N, c.K, c.epilogue, p.bm, p.stages, p.G, p.n_tiles, p.kblocks, p.pmax, p.cs);
@@ -672,6 +692,10 @@ int gemm_sk_launch(const SkCall& c) {
   a.C2 = (float*)c.C2; a.ldc2 = c.ldc2;
   a.cnt = (uint32_t*)c.ws;
   a.part = (float*)((char*)c.ws + SK_PART_OFF);
+  if (c.part_out != nullptr) {
+    a.part = c.part_out;
+    a.part_only = 1;
+  }
   a.trace = c.trace;
   a.pf = pf_args(c.pf);
   CUtensorMap mx, mw;

@@ -687,7 +687,7 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
   if (ws) SLX_CHECK_ALIGN(ws, 256);
   if (w_layout == SLX_W_TILED) {   // decode: stream-K kernel (gemm_sk.cu) when it applies
     SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
-              ws, ws ? ws_bytes : 0, stream, g_trace, pf};
+              ws, ws ? ws_bytes : 0, stream, g_trace, pf, nullptr, 0, 0};
     const int st = gemm_sk_launch(sc);
     if (st != SLX_ERR_UNSUPPORTED) return st;
   }
@@ -720,6 +720,23 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
   dim3 grid((unsigned)(p.n_tiles * p.splits), (unsigned)p.m_tiles);
   return dispatch_tc(epilogue, c_dtype, p.bn, mx, mw, a, grid, p.smem,
                      p.gsplit ? 1u : (unsigned)p.splits, (cudaStream_t)stream);
+}
+
+extern "C" size_t slx_gemm_splitk_bytes(int M, int N, int splits) {
+  return gemm_sk_splitk_bytes(M, N, splits);
+}
+
+extern "C" int slx_gemm_bf16_splitk(const void* A, int lda, const void* W, int M, int N, int K,
+                                    int splits, float* part, size_t part_bytes,
+                                    const slx_l2_prefetch* pf, void* stream) {
+  SLX_CHECK_ARG(A && W && part && M > 0 && N > 0 && K > 0 && lda >= K && K % 8 == 0 &&
+                lda % 8 == 0 && N % 16 == 0 && splits >= 1);
+  SLX_CHECK_ALIGN(A, 16);
+  SLX_CHECK_ALIGN(W, 16);
+  SLX_CHECK_ALIGN(part, 16);
+  SkCall sc{A, lda, W, nullptr, 0, SLX_DT_BF16, nullptr, 0, M, N, K, SLX_EPI_NONE, N, nullptr, 0,
+            nullptr, 0, stream, g_trace, pf, part, splits, part_bytes};
+  return gemm_sk_launch(sc);
 }
 
 // ------------------------------------------------------------------ weight packing

@@ -148,7 +148,8 @@ template <typename T>
 __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict__ out, int ldo,
                                                                    T* __restrict__ x, int ldx,
                                                                    const bf16* __restrict__ w,
-                                                                   int d, float eps, DeltaArgs lora) {
+                                                                   int d, float eps, DeltaArgs lora,
+                                                                   SplitArgs sk) {
   __shared__ float vs[DELTA_VS];
   __shared__ float red[8];
   const int t = blockIdx.x / RNL_CL, cr = blockIdx.x % RNL_CL;
@@ -165,16 +166,36 @@ __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict
   pdl_trigger();
   float f[8];
   Vec8<T>::load(xr + i0, f);
+  if (sk.part != nullptr) {   // the projection's residual epilogue: round(x + sum of pieces)
+    float ps[8];
+    split_sum8(sk, t, i0, ps);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + ps[j]));
+    if (dt.slot < 0) Vec8<T>::store(xr + i0, f);
+  }
   if (fast) {
-    delta_stage_v(lora, dt, vs, threadIdx.x, blockDim.x);
+    if (lora.v == nullptr) {   // LoRA v from the pieces' stacked columns
+      for (int e = threadIdx.x; e < lora.n_targets * 64; e += blockDim.x) {
+        const int i = e >> 6, j = e & 63;
+        int off = 0;
+#pragma unroll
+        for (int q = 0; q < SLX_LORA_MAX_TARGETS; ++q)
+          if (q == i) off = lora.v_col_off[q];
+        if (j < dt.rank) vs[e] = split_sum1(sk, t, sk.n_main + off + dt.slot * lora.max_rank + j) * dt.scale;
+      }
+    } else {
+      delta_stage_v(lora, dt, vs, threadIdx.x, blockDim.x);
+    }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + delta_finish<2>(dt, dr[j], vs)));
     Vec8<T>::store(xr + i0, f);
-  } else if (dt.slot >= 0) {
+  } else if (dt.slot >= 0 && lora.v != nullptr) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + delta_col(lora, dt, i0 + j)));
     Vec8<T>::store(xr + i0, f);
+  } else if (dt.slot >= 0 && sk.part != nullptr) {
+    Vec8<T>::store(xr + i0, f);   // rank > 16 with v in the pieces: not fused (host rejects)
   }
   float ss = 0.f;
 #pragma unroll
@@ -743,11 +764,36 @@ extern "C" int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx,
   const char* e = getenv("SLX_RMSNORM_CLUSTER");
   if (d % (RNL_CL * 8 * 32) == 0 && d / (RNL_CL * 8) <= 128 && !(e && e[0] == '0')) {
     const int thr = d / (RNL_CL * 8);
-    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la));
+    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, SplitArgs{}));
     return st;
   }
   int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
   DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_kernel<T>, dim3(n_tok), dim3(threads), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la));
+  return st;
+}
+
+extern "C" int slx_rmsnorm_fused(int dtype, void* out, int ldo, void* x, int ldx, const void* w,
+                                 int n_tok, int d, float eps, const slx_splitk_in* sk,
+                                 const slx_lora_delta* lora, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && d > 0 && ldo % 8 == 0 && ldx % 8 == 0 && ldo >= d && ldx >= d &&
+                out && x && w && delta_valid(lora, sk != nullptr));
+  SLX_CHECK_ALIGN(out, 16);
+  SLX_CHECK_ALIGN(x, 16);
+  SLX_CHECK_ALIGN(w, 16);
+  if (sk != nullptr) {
+    SLX_CHECK_ARG(sk->part && sk->splits >= 1 && sk->splits <= 16 && sk->bm >= n_tok &&
+                  sk->bm % 16 == 0 && sk->n_main >= d);
+    SLX_CHECK_ALIGN(sk->part, 16);
+    if (lora && lora->n_targets > 0 && lora->v == nullptr && lora->max_rank > 16)
+      return SLX_ERR_UNSUPPORTED;
+  }
+  if (d % (RNL_CL * 8 * 32) != 0 || d / (RNL_CL * 8) > 128) return SLX_ERR_UNSUPPORTED;
+  if (n_tok == 0) return SLX_OK;
+  const DeltaArgs la = delta_args(lora);
+  const SplitArgs sa = split_args(sk);
+  const int thr = d / (RNL_CL * 8);
+  int st = SLX_OK;
+  DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, sa));
   return st;
 }
 

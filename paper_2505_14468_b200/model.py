@@ -195,6 +195,9 @@ class MultiLoraModel:
         self.use_stacked_decode = bool(self.stack)
         # decode: q/k/v expand fused into the attention kernel, o expand into the post-norm
         self.fuse_expand = True
+        # decode: o / down projections as split-K pieces reduced by the following RMSNorm
+        self.splitk_consumer = os.environ.get("SLX_SPLITK_CONSUMER", "1") != "0"
+        self.splitk_splits = int(os.environ.get("SLX_SPLITK_SPLITS", "8"))
         # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off)
         self.l2_prefetch_mb = float(os.environ.get("SLX_L2_PF_MB", "16"))
         self._pf_cache: dict = {}
@@ -491,13 +494,26 @@ class MultiLoraModel:
                 and self.use_tc_sgmv and not (self.use_stacked_decode and T <= 128)):
             sgmv_plan = self._sgmv_plan(segments, slot.cpu().numpy())
             v_buf = torch.empty((T, 64), dtype=dt, device=dev)
+        # decode: o / down as split-K pieces reduced by the next RMSNorm (no GEMM reduction tail)
+        sk_mode = (decode and dt == torch.bfloat16 and self.splitk_consumer and T <= 64
+                   and d % 2048 == 0 and self.pool.max_rank <= 16)
+        if sk_mode:
+            S = self.splitk_splits
+            part_o = torch.empty(ops.splitk_bytes(T, d + self._extra_rows("wo"), S) // 4,
+                                 dtype=torch.float32, device=dev)
+            part_dn = torch.empty(ops.splitk_bytes(T, d, S) // 4, dtype=torch.float32, device=dev)
+        pending = None   # split-K pieces of the down projection, consumed by the next norm
         ops.embedding(x, w["embed"], tokens)
         if self.targets:
             ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
         qkv_cols = {"q": (0, qd, qd), "k": (qd, kvd, kvd), "v": (qd + kvd, kvd, kvd)}
         for l in range(cfg.layers):
             p = f"layers.{l}."
-            ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
+            if pending is not None:
+                ops.rmsnorm_fused(h, x, w[p + "input_norm"], cfg.rms_eps, pending)
+                pending = None
+            else:
+                ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
             d_qkv = None
             pfd = decode and dt == torch.bfloat16
             nxt = f"layers.{l + 1}.w_qkv" if l + 1 < cfg.layers else "lm_head"
@@ -531,7 +547,12 @@ class MultiLoraModel:
                     ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
                                   self.k_cache[l], self.v_cache[l])
             d_o = None
-            if stacked and "wo" in self.stack:
+            if sk_mode and "wo" in self.stack:
+                sk_o = ops.gemm_splitk(attn, w[p + "wo"], S, part_o, prefetch=pf_o)
+                d_o = self._delta(l, "wo", None, slot, {"o": (0, d, d)})
+                ops.rmsnorm_fused(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o)
+                d_o = "done"
+            elif stacked and "wo" in self.stack:
                 ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o,
                          prefetch=pf_o)
                 if decode and self.fuse_expand:
@@ -543,7 +564,9 @@ class MultiLoraModel:
                 if not (sgmv_plan is not None and
                         self._sgmv_tc(x, attn, l, ("o",), {"o": (0, d, d)}, sgmv_plan, v_buf)):
                     self._lora(x, attn, l, ("o",), {"o": (0, d, d)})
-            if d_o is not None:
+            if d_o == "done":
+                pass
+            elif d_o is not None:
                 ops.rmsnorm_lora(h, x, w[p + "post_norm"], cfg.rms_eps, d_o)
             else:
                 ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
@@ -553,11 +576,20 @@ class MultiLoraModel:
                 self._gemm(h, w[p + "w_gu"], gu)
                 self._lora(gu, h, l, ("gate", "up"), {"gate": (0, 128, 256), "up": (128, 128, 256)})
                 ops.silu_mul_blocked(mlp, gu, self.ffn_pad)
-            self._gemm(mlp, w[p + "w_down"], x, residual=x, prefetch=pf_dn)
-            self._lora(x, mlp, l, ("down",), {"down": (0, d, d)}, d_in=cfg.ffn)
-        rows = x if logit_rows is None else x.index_select(0, logit_rows)
-        hn = torch.empty_like(rows)
-        ops.rmsnorm(hn, rows, w["final_norm"], cfg.rms_eps)
+            if sk_mode and "down" not in self.targets:
+                pending = ops.gemm_splitk(mlp, w[p + "w_down"], S, part_dn, prefetch=pf_dn)
+            else:
+                self._gemm(mlp, w[p + "w_down"], x, residual=x, prefetch=pf_dn)
+                self._lora(x, mlp, l, ("down",), {"down": (0, d, d)}, d_in=cfg.ffn)
+        if pending is not None:
+            hn = torch.empty_like(x)
+            ops.rmsnorm_fused(hn, x, w["final_norm"], cfg.rms_eps, pending)
+            if logit_rows is not None:
+                hn = hn.index_select(0, logit_rows)
+        else:
+            rows = x if logit_rows is None else x.index_select(0, logit_rows)
+            hn = torch.empty_like(rows)
+            ops.rmsnorm(hn, rows, w["final_norm"], cfg.rms_eps)
         if dt == torch.bfloat16:
             return self._gemm(hn, w["lm_head"], out_dtype=torch.float32)
         return self._gemm(hn, w["lm_head"])

@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import (DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED,
-                   L2Prefetch, LoraDelta, LoraTarget, check)
+                   L2Prefetch, LoraDelta, LoraTarget, SplitKIn, check)
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
 
@@ -352,19 +352,54 @@ def rmsnorm(out, x, w, eps: float):
     return out
 
 
-def make_delta(v_all: torch.Tensor, tok_slot, slot_rank, slot_scale, max_rank: int, targets):
+def make_delta(v_all: torch.Tensor | None, tok_slot, slot_rank, slot_scale, max_rank: int, targets):
     """slx_lora_delta for a fused decode expand.  targets: [(b_ptr_table, v_col_off, y_col_off,
-    d_out)] (<= 4); v_all: the fp32 GEMM side output [n_tok, ldv]."""
+    d_out)] (<= 4); v_all: the fp32 GEMM side output [n_tok, ldv], or None when the consumer
+    takes v from split-K pieces (v_col_off then counts from the pieces' n_main)."""
     targets = list(targets)
-    if not 1 <= len(targets) <= 4 or v_all.dtype != torch.float32:
+    if not 1 <= len(targets) <= 4 or (v_all is not None and v_all.dtype != torch.float32):
         raise ValueError("make_delta: 1..4 targets and an fp32 v_all")
     d = LoraDelta()
-    d.v, d.ldv = v_all.data_ptr(), _ld(v_all)
+    if v_all is not None:
+        d.v, d.ldv = v_all.data_ptr(), _ld(v_all)
     d.tok_slot, d.slot_rank, d.slot_scale = tok_slot.data_ptr(), slot_rank.data_ptr(), slot_scale.data_ptr()
     d.max_rank, d.n_targets = max_rank, len(targets)
     for i, (b, voff, yoff, dout) in enumerate(targets):
         d.b_ptrs[i], d.v_col_off[i], d.y_col_off[i], d.d_out[i] = b.data_ptr(), voff, yoff, dout
     return d
+
+
+def splitk_bytes(M: int, N: int, splits: int) -> int:
+    return _lib.load().slx_gemm_splitk_bytes(M, N, splits)
+
+
+@_op("gemm", 1)
+def gemm_splitk(a: torch.Tensor, w, splits: int, part: torch.Tensor, prefetch=None) -> SplitKIn:
+    """Decode projection as split-K pieces (no epilogue) for the consuming kernel; returns the
+    slx_splitk_in describing them.  w: PackedWeight (main + stacked rows)."""
+    if a.dtype != torch.bfloat16 or not isinstance(w, PackedWeight):
+        raise ValueError("gemm_splitk: bf16 activations and a packed weight")
+    M, K = a.shape
+    N = w.n + w.n_extra
+    check(_lib.load().slx_gemm_bf16_splitk(_ptr(a), _ld(a), _ptr(w.data), M, N, K, splits,
+                                           _ptr(part), part.numel() * part.element_size(),
+                                           None if prefetch is None else ctypes.byref(prefetch),
+                                           _stream()), "slx_gemm_bf16_splitk")
+    sk = SplitKIn()
+    sk.part, sk.splits, sk.bm, sk.n_main = part.data_ptr(), splits, (M + 15) // 16 * 16, w.n
+    return sk
+
+
+@_op("rmsnorm", 1)
+def rmsnorm_fused(out, x, w, eps: float, sk=None, delta=None):
+    """x = round(x + split-K pieces) (the projection's residual epilogue), x += LoRA delta
+    (v from the pieces when the delta has no v), out = rmsnorm(x)."""
+    check(_lib.load().slx_rmsnorm_fused(_dt(out), _ptr(out), _ld(out), _ptr(x), _ld(x), _ptr(w),
+                                        x.shape[0], w.numel(), float(eps),
+                                        None if sk is None else ctypes.byref(sk),
+                                        None if delta is None else ctypes.byref(delta), _stream()),
+          "slx_rmsnorm_fused")
+    return out
 
 
 @_op("rmsnorm", 1)

@@ -412,6 +412,32 @@ def test_rmsnorm_lora_cluster(d, rank, monkeypatch):
     torch.testing.assert_close(res["1"][1].float(), hr, rtol=2e-2, atol=2e-2)
 
 
+@pytest.mark.parametrize("M,N,K,splits", [(64, 4608, 4096, 8), (17, 4096, 11008, 8), (1, 512, 256, 3)])
+def test_gemm_splitk_pieces_and_consumer(M, N, K, splits):
+    """Split-K pieces (slx_gemm_bf16_splitk) sum to the fp32 product in the documented layout;
+    the fused RMSNorm consumer reproduces residual add + norm."""
+    g = torch.Generator(device=DEV).manual_seed(M + N)
+    a = bf(torch.randn(M, K, device=DEV, generator=g))
+    w = bf(torch.randn(N, K, device=DEV, generator=g) * 0.05)
+    ref = a.float() @ w.float().T
+    pw = ops.pack_weight(w)
+    part = torch.empty(ops.splitk_bytes(M, N, splits) // 4, device=DEV)
+    sk = ops.gemm_splitk(a, pw, splits, part)
+    bm = (M + 15) // 16 * 16
+    pc = part.view(-1, splits, 16, bm, 16)[: (N + 255) // 256]    # [tile][piece][chunk][row][16]
+    got = pc.sum(1).permute(2, 0, 1, 3).reshape(bm, -1)[:M, :N]
+    torch.testing.assert_close(got, ref, rtol=1e-4, atol=1e-3)
+    if N % 2048 == 0 and N <= 8192:
+        x0 = bf(torch.randn(M, N, device=DEV, generator=g))
+        wn = bf(torch.rand(N, device=DEV, generator=g) + 0.5)
+        x, h = x0.clone(), torch.empty_like(x0)
+        ops.rmsnorm_fused(h, x, wn, 1e-5, sk)
+        xr = (x0.float() + ref).bfloat16().float()
+        torch.testing.assert_close(x.float(), xr, rtol=1e-2, atol=2e-2)
+        hr = xr * torch.rsqrt(xr.pow(2).mean(-1, keepdim=True) + 1e-5) * wn.float()
+        torch.testing.assert_close(h.float(), hr, rtol=2e-2, atol=2e-2)
+
+
 @pytest.mark.parametrize("M", [1, 64, 300])
 def test_gemm_lora_side_output(M):
     """Stacked extra rows of a packed weight land, in fp32, in the side output; the main

@@ -147,6 +147,35 @@ def test_bf16_stacked_decode_shrink_matches_sgmv_path(golden):
     np.testing.assert_allclose(ev[1], ev2[1], rtol=1e-2, atol=1e-2)
 
 
+def test_bf16_decode_splitk_consumer_matches_oracle():
+    """Decode with the o / down projections as split-K pieces reduced by the following RMSNorm
+    (residual epilogue, o-LoRA v and delta fused there) == the GEMM-side reduction == oracle."""
+    from paper_2505_14468_b200.config import BackboneConfig
+    cfg = BackboneConfig("w2048", hidden=2048, layers=2, heads=16, kv_heads=16, head_dim=128,
+                         ffn=2048, vocab=1000)
+    w = init_backbone(cfg, 11)
+    loras = [LoraConfig(16, 32.0), LoraConfig(8, 16.0), LoraConfig(16, 8.0)]
+    ads = [init_adapter(cfg, lo, 11, a) for a, lo in enumerate(loras)]
+    prompts = [[5, 9, 200, 31], [7, 7, 7], [100, 2, 3, 4, 5], [9], [44, 45]]
+    ids = [0, 1, 2, -1, 1]
+    toks = [11, 12, 13, 14, 15]
+    out = {}
+    for sk in (True, False):
+        m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=8, max_ctx=64, n_slots=4,
+                           max_rank=16, max_tokens=256)
+        m.splitk_consumer = sk
+        m.load_backbone(w)
+        for a, (ad, lo) in enumerate(zip(ads, loras)):
+            m.pool.load(a, ad, lo)
+        seqs, _ = m.prefill(prompts, ids)
+        out[sk] = m.decode(seqs, toks, ids).cpu().numpy()
+    np.testing.assert_allclose(out[True], out[False], rtol=2e-2, atol=2e-2)
+    orc = OracleModel(cfg, w, ads, [lo.scale for lo in loras], loras[0].targets)
+    orc.prefill(prompts, ids)
+    ref = orc.decode(list(range(len(prompts))), toks, ids)
+    np.testing.assert_allclose(out[True], ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
 def test_bf16_prefill_tc_path_matches_oracle():
     """Prefill with the tensor-core paths (flash attention, SGMV as grouped tcgen05 GEMMs) on a
     head_dim-128 GQA model with mixed adapter ranks {8,16,64} == SIMT paths == oracle."""
