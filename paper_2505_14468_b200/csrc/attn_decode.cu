@@ -23,6 +23,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "gemm_host.h"
 #include "tc_ptx.cuh"
 
 namespace slx {
@@ -56,7 +57,14 @@ struct AdArgs {
   PfArgs pf;
   int pf_early;   // SLX_ATTN_PF_EARLY=1: prefetch at kernel start instead of after the last item
   int dbg_stream; // SLX_ATTN_DBG_STREAM=1 (debug): consumers only drain the rings (copy roofline)
+  unsigned long long* trace;   // slx_debug_gemm_trace timeline window (nullptr: off)
 };
+
+__device__ __forceinline__ unsigned long long ad_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
+  return t;
+}
 
 struct ItemMeta {
   const bf16* b[3];   // B rows of the three parts' column ranges
@@ -123,6 +131,10 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs 
 
   const int tid = threadIdx.x;
   const int n_items = a.n_tok * a.H;
+  if (tid == 0 && a.trace) {
+    a.trace[blockIdx.x * 16 + 0] = ad_timer();
+    if (blockIdx.x == 0) a.trace[4095] = 5;
+  }
   if (tid == 0) {
     for (int s = 0; s < AD_STAGES; ++s) {
       tc::mbar_init(&kv_full[s], 1);
@@ -200,6 +212,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs 
           if (a.pf_early) l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);
           pdl_wait();
           pdl_trigger();
+          if (a.trace) a.trace[blockIdx.x * 16 + 2] = ad_timer();
         }
         for (int i = 0; i < nloc; ++i, ++j) {
           const ItemMeta& mt = meta[i];
@@ -452,6 +465,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs 
     }
     group_sync(g);   // scratch reused by the group's next item
   }
+  if (gt == 0 && a.trace) a.trace[blockIdx.x * 16 + 7 + g] = ad_timer();
 }
 
 }  // namespace
@@ -471,6 +485,7 @@ int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int
   a.pf_early = (e && e[0] == '1') ? 1 : 0;
   const char* ed = getenv("SLX_ATTN_DBG_STREAM");
   a.dbg_stream = (ed && ed[0] == '1') ? 1 : 0;
+  a.trace = next_trace_window(5);
   const int items = n_tok * heads;
   const int grid = items < sm_count() ? items : sm_count();
   auto go = [&](auto kernel, size_t smem) -> int {

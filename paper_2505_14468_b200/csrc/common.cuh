@@ -305,21 +305,23 @@ __device__ __forceinline__ void split_sum8(const SplitArgs& sa, int m, int col, 
   const size_t piece = (size_t)sa.bm * 256;
   const float* p = sa.part + (size_t)(col >> 8) * sa.splits * piece +
                    ((size_t)((col & 255) >> 4) * sa.bm + m) * 16 + (col & 15);
-  float4 q[16][2];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    if (i < sa.splits) {
-      q[i][0] = __ldcg(reinterpret_cast<const float4*>(p + i * piece));
-      q[i][1] = __ldcg(reinterpret_cast<const float4*>(p + i * piece) + 1);
-    }
-  }
 #pragma unroll
   for (int e = 0; e < 8; ++e) out[e] = 0.f;
+  for (int i0 = 0; i0 < sa.splits; i0 += 8) {   // pieces in order, 8 loads in flight
+    float4 q[8][2];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    if (i < sa.splits) {
-      out[0] += q[i][0].x; out[1] += q[i][0].y; out[2] += q[i][0].z; out[3] += q[i][0].w;
-      out[4] += q[i][1].x; out[5] += q[i][1].y; out[6] += q[i][1].z; out[7] += q[i][1].w;
+    for (int i = 0; i < 8; ++i) {
+      if (i0 + i < sa.splits) {
+        q[i][0] = __ldcg(reinterpret_cast<const float4*>(p + (i0 + i) * piece));
+        q[i][1] = __ldcg(reinterpret_cast<const float4*>(p + (i0 + i) * piece) + 1);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i0 + i < sa.splits) {
+        out[0] += q[i][0].x; out[1] += q[i][0].y; out[2] += q[i][0].z; out[3] += q[i][0].w;
+        out[4] += q[i][1].x; out[5] += q[i][1].y; out[6] += q[i][1].z; out[7] += q[i][1].w;
+      }
     }
   }
 }

@@ -26,6 +26,9 @@ struct SkCall {
   size_t part_bytes;
 };
 int gemm_sk_launch(const SkCall& c);
+// Debug timeline window for the next traced launch (nullptr when tracing is off); kinds:
+// 1-3 GEMM (epilogue + 1), 4 split-K GEMM, 5 decode attention.
+unsigned long long* next_trace_window(int kind);
 size_t gemm_sk_workspace_bytes(int M, int N, int K);
 size_t gemm_sk_splitk_bytes(int M, int N, int splits);
 }  // namespace slx

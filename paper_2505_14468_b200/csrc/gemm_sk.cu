@@ -155,6 +155,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
 
   if (threadIdx.x == 0) {
     SK_TR(0);
+    if (g.trace && blockIdx.x == 0) g.trace[4095] = g.part_only ? 4 : 1 + EPI;
     tc::tma_prefetch_desc(&tmap_x);
     tc::tma_prefetch_desc(&tmap_w);
     for (int s = 0; s < g.stages; ++s) {

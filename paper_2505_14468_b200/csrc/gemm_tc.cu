@@ -630,12 +630,23 @@ static int dispatch_tc(int epi, int c_dtype, int bn, const CUtensorMap& mx, cons
 
 using namespace slx;
 
-static unsigned long long* g_trace = nullptr;
+static unsigned long long* g_trace_base = nullptr;
+static unsigned g_trace_launch = 0;
+// Debug timeline: every traced launch gets its own 4096-slot window (<= 256 CTAs x 16 stamps)
+// and records its kind in the window's last slot.
+namespace slx {
+unsigned long long* next_trace_window(int kind) {
+  if (g_trace_base == nullptr) return nullptr;
+  (void)kind;   // the kernel writes its kind into the window's last slot
+  return g_trace_base + (size_t)(g_trace_launch++) * 4096;
+}
+}  // namespace slx
 // Debug: every following slx_gemm_bf16 launch records 8 globaltimer stamps per CTA into buf
 // ([grid CTAs][8] u64: entry, prologue done, producer past PDL wait, first stage landed, last MMA
 // issued, accumulator ready, split-K rendezvous passed, exit).  NULL turns it off.
 extern "C" int slx_debug_gemm_trace(void* buf) {
-  g_trace = (unsigned long long*)buf;
+  g_trace_base = (unsigned long long*)buf;
+  g_trace_launch = 0;
   return SLX_OK;
 }
 
@@ -687,7 +698,7 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
   if (ws) SLX_CHECK_ALIGN(ws, 256);
   if (w_layout == SLX_W_TILED) {   // decode: stream-K kernel (gemm_sk.cu) when it applies
     SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
-              ws, ws ? ws_bytes : 0, stream, g_trace, pf, nullptr, 0, 0};
+              ws, ws ? ws_bytes : 0, stream, next_trace_window(1 + epilogue), pf, nullptr, 0, 0};
     const int st = gemm_sk_launch(sc);
     if (st != SLX_ERR_UNSUPPORTED) return st;
   }
@@ -706,7 +717,7 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
   a.C2 = (float*)C2;
   a.ldc2 = ldc2;
   a.gsplit = p.gsplit;
-  a.trace = g_trace;
+  a.trace = nullptr;
   if (p.gsplit) {
     a.ws_cnt = (int*)((char*)ws + 32768);   // [tiles][2]: arrival, departure ([0,32K): gemm_sk)
     a.ws_part = (float*)((char*)ws + GS_CNT_BYTES);
@@ -735,7 +746,7 @@ extern "C" int slx_gemm_bf16_splitk(const void* A, int lda, const void* W, int M
   SLX_CHECK_ALIGN(W, 16);
   SLX_CHECK_ALIGN(part, 16);
   SkCall sc{A, lda, W, nullptr, 0, SLX_DT_BF16, nullptr, 0, M, N, K, SLX_EPI_NONE, N, nullptr, 0,
-            nullptr, 0, stream, g_trace, pf, part, splits, part_bytes};
+            nullptr, 0, stream, next_trace_window(4), pf, part, splits, part_bytes};
   return gemm_sk_launch(sc);
 }
 

@@ -6,6 +6,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "gemm_host.h"
 
 namespace slx {
 
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(512) rmsnorm_lora_kernel(T* __restrict__ out, 
   }
 }
 
+constexpr int AD_LORA_FAST_RANK = 16;
 // Cluster variant: one 8-CTA cluster per token, each CTA d/8 columns (8 per thread), the
 // sum of squares reduced over the cluster through DSMEM in a fixed rank order.  Spreads the
 // o-projection B rows (d x rank per token) over 8 SMs instead of one.
@@ -149,9 +151,19 @@ __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict
                                                                    T* __restrict__ x, int ldx,
                                                                    const bf16* __restrict__ w,
                                                                    int d, float eps, DeltaArgs lora,
-                                                                   SplitArgs sk) {
+                                                                   SplitArgs sk,
+                                                                   unsigned long long* trace) {
   __shared__ float vs[DELTA_VS];
   __shared__ float red[8];
+  auto stamp = [&](int i) {
+    if (trace && threadIdx.x == 0) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt)::"memory");
+      trace[(blockIdx.x % 256) * 16 + i] = tt;
+      if (blockIdx.x == 0 && i == 0) trace[4095] = 6;
+    }
+  };
+  stamp(0);
   const int t = blockIdx.x / RNL_CL, cr = blockIdx.x % RNL_CL;
   const int i0 = cr * (d / RNL_CL) + threadIdx.x * 8;
   T* xr = x + (size_t)t * ldx;
@@ -164,6 +176,7 @@ __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict
   }
   pdl_wait();
   pdl_trigger();
+  stamp(2);
   float f[8];
   Vec8<T>::load(xr + i0, f);
   if (sk.part != nullptr) {   // the projection's residual epilogue: round(x + sum of pieces)
@@ -208,7 +221,9 @@ __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) c += red[q];
     red[4] = c;   // this CTA's partial
   }
+  stamp(3);
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  stamp(4);
   float tot = 0.f;
   {
     const uint32_t a_local = static_cast<uint32_t>(__cvta_generic_to_shared(&red[4]));
@@ -229,6 +244,88 @@ __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict
   Vec8<T>::store(out + (size_t)t * ldo + i0, f);
   // keep red[4] alive until every peer has read it
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  stamp(7);
+}
+
+// One CTA per token (d / 8 threads, 8 columns each): the same fused residual-pieces + LoRA +
+// RMSNorm without a cluster, so it launches as one small wave and its CTAs can start early
+// under PDL.  The LoRA B rows are loaded after the pieces (register budget at 512+ threads).
+template <typename T>
+__global__ void __launch_bounds__(640) rmsnorm_fused_tok_kernel(T* __restrict__ out, int ldo,
+                                                                 T* __restrict__ x, int ldx,
+                                                                 const bf16* __restrict__ w, int d,
+                                                                 float eps, DeltaArgs lora,
+                                                                 SplitArgs sk,
+                                                                 unsigned long long* trace) {
+  __shared__ float vs[DELTA_VS];
+  __shared__ float red[33];
+  auto stamp = [&](int i) {
+    if (trace && threadIdx.x == 0) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt)::"memory");
+      trace[(blockIdx.x % 256) * 16 + i] = tt;
+      if (blockIdx.x == 0 && i == 0) trace[4095] = 6;
+    }
+  };
+  stamp(0);
+  const int t = blockIdx.x;
+  const int i0 = threadIdx.x * 8;
+  T* xr = x + (size_t)t * ldx;
+  const DeltaTok dt = delta_tok(lora, t);   // slot tables: >= 2 launches old
+  pdl_wait();
+  pdl_trigger();
+  stamp(2);
+  float f[8];
+  Vec8<T>::load(xr + i0, f);
+  if (sk.part != nullptr) {
+    float ps[8];
+    split_sum8(sk, t, i0, ps);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + ps[j]));
+  }
+  if (dt.slot >= 0 && dt.rank <= AD_LORA_FAST_RANK) {
+    if (lora.v == nullptr) {
+      for (int e = threadIdx.x; e < lora.n_targets * 64; e += blockDim.x) {
+        const int i = e >> 6, j = e & 63;
+        int off = 0;
+#pragma unroll
+        for (int q = 0; q < SLX_LORA_MAX_TARGETS; ++q)
+          if (q == i) off = lora.v_col_off[q];
+        if (j < dt.rank) vs[e] = split_sum1(sk, t, sk.n_main + off + dt.slot * lora.max_rank + j) * dt.scale;
+      }
+    } else {
+      delta_stage_v(lora, dt, vs, threadIdx.x, blockDim.x);
+    }
+    DeltaRow<2> dr[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) delta_prefetch<2>(lora, dt, i0 + j, dr[j]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + delta_finish<2>(dt, dr[j], vs)));
+  } else if (dt.slot >= 0 && lora.v != nullptr) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[j] = to_f32(from_f32<T>(f[j] + delta_col(lora, dt, i0 + j)));
+  }
+  if (sk.part != nullptr || dt.slot >= 0) Vec8<T>::store(xr + i0, f);
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) ss += f[j] * f[j];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;   // fixed order
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[32] = v;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[32] / (float)d + eps);
+  float g[8];
+  Vec8<bf16>::load(w + i0, g);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) f[j] = (f[j] * inv) * g[j];
+  Vec8<T>::store(out + (size_t)t * ldo + i0, f);
+  stamp(7);
 }
 
 // ------------------------------------------------------------------ RoPE + KV write
@@ -764,7 +861,7 @@ extern "C" int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx,
   const char* e = getenv("SLX_RMSNORM_CLUSTER");
   if (d % (RNL_CL * 8 * 32) == 0 && d / (RNL_CL * 8) <= 128 && !(e && e[0] == '0')) {
     const int thr = d / (RNL_CL * 8);
-    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, SplitArgs{}));
+    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, SplitArgs{}, next_trace_window(6)));
     return st;
   }
   int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
@@ -787,13 +884,21 @@ extern "C" int slx_rmsnorm_fused(int dtype, void* out, int ldo, void* x, int ldx
     if (lora && lora->n_targets > 0 && lora->v == nullptr && lora->max_rank > 16)
       return SLX_ERR_UNSUPPORTED;
   }
-  if (d % (RNL_CL * 8 * 32) != 0 || d / (RNL_CL * 8) > 128) return SLX_ERR_UNSUPPORTED;
   if (n_tok == 0) return SLX_OK;
   const DeltaArgs la = delta_args(lora);
   const SplitArgs sa = split_args(sk);
-  const int thr = d / (RNL_CL * 8);
   int st = SLX_OK;
-  DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, sa));
+  const char* e = getenv("SLX_RMSNORM_CLUSTER");
+  // default: the 8-CTA cluster kernel (measured faster in the decode graph); SLX_RMSNORM_CLUSTER=0
+  // or a d the cluster split cannot take: one CTA per token
+  const bool cl_ok = d % (RNL_CL * 8 * 32) == 0 && d / (RNL_CL * 8) <= 128;
+  if ((!cl_ok || (e && e[0] == '0')) && d % 256 == 0 && d / 8 <= 640 && (!sk || sk->splits <= 8)) {
+    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_fused_tok_kernel<T>, dim3(n_tok), dim3(d / 8), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, sa, next_trace_window(6)));
+    return st;
+  }
+  if (d % (RNL_CL * 8 * 32) != 0 || d / (RNL_CL * 8) > 128) return SLX_ERR_UNSUPPORTED;
+  const int thr = d / (RNL_CL * 8);
+  DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, sa, next_trace_window(6)));
   return st;
 }
 

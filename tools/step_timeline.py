@@ -1,0 +1,82 @@
+"""In-graph timeline of the decode step: GEMM and attention launches record globaltimer stamps
+(slx_debug_gemm_trace windows); prints per launch the first CTA entry, first data, last CTA exit
+relative to the step start and the gap to the next traced launch.  python tools/step_timeline.py"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2505_14468_b200 import _lib  # noqa: E402
+from paper_2505_14468_b200.config import LLAMA2_7B, LoraConfig  # noqa: E402
+from paper_2505_14468_b200.engine import DecodeGraph  # noqa: E402
+from paper_2505_14468_b200.model import MultiLoraModel  # noqa: E402
+
+lib = _lib.load()
+cfg = LLAMA2_7B
+lora = LoraConfig(bench.RANK, bench.ALPHA, ("q", "k", "v", "o"))
+m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=bench.BATCH, max_ctx=bench.CTX + 1,
+                   n_slots=bench.N_ADAPTERS, max_rank=bench.RANK, max_tokens=bench.BATCH)
+m.random_backbone(seed=0)
+for a in range(bench.N_ADAPTERS):
+    m.pool.load_random(a, lora, seed=1000 + a)
+seqs = [m.alloc_seq() for _ in range(bench.BATCH)]
+dg = DecodeGraph(m, seqs, bench.tok_slots().tolist(), fixed_pos=bench.CTX)
+dg.capture()      # untraced warm-up / plans
+buf = torch.zeros(200 * 4096, dtype=torch.int64, device="cuda")
+lib.slx_debug_gemm_trace(buf.data_ptr())
+dgt = DecodeGraph(m, seqs, bench.tok_slots().tolist(), fixed_pos=bench.CTX)
+dgt.capture()
+lib.slx_debug_gemm_trace(None)
+for _ in range(3):
+    dgt.replay()
+torch.cuda.synchronize()
+dgt.replay()
+torch.cuda.synchronize()
+t = buf.view(200, 4096).cpu().numpy()
+names = {1: "gemm", 2: "gemm+res", 3: "gemm+silu", 4: "gemm-splitk", 5: "attention", 6: "rmsnorm"}
+rows = []
+for i in range(200):
+    kind = int(t[i, 4095] & 0xffffffff)
+    if kind == 0:
+        continue
+    st = t[i, :4095 - 15].reshape(-1, 16)
+    st = st[st[:, 0] > 0]
+    if len(st) == 0:
+        continue
+    entry = st[:, 0].min()
+    if kind == 5:
+        exit_ = max(st[:, 7].max(), st[:, 8].max())
+        first = st[:, 2][st[:, 2] > 0].min() if (st[:, 2] > 0).any() else entry
+    elif kind == 6:
+        exit_ = st[:, 7].max()
+        first = st[:, 2].max()   # last CTA past the PDL wait
+    else:
+        exit_ = st[:, 7].max()
+        first = st[:, 3][st[:, 3] > 0].min() if (st[:, 3] > 0).any() else entry
+    rows.append((names.get(kind, str(kind)), entry, first, exit_, len(st)))
+rows = rows[-(7 * cfg.layers + 2):]   # the captured graph's launches (warm-up windows come first)
+t0 = rows[0][1]
+prev_end = None
+tot = {}
+print(f"{'kernel':12s} {'ctas':>5s} {'start':>9s} {'1st data':>9s} {'end':>9s} {'dur':>7s} {'gap':>7s}")
+for name, e, f, x, n in rows[:22]:
+    gap = (e - prev_end) / 1000 if prev_end is not None else 0.0
+    print(f"{name:12s} {n:5d} {(e - t0) / 1000:9.2f} {(f - t0) / 1000:9.2f} {(x - t0) / 1000:9.2f} "
+          f"{(x - e) / 1000:7.2f} {gap:7.2f}")
+    prev_end = x
+gaps = {}
+for i, (name, e, f, x, n) in enumerate(rows):
+    d = tot.setdefault(name, [0, 0.0, 0.0])
+    d[0] += 1
+    d[1] += (x - e) / 1000
+    d[2] += (f - e) / 1000
+    if i + 1 < len(rows):
+        gaps.setdefault((name, rows[i + 1][0]), []).append((rows[i + 1][1] - x) / 1000)
+print("step span (first entry -> last exit):", (rows[-1][3] - t0) / 1000, "us")
+for k, (n, us, fd) in tot.items():
+    print(f"  {k:12s} {n:3d} launches, mean entry->exit {us / n:7.2f} us, entry->first data {fd / n:6.2f} us")
+for (a, b), v in gaps.items():
+    print(f"  gap {a:>12s} -> {b:12s}: mean {np.mean(v):7.2f} us (next entry - this exit)")
