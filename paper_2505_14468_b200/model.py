@@ -496,7 +496,7 @@ class MultiLoraModel:
             v_buf = torch.empty((T, 64), dtype=dt, device=dev)
         # decode: o / down as split-K pieces reduced by the next RMSNorm (no GEMM reduction tail)
         sk_mode = (decode and dt == torch.bfloat16 and self.splitk_consumer and T <= 64
-                   and d % 2048 == 0 and self.pool.max_rank <= 16)
+                   and d % 256 == 0 and d <= 5120 and self.pool.max_rank <= 16)
         if sk_mode:
             S = self.splitk_splits
             part_o = torch.empty(ops.splitk_bytes(T, d + self._extra_rows("wo"), S) // 4,
