@@ -86,6 +86,9 @@ SLX_API size_t slx_gemm_workspace_bytes(int M, int N, int K, int epilogue);
 SLX_API int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
                   int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes, void* stream);
+typedef struct slx_lora_delta slx_lora_delta;   /* defined with the K2/K3 entry points */
+typedef struct slx_splitk_in slx_splitk_in;     /* defined with the K4 entry points */
+
 /* L2 prefetch hint: up to two device regions the NEXT kernel on the stream streams first.  A
  * kernel that takes one issues cp.async.bulk.prefetch.L2 of them (split over its CTAs) as soon
  * as its own HBM stream has been issued, so HBM stays busy across the kernel boundary (its
@@ -109,6 +112,29 @@ SLX_API size_t slx_gemm_splitk_bytes(int M, int N, int splits);
 SLX_API int slx_gemm_bf16_splitk(const void* A, int lda, const void* W, int M, int N, int K,
                   int splits, float* part, size_t part_bytes, const slx_l2_prefetch* pf,
                   void* stream);
+/* Fused input RMSNorm (decode, M <= 64, W tiled): before the mainloop needs its A operand, the
+ * GEMM's CTAs build it across the grid (two grid barriers; all CTAs are co-resident):
+ *   x = round(x + sum of the split-K pieces `sk`)  (the previous projection's residual epilogue)
+ *   x = round(x + LoRA delta `lora`)               (one target spanning the row; v from `sk` when
+ *                                                   lora->v is NULL; rank <= 16)
+ *   h = rmsnorm(x) * w                             (h = the GEMM's A, written to `A`)
+ * x is updated in place.  ss: >= M * 148 floats of scratch; bar: two zero-initialised uint32
+ * counters owned by this call site (monotonic; one grid size per call site). */
+typedef struct slx_norm_in {
+  void* x;
+  int ldx;
+  const void* w;
+  float eps;
+  const slx_splitk_in* sk;     /* may be NULL */
+  const slx_lora_delta* lora;  /* may be NULL */
+  float* ss;
+  size_t ss_bytes;
+  uint32_t* bar;
+} slx_norm_in;
+SLX_API int slx_gemm_bf16_norm(void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
+                  const void* R, int ldr, int M, int N, int K, int epilogue, int n_main, void* C2,
+                  int ldc2, void* ws, size_t ws_bytes, const slx_norm_in* norm,
+                  const slx_l2_prefetch* pf, void* stream);
 /* Debug only: following slx_gemm_bf16 launches write 16 u64 globaltimer slots per CTA into
  * the device buffer `buf` (phase timeline: entry, prologue, past PDL wait, first stage landed,
  * last MMA issued, accumulator ready, split-K reduction start, exit, reduction end, segment

@@ -52,6 +52,12 @@ class SplitKIn(ctypes.Structure):
     _fields_ = [("part", _p), ("splits", _i), ("bm", _i), ("n_main", _i)]
 
 
+class NormIn(ctypes.Structure):
+    """slx_norm_in: fused input-RMSNorm prologue of a decode GEMM."""
+    _fields_ = [("x", _p), ("ldx", _i), ("w", _p), ("eps", _f), ("sk", ctypes.POINTER(SplitKIn)),
+                ("lora", ctypes.POINTER(LoraDelta)), ("ss", _p), ("ss_bytes", _sz), ("bar", _p)]
+
+
 class L2Prefetch(ctypes.Structure):
     """slx_l2_prefetch: the next kernel's first bytes (two regions)."""
     _fields_ = [("ptr", _p * 2), ("bytes", _sz * 2)]
@@ -68,6 +74,8 @@ SIGNATURES = {
     "slx_debug_gemm_trace": (_i, [_p]),
     "slx_gemm_splitk_bytes": (_sz, [_i, _i, _i]),
     "slx_gemm_bf16_splitk": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _sz, ctypes.POINTER(L2Prefetch), _p]),
+    "slx_gemm_bf16_norm": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _p, _i, _p, _sz,
+                                ctypes.POINTER(NormIn), ctypes.POINTER(L2Prefetch), _p]),
     "slx_gemm_bf16_pf": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p,
                               _sz, ctypes.POINTER(L2Prefetch), _p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),

@@ -330,7 +330,14 @@ __device__ __forceinline__ float split_sum1(const SplitArgs& sa, int m, int col)
   const float* p = sa.part + (size_t)(col >> 8) * sa.splits * piece +
                    ((size_t)((col & 255) >> 4) * sa.bm + m) * 16 + (col & 15);
   float s = 0.f;
-  for (int i = 0; i < sa.splits; ++i) s += __ldcg(p + i * piece);
+  for (int i0 = 0; i0 < sa.splits; i0 += 8) {   // 8 loads in flight, summed in piece order
+    float q[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = i0 + i < sa.splits ? __ldcg(p + (i0 + i) * piece) : 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i0 + i < sa.splits) s += q[i];
+  }
   return s;
 }
 }  // namespace slx

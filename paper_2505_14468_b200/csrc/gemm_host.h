@@ -24,6 +24,7 @@ struct SkCall {
   float* part_out;    // slx_gemm_bf16_splitk: pieces out (no epilogue), `splits` per tile
   int splits;
   size_t part_bytes;
+  const slx_norm_in* norm;   // slx_gemm_bf16_norm: fused input RMSNorm prologue (A = norm->h)
 };
 int gemm_sk_launch(const SkCall& c);
 // Debug timeline window for the next traced launch (nullptr when tracing is off); kinds:

@@ -698,7 +698,8 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
   if (ws) SLX_CHECK_ALIGN(ws, 256);
   if (w_layout == SLX_W_TILED) {   // decode: stream-K kernel (gemm_sk.cu) when it applies
     SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
-              ws, ws ? ws_bytes : 0, stream, next_trace_window(1 + epilogue), pf, nullptr, 0, 0};
+              ws, ws ? ws_bytes : 0, stream, next_trace_window(1 + epilogue), pf, nullptr, 0, 0,
+              nullptr};
     const int st = gemm_sk_launch(sc);
     if (st != SLX_ERR_UNSUPPORTED) return st;
   }
@@ -733,6 +734,32 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
                      p.gsplit ? 1u : (unsigned)p.splits, (cudaStream_t)stream);
 }
 
+extern "C" int slx_gemm_bf16_norm(void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
+                                  const void* R, int ldr, int M, int N, int K, int epilogue,
+                                  int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes,
+                                  const slx_norm_in* norm, const slx_l2_prefetch* pf,
+                                  void* stream) {
+  SLX_CHECK_ARG(norm && norm->x && norm->w && norm->ss && norm->bar && A && W && C && M > 0 &&
+                M <= 64 && N > 0 && K > 0 && K % 8 == 0 && lda >= K && lda % 8 == 0 &&
+                norm->ldx >= K && norm->ldx % 8 == 0 && norm->ss_bytes >= (size_t)M * 148 * 4);
+  SLX_CHECK_ARG(delta_valid(norm->lora, norm->sk != nullptr));
+  if (norm->lora && norm->lora->n_targets > 0)
+    SLX_CHECK_ARG(norm->lora->n_targets == 1 && norm->lora->max_rank <= 16 &&
+                  (norm->lora->v || norm->sk) && norm->lora->y_col_off[0] == 0 &&
+                  norm->lora->d_out[0] >= K);
+  if (norm->sk) SLX_CHECK_ARG(norm->sk->part && norm->sk->splits >= 1 && norm->sk->bm >= M &&
+                              norm->sk->n_main >= K);
+  SLX_CHECK_ALIGN(norm->x, 16);
+  SLX_CHECK_ALIGN(A, 16);
+  if (C2 == nullptr) n_main = N;
+  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= n_main && ldr % 8 == 0);
+  SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
+            ws, ws ? ws_bytes : 0, stream, next_trace_window(1 + epilogue), pf, nullptr, 0, 0,
+            norm};
+  const int st = gemm_sk_launch(sc);
+  return st == SLX_ERR_UNSUPPORTED ? SLX_ERR_UNSUPPORTED : st;
+}
+
 extern "C" size_t slx_gemm_splitk_bytes(int M, int N, int splits) {
   return gemm_sk_splitk_bytes(M, N, splits);
 }
@@ -746,7 +773,7 @@ extern "C" int slx_gemm_bf16_splitk(const void* A, int lda, const void* W, int M
   SLX_CHECK_ALIGN(W, 16);
   SLX_CHECK_ALIGN(part, 16);
   SkCall sc{A, lda, W, nullptr, 0, SLX_DT_BF16, nullptr, 0, M, N, K, SLX_EPI_NONE, N, nullptr, 0,
-            nullptr, 0, stream, next_trace_window(4), pf, part, splits, part_bytes};
+            nullptr, 0, stream, next_trace_window(4), pf, part, splits, part_bytes, nullptr};
   return gemm_sk_launch(sc);
 }
 

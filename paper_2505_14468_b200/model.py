@@ -198,6 +198,12 @@ class MultiLoraModel:
         # decode: o / down projections as split-K pieces reduced by the following RMSNorm
         self.splitk_consumer = os.environ.get("SLX_SPLITK_CONSUMER", "1") != "0"
         self.splitk_splits = int(os.environ.get("SLX_SPLITK_SPLITS", "8"))
+        # decode: the RMSNorms fused into the GEMM that consumes them (grid-wide prologue).
+        # Off by default: measured slower (the prologue's dependent L2 round trips queue behind
+        # the weight stream the producer has already started; SLX_FUSE_NORM=1 to enable).
+        self.fuse_norm = os.environ.get("SLX_FUSE_NORM", "0") == "1"
+        self.norm_ss = torch.zeros(64 * 148, dtype=torch.float32, device=self.device)
+        self.norm_bar = torch.zeros(8, dtype=torch.int32, device=self.device)   # 3 call sites
         # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off)
         self.l2_prefetch_mb = float(os.environ.get("SLX_L2_PF_MB", "16"))
         self._pf_cache: dict = {}
@@ -495,21 +501,27 @@ class MultiLoraModel:
             sgmv_plan = self._sgmv_plan(segments, slot.cpu().numpy())
             v_buf = torch.empty((T, 64), dtype=dt, device=dev)
         # decode: o / down as split-K pieces reduced by the next RMSNorm (no GEMM reduction tail)
-        sk_mode = (decode and dt == torch.bfloat16 and self.splitk_consumer and T <= 64
+        sk_mode = (decode and dt == torch.bfloat16 and self.splitk_consumer and self.fuse_expand
+                   and self.use_stacked_decode and T <= 64
                    and d % 256 == 0 and d <= 5120 and self.pool.max_rank <= 16)
         if sk_mode:
-            S = self.splitk_splits
+            S = min(self.splitk_splits, (d + 63) // 64)                   # o: K = q_dim
+            S_dn = min(self.splitk_splits, self.ffn_pad // 64)           # down: K = ffn
             part_o = torch.empty(ops.splitk_bytes(T, d + self._extra_rows("wo"), S) // 4,
                                  dtype=torch.float32, device=dev)
-            part_dn = torch.empty(ops.splitk_bytes(T, d, S) // 4, dtype=torch.float32, device=dev)
+            part_dn = torch.empty(ops.splitk_bytes(T, d, S_dn) // 4, dtype=torch.float32,
+                                  device=dev)
         pending = None   # split-K pieces of the down projection, consumed by the next norm
         ops.embedding(x, w["embed"], tokens)
         if self.targets:
             ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
         qkv_cols = {"q": (0, qd, qd), "k": (qd, kvd, kvd), "v": (qd + kvd, kvd, kvd)}
+        fnorm = sk_mode and self.fuse_norm and self.fuse_expand and "w_qkv" in self.stack
         for l in range(cfg.layers):
             p = f"layers.{l}."
-            if pending is not None:
+            if fnorm:
+                pass   # built by the qkv GEMM's prologue below
+            elif pending is not None:
                 ops.rmsnorm_fused(h, x, w[p + "input_norm"], cfg.rms_eps, pending)
                 pending = None
             else:
@@ -522,7 +534,13 @@ class MultiLoraModel:
             pf_o = self._pf(p + "w_gu", w[p + "w_gu"]) if pfd else None
             pf_gu = self._pf(p + "w_down", w[p + "w_down"]) if pfd else None
             pf_dn = self._pf(nxt, w[nxt]) if pfd else None
-            if stacked and "w_qkv" in self.stack:
+            if fnorm:
+                nq = ops.norm_in(x, w[p + "input_norm"], cfg.rms_eps, self.norm_ss,
+                                 self.norm_bar[0:2], sk=pending)
+                pending = None
+                ops.gemm_norm(h, w[p + "w_qkv"], qkv, nq, side=v_qkv, prefetch=pf_qkv)
+                d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
+            elif stacked and "w_qkv" in self.stack:
                 ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv, prefetch=pf_qkv)
                 if decode and self.fuse_expand:
                     d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
@@ -550,7 +568,12 @@ class MultiLoraModel:
             if sk_mode and "wo" in self.stack:
                 sk_o = ops.gemm_splitk(attn, w[p + "wo"], S, part_o, prefetch=pf_o)
                 d_o = self._delta(l, "wo", None, slot, {"o": (0, d, d)})
-                ops.rmsnorm_fused(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o)
+                if fnorm and fused_silu:
+                    ngu = ops.norm_in(x, w[p + "post_norm"], cfg.rms_eps, self.norm_ss,
+                                      self.norm_bar[2:4], sk=sk_o, delta=d_o)
+                else:
+                    ops.rmsnorm_fused(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o)
+                    ngu = None
                 d_o = "done"
             elif stacked and "wo" in self.stack:
                 ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o,
@@ -570,17 +593,25 @@ class MultiLoraModel:
                 ops.rmsnorm_lora(h, x, w[p + "post_norm"], cfg.rms_eps, d_o)
             else:
                 ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
-            if fused_silu:
+            if fused_silu and d_o == "done" and ngu is not None:
+                ops.gemm_norm(h, w[p + "w_gu"], mlp, ngu, epilogue=EPI_SILU_MUL, prefetch=pf_gu)
+            elif fused_silu:
                 self._gemm(h, w[p + "w_gu"], mlp, silu=True, prefetch=pf_gu)
             else:
                 self._gemm(h, w[p + "w_gu"], gu)
                 self._lora(gu, h, l, ("gate", "up"), {"gate": (0, 128, 256), "up": (128, 128, 256)})
                 ops.silu_mul_blocked(mlp, gu, self.ffn_pad)
             if sk_mode and "down" not in self.targets:
-                pending = ops.gemm_splitk(mlp, w[p + "w_down"], S, part_dn, prefetch=pf_dn)
+                pending = ops.gemm_splitk(mlp, w[p + "w_down"], S_dn, part_dn, prefetch=pf_dn)
             else:
                 self._gemm(mlp, w[p + "w_down"], x, residual=x, prefetch=pf_dn)
                 self._lora(x, mlp, l, ("down",), {"down": (0, d, d)}, d_in=cfg.ffn)
+        if pending is not None and fnorm and logit_rows is None:
+            hn = torch.empty_like(x)
+            nf = ops.norm_in(x, w["final_norm"], cfg.rms_eps, self.norm_ss, self.norm_bar[4:6],
+                             sk=pending)
+            logits = torch.empty((T, cfg.vocab), dtype=torch.float32, device=dev)
+            return ops.gemm_norm(hn, w["lm_head"], logits, nf)
         if pending is not None:
             hn = torch.empty_like(x)
             ops.rmsnorm_fused(hn, x, w["final_norm"], cfg.rms_eps, pending)

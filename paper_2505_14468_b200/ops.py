@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import (DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED,
-                   L2Prefetch, LoraDelta, LoraTarget, SplitKIn, check)
+                   L2Prefetch, LoraDelta, LoraTarget, NormIn, SplitKIn, check)
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
 
@@ -224,6 +224,41 @@ def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
                                        _ld(side) if n_tot > n_main else 0, _ptr(wsb), wsb.numel(),
                                        None if prefetch is None else ctypes.byref(prefetch),
                                        _stream()), "slx_gemm_bf16")
+    return out
+
+
+def norm_in(x: torch.Tensor, w: torch.Tensor, eps: float, ss: torch.Tensor, bar: torch.Tensor,
+            sk=None, delta=None) -> NormIn:
+    """slx_norm_in for gemm_norm: x (residual stream, updated in place), norm weight w, split-K
+    pieces `sk` of the previous projection, residual LoRA `delta`; ss / bar: scratch and this
+    call site's two grid-barrier counters."""
+    n = NormIn()
+    n.x, n.ldx, n.w, n.eps = x.data_ptr(), _ld(x), w.data_ptr(), float(eps)
+    if sk is not None:
+        n.sk = ctypes.pointer(sk)
+    if delta is not None:
+        n.lora = ctypes.pointer(delta)
+    n.ss, n.ss_bytes, n.bar = ss.data_ptr(), ss.numel() * ss.element_size(), bar.data_ptr()
+    n._keep = (sk, delta)
+    return n
+
+
+@_op("gemm", 1)
+def gemm_norm(h: torch.Tensor, w, out: torch.Tensor, norm: NormIn, *, epilogue: int = EPI_NONE,
+              side: torch.Tensor | None = None, out_dtype=None, ws=None, prefetch=None) -> torch.Tensor:
+    """Decode GEMM whose A operand h = rmsnorm(x + pieces + LoRA delta) is built by the GEMM's
+    own CTAs (slx_gemm_bf16_norm); x is updated in place, h written."""
+    if h.dtype != torch.bfloat16 or not isinstance(w, PackedWeight):
+        raise ValueError("gemm_norm: bf16 activations and a packed weight")
+    M, K = h.shape
+    N = w.n + (w.n_extra if side is not None else 0)
+    wsb = (ws if ws is not None else default_workspace(h.device)).get(
+        _lib.load().slx_gemm_workspace_bytes(M, N, K, epilogue))
+    check(_lib.load().slx_gemm_bf16_norm(
+        _ptr(h), _ld(h), _ptr(w.data), _ptr(out), _ld(out), _dt(out), None, 0, M, N, K, epilogue,
+        w.n, _ptr(side) if side is not None else None, _ld(side) if side is not None else 0,
+        _ptr(wsb), wsb.numel(), ctypes.byref(norm),
+        None if prefetch is None else ctypes.byref(prefetch), _stream()), "slx_gemm_bf16_norm")
     return out
 
 

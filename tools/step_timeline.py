@@ -76,6 +76,23 @@ for i, (name, e, f, x, n) in enumerate(rows):
     if i + 1 < len(rows):
         gaps.setdefault((name, rows[i + 1][0]), []).append((rows[i + 1][1] - x) / 1000)
 print("step span (first entry -> last exit):", (rows[-1][3] - t0) / 1000, "us")
+# fused-norm prologue phases (GEMM windows with stamps 10..14)
+ph = {}
+for i in range(200):
+    kind = int(t[i, 4095] & 0xffffffff)
+    if kind not in (1, 2, 3):
+        continue
+    st = t[i, :4095 - 15].reshape(-1, 16)
+    st = st[st[:, 0] > 0]
+    if len(st) == 0 or not (st[:, 10] > 0).any():
+        continue
+    e = st[:, 0].min()
+    for k in (10, 11, 12, 13, 14, 2):
+        col = st[:, k][st[:, k] > 0]
+        ph.setdefault((kind, k), []).append(((col.min() - e) / 1000, (col.max() - e) / 1000))
+for (kind, k), v in sorted(ph.items()):
+    v = np.array(v)
+    print(f"  prologue kind {kind} stamp {k:2d}: min {v[:, 0].mean():7.2f}  max {v[:, 1].mean():7.2f} us after entry")
 for k, (n, us, fd) in tot.items():
     print(f"  {k:12s} {n:3d} launches, mean entry->exit {us / n:7.2f} us, entry->first data {fd / n:6.2f} us")
 for (a, b), v in gaps.items():
