@@ -151,6 +151,18 @@ SLX_API int slx_gemm_grouped_bf16(const void* A, int lda, int M, int K, int n_gr
                   const uint64_t* w_ptrs, const int* w_rows, const int* w_cols, const int* w_ld,
                   const float* alpha, void* C, int ldc, int c_dtype, const void* R, int ldr, int N,
                   int epilogue, const void* gtiles, int n_gtiles, void* stream);
+/* Prefill backbone GEMM with the LoRA expand folded into its mainloop (grouped tiles
+ * {group, m0, m_rows, n0}, 256 columns each): C = A . W^T (+ R) for every tile, and a tile whose
+ * group >= 0 accumulates one more K block v[m, t*64 : t*64+64] . B_(group, t)[n - t_bound[t], :]^T,
+ * t = the target whose column range [t_bound[t], t_bound[t+1]) holds the tile (t_bound[t] % 256
+ * == 0).  v [M, ldv] bf16 is the LoRA shrink with the scale folded in (slx_gemm_grouped_bf16
+ * with alpha = scale), zero beyond each adapter's rank; b_ptrs[a * n_targets + t] = B [b_rows[t],
+ * ranks[a]] row-major.  <= 16 adapters, <= 3 targets.  No separate expand, no y read-modify-write. */
+SLX_API int slx_gemm_bf16_lorafold(const void* A, int lda, const void* W, int w_layout, void* C,
+                  int ldc, int c_dtype, const void* R, int ldr, int M, int N, int K, int epilogue,
+                  const void* gtiles, int n_gtiles, const void* v, int ldv, int n_targets,
+                  const int* t_bound, int n_adapters, const uint64_t* b_ptrs, const int* b_rows,
+                  const int* ranks, void* stream);
 /* Pack a row-major bf16 W[N, K] (row stride ld) into the SLX_W_TILED layout (device kernel).
  * dst must hold slx_packed_weight_elems(N, K) elements. */
 SLX_API size_t slx_packed_weight_elems(int N, int K);

@@ -80,6 +80,8 @@ SIGNATURES = {
                               _sz, ctypes.POINTER(L2Prefetch), _p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),
     "slx_gemm_group_tile_bytes": (_sz, []),
+    "slx_gemm_bf16_lorafold": (_i, [_p, _i, _p, _i, _p, _i, _i, _p, _i, _i, _i, _i, _i, _p, _i, _p, _i,
+                                    _i, _p, _i, _p, _p, _p, _p]),
     "slx_gemm_grouped_bf16": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p, _i, _i,
                                    _i, _p, _i, _p]),
     "slx_lora_expand": (_i, [_i, _p, _i, _p, _i, _i, _p, _p, _i, _i, _i,

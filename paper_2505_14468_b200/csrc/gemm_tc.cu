@@ -42,12 +42,14 @@ constexpr int TC_MAX_CLUSTER = 8;
 // Grouped mode (SGMV on the tensor cores): CTA x-index -> one GroupTile; each group (adapter
 // segment) has its own row-major W tensor map and alpha (the LoRA scale).
 constexpr int TC_MAX_GROUPS = 16;
+constexpr int TC_MAX_MAPS = 48;   // LoRA fold: (adapter, target) B maps, <= 16 adapters x 3
 struct GroupTile {
   int group, m0, m_rows, n0;
 };
 struct GroupMaps {
-  CUtensorMap w[TC_MAX_GROUPS];
-  float alpha[TC_MAX_GROUPS];
+  CUtensorMap w[TC_MAX_MAPS];
+  float alpha[TC_MAX_MAPS];
+  CUtensorMap v;   // LoRA fold: the shrink output v [T, 64 * n_targets] (scale folded in)
 };
 
 struct GemmArgs {
@@ -70,6 +72,12 @@ struct GemmArgs {
   float* ws_part;            // [tiles][S][bm][BN] fp32 partials
   int* ws_cnt;               // [tiles] arrival counters (zero; self-cleaning)
   unsigned long long* trace; // debug (slx_debug_gemm_trace): 8 globaltimer stamps per CTA
+  // LoRA fold (slx_gemm_bf16_lorafold, grouped tiles): the main K range uses the backbone W
+  // (tmap_w) for every tile; a tile whose group >= 0 adds ONE more k-block
+  //   D += v[m0.., t*64 : t*64+64] . B_(group, t)[n0 - lbound[t] .., :64]^T
+  // (t = target of the tile's columns), i.e. the LoRA expand rides in the backbone mainloop.
+  int lfold, lnt;
+  int lbound[4];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -171,8 +179,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   const int m0 = GROUPED ? gt.m0 : blockIdx.y * 128;
   const int n0 = GROUPED ? gt.n0 : tile * TC_BN;
   const int m_lim = GROUPED ? gt.m0 + gt.m_rows : g.M;
-  const float alpha = GROUPED ? gm.alpha[gt.group] : 1.f;
-  const CUtensorMap* wmap = GROUPED ? &gm.w[gt.group] : &tmap_w;
+  const bool lfold = GROUPED && g.lfold;
+  const float alpha = (GROUPED && !lfold) ? gm.alpha[gt.group] : 1.f;
+  const CUtensorMap* wmap = (GROUPED && !lfold) ? &gm.w[gt.group] : &tmap_w;
+  int ltgt = 0;
+  if (lfold) {
+#pragma unroll
+    for (int t = 1; t < 4; ++t)
+      if (t < g.lnt && n0 >= g.lbound[t]) ltgt = t;
+  }
+  const bool lblk = lfold && gt.group >= 0;            // one extra (LoRA) k-block
+  const int n_tot = n_kb + (lblk ? 1 : 0);
 
   if (threadIdx.x == 0) {
     tc::tma_prefetch_desc(&tmap_x);
@@ -217,20 +234,28 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     SLX_TR(2);
     for (int i = 0; i < npre; ++i)
       tc::tma_load_2d(smem + i * stage_bytes, &tmap_x, &full[i], (kb_lo + i) * TC_BK, m0, pol_x);
-    for (int i = npre; i < n_kb; ++i) {
+    for (int i = npre; i < n_tot; ++i) {
       const int s = i % g.stages;
       tc::mbar_wait(&empty[s], ((i / g.stages) & 1) ^ 1);
       uint8_t* st = smem + s * stage_bytes;
       tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
-      load_w(st, &full[s], kb_lo + i);
-      tc::tma_load_2d(st, &tmap_x, &full[s], (kb_lo + i) * TC_BK, m0, pol_x);
+      if (i < n_kb) {
+        load_w(st, &full[s], kb_lo + i);
+        tc::tma_load_2d(st, &tmap_x, &full[s], (kb_lo + i) * TC_BK, m0, pol_x);
+      } else {   // LoRA k-block: v slice of the tile's target x B rows of (adapter, target)
+        const CUtensorMap* bmap = &gm.w[gt.group * g.lnt + ltgt];
+        for (int b = 0; b < WB; ++b)
+          tc::tma_load_2d(st + x_bytes + b * W_BLOCK_BYTES, bmap, &full[s], 0,
+                          n0 - g.lbound[ltgt] + b * 128, pol_x);
+        tc::tma_load_2d(st, &gm.v, &full[s], ltgt * TC_BK, m0, pol_x);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread): D[128 x 256] += X[128 x 16] . W[256 x 16]^T.
     // Rows >= bm of the X operand read stale shared memory; they only feed D rows that are
     // never stored.
     const uint32_t idesc = tc::idesc_bf16_f32(128, TC_BN);
-    for (int i = 0; i < n_kb; ++i) {
+    for (int i = 0; i < n_tot; ++i) {
       const int s = i % g.stages;
       tc::mbar_wait(&full[s], (i / g.stages) & 1);
       tc::fence_after_sync();
@@ -847,6 +872,68 @@ extern "C" int slx_pack_weight_rows(void* dst, const void* src, int n_rows, int 
 
 // ------------------------------------------------------------------ grouped GEMM (SGMV)
 extern "C" size_t slx_gemm_group_tile_bytes(void) { return sizeof(GroupTile); }
+
+extern "C" int slx_gemm_bf16_lorafold(const void* A, int lda, const void* W, int w_layout, void* C,
+                                      int ldc, int c_dtype, const void* R, int ldr, int M, int N,
+                                      int K, int epilogue, const void* gtiles, int n_gtiles,
+                                      const void* v, int ldv, int n_targets, const int* t_bound,
+                                      int n_adapters, const uint64_t* b_ptrs, const int* b_rows,
+                                      const int* ranks, void* stream) {
+  SLX_CHECK_ARG(A && W && C && v && gtiles && t_bound && M > 0 && N > 0 && K > 0 &&
+                K % 8 == 0 && lda >= K && lda % 8 == 0 && ldc % 8 == 0 && n_gtiles >= 0 &&
+                n_targets >= 1 && n_targets <= 3 && n_adapters >= 0 && n_adapters <= 16 &&
+                n_adapters * n_targets <= TC_MAX_MAPS && ldv >= 64 * n_targets && ldv % 8 == 0);
+  SLX_CHECK_ARG(w_layout == SLX_W_ROWMAJOR || w_layout == SLX_W_TILED);
+  SLX_CHECK_ARG(epilogue == SLX_EPI_NONE || epilogue == SLX_EPI_RESIDUAL);
+  SLX_CHECK_ARG(c_dtype == SLX_DT_BF16 || c_dtype == SLX_DT_F32);
+  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr % 8 == 0);
+  SLX_CHECK_ALIGN(A, 16);
+  SLX_CHECK_ALIGN(C, 16);
+  SLX_CHECK_ALIGN(v, 16);
+  for (int t = 0; t < n_targets; ++t)   // target column ranges start on 256-column tiles
+    SLX_CHECK_ARG(t_bound[t] % 256 == 0 && (t == 0 ? t_bound[t] == 0 : t_bound[t] > t_bound[t - 1]));
+  if (n_gtiles == 0) return SLX_OK;
+  GroupMaps gm{};
+  for (int a = 0; a < n_adapters; ++a) {
+    SLX_CHECK_ARG(ranks[a] > 0 && ranks[a] <= 64 && ranks[a] % 8 == 0);
+    for (int t = 0; t < n_targets; ++t) {
+      const int i = a * n_targets + t;
+      // B_(a, t) [d_out, rank] row-major: columns >= rank of the 64-wide box read as zeros
+      if (b_ptrs[i] == 0 || !make_tmap(&gm.w[i], (const void*)b_ptrs[i], b_rows[t], ranks[a],
+                                       ranks[a], 128))
+        return b_ptrs[i] == 0 ? SLX_ERR_INVALID : SLX_ERR_CUDA;
+      gm.alpha[i] = 1.f;
+    }
+  }
+  if (!make_tmap(&gm.v, v, M, 64 * n_targets, ldv, 128)) return SLX_ERR_CUDA;
+  GemmArgs a{};
+  a.M = M; a.N = N; a.K = K;
+  a.bm = 128; a.kblocks = ceil_div(K, TC_BK); a.splits = 1; a.n_tiles = 1;
+  const size_t stage = (size_t)128 * TC_BK * 2 + 2 * W_BLOCK_BYTES;
+  a.stages = 4;
+  const size_t smem = (size_t)a.stages * stage + BAR_BYTES + 1024;
+  a.C = C; a.ldc = ldc; a.R = R; a.ldr = ldr; a.w_tiled = w_layout == SLX_W_TILED; a.n_main = N;
+  a.gtiles = (const GroupTile*)gtiles;
+  a.lfold = 1;
+  a.lnt = n_targets;
+  for (int t = 0; t < 4; ++t) a.lbound[t] = t < n_targets ? t_bound[t] : 0;
+  CUtensorMap mx, mw;
+  const int kb = ceil_div(K, TC_BK);
+  const int w_rows = a.w_tiled ? ceil_div(N, 128) * kb * 128 : N;
+  const int w_cols = a.w_tiled ? TC_BK : K;
+  if (!make_tmap(&mx, A, M, K, lda, 128) || !make_tmap(&mw, W, w_rows, w_cols, w_cols, 128))
+    return SLX_ERR_CUDA;
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((unsigned)n_gtiles, 1);
+  if (c_dtype == SLX_DT_BF16) {
+    if (epilogue == SLX_EPI_NONE)
+      return launch_tc<SLX_EPI_NONE, bf16, 256, true>(mx, mw, a, grid, smem, 1u, s, gm);
+    return launch_tc<SLX_EPI_RESIDUAL, bf16, 256, true>(mx, mw, a, grid, smem, 1u, s, gm);
+  }
+  if (epilogue == SLX_EPI_NONE)
+    return launch_tc<SLX_EPI_NONE, float, 256, true>(mx, mw, a, grid, smem, 1u, s, gm);
+  return launch_tc<SLX_EPI_RESIDUAL, float, 256, true>(mx, mw, a, grid, smem, 1u, s, gm);
+}
 
 extern "C" int slx_gemm_grouped_bf16(const void* A, int lda, int M, int K, int n_groups,
                                      const uint64_t* w_ptrs, const int* w_rows, const int* w_cols,

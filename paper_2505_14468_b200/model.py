@@ -208,6 +208,8 @@ class MultiLoraModel:
         self.l2_prefetch_mb = float(os.environ.get("SLX_L2_PF_MB", "16"))
         self._pf_cache: dict = {}
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
+        # prefill: the LoRA expand folded into the backbone GEMM as one extra K block
+        self.lora_fold = os.environ.get("SLX_LORA_FOLD", "1") != "0"
         self.pool.on_install = self._stack_install
         self.pool.on_evict = self._stack_evict
 
@@ -388,6 +390,56 @@ class MultiLoraModel:
             launches.append((chunk, dev(shrink), {do: dev(v) for do, v in expand.items()}))
         return launches
 
+    def _fold_plan(self, segments, slot_host, T: int):
+        """Prefill LoRA folded into the backbone GEMMs: grouped tiles of the qkv / o GEMMs
+        (segment-aligned 128-row blocks, group = the adapter's index, -1 = none) and the shrink
+        tiles.  None when the batch does not fit the fold (> 16 adapters, partial target sets,
+        short segments that would waste tensor-core rows)."""
+        cfg = self.cfg
+        if set(self.targets) != {"q", "k", "v", "o"} or self.pool.max_rank > 64:
+            return None
+        if cfg.q_dim % 256 or cfg.kv_dim % 256 or cfg.hidden % 256:
+            return None
+        slots = sorted({int(slot_host[t0]) for t0, _n, _s, _p in segments
+                        if int(slot_host[t0]) >= 0 and self.pool.configs[int(slot_host[t0])] is not None})
+        if len(slots) > ops.GROUP_MAX or any(set(self.pool.configs[a].targets) != set(self.targets)
+                                             for a in slots):
+            return None
+        gi = {a: i for i, a in enumerate(slots)}
+        nq = cfg.q_dim + 2 * cfg.kv_dim
+        tq, to, sh = [], [], []
+        n_mtiles = 0
+        for tok0, n, _seq, _p0 in segments:
+            a = int(slot_host[tok0])
+            g = gi.get(a, -1)
+            for m0 in range(tok0, tok0 + n, 128):
+                mr = min(128, tok0 + n - m0)
+                n_mtiles += 1
+                tq += [(g, m0, mr, n0) for n0 in range(0, nq, 256)]
+                to += [(g, m0, mr, n0) for n0 in range(0, cfg.hidden, 256)]
+                if g >= 0:
+                    sh.append((g, m0, mr, 0))
+        if n_mtiles > 1.25 * ((T + 127) // 128) + 1:
+            return None
+        dev = lambda rows: torch.tensor(rows, dtype=torch.int32).reshape(-1, 4).to(self.device)  # noqa: E731
+        return slots, dev(tq), dev(to), dev(sh) if sh else None
+
+    def _fold_lora(self, layer: int, slots, proj: str):
+        """(A groups for the shrink per target, B pointers adapter-major, ranks)."""
+        names = ("q", "k", "v") if proj == "w_qkv" else ("o",)
+        ga = {t: [] for t in names}
+        bp, ranks = [], []
+        for a in slots:
+            lo = self.pool.configs[a]
+            base = self.pool.blobs[a].data_ptr()
+            ranks.append(lo.rank)
+            for t in names:
+                di, do = self.cfg.target_dims(t)
+                ao, bo = self.pool.offsets(lo.rank, layer, t)
+                ga[t].append((base + 2 * ao, lo.rank, di, di, lo.scale))
+                bp.append(base + 2 * bo)
+        return ga, bp, ranks
+
     def _sgmv_tc(self, y, x, layer: int, names, cols, plan, v_buf) -> bool:
         """Prefill LoRA for contiguous targets via two grouped tcgen05 GEMMs per target:
         v = scale * x A^T (shrink, bf16 [T, 64]) then y[:, off:] += v B^T (expand)."""
@@ -496,10 +548,19 @@ class MultiLoraModel:
         if flash:
             tiles = ops.prefill_tiles(segments, dev)
         sgmv_plan = None
+        fold = None
         if (segments is not None and not decode and dt == torch.bfloat16 and self.targets
                 and self.use_tc_sgmv and not (self.use_stacked_decode and T <= 128)):
-            sgmv_plan = self._sgmv_plan(segments, slot.cpu().numpy())
-            v_buf = torch.empty((T, 64), dtype=dt, device=dev)
+            slot_host = slot.cpu().numpy()
+            if self.lora_fold:
+                fold = self._fold_plan(segments, slot_host, T)
+            if fold is None:
+                sgmv_plan = self._sgmv_plan(segments, slot_host)
+                v_buf = torch.empty((T, 64), dtype=dt, device=dev)
+            else:
+                v_qkv_f = torch.zeros((T, 192), dtype=dt, device=dev)
+                v_o_f = torch.zeros((T, 64), dtype=dt, device=dev)
+                bq = [cfg.q_dim, cfg.kv_dim, cfg.kv_dim]
         # decode: o / down as split-K pieces reduced by the next RMSNorm (no GEMM reduction tail)
         sk_mode = (decode and dt == torch.bfloat16 and self.splitk_consumer and self.fuse_expand
                    and self.use_stacked_decode and T <= 64
@@ -534,7 +595,14 @@ class MultiLoraModel:
             pf_o = self._pf(p + "w_gu", w[p + "w_gu"]) if pfd else None
             pf_gu = self._pf(p + "w_down", w[p + "w_down"]) if pfd else None
             pf_dn = self._pf(nxt, w[nxt]) if pfd else None
-            if fnorm:
+            if fold is not None:
+                ga, bp, rk = self._fold_lora(l, fold[0], "w_qkv")
+                if fold[3] is not None:
+                    for i, t in enumerate(("q", "k", "v")):
+                        ops.gemm_grouped(h, cfg.hidden, ga[t], fold[3], v_qkv_f[:, 64 * i:64 * i + 64], 64)
+                ops.gemm_lorafold(h, w[p + "w_qkv"], qkv, fold[1], v_qkv_f,
+                                  [0, cfg.q_dim, cfg.q_dim + cfg.kv_dim], bp, bq, rk)
+            elif fnorm:
                 nq = ops.norm_in(x, w[p + "input_norm"], cfg.rms_eps, self.norm_ss,
                                  self.norm_bar[0:2], sk=pending)
                 pending = None
@@ -575,6 +643,12 @@ class MultiLoraModel:
                     ops.rmsnorm_fused(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o)
                     ngu = None
                 d_o = "done"
+            elif fold is not None:
+                ga, bp, rk = self._fold_lora(l, fold[0], "wo")
+                if fold[3] is not None:
+                    ops.gemm_grouped(attn, cfg.q_dim, ga["o"], fold[3], v_o_f, 64)
+                ops.gemm_lorafold(attn, w[p + "wo"], x, fold[2], v_o_f, [0], bp, [cfg.hidden], rk,
+                                  residual=x)
             elif stacked and "wo" in self.stack:
                 ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o,
                          prefetch=pf_o)

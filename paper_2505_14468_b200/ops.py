@@ -353,6 +353,27 @@ def lora_expand(y: torch.Tensor, v_all: torch.Tensor, slot_rank, slot_scale, max
 GROUP_MAX = 16
 
 
+@_op("gemm", 1)
+def gemm_lorafold(a: torch.Tensor, w, out: torch.Tensor, gtiles: torch.Tensor, v: torch.Tensor,
+                  t_bound, b_ptrs, b_rows, ranks, residual: torch.Tensor | None = None) -> torch.Tensor:
+    """Prefill backbone GEMM with the LoRA expand as one extra K block per grouped tile
+    (slx_gemm_bf16_lorafold).  w: PackedWeight; v: bf16 [T, 64 * targets] shrink (scale folded);
+    b_ptrs: per (adapter, target) B addresses (adapter-major)."""
+    if a.dtype != torch.bfloat16 or not isinstance(w, PackedWeight) or v.dtype != torch.bfloat16:
+        raise ValueError("gemm_lorafold: bf16 activations, packed weight, bf16 v")
+    M, K = a.shape
+    nt = len(t_bound)
+    arr = lambda t, vals: (t * len(vals))(*vals)  # noqa: E731
+    epi = EPI_RESIDUAL if residual is not None else EPI_NONE
+    check(_lib.load().slx_gemm_bf16_lorafold(
+        _ptr(a), _ld(a), _ptr(w.data), W_TILED, _ptr(out), _ld(out), _dt(out), _ptr(residual),
+        _ld(residual) if residual is not None else 0, M, w.n, K, epi, _ptr(gtiles), gtiles.shape[0],
+        _ptr(v), _ld(v), nt, arr(ctypes.c_int, list(t_bound)), len(ranks),
+        arr(ctypes.c_uint64, list(b_ptrs)), arr(ctypes.c_int, list(b_rows)),
+        arr(ctypes.c_int, list(ranks)), _stream()), "slx_gemm_bf16_lorafold")
+    return out
+
+
 @_op("lora", 1)
 def gemm_grouped(a: torch.Tensor, k: int, groups, gtiles: torch.Tensor, out: torch.Tensor, n: int,
                  residual: torch.Tensor | None = None) -> torch.Tensor:

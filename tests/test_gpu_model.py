@@ -147,6 +147,35 @@ def test_bf16_stacked_decode_shrink_matches_sgmv_path(golden):
     np.testing.assert_allclose(ev[1], ev2[1], rtol=1e-2, atol=1e-2)
 
 
+def test_bf16_prefill_lora_fold_matches_oracle(monkeypatch):
+    """Prefill with the LoRA expand folded into the backbone qkv / o GEMMs (one extra K block
+    per segment-aligned tile) == the separate shrink/expand SGMV path == oracle; mixed ranks,
+    a prompt without adapter, a segment that is not a multiple of 128 tokens."""
+    from paper_2505_14468_b200.config import BackboneConfig
+    cfg = BackboneConfig("small128", hidden=512, layers=2, heads=4, kv_heads=2, head_dim=128,
+                         ffn=1024, vocab=1000)
+    w = init_backbone(cfg, 5)
+    loras = [LoraConfig(8, 16.0), LoraConfig(64, 32.0), LoraConfig(16, 16.0)]
+    ads = [init_adapter(cfg, lo, 5, a) for a, lo in enumerate(loras)]
+    rng = np.random.default_rng(9)
+    prompts = [list(map(int, rng.integers(1, cfg.vocab, size=L))) for L in (256, 128, 200, 384)]
+    ids = [1, 0, -1, 2]
+    out = {}
+    for fold in (True, False):
+        m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=8, max_ctx=512, n_slots=4,
+                           max_rank=64, max_tokens=1024)
+        m.lora_fold = fold
+        m.load_backbone(w)
+        for a, (ad, lo) in enumerate(zip(ads, loras)):
+            m.pool.load(a, ad, lo)
+        _, lg = m.prefill(prompts, ids)
+        out[fold] = lg.cpu().numpy()
+    np.testing.assert_allclose(out[True], out[False], rtol=2e-2, atol=2e-2)
+    orc = OracleModel(cfg, w, ads, [lo.scale for lo in loras], loras[0].targets)
+    ref = orc.prefill(prompts, ids)
+    np.testing.assert_allclose(out[True], ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
 def test_bf16_decode_splitk_consumer_matches_oracle():
     """Decode with the o / down projections as split-K pieces reduced by the following RMSNorm
     (residual epilogue, o-LoRA v and delta fused there) == the GEMM-side reduction == oracle."""
