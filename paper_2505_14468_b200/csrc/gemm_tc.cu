@@ -78,6 +78,9 @@ struct GemmArgs {
   // (t = target of the tile's columns), i.e. the LoRA expand rides in the backbone mainloop.
   int lfold, lnt;
   int lbound[4];
+  // rasterised 1-D grid (prefill, no split): tiles visited in groups of `raster` m-tiles x all
+  // n-tiles, so the ~148 co-resident CTAs share a few X row blocks and W tiles in L2
+  int raster, m_tiles;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -167,8 +170,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) SLX_TR(0);
   const int S = g.splits;
-  const int tile = blockIdx.x / S;
-  const int split = blockIdx.x % S;   // == cluster rank (cluster dims (S,1,1))
+  int tile, mt;
+  if (!GROUPED && g.raster > 0) {
+    const int L = blockIdx.x, per = g.raster * g.n_tiles;
+    const int grp = L / per, rem = L - grp * per;
+    const int gsz = min(g.raster, g.m_tiles - grp * g.raster);
+    mt = grp * g.raster + rem % gsz;
+    tile = rem / gsz;
+  } else {
+    tile = blockIdx.x / S;
+    mt = blockIdx.y;
+  }
+  const int split = g.raster > 0 ? 0 : blockIdx.x % S;   // == cluster rank (cluster dims (S,1,1))
   const int kb_per = (g.kblocks + S - 1) / S;
   const int kb_lo = split * kb_per;
   const int kb_hi = min(g.kblocks, kb_lo + kb_per);
@@ -176,7 +189,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   // grouped mode: the tile table comes from the host stream; read it after the PDL wait
   if (GROUPED) pdl_wait();
   const GroupTile gt = GROUPED ? g.gtiles[blockIdx.x] : GroupTile{0, 0, 0, 0};
-  const int m0 = GROUPED ? gt.m0 : blockIdx.y * 128;
+  const int m0 = GROUPED ? gt.m0 : mt * 128;
   const int n0 = GROUPED ? gt.n0 : tile * TC_BN;
   const int m_lim = GROUPED ? gt.m0 + gt.m_rows : g.M;
   const bool lfold = GROUPED && g.lfold;
@@ -755,6 +768,12 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
   if (!make_tmap(&mx, A, M, K, lda, p.bm) || !make_tmap(&mw, W, w_rows, w_cols, w_cols, 128))
     return SLX_ERR_CUDA;
   dim3 grid((unsigned)(p.n_tiles * p.splits), (unsigned)p.m_tiles);
+  const int raster = env_int("SLX_GEMM_RASTER", 16);   // measured best of {4, 8, 16}
+  if (p.splits == 1 && p.m_tiles > 1 && raster > 0) {
+    a.raster = raster;
+    a.m_tiles = p.m_tiles;
+    grid = dim3((unsigned)(p.n_tiles * p.m_tiles), 1);
+  }
   return dispatch_tc(epilogue, c_dtype, p.bn, mx, mw, a, grid, p.smem,
                      p.gsplit ? 1u : (unsigned)p.splits, (cudaStream_t)stream);
 }

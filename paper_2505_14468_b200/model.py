@@ -407,20 +407,25 @@ class MultiLoraModel:
             return None
         gi = {a: i for i, a in enumerate(slots)}
         nq = cfg.q_dim + 2 * cfg.kv_dim
-        tq, to, sh = [], [], []
-        n_mtiles = 0
+        mblocks, sh = [], []
         for tok0, n, _seq, _p0 in segments:
-            a = int(slot_host[tok0])
-            g = gi.get(a, -1)
+            g = gi.get(int(slot_host[tok0]), -1)
             for m0 in range(tok0, tok0 + n, 128):
-                mr = min(128, tok0 + n - m0)
-                n_mtiles += 1
-                tq += [(g, m0, mr, n0) for n0 in range(0, nq, 256)]
-                to += [(g, m0, mr, n0) for n0 in range(0, cfg.hidden, 256)]
+                mblocks.append((g, m0, min(128, tok0 + n - m0)))
                 if g >= 0:
-                    sh.append((g, m0, mr, 0))
-        if n_mtiles > 1.25 * ((T + 127) // 128) + 1:
+                    sh.append((g, m0, min(128, tok0 + n - m0), 0))
+        if len(mblocks) > 1.25 * ((T + 127) // 128) + 1:
             return None
+        # rasterised tile order (groups of 16 row blocks x every column tile): the co-resident
+        # CTAs share a few activation row blocks and weight tiles in L2
+        def raster(n_cols):
+            out = []
+            for r0 in range(0, len(mblocks), 16):
+                grp = mblocks[r0:r0 + 16]
+                for n0 in range(0, n_cols, 256):
+                    out += [(g, m0, mr, n0) for g, m0, mr in grp]
+            return out
+        tq, to = raster(nq), raster(cfg.hidden)
         dev = lambda rows: torch.tensor(rows, dtype=torch.int32).reshape(-1, 4).to(self.device)  # noqa: E731
         return slots, dev(tq), dev(to), dev(sh) if sh else None
 
