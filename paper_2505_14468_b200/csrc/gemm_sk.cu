@@ -285,7 +285,10 @@ __device__ __noinline__ void norm_prologue(const SkArgs& g, int c, int et, float
   }
 }
 
-template <int EPI, typename OutT>
+// PO (part only, slx_gemm_bf16_splitk): every segment is written as an fp32 piece and nothing
+// else — the reduction, cluster, norm-prologue and direct-epilogue code is compiled out, which
+// keeps the register footprint small enough for the consumer's CTAs to co-reside under PDL.
+template <int EPI, typename OutT, bool PO = false>
 __global__ void __launch_bounds__(SK_THREADS, 1)
 gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                SkArgs g) {
@@ -310,7 +313,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
 
   if (threadIdx.x == 0) {
     SK_TR(0);
-    if (g.trace && blockIdx.x == 0) g.trace[4095] = g.part_only ? 4 : 1 + EPI;
+    if (g.trace && blockIdx.x == 0) g.trace[4095] = PO ? 4 : 1 + EPI;
     tc::tma_prefetch_desc(&tmap_x);
     tc::tma_prefetch_desc(&tmap_w);
     for (int s = 0; s < g.stages; ++s) {
@@ -411,7 +414,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       SK_TR(4);
     }
     __syncwarp();
-  } else if (g.cs > 1) {
+  } else if (!PO && g.cs > 1) {
     // ------------------------------------------- epilogue, cluster mode (warps 2-5)
     // This CTA holds piece `rank` of tile c / cs (exactly one segment).  Pieces are staged in
     // each CTA's own (now idle) pipeline smem as [chunk][row][16] fp32 and reduced through
@@ -522,11 +525,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
         const int tile = u / kb, k0 = u - tile * kb;
         const int k1 = min(kb, k0 + (hi - u));
         u += k1 - k0;
-        if (!(k0 == 0 && k1 == kb) && !g.part_only) base[j] = tc::ld_relaxed_gpu(&g.cnt[2 * tile + 1]);
+        if (!(k0 == 0 && k1 == kb) && !PO) base[j] = tc::ld_relaxed_gpu(&g.cnt[2 * tile + 1]);
       }
     }
 
-    if (g.nx != nullptr) norm_prologue(g, c, et, n_ss, n_sv, h_ready);
+    if (!PO && g.nx != nullptr) norm_prologue(g, c, et, n_ss, n_sv, h_ready);
 
     // phase 1: drain every segment (direct epilogue for whole tiles, fp32 piece otherwise)
     int j = 0;
@@ -541,7 +544,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       tc::fence_after_sync();
       if (j == 0 && et == 0) SK_TR(5);
       const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * SK_BN);
-      const bool whole = k0 == 0 && k1 == kb && !g.part_only;
+      const bool whole = k0 == 0 && k1 == kb && !PO;
       if (whole) {
         if (qlive) {
           const int m = r;
@@ -597,12 +600,12 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       if (et == 0) {
         tc::mbar_arrive(&tempty[acc]);
         // release at gpu scope after the CTA barrier publishes every thread's piece stores
-        if (!whole && !g.part_only) tc::red_release_gpu_add(&g.cnt[2 * tile], 1u);
+        if (!whole && !PO) tc::red_release_gpu_add(&g.cnt[2 * tile], 1u);
       }
     }
 
     // phase 2: wait for every split tile held, then reduce this CTA's slice of each
-    if (g.part_only) {   // the consumer reduces the pieces (no rendezvous, no tail)
+    if (PO) {   // the consumer reduces the pieces (no rendezvous, no tail)
       if (et == 0) SK_TR(8);
     } else {
     if (et == 0) {
@@ -695,7 +698,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     }
   }
 
-  if (warp < 2 && g.cs > 1) {   // producer / MMA warps join the epilogue's cluster barriers
+  if (!PO && warp < 2 && g.cs > 1) {   // producer / MMA warps join the epilogue's cluster barriers
     tc::cluster_sync();
     tc::cluster_sync();
   }
@@ -778,10 +781,10 @@ bool sk_plan(int M, int N, int K, SkPlan* p) {
   return true;
 }
 
-template <int EPI, typename OutT>
+template <int EPI, typename OutT, bool PO = false>
 int sk_launch_t(const CUtensorMap& mx, const CUtensorMap& mw, const SkArgs& a, const SkPlan& p,
                 cudaStream_t s) {
-  auto k = gemm_sk_kernel<EPI, OutT>;
+  auto k = gemm_sk_kernel<EPI, OutT, PO>;
   static bool configured = false;
   if (!configured) {
     configure_kernel((const void*)k);
@@ -876,6 +879,7 @@ int gemm_sk_launch(const SkCall& c) {
     return SLX_ERR_CUDA;
   cudaStream_t s = (cudaStream_t)c.stream;
   const bool f32 = c.c_dtype == SLX_DT_F32;
+  if (a.part_only) return sk_launch_t<SLX_EPI_NONE, bf16, true>(mx, mw, a, p, s);
   switch (c.epilogue) {
     case SLX_EPI_NONE:
       return f32 ? sk_launch_t<SLX_EPI_NONE, float>(mx, mw, a, p, s)
