@@ -56,7 +56,8 @@ struct AdArgs {
   DeltaArgs lora;
   PfArgs pf;
   int pf_early;   // SLX_ATTN_PF_EARLY=1: prefetch at kernel start instead of after the last item
-  int dbg_stream; // SLX_ATTN_DBG_STREAM=1 (debug): consumers only drain the rings (copy roofline)
+  int dbg_stream; // SLX_ATTN_DBG_STREAM (debug): 1 consumers only drain the rings (copy roofline),
+                  // 2 skip the LoRA math, 3 LoRA B rows read from global instead of staged
   unsigned long long* trace;   // slx_debug_gemm_trace timeline window (nullptr: off)
 };
 
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs 
           const ItemMeta& mt = meta[i];
           const int hs = j % AD_HSLOTS;
           const bool stage_v = mt.rank <= AD_VMAX;
-          const bool stage_b = mt.rank <= AD_BST;
+          const bool stage_b = mt.rank <= AD_BST && a.dbg_stream != 3;
           uint32_t bytes = 3 * D * 2 + D * 4;
           for (int p = 0; p < 3; ++p)
             if (mt.ti[p] >= 0 && stage_v)
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs 
     const int pos = hd->pos, seq = hd->seq, rank = hd->rank;
     const int nb = (pos + KB - 1) / KB;
     const int kv0 = hd->kv_base;
-    if (a.dbg_stream) {   // copy-engine roofline: drain the header and the KV blocks only
+    if (a.dbg_stream == 1) {   // copy-engine roofline: drain the header and the KV blocks only
       group_sync(g);
       if (gt == 0) tc::mbar_arrive(&h_empty[hs]);
       for (int b = 0; b < nb; ++b) {
@@ -310,7 +311,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs 
     for (int i = gt; i < 3 * D; i += AD_GT) {
       const int p = i / D, e = i - p * D;
       float v = __bfloat162float(hd->row[p][e]);
-      const bf16* bp = hd->b[p];
+      const bf16* bp = a.dbg_stream == 2 ? nullptr : hd->b[p];
       if (bp != nullptr) {
         const bf16* br = (hd->bstaged ? hd->bs[p] : bp) + (size_t)e * rank;
         const float* vv = sc_.sv[p];
@@ -484,7 +485,7 @@ int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int
   const char* e = getenv("SLX_ATTN_PF_EARLY");
   a.pf_early = (e && e[0] == '1') ? 1 : 0;
   const char* ed = getenv("SLX_ATTN_DBG_STREAM");
-  a.dbg_stream = (ed && ed[0] == '1') ? 1 : 0;
+  a.dbg_stream = ed ? atoi(ed) : 0;   // 2: skip the LoRA math, 3: B rows not staged
   a.trace = next_trace_window(5);
   const int items = n_tok * heads;
   const int grid = items < sm_count() ? items : sm_count();

@@ -156,10 +156,10 @@ __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict
   __shared__ float vs[DELTA_VS];
   __shared__ float red[8];
   auto stamp = [&](int i) {
-    if (trace && threadIdx.x == 0) {
+    if (trace && threadIdx.x == 0 && blockIdx.x % RNL_CL == 0) {   // cluster rank 0 per token
       unsigned long long tt;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt)::"memory");
-      trace[(blockIdx.x % 256) * 16 + i] = tt;
+      trace[(blockIdx.x / RNL_CL % 256) * 16 + i] = tt;
       if (blockIdx.x == 0 && i == 0) trace[4095] = 6;
     }
   };

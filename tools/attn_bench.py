@@ -9,13 +9,13 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle import llama_lora as orc  # noqa: E402
+from paper_2505_14468_b200.model import rope_tables  # noqa: E402
 from paper_2505_14468_b200 import ops  # noqa: E402
 
 DEV = "cuda"
 REPS = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 B, H, D, CTX, R, NS = 64, 32, 128, int(os.environ.get("CTX", 128)), 16, 32
-cos, sin = orc.rope_table(CTX + 8, D, 10000.0)
+cos, sin = rope_tables(CTX + 8, D, 10000.0)
 cos_d, sin_d = torch.from_numpy(cos).to(DEV), torch.from_numpy(sin).to(DEV)
 pools = [(torch.randn(B, H, CTX + 1, D, device=DEV).bfloat16(),
           torch.randn(B, H, CTX + 1, D, device=DEV).bfloat16()) for _ in range(3)]
@@ -63,8 +63,8 @@ def run(pipe, lora):
     return {"pipe": pipe, "lora": lora, "ctx": CTX, "us": round(us, 2), "GB/s": round(kv_bytes / us / 1e3, 1)}
 
 
-for pipe in (("1",) if os.environ.get("SLX_ATTN_DBG_STREAM") else ("1", "0")):
+for pipe in (("1",) if os.environ.get("SLX_ATTN_DBG_STREAM") or os.environ.get("PIPE_ONLY") else ("1", "0")):
     for lora in (False, True):
         r = run(pipe, lora)
-        r["kb"] = os.environ.get("SLX_ATTN_KB", "64")
+        r["cfg"] = os.environ.get("SLX_ATTN_CFG", "0")
         print(json.dumps(r), flush=True)

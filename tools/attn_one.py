@@ -6,12 +6,12 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle import llama_lora as orc  # noqa: E402
+from paper_2505_14468_b200.model import rope_tables  # noqa: E402
 from paper_2505_14468_b200 import ops  # noqa: E402
 
 DEV = "cuda"
 B, H, D, CTX, R, NS = 64, 32, 128, 128, 16, 32
-cos, sin = orc.rope_table(CTX + 8, D, 10000.0)
+cos, sin = rope_tables(CTX + 8, D, 10000.0)
 cos_d, sin_d = torch.from_numpy(cos).to(DEV), torch.from_numpy(sin).to(DEV)
 kc = torch.randn(B, H, CTX + 1, D, device=DEV).bfloat16()
 vc = torch.randn(B, H, CTX + 1, D, device=DEV).bfloat16()

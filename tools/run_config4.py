@@ -10,7 +10,7 @@ cluster (180 GB HBM each, two host containers per GPU).  Runs slorasim.run twice
               written by tools/calibrate_b200.py); remote-storage cold fetches (2 GB/s) are kept.
 The simulator is imported from /root/reference (CPU only; not used on the GPU box).
 SLOs follow the reference rule: 5x the warm prefill (profiles.py:28).
-python tools/run_config4.py [--adapters 8] [--duration 120] [--rate 0.05 0.1 0.3]"""
+python tools/run_config4.py [--adapters 8] [--duration 120] [--rate 0.05 0.1 0.3] [--replan-period 10]"""
 import argparse
 import json
 import os
@@ -92,6 +92,8 @@ def main():
     ap.add_argument("--rate", type=float, nargs="+", default=[0.05, 0.1, 0.3])
     ap.add_argument("--gpus", type=int, default=8)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--replan-period", type=float, default=10.0,
+                    help="SimConfig.replan_period_s (reference default 10 s; SURVEY 8d: raise it at 130 fns)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_config4_sim.json"))
     a = ap.parse_args()
     cal = json.load(open(os.path.join(ROOT, "profiles", "r01_calibrated_specs.json")))
@@ -100,13 +102,14 @@ def main():
                      "gpus": a.gpus, "gpu_mem_bytes": 180e9, "duration_s": a.duration,
                      "trace": "BURSTY (reference generate_trace)",
                      "sim": "reference slorasim.run, SimConfig defaults (offload, preload, sharing on)",
+                     "replan_period_s": a.replan_period,
                      "calibration_device": cal["device"]}, "runs": {}}
     for rate, name, params in [(r, n, p) for r in a.rate
                                for n, p in (("paper", PAPER), ("b200", b200_params(cal)))]:
         cat = catalog(params, a.adapters)
         trace, retries = bursty_trace([f.id for f in cat], a.duration, rate, a.seed)
         t0 = time.time()
-        result = run(SimConfig(seed=a.seed), cl, cat, trace)
+        result = run(SimConfig(seed=a.seed, replan_period_s=a.replan_period), cl, cat, trace)
         rep = metrics.build_report(name, result, profiles.default_pricing())
         o = rep.overall
         res["runs"][f"{name}@{rate}"] = {

@@ -38,6 +38,7 @@ torch.cuda.synchronize()
 t = buf.view(200, 4096).cpu().numpy()
 names = {1: "gemm", 2: "gemm+res", 3: "gemm+silu", 4: "gemm-splitk", 5: "attention", 6: "rmsnorm"}
 rows = []
+stamps = []
 for i in range(200):
     kind = int(t[i, 4095] & 0xffffffff)
     if kind == 0:
@@ -57,7 +58,9 @@ for i in range(200):
         exit_ = st[:, 7].max()
         first = st[:, 3][st[:, 3] > 0].min() if (st[:, 3] > 0).any() else entry
     rows.append((names.get(kind, str(kind)), entry, first, exit_, len(st)))
-rows = rows[-(7 * cfg.layers + 2):]   # the captured graph's launches (warm-up windows come first)
+    stamps.append(st)
+rows = rows[-(7 * cfg.layers + 2):]
+stamps = stamps[-len(rows):]   # the captured graph's launches (warm-up windows come first)
 t0 = rows[0][1]
 prev_end = None
 tot = {}
@@ -74,7 +77,8 @@ for i, (name, e, f, x, n) in enumerate(rows):
     d[1] += (x - e) / 1000
     d[2] += (f - e) / 1000
     if i + 1 < len(rows):
-        gaps.setdefault((name, rows[i + 1][0]), []).append((rows[i + 1][1] - x) / 1000)
+        gaps.setdefault((name, rows[i + 1][0]), []).append(((rows[i + 1][1] - x) / 1000,
+                                                             (rows[i + 1][2] - x) / 1000))
 print("step span (first entry -> last exit):", (rows[-1][3] - t0) / 1000, "us")
 # fused-norm prologue phases (GEMM windows with stamps 10..14)
 ph = {}
@@ -93,7 +97,40 @@ for i in range(200):
 for (kind, k), v in sorted(ph.items()):
     v = np.array(v)
     print(f"  prologue kind {kind} stamp {k:2d}: min {v[:, 0].mean():7.2f}  max {v[:, 1].mean():7.2f} us after entry")
+# critical-path share: exit-to-exit time attributed to each launch, split into
+# (previous exit -> this first data) and (this first data -> this exit)
+cp = {}
+for i in range(1, len(rows)):
+    key = (rows[i - 1][0], rows[i][0])
+    d = cp.setdefault(key, [0, 0.0, 0.0])
+    d[0] += 1
+    d[1] += (rows[i][2] - rows[i - 1][3]) / 1000
+    d[2] += (rows[i][3] - rows[i][2]) / 1000
+tot_cp = 0.0
+for (a, b), (n, w, r) in cp.items():
+    print(f"  exit-to-exit {a:>12s} -> {b:12s}: {(w + r) / n:7.2f} us = wait {w / n:6.2f} + run {r / n:6.2f}  (x{n})")
+    tot_cp += w + r
+print(f"  sum of exit-to-exit: {tot_cp:.1f} us")
+# per dependent launch: stamps 0..8 (min / median / max over CTAs) relative to the previous exit
+det = {}
+for i in range(1, len(rows)):
+    key = (rows[i - 1][0], rows[i][0])
+    st = stamps[i]
+    prev_exit = rows[i - 1][3]
+    acc = det.setdefault(key, {})
+    for k in range(9):
+        col = st[:, k][st[:, k] > 0]
+        if len(col):
+            acc.setdefault(k, []).append(((col.min() - prev_exit) / 1000, np.median(col - prev_exit) / 1000,
+                                          (col.max() - prev_exit) / 1000))
+for (a, b), acc in det.items():
+    print(f"  stamps of {b} after {a} exit (min/med/max over CTAs, us):")
+    for k, v in sorted(acc.items()):
+        v = np.array(v).mean(axis=0)
+        print(f"     stamp {k}: {v[0]:8.2f} {v[1]:8.2f} {v[2]:8.2f}")
 for k, (n, us, fd) in tot.items():
     print(f"  {k:12s} {n:3d} launches, mean entry->exit {us / n:7.2f} us, entry->first data {fd / n:6.2f} us")
 for (a, b), v in gaps.items():
-    print(f"  gap {a:>12s} -> {b:12s}: mean {np.mean(v):7.2f} us (next entry - this exit)")
+    v = np.array(v)
+    print(f"  gap {a:>12s} -> {b:12s}: entry {v[:, 0].mean():7.2f} us, first data {v[:, 1].mean():7.2f} us "
+          f"after this exit")
