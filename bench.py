@@ -238,6 +238,11 @@ def run_ours(args):
         m.k_cache[l].normal_(generator=g)
         m.v_cache[l].normal_(generator=g)
     seqs = [m.alloc_seq() for _ in range(BATCH)]
+    led = m.memory_ledger()   # what the reference's ResidencyLedger books per GPU
+    hbm_ledger = {k: round(led[k] / 1e9, 4) for k in ("backbone", "adapter_pool",
+                                                       "adapter_stacked_rows", "kv_pool",
+                                                       "workspace", "total")}
+    hbm_ledger["kv_slot_mb"] = round(led["kv_slot_bytes"] / 1e6, 3)
     slots = tok_slots()
     dg = DecodeGraph(m, seqs, slots.tolist(), fixed_pos=CTX)
     dg.tok.copy_(torch.randint(1, cfg.vocab, (BATCH,), generator=g, device=m.device, dtype=torch.int32))
@@ -382,6 +387,7 @@ def run_ours(args):
                                        "shrink rides in the projection GEMMs as stacked rows, the "
                                        "expand is fused into attention / post-attention RMSNorm"},
             "kernels": kernels,
+            "hbm_ledger_gb": hbm_ledger,
             "clocks": clk.summary(),
             "cpu_baseline": cpu_baseline,
         }

@@ -21,7 +21,7 @@ import os
 import numpy as np
 import torch
 
-from . import ops
+from . import _lib, ops
 from ._lib import EPI_RESIDUAL, EPI_SILU_MUL
 from .config import ATTN_TARGETS, BackboneConfig, LoraConfig
 
@@ -325,6 +325,59 @@ class MultiLoraModel:
                 pw = self.w[f"layers.{l}.{proj}"]
                 for t in ts:
                     ops.pack_rows(pw, None, self.pool.max_rank, pw.n + self._stack_rows(proj, t, slot))
+
+    def memory_ledger(self) -> dict:
+        """Device bytes this model holds, in the categories the reference's ResidencyLedger
+        books per GPU (``/root/reference/pkg/src/slorasim/ledger.py:47-182``): the one backbone
+        copy (``ledger.py:130-134``), the adapter residents (pool slots plus their stacked
+        decode-shrink rows inside the packed q/k/v/o weights), the KV pool (one fixed
+        ``kv_slot_bytes`` reservation per sequence slot) and workspaces.  ``total`` equals the
+        growth of the caching allocator's requested bytes from constructing and loading the
+        model (tests/test_gpu_runtime.py)."""
+        lib = _lib.load()
+        seen: set = set()
+        cats = {"backbone": 0, "adapter_pool": 0, "adapter_stacked_rows": 0, "kv_pool": 0,
+                "workspace": 0}
+        n_storages = [0]
+
+        def add(cat, t, stacked: int = 0):
+            t = getattr(t, "data", t)
+            if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+                return
+            st = t.untyped_storage()
+            if st.data_ptr() in seen:
+                return
+            seen.add(st.data_ptr())
+            nb = st.nbytes()
+            cats[cat] += nb - stacked
+            cats["adapter_stacked_rows"] += stacked
+            n_storages[0] += 1
+
+        for t in self.w.values():
+            stacked = 0
+            if isinstance(t, ops.PackedWeight) and t.n_extra:
+                stacked = t.data.numel() * 2 - int(lib.slx_packed_weight_elems(t.n, t.k)) * 2
+            add("backbone", t, stacked)
+        for b in self.pool.blobs:
+            if b is not None:
+                add("adapter_pool", b)
+        for t in self.k_cache + self.v_cache:
+            add("kv_pool", t)
+
+        def walk(obj, depth=0):
+            if depth > 2:
+                return
+            for v in (obj.values() if isinstance(obj, dict) else
+                      obj if isinstance(obj, (list, tuple)) else vars(obj).values()):
+                if isinstance(v, torch.Tensor) or isinstance(v, ops.PackedWeight):
+                    add("workspace", v)
+                elif isinstance(v, (dict, list, tuple)):
+                    walk(v, depth + 1)
+        walk(self)
+        walk(self.pool)
+        kv_slot = self.cfg.kv_bytes_per_token() * self.max_ctx * (2 if self.dtype == torch.float32 else 1)
+        return {**cats, "total": sum(cats.values()), "storages": n_storages[0],
+                "kv_slot_bytes": kv_slot, "max_seqs": self.max_seqs}
 
     def backbone_bytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in self.w.values())

@@ -94,3 +94,38 @@ def test_calibration_feeds_the_batcher(golden):
     assert predict_ttft(spec, 1) == spec.prefill_base_ms
     assert max_batch_size(spec) >= 1
     assert len(raw["prefill_ms"]) == 4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_memory_ledger_matches_allocator(golden, dtype):
+    """§8 a7: the ledger categories (backbone / adapter residents / KV pool / workspaces) add up
+    to exactly the bytes the caching allocator handed out for the model, and installing / evicting an
+    adapter moves both by the adapter's bytes (the reference books one backbone per GPU plus
+    one reservation per resident adapter, ledger.py:108-134)."""
+    def requested():
+        return torch.cuda.memory_stats()["requested_bytes.all.current"]
+
+    torch.cuda.synchronize()
+    base = requested()
+    seed = int(golden["seed"])
+    m = MultiLoraModel(TINY, dtype=dtype, max_seqs=8, max_ctx=128, n_slots=8, max_rank=16,
+                       max_tokens=512)
+    m.load_backbone(init_backbone(TINY, seed))
+    ads = [init_adapter(TINY, TINY_LORA, seed, a) for a in range(3)]
+    for a, ad in enumerate(ads):
+        m.pool.load(a, ad, TINY_LORA)
+    torch.cuda.synchronize()
+    led = m.memory_ledger()
+    assert led["total"] == requested() - base, led
+    assert led["kv_pool"] == m.max_seqs * led["kv_slot_bytes"]
+    assert led["backbone"] >= m.backbone_bytes()
+    one = led["adapter_pool"] // 3
+    assert one == m.pool.resident_bytes() // 3 and one > 0
+    if dtype == torch.bfloat16:
+        assert led["adapter_stacked_rows"] > 0   # decode-shrink rows of every slot
+    m.pool.evict(2)
+    torch.cuda.synchronize()
+    led2 = m.memory_ledger()
+    assert led["adapter_pool"] - led2["adapter_pool"] == one
+    assert led2["total"] == requested() - base, led2
