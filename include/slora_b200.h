@@ -328,6 +328,12 @@ SLX_API int slx_host_unregister(void* ptr);
 /* Chunked pinned-host -> device copy on `stream`; records `done_event` (cudaEvent_t or NULL). */
 SLX_API int slx_preload_h2d(void* dst_dev, const void* src_pinned, size_t bytes, size_t chunk_bytes,
                     void* stream, void* done_event);
+/* Chunked device -> pinned-host copy on `stream` (demotion of an evicted model to the
+ * container tier); records `done_event` (cudaEvent_t or NULL).
+ * Replaces the modelled demotion of apply_evictions: the GPU bytes leave at once and the
+ * container copy is usable after size / demotion_gbps (offload.py:198-226, engine.py:76). */
+SLX_API int slx_offload_d2h(void* dst_pinned, const void* src_dev, size_t bytes, size_t chunk_bytes,
+                    void* stream, void* done_event);
 /* NCCL communicator owned by the pre-loader (the only collective of the system). */
 SLX_API int slx_nccl_unique_id_bytes(void);
 SLX_API int slx_nccl_get_unique_id(void* out_id);

@@ -119,6 +119,7 @@ SIGNATURES = {
     "slx_host_register": (_i, [_p, _sz]),
     "slx_host_unregister": (_i, [_p]),
     "slx_preload_h2d": (_i, [_p, _p, _sz, _sz, _p, _p]),
+    "slx_offload_d2h": (_i, [_p, _p, _sz, _sz, _p, _p]),
     "slx_nccl_unique_id_bytes": (_i, []),
     "slx_nccl_get_unique_id": (_i, [_p]),
     "slx_nccl_comm_init": (_i, [ctypes.POINTER(_p), _i, _p, _i]),

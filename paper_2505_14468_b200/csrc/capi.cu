@@ -81,6 +81,20 @@ extern "C" int slx_preload_h2d(void* dst_dev, const void* src_pinned, size_t byt
   return SLX_OK;
 }
 
+extern "C" int slx_offload_d2h(void* dst_pinned, const void* src_dev, size_t bytes,
+                               size_t chunk_bytes, void* stream, void* done_event) {
+  SLX_CHECK_ARG(dst_pinned && src_dev && chunk_bytes > 0);
+  cudaStream_t s = (cudaStream_t)stream;
+  for (size_t off = 0; off < bytes; off += chunk_bytes) {
+    const size_t n = bytes - off < chunk_bytes ? bytes - off : chunk_bytes;
+    if (cudaMemcpyAsync((char*)dst_pinned + off, (const char*)src_dev + off, n,
+                        cudaMemcpyDeviceToHost, s) != cudaSuccess)
+      return SLX_ERR_CUDA;
+  }
+  if (done_event && cudaEventRecord((cudaEvent_t)done_event, s) != cudaSuccess) return SLX_ERR_CUDA;
+  return SLX_OK;
+}
+
 extern "C" int slx_nccl_unique_id_bytes(void) { return (int)sizeof(ncclUniqueId); }
 
 extern "C" int slx_nccl_get_unique_id(void* out_id) {

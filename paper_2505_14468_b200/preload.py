@@ -65,15 +65,26 @@ class HostArtifactStore:
             raw = data.detach().contiguous().cpu().view(torch.uint8).numpy().reshape(-1)
         else:
             raw = np.ascontiguousarray(data).view(np.uint8).reshape(-1)
-        off = (self.used + 4095) // 4096 * 4096
-        if off + raw.size > self.capacity:
-            raise MemoryError(f"host artifact store full ({self.capacity} bytes)")
-        start = self.base_off + off
+        art = self.reserve(name, int(raw.size))
+        start = self.base_off + art.offset
         self.buf[start:start + raw.size] = raw
-        art = HostArtifact(name, off, int(raw.size))
-        self.items[name] = art
-        self.used = off + raw.size
         return art
+
+    def reserve(self, name: str, nbytes: int) -> HostArtifact:
+        """Space for an artifact (filled by ``put`` or by a device->host demotion)."""
+        off = (self.used + 4095) // 4096 * 4096
+        if off + nbytes > self.capacity:
+            raise MemoryError(f"host artifact store full ({self.capacity} bytes)")
+        art = HostArtifact(name, off, int(nbytes))
+        self.items[name] = art
+        self.used = off + nbytes
+        return art
+
+    def view(self, name: str) -> np.ndarray:
+        """The artifact's bytes (host view)."""
+        art = self.items[name]
+        start = self.base_off + art.offset
+        return self.buf[start:start + art.nbytes]
 
     def close(self) -> None:
         if self.registered:
