@@ -38,10 +38,13 @@ class ServingRuntime:
     def now_ms(self) -> float:
         return (time.perf_counter() - self.t0) * 1000.0
 
-    def submit(self, request_id, function_id: str, prompt, max_new_tokens: int) -> None:
+    def submit(self, request_id, function_id: str, prompt, max_new_tokens: int,
+               arrival_ms: float | None = None) -> None:
+        """Queue a request (``arrival_ms``: its arrival on this runtime's clock; now if None)."""
         if function_id not in self.functions:
             raise KeyError(f"unknown function {function_id!r}")
-        r = Request(request_id, function_id, list(prompt), int(max_new_tokens), self.now_ms())
+        r = Request(request_id, function_id, list(prompt), int(max_new_tokens),
+                    self.now_ms() if arrival_ms is None else float(arrival_ms))
         r.adapter_slot = self.functions[function_id][1]
         self.requests[request_id] = r
         self.queues[function_id].enqueue(request_id, r.arrival_ms)
