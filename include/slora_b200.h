@@ -298,12 +298,16 @@ SLX_API int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, const 
                   const int32_t* tok_pos, const int32_t* tok_seq, const float* cos_tab,
                   const float* sin_tab, int max_pos, void* k_cache, void* v_cache, int max_ctx,
                   const slx_lora_delta* lora, void* stream);
-/* Same + L2 prefetch hint for the next kernel (issued by the last wave of CTAs; pf may be NULL). */
+/* Same + L2 prefetch hint for the next kernel (issued by the last wave of CTAs; pf may be NULL)
+ * and the pool's sequence-slot count `pool_seqs` (k/v caches are [pool_seqs][kv_heads][max_ctx]
+ * [head_dim]; 0 = unknown): with it, bf16 MHA runs the tensor-core consumer over 128B-swizzled
+ * TMA tiles of the pool. */
 SLX_API int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const void* qkv,
                   int ld_qkv, int n_tok, int heads, int kv_heads, int head_dim,
                   const int32_t* tok_pos, const int32_t* tok_seq, const float* cos_tab,
                   const float* sin_tab, int max_pos, void* k_cache, void* v_cache, int max_ctx,
-                  const slx_lora_delta* lora, const slx_l2_prefetch* pf, void* stream);
+                  int pool_seqs, const slx_lora_delta* lora, const slx_l2_prefetch* pf,
+                  void* stream);
 /* Prefill (tensor cores, mma.sync flash attention, head_dim 128, bf16): `tiles` is a device
  * array of n_tiles {int tok0, nq, seq, pos0} (<= 64 queries of one segment each, size
  * slx_flash_prefill_tile_bytes()); query t of a tile attends cache positions 0..pos0+t of

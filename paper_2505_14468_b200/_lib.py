@@ -110,7 +110,7 @@ SIGNATURES = {
     "slx_rope_attention_decode_lora": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i,
                                             _p, _p, _i, ctypes.POINTER(LoraDelta), _p]),
     "slx_rope_attention_decode_pf": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i,
-                                          _p, _p, _i, ctypes.POINTER(LoraDelta),
+                                          _p, _p, _i, _i, ctypes.POINTER(LoraDelta),
                                           ctypes.POINTER(L2Prefetch), _p]),
     "slx_flash_prefill_tile_bytes": (_sz, []),
     "slx_attention_prefill": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _i, _p, _p, _i, _p]),

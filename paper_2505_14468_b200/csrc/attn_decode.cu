@@ -40,6 +40,7 @@ constexpr int AD_VMAX = 64;                   // LoRA rank staged in the header 
 constexpr int AD_BST = 16;                    // LoRA rank whose B rows are staged by TMA
 
 struct AdArgs {
+  CUtensorMap tmk, tmv;   // K / V pools as 2-D [rows, D] bf16, 64 x 64 boxes, 128B swizzle (MMA)
   bf16* out;
   int ldo;
   const bf16* qkv;
@@ -100,6 +101,26 @@ struct __align__(16) AdScratch {
   bf16 qb[D];
 };
 
+__device__ __forceinline__ void ad_ldsm_x4(uint32_t* r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ad_ldsm_x4_t(uint32_t* r, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ad_mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t ad_pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
 template <int D, int KB>
 constexpr size_t ad_stage_bytes() { return (size_t)2 * KB * D * 2; }
 
@@ -117,8 +138,8 @@ __device__ __forceinline__ float2 bf2_unpack(uint32_t w) {
   return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
 
-template <int D, int KB>
-__global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs a) {
+template <int D, int KB, bool MMA>
+__global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const __grid_constant__ AdArgs a) {
   constexpr int HALF = D / 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* ring = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -162,9 +183,19 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs 
       const uint32_t bytes = (uint32_t)nk * D * 2;
       const size_t off = (((size_t)seq * a.H + h) * a.max_ctx + (size_t)blk * KB) * D;
       uint8_t* st = ring + (size_t)s * ad_stage_bytes<D, KB>();
-      tc::mbar_arrive_expect_tx(&kv_full[s], 2 * bytes);
-      tc::bulk_g2s(st, a.kc + off, bytes, &kv_full[s], pol_kv);
-      tc::bulk_g2s(st + KB * D * 2, a.vc + off, bytes, &kv_full[s], pol_kv);
+      if constexpr (MMA) {   // whole 64-row boxes (rows past pos are masked), swizzled
+        const int row = (int)(off / D);
+        tc::mbar_arrive_expect_tx(&kv_full[s], 2 * KB * D * 2);
+#pragma unroll
+        for (int hf = 0; hf < D / 64; ++hf) {
+          tc::tma_load_2d(st + hf * KB * 128, &a.tmk, &kv_full[s], hf * 64, row, pol_kv);
+          tc::tma_load_2d(st + KB * D * 2 + hf * KB * 128, &a.tmv, &kv_full[s], hf * 64, row, pol_kv);
+        }
+      } else {
+        tc::mbar_arrive_expect_tx(&kv_full[s], 2 * bytes);
+        tc::bulk_g2s(st, a.kc + off, bytes, &kv_full[s], pol_kv);
+        tc::bulk_g2s(st + KB * D * 2, a.vc + off, bytes, &kv_full[s], pol_kv);
+      }
       ++kv_it;
     };
     bool waited = false;
@@ -367,89 +398,181 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs 
         part += __bfloat162float(sc_.qb[lane * DPL + e]) * sc_.kn[lane * DPL + e];
       s_new = warp_sum(part) * a.scale_log2;
     }
-    float m = gw == 0 ? s_new : -INFINITY, l = gw == 0 ? 1.f : 0.f;
-    // P.V accumulators (packed fp32 pairs: FFMA2), dims [lane*DPL, lane*DPL + DPL)
-    float2 acc2[DPL / 2];
+    if constexpr (MMA) {
+      // Tensor-core scores and P.V (mma.sync m16n8k16, fp32 accumulate) on the 128B-swizzled
+      // TMA tiles: warp gw owns keys [16 gw, 16 gw + 16) of every block.  Scores: A = the 16 K
+      // rows (ldmatrix), B = q replicated over the 8 columns, so lane (g, c) holds the scores
+      // of keys g and g + 8.  P.V: A = P (bf16, rows replicated), B = V via ldmatrix.trans; lane
+      // (g, c) accumulates dims 8 nt + 2c, +1 of every n-tile nt.
+      const int gq = lane >> 2, cq = lane & 3;
+      uint32_t qf[D / 16][2];
 #pragma unroll
-    for (int e = 0; e < DPL / 2; ++e)
-      acc2[e] = gw == 0 ? make_float2(sc_.vn[lane * DPL + 2 * e], sc_.vn[lane * DPL + 2 * e + 1])
-                        : make_float2(0.f, 0.f);
-    const int key = gw * KPW + wkey;
-    // this lane's q slice in its key-rotated chunk order (the key index of the lane is the same
-    // in every block), unpacked to fp32 pairs once per item
-    float2 q2[CPL][4];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      const int cc = (c + key) & (CPL - 1);
-      const uint4 u = *reinterpret_cast<const uint4*>(sc_.qb + lq * (D / LPK) + cc * 8);
-      q2[c][0] = bf2_unpack(u.x); q2[c][1] = bf2_unpack(u.y);
-      q2[c][2] = bf2_unpack(u.z); q2[c][3] = bf2_unpack(u.w);
-    }
-    for (int b = 0; b < nb; ++b) {
-      const int it = kv0 + b, s = it % AD_STAGES;
-      const int nk = min(KB, pos - b * KB);
-      tc::mbar_wait(&kv_full[s], (it / AD_STAGES) & 1);
-      const bf16* Ks = reinterpret_cast<const bf16*>(ring + (size_t)s * ad_stage_bytes<D, KB>());
-      const bf16* Vs = Ks + KB * D;
-      // scores: LPK lanes per key, each a D/LPK slice read in the key-rotated chunk order
-      float sc = 0.f;
-      if (key < nk) {
-        const bf16* kr = Ks + (size_t)key * D + lq * (D / LPK);
-        float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const int cc = (c + key) & (CPL - 1);
-          const uint4 u = *reinterpret_cast<const uint4*>(kr + cc * 8);
-          s0 = __ffma2_rn(q2[c][0], bf2_unpack(u.x), s0);
-          s1 = __ffma2_rn(q2[c][1], bf2_unpack(u.y), s1);
-          s0 = __ffma2_rn(q2[c][2], bf2_unpack(u.z), s0);
-          s1 = __ffma2_rn(q2[c][3], bf2_unpack(u.w), s1);
-        }
-        sc = (s0.x + s0.y) + (s1.x + s1.y);
+      for (int ks = 0; ks < D / 16; ++ks) {
+        qf[ks][0] = *reinterpret_cast<const uint32_t*>(sc_.qb + ks * 16 + 2 * cq);
+        qf[ks][1] = *reinterpret_cast<const uint32_t*>(sc_.qb + ks * 16 + 2 * cq + 8);
       }
+      float o[D / 8][4];
 #pragma unroll
-      for (int o = 1; o < LPK; o <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-      sc = key < nk ? sc * a.scale_log2 : -INFINITY;
-      const float m_new = fmaxf(m, warp_max(sc));
-      const float corr = m_new == -INFINITY ? 1.f : exp2f(m - m_new);
-      const float p = key < nk ? exp2f(sc - m_new) : 0.f;
-      l = l * corr + warp_sum(lq == 0 ? p : 0.f);
-      const float2 corr2 = make_float2(corr, corr);
+      for (int nt = 0; nt < D / 8; ++nt) {
+        const float v0 = gw == 0 ? sc_.vn[nt * 8 + 2 * cq] : 0.f;
+        const float v1 = gw == 0 ? sc_.vn[nt * 8 + 2 * cq + 1] : 0.f;
+        o[nt][0] = v0; o[nt][1] = v1; o[nt][2] = v0; o[nt][3] = v1;
+      }
+      float m = gw == 0 ? s_new : -INFINITY;
+      float l = (gw == 0 && lane == 0) ? 1.f : 0.f;   // lane-partial sums, reduced at the end
+      const int mi = lane >> 3;
+      const int rr = gw * 16 + (mi & 1) * 8 + (lane & 7);   // this lane's ldmatrix row (key)
+      const uint32_t rowoff = (uint32_t)rr * 128;
+      const int sw = rr & 7;                                  // 128B swizzle of that row
+      for (int b = 0; b < nb; ++b) {
+        const int it = kv0 + b, s = it % AD_STAGES;
+        const int nk = min(KB, pos - b * KB);
+        tc::mbar_wait(&kv_full[s], (it / AD_STAGES) & 1);
+        const uint32_t kbase = tc::smem_u32(ring + (size_t)s * ad_stage_bytes<D, KB>());
+        const uint32_t vbase = kbase + KB * D * 2;
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int e = 0; e < DPL / 2; ++e) acc2[e] = __fmul2_rn(acc2[e], corr2);
-      // P.V over the warp's keys
+        for (int ks = 0; ks < D / 16; ++ks) {
+          const int ch = ((ks & 3) << 1) + (mi >> 1);
+          uint32_t af[4];
+          ad_ldsm_x4(af, kbase + (uint32_t)((ks >> 2) * KB * 128) + rowoff + (uint32_t)((ch ^ sw) << 4));
+          ad_mma16816((ks & 1) ? sb : sa, af, qf[ks][0], qf[ks][1]);
+        }
+        float s0 = (sa[0] + sb[0]) * a.scale_log2;
+        float s1 = (sa[2] + sb[2]) * a.scale_log2;
+        if (gw * 16 + gq >= nk) s0 = -INFINITY;
+        if (gw * 16 + gq + 8 >= nk) s1 = -INFINITY;
+        float mx = fmaxf(s0, s1);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        const float m_new = fmaxf(m, mx);
+        const float corr = m_new == -INFINITY ? 1.f : exp2f(m - m_new);
+        const float p0 = s0 == -INFINITY ? 0.f : exp2f(s0 - m_new);
+        const float p1 = s1 == -INFINITY ? 0.f : exp2f(s1 - m_new);
+        l = l * corr + (cq == 0 ? p0 + p1 : 0.f);
+        m = m_new;
+        const float pa = __shfl_sync(0xffffffffu, p0, 8 * cq);
+        const float pb = __shfl_sync(0xffffffffu, p0, 8 * cq + 4);
+        const float pc = __shfl_sync(0xffffffffu, p1, 8 * cq);
+        const float pd = __shfl_sync(0xffffffffu, p1, 8 * cq + 4);
+        uint32_t pf[4];
+        pf[0] = ad_pack_bf16(pa, pb);
+        pf[1] = pf[0];
+        pf[2] = ad_pack_bf16(pc, pd);
+        pf[3] = pf[2];
 #pragma unroll
-      for (int kk = 0; kk < KPW; ++kk) {
-        const float pk = __shfl_sync(0xffffffffu, p, kk * LPK);
-        if (gw * KPW + kk < nk) {
-          const float2 p2 = make_float2(pk, pk);
-          const bf16* vr = Vs + (size_t)(gw * KPW + kk) * D + lane * DPL;
-          if (DPL == 4) {
-            const uint2 u = *reinterpret_cast<const uint2*>(vr);
-            acc2[0] = __ffma2_rn(p2, bf2_unpack(u.x), acc2[0]);
-            acc2[(DPL / 2) - 1] = __ffma2_rn(p2, bf2_unpack(u.y), acc2[(DPL / 2) - 1]);
-          } else {
-            acc2[0] = __ffma2_rn(p2, bf2_unpack(*reinterpret_cast<const uint32_t*>(vr)), acc2[0]);
+        for (int nt = 0; nt < D / 8; ++nt) {
+          o[nt][0] *= corr; o[nt][1] *= corr; o[nt][2] *= corr; o[nt][3] *= corr;
+        }
+#pragma unroll
+        for (int j = 0; j < D / 16; ++j) {
+          const int ch = ((j & 3) << 1) + (mi >> 1);
+          uint32_t bf[4];
+          ad_ldsm_x4_t(bf, vbase + (uint32_t)((j >> 2) * KB * 128) + rowoff + (uint32_t)((ch ^ sw) << 4));
+          ad_mma16816(o[2 * j], pf, bf[0], bf[1]);
+          ad_mma16816(o[2 * j + 1], pf, bf[2], bf[3]);
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&kv_empty[s]);   // this warp is done with the stage
+      }
+      l = warp_sum(l);
+      if (lane == 0) {
+        sc_.red[gw] = m;
+        sc_.red[AD_GW + gw] = l;
+      }
+      if (gq == 0) {
+#pragma unroll
+        for (int nt = 0; nt < D / 8; ++nt) {
+          sc_.pv[gw][nt * 8 + 2 * cq] = o[nt][0];
+          sc_.pv[gw][nt * 8 + 2 * cq + 1] = o[nt][1];
+        }
+      }
+    } else {
+      float m = gw == 0 ? s_new : -INFINITY, l = gw == 0 ? 1.f : 0.f;
+      // P.V accumulators (packed fp32 pairs: FFMA2), dims [lane*DPL, lane*DPL + DPL)
+      float2 acc2[DPL / 2];
+  #pragma unroll
+      for (int e = 0; e < DPL / 2; ++e)
+        acc2[e] = gw == 0 ? make_float2(sc_.vn[lane * DPL + 2 * e], sc_.vn[lane * DPL + 2 * e + 1])
+                          : make_float2(0.f, 0.f);
+      const int key = gw * KPW + wkey;
+      // this lane's q slice in its key-rotated chunk order (the key index of the lane is the same
+      // in every block), unpacked to fp32 pairs once per item
+      float2 q2[CPL][4];
+  #pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int cc = (c + key) & (CPL - 1);
+        const uint4 u = *reinterpret_cast<const uint4*>(sc_.qb + lq * (D / LPK) + cc * 8);
+        q2[c][0] = bf2_unpack(u.x); q2[c][1] = bf2_unpack(u.y);
+        q2[c][2] = bf2_unpack(u.z); q2[c][3] = bf2_unpack(u.w);
+      }
+      for (int b = 0; b < nb; ++b) {
+        const int it = kv0 + b, s = it % AD_STAGES;
+        const int nk = min(KB, pos - b * KB);
+        tc::mbar_wait(&kv_full[s], (it / AD_STAGES) & 1);
+        const bf16* Ks = reinterpret_cast<const bf16*>(ring + (size_t)s * ad_stage_bytes<D, KB>());
+        const bf16* Vs = Ks + KB * D;
+        // scores: LPK lanes per key, each a D/LPK slice read in the key-rotated chunk order
+        float sc = 0.f;
+        if (key < nk) {
+          const bf16* kr = Ks + (size_t)key * D + lq * (D / LPK);
+          float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+  #pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const int cc = (c + key) & (CPL - 1);
+            const uint4 u = *reinterpret_cast<const uint4*>(kr + cc * 8);
+            s0 = __ffma2_rn(q2[c][0], bf2_unpack(u.x), s0);
+            s1 = __ffma2_rn(q2[c][1], bf2_unpack(u.y), s1);
+            s0 = __ffma2_rn(q2[c][2], bf2_unpack(u.z), s0);
+            s1 = __ffma2_rn(q2[c][3], bf2_unpack(u.w), s1);
+          }
+          sc = (s0.x + s0.y) + (s1.x + s1.y);
+        }
+  #pragma unroll
+        for (int o = 1; o < LPK; o <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+        sc = key < nk ? sc * a.scale_log2 : -INFINITY;
+        const float m_new = fmaxf(m, warp_max(sc));
+        const float corr = m_new == -INFINITY ? 1.f : exp2f(m - m_new);
+        const float p = key < nk ? exp2f(sc - m_new) : 0.f;
+        l = l * corr + warp_sum(lq == 0 ? p : 0.f);
+        const float2 corr2 = make_float2(corr, corr);
+  #pragma unroll
+        for (int e = 0; e < DPL / 2; ++e) acc2[e] = __fmul2_rn(acc2[e], corr2);
+        // P.V over the warp's keys
+  #pragma unroll
+        for (int kk = 0; kk < KPW; ++kk) {
+          const float pk = __shfl_sync(0xffffffffu, p, kk * LPK);
+          if (gw * KPW + kk < nk) {
+            const float2 p2 = make_float2(pk, pk);
+            const bf16* vr = Vs + (size_t)(gw * KPW + kk) * D + lane * DPL;
+            if (DPL == 4) {
+              const uint2 u = *reinterpret_cast<const uint2*>(vr);
+              acc2[0] = __ffma2_rn(p2, bf2_unpack(u.x), acc2[0]);
+              acc2[(DPL / 2) - 1] = __ffma2_rn(p2, bf2_unpack(u.y), acc2[(DPL / 2) - 1]);
+            } else {
+              acc2[0] = __ffma2_rn(p2, bf2_unpack(*reinterpret_cast<const uint32_t*>(vr)), acc2[0]);
+            }
           }
         }
+        m = m_new;
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&kv_empty[s]);   // this warp is done with the stage
       }
-      m = m_new;
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&kv_empty[s]);   // this warp is done with the stage
+      float acc[DPL];
+  #pragma unroll
+      for (int e = 0; e < DPL / 2; ++e) {
+        acc[2 * e] = acc2[e].x;
+        acc[2 * e + 1] = acc2[e].y;
+      }
+      // ---- merge the group's warp states (fixed order) and write the head's output
+      if (lane == 0) {
+        sc_.red[gw] = m;
+        sc_.red[AD_GW + gw] = l;
+      }
+  #pragma unroll
+      for (int e = 0; e < DPL; ++e) sc_.pv[gw][lane * DPL + e] = acc[e];
     }
-    float acc[DPL];
-#pragma unroll
-    for (int e = 0; e < DPL / 2; ++e) {
-      acc[2 * e] = acc2[e].x;
-      acc[2 * e + 1] = acc2[e].y;
-    }
-    // ---- merge the group's warp states (fixed order) and write the head's output
-    if (lane == 0) {
-      sc_.red[gw] = m;
-      sc_.red[AD_GW + gw] = l;
-    }
-#pragma unroll
-    for (int e = 0; e < DPL; ++e) sc_.pv[gw][lane * DPL + e] = acc[e];
     group_sync(g);
     if (gt < D) {
       float mx = sc_.red[0];
@@ -475,7 +598,8 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(AdArgs 
 int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int n_tok, int heads,
                             int head_dim, const int32_t* tok_pos, const int32_t* tok_seq,
                             const float* cos_tab, const float* sin_tab, void* k_cache,
-                            void* v_cache, int max_ctx, float scale_log2, const DeltaArgs& lora,
+                            void* v_cache, int max_ctx, long long n_pool_rows, float scale_log2,
+                            const DeltaArgs& lora,
                             const PfArgs& pf, cudaStream_t stream) {
   AdArgs a{};
   a.out = (bf16*)out; a.ldo = ldo; a.qkv = (const bf16*)qkv; a.ld = ld_qkv;
@@ -496,8 +620,17 @@ int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return launch_ex(kernel, dim3((unsigned)grid), dim3(AD_THREADS), smem, stream, 1u, a);
   };
-  if (head_dim == 128) return go(attn_decode_pipe_kernel<128, 64>, ad_smem<128, 64>());
-  if (head_dim == 64) return go(attn_decode_pipe_kernel<64, 128>, ad_smem<64, 128>());
+  if (env_int("SLX_ATTN_MMA", 1)) {
+    const int rows = (int)n_pool_rows;
+    if ((head_dim == 128 || head_dim == 64) && n_pool_rows > 0 && n_pool_rows < (1LL << 31) &&
+        make_tmap(&a.tmk, k_cache, rows, head_dim, head_dim, 64) &&
+        make_tmap(&a.tmv, v_cache, rows, head_dim, head_dim, 64)) {
+      if (head_dim == 128) return go(attn_decode_pipe_kernel<128, 64, true>, ad_smem<128, 64>());
+      return go(attn_decode_pipe_kernel<64, 64, true>, ad_smem<64, 64>());
+    }
+  }
+  if (head_dim == 128) return go(attn_decode_pipe_kernel<128, 64, false>, ad_smem<128, 64>());
+  if (head_dim == 64) return go(attn_decode_pipe_kernel<64, 128, false>, ad_smem<64, 128>());
   return SLX_ERR_UNSUPPORTED;
 }
 

@@ -13,7 +13,8 @@ namespace slx {
 int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int n_tok, int heads,
                             int head_dim, const int32_t* tok_pos, const int32_t* tok_seq,
                             const float* cos_tab, const float* sin_tab, void* k_cache,
-                            void* v_cache, int max_ctx, float scale_log2, const DeltaArgs& lora,
+                            void* v_cache, int max_ctx, long long n_pool_rows, float scale_log2,
+                            const DeltaArgs& lora,
                             const PfArgs& pf, cudaStream_t stream);   // attn_decode.cu
 
 static bool attn_pipe_enabled() {   // SLX_ATTN_PIPE=0: the per-(token, head) kernel (A/B tests)
@@ -1011,7 +1012,7 @@ extern "C" int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, con
                                               const slx_lora_delta* lora, void* stream) {
   return slx_rope_attention_decode_pf(dtype, out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads,
                                       head_dim, tok_pos, tok_seq, cos_tab, sin_tab, max_pos,
-                                      k_cache, v_cache, max_ctx, lora, nullptr, stream);
+                                      k_cache, v_cache, max_ctx, 0, lora, nullptr, stream);
 }
 
 extern "C" int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const void* qkv,
@@ -1019,13 +1020,13 @@ extern "C" int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const
                                             int head_dim, const int32_t* tok_pos,
                                             const int32_t* tok_seq, const float* cos_tab,
                                             const float* sin_tab, int max_pos, void* k_cache,
-                                            void* v_cache, int max_ctx,
+                                            void* v_cache, int max_ctx, int pool_seqs,
                                             const slx_lora_delta* lora, const slx_l2_prefetch* pf,
                                             void* stream) {
   SLX_CHECK_ARG(n_tok >= 0 && heads > 0 && kv_heads > 0 && heads % kv_heads == 0 &&
                 ld_qkv >= (heads + 2 * kv_heads) * head_dim && ldo >= heads * head_dim && out &&
                 qkv && tok_pos && tok_seq && cos_tab && sin_tab && k_cache && v_cache &&
-                max_pos > 0 && max_ctx > 0);
+                max_pos > 0 && max_ctx > 0 && pool_seqs >= 0);
   SLX_CHECK_ARG(ldo % 8 == 0 && ld_qkv % 8 == 0 && delta_valid(lora));
   SLX_CHECK_ALIGN(k_cache, 16);
   SLX_CHECK_ALIGN(v_cache, 16);
@@ -1038,7 +1039,8 @@ extern "C" int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const
   if (dtype == SLX_DT_BF16 && heads == kv_heads && attn_pipe_enabled() && ld_qkv % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(qkv) & 15) == 0)
     return attn_decode_pipe_launch(out, ldo, qkv, ld_qkv, n_tok, heads, head_dim, tok_pos, tok_seq,
-                                   cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s);
+                                   cos_tab, sin_tab, k_cache, v_cache, max_ctx,
+                                   (long long)pool_seqs * kv_heads * max_ctx, scale, la, pa, s);
   if (dtype == SLX_DT_BF16)
     return head_dim == 64 ? launch_rope_attn<bf16, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s)
                           : launch_rope_attn<bf16, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s);

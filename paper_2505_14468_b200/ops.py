@@ -495,7 +495,8 @@ def rope_attention_decode(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq,
     check(_lib.load().slx_rope_attention_decode_pf(
         _dt(out), _ptr(out), _ld(out), _ptr(qkv), _ld(qkv), qkv.shape[0], heads, kv_heads, head_dim,
         _ptr(tok_pos), _ptr(tok_seq), _ptr(cos), _ptr(sin), cos.shape[0], _ptr(k_cache),
-        _ptr(v_cache), k_cache.shape[2], None if lora is None else ctypes.byref(lora),
+        _ptr(v_cache), k_cache.shape[2], k_cache.shape[0],
+        None if lora is None else ctypes.byref(lora),
         None if prefetch is None else ctypes.byref(prefetch), _stream()),
         "slx_rope_attention_decode")
     return out
