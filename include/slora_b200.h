@@ -135,6 +135,26 @@ SLX_API int slx_gemm_bf16_norm(void* A, int lda, const void* W, void* C, int ldc
                   const void* R, int ldr, int M, int N, int K, int epilogue, int n_main, void* C2,
                   int ldc2, void* ws, size_t ws_bytes, const slx_norm_in* norm,
                   const slx_l2_prefetch* pf, void* stream);
+/* Row RMS across two decode GEMMs, so the RMSNorm between them needs no kernel of its own:
+ *   producer (epilogue SLX_EPI_RESIDUAL, bf16 C): ss_out[m * ss_out_ld + n / 16] = sum of
+ *     squares of the 16 stored values C[m, n .. n+16) (main columns; ss_out_ld >= n_main / 16);
+ *   consumer (epilogue SLX_EPI_NONE or SLX_EPI_RESIDUAL): row m of A.W^T (and of the side
+ *     output) is scaled by 1 / sqrt(sum(ss_in[m * ss_in_n .. + ss_in_n)) / d + eps) before the
+ *     epilogue — i.e. rmsnorm(A) . W^T when the norm weight is folded into W's columns.
+ * Either pointer may be NULL.  Decode shapes only (tiled weights, M <= 64): SLX_ERR_UNSUPPORTED
+ * otherwise. */
+typedef struct slx_row_ss {
+  float* ss_out;
+  int ss_out_ld;
+  const float* ss_in;
+  int ss_in_n;
+  int d;
+  float eps;
+} slx_row_ss;
+SLX_API int slx_gemm_bf16_rss(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
+                  const void* R, int ldr, int M, int N, int K, int epilogue, int n_main, void* C2,
+                  int ldc2, void* ws, size_t ws_bytes, const slx_row_ss* rss,
+                  const slx_l2_prefetch* pf, void* stream);
 /* Debug only: following slx_gemm_bf16 launches write 16 u64 globaltimer slots per CTA into
  * the device buffer `buf` (phase timeline: entry, prologue, past PDL wait, first stage landed,
  * last MMA issued, accumulator ready, split-K reduction start, exit, reduction end, segment

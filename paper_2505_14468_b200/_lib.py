@@ -58,6 +58,12 @@ class NormIn(ctypes.Structure):
                 ("lora", ctypes.POINTER(LoraDelta)), ("ss", _p), ("ss_bytes", _sz), ("bar", _p)]
 
 
+class RowSS(ctypes.Structure):
+    """slx_row_ss: row sums of squares written by one decode GEMM, row scales of the next."""
+    _fields_ = [("ss_out", _p), ("ss_out_ld", _i), ("ss_in", _p), ("ss_in_n", _i), ("d", _i),
+                ("eps", _f)]
+
+
 class L2Prefetch(ctypes.Structure):
     """slx_l2_prefetch: the next kernel's first bytes (two regions)."""
     _fields_ = [("ptr", _p * 2), ("bytes", _sz * 2)]
@@ -76,6 +82,8 @@ SIGNATURES = {
     "slx_gemm_bf16_splitk": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _sz, ctypes.POINTER(L2Prefetch), _p]),
     "slx_gemm_bf16_norm": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _p, _i, _p, _sz,
                                 ctypes.POINTER(NormIn), ctypes.POINTER(L2Prefetch), _p]),
+    "slx_gemm_bf16_rss": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _p, _i, _p, _sz,
+                               ctypes.POINTER(RowSS), ctypes.POINTER(L2Prefetch), _p]),
     "slx_gemm_bf16_pf": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p,
                               _sz, ctypes.POINTER(L2Prefetch), _p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),

@@ -25,6 +25,7 @@ struct SkCall {
   int splits;
   size_t part_bytes;
   const slx_norm_in* norm;   // slx_gemm_bf16_norm: fused input RMSNorm prologue (A = norm->h)
+  const slx_row_ss* rss = nullptr;   // slx_gemm_bf16_rss: row sums of squares out / row scales in
 };
 int gemm_sk_launch(const SkCall& c);
 // Debug timeline window for the next traced launch (nullptr when tracing is off); kinds:

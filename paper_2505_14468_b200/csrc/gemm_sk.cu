@@ -79,6 +79,15 @@ struct SkArgs {
   int ldnh;
   float* nss;        // [M][G] partial sums of squares
   uint32_t* nbar;    // [2] grid-barrier counters of this call site (monotonic)
+  // row RMS (slx_gemm_bf16_rss): producer side writes the sum of squares of every stored
+  // 16-column chunk of C (bf16-rounded, main columns) to ss_out[m * ss_ld + n / 16]; consumer
+  // side scales row m of the accumulator by rsqrt(sum(ss_in[m * ss_n ..]) / ss_d + ss_eps)
+  // before the epilogue (the RMSNorm of its A operand, whose weight is folded into W)
+  float* ss_out;
+  int ss_ld;
+  const float* ss_in;
+  int ss_n, ss_d;
+  float ss_eps;
 };
 
 __device__ __forceinline__ unsigned long long sk_timer() {
@@ -124,7 +133,12 @@ __device__ __forceinline__ void sk_load_res(const SkArgs& g, int m, int n, int l
 
 // Final values of 16 columns [n, n+16) of row m (not SiLU): side output or C (+ residual).
 template <int EPI, typename OutT>
-__device__ __forceinline__ void sk_finish(const SkArgs& g, int m, int n, float* v, const float* res) {
+__device__ __forceinline__ void sk_finish(const SkArgs& g, int m, int n, float* v, const float* res,
+                                          float rsc = 1.f) {
+  if (rsc != 1.f) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] *= rsc;
+  }
   if (g.C2 != nullptr && n >= g.n_main) {
     float* row = g.C2 + (size_t)m * g.ldc2 + (n - g.n_main);
     if (n + 16 <= g.N) {
@@ -143,7 +157,34 @@ __device__ __forceinline__ void sk_finish(const SkArgs& g, int m, int n, float* 
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] += res[j];
   }
+  if (g.ss_out != nullptr) {   // sum of squares of the values as stored
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float y = to_f32(from_f32<OutT>(v[j]));
+      ss = n + j < lim ? fmaf(y, y, ss) : ss;
+    }
+    g.ss_out[(size_t)m * g.ss_ld + n / 16] = ss;
+  }
   sk_store16(reinterpret_cast<OutT*>(g.C) + (size_t)m * g.ldc, n, lim, v);
+}
+
+// Row scales of the consumer side (epilogue threads; rows < M): 1 / sqrt(mean of squares + eps)
+// from the producer's chunk partials, summed in a fixed order (deterministic).
+__device__ __forceinline__ void sk_row_scales(const SkArgs& g, int et, float* srow) {
+  if (et < g.M) {
+    const float* p = g.ss_in + (size_t)et * g.ss_n;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int i = 0;
+    for (; i + 8 <= g.ss_n; i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __ldcg(p + i + j);
+    }
+    for (; i < g.ss_n; ++i) acc[0] += __ldcg(p + i);
+    const float tot = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    srow[et] = 1.0f / sqrtf(tot / (float)g.ss_d + g.ss_eps);
+  }
+  tc::named_bar_sync(1, 128);
 }
 
 // fast-math SiLU: no IEEE-division slow path (whose per-element branch serialises the epilogue)
@@ -426,6 +467,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     const int n_out = silu ? g.N / 2 : g.N;
     float* stg = reinterpret_cast<float*>(smem);
     if (g.nx != nullptr) norm_prologue(g, c, et, n_ss, n_sv, h_ready);
+    if (g.ss_in != nullptr) sk_row_scales(g, et, n_ss);   // overlaps the mainloop
     tc::mbar_wait(&tfull[0], 0);
     if (et == 0) SK_TR(9);
     __syncwarp();
@@ -501,7 +543,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
         for (int e = 0; e < 16; ++e) a[e] = sk_silu(a[e]) * b[e];
         sk_store16(reinterpret_cast<OutT*>(g.C) + (size_t)m * g.ldc, tile * 128 + ch * 16, n_out, a);
       } else if (n < g.N) {
-        sk_finish<EPI, OutT>(g, m, n, a, res);
+        sk_finish<EPI, OutT>(g, m, n, a, res, g.ss_in ? n_ss[m] : 1.f);
       }
     }
     if (et == 0) SK_TR(8);
@@ -530,6 +572,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     }
 
     if (!PO && g.nx != nullptr) norm_prologue(g, c, et, n_ss, n_sv, h_ready);
+    if (!PO && g.ss_in != nullptr) sk_row_scales(g, et, n_ss);   // overlaps the mainloop
 
     // phase 1: drain every segment (direct epilogue for whole tiles, fp32 piece otherwise)
     int j = 0;
@@ -570,8 +613,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
                   sk_load_res<OutT>(g, m, n, lim, r0);
                   sk_load_res<OutT>(g, m, n + 16, lim, r1);
                 }
-                sk_finish<EPI, OutT>(g, m, n, v0, r0);
-                if (n + 16 < g.N) sk_finish<EPI, OutT>(g, m, n + 16, v1, r1);
+                const float rsc = g.ss_in ? n_ss[m] : 1.f;
+                sk_finish<EPI, OutT>(g, m, n, v0, r0, rsc);
+                if (n + 16 < g.N) sk_finish<EPI, OutT>(g, m, n + 16, v1, r1, rsc);
               }
             }
           }
@@ -686,7 +730,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
           for (int e = 0; e < 16; ++e) a[e] = sk_silu(a[e]) * b[e];
           sk_store16(reinterpret_cast<OutT*>(g.C) + (size_t)m * g.ldc, tile * 128 + ch * 16, n_out, a);
         } else if (n < g.N) {
-          sk_finish<EPI, OutT>(g, m, n, a, res);
+          sk_finish<EPI, OutT>(g, m, n, a, res, g.ss_in ? n_ss[m] : 1.f);
         }
       }
       if (et == 0 && dbg_t == 0) SK_TR(13);
@@ -870,6 +914,10 @@ int gemm_sk_launch(const SkCall& c) {
     a.nlora = delta_args(n.lora);
     a.nh = (bf16*)c.A; a.ldnh = c.lda;
     a.nss = n.ss; a.nbar = n.bar;
+  }
+  if (c.rss != nullptr) {
+    a.ss_out = c.rss->ss_out; a.ss_ld = c.rss->ss_out_ld;
+    a.ss_in = c.rss->ss_in; a.ss_n = c.rss->ss_in_n; a.ss_d = c.rss->d; a.ss_eps = c.rss->eps;
   }
   a.trace = c.trace;
   a.pf = pf_args(c.pf);

@@ -705,6 +705,40 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
                           C2, ldc2, ws, ws_bytes, nullptr, stream);
 }
 
+extern "C" int slx_gemm_bf16_rss(const void* A, int lda, const void* W, void* C, int ldc,
+                                 int c_dtype, const void* R, int ldr, int M, int N, int K,
+                                 int epilogue, int n_main, void* C2, int ldc2, void* ws,
+                                 size_t ws_bytes, const slx_row_ss* rss,
+                                 const slx_l2_prefetch* pf, void* stream) {
+  SLX_CHECK_ARG(rss != nullptr && A && W && C && M >= 0 && N > 0 && K > 0 && lda >= K &&
+                K % 8 == 0 && lda % 8 == 0 && ldc % 8 == 0 && ws != nullptr);
+  SLX_CHECK_ARG(epilogue == SLX_EPI_NONE || epilogue == SLX_EPI_RESIDUAL);
+  SLX_CHECK_ARG(c_dtype == SLX_DT_BF16 || c_dtype == SLX_DT_F32);
+  SLX_CHECK_ALIGN(A, 16);
+  SLX_CHECK_ALIGN(W, 16);
+  SLX_CHECK_ALIGN(C, 16);
+  SLX_CHECK_ALIGN(ws, 256);
+  if (C2 != nullptr) {
+    SLX_CHECK_ARG(n_main > 0 && n_main < N && n_main % 16 == 0 && ldc2 >= N - n_main &&
+                  ldc2 % 4 == 0 && ldc >= n_main);
+    SLX_CHECK_ALIGN(C2, 16);
+  } else {
+    SLX_CHECK_ARG(ldc >= N);
+    n_main = N;
+  }
+  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= n_main && ldr % 8 == 0);
+  if (rss->ss_out != nullptr)
+    SLX_CHECK_ARG(epilogue == SLX_EPI_RESIDUAL && c_dtype == SLX_DT_BF16 &&
+                  rss->ss_out_ld >= (n_main + 15) / 16);
+  if (rss->ss_in != nullptr) SLX_CHECK_ARG(rss->ss_in_n > 0 && rss->d > 0 && rss->eps >= 0.f);
+  if (M == 0) return SLX_OK;
+  if (M > 64) return SLX_ERR_UNSUPPORTED;
+  SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
+            ws, ws_bytes, stream, next_trace_window(1 + epilogue), pf, nullptr, 0, 0, nullptr};
+  sc.rss = rss;
+  return gemm_sk_launch(sc);
+}
+
 extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, int ldc,
                                 int c_dtype, const void* R, int ldr, int M, int N, int K,
                                 int epilogue, int w_layout, int n_main, void* C2, int ldc2,

@@ -208,6 +208,15 @@ class MultiLoraModel:
         self.l2_prefetch_mb = float(os.environ.get("SLX_L2_PF_MB", "16"))
         self._pf_cache: dict = {}
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
+        # decode: the pre-attention RMSNorm of layers >= 1 folded across two GEMMs — the down
+        # projection writes the residual plus its row sums of squares, the next q/k/v GEMM reads
+        # the raw residual with the norm weight folded into its columns (and stacked A rows) and
+        # scales its rows by 1/rms in the epilogue (no norm kernel between them).  Off by
+        # default: measured 0.55 ms/step SLOWER on the 7B step — the down projection then needs
+        # its own split-K reduction, whose rendezvous tail (~10 us) outweighs the norm kernel
+        # and boundary it removes.  SLX_NORM_FOLD=1 (read at construction: it also keeps a
+        # folded copy of every q/k/v weight).
+        self.norm_fold = os.environ.get("SLX_NORM_FOLD", "0") == "1"
         # prefill: the LoRA expand folded into the backbone GEMM as one extra K block
         self.lora_fold = os.environ.get("SLX_LORA_FOLD", "1") != "0"
         self.pool.on_install = self._stack_install
@@ -267,6 +276,8 @@ class MultiLoraModel:
             down[:, :cfg.ffn] = rn(cfg.hidden, cfg.ffn)
             w[p + "w_down"] = down
             if self.dtype == torch.bfloat16:   # pack layer by layer to bound peak memory
+                if l > 0 and self.norm_fold:
+                    w[p + "w_qkv_fold"] = self._fold_qkv(w[p + "w_qkv"], w[p + "input_norm"])
                 for k in self.PROJ:
                     w[p + k] = ops.pack_weight(w[p + k], self._extra_rows(k))
         if self.dtype == torch.bfloat16:
@@ -281,9 +292,17 @@ class MultiLoraModel:
         if self.dtype != torch.bfloat16:
             return
         for k in list(self.w):
+            if self.norm_fold and k.endswith(".w_qkv") and not k.startswith("layers.0."):
+                pre = k[:-len("w_qkv")]
+                self.w[pre + "w_qkv_fold"] = self._fold_qkv(self.w[k], self.w[pre + "input_norm"])
             if k == "lm_head" or k.split(".")[-1] in self.PROJ:
                 self.w[k] = ops.pack_weight(self.w[k], self._extra_rows(k.split(".")[-1]))
         torch.cuda.synchronize(self.device)
+
+    def _fold_qkv(self, w_qkv: torch.Tensor, g: torch.Tensor):
+        """Packed W_qkv . diag(g) (the input RMSNorm weight folded into the columns)."""
+        wf = (w_qkv.float() * g.float()[None, :]).to(torch.bfloat16)
+        return ops.pack_weight(wf, self._extra_rows("w_qkv"))
 
     def _extra_rows(self, proj: str) -> int:
         targets = self.stack.get(proj, ())
@@ -302,14 +321,22 @@ class MultiLoraModel:
                 if t not in ts:
                     continue
                 pw = self.w[f"layers.{l}.{proj}"]
+                pf = self.w.get(f"layers.{l}.{proj}_fold")
                 row0 = pw.n + self._stack_rows(proj, t, slot)
                 if t in lora.targets:
                     a = blob[ao:ao + lora.rank * di].view(lora.rank, di)
                     ops.pack_rows(pw, a, lora.rank, row0)
+                    if pf is not None:   # folded copy: A . diag(input_norm)
+                        g = self.w[f"layers.{l}.input_norm"].float()
+                        ops.pack_rows(pf, (a.float() * g[None, :]).to(torch.bfloat16), lora.rank, row0)
                     if lora.rank < R:
                         ops.pack_rows(pw, None, R - lora.rank, row0 + lora.rank)
+                        if pf is not None:
+                            ops.pack_rows(pf, None, R - lora.rank, row0 + lora.rank)
                 else:
                     ops.pack_rows(pw, None, R, row0)
+                    if pf is not None:
+                        ops.pack_rows(pf, None, R, row0)
 
     def _restack(self) -> None:
         """(Re)write the stacked A rows of every resident adapter (backbone loaded later)."""
@@ -323,8 +350,11 @@ class MultiLoraModel:
         for l in range(self.cfg.layers):
             for proj, ts in self.stack.items():
                 pw = self.w[f"layers.{l}.{proj}"]
+                pf = self.w.get(f"layers.{l}.{proj}_fold")
                 for t in ts:
                     ops.pack_rows(pw, None, self.pool.max_rank, pw.n + self._stack_rows(proj, t, slot))
+                    if pf is not None:
+                        ops.pack_rows(pf, None, self.pool.max_rank, pf.n + self._stack_rows(proj, t, slot))
 
     def memory_ledger(self) -> dict:
         """Device bytes this model holds, in the categories the reference's ResidencyLedger
@@ -631,6 +661,11 @@ class MultiLoraModel:
             part_dn = torch.empty(ops.splitk_bytes(T, d, S_dn) // 4, dtype=torch.float32,
                                   device=dev)
         pending = None   # split-K pieces of the down projection, consumed by the next norm
+        fnorm0 = sk_mode and self.fuse_norm and self.fuse_expand and "w_qkv" in self.stack
+        rss_mode = (sk_mode and self.norm_fold and not fnorm0 and "w_qkv" in self.stack
+                    and "down" not in self.targets and "layers.1.w_qkv_fold" in w)
+        if rss_mode:
+            ss_rows = torch.empty((T, d // 16), dtype=torch.float32, device=dev)
         ops.embedding(x, w["embed"], tokens)
         if self.targets:
             ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
@@ -638,8 +673,9 @@ class MultiLoraModel:
         fnorm = sk_mode and self.fuse_norm and self.fuse_expand and "w_qkv" in self.stack
         for l in range(cfg.layers):
             p = f"layers.{l}."
-            if fnorm:
-                pass   # built by the qkv GEMM's prologue below
+            folded = rss_mode and l > 0   # x and its row sums of squares come from the down GEMM
+            if fnorm or folded:
+                pass   # built by the qkv GEMM's prologue / folded into it
             elif pending is not None:
                 ops.rmsnorm_fused(h, x, w[p + "input_norm"], cfg.rms_eps, pending)
                 pending = None
@@ -647,7 +683,8 @@ class MultiLoraModel:
                 ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
             d_qkv = None
             pfd = decode and dt == torch.bfloat16
-            nxt = f"layers.{l + 1}.w_qkv" if l + 1 < cfg.layers else "lm_head"
+            nxt = (f"layers.{l + 1}.w_qkv" + ("_fold" if rss_mode else "")
+                   if l + 1 < cfg.layers else "lm_head")
             pf_qkv = self._pf(("kv", l), self.k_cache[l], self.v_cache[l]) if pfd else None
             pf_att = self._pf(p + "wo", w[p + "wo"]) if pfd else None
             pf_o = self._pf(p + "w_gu", w[p + "w_gu"]) if pfd else None
@@ -665,6 +702,10 @@ class MultiLoraModel:
                                  self.norm_bar[0:2], sk=pending)
                 pending = None
                 ops.gemm_norm(h, w[p + "w_qkv"], qkv, nq, side=v_qkv, prefetch=pf_qkv)
+                d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
+            elif folded:
+                ops.gemm_rss(x, w[p + "w_qkv_fold"], qkv, side=v_qkv, ss_in=ss_rows, norm_dim=d,
+                             eps=cfg.rms_eps, prefetch=pf_qkv)
                 d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
             elif stacked and "w_qkv" in self.stack:
                 ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv, prefetch=pf_qkv)
@@ -733,7 +774,10 @@ class MultiLoraModel:
                 self._gemm(h, w[p + "w_gu"], gu)
                 self._lora(gu, h, l, ("gate", "up"), {"gate": (0, 128, 256), "up": (128, 128, 256)})
                 ops.silu_mul_blocked(mlp, gu, self.ffn_pad)
-            if sk_mode and "down" not in self.targets:
+            if rss_mode and l + 1 < cfg.layers:
+                ops.gemm_rss(mlp, w[p + "w_down"], x, epilogue=EPI_RESIDUAL, residual=x,
+                             ss_out=ss_rows, prefetch=pf_dn)
+            elif sk_mode and "down" not in self.targets:
                 pending = ops.gemm_splitk(mlp, w[p + "w_down"], S_dn, part_dn, prefetch=pf_dn)
             else:
                 self._gemm(mlp, w[p + "w_down"], x, residual=x, prefetch=pf_dn)

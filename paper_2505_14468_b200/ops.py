@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import (DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED,
-                   L2Prefetch, LoraDelta, LoraTarget, NormIn, SplitKIn, check)
+                   L2Prefetch, LoraDelta, LoraTarget, NormIn, RowSS, SplitKIn, check)
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
 
@@ -224,6 +224,36 @@ def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
                                        _ld(side) if n_tot > n_main else 0, _ptr(wsb), wsb.numel(),
                                        None if prefetch is None else ctypes.byref(prefetch),
                                        _stream()), "slx_gemm_bf16")
+    return out
+
+
+@_op("gemm", 1)
+def gemm_rss(a: torch.Tensor, w, out: torch.Tensor, *, epilogue: int = EPI_NONE,
+             residual: torch.Tensor | None = None, side: torch.Tensor | None = None,
+             ss_out: torch.Tensor | None = None, ss_in: torch.Tensor | None = None,
+             norm_dim: int = 0, eps: float = 0.0, ws=None, prefetch=None) -> torch.Tensor:
+    """Decode GEMM with row RMS across kernels (slx_gemm_bf16_rss): ``ss_out`` (fp32 [M, >=N/16])
+    receives the per-16-column sums of squares of the stored output (residual epilogue); with
+    ``ss_in`` (fp32 [M, n]) the rows are scaled by 1/sqrt(sum/norm_dim + eps) — the RMSNorm of
+    ``a`` whose weight is folded into ``w``."""
+    if not isinstance(w, PackedWeight) or a.dtype != torch.bfloat16:
+        raise ValueError("gemm_rss: bf16 activations and a packed weight")
+    M, K = a.shape
+    N = w.n + (w.n_extra if side is not None else 0)
+    r = RowSS()
+    if ss_out is not None:
+        r.ss_out, r.ss_out_ld = ss_out.data_ptr(), _ld(ss_out)
+    if ss_in is not None:
+        r.ss_in, r.ss_in_n, r.d, r.eps = ss_in.data_ptr(), ss_in.shape[1], int(norm_dim), float(eps)
+    wsb = (ws if ws is not None else default_workspace(a.device)).get(
+        _lib.load().slx_gemm_workspace_bytes(M, N, K, epilogue))
+    check(_lib.load().slx_gemm_bf16_rss(_ptr(a), _ld(a), _ptr(w.data), _ptr(out), _ld(out), _dt(out),
+                                        _ptr(residual), _ld(residual) if residual is not None else 0,
+                                        M, N, K, epilogue, w.n, _ptr(side) if side is not None else None,
+                                        _ld(side) if side is not None else 0, _ptr(wsb), wsb.numel(),
+                                        ctypes.byref(r),
+                                        None if prefetch is None else ctypes.byref(prefetch),
+                                        _stream()), "slx_gemm_bf16_rss")
     return out
 
 

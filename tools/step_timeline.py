@@ -54,8 +54,8 @@ for i in range(200):
     elif kind == 6:
         exit_ = st[:, 7].max()
         first = st[:, 2].max()   # last CTA past the PDL wait
-    else:
-        exit_ = st[:, 7].max()
+    else:   # GEMMs: thread 0 stamps 7 before the epilogue warps finish (stamp 8)
+        exit_ = max(st[:, 7].max(), st[:, 8].max())
         first = st[:, 3][st[:, 3] > 0].min() if (st[:, 3] > 0).any() else entry
     rows.append((names.get(kind, str(kind)), entry, first, exit_, len(st)))
     stamps.append(st)
