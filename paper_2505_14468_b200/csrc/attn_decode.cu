@@ -199,6 +199,14 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       ++kv_it;
     };
     bool waited = false;
+    if (pl == 0 && (int)blockIdx.x < n_items) {
+      // item 0's cached keys were written >= 2 launches back: request them first, before the
+      // metadata of the batch (slot / rank / B pointers: dependent loads) is resolved
+      const int t0 = blockIdx.x / a.H, h0 = blockIdx.x % a.H;
+      const int pos0 = a.tok_pos[t0], seq0 = a.tok_seq[t0];
+      n_pre = min((pos0 + KB - 1) / KB, AD_STAGES);
+      for (int b = 0; b < n_pre; ++b) issue_kv(seq0, h0, b, pos0);
+    }
     for (int w0 = blockIdx.x; w0 < n_items; w0 += 32 * gridDim.x) {
       // ---- metadata of items w0 + i * gridDim.x, lane i (inputs / adapter pool: >= 2 launches old)
       {
@@ -238,9 +246,6 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       if (pl == 0) {
         const int nloc = min(32, (n_items - w0 + (int)gridDim.x - 1) / (int)gridDim.x);
         if (!waited) {
-          // item 0's cached keys were written >= 2 launches back: start before the PDL wait
-          n_pre = min((meta[0].pos + KB - 1) / KB, AD_STAGES);
-          for (int b = 0; b < n_pre; ++b) issue_kv(meta[0].seq, meta[0].h, b, meta[0].pos);
           if (a.pf_early) l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);
           pdl_wait();
           pdl_trigger();
