@@ -370,6 +370,56 @@ __global__ void rope_kv_kernel(T* __restrict__ qkv, int ld, int H, int Hkv, int 
   }
 }
 
+// Vectorised variant (head_dim % 16 == 0, 16-byte aligned rows): each thread rotates 8 pairs
+// with 16-byte loads / stores, same arithmetic and rounding as rope_kv_kernel.
+template <typename T>
+__global__ void __launch_bounds__(128) rope_kv_vec_kernel(T* __restrict__ qkv, int ld, int H, int Hkv, int D,
+                                   const int32_t* __restrict__ tok_pos,
+                                   const int32_t* __restrict__ tok_seq,
+                                   const float* __restrict__ cos_tab,
+                                   const float* __restrict__ sin_tab, T* __restrict__ kc,
+                                   T* __restrict__ vc, int max_ctx) {
+  pdl_wait();
+  pdl_trigger();
+  const int t = blockIdx.x;
+  const int pos = tok_pos[t];
+  const int seq = tok_seq[t];
+  const int half = D >> 1, hv = half >> 3;
+  T* row = qkv + (size_t)t * ld;
+  const float* cr = cos_tab + (size_t)pos * half;
+  const float* sr = sin_tab + (size_t)pos * half;
+  const int n_rot = (H + Hkv) * hv;
+  for (int idx = threadIdx.x; idx < n_rot; idx += blockDim.x) {
+    const int h = idx / hv, i = (idx - h * hv) * 8;
+    T* base = row + h * D;
+    float x1[8], x2[8], c[8], sn[8], r1[8], r2[8];
+    Vec8<T>::load(base + i, x1);
+    Vec8<T>::load(base + i + half, x2);
+    Vec8<float>::load(cr + i, c);
+    Vec8<float>::load(sr + i, sn);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      r1[j] = x1[j] * c[j] - x2[j] * sn[j];
+      r2[j] = x2[j] * c[j] + x1[j] * sn[j];
+    }
+    Vec8<T>::store(base + i, r1);
+    Vec8<T>::store(base + i + half, r2);
+    if (h >= H) {
+      T* dst = kc + (((size_t)seq * Hkv + (h - H)) * max_ctx + pos) * D;
+      Vec8<T>::store(dst + i, r1);
+      Vec8<T>::store(dst + i + half, r2);
+    }
+  }
+  const T* vsrc = row + (H + Hkv) * D;
+  const int dv = D >> 3;
+  for (int idx = threadIdx.x; idx < Hkv * dv; idx += blockDim.x) {
+    const int hk = idx / dv, i = (idx - hk * dv) * 8;
+    float v[8];
+    Vec8<T>::load(vsrc + hk * D + i, v);
+    Vec8<T>::store(vc + (((size_t)seq * Hkv + hk) * max_ctx + pos) * D + i, v);
+  }
+}
+
 // ------------------------------------------------------------------ attention over the KV pool
 // One CTA of 4 warps per (token, head); warp w streams key chunks c = w, w+4, ... of 32 keys.
 // Lane j of a chunk loads key row j0+j with 16-byte loads (the whole chunk's K in flight at
@@ -914,6 +964,15 @@ extern "C" int slx_rope_kv_write(int dtype, void* qkv, int ld_qkv, int n_tok, in
                 v_cache);
   if (n_tok == 0) return SLX_OK;
   int st = SLX_OK;
+  // bf16 only: the fp32 parity mode keeps the scalar kernel's exact FMA contraction
+  const bool vec = dtype == SLX_DT_BF16 && head_dim % 16 == 0 && ld_qkv % 8 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(qkv) | reinterpret_cast<uintptr_t>(k_cache) |
+                     reinterpret_cast<uintptr_t>(v_cache) | reinterpret_cast<uintptr_t>(cos_tab) |
+                     reinterpret_cast<uintptr_t>(sin_tab)) & 31) == 0;
+  if (vec)
+    return launch_ex(rope_kv_vec_kernel<bf16>, dim3(n_tok), dim3(128), 0, (cudaStream_t)stream, 1u,
+                     (bf16*)qkv, ld_qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos_tab,
+                     sin_tab, (bf16*)k_cache, (bf16*)v_cache, max_ctx);
   DISPATCH_DT(dtype, st = launch_ex(rope_kv_kernel<T>, dim3(n_tok), dim3(256), 0, (cudaStream_t)stream, 1u, (T*)qkv, ld_qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos_tab,
                          sin_tab, (T*)k_cache, (T*)v_cache, max_ctx));
   return st;

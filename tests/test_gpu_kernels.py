@@ -300,6 +300,29 @@ def test_rope_kv_attention_match_oracle(dtype, H, Hkv, D):
     np.testing.assert_allclose(kc[1, :, :13].float().cpu().numpy().transpose(1, 0, 2), k[1:14], rtol=tol, atol=tol)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16])
+@pytest.mark.parametrize("H,Hkv,D", [(4, 4, 64), (8, 2, 128)])
+def test_rope_kv_vectorised_equals_scalar(dtype, H, Hkv, D):
+    """The 16-byte vectorised bf16 RoPE + KV write (aligned rows) == the scalar kernel
+    (unaligned row stride), bit for bit: rotated q/k in place and the appended k/v."""
+    g = torch.Generator(device=DEV).manual_seed(D)
+    T, W = 37, (H + 2 * Hkv) * D
+    base = torch.randn(T, W, generator=g, device=DEV).to(dtype)
+    pos = torch.arange(T, dtype=torch.int32, device=DEV) // 5 + 3   # unique (seq, pos) rows
+    seq = torch.arange(T, dtype=torch.int32, device=DEV) % 5
+    cos, sin = (torch.from_numpy(t).to(DEV) for t in orc.rope_table(64, D, 10000.0))
+    res = []
+    for ld in (W, W + 1):   # ld % 8 != 0 forces the scalar kernel
+        buf = torch.zeros(T, ld, dtype=dtype, device=DEV)
+        buf[:, :W] = base
+        kc = torch.zeros(5, Hkv, 64, D, dtype=dtype, device=DEV)
+        vc = torch.zeros_like(kc)
+        ops.rope_kv_write(buf[:, :W], H, Hkv, D, pos, seq, cos, sin, kc, vc)
+        res.append((buf[:, :W].clone(), kc, vc))
+    for a, b in zip(res[0], res[1]):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("H,Hkv,D", [(4, 4, 64), (32, 32, 128), (8, 2, 128)])
 @pytest.mark.parametrize("ctx", [0, 5, 128, 300])
