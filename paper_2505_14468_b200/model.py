@@ -650,8 +650,10 @@ class MultiLoraModel:
                 v_o_f = torch.zeros((T, 64), dtype=dt, device=dev)
                 bq = [cfg.q_dim, cfg.kv_dim, cfg.kv_dim]
         # decode: o / down as split-K pieces reduced by the next RMSNorm (no GEMM reduction tail)
+        # (a model without LoRA targets takes the same path, so the bare-backbone step is
+        # comparable kernel for kernel)
         sk_mode = (decode and dt == torch.bfloat16 and self.splitk_consumer and self.fuse_expand
-                   and self.use_stacked_decode and T <= 64
+                   and (self.use_stacked_decode or not self.targets) and T <= 64
                    and d % 256 == 0 and d <= 5120 and self.pool.max_rank <= 16)
         if sk_mode:
             S = min(self.splitk_splits, (d + 63) // 64)                   # o: K = q_dim
@@ -732,9 +734,9 @@ class MultiLoraModel:
                     ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
                                   self.k_cache[l], self.v_cache[l])
             d_o = None
-            if sk_mode and "wo" in self.stack:
+            if sk_mode and ("wo" in self.stack or "o" not in self.targets):
                 sk_o = ops.gemm_splitk(attn, w[p + "wo"], S, part_o, prefetch=pf_o)
-                d_o = self._delta(l, "wo", None, slot, {"o": (0, d, d)})
+                d_o = self._delta(l, "wo", None, slot, {"o": (0, d, d)}) if "wo" in self.stack else None
                 if fnorm and fused_silu:
                     ngu = ops.norm_in(x, w[p + "post_norm"], cfg.rms_eps, self.norm_ss,
                                       self.norm_bar[2:4], sk=sk_o, delta=d_o)

@@ -239,3 +239,26 @@ def test_bf16_prefill_tc_path_matches_oracle():
     orc = OracleModel(cfg, w, ads, [lo.scale for lo in loras], loras[0].targets)
     ref = orc.prefill(prompts, ids)
     np.testing.assert_allclose(out[True], ref, rtol=BF16_RTOL, atol=BF16_ATOL)
+
+
+def test_bf16_bare_backbone_decode_takes_the_splitk_path():
+    """A model without LoRA targets decodes through the same split-K path as the LoRA model
+    (bench's bare-backbone reference for the LoRA marginal) and agrees with the LoRA model on
+    tokens that carry no adapter."""
+    from paper_2505_14468_b200.config import BackboneConfig
+    cfg = BackboneConfig("w2048", hidden=2048, layers=2, heads=16, kv_heads=16, head_dim=128,
+                         ffn=2048, vocab=1000)
+    w = init_backbone(cfg, 5)
+    lo = LoraConfig(16, 32.0)
+    prompts, toks = [[5, 9, 200, 31], [7, 7, 7], [44, 45]], [11, 12, 13]
+    out = {}
+    for targets in ((), lo.targets):
+        m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=4, max_ctx=64, n_slots=2,
+                           max_rank=16, max_tokens=128, lora_targets=targets)
+        m.load_backbone(w)
+        if targets:
+            m.pool.load(0, init_adapter(cfg, lo, 5, 0), lo)
+        ids = [-1, -1, -1]
+        seqs, _ = m.prefill(prompts, ids)
+        out[bool(targets)] = m.decode(seqs, toks, ids).cpu().numpy()
+    np.testing.assert_allclose(out[False], out[True], rtol=2e-2, atol=2e-2)
