@@ -96,7 +96,17 @@ typedef struct slx_splitk_in slx_splitk_in;     /* defined with the K4 entry poi
 typedef struct slx_l2_prefetch {
   const void* ptr[2];
   size_t bytes[2];
+  /* and/or: a window of every CTA's unit range of the NEXT decode GEMM (stream-K partition of
+   * the tiled weight gemm_w with gemm_n rows, gemm_k columns, for gemm_m tokens): units
+   * [unit0, unit0 + units) after each CTA's first unit (a unit = 256 weight rows x 64 k = two
+   * 16 KB boxes), so every CTA of that GEMM finds its first bytes in L2.  gemm_w NULL: off. */
+  const void* gemm_w;
+  int gemm_m, gemm_n, gemm_k;
+  int unit0, units;
 } slx_l2_prefetch;
+/* CTAs of the stream-K decode GEMM slx_gemm_bf16 launches for (M, N, K) on tiled weights
+ * (0: another kernel) — sizes slx_l2_prefetch unit windows. */
+SLX_API int slx_gemm_sk_ctas(int M, int N, int K);
 /* slx_gemm_bf16 + an L2 prefetch hint for the next kernel (pf may be NULL). */
 SLX_API int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
@@ -287,10 +297,11 @@ SLX_API int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx, co
 /* The residual epilogue of a split-K projection fused in front: x[t, :] = round(x + sum of the
  * pieces) (what slx_gemm_bf16's residual epilogue would have stored), then the LoRA add (its v
  * taken from the pieces' columns >= n_main when lora->v is NULL) and the RMSNorm, as
- * slx_rmsnorm_lora.  d % 2048 == 0 (8-CTA cluster per token). */
+ * slx_rmsnorm_lora.  d % 2048 == 0 (8-CTA cluster per token).  `pf` (may be NULL): L2 prefetch
+ * of the next GEMM's weights, issued at kernel entry (before the PDL wait). */
 SLX_API int slx_rmsnorm_fused(int dtype, void* out, int ldo, void* x, int ldx, const void* w,
                 int n_tok, int d, float eps, const slx_splitk_in* sk, const slx_lora_delta* lora,
-                void* stream);
+                const slx_l2_prefetch* pf, void* stream);
 /* qkv [n_tok, (H + 2 Hkv) D]: rotate q,k in place (rotate-half, cos/sin tables fp32
  * [max_pos, D/2]) and write k, v at (tok_seq[t], tok_pos[t]) of the caches. */
 SLX_API int slx_rope_kv_write(int dtype, void* qkv, int ld_qkv, int n_tok, int heads, int kv_heads,

@@ -66,7 +66,8 @@ class RowSS(ctypes.Structure):
 
 class L2Prefetch(ctypes.Structure):
     """slx_l2_prefetch: the next kernel's first bytes (two regions)."""
-    _fields_ = [("ptr", _p * 2), ("bytes", _sz * 2)]
+    _fields_ = [("ptr", _p * 2), ("bytes", _sz * 2), ("gemm_w", _p), ("gemm_m", _i),
+                ("gemm_n", _i), ("gemm_k", _i), ("unit0", _i), ("units", _i)]
 
 
 # name -> (restype, argtypes): every symbol declared in include/slora_b200.h
@@ -84,6 +85,7 @@ SIGNATURES = {
                                 ctypes.POINTER(NormIn), ctypes.POINTER(L2Prefetch), _p]),
     "slx_gemm_bf16_rss": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _p, _i, _p, _sz,
                                ctypes.POINTER(RowSS), ctypes.POINTER(L2Prefetch), _p]),
+    "slx_gemm_sk_ctas": (_i, [_i, _i, _i]),
     "slx_gemm_bf16_pf": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p,
                               _sz, ctypes.POINTER(L2Prefetch), _p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),
@@ -110,7 +112,7 @@ SIGNATURES = {
     "slx_rmsnorm": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _f, _p]),
     "slx_rmsnorm_lora": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _f, ctypes.POINTER(LoraDelta), _p]),
     "slx_rmsnorm_fused": (_i, [_i, _p, _i, _p, _i, _p, _i, _i, _f, ctypes.POINTER(SplitKIn),
-                               ctypes.POINTER(LoraDelta), _p]),
+                               ctypes.POINTER(LoraDelta), ctypes.POINTER(L2Prefetch), _p]),
     "slx_rope_kv_write": (_i, [_i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p, _i, _p]),
     "slx_attention": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p]),
     "slx_rope_attention_decode": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p,

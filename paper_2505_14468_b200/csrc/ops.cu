@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict
                                                                    T* __restrict__ x, int ldx,
                                                                    const bf16* __restrict__ w,
                                                                    int d, float eps, DeltaArgs lora,
-                                                                   SplitArgs sk,
+                                                                   SplitArgs sk, PfArgs pf,
                                                                    unsigned long long* trace) {
   __shared__ float vs[DELTA_VS];
   __shared__ float red[8];
@@ -165,6 +165,9 @@ __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict
     }
   };
   stamp(0);
+  // the next GEMM's weights beyond what the previous kernel prefetched (constant: before the
+  // wait), so HBM keeps streaming while this latency-bound kernel runs
+  if (threadIdx.x == 0) l2_prefetch_part(pf, blockIdx.x, gridDim.x);
   const int t = blockIdx.x / RNL_CL, cr = blockIdx.x % RNL_CL;
   const int i0 = cr * (d / RNL_CL) + threadIdx.x * 8;
   T* xr = x + (size_t)t * ldx;
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(640) rmsnorm_fused_tok_kernel(T* __restrict__ 
                                                                  T* __restrict__ x, int ldx,
                                                                  const bf16* __restrict__ w, int d,
                                                                  float eps, DeltaArgs lora,
-                                                                 SplitArgs sk,
+                                                                 SplitArgs sk, PfArgs pf,
                                                                  unsigned long long* trace) {
   __shared__ float vs[DELTA_VS];
   __shared__ float red[33];
@@ -269,6 +272,7 @@ __global__ void __launch_bounds__(640) rmsnorm_fused_tok_kernel(T* __restrict__ 
     }
   };
   stamp(0);
+  if (threadIdx.x == 0) l2_prefetch_part(pf, blockIdx.x, gridDim.x);   // next GEMM, pre-wait
   const int t = blockIdx.x;
   const int i0 = threadIdx.x * 8;
   T* xr = x + (size_t)t * ldx;
@@ -912,7 +916,7 @@ extern "C" int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx,
   const char* e = getenv("SLX_RMSNORM_CLUSTER");
   if (d % (RNL_CL * 8 * 32) == 0 && d / (RNL_CL * 8) <= 128 && !(e && e[0] == '0')) {
     const int thr = d / (RNL_CL * 8);
-    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, SplitArgs{}, next_trace_window(6)));
+    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, SplitArgs{}, PfArgs{}, next_trace_window(6)));
     return st;
   }
   int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
@@ -922,7 +926,8 @@ extern "C" int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx,
 
 extern "C" int slx_rmsnorm_fused(int dtype, void* out, int ldo, void* x, int ldx, const void* w,
                                  int n_tok, int d, float eps, const slx_splitk_in* sk,
-                                 const slx_lora_delta* lora, void* stream) {
+                                 const slx_lora_delta* lora, const slx_l2_prefetch* pf,
+                                 void* stream) {
   SLX_CHECK_ARG(n_tok >= 0 && d > 0 && ldo % 8 == 0 && ldx % 8 == 0 && ldo >= d && ldx >= d &&
                 out && x && w && delta_valid(lora, sk != nullptr));
   SLX_CHECK_ALIGN(out, 16);
@@ -938,18 +943,19 @@ extern "C" int slx_rmsnorm_fused(int dtype, void* out, int ldo, void* x, int ldx
   if (n_tok == 0) return SLX_OK;
   const DeltaArgs la = delta_args(lora);
   const SplitArgs sa = split_args(sk);
+  const PfArgs pa = pf_args(pf);
   int st = SLX_OK;
   const char* e = getenv("SLX_RMSNORM_CLUSTER");
   // default: the 8-CTA cluster kernel (measured faster in the decode graph); SLX_RMSNORM_CLUSTER=0
   // or a d the cluster split cannot take: one CTA per token
   const bool cl_ok = d % (RNL_CL * 8 * 32) == 0 && d / (RNL_CL * 8) <= 128;
   if ((!cl_ok || (e && e[0] == '0')) && d % 256 == 0 && d / 8 <= 640 && (!sk || sk->splits <= 8)) {
-    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_fused_tok_kernel<T>, dim3(n_tok), dim3(d / 8), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, sa, next_trace_window(6)));
+    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_fused_tok_kernel<T>, dim3(n_tok), dim3(d / 8), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, sa, pa, next_trace_window(6)));
     return st;
   }
   if (d % (RNL_CL * 8 * 32) != 0 || d / (RNL_CL * 8) > 128) return SLX_ERR_UNSUPPORTED;
   const int thr = d / (RNL_CL * 8);
-  DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, sa, next_trace_window(6)));
+  DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, sa, pa, next_trace_window(6)));
   return st;
 }
 

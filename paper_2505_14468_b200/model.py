@@ -206,6 +206,12 @@ class MultiLoraModel:
         self.norm_bar = torch.zeros(8, dtype=torch.int32, device=self.device)   # 3 call sites
         # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off)
         self.l2_prefetch_mb = float(os.environ.get("SLX_L2_PF_MB", "16"))
+        # ... aimed at the first units of EVERY CTA of the next stream-K GEMM (gate/up, q/k/v)
+        # instead of the weight's first bytes.  The RMSNorm kernel in front of that GEMM can
+        # continue it (SLX_NORM_PF_MB, issued at its entry); measured slower (32 MB: +0.2 ms per
+        # step — the prefetch stream delays the norm's own L2 round trips), so 0 by default.
+        self.pf_gemm = os.environ.get("SLX_PF_GEMM", "1") != "0"
+        self.norm_pf_mb = float(os.environ.get("SLX_NORM_PF_MB", "0"))
         self._pf_cache: dict = {}
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
         # decode: the pre-attention RMSNorm of layers >= 1 folded across two GEMMs — the down
@@ -577,6 +583,24 @@ class MultiLoraModel:
             self._pf_cache[key] = ops.l2_prefetch(*[(getattr(t, "data", t), n) for t in tensors])
         return self._pf_cache[key]
 
+    def _pf_gemm(self, key, w, m: int, n_rows: int, mb: float, after_mb: float = 0.0):
+        """Cached slx_l2_prefetch of a window of every CTA's unit range of the decode GEMM over
+        packed weight ``w`` (``n_rows`` computed rows, ``m`` tokens): ``mb`` MB in total,
+        after the first ``after_mb`` MB (the window an earlier kernel prefetched)."""
+        if mb <= 0:
+            return None
+        key = (key, m)
+        if key not in self._pf_cache:
+            G = ops.gemm_sk_ctas(m, n_rows, w.k)
+            if G <= 0:
+                self._pf_cache[key] = None
+            else:
+                per = G * 32768.0
+                u0 = int(round(after_mb * (1 << 20) / per))
+                units = int(round(mb * (1 << 20) / per))
+                self._pf_cache[key] = ops.l2_prefetch_gemm(w, m, n_rows, u0, units)
+        return self._pf_cache[key]
+
     def _pf_all(self, key, t):
         """slx_l2_prefetch of a whole (packed) weight (spread over a long kernel)."""
         if self.l2_prefetch_mb <= 0:
@@ -679,7 +703,13 @@ class MultiLoraModel:
             if fnorm or folded:
                 pass   # built by the qkv GEMM's prologue / folded into it
             elif pending is not None:
-                ops.rmsnorm_fused(h, x, w[p + "input_norm"], cfg.rms_eps, pending)
+                pf_n = None
+                if self.pf_gemm and decode and dt == torch.bfloat16:
+                    wq = w[p + "w_qkv"]
+                    nq = wq.n + (wq.n_extra if stacked and "w_qkv" in self.stack else 0)
+                    pf_n = self._pf_gemm(p + "w_qkv/norm", wq, T, nq, self.norm_pf_mb,
+                                         self.l2_prefetch_mb)
+                ops.rmsnorm_fused(h, x, w[p + "input_norm"], cfg.rms_eps, pending, prefetch=pf_n)
                 pending = None
             else:
                 ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
@@ -692,6 +722,16 @@ class MultiLoraModel:
             pf_o = self._pf(p + "w_gu", w[p + "w_gu"]) if pfd else None
             pf_gu = self._pf(p + "w_down", w[p + "w_down"]) if pfd else None
             pf_dn = self._pf(nxt, w[nxt]) if pfd else None
+            pf_gu_n = None
+            if pfd and self.pf_gemm and isinstance(w[p + "w_gu"], ops.PackedWeight):
+                wg = w[p + "w_gu"]
+                pf_o = self._pf_gemm(p + "w_gu/o", wg, T, wg.n, self.l2_prefetch_mb) or pf_o
+                pf_gu_n = self._pf_gemm(p + "w_gu/norm", wg, T, wg.n, self.norm_pf_mb,
+                                        self.l2_prefetch_mb)
+                if l + 1 < cfg.layers and not rss_mode:
+                    wq = w[nxt]
+                    nq = wq.n + (wq.n_extra if stacked and "w_qkv" in self.stack else 0)
+                    pf_dn = self._pf_gemm(nxt + "/down", wq, T, nq, self.l2_prefetch_mb) or pf_dn
             if fold is not None:
                 ga, bp, rk = self._fold_lora(l, fold[0], "w_qkv")
                 if fold[3] is not None:
@@ -741,7 +781,8 @@ class MultiLoraModel:
                     ngu = ops.norm_in(x, w[p + "post_norm"], cfg.rms_eps, self.norm_ss,
                                       self.norm_bar[2:4], sk=sk_o, delta=d_o)
                 else:
-                    ops.rmsnorm_fused(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o)
+                    ops.rmsnorm_fused(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o,
+                                      prefetch=pf_gu_n)
                     ngu = None
                 d_o = "done"
             elif fold is not None:

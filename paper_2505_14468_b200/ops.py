@@ -184,6 +184,23 @@ def l2_prefetch(*regions) -> L2Prefetch | None:
     return pf
 
 
+def gemm_sk_ctas(m: int, n: int, k: int) -> int:
+    return int(_lib.load().slx_gemm_sk_ctas(m, n, k))
+
+
+def l2_prefetch_gemm(w: "PackedWeight", m: int, n_rows: int, unit0: int, units: int,
+                     base: L2Prefetch | None = None) -> L2Prefetch | None:
+    """slx_l2_prefetch of units [unit0, unit0 + units) of every CTA's range of the next decode
+    GEMM over the packed weight ``w`` (``n_rows`` = rows it computes, main + stacked) for ``m``
+    tokens; added to ``base``'s regions when given."""
+    if units <= 0:
+        return base
+    pf = base if base is not None else L2Prefetch()
+    pf.gemm_w, pf.gemm_m, pf.gemm_n, pf.gemm_k = w.data.data_ptr(), int(m), int(n_rows), int(w.k)
+    pf.unit0, pf.units = int(unit0), int(units)
+    return pf
+
+
 @_op("gemm", 1)
 def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
          epilogue: int = EPI_NONE, residual: torch.Tensor | None = None,
@@ -477,13 +494,16 @@ def gemm_splitk(a: torch.Tensor, w, splits: int, part: torch.Tensor, prefetch=No
 
 
 @_op("rmsnorm", 1)
-def rmsnorm_fused(out, x, w, eps: float, sk=None, delta=None):
+def rmsnorm_fused(out, x, w, eps: float, sk=None, delta=None, prefetch=None):
     """x = round(x + split-K pieces) (the projection's residual epilogue), x += LoRA delta
-    (v from the pieces when the delta has no v), out = rmsnorm(x)."""
+    (v from the pieces when the delta has no v), out = rmsnorm(x); ``prefetch`` (l2_prefetch):
+    the next GEMM's weights, requested at kernel entry."""
     check(_lib.load().slx_rmsnorm_fused(_dt(out), _ptr(out), _ld(out), _ptr(x), _ld(x), _ptr(w),
                                         x.shape[0], w.numel(), float(eps),
                                         None if sk is None else ctypes.byref(sk),
-                                        None if delta is None else ctypes.byref(delta), _stream()),
+                                        None if delta is None else ctypes.byref(delta),
+                                        None if prefetch is None else ctypes.byref(prefetch),
+                                        _stream()),
           "slx_rmsnorm_fused")
     return out
 
