@@ -340,9 +340,10 @@ SLX_API int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const vo
                   int pool_seqs, const slx_lora_delta* lora, const slx_l2_prefetch* pf,
                   void* stream);
 /* Prefill (tensor cores, mma.sync flash attention, head_dim 128, bf16): `tiles` is a device
- * array of n_tiles {int tok0, nq, seq, pos0} (<= 64 queries of one segment each, size
+ * array of n_tiles {int tok0, nq, seq, pos0} (<= slx_flash_prefill_tile_queries() queries of one segment each, size
  * slx_flash_prefill_tile_bytes()); query t of a tile attends cache positions 0..pos0+t of
  * its sequence (k/v already appended by slx_rope_kv_write, q rotated in qkv). */
+SLX_API int slx_flash_prefill_tile_queries(void);   /* max queries per tile (nq) */
 SLX_API size_t slx_flash_prefill_tile_bytes(void);
 SLX_API int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld_qkv, int heads,
                   int kv_heads, int head_dim, const void* tiles, int n_tiles, const void* k_cache,

@@ -122,6 +122,7 @@ SIGNATURES = {
     "slx_rope_attention_decode_pf": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i,
                                           _p, _p, _i, _i, ctypes.POINTER(LoraDelta),
                                           ctypes.POINTER(L2Prefetch), _p]),
+    "slx_flash_prefill_tile_queries": (_i, []),
     "slx_flash_prefill_tile_bytes": (_sz, []),
     "slx_attention_prefill": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _i, _p, _p, _i, _p]),
     "slx_silu_mul_blocked": (_i, [_i, _p, _i, _p, _i, _i, _i, _p]),

@@ -11,12 +11,12 @@
 
 namespace slx {
 
-constexpr int FA_BQ = 64, FA_BK = 64, FA_D = 128, FA_THREADS = 128;
+constexpr int FA_BQ = 64, FA_BK = 64, FA_D = 128, FA_THREADS = 128;   // 4 warps x 16 query rows (128-query tiles of 8 warps measured slower)
 constexpr int FA_LD = FA_D + 8;   // padded smem row (bf16 elements): conflict-free ldmatrix
 
 struct FaTile {
   int tok0;    // first query token (row of qkv / out)
-  int nq;      // queries in this tile (<= 64)
+  int nq;      // queries in this tile (<= FA_BQ)
   int seq;     // KV pool sequence slot
   int pos0;    // cache position of the first query
 };
@@ -56,13 +56,15 @@ flash_prefill_kernel(bf16* __restrict__ out, int ldo, const bf16* __restrict__ q
                      int Hkv, const FaTile* __restrict__ tiles, const bf16* __restrict__ kc,
                      const bf16* __restrict__ vc, int max_ctx, float scale_log2) {
   extern __shared__ __align__(128) uint8_t fsm_raw[];
-  bf16* Qs = reinterpret_cast<bf16*>(fsm_raw);             // [64][LD]
+  bf16* Qs = reinterpret_cast<bf16*>(fsm_raw);             // [FA_BQ][LD]
   bf16* Ks = Qs + FA_BQ * FA_LD;                            // [2][64][LD]
   bf16* Vs = Ks + 2 * FA_BK * FA_LD;                        // [2][64][LD]
   pdl_wait();
   pdl_trigger();
-  const FaTile tile = tiles[blockIdx.x];
-  const int h = blockIdx.y, hk = h / (H / Hkv);
+  // grid (heads, tiles): all heads of a tile launch together, tiles in table order (the host
+  // sorts them longest first, so the last wave holds the short tiles)
+  const FaTile tile = tiles[blockIdx.y];
+  const int h = blockIdx.x, hk = h / (H / Hkv);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bf16* kbase = kc + ((size_t)tile.seq * Hkv + hk) * max_ctx * FA_D;
   const bf16* vbase = vc + ((size_t)tile.seq * Hkv + hk) * max_ctx * FA_D;
@@ -219,6 +221,7 @@ flash_prefill_kernel(bf16* __restrict__ out, int ldo, const bf16* __restrict__ q
 using namespace slx;
 
 extern "C" size_t slx_flash_prefill_tile_bytes(void) { return sizeof(FaTile); }
+extern "C" int slx_flash_prefill_tile_queries(void) { return FA_BQ; }
 
 extern "C" int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld_qkv, int heads,
                                      int kv_heads, int head_dim, const void* tiles, int n_tiles,
@@ -242,7 +245,7 @@ extern "C" int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld
     configured = true;
   }
   const float scale = 1.4426950408889634f / sqrtf((float)head_dim);
-  return launch_ex(flash_prefill_kernel, dim3((unsigned)n_tiles, (unsigned)heads),
+  return launch_ex(flash_prefill_kernel, dim3((unsigned)heads, (unsigned)n_tiles),
                    dim3(FA_THREADS), smem, (cudaStream_t)stream, 1u, (bf16*)out, ldo,
                    (const bf16*)qkv, ld_qkv, heads, kv_heads, (const FaTile*)tiles,
                    (const bf16*)k_cache, (const bf16*)v_cache, max_ctx, scale);

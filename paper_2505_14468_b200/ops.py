@@ -552,12 +552,16 @@ def rope_attention_decode(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq,
     return out
 
 
-def prefill_tiles(segments, device, bq: int = 64) -> torch.Tensor:
-    """[(tok0, n, seq, pos0)] segments -> int32 [n_tiles, 4] tile table of <= bq queries."""
+def prefill_tiles(segments, device, bq: int | None = None) -> torch.Tensor:
+    """[(tok0, n, seq, pos0)] segments -> int32 [n_tiles, 4] tile table of <= bq queries (the
+    flash kernel's tile height by default), longest causal work (keys = pos0 + n) first."""
+    if bq is None:
+        bq = int(_lib.load().slx_flash_prefill_tile_queries())
     rows = []
     for tok0, n, seq, pos0 in segments:
         for q in range(0, n, bq):
             rows.append((tok0 + q, min(bq, n - q), seq, pos0 + q))
+    rows.sort(key=lambda r: -(r[3] + r[1]))
     return torch.tensor(rows, dtype=torch.int32).reshape(-1, 4).to(device)
 
 
