@@ -52,6 +52,37 @@ int main() {
   cudaFuncSetAttribute(kA<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaStream_t s;
   cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+  cudaFuncSetAttribute(kB, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int acl : {1, 2}) {
+    unsigned long long ha[4096], hb[4096];
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaLaunchConfig_t c = {};
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      at[1].id = cudaLaunchAttributeClusterDimension;
+      at[1].val.clusterDim.x = acl; at[1].val.clusterDim.y = 1; at[1].val.clusterDim.z = 1;
+      c.gridDim = dim3(108); c.blockDim = dim3(192); c.dynamicSmemBytes = 200 * 1024; c.stream = s;
+      c.attrs = at; c.numAttrs = acl > 1 ? 2 : 1;
+      cudaLaunchKernelEx(&c, kA<true>, 10000, sa);
+      cudaLaunchConfig_t d = {};
+      d.gridDim = dim3(148); d.blockDim = dim3(288); d.dynamicSmemBytes = 200 * 1024; d.stream = s;
+      d.attrs = at; d.numAttrs = 1;
+      cudaLaunchKernelEx(&d, kB, sb);
+      cudaStreamSynchronize(s);
+    }
+    cudaError_t e = cudaGetLastError();
+    cudaMemcpy(ha, sa, 108 * 16, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hb, sb, 148 * 16, cudaMemcpyDeviceToHost);
+    unsigned long long a0 = ~0ull, a1 = 0, b0 = ~0ull, b1 = 0;
+    int early = 0;
+    for (int i = 0; i < 108; ++i) { a0 = ha[2 * i] < a0 ? ha[2 * i] : a0; a1 = ha[2 * i + 1] > a1 ? ha[2 * i + 1] : a1; }
+    for (int i = 0; i < 148; ++i) { b0 = hb[2 * i] < b0 ? hb[2 * i] : b0; b1 = hb[2 * i + 1] > b1 ? hb[2 * i + 1] : b1; }
+    for (int i = 0; i < 148; ++i) early += hb[2 * i] < a1;
+    printf("A cluster %d (108 CTAs, tcgen05, 200 KB) -> B (148 x 288, 200 KB): A end %.2f | B first entry %.2f, CTAs entered before A end %d, last release %.2f us %s\n",
+           acl, (a1 - a0) / 1e3, ((long long)(b0 - a0)) / 1e3, early, ((long long)(b1 - a0)) / 1e3,
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+  }
   for (int co : {-1, 100})
   for (int tm = 0; tm < 2; ++tm)
     for (int cl : {1, 8})
