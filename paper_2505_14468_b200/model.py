@@ -197,7 +197,11 @@ class MultiLoraModel:
         self.fuse_expand = True
         # decode: o / down projections as split-K pieces reduced by the following RMSNorm
         self.splitk_consumer = os.environ.get("SLX_SPLITK_CONSUMER", "1") != "0"
-        self.splitk_splits = int(os.environ.get("SLX_SPLITK_SPLITS", "8"))
+        # pieces per tile: o 6 (96 CTAs), down 8 (128 CTAs) — measured best on the 7B step
+        # (o at 8: +50 us/step); SLX_SPLITK_SPLITS overrides both
+        sk_all = os.environ.get("SLX_SPLITK_SPLITS")
+        self.splitk_splits_o = int(os.environ.get("SLX_SPLITK_SPLITS_O", sk_all or "6"))
+        self.splitk_splits_dn = int(os.environ.get("SLX_SPLITK_SPLITS_DN", sk_all or "8"))
         # decode: the RMSNorms fused into the GEMM that consumes them (grid-wide prologue).
         # Off by default: measured slower (the prologue's dependent L2 round trips queue behind
         # the weight stream the producer has already started; SLX_FUSE_NORM=1 to enable).
@@ -680,8 +684,8 @@ class MultiLoraModel:
                    and (self.use_stacked_decode or not self.targets) and T <= 64
                    and d % 256 == 0 and d <= 5120 and self.pool.max_rank <= 16)
         if sk_mode:
-            S = min(self.splitk_splits, (d + 63) // 64)                   # o: K = q_dim
-            S_dn = min(self.splitk_splits, self.ffn_pad // 64)           # down: K = ffn
+            S = min(self.splitk_splits_o, (d + 63) // 64)               # o: K = q_dim
+            S_dn = min(self.splitk_splits_dn, self.ffn_pad // 64)       # down: K = ffn
             part_o = torch.empty(ops.splitk_bytes(T, d + self._extra_rows("wo"), S) // 4,
                                  dtype=torch.float32, device=dev)
             part_dn = torch.empty(ops.splitk_bytes(T, d, S_dn) // 4, dtype=torch.float32,
