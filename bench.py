@@ -31,10 +31,13 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "multi-LoRA decode tokens/s (Llama-2-7B shape, 32 x r16 adapters, batch 64, ctx 128)"
+# SLX_BENCH_CTX: context of the resident sequences (SURVEY 8d also quotes config 2 at 512);
+# the driver's line is the default 128
+_CTX_ENV = int(os.environ.get("SLX_BENCH_CTX", "128"))
+METRIC = f"multi-LoRA decode tokens/s (Llama-2-7B shape, 32 x r16 adapters, batch 64, ctx {_CTX_ENV})"
 UNIT = "tokens/s"
-BATCH, N_ADAPTERS, RANK, ALPHA, CTX = 64, 32, 16, 32.0, 128
-WORKLOAD = "config2: llama2-7b-shape bf16 decode, 32 x r16 LoRA (q,k,v,o), batch 64, ctx 128"
+BATCH, N_ADAPTERS, RANK, ALPHA, CTX = 64, 32, 16, 32.0, _CTX_ENV
+WORKLOAD = f"config2: llama2-7b-shape bf16 decode, 32 x r16 LoRA (q,k,v,o), batch 64, ctx {_CTX_ENV}"
 
 
 def dist_env():

@@ -128,7 +128,7 @@ template <int D, int KB>
 constexpr size_t ad_smem() {
   return 1024 + (size_t)AD_STAGES * ad_stage_bytes<D, KB>() + AD_HSLOTS * sizeof(AdHeader<D>) +
          AD_GROUPS * sizeof(AdScratch<D>) + 32 * sizeof(ItemMeta) +
-         (size_t)(2 * AD_STAGES + 2 * AD_HSLOTS) * 8;
+         (size_t)(2 * AD_STAGES + 2 * AD_HSLOTS) * 8 + 16;
 }
 
 __device__ __forceinline__ void group_sync(int g) { tc::named_bar_sync(1 + g, AD_GT); }
@@ -150,6 +150,12 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
   uint64_t* kv_empty = kv_full + AD_STAGES;
   uint64_t* h_full = kv_empty + AD_STAGES;
   uint64_t* h_empty = h_full + AD_HSLOTS;
+  // KV blocks issued so far (producer lane 0).  The two consumer groups work on different
+  // items, so one can reach ring index i while the slot's previous use (i - STAGES, the other
+  // group's block) is still pending; an mbarrier parity wait cannot tell phase i from phase
+  // i - 2 STAGES.  A consumer therefore waits until block i has been issued (which implies
+  // phase i - STAGES completed) before its parity wait.
+  volatile int* kv_issued = reinterpret_cast<volatile int*>(h_empty + AD_HSLOTS);
 
   const int tid = threadIdx.x;
   const int n_items = a.n_tok * a.H;
@@ -166,6 +172,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       tc::mbar_init(&h_full[i], 1);
       tc::mbar_init(&h_empty[i], 1);
     }
+    *kv_issued = 0;
     tc::fence_barrier_init();
   }
   __syncthreads();
@@ -197,6 +204,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
         tc::bulk_g2s(st + KB * D * 2, a.vc + off, bytes, &kv_full[s], pol_kv);
       }
       ++kv_it;
+      *kv_issued = kv_it;   // published by the st.volatile; ordered after the TMA issue above
     };
     bool waited = false;
     if (pl == 0 && (int)blockIdx.x < n_items) {
@@ -328,6 +336,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       if (gt == 0) tc::mbar_arrive(&h_empty[hs]);
       for (int b = 0; b < nb; ++b) {
         const int it = kv0 + b;
+        while (*kv_issued <= it) {}
         tc::mbar_wait(&kv_full[it % AD_STAGES], (it / AD_STAGES) & 1);
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&kv_empty[it % AD_STAGES]);
@@ -432,6 +441,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       for (int b = 0; b < nb; ++b) {
         const int it = kv0 + b, s = it % AD_STAGES;
         const int nk = min(KB, pos - b * KB);
+        while (*kv_issued <= it) {}
         tc::mbar_wait(&kv_full[s], (it / AD_STAGES) & 1);
         const uint32_t kbase = tc::smem_u32(ring + (size_t)s * ad_stage_bytes<D, KB>());
         const uint32_t vbase = kbase + KB * D * 2;
@@ -515,6 +525,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       for (int b = 0; b < nb; ++b) {
         const int it = kv0 + b, s = it % AD_STAGES;
         const int nk = min(KB, pos - b * KB);
+        while (*kv_issued <= it) {}
         tc::mbar_wait(&kv_full[s], (it / AD_STAGES) & 1);
         const bf16* Ks = reinterpret_cast<const bf16*>(ring + (size_t)s * ad_stage_bytes<D, KB>());
         const bf16* Vs = Ks + KB * D;

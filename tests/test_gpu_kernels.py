@@ -359,14 +359,19 @@ def test_rope_attention_decode_fused(dtype, H, Hkv, D, ctx):
         np.testing.assert_allclose(out_f[b].float().cpu().numpy(), ref.reshape(-1), rtol=tol * 5, atol=tol * 5)
 
 
-@pytest.mark.parametrize("ctx", [0, 1, 127, 128, 129, 300])
-@pytest.mark.parametrize("B,H,D,rank", [(24, 32, 128, 16), (5, 4, 64, 8), (7, 8, 128, 64)])
-def test_attention_decode_pipe_lora(B, H, D, rank, ctx, monkeypatch):
-    """Persistent TMA-pipelined decode attention (several items per CTA, multi-block contexts)
-    with the fused q/k/v LoRA delta == the per-(token, head) kernel; ranks staged (<= 16) and
-    not staged (64); tokens without an adapter; identical KV append."""
+@pytest.mark.parametrize("mma", ["1", "0"])
+@pytest.mark.parametrize("ctx", [0, 1, 127, 128, 129, 300, 512, 1000])
+@pytest.mark.parametrize("B,H,D,rank", [(24, 32, 128, 16), (5, 4, 64, 8), (7, 8, 128, 64),
+                                        (64, 32, 128, 16)])
+def test_attention_decode_pipe_lora(B, H, D, rank, ctx, mma, monkeypatch):
+    """Persistent TMA-pipelined decode attention (several items per CTA, multi-block contexts;
+    tensor-core and FFMA2 consumers) with the fused q/k/v LoRA delta == the per-(token, head)
+    kernel; ranks staged (<= 16) and not staged (64); tokens without an adapter; identical KV
+    append.  Long contexts with 14 items per CTA exercise the shared KV ring's guard against
+    a consumer group waiting two laps ahead of the producer."""
+    monkeypatch.setenv("SLX_ATTN_MMA", mma)
     rng = np.random.default_rng(ctx + B + rank)
-    max_ctx, n_slots = 320, 3
+    max_ctx, n_slots = max(320, ctx + 8), 3
     cos, sin = orc.rope_table(max_ctx, D, 10000.0)
     cos_d, sin_d = torch.from_numpy(cos).to(DEV), torch.from_numpy(sin).to(DEV)
     kc = bf(torch.from_numpy(rng.standard_normal((B, H, max_ctx, D)).astype(np.float32)).to(DEV))
