@@ -94,3 +94,30 @@ def test_config2_full_step_deterministic_and_permutation_equivariant():
     c = step(perm)
     assert torch.equal(c, a[perm])   # rows are independent in every kernel
     assert torch.isfinite(a).all()
+
+
+def test_13b_widths_one_layer_decode_matches_oracle():
+    """The 13B widths (hidden 5120, 40 heads, ffn 13824: the one-CTA-per-token RMSNorm, 20-tile
+    projections) through the same decode path, mixed ranks {8, 16} on q,k,v,o."""
+    cfg = BackboneConfig("13b-1layer", hidden=5120, layers=1, heads=40, kv_heads=40, head_dim=128,
+                         ffn=13824, vocab=32000)
+    loras = [LoraConfig(16, 32.0, ("q", "k", "v", "o")), LoraConfig(8, 16.0, ("q", "k", "v", "o"))]
+    w = init_backbone(cfg, 31)
+    ads = [init_adapter(cfg, loras[a % 2], 31, a) for a in range(8)]
+    m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=48, max_ctx=40, n_slots=8,
+                       max_rank=16, max_tokens=48 * 24)
+    m.load_backbone(w)
+    for a, ad in enumerate(ads):
+        m.pool.load(a, ad, loras[a % 2])
+    rng = np.random.default_rng(4)
+    prompts = [list(map(int, rng.integers(1, cfg.vocab, size=int(rng.integers(1, 24)))))
+               for _ in range(48)]
+    ids = [int(i) for i in rng.integers(-1, 8, size=48)]
+    seqs, pre = m.prefill(prompts, ids)
+    toks = list(map(int, rng.integers(1, cfg.vocab, size=48)))
+    got = m.decode(seqs, toks, ids).float().cpu().numpy()
+    orc = OracleModel(cfg, w, ads, [loras[a % 2].scale for a in range(8)], loras[0].targets)
+    ref_pre = orc.prefill(prompts, ids)
+    ref = orc.decode(list(range(48)), toks, ids)
+    _check(pre.float().cpu().numpy(), ref_pre)
+    _check(got, ref)
