@@ -2,7 +2,8 @@
 //
 // CTA = (64-query tile of one prefill segment, head); 4 warps x 16 query rows.  Key/value
 // blocks of 64 rows are streamed from the pool ([seq][kv_head][pos][128], written by
-// slx_rope_kv_write) into shared memory with cp.async (double buffered); S = Q K^T and
+// slx_rope_kv_write) into shared memory with cp.async (K double buffered, V single: 68 KB,
+// so three CTAs — 12 warps — share an SM; measured 68 -> 64.5 ms on config 3); S = Q K^T and
 // O += P V use mma.sync m16n8k16 (bf16 in, fp32 accumulate) with ldmatrix fragments, and the
 // softmax is the online exp2 formulation with rows owned by quads of a warp.  Query t of a
 // segment starting at cache position p0 attends positions 0..p0+t (prefix + causal).
@@ -51,14 +52,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-__global__ void __launch_bounds__(FA_THREADS)
+__global__ void __launch_bounds__(FA_THREADS, 3)
 flash_prefill_kernel(bf16* __restrict__ out, int ldo, const bf16* __restrict__ qkv, int ld, int H,
                      int Hkv, const FaTile* __restrict__ tiles, const bf16* __restrict__ kc,
                      const bf16* __restrict__ vc, int max_ctx, float scale_log2) {
   extern __shared__ __align__(128) uint8_t fsm_raw[];
   bf16* Qs = reinterpret_cast<bf16*>(fsm_raw);             // [FA_BQ][LD]
-  bf16* Ks = Qs + FA_BQ * FA_LD;                            // [2][64][LD]
-  bf16* Vs = Ks + 2 * FA_BK * FA_LD;                        // [2][64][LD]
+  bf16* Ks = Qs + FA_BQ * FA_LD;                            // [2][64][LD] (double buffered)
+  bf16* Vs = Ks + 2 * FA_BK * FA_LD;                        // [64][LD] (single: 68 KB smem,
+                                                            // 3 CTAs per SM)
   pdl_wait();
   pdl_trigger();
   // grid (heads, tiles): all heads of a tile launch together, tiles in table order (the host
@@ -77,18 +79,26 @@ flash_prefill_kernel(bf16* __restrict__ out, int ldo, const bf16* __restrict__ q
     cp16(Qs + r * FA_LD + c * 8, qkv + (size_t)(tile.tok0 + min(r, tile.nq - 1)) * ld + h * FA_D + c * 8,
          r < tile.nq);
   }
-  auto stage = [&](int b, int buf) {
+  auto stage_k = [&](int b, int buf) {
     const int k0 = b * FA_BK;
     for (int e = tid; e < FA_BK * (FA_D / 8); e += FA_THREADS) {
       const int r = e / (FA_D / 8), c = e % (FA_D / 8);
-      const bool ok = k0 + r < n_keys;
       const size_t off = (size_t)min(k0 + r, n_keys - 1) * FA_D + c * 8;
-      cp16(Ks + (buf * FA_BK + r) * FA_LD + c * 8, kbase + off, ok);
-      cp16(Vs + (buf * FA_BK + r) * FA_LD + c * 8, vbase + off, ok);
+      cp16(Ks + (buf * FA_BK + r) * FA_LD + c * 8, kbase + off, k0 + r < n_keys);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  stage(0, 0);
+  auto stage_v = [&](int b) {
+    const int k0 = b * FA_BK;
+    for (int e = tid; e < FA_BK * (FA_D / 8); e += FA_THREADS) {
+      const int r = e / (FA_D / 8), c = e % (FA_D / 8);
+      const size_t off = (size_t)min(k0 + r, n_keys - 1) * FA_D + c * 8;
+      cp16(Vs + r * FA_LD + c * 8, vbase + off, k0 + r < n_keys);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage_k(0, 0);
+  stage_v(0);
 
   // per thread: 2 query rows (lane/4 and lane/4+8 of the warp's 16), quad-shared
   const int qr0 = warp * 16 + (lane >> 2);
@@ -100,13 +110,9 @@ flash_prefill_kernel(bf16* __restrict__ out, int ldo, const bf16* __restrict__ q
   uint32_t qf[FA_D / 16][4];
 
   for (int b = 0; b < nblk; ++b) {
-    if (b + 1 < nblk) {
-      stage(b + 1, (b + 1) & 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");   // K(b), V(b) (and Q) landed
     __syncthreads();
+    if (b + 1 < nblk) stage_k(b + 1, (b + 1) & 1);         // overlaps S = Q K^T and softmax
     if (b == 0) {
 #pragma unroll
       for (int kk = 0; kk < FA_D / 16; ++kk) {
@@ -115,7 +121,7 @@ flash_prefill_kernel(bf16* __restrict__ out, int ldo, const bf16* __restrict__ q
       }
     }
     const bf16* K = Ks + (b & 1) * FA_BK * FA_LD;
-    const bf16* V = Vs + (b & 1) * FA_BK * FA_LD;
+    const bf16* V = Vs;
     // S = Q K^T for this warp's 16 rows x 64 keys
     float sacc[FA_BK / 8][4];
 #pragma unroll
@@ -199,7 +205,8 @@ flash_prefill_kernel(bf16* __restrict__ out, int ldo, const bf16* __restrict__ q
         mma16816(o[2 * j + 1], a, b2, b3);
       }
     }
-    __syncthreads();   // this buffer is refilled two blocks later
+    __syncthreads();   // every warp is done with V(b) (and K(b), refilled next iteration)
+    if (b + 1 < nblk) stage_v(b + 1);
   }
   // normalise and store
   const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
@@ -236,7 +243,7 @@ extern "C" int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld
   SLX_CHECK_ALIGN(k_cache, 16);
   SLX_CHECK_ALIGN(v_cache, 16);
   if (n_tiles == 0) return SLX_OK;
-  const size_t smem = (size_t)(FA_BQ + 4 * FA_BK) * FA_LD * sizeof(bf16);
+  const size_t smem = (size_t)(FA_BQ + 3 * FA_BK) * FA_LD * sizeof(bf16);
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(flash_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
