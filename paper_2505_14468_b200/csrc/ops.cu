@@ -773,9 +773,21 @@ __global__ void argmax_kernel(int32_t* __restrict__ out, const T* __restrict__ x
   const T* row = x + (size_t)blockIdx.x * ld;
   float best = -FLT_MAX;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float v = to_f32(row[i]);
-    if (v > best) { best = v; bi = i; }
+  if (sizeof(T) == 4 && n % 4 == 0 && ld % 4 == 0 &&
+      (reinterpret_cast<uintptr_t>(x) & 15) == 0) {   // fp32 logits: 16-byte loads
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    for (int i = threadIdx.x; i < n / 4; i += blockDim.x) {
+      const float4 v = r4[i];   // indices 4i .. 4i+3 in order: strict > keeps the first max
+      if (v.x > best) { best = v.x; bi = 4 * i; }
+      if (v.y > best) { best = v.y; bi = 4 * i + 1; }
+      if (v.z > best) { best = v.z; bi = 4 * i + 2; }
+      if (v.w > best) { best = v.w; bi = 4 * i + 3; }
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const float v = to_f32(row[i]);
+      if (v > best) { best = v; bi = i; }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1028,7 +1040,7 @@ extern "C" int slx_argmax(int dtype, int32_t* out, const void* logits, int ld, i
   SLX_CHECK_ARG(n_rows >= 0 && n_cols > 0 && ld >= n_cols && out && logits);
   if (n_rows == 0) return SLX_OK;
   int st = SLX_OK;
-  DISPATCH_DT(dtype, st = launch_ex(argmax_kernel<T>, dim3(n_rows), dim3(1024), 0, (cudaStream_t)stream, 1u, out, (const T*)logits, ld, n_cols));
+  DISPATCH_DT(dtype, st = launch_ex(argmax_kernel<T>, dim3(n_rows), dim3(512), 0, (cudaStream_t)stream, 1u, out, (const T*)logits, ld, n_cols));
   return st;
 }
 

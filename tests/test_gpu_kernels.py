@@ -261,11 +261,17 @@ def test_rmsnorm_embedding_argmax(dtype):
     e = torch.empty(4, 256, dtype=dtype, device=DEV)
     ops.embedding(e, torch.from_numpy(table).to(DEV, torch.bfloat16), torch.from_numpy(toks).to(DEV))
     assert np.array_equal(e.float().cpu().numpy(), table[toks])
-    lg = rng.standard_normal((5, 32000)).astype(np.float32)
-    lg[2, 7] = lg[2, 9] = 100.0  # tie -> lowest index
-    am = torch.empty(5, dtype=torch.int32, device=DEV)
+    lg = rng.standard_normal((6, 32000)).astype(np.float32)
+    lg[2, 7] = lg[2, 9] = 100.0  # tie -> lowest index (different 16-byte chunks)
+    lg[3, 5] = lg[3, 6] = 100.0  # tie inside one 16-byte chunk
+    lg[4, 31999] = lg[4, 4 * 512 + 1] = 100.0   # tie across threads of the vectorised scan
+    lg[5, :] = -3.0              # all equal -> index 0
+    am = torch.empty(6, dtype=torch.int32, device=DEV)
     ops.argmax(am, torch.from_numpy(lg).to(DEV))
     assert am.cpu().numpy().tolist() == np.argmax(lg, -1).tolist()
+    am2 = torch.empty(6, dtype=torch.int32, device=DEV)   # odd width: the scalar scan
+    ops.argmax(am2, torch.from_numpy(np.ascontiguousarray(lg[:, :31999])).to(DEV))
+    assert am2.cpu().numpy().tolist() == np.argmax(lg[:, :31999], -1).tolist()
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
