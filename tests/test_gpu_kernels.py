@@ -518,3 +518,18 @@ def test_flash_prefill_matches_oracle(H, Hkv, segs):
                             vv[s_].transpose(1, 0, 2)[:p0 + n], np.arange(p0, p0 + n))
         np.testing.assert_allclose(out[tok0:tok0 + n].float().cpu().numpy(), ref.reshape(n, -1),
                                    rtol=3e-2, atol=3e-2)
+
+
+@pytest.mark.parametrize("d", [256, 4096, 5120])
+def test_rmsnorm_prefill_batch_matches_oracle(d):
+    """bf16 RMSNorm of a prefill-sized batch (300 tokens, up to the 13B width) vs the oracle."""
+    rng = np.random.default_rng(d)
+    T = 300
+    x = rng.standard_normal((T, d)).astype(np.float32)
+    w = (rng.random(d).astype(np.float32) + 0.5)
+    xd = torch.from_numpy(x).to(DEV, torch.bfloat16)
+    wd = torch.from_numpy(w).to(DEV, torch.bfloat16)
+    out = torch.empty_like(xd)
+    ops.rmsnorm(out, xd, wd, 1e-5)
+    ref = orc.rmsnorm(xd.float().cpu().numpy(), wd.float().cpu().numpy(), 1e-5)
+    np.testing.assert_allclose(out.float().cpu().numpy(), ref, rtol=1e-2, atol=1e-2)
