@@ -353,30 +353,56 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       }
       group_sync(g);
     }
-    for (int i = gt; i < 3 * D; i += AD_GT) {
-      const int p = i / D, e = i - p * D;
-      float v = __bfloat162float(hd->row[p][e]);
-      const bf16* bp = a.dbg_stream == 2 ? nullptr : hd->b[p];
-      if (bp != nullptr) {
-        const bf16* br = (hd->bstaged ? hd->bs[p] : bp) + (size_t)e * rank;
-        const float* vv = sc_.sv[p];
-        float acc = 0.f;
-        for (int jj = 0; jj < rank; jj += 8) {
-          const uint4 u = *reinterpret_cast<const uint4*>(br + jj);
-          const float4 v0 = *reinterpret_cast<const float4*>(vv + jj);
-          const float4 v1 = *reinterpret_cast<const float4*>(vv + jj + 4);
-          const float2 b0 = bf2_unpack(u.x), b1 = bf2_unpack(u.y), b2 = bf2_unpack(u.z), b3 = bf2_unpack(u.w);
-          acc = fmaf(v0.x, b0.x, acc); acc = fmaf(v0.y, b0.y, acc);
-          acc = fmaf(v0.z, b1.x, acc); acc = fmaf(v0.w, b1.y, acc);
-          acc = fmaf(v1.x, b2.x, acc); acc = fmaf(v1.y, b2.y, acc);
-          acc = fmaf(v1.z, b3.x, acc); acc = fmaf(v1.w, b3.y, acc);
-        }
-        v = __bfloat162float(__float2bfloat16_rn(v + acc));
-      } else if (hd->slot >= 0 && rank > AD_VMAX) {
-        const int col = (p == 0 ? h : (p == 1 ? a.H + h : 2 * a.H + h)) * D + e;
-        v = __bfloat162float(__float2bfloat16_rn(v + delta_col(a.lora, delta_tok(a.lora, t), col)));
+    {
+      // this thread's (up to NIT) outputs of the 3 x D q/k/v slice, their LoRA dot products
+      // interleaved (independent accumulators; each one's fmaf order as slx_lora_expand)
+      constexpr int NIT = (3 * D + AD_GT - 1) / AD_GT;
+      float acc[NIT];
+      const bf16* brs[NIT];
+      const float* vvs[NIT];
+      bool on[NIT];
+      int jr = 0;   // rank of the fused deltas (shared by the item's parts)
+#pragma unroll
+      for (int k = 0; k < NIT; ++k) {
+        const int i = gt + k * AD_GT;
+        const int p = i / D, e = i - p * D;
+        const bf16* bp = (i < 3 * D && a.dbg_stream != 2) ? hd->b[p] : nullptr;
+        on[k] = bp != nullptr;
+        brs[k] = on[k] ? (hd->bstaged ? hd->bs[p] : bp) + (size_t)e * rank : nullptr;
+        vvs[k] = sc_.sv[i < 3 * D ? p : 0];
+        acc[k] = 0.f;
+        if (on[k]) jr = rank;
       }
-      sc_.raw[p][e] = v;
+      for (int jj = 0; jj < jr; jj += 8) {
+#pragma unroll
+        for (int k = 0; k < NIT; ++k) {
+          if (!on[k]) continue;
+          const uint4 u = *reinterpret_cast<const uint4*>(brs[k] + jj);
+          const float4 v0 = *reinterpret_cast<const float4*>(vvs[k] + jj);
+          const float4 v1 = *reinterpret_cast<const float4*>(vvs[k] + jj + 4);
+          const float2 b0 = bf2_unpack(u.x), b1 = bf2_unpack(u.y), b2 = bf2_unpack(u.z), b3 = bf2_unpack(u.w);
+          float c = acc[k];
+          c = fmaf(v0.x, b0.x, c); c = fmaf(v0.y, b0.y, c);
+          c = fmaf(v0.z, b1.x, c); c = fmaf(v0.w, b1.y, c);
+          c = fmaf(v1.x, b2.x, c); c = fmaf(v1.y, b2.y, c);
+          c = fmaf(v1.z, b3.x, c); c = fmaf(v1.w, b3.y, c);
+          acc[k] = c;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NIT; ++k) {
+        const int i = gt + k * AD_GT;
+        if (i >= 3 * D) continue;
+        const int p = i / D, e = i - p * D;
+        float v = __bfloat162float(hd->row[p][e]);
+        if (on[k]) {
+          v = __bfloat162float(__float2bfloat16_rn(v + acc[k]));
+        } else if (hd->slot >= 0 && rank > AD_VMAX) {
+          const int col = (p == 0 ? h : (p == 1 ? a.H + h : 2 * a.H + h)) * D + e;
+          v = __bfloat162float(__float2bfloat16_rn(v + delta_col(a.lora, delta_tok(a.lora, t), col)));
+        }
+        sc_.raw[p][e] = v;
+      }
     }
     group_sync(g);
     // ---- RoPE (rotate-half), new key / value appended at pos
