@@ -344,15 +344,6 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       continue;
     }
     // ---- q/k/v of this head with the fused LoRA expand (sequential fmaf: as slx_lora_expand)
-    const bool lora_v = hd->b[0] != nullptr || hd->b[1] != nullptr || hd->b[2] != nullptr;
-    if (lora_v) {   // scale * v once per item
-      const float sc = hd->lscale;
-      for (int i = gt; i < 3 * AD_VMAX; i += AD_GT) {
-        const int p = i / AD_VMAX, jj = i - p * AD_VMAX;
-        if (jj < rank) sc_.sv[p][jj] = hd->v[p][jj] * sc;
-      }
-      group_sync(g);
-    }
     {
       // this thread's (up to NIT) outputs of the 3 x D q/k/v slice, their LoRA dot products
       // interleaved (independent accumulators; each one's fmaf order as slx_lora_expand)
@@ -369,17 +360,22 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
         const bf16* bp = (i < 3 * D && a.dbg_stream != 2) ? hd->b[p] : nullptr;
         on[k] = bp != nullptr;
         brs[k] = on[k] ? (hd->bstaged ? hd->bs[p] : bp) + (size_t)e * rank : nullptr;
-        vvs[k] = sc_.sv[i < 3 * D ? p : 0];
+        vvs[k] = hd->v[i < 3 * D ? p : 0];   // scale * v formed in the loop (same rounding)
         acc[k] = 0.f;
         if (on[k]) jr = rank;
       }
+      const float lsc = hd->lscale;
       for (int jj = 0; jj < jr; jj += 8) {
 #pragma unroll
         for (int k = 0; k < NIT; ++k) {
           if (!on[k]) continue;
           const uint4 u = *reinterpret_cast<const uint4*>(brs[k] + jj);
-          const float4 v0 = *reinterpret_cast<const float4*>(vvs[k] + jj);
-          const float4 v1 = *reinterpret_cast<const float4*>(vvs[k] + jj + 4);
+          float4 v0 = *reinterpret_cast<const float4*>(vvs[k] + jj);
+          float4 v1 = *reinterpret_cast<const float4*>(vvs[k] + jj + 4);
+          v0.x = __fmul_rn(v0.x, lsc); v0.y = __fmul_rn(v0.y, lsc);
+          v0.z = __fmul_rn(v0.z, lsc); v0.w = __fmul_rn(v0.w, lsc);
+          v1.x = __fmul_rn(v1.x, lsc); v1.y = __fmul_rn(v1.y, lsc);
+          v1.z = __fmul_rn(v1.z, lsc); v1.w = __fmul_rn(v1.w, lsc);
           const float2 b0 = bf2_unpack(u.x), b1 = bf2_unpack(u.y), b2 = bf2_unpack(u.z), b3 = bf2_unpack(u.w);
           float c = acc[k];
           c = fmaf(v0.x, b0.x, c); c = fmaf(v0.y, b0.y, c);
