@@ -38,7 +38,7 @@ extern "C" {
 #define SLX_API
 #endif
 
-#define SLX_ABI_VERSION 1
+#define SLX_ABI_VERSION 2
 
 enum {
   SLX_OK = 0,
@@ -107,11 +107,24 @@ typedef struct slx_l2_prefetch {
 /* CTAs of the stream-K decode GEMM slx_gemm_bf16 launches for (M, N, K) on tiled weights
  * (0: another kernel) — sizes slx_l2_prefetch unit windows. */
 SLX_API int slx_gemm_sk_ctas(int M, int N, int K);
-/* slx_gemm_bf16 + an L2 prefetch hint for the next kernel (pf may be NULL). */
-SLX_API int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
+/* Explicit tiling choices (tests / tuning tools; NULL or all-zero = the planner's choice, which
+ * is what the product uses).  The library reads no environment variables. */
+typedef struct slx_gemm_tuning {
+  int tile_kernel;   /* 1: never the stream-K decode kernel (tile kernel, any M) */
+  int ctas_per_sm;   /* tile kernel: 1 or 2 */
+  int splits;        /* tile kernel: K splits per output tile (1..8) */
+  int bn;            /* tile kernel: 128 or 256 weight rows per tile */
+  int gsplit;        /* tile kernel: 1 = split-K reduced through global partials, 2 = DSMEM cluster */
+  int sk_ctas;       /* stream-K: CTAs (all-SM stream-K partition with this many CTAs) */
+  int sk_min_units;  /* stream-K: minimum k-blocks per piece (default 4) */
+  int sk_no_cluster; /* stream-K: 1 = reduce uniform splits through global pieces, not DSMEM */
+} slx_gemm_tuning;
+/* slx_gemm_bf16 + an L2 prefetch hint for the next kernel (pf may be NULL) + explicit tiling
+ * (tuning may be NULL). */
+SLX_API int slx_gemm_bf16_ex(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
                   int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes,
-                  const slx_l2_prefetch* pf, void* stream);
+                  const slx_l2_prefetch* pf, const slx_gemm_tuning* tuning, void* stream);
 /* Decode split-K handed to the consumer: W tiled, M <= 64; the N columns are cut in 256-wide
  * tiles and the K range of each tile in `splits` equal pieces, one CTA per piece; every piece
  * is written in fp32 to `part` with no reduction and no epilogue, so the kernel has no tail.
@@ -122,49 +135,6 @@ SLX_API size_t slx_gemm_splitk_bytes(int M, int N, int splits);
 SLX_API int slx_gemm_bf16_splitk(const void* A, int lda, const void* W, int M, int N, int K,
                   int splits, float* part, size_t part_bytes, const slx_l2_prefetch* pf,
                   void* stream);
-/* Fused input RMSNorm (decode, M <= 64, W tiled): before the mainloop needs its A operand, the
- * GEMM's CTAs build it across the grid (two grid barriers; all CTAs are co-resident):
- *   x = round(x + sum of the split-K pieces `sk`)  (the previous projection's residual epilogue)
- *   x = round(x + LoRA delta `lora`)               (one target spanning the row; v from `sk` when
- *                                                   lora->v is NULL; rank <= 16)
- *   h = rmsnorm(x) * w                             (h = the GEMM's A, written to `A`)
- * x is updated in place.  ss: >= M * 148 floats of scratch; bar: two zero-initialised uint32
- * counters owned by this call site (monotonic; one grid size per call site). */
-typedef struct slx_norm_in {
-  void* x;
-  int ldx;
-  const void* w;
-  float eps;
-  const slx_splitk_in* sk;     /* may be NULL */
-  const slx_lora_delta* lora;  /* may be NULL */
-  float* ss;
-  size_t ss_bytes;
-  uint32_t* bar;
-} slx_norm_in;
-SLX_API int slx_gemm_bf16_norm(void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
-                  const void* R, int ldr, int M, int N, int K, int epilogue, int n_main, void* C2,
-                  int ldc2, void* ws, size_t ws_bytes, const slx_norm_in* norm,
-                  const slx_l2_prefetch* pf, void* stream);
-/* Row RMS across two decode GEMMs, so the RMSNorm between them needs no kernel of its own:
- *   producer (epilogue SLX_EPI_RESIDUAL, bf16 C): ss_out[m * ss_out_ld + n / 16] = sum of
- *     squares of the 16 stored values C[m, n .. n+16) (main columns; ss_out_ld >= n_main / 16);
- *   consumer (epilogue SLX_EPI_NONE or SLX_EPI_RESIDUAL): row m of A.W^T (and of the side
- *     output) is scaled by 1 / sqrt(sum(ss_in[m * ss_in_n .. + ss_in_n)) / d + eps) before the
- *     epilogue — i.e. rmsnorm(A) . W^T when the norm weight is folded into W's columns.
- * Either pointer may be NULL.  Decode shapes only (tiled weights, M <= 64): SLX_ERR_UNSUPPORTED
- * otherwise. */
-typedef struct slx_row_ss {
-  float* ss_out;
-  int ss_out_ld;
-  const float* ss_in;
-  int ss_in_n;
-  int d;
-  float eps;
-} slx_row_ss;
-SLX_API int slx_gemm_bf16_rss(const void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
-                  const void* R, int ldr, int M, int N, int K, int epilogue, int n_main, void* C2,
-                  int ldc2, void* ws, size_t ws_bytes, const slx_row_ss* rss,
-                  const slx_l2_prefetch* pf, void* stream);
 /* Debug only: following slx_gemm_bf16 launches write 16 u64 globaltimer slots per CTA into
  * the device buffer `buf` (phase timeline: entry, prologue, past PDL wait, first stage landed,
  * last MMA issued, accumulator ready, split-K reduction start, exit, reduction end, segment
@@ -243,21 +213,35 @@ SLX_API int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, int 
                   const int32_t* slot_rank, const float* slot_scale, int n_slots, int max_rank,
                   int n_targets, const slx_lora_target* targets, const int* v_col_off,
                   void* ws, size_t ws_bytes, void* stream);
+/* Gathered shrink (decode with a large adapter pool): over the plan in ws (slx_lora_plan_tokens)
+ * v[t, v_col_off[i] + j] = x_t . A_{slot(t), i}[j] for j < rank (fp32, unscaled), reading each
+ * adapter present in the batch once per plan tile of <= 8 tokens (a_ptrs of the targets; b_ptrs
+ * unused).  Rows of tokens without an adapter are not written.  Consumers: slx_lora_delta with
+ * v_slot_stride = 0. */
+SLX_API int slx_lora_shrink(int dtype, float* v, int ldv, const void* x, int ldx, int n_tok,
+                  int d_in, const int32_t* slot_rank, int n_slots, int max_rank, int n_targets,
+                  const slx_lora_target* targets, const int* v_col_off, void* ws,
+                  size_t ws_bytes, void* stream);
 /* Fused decode expand: a consumer kernel adds the LoRA term of the projection it reads while
  * loading it, instead of a separate expand launch + read-modify-write of y.  For output
  * column n of target i of token t (slot s = tok_slot[t] >= 0, rank r = slot_rank[s]):
  *   delta = sum_{j < r} (v[t, v_col_off[i] + s * max_rank + j] * slot_scale[s]) * B_s[n, j]
  * (sequential fmaf in j: bit-identical to slx_lora_expand).  The target's outputs are the row
  * columns [y_col_off[i], y_col_off[i] + d_out[i]).  b_ptrs[i]: device uint64 [n_slots] table of
- * B_s [d_out, r] (bf16; 0 = adapter does not target it). */
+ * B_s [d_out, r] (bf16; 0 = adapter does not target it).
+ * v column of (target i, slot s, rank index j) = v_col_off[i] + s * v_slot_stride + j:
+ * v_slot_stride = max_rank for the stacked shrink (every slot's block), 0 for a gathered shrink
+ * that writes only the token's own adapter (slx_lora_shrink_gather).
+ * Preconditions: ranks are multiples of 8 and <= max_rank (16-byte B rows); v 16-byte aligned. */
 typedef struct slx_lora_delta {
-  const float* v;            /* fp32 [n_tok, ldv]: the GEMM side output (stacked shrink) */
+  const float* v;            /* fp32 [n_tok, ldv]: the shrink output */
   int ldv;
   const int32_t* tok_slot;   /* [n_tok], -1 = no adapter */
   const int32_t* slot_rank;  /* [n_slots] */
   const float* slot_scale;   /* [n_slots] */
   int max_rank;
   int n_targets;             /* 0 .. SLX_LORA_MAX_TARGETS */
+  int v_slot_stride;         /* see above (multiple of 4) */
   const uint64_t* b_ptrs[SLX_LORA_MAX_TARGETS];
   int v_col_off[SLX_LORA_MAX_TARGETS];
   int y_col_off[SLX_LORA_MAX_TARGETS];
@@ -315,25 +299,17 @@ SLX_API int slx_attention(int dtype, void* out, int ldo, const void* qkv, int ld
                   const int32_t* tok_seq, const void* k_cache, const void* v_cache, int max_ctx,
                   void* stream);
 /* Decode step fusion of slx_rope_kv_write + slx_attention when every token is the NEXT
- * position of its own sequence (tok_pos[t] = cached length): RoPE on q and the new key in
- * registers, k/v appended to the pool, attention over cached positions [0, pos) + the new key. */
-SLX_API int slx_rope_attention_decode(int dtype, void* out, int ldo, const void* qkv, int ld_qkv,
-                  int n_tok, int heads, int kv_heads, int head_dim, const int32_t* tok_pos,
-                  const int32_t* tok_seq, const float* cos_tab, const float* sin_tab, int max_pos,
-                  void* k_cache, void* v_cache, int max_ctx, void* stream);
-/* Same, with the q/k/v LoRA expand fused in: the row values of q (head h), k and v (kv head)
- * get the slx_lora_delta of their qkv-row columns added before RoPE / the KV append (lora may
- * be NULL).  qkv itself is not modified. */
-SLX_API int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, const void* qkv,
-                  int ld_qkv, int n_tok, int heads, int kv_heads, int head_dim,
-                  const int32_t* tok_pos, const int32_t* tok_seq, const float* cos_tab,
-                  const float* sin_tab, int max_pos, void* k_cache, void* v_cache, int max_ctx,
-                  const slx_lora_delta* lora, void* stream);
-/* Same + L2 prefetch hint for the next kernel (issued by the last wave of CTAs; pf may be NULL)
- * and the pool's sequence-slot count `pool_seqs` (k/v caches are [pool_seqs][kv_heads][max_ctx]
- * [head_dim]; 0 = unknown): with it, bf16 MHA runs the tensor-core consumer over 128B-swizzled
- * TMA tiles of the pool. */
-SLX_API int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const void* qkv,
+ * position of its own sequence (tok_pos[t] = cached length): RoPE on q and the new key, k/v
+ * appended to the pool, attention over cached positions [0, pos) + the new key.  `lora` (may be
+ * NULL) fuses the q/k/v LoRA expand: the row values of q (head h), k and v (kv head) get the
+ * slx_lora_delta of their qkv-row columns added before RoPE / the append (qkv is not
+ * modified).  `pf` (may be NULL): L2 prefetch of the next kernel's first bytes.  `pool_seqs`:
+ * sequence slots of the k/v caches ([pool_seqs][kv_heads][max_ctx][head_dim]).
+ * bf16 MHA (head_dim 64/128) runs the persistent TMA-pipelined tensor-core kernel; fp32 parity
+ * mode and GQA run one CTA per (token, head).  Preconditions: tok_pos[t] < max_ctx; KV rows
+ * past tok_pos of a sequence are finite (whole 64-row boxes are multiplied by P = 0 there;
+ * the model zero-fills its pool); adapter ranks are multiples of 8. */
+SLX_API int slx_rope_attention_decode(int dtype, void* out, int ldo, const void* qkv,
                   int ld_qkv, int n_tok, int heads, int kv_heads, int head_dim,
                   const int32_t* tok_pos, const int32_t* tok_seq, const float* cos_tab,
                   const float* sin_tab, int max_pos, void* k_cache, void* v_cache, int max_ctx,

@@ -12,6 +12,7 @@ import os
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libslora_b200.so")
 
+ABI_VERSION = 2
 SLX_OK = 0
 SLX_ERR_INVALID = -1
 SLX_ERR_ALIGN = -2
@@ -43,7 +44,8 @@ class LoraTarget(ctypes.Structure):
 class LoraDelta(ctypes.Structure):
     """slx_lora_delta: fused decode expand in a consumer kernel."""
     _fields_ = [("v", _p), ("ldv", _i), ("tok_slot", _p), ("slot_rank", _p), ("slot_scale", _p),
-                ("max_rank", _i), ("n_targets", _i), ("b_ptrs", _p * 4), ("v_col_off", _i * 4),
+                ("max_rank", _i), ("n_targets", _i), ("v_slot_stride", _i), ("b_ptrs", _p * 4),
+                ("v_col_off", _i * 4),
                 ("y_col_off", _i * 4), ("d_out", _i * 4)]
 
 
@@ -52,16 +54,10 @@ class SplitKIn(ctypes.Structure):
     _fields_ = [("part", _p), ("splits", _i), ("bm", _i), ("n_main", _i)]
 
 
-class NormIn(ctypes.Structure):
-    """slx_norm_in: fused input-RMSNorm prologue of a decode GEMM."""
-    _fields_ = [("x", _p), ("ldx", _i), ("w", _p), ("eps", _f), ("sk", ctypes.POINTER(SplitKIn)),
-                ("lora", ctypes.POINTER(LoraDelta)), ("ss", _p), ("ss_bytes", _sz), ("bar", _p)]
-
-
-class RowSS(ctypes.Structure):
-    """slx_row_ss: row sums of squares written by one decode GEMM, row scales of the next."""
-    _fields_ = [("ss_out", _p), ("ss_out_ld", _i), ("ss_in", _p), ("ss_in_n", _i), ("d", _i),
-                ("eps", _f)]
+class GemmTuning(ctypes.Structure):
+    """slx_gemm_tuning: explicit tiling for tests / tools (all zero = the planner's choice)."""
+    _fields_ = [("tile_kernel", _i), ("ctas_per_sm", _i), ("splits", _i), ("bn", _i),
+                ("gsplit", _i), ("sk_ctas", _i), ("sk_min_units", _i), ("sk_no_cluster", _i)]
 
 
 class L2Prefetch(ctypes.Structure):
@@ -81,13 +77,9 @@ SIGNATURES = {
     "slx_debug_gemm_trace": (_i, [_p]),
     "slx_gemm_splitk_bytes": (_sz, [_i, _i, _i]),
     "slx_gemm_bf16_splitk": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _sz, ctypes.POINTER(L2Prefetch), _p]),
-    "slx_gemm_bf16_norm": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _p, _i, _p, _sz,
-                                ctypes.POINTER(NormIn), ctypes.POINTER(L2Prefetch), _p]),
-    "slx_gemm_bf16_rss": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _p, _i, _p, _sz,
-                               ctypes.POINTER(RowSS), ctypes.POINTER(L2Prefetch), _p]),
     "slx_gemm_sk_ctas": (_i, [_i, _i, _i]),
-    "slx_gemm_bf16_pf": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p,
-                              _sz, ctypes.POINTER(L2Prefetch), _p]),
+    "slx_gemm_bf16_ex": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p,
+                              _sz, ctypes.POINTER(L2Prefetch), ctypes.POINTER(GemmTuning), _p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),
     "slx_gemm_group_tile_bytes": (_sz, []),
     "slx_gemm_bf16_lorafold": (_i, [_p, _i, _p, _i, _p, _i, _i, _p, _i, _i, _i, _i, _i, _p, _i, _p, _i,
@@ -95,6 +87,8 @@ SIGNATURES = {
     "slx_gemm_grouped_bf16": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p, _i, _i,
                                    _i, _p, _i, _p]),
     "slx_lora_expand": (_i, [_i, _p, _i, _p, _i, _i, _p, _p, _i, _i, _i,
+                             ctypes.POINTER(LoraTarget), ctypes.POINTER(_i), _p, _sz, _p]),
+    "slx_lora_shrink": (_i, [_i, _p, _i, _p, _i, _i, _i, _p, _i, _i, _i,
                              ctypes.POINTER(LoraTarget), ctypes.POINTER(_i), _p, _sz, _p]),
     "slx_packed_weight_elems": (_sz, [_i, _i]),
     "slx_pack_weight": (_i, [_p, _p, _i, _i, _i, _p]),
@@ -115,13 +109,9 @@ SIGNATURES = {
                                ctypes.POINTER(LoraDelta), ctypes.POINTER(L2Prefetch), _p]),
     "slx_rope_kv_write": (_i, [_i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p, _i, _p]),
     "slx_attention": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p]),
-    "slx_rope_attention_decode": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i, _p, _p,
-                                       _i, _p]),
-    "slx_rope_attention_decode_lora": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i,
-                                            _p, _p, _i, ctypes.POINTER(LoraDelta), _p]),
-    "slx_rope_attention_decode_pf": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i,
-                                          _p, _p, _i, _i, ctypes.POINTER(LoraDelta),
-                                          ctypes.POINTER(L2Prefetch), _p]),
+    "slx_rope_attention_decode": (_i, [_i, _p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _i,
+                                       _p, _p, _i, _i, ctypes.POINTER(LoraDelta),
+                                       ctypes.POINTER(L2Prefetch), _p]),
     "slx_flash_prefill_tile_queries": (_i, []),
     "slx_flash_prefill_tile_bytes": (_sz, []),
     "slx_attention_prefill": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _i, _p, _p, _i, _p]),
@@ -159,7 +149,7 @@ def load() -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.slx_abi_version() != 1:
+        if lib.slx_abi_version() != ABI_VERSION:
             raise ImportError("libslora_b200 ABI version mismatch")
         _LIB = lib
     return _LIB

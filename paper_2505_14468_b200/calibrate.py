@@ -78,7 +78,9 @@ def profile_function_spec(model, function_id: str, adapter_slot: int, *,
     times = [measure_prefill_ms(model, adapter_slot, b, prompt_len) for b in batch_sizes]
     t0, alpha = fit_latency_law(batch_sizes, times)
     decode = measure_decode_ms(model, adapter_slot, decode_batch, prompt_len)
-    kv = model.cfg.kv_bytes_per_token() * (prompt_len + max_new_tokens)
+    # the pool reserves max_ctx positions per sequence slot (MultiLoraModel.memory_ledger's
+    # kv_slot_bytes), whatever the request's length: that is what admission must book
+    kv = model.cfg.kv_bytes_per_token() * model.max_ctx
     if model.dtype == torch.float32:
         kv *= 2
     arts = []

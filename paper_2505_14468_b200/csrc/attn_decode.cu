@@ -3,8 +3,7 @@
 // One work item = (token t, head h): the token is the NEXT position `pos` of its own sequence.
 // Per layer of the 7B decode step the kernel streams 64 tok x 32 heads x 128 cached keys x
 // (K + V) = 134 MB of KV cache, so it is HBM-bound and the design goal is to keep every SM's
-// copy engine busy (the copy ring alone streams at ~7 TB/s, SLX_ATTN_DBG_STREAM=1).  One
-// persistent CTA per SM:
+// copy engine busy (the copy ring alone streams at ~7 TB/s).  One persistent CTA per SM:
 //   * a producer warp: its 32 lanes resolve the metadata of 32 items at a time (position,
 //     sequence, adapter slot / rank / scale, LoRA B rows), then lane 0 issues 1-D bulk copies
 //     (TMA) of whole K and V blocks (one contiguous run each in the [seq][head][max_ctx][D]
@@ -14,14 +13,15 @@
 //   * two consumer groups of 4 warps taking alternate items, so one group's latency chain
 //     (fused LoRA delta — bit-identical to slx_lora_expand —, RoPE, k/v append, barriers)
 //     overlaps the other's attention.  Within a group each warp runs its own online softmax
-//     over its keys of every block (no CTA barrier per block); two lanes share a key, reading
-//     K in a per-key rotated chunk order, so the unpadded TMA layout is bank-conflict free.
+//     over its keys of every block (no CTA barrier per block) on the tensor cores (mma.sync
+//     m16n8k16 from ldmatrix on the 128B-swizzled 2-D TMA tiles).
+// Preconditions (slx_rope_attention_decode in slora_b200.h): adapter ranks are multiples of 8,
+// and KV rows past `pos` of a sequence hold finite values (whole 64-row boxes are multiplied by
+// P = 0 there; the model zero-fills its pool).
 // ops.cu's one-CTA-per-(token, head) kernel stays for fp32 / GQA.
 //
 // Reference: the decode gap the simulator models as decode_ms_per_token x M
 // (/root/reference/pkg/src/slorasim/engine.py:888,909).
-#include <stdlib.h>
-
 #include "common.cuh"
 #include "gemm_host.h"
 #include "tc_ptx.cuh"
@@ -56,9 +56,6 @@ struct AdArgs {
   float scale_log2;
   DeltaArgs lora;
   PfArgs pf;
-  int pf_early;   // SLX_ATTN_PF_EARLY=1: prefetch at kernel start instead of after the last item
-  int dbg_stream; // SLX_ATTN_DBG_STREAM (debug): 1 consumers only drain the rings (copy roofline),
-                  // 2 skip the LoRA math, 3 LoRA B rows read from global instead of staged
   unsigned long long* trace;   // slx_debug_gemm_trace timeline window (nullptr: off)
 };
 
@@ -97,7 +94,6 @@ struct __align__(16) AdScratch {
   float kn[D], vn[D];
   float pv[AD_GW][D];
   float red[2 * AD_GW];
-  float sv[3][AD_VMAX];          // scale * LoRA v
   bf16 qb[D];
 };
 
@@ -138,7 +134,7 @@ __device__ __forceinline__ float2 bf2_unpack(uint32_t w) {
   return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
 }
 
-template <int D, int KB, bool MMA>
+template <int D, int KB>
 __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const __grid_constant__ AdArgs a) {
   constexpr int HALF = D / 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -186,22 +182,15 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
     auto issue_kv = [&](int seq, int h, int blk, int pos) {
       const int s = kv_it % AD_STAGES;
       tc::mbar_wait(&kv_empty[s], ((kv_it / AD_STAGES) & 1) ^ 1);
-      const int nk = min(KB, pos - blk * KB);
-      const uint32_t bytes = (uint32_t)nk * D * 2;
       const size_t off = (((size_t)seq * a.H + h) * a.max_ctx + (size_t)blk * KB) * D;
       uint8_t* st = ring + (size_t)s * ad_stage_bytes<D, KB>();
-      if constexpr (MMA) {   // whole 64-row boxes (rows past pos are masked), swizzled
-        const int row = (int)(off / D);
-        tc::mbar_arrive_expect_tx(&kv_full[s], 2 * KB * D * 2);
+      // whole 64-row boxes (rows past pos are masked), 128B-swizzled
+      const int row = (int)(off / D);
+      tc::mbar_arrive_expect_tx(&kv_full[s], 2 * KB * D * 2);
 #pragma unroll
-        for (int hf = 0; hf < D / 64; ++hf) {
-          tc::tma_load_2d(st + hf * KB * 128, &a.tmk, &kv_full[s], hf * 64, row, pol_kv);
-          tc::tma_load_2d(st + KB * D * 2 + hf * KB * 128, &a.tmv, &kv_full[s], hf * 64, row, pol_kv);
-        }
-      } else {
-        tc::mbar_arrive_expect_tx(&kv_full[s], 2 * bytes);
-        tc::bulk_g2s(st, a.kc + off, bytes, &kv_full[s], pol_kv);
-        tc::bulk_g2s(st + KB * D * 2, a.vc + off, bytes, &kv_full[s], pol_kv);
+      for (int hf = 0; hf < D / 64; ++hf) {
+        tc::tma_load_2d(st + hf * KB * 128, &a.tmk, &kv_full[s], hf * 64, row, pol_kv);
+        tc::tma_load_2d(st + KB * D * 2 + hf * KB * 128, &a.tmv, &kv_full[s], hf * 64, row, pol_kv);
       }
       ++kv_it;
       *kv_issued = kv_it;   // published by the st.volatile; ordered after the TMA issue above
@@ -241,7 +230,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
                   if (B != nullptr) {
                     mt.ti[p] = i;
                     mt.b[p] = B + (size_t)n * dt.rank;
-                    mt.voff[p] = a.lora.v_col_off[i] + dt.slot * a.lora.max_rank;
+                    mt.voff[p] = a.lora.v_col_off[i] + dt.slot * a.lora.v_slot_stride;
                   }
                 }
               }
@@ -254,7 +243,6 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       if (pl == 0) {
         const int nloc = min(32, (n_items - w0 + (int)gridDim.x - 1) / (int)gridDim.x);
         if (!waited) {
-          if (a.pf_early) l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);
           pdl_wait();
           pdl_trigger();
           if (a.trace) a.trace[blockIdx.x * 16 + 2] = ad_timer();
@@ -263,7 +251,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
           const ItemMeta& mt = meta[i];
           const int hs = j % AD_HSLOTS;
           const bool stage_v = mt.rank <= AD_VMAX;
-          const bool stage_b = mt.rank <= AD_BST && a.dbg_stream != 3;
+          const bool stage_b = mt.rank <= AD_BST;
           uint32_t bytes = 3 * D * 2 + D * 4;
           for (int p = 0; p < 3; ++p)
             if (mt.ti[p] >= 0 && stage_v)
@@ -304,7 +292,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       pdl_wait();
       pdl_trigger();
     }
-    if (pl == 0 && !a.pf_early) l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);
+    if (pl == 0) l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);
     __syncwarp();
     return;
   }
@@ -317,11 +305,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
   const int g = tid / AD_GT, gt = tid % AD_GT;
   const int gw = gt >> 5, lane = tid & 31;
   AdScratch<D>& sc_ = scr[g];
-  constexpr int KPW = KB / AD_GW;        // keys per warp per block
-  constexpr int LPK = 32 / KPW;          // lanes per key in the scores
-  constexpr int CPL = D / LPK / 8;       // 16-byte chunks per lane
-  constexpr int DPL = D / 32;            // output dims per lane in P.V (4 | 2)
-  const int wkey = lane / LPK, lq = lane % LPK;
+  constexpr int DPL = D / 32;            // dims per lane of the new key's score
   for (int j = g; (int)blockIdx.x + j * (int)gridDim.x < n_items; j += AD_GROUPS) {
     const int w = blockIdx.x + j * (int)gridDim.x;
     const int t = w / a.H, h = w % a.H;
@@ -331,18 +315,6 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
     const int pos = hd->pos, seq = hd->seq, rank = hd->rank;
     const int nb = (pos + KB - 1) / KB;
     const int kv0 = hd->kv_base;
-    if (a.dbg_stream == 1) {   // copy-engine roofline: drain the header and the KV blocks only
-      group_sync(g);
-      if (gt == 0) tc::mbar_arrive(&h_empty[hs]);
-      for (int b = 0; b < nb; ++b) {
-        const int it = kv0 + b;
-        while (*kv_issued <= it) {}
-        tc::mbar_wait(&kv_full[it % AD_STAGES], (it / AD_STAGES) & 1);
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&kv_empty[it % AD_STAGES]);
-      }
-      continue;
-    }
     // ---- q/k/v of this head with the fused LoRA expand (sequential fmaf: as slx_lora_expand)
     {
       // this thread's (up to NIT) outputs of the 3 x D q/k/v slice, their LoRA dot products
@@ -357,7 +329,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       for (int k = 0; k < NIT; ++k) {
         const int i = gt + k * AD_GT;
         const int p = i / D, e = i - p * D;
-        const bf16* bp = (i < 3 * D && a.dbg_stream != 2) ? hd->b[p] : nullptr;
+        const bf16* bp = i < 3 * D ? hd->b[p] : nullptr;
         on[k] = bp != nullptr;
         brs[k] = on[k] ? (hd->bstaged ? hd->bs[p] : bp) + (size_t)e * rank : nullptr;
         vvs[k] = hd->v[i < 3 * D ? p : 0];   // scale * v formed in the loop (same rounding)
@@ -434,7 +406,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
         part += __bfloat162float(sc_.qb[lane * DPL + e]) * sc_.kn[lane * DPL + e];
       s_new = warp_sum(part) * a.scale_log2;
     }
-    if constexpr (MMA) {
+    {
       // Tensor-core scores and P.V (mma.sync m16n8k16, fp32 accumulate) on the 128B-swizzled
       // TMA tiles: warp gw owns keys [16 gw, 16 gw + 16) of every block.  Scores: A = the 16 K
       // rows (ldmatrix), B = q replicated over the 8 columns, so lane (g, c) holds the scores
@@ -525,91 +497,6 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
           sc_.pv[gw][nt * 8 + 2 * cq + 1] = o[nt][1];
         }
       }
-    } else {
-      float m = gw == 0 ? s_new : -INFINITY, l = gw == 0 ? 1.f : 0.f;
-      // P.V accumulators (packed fp32 pairs: FFMA2), dims [lane*DPL, lane*DPL + DPL)
-      float2 acc2[DPL / 2];
-  #pragma unroll
-      for (int e = 0; e < DPL / 2; ++e)
-        acc2[e] = gw == 0 ? make_float2(sc_.vn[lane * DPL + 2 * e], sc_.vn[lane * DPL + 2 * e + 1])
-                          : make_float2(0.f, 0.f);
-      const int key = gw * KPW + wkey;
-      // this lane's q slice in its key-rotated chunk order (the key index of the lane is the same
-      // in every block), unpacked to fp32 pairs once per item
-      float2 q2[CPL][4];
-  #pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const int cc = (c + key) & (CPL - 1);
-        const uint4 u = *reinterpret_cast<const uint4*>(sc_.qb + lq * (D / LPK) + cc * 8);
-        q2[c][0] = bf2_unpack(u.x); q2[c][1] = bf2_unpack(u.y);
-        q2[c][2] = bf2_unpack(u.z); q2[c][3] = bf2_unpack(u.w);
-      }
-      for (int b = 0; b < nb; ++b) {
-        const int it = kv0 + b, s = it % AD_STAGES;
-        const int nk = min(KB, pos - b * KB);
-        while (*kv_issued <= it) {}
-        tc::mbar_wait(&kv_full[s], (it / AD_STAGES) & 1);
-        const bf16* Ks = reinterpret_cast<const bf16*>(ring + (size_t)s * ad_stage_bytes<D, KB>());
-        const bf16* Vs = Ks + KB * D;
-        // scores: LPK lanes per key, each a D/LPK slice read in the key-rotated chunk order
-        float sc = 0.f;
-        if (key < nk) {
-          const bf16* kr = Ks + (size_t)key * D + lq * (D / LPK);
-          float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
-  #pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const int cc = (c + key) & (CPL - 1);
-            const uint4 u = *reinterpret_cast<const uint4*>(kr + cc * 8);
-            s0 = __ffma2_rn(q2[c][0], bf2_unpack(u.x), s0);
-            s1 = __ffma2_rn(q2[c][1], bf2_unpack(u.y), s1);
-            s0 = __ffma2_rn(q2[c][2], bf2_unpack(u.z), s0);
-            s1 = __ffma2_rn(q2[c][3], bf2_unpack(u.w), s1);
-          }
-          sc = (s0.x + s0.y) + (s1.x + s1.y);
-        }
-  #pragma unroll
-        for (int o = 1; o < LPK; o <<= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-        sc = key < nk ? sc * a.scale_log2 : -INFINITY;
-        const float m_new = fmaxf(m, warp_max(sc));
-        const float corr = m_new == -INFINITY ? 1.f : exp2f(m - m_new);
-        const float p = key < nk ? exp2f(sc - m_new) : 0.f;
-        l = l * corr + warp_sum(lq == 0 ? p : 0.f);
-        const float2 corr2 = make_float2(corr, corr);
-  #pragma unroll
-        for (int e = 0; e < DPL / 2; ++e) acc2[e] = __fmul2_rn(acc2[e], corr2);
-        // P.V over the warp's keys
-  #pragma unroll
-        for (int kk = 0; kk < KPW; ++kk) {
-          const float pk = __shfl_sync(0xffffffffu, p, kk * LPK);
-          if (gw * KPW + kk < nk) {
-            const float2 p2 = make_float2(pk, pk);
-            const bf16* vr = Vs + (size_t)(gw * KPW + kk) * D + lane * DPL;
-            if (DPL == 4) {
-              const uint2 u = *reinterpret_cast<const uint2*>(vr);
-              acc2[0] = __ffma2_rn(p2, bf2_unpack(u.x), acc2[0]);
-              acc2[(DPL / 2) - 1] = __ffma2_rn(p2, bf2_unpack(u.y), acc2[(DPL / 2) - 1]);
-            } else {
-              acc2[0] = __ffma2_rn(p2, bf2_unpack(*reinterpret_cast<const uint32_t*>(vr)), acc2[0]);
-            }
-          }
-        }
-        m = m_new;
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&kv_empty[s]);   // this warp is done with the stage
-      }
-      float acc[DPL];
-  #pragma unroll
-      for (int e = 0; e < DPL / 2; ++e) {
-        acc[2 * e] = acc2[e].x;
-        acc[2 * e + 1] = acc2[e].y;
-      }
-      // ---- merge the group's warp states (fixed order) and write the head's output
-      if (lane == 0) {
-        sc_.red[gw] = m;
-        sc_.red[AD_GW + gw] = l;
-      }
-  #pragma unroll
-      for (int e = 0; e < DPL; ++e) sc_.pv[gw][lane * DPL + e] = acc[e];
     }
     group_sync(g);
     if (gt < D) {
@@ -632,7 +519,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
 
 }  // namespace
 
-// Host launcher used by slx_rope_attention_decode_pf (ops.cu) for bf16 MHA, D in {64, 128}.
+// Host launcher used by slx_rope_attention_decode (ops.cu) for bf16 MHA, D in {64, 128}.
 int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int n_tok, int heads,
                             int head_dim, const int32_t* tok_pos, const int32_t* tok_seq,
                             const float* cos_tab, const float* sin_tab, void* k_cache,
@@ -644,10 +531,6 @@ int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int
   a.n_tok = n_tok; a.H = heads; a.tok_pos = tok_pos; a.tok_seq = tok_seq;
   a.cos_tab = cos_tab; a.sin_tab = sin_tab; a.kc = (bf16*)k_cache; a.vc = (bf16*)v_cache;
   a.max_ctx = max_ctx; a.scale_log2 = scale_log2; a.lora = lora; a.pf = pf;
-  const char* e = getenv("SLX_ATTN_PF_EARLY");
-  a.pf_early = (e && e[0] == '1') ? 1 : 0;
-  const char* ed = getenv("SLX_ATTN_DBG_STREAM");
-  a.dbg_stream = ed ? atoi(ed) : 0;   // 2: skip the LoRA math, 3: B rows not staged
   a.trace = next_trace_window(5);
   const int items = n_tok * heads;
   const int grid = items < sm_count() ? items : sm_count();
@@ -658,18 +541,14 @@ int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int
     cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return launch_ex(kernel, dim3((unsigned)grid), dim3(AD_THREADS), smem, stream, 1u, a);
   };
-  if (env_int("SLX_ATTN_MMA", 1)) {
-    const int rows = (int)n_pool_rows;
-    if ((head_dim == 128 || head_dim == 64) && n_pool_rows > 0 && n_pool_rows < (1LL << 31) &&
-        make_tmap(&a.tmk, k_cache, rows, head_dim, head_dim, 64) &&
-        make_tmap(&a.tmv, v_cache, rows, head_dim, head_dim, 64)) {
-      if (head_dim == 128) return go(attn_decode_pipe_kernel<128, 64, true>, ad_smem<128, 64>());
-      return go(attn_decode_pipe_kernel<64, 64, true>, ad_smem<64, 64>());
-    }
-  }
-  if (head_dim == 128) return go(attn_decode_pipe_kernel<128, 64, false>, ad_smem<128, 64>());
-  if (head_dim == 64) return go(attn_decode_pipe_kernel<64, 128, false>, ad_smem<64, 128>());
-  return SLX_ERR_UNSUPPORTED;
+  const int rows = (int)n_pool_rows;
+  if ((head_dim != 128 && head_dim != 64) || n_pool_rows <= 0 || n_pool_rows >= (1LL << 31))
+    return SLX_ERR_UNSUPPORTED;
+  if (!make_tmap(&a.tmk, k_cache, rows, head_dim, head_dim, 64) ||
+      !make_tmap(&a.tmv, v_cache, rows, head_dim, head_dim, 64))
+    return SLX_ERR_CUDA;
+  if (head_dim == 128) return go(attn_decode_pipe_kernel<128, 64>, ad_smem<128, 64>());
+  return go(attn_decode_pipe_kernel<64, 64>, ad_smem<64, 64>());
 }
 
 }  // namespace slx

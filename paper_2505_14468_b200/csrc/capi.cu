@@ -22,14 +22,6 @@ int sm_count() {
   }
   return n;
 }
-bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SLX_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
 }  // namespace slx
 
 using namespace slx;

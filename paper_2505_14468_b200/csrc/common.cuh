@@ -4,7 +4,6 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 #include <utility>
 
@@ -108,6 +107,7 @@ struct DeltaArgs {
   const int32_t* slot_rank;
   const float* slot_scale;
   int max_rank, n_targets;
+  int v_slot_stride;   // v column of (target i, slot s, j) = v_col_off[i] + s * v_slot_stride + j
   const uint64_t* b_ptrs[SLX_LORA_MAX_TARGETS];
   int v_col_off[SLX_LORA_MAX_TARGETS], y_col_off[SLX_LORA_MAX_TARGETS], d_out[SLX_LORA_MAX_TARGETS];
 };
@@ -116,6 +116,7 @@ inline DeltaArgs delta_args(const slx_lora_delta* d) {
   if (d == nullptr) return a;
   a.v = d->v; a.ldv = d->ldv; a.tok_slot = d->tok_slot; a.slot_rank = d->slot_rank;
   a.slot_scale = d->slot_scale; a.max_rank = d->max_rank; a.n_targets = d->n_targets;
+  a.v_slot_stride = d->v_slot_stride;
   for (int i = 0; i < SLX_LORA_MAX_TARGETS; ++i) {
     a.b_ptrs[i] = i < d->n_targets ? d->b_ptrs[i] : nullptr;
     a.v_col_off[i] = d->v_col_off[i]; a.y_col_off[i] = d->y_col_off[i]; a.d_out[i] = d->d_out[i];
@@ -130,6 +131,7 @@ inline bool delta_valid(const slx_lora_delta* d, bool v_optional = false) {
     return false;
   // 16-byte v / B vectors: ldv, offsets, max_rank multiples of 4 / 8; v 16-byte aligned
   if (d->ldv % 4 || d->max_rank % 8 || (reinterpret_cast<uintptr_t>(d->v) & 15)) return false;
+  if (d->v_slot_stride < 0 || d->v_slot_stride % 4) return false;
   for (int i = 0; i < d->n_targets; ++i)
     if (!d->b_ptrs[i] || d->d_out[i] <= 0 || d->y_col_off[i] < 0 || d->v_col_off[i] < 0 ||
         d->v_col_off[i] % 4)
@@ -155,10 +157,10 @@ __device__ __forceinline__ DeltaTok delta_tok(const DeltaArgs& d, int t) {
 }
 // LoRA delta of row column `col` (0 when no target covers it / no adapter).
 __device__ __forceinline__ float delta_dot(const DeltaTok& k, const uint64_t* b_tab, int v_off, int n,
-                                           int max_rank) {
+                                           int v_slot_stride) {
   const bf16* B = reinterpret_cast<const bf16*>(b_tab[k.slot]);
   if (B == nullptr) return 0.f;
-  const float* vr = k.vrow + v_off + k.slot * max_rank;
+  const float* vr = k.vrow + v_off + k.slot * v_slot_stride;
   const bf16* br = B + (size_t)n * k.rank;   // rank % 8 == 0 (pool invariant): 16 B rows
   float acc = 0.f;
   for (int j = 0; j < k.rank; j += 8) {
@@ -197,7 +199,7 @@ __device__ __forceinline__ void delta_prefetch(const DeltaArgs& d, const DeltaTo
   }
 }
 constexpr int DELTA_VS = SLX_LORA_MAX_TARGETS * 64;   // staged floats (rank <= 64)
-// vs[i * 64 + j] = v[t, v_col_off[i] + slot * max_rank + j] * scale  (j < rank), cooperative.
+// vs[i * 64 + j] = v[t, v_col_off[i] + slot * v_slot_stride + j] * scale  (j < rank), cooperative.
 __device__ __forceinline__ void delta_stage_v(const DeltaArgs& d, const DeltaTok& k, float* vs,
                                               int tid, int nthreads) {
   if (k.slot < 0 || k.rank == 0) return;
@@ -207,7 +209,7 @@ __device__ __forceinline__ void delta_stage_v(const DeltaArgs& d, const DeltaTok
 #pragma unroll
     for (int q = 0; q < SLX_LORA_MAX_TARGETS; ++q)
       if (q == i) off = d.v_col_off[q];
-    if (j < k.rank) vs[e] = k.vrow[off + k.slot * d.max_rank + j] * k.scale;
+    if (j < k.rank) vs[e] = k.vrow[off + k.slot * d.v_slot_stride + j] * k.scale;
   }
 }
 // delta = sum_j vs[j] * B[j], sequential fmaf (bit-identical to delta_col)
@@ -240,7 +242,7 @@ __device__ __forceinline__ float delta_col(const DeltaArgs& d, const DeltaTok& k
     const int n = col - d.y_col_off[i];
     if (!hit && i < d.n_targets && n >= 0 && n < d.d_out[i]) {
       hit = true;
-      res = delta_dot(k, d.b_ptrs[i], d.v_col_off[i], n, d.max_rank);
+      res = delta_dot(k, d.b_ptrs[i], d.v_col_off[i], n, d.v_slot_stride);
     }
   }
   return res;
@@ -252,7 +254,6 @@ namespace slx {
 struct PfArgs {
   const char* ptr[2];
   unsigned long long bytes[2];
-  int evict_last;   // SLX_PF_EVICT_LAST (debug / tuning): prefetch with an evict_last policy
   // stream-K window of the next decode GEMM (slx_l2_prefetch.gemm_w): weight base, k-blocks,
   // units, CTAs, 128-row blocks, unit window [u0, u0 + m) of every CTA's range
   const char* gw;
@@ -263,8 +264,6 @@ bool sk_partition(int M, int N, int K, int* kblocks, int* units, int* ctas);
 inline PfArgs pf_args(const slx_l2_prefetch* p) {
   PfArgs a{};
   if (p == nullptr) return a;
-  const char* e = getenv("SLX_PF_EVICT_LAST");
-  a.evict_last = (e && e[0] == '1') ? 1 : 0;
   for (int i = 0; i < 2; ++i) {
     a.ptr[i] = static_cast<const char*>(p->ptr[i]);
     a.bytes[i] = p->ptr[i] ? (p->bytes[i] & ~15ull) : 0;
@@ -305,11 +304,8 @@ __device__ __forceinline__ void l2_prefetch_part(const PfArgs& pf, int part, int
     const unsigned long long per = ((n + parts - 1) / parts + 15) & ~15ull;
     unsigned long long lo = per * part, hi = lo + per;
     hi = hi > n ? n : hi;
-    uint64_t pol;   // evict_last: keep the prefetched lines until the next kernel streams them
-    if (pf.evict_last)
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    else
-      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
     for (unsigned long long o = lo; o < hi; o += 65536) {
       const unsigned sz = (unsigned)((hi - o) < 65536 ? (hi - o) : 65536);
       asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(pf.ptr[r] + o),
@@ -388,7 +384,6 @@ __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-bool pdl_enabled();  // SLX_PDL=0 disables (debug)
 
 template <typename... KArgs, typename... Args>
 inline int launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -400,11 +395,9 @@ inline int launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.stream = stream;
   cudaLaunchAttribute attrs[2];
   unsigned n = 0;
-  if (pdl_enabled()) {
-    attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attrs[n].val.programmaticStreamSerializationAllowed = 1;
-    ++n;
-  }
+  attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[n].val.programmaticStreamSerializationAllowed = 1;
+  ++n;
   if (cluster_x > 1) {
     attrs[n].id = cudaLaunchAttributeClusterDimension;
     attrs[n].val.clusterDim.x = cluster_x;

@@ -10,12 +10,12 @@ namespace slx {
 // K-major bf16 matrix [rows, cols] with row stride ld (elements); TMA box = box_rows x 64,
 // SWIZZLE_128B (the tcgen05 smem descriptor layout).
 bool make_tmap(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, int box_rows);
-int env_int(const char* name, int dflt);
 // Max dynamic smem opt-in + smem-heavy carveout for a kernel (idempotent).
 void configure_kernel(const void* k);
 
 // Stream-K decode GEMM (gemm_sk.cu).  Returns SLX_ERR_UNSUPPORTED when the shape is outside
-// its envelope (M > 64, row-major W, workspace too small), so the caller can use gemm_tc.
+// its envelope (M > 64, row-major W, workspace too small, tuning->tile_kernel), so the caller
+// can use gemm_tc.
 struct SkCall {
   const void* A; int lda; const void* W; void* C; int ldc; int c_dtype;
   const void* R; int ldr; int M, N, K, epilogue, n_main; void* C2; int ldc2;
@@ -24,8 +24,7 @@ struct SkCall {
   float* part_out;    // slx_gemm_bf16_splitk: pieces out (no epilogue), `splits` per tile
   int splits;
   size_t part_bytes;
-  const slx_norm_in* norm;   // slx_gemm_bf16_norm: fused input RMSNorm prologue (A = norm->h)
-  const slx_row_ss* rss = nullptr;   // slx_gemm_bf16_rss: row sums of squares out / row scales in
+  const slx_gemm_tuning* tuning;   // explicit tiling (tests / tools); nullptr = planner
 };
 int gemm_sk_launch(const SkCall& c);
 // Debug timeline window for the next traced launch (nullptr when tracing is off); kinds:

@@ -25,7 +25,6 @@
 // Replaces the modelled decode step of the reference (engine.py:888,909 decode_ms_per_token;
 // batching.py:17-21) with the real projections of the decode step.
 #include <cuda.h>
-#include <stdio.h>
 
 #include "common.cuh"
 #include "gemm_host.h"
@@ -44,10 +43,7 @@ constexpr int SK_PB = 8;                        // pieces loaded per batch in th
 constexpr int SK_WBOX = 128 * SK_BK * 2;        // one contiguous 16 KB weight box
 constexpr size_t SK_CNT_BYTES = 32 * 1024;      // counters at the head of ws: 2 u32 per tile
 constexpr size_t SK_PART_OFF = 64 * 1024;       // partials (gemm_tc's counters sit in [32K, 64K))
-// fused input-norm prologue scratch: h_ready mbarrier, epoch, per-thread ss, staged LoRA v
-constexpr int SK_NORM_VMAX = 16;
-constexpr size_t SK_NORM_BYTES = 16 + 128 * 4 + SK_MAX_M * SK_NORM_VMAX * 4;
-constexpr size_t SK_BAR_BYTES = (2 * SK_MAX_STAGES + 4) * 8 + 16 + 4 * SK_MAX_SEGS + SK_NORM_BYTES;
+constexpr size_t SK_BAR_BYTES = (2 * SK_MAX_STAGES + 4) * 8 + 16 + 4 * SK_MAX_SEGS + 16;
 
 struct SkArgs {
   int M, N, bm, stages, kblocks, n_tiles, G, pmax;
@@ -66,28 +62,6 @@ struct SkArgs {
   unsigned long long* trace;
   PfArgs pf;     // L2 prefetch of the next kernel's first bytes, after our last TMA issue
   int part_only; // slx_gemm_bf16_splitk: every piece written to `part`, reduced by the consumer
-  // fused input RMSNorm (slx_gemm_bf16_norm): the epilogue warps build the A operand
-  // h = rmsnorm(x + split-K pieces + LoRA delta) across all CTAs (two grid barriers) while the
-  // producer is already streaming the first weight stages
-  bf16* nx;          // residual stream [M, ldnx] (nullptr: no prologue)
-  int ldnx, nd;
-  const bf16* nw;
-  float neps;
-  SplitArgs nsk;
-  DeltaArgs nlora;
-  bf16* nh;
-  int ldnh;
-  float* nss;        // [M][G] partial sums of squares
-  uint32_t* nbar;    // [2] grid-barrier counters of this call site (monotonic)
-  // row RMS (slx_gemm_bf16_rss): producer side writes the sum of squares of every stored
-  // 16-column chunk of C (bf16-rounded, main columns) to ss_out[m * ss_ld + n / 16]; consumer
-  // side scales row m of the accumulator by rsqrt(sum(ss_in[m * ss_n ..]) / ss_d + ss_eps)
-  // before the epilogue (the RMSNorm of its A operand, whose weight is folded into W)
-  float* ss_out;
-  int ss_ld;
-  const float* ss_in;
-  int ss_n, ss_d;
-  float ss_eps;
 };
 
 __device__ __forceinline__ unsigned long long sk_timer() {
@@ -133,12 +107,7 @@ __device__ __forceinline__ void sk_load_res(const SkArgs& g, int m, int n, int l
 
 // Final values of 16 columns [n, n+16) of row m (not SiLU): side output or C (+ residual).
 template <int EPI, typename OutT>
-__device__ __forceinline__ void sk_finish(const SkArgs& g, int m, int n, float* v, const float* res,
-                                          float rsc = 1.f) {
-  if (rsc != 1.f) {
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] *= rsc;
-  }
+__device__ __forceinline__ void sk_finish(const SkArgs& g, int m, int n, float* v, const float* res) {
   if (g.C2 != nullptr && n >= g.n_main) {
     float* row = g.C2 + (size_t)m * g.ldc2 + (n - g.n_main);
     if (n + 16 <= g.N) {
@@ -157,177 +126,14 @@ __device__ __forceinline__ void sk_finish(const SkArgs& g, int m, int n, float* 
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] += res[j];
   }
-  if (g.ss_out != nullptr) {   // sum of squares of the values as stored
-    float ss = 0.f;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float y = to_f32(from_f32<OutT>(v[j]));
-      ss = n + j < lim ? fmaf(y, y, ss) : ss;
-    }
-    g.ss_out[(size_t)m * g.ss_ld + n / 16] = ss;
-  }
   sk_store16(reinterpret_cast<OutT*>(g.C) + (size_t)m * g.ldc, n, lim, v);
-}
-
-// Row scales of the consumer side (epilogue threads; rows < M): 1 / sqrt(mean of squares + eps)
-// from the producer's chunk partials, summed in a fixed order (deterministic).
-__device__ __forceinline__ void sk_row_scales(const SkArgs& g, int et, float* srow) {
-  if (et < g.M) {
-    const float* p = g.ss_in + (size_t)et * g.ss_n;
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    int i = 0;
-    for (; i + 8 <= g.ss_n; i += 8) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] += __ldcg(p + i + j);
-    }
-    for (; i < g.ss_n; ++i) acc[0] += __ldcg(p + i);
-    const float tot = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-    srow[et] = 1.0f / sqrtf(tot / (float)g.ss_d + g.ss_eps);
-  }
-  tc::named_bar_sync(1, 128);
 }
 
 // fast-math SiLU: no IEEE-division slow path (whose per-element branch serialises the epilogue)
 __device__ __forceinline__ float sk_silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
-// Grid-wide barrier over the G co-resident CTAs of this launch on a monotonic counter: returns
-// once all G arrived (one thread per CTA calls it after a CTA-level sync of its writers).
-__device__ __forceinline__ void sk_grid_barrier(uint32_t* ctr, int G) {
-  __threadfence();
-  const uint32_t old = atomicAdd(ctr, 1u);
-  const uint32_t target = (old / (uint32_t)G + 1u) * (uint32_t)G;
-  while ((int)(tc::ld_acquire_gpu(ctr) - target) < 0) __nanosleep(32);
-}
-
-// Fused input RMSNorm, run by the 128 epilogue threads of every CTA before the mainloop needs
-// its A operand:
-//   phase A  x[m, slice] = round(x + sum of split-K pieces) (+ round LoRA delta), written back;
-//            per-row partial sum of squares of the slice -> nss[m][c]
-//   barrier  all CTAs
-//   phase B  h[m, slice] = x * rsqrt(sum_c nss[m][c] / d + eps) * w   (fixed order over c)
-//   barrier  all CTAs -> h_ready (the producer starts the X loads)
-// Slices: CTA c owns columns [c*SW, c*SW + SW), SW = ceil(d / G) rounded up to 8.
-__device__ __noinline__ void norm_prologue(const SkArgs& g, int c, int et, float* n_ss,
-                                           float* n_sv, uint64_t* h_ready) {
-  const int d = g.nd, G = g.G, M = g.M;
-  const int SW = ((d + G - 1) / G + 7) / 8 * 8;
-  const int c0 = min(d, c * SW), c1 = min(d, c0 + SW);
-  const int ng = (c1 - c0) / 8;
-  const int m = et >> 1, half = et & 1;   // 2 threads per row (M <= 64)
-  const bool live = m < M;
-  const DeltaArgs& lo = g.nlora;
-  // LoRA v of every row's adapter (o projection: one target), v from the pieces or lo.v
-  DeltaTok dt{-1, 0, 0.f, nullptr};
-  if (live) dt = delta_tok(lo, m);
-  if (live && dt.slot >= 0 && dt.rank > 0) {
-    for (int j = half; j < dt.rank; j += 2) {
-      const int col = lo.v_col_off[0] + dt.slot * lo.max_rank + j;
-      const float v = lo.v ? dt.vrow[col] : split_sum1(g.nsk, m, g.nsk.n_main + col);
-      n_sv[m * SK_NORM_VMAX + j] = v * dt.scale;
-    }
-  }
-  tc::named_bar_sync(1, 128);
-  if (et == 0) SK_TR(10);
-  // phase A
-  float ss = 0.f;
-  if (live) {
-    bf16* xr = g.nx + (size_t)m * g.ldnx;
-    const bf16* B = (dt.slot >= 0 && dt.rank > 0) ? reinterpret_cast<const bf16*>(lo.b_ptrs[0][dt.slot])
-                                                  : nullptr;
-    for (int q = half; q < ng; q += 2) {
-      const int col = c0 + q * 8;
-      float f[8];
-      Vec8<bf16>::load(xr + col, f);
-      if (g.nsk.part != nullptr) {
-        float ps[8];
-        split_sum8(g.nsk, m, col, ps);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = __bfloat162float(__float2bfloat16_rn(f[e] + ps[e]));
-      }
-      if (B != nullptr) {   // sequential fmaf over the rank: bit-identical to slx_lora_expand
-        const float* sv = n_sv + m * SK_NORM_VMAX;
-        uint4 bq[8][2];     // the 8 columns' B rows (rank <= 16), all loads in flight
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const uint4* br = reinterpret_cast<const uint4*>(B + (size_t)(col + e - lo.y_col_off[0]) * dt.rank);
-          bq[e][0] = __ldg(br);
-          bq[e][1] = dt.rank > 8 ? __ldg(br + 1) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          float acc = 0.f;
-#pragma unroll
-          for (int h2 = 0; h2 < 2; ++h2) {
-            if (h2 * 8 < dt.rank) {
-              const uint32_t wv[4] = {bq[e][h2].x, bq[e][h2].y, bq[e][h2].z, bq[e][h2].w};
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                acc = fmaf(sv[h2 * 8 + 2 * u], __uint_as_float(wv[u] << 16), acc);
-                acc = fmaf(sv[h2 * 8 + 2 * u + 1], __uint_as_float(wv[u] & 0xffff0000u), acc);
-              }
-            }
-          }
-          f[e] = __bfloat162float(__float2bfloat16_rn(f[e] + acc));
-        }
-      }
-      Vec8<bf16>::store(xr + col, f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) ss += f[e] * f[e];
-    }
-  }
-  n_ss[et] = ss;
-  tc::named_bar_sync(1, 128);
-  if (live && half == 0) g.nss[(size_t)m * G + c] = n_ss[et] + n_ss[et + 1];
-  tc::named_bar_sync(1, 128);
-  if (et == 0) SK_TR(11);
-  if (et == 0) sk_grid_barrier(&g.nbar[0], G);
-  tc::named_bar_sync(1, 128);
-  if (et == 0) SK_TR(12);
-  // phase B
-  // row totals: each of the row's 2 threads sums half of the G partials (16 loads in flight),
-  // combined in a fixed order through shared memory
-  {
-    float tot = 0.f;
-    if (live) {
-      const float* sp = g.nss + (size_t)m * G;
-      const int h0 = half * ((G + 1) / 2), h1 = half ? G : (G + 1) / 2;
-      for (int q0 = h0; q0 < h1; q0 += 16) {
-        float v[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) v[u] = q0 + u < h1 ? __ldcg(sp + q0 + u) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 16; ++u) tot += v[u];
-      }
-    }
-    n_ss[et] = tot;
-  }
-  tc::named_bar_sync(1, 128);
-  if (live) {
-    const float tot = n_ss[2 * m] + n_ss[2 * m + 1];
-    const float inv = 1.0f / sqrtf(tot / (float)d + g.neps);
-    const bf16* xr = g.nx + (size_t)m * g.ldnx;
-    bf16* hr = g.nh + (size_t)m * g.ldnh;
-    for (int q = half; q < ng; q += 2) {
-      const int col = c0 + q * 8;
-      float f[8], w8[8];
-      Vec8<bf16>::load(xr + col, f);
-      Vec8<bf16>::load(g.nw + col, w8);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = (f[e] * inv) * w8[e];
-      Vec8<bf16>::store(hr + col, f);
-    }
-  }
-  tc::named_bar_sync(1, 128);
-  if (et == 0) {
-    SK_TR(13);
-    sk_grid_barrier(&g.nbar[1], G);
-    SK_TR(14);
-    tc::mbar_arrive(h_ready);
-  }
-}
-
 // PO (part only, slx_gemm_bf16_splitk): every segment is written as an fp32 piece and nothing
-// else — the reduction, cluster, norm-prologue and direct-epilogue code is compiled out, which
+// else — the reduction, cluster and direct-epilogue code is compiled out, which
 // keeps the register footprint small enough for the consumer's CTAs to co-reside under PDL.
 template <int EPI, typename OutT, bool PO = false>
 __global__ void __launch_bounds__(SK_THREADS, 1)
@@ -342,9 +148,6 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   uint64_t* tfull = empty + SK_MAX_STAGES;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;              // [2] accumulator drained
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  uint64_t* h_ready = reinterpret_cast<uint64_t*>(tmem_slot + 4 + SK_MAX_SEGS + (SK_MAX_SEGS & 1));
-  float* n_ss = reinterpret_cast<float*>(h_ready + 2);           // [128]
-  float* n_sv = n_ss + 128;                                      // [SK_MAX_M][SK_NORM_VMAX]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x;
@@ -365,7 +168,6 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       tc::mbar_init(&tfull[a], 1);
       tc::mbar_init(&tempty[a], 1);
     }
-    tc::mbar_init(h_ready, 1);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * SK_BN);
@@ -403,10 +205,6 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       }
       pdl_wait();
       pdl_trigger();
-      if (g.nx != nullptr) {   // A operand built by this grid's prologue
-        tc::mbar_wait(h_ready, 0);
-        asm volatile("fence.proxy.async.global;" ::: "memory");   // generic stores -> TMA reads
-      }
       SK_TR(2);
       for (int i = 0; i < npre; ++i) load_x(i, smem + i * stage_bytes, &full[i]);
       for (int i = npre; i < n_units; ++i) {
@@ -466,8 +264,6 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     const int cs = g.cs, rank = c % cs, tile = c / cs;
     const int n_out = silu ? g.N / 2 : g.N;
     float* stg = reinterpret_cast<float*>(smem);
-    if (g.nx != nullptr) norm_prologue(g, c, et, n_ss, n_sv, h_ready);
-    if (g.ss_in != nullptr) sk_row_scales(g, et, n_ss);   // overlaps the mainloop
     tc::mbar_wait(&tfull[0], 0);
     if (et == 0) SK_TR(9);
     __syncwarp();
@@ -543,7 +339,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
         for (int e = 0; e < 16; ++e) a[e] = sk_silu(a[e]) * b[e];
         sk_store16(reinterpret_cast<OutT*>(g.C) + (size_t)m * g.ldc, tile * 128 + ch * 16, n_out, a);
       } else if (n < g.N) {
-        sk_finish<EPI, OutT>(g, m, n, a, res, g.ss_in ? n_ss[m] : 1.f);
+        sk_finish<EPI, OutT>(g, m, n, a, res);
       }
     }
     if (et == 0) SK_TR(8);
@@ -570,9 +366,6 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
         if (!(k0 == 0 && k1 == kb) && !PO) base[j] = tc::ld_relaxed_gpu(&g.cnt[2 * tile + 1]);
       }
     }
-
-    if (!PO && g.nx != nullptr) norm_prologue(g, c, et, n_ss, n_sv, h_ready);
-    if (!PO && g.ss_in != nullptr) sk_row_scales(g, et, n_ss);   // overlaps the mainloop
 
     // phase 1: drain every segment (direct epilogue for whole tiles, fp32 piece otherwise)
     int j = 0;
@@ -613,9 +406,8 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
                   sk_load_res<OutT>(g, m, n, lim, r0);
                   sk_load_res<OutT>(g, m, n + 16, lim, r1);
                 }
-                const float rsc = g.ss_in ? n_ss[m] : 1.f;
-                sk_finish<EPI, OutT>(g, m, n, v0, r0, rsc);
-                if (n + 16 < g.N) sk_finish<EPI, OutT>(g, m, n + 16, v1, r1, rsc);
+                sk_finish<EPI, OutT>(g, m, n, v0, r0);
+                if (n + 16 < g.N) sk_finish<EPI, OutT>(g, m, n + 16, v1, r1);
               }
             }
           }
@@ -730,7 +522,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
           for (int e = 0; e < 16; ++e) a[e] = sk_silu(a[e]) * b[e];
           sk_store16(reinterpret_cast<OutT*>(g.C) + (size_t)m * g.ldc, tile * 128 + ch * 16, n_out, a);
         } else if (n < g.N) {
-          sk_finish<EPI, OutT>(g, m, n, a, res, g.ss_in ? n_ss[m] : 1.f);
+          sk_finish<EPI, OutT>(g, m, n, a, res);
         }
       }
       if (et == 0 && dbg_t == 0) SK_TR(13);
@@ -763,7 +555,7 @@ struct SkPlan {
 
 int sk_max_clusters(size_t smem, int cluster);
 
-bool sk_plan(int M, int N, int K, SkPlan* p) {
+bool sk_plan(int M, int N, int K, SkPlan* p, const slx_gemm_tuning* tu) {
   if (M <= 0 || M > SK_MAX_M) return false;
   p->bm = (M + 15) / 16 * 16;
   p->kblocks = ceil_div(K, SK_BK);
@@ -776,7 +568,7 @@ bool sk_plan(int M, int N, int K, SkPlan* p) {
   // reduction at all; measured (tools/gemm_bench.py) to beat an all-SM stream-K grid with uneven
   // pieces.  More tiles than SMs: plain stream-K over all SMs.
   const int sms = sm_count();
-  const int min_units = env_int("SLX_SK_MIN_UNITS", 4);
+  const int min_units = (tu && tu->sk_min_units > 0) ? tu->sk_min_units : 4;
   long long G;
   if (p->n_tiles <= sms) {
     int s = sms / p->n_tiles;
@@ -787,7 +579,7 @@ bool sk_plan(int M, int N, int K, SkPlan* p) {
     G = sms;
   }
   G = G < 1 ? 1 : G;
-  const int e_g = env_int("SLX_SK_CTAS", 0);
+  const int e_g = tu ? tu->sk_ctas : 0;
   if (e_g > 0) {
     G = p->U / (min_units > 0 ? min_units : 1);
     G = G < 1 ? 1 : (G > sms ? sms : G);
@@ -807,8 +599,6 @@ bool sk_plan(int M, int N, int K, SkPlan* p) {
   const size_t stage = (size_t)p->bm * SK_BK * 2 + 2 * SK_WBOX;
   int st = (int)((227 * 1024 - 1024 - SK_BAR_BYTES) / stage);
   st = st > SK_MAX_STAGES ? SK_MAX_STAGES : st;
-  const int e_st = env_int("SLX_SK_STAGES", 0);
-  if (e_st >= 2 && e_st < st) st = e_st;
   p->stages = st;
   p->smem = (size_t)st * stage + SK_BAR_BYTES + 1024;
   p->ws = SK_PART_OFF + (size_t)p->n_tiles * pmax * p->bm * SK_BN * 4;
@@ -816,7 +606,7 @@ bool sk_plan(int M, int N, int K, SkPlan* p) {
   // cluster of s when all n_tiles clusters are co-resident and the staged piece fits the
   // pipeline smem.
   const int s_split = p->G / p->n_tiles;
-  if (env_int("SLX_SK_CLUSTER", 1) && s_split >= 2 && s_split <= 8 &&
+  if (!(tu && tu->sk_no_cluster) && s_split >= 2 && s_split <= 8 &&
       p->G == p->n_tiles * s_split && (size_t)p->bm * SK_BN * 4 <= (size_t)st * stage &&
       sk_max_clusters(p->smem, s_split) >= p->n_tiles) {
     p->cs = s_split;
@@ -875,26 +665,23 @@ size_t gemm_sk_splitk_bytes(int M, int N, int splits) {
 
 size_t gemm_sk_workspace_bytes(int M, int N, int K) {
   SkPlan p{};
-  return sk_plan(M, N, K, &p) ? p.ws : 0;
+  return sk_plan(M, N, K, &p, nullptr) ? p.ws : 0;
 }
 
 int gemm_sk_launch(const SkCall& c) {
   SkPlan p{};
   if (c.part_out != nullptr) {
     // split-K pieces for the consumer: G = n_tiles * splits, every CTA exactly one piece
-    if (!sk_plan(c.M, c.N, c.K, &p)) return SLX_ERR_UNSUPPORTED;
+    if (!sk_plan(c.M, c.N, c.K, &p, nullptr)) return SLX_ERR_UNSUPPORTED;
     if (c.splits < 1 || c.splits > 16 || p.kblocks / c.splits < 1) return SLX_ERR_INVALID;
     p.G = p.n_tiles * c.splits;
     p.pmax = c.splits;
     p.cs = 1;
     if ((size_t)p.n_tiles * c.splits * p.bm * SK_BN * 4 > c.part_bytes) return SLX_ERR_WORKSPACE;
   } else {
-    if (env_int("SLX_GEMM_SK", 1) == 0 || c.ws == nullptr) return SLX_ERR_UNSUPPORTED;
-    if (!sk_plan(c.M, c.N, c.K, &p) || p.ws > c.ws_bytes) return SLX_ERR_UNSUPPORTED;
+    if ((c.tuning && c.tuning->tile_kernel) || c.ws == nullptr) return SLX_ERR_UNSUPPORTED;
+    if (!sk_plan(c.M, c.N, c.K, &p, c.tuning) || p.ws > c.ws_bytes) return SLX_ERR_UNSUPPORTED;
   }
-  if (env_int("SLX_GEMM_DEBUG", 0))
-    fprintf(stderr, "[slx_gemm_sk] M=%d N=%d K=%d epi=%d bm=%d stages=%d G=%d tiles=%d kb=%d pmax=%d cluster=%d\n",
-            c.M, c.N, c.K, c.epilogue, p.bm, p.stages, p.G, p.n_tiles, p.kblocks, p.pmax, p.cs);
   SkArgs a{};
   a.M = c.M; a.N = c.N; a.bm = p.bm; a.stages = p.stages; a.kblocks = p.kblocks;
   a.n_tiles = p.n_tiles; a.G = p.G; a.pmax = p.pmax; a.U = (int)p.U; a.cs = p.cs;
@@ -906,18 +693,6 @@ int gemm_sk_launch(const SkCall& c) {
   if (c.part_out != nullptr) {
     a.part = c.part_out;
     a.part_only = 1;
-  }
-  if (c.norm != nullptr) {
-    const slx_norm_in& n = *c.norm;
-    a.nx = (bf16*)n.x; a.ldnx = n.ldx; a.nd = c.K; a.nw = (const bf16*)n.w; a.neps = n.eps;
-    a.nsk = split_args(n.sk);
-    a.nlora = delta_args(n.lora);
-    a.nh = (bf16*)c.A; a.ldnh = c.lda;
-    a.nss = n.ss; a.nbar = n.bar;
-  }
-  if (c.rss != nullptr) {
-    a.ss_out = c.rss->ss_out; a.ss_ld = c.rss->ss_out_ld;
-    a.ss_in = c.rss->ss_in; a.ss_n = c.rss->ss_in_n; a.ss_d = c.rss->d; a.ss_eps = c.rss->eps;
   }
   a.trace = c.trace;
   a.pf = pf_args(c.pf);
@@ -945,7 +720,7 @@ int gemm_sk_launch(const SkCall& c) {
 
 bool sk_partition(int M, int N, int K, int* kblocks, int* units, int* ctas) {
   SkPlan p;
-  if (env_int("SLX_GEMM_SK", 1) == 0 || !sk_plan(M, N, K, &p)) return false;
+  if (!sk_plan(M, N, K, &p, nullptr)) return false;
   *kblocks = p.kblocks;
   *units = (int)p.U;
   *ctas = p.G;

@@ -23,8 +23,6 @@
 // Replaces the modelled prefill/decode time of the reference (batching.py:17-21 T0+alpha(b-1);
 // engine.py:832 prefill work, engine.py:888,909 decode_ms_per_token) with the real projections.
 #include <cuda.h>
-#include <stdio.h>
-#include <stdlib.h>
 
 #include "common.cuh"
 #include "gemm_host.h"
@@ -495,11 +493,6 @@ bool make_tmap(CUtensorMap* map, const void* ptr, int rows, int cols, int ld, in
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return (e && *e) ? atoi(e) : dflt;
-}
-
 void configure_kernel(const void* k) {
   cudaFuncAttributes fa{};
   cudaFuncGetAttributes(&fa, k);   // the opt-in limit counts static + dynamic shared memory
@@ -555,16 +548,17 @@ static int max_active_clusters(size_t smem, int cluster) {
 
 // Few tiles (decode): pick CTAs/SM (1 or 2) and the cluster split S that cover the most SMs
 // in ONE wave (cudaOccupancyMaxActiveClusters), every split keeping >= 4 k-blocks and its
-// partial tile fitting the pipeline smem.  SLX_GEMM_{CTAS,SPLITS,STAGES} override (tuning).
-static GemmPlan plan_gemm(int M, int N, int K, bool silu, size_t ws_bytes) {
+// partial tile fitting the pipeline smem.  An explicit slx_gemm_tuning overrides (tests).
+static GemmPlan plan_gemm(int M, int N, int K, bool silu, size_t ws_bytes,
+                          const slx_gemm_tuning* tu) {
   GemmPlan p{};
   p.kblocks = ceil_div(K, TC_BK);
   p.m_tiles = ceil_div(M, 128);
   p.bm = M >= 128 ? 128 : ((M + 15) / 16) * 16;
   const int sms = sm_count();
-  const int e_ctas = env_int("SLX_GEMM_CTAS", 0), e_s = env_int("SLX_GEMM_SPLITS", 0);
-  const int e_st = env_int("SLX_GEMM_STAGES", 0), e_bn = env_int("SLX_GEMM_BN", 0);
-  const int e_gs = env_int("SLX_GEMM_GSPLIT", -1);
+  const int e_ctas = tu ? tu->ctas_per_sm : 0, e_s = tu ? tu->splits : 0;
+  const int e_bn = tu ? tu->bn : 0;
+  const int e_gs = (tu && tu->gsplit) ? (tu->gsplit == 1 ? 1 : 0) : -1;
   double best = -1.0;
   for (int bn = 256; bn >= 128; bn -= 128) {
     if (silu && bn != 256) continue;
@@ -580,7 +574,6 @@ static GemmPlan plan_gemm(int M, int N, int K, bool silu, size_t ws_bytes) {
       const size_t budget = ctas == 2 ? 112 * 1024 - 1024 - BAR_BYTES : 225 * 1024 - 1024 - BAR_BYTES;
       int st = (int)(budget / stage);
       st = st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
-      if (e_st >= 2 && e_st < st) st = e_st;
       if (st < 2) continue;
       const size_t smem = (size_t)st * stage + BAR_BYTES + 1024;
       for (int gs = 0; gs <= 1; ++gs) {
@@ -701,49 +694,15 @@ extern "C" int slx_gemm_bf16(const void* A, int lda, const void* W, void* C, int
                              const void* R, int ldr, int M, int N, int K, int epilogue,
                              int w_layout, int n_main, void* C2, int ldc2, void* ws,
                              size_t ws_bytes, void* stream) {
-  return slx_gemm_bf16_pf(A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, w_layout, n_main,
-                          C2, ldc2, ws, ws_bytes, nullptr, stream);
+  return slx_gemm_bf16_ex(A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, w_layout, n_main,
+                          C2, ldc2, ws, ws_bytes, nullptr, nullptr, stream);
 }
 
-extern "C" int slx_gemm_bf16_rss(const void* A, int lda, const void* W, void* C, int ldc,
-                                 int c_dtype, const void* R, int ldr, int M, int N, int K,
-                                 int epilogue, int n_main, void* C2, int ldc2, void* ws,
-                                 size_t ws_bytes, const slx_row_ss* rss,
-                                 const slx_l2_prefetch* pf, void* stream) {
-  SLX_CHECK_ARG(rss != nullptr && A && W && C && M >= 0 && N > 0 && K > 0 && lda >= K &&
-                K % 8 == 0 && lda % 8 == 0 && ldc % 8 == 0 && ws != nullptr);
-  SLX_CHECK_ARG(epilogue == SLX_EPI_NONE || epilogue == SLX_EPI_RESIDUAL);
-  SLX_CHECK_ARG(c_dtype == SLX_DT_BF16 || c_dtype == SLX_DT_F32);
-  SLX_CHECK_ALIGN(A, 16);
-  SLX_CHECK_ALIGN(W, 16);
-  SLX_CHECK_ALIGN(C, 16);
-  SLX_CHECK_ALIGN(ws, 256);
-  if (C2 != nullptr) {
-    SLX_CHECK_ARG(n_main > 0 && n_main < N && n_main % 16 == 0 && ldc2 >= N - n_main &&
-                  ldc2 % 4 == 0 && ldc >= n_main);
-    SLX_CHECK_ALIGN(C2, 16);
-  } else {
-    SLX_CHECK_ARG(ldc >= N);
-    n_main = N;
-  }
-  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= n_main && ldr % 8 == 0);
-  if (rss->ss_out != nullptr)
-    SLX_CHECK_ARG(epilogue == SLX_EPI_RESIDUAL && c_dtype == SLX_DT_BF16 &&
-                  rss->ss_out_ld >= (n_main + 15) / 16);
-  if (rss->ss_in != nullptr) SLX_CHECK_ARG(rss->ss_in_n > 0 && rss->d > 0 && rss->eps >= 0.f);
-  if (M == 0) return SLX_OK;
-  if (M > 64) return SLX_ERR_UNSUPPORTED;
-  SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
-            ws, ws_bytes, stream, next_trace_window(1 + epilogue), pf, nullptr, 0, 0, nullptr};
-  sc.rss = rss;
-  return gemm_sk_launch(sc);
-}
-
-extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, int ldc,
+extern "C" int slx_gemm_bf16_ex(const void* A, int lda, const void* W, void* C, int ldc,
                                 int c_dtype, const void* R, int ldr, int M, int N, int K,
                                 int epilogue, int w_layout, int n_main, void* C2, int ldc2,
                                 void* ws, size_t ws_bytes, const slx_l2_prefetch* pf,
-                                void* stream) {
+                                const slx_gemm_tuning* tuning, void* stream) {
   SLX_CHECK_ARG(w_layout == SLX_W_ROWMAJOR || w_layout == SLX_W_TILED);
   SLX_CHECK_ARG(A && W && C && M >= 0 && N > 0 && K > 0 && lda >= K && K % 8 == 0 &&
                 lda % 8 == 0 && ldc % 8 == 0);
@@ -771,15 +730,11 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
   if (w_layout == SLX_W_TILED) {   // decode: stream-K kernel (gemm_sk.cu) when it applies
     SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
               ws, ws ? ws_bytes : 0, stream, next_trace_window(1 + epilogue), pf, nullptr, 0, 0,
-              nullptr};
+              tuning};
     const int st = gemm_sk_launch(sc);
     if (st != SLX_ERR_UNSUPPORTED) return st;
   }
-  GemmPlan p = plan_gemm(M, N, K, epilogue == SLX_EPI_SILU_MUL, ws ? ws_bytes : 0);
-  if (env_int("SLX_GEMM_DEBUG", 0))
-    fprintf(stderr, "[slx_gemm] M=%d N=%d K=%d epi=%d bn=%d bm=%d stages=%d splits=%d%s tiles=%dx%d smem=%zu\n",
-            M, N, K, epilogue, p.bn, p.bm, p.stages, p.splits, p.gsplit ? "(global)" : "",
-            p.n_tiles, p.m_tiles, p.smem);
+  GemmPlan p = plan_gemm(M, N, K, epilogue == SLX_EPI_SILU_MUL, ws ? ws_bytes : 0, tuning);
   GemmArgs a{};
   a.M = M; a.N = N; a.K = K;
   a.bm = p.bm; a.stages = p.stages; a.kblocks = p.kblocks; a.splits = p.splits;
@@ -802,7 +757,7 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
   if (!make_tmap(&mx, A, M, K, lda, p.bm) || !make_tmap(&mw, W, w_rows, w_cols, w_cols, 128))
     return SLX_ERR_CUDA;
   dim3 grid((unsigned)(p.n_tiles * p.splits), (unsigned)p.m_tiles);
-  const int raster = env_int("SLX_GEMM_RASTER", 16);   // measured best of {4, 8, 16}
+  constexpr int raster = 16;   // measured best of {4, 8, 16}
   if (p.splits == 1 && p.m_tiles > 1 && raster > 0) {
     a.raster = raster;
     a.m_tiles = p.m_tiles;
@@ -810,32 +765,6 @@ extern "C" int slx_gemm_bf16_pf(const void* A, int lda, const void* W, void* C, 
   }
   return dispatch_tc(epilogue, c_dtype, p.bn, mx, mw, a, grid, p.smem,
                      p.gsplit ? 1u : (unsigned)p.splits, (cudaStream_t)stream);
-}
-
-extern "C" int slx_gemm_bf16_norm(void* A, int lda, const void* W, void* C, int ldc, int c_dtype,
-                                  const void* R, int ldr, int M, int N, int K, int epilogue,
-                                  int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes,
-                                  const slx_norm_in* norm, const slx_l2_prefetch* pf,
-                                  void* stream) {
-  SLX_CHECK_ARG(norm && norm->x && norm->w && norm->ss && norm->bar && A && W && C && M > 0 &&
-                M <= 64 && N > 0 && K > 0 && K % 8 == 0 && lda >= K && lda % 8 == 0 &&
-                norm->ldx >= K && norm->ldx % 8 == 0 && norm->ss_bytes >= (size_t)M * 148 * 4);
-  SLX_CHECK_ARG(delta_valid(norm->lora, norm->sk != nullptr));
-  if (norm->lora && norm->lora->n_targets > 0)
-    SLX_CHECK_ARG(norm->lora->n_targets == 1 && norm->lora->max_rank <= 16 &&
-                  (norm->lora->v || norm->sk) && norm->lora->y_col_off[0] == 0 &&
-                  norm->lora->d_out[0] >= K);
-  if (norm->sk) SLX_CHECK_ARG(norm->sk->part && norm->sk->splits >= 1 && norm->sk->bm >= M &&
-                              norm->sk->n_main >= K);
-  SLX_CHECK_ALIGN(norm->x, 16);
-  SLX_CHECK_ALIGN(A, 16);
-  if (C2 == nullptr) n_main = N;
-  if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr >= n_main && ldr % 8 == 0);
-  SkCall sc{A, lda, W, C, ldc, c_dtype, R, ldr, M, N, K, epilogue, n_main, C2, ldc2,
-            ws, ws ? ws_bytes : 0, stream, next_trace_window(1 + epilogue), pf, nullptr, 0, 0,
-            norm};
-  const int st = gemm_sk_launch(sc);
-  return st == SLX_ERR_UNSUPPORTED ? SLX_ERR_UNSUPPORTED : st;
 }
 
 extern "C" size_t slx_gemm_splitk_bytes(int M, int N, int splits) {

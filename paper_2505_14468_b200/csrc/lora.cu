@@ -459,6 +459,99 @@ lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, 
 }
 
 
+// ---------------------------------------------------------------- gathered decode shrink
+// Large adapter pools (decode): instead of stacking every slot's A rows into the projection
+// GEMM (bytes grow with the pool), the shrink reads only the adapters present in the batch,
+// each ONCE per plan tile.  One cluster of KS CTAs per (tile, target): CTA q stages x[tile
+// tokens, k-chunk q] and A_s[:, k-chunk q] with one burst of cp.async, computes the partial
+// dot products (warp per output, shuffle reduce), and the cluster reduces the KS partials
+// through DSMEM in a fixed order (deterministic); CTA q writes outputs o = q, q + KS, ...
+//   v[t, v_col_off[tgt] + j] = x_t . A_{slot(t), tgt}[j]   (j < rank; unscaled)
+// The fused expands (slx_lora_delta with v_slot_stride = 0) consume v.
+struct ShrinkOut {
+  int v_off[SLX_LORA_MAX_TARGETS];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(FU_THREADS)
+lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, int ldx, int d_in,
+                     int ks, int kc, const int32_t* __restrict__ slot_rank, int max_rank,
+                     TargetArgs ta, ShrinkOut so, LoraWs ws) {
+  extern __shared__ __align__(16) uint8_t ssm[];
+  const int q = (int)tc::cluster_ctarank();
+  const int tile_id = blockIdx.x / ks;
+  const int tgt = blockIdx.y;
+  // plan (start of the step) and adapter pool (static): >= 2 launches back, read before the wait
+  const bool live = tile_id < *ws.n_tiles;   // uniform over the cluster
+  LoraTile tile{0, 0, 0, 0};
+  int rank = 0;
+  const bf16* A = nullptr;
+  const int k_lo = min(d_in, q * kc), k_hi = min(d_in, k_lo + kc);
+  const int kl = k_hi - k_lo;
+  // smem: xs [TT][kc] T | as [max_rank][kc] bf16 | vpart [TT][max_rank] f32 | toks [TT]
+  T* xs = reinterpret_cast<T*>(ssm);
+  bf16* as = reinterpret_cast<bf16*>(xs + (size_t)LORA_TT * kc);
+  float* vpart = reinterpret_cast<float*>(as + (size_t)max_rank * kc);
+  int* toks = reinterpret_cast<int*>(vpart + LORA_TT * max_rank);
+  if (live) {
+    tile = ws.tiles[tile_id];
+    rank = min(slot_rank[tile.slot], max_rank);
+    A = reinterpret_cast<const bf16*>(ta.a_ptrs[tgt][tile.slot]);
+    if (A == nullptr) rank = 0;   // the adapter does not target this projection
+    const int achunks = kl / 8;
+    for (int e = threadIdx.x; e < rank * achunks; e += FU_THREADS) {
+      const int j = e / achunks, c = e % achunks;
+      cp_async16(as + (size_t)j * kc + c * 8, A + (size_t)j * d_in + k_lo + c * 8);
+    }
+    if (threadIdx.x < LORA_TT)
+      toks[threadIdx.x] = threadIdx.x < tile.count ? ws.perm[tile.start + threadIdx.x] : 0;
+  }
+  pdl_wait();   // x comes from the kernel just before us
+  pdl_trigger();
+  if (!live) return;
+  __syncthreads();
+  const int cnt = tile.count;
+  constexpr int XV = 16 / sizeof(T);
+  const int xchunks = kl / XV;
+  for (int e = threadIdx.x; e < cnt * xchunks; e += FU_THREADS) {
+    const int i = e / xchunks, c = e % xchunks;
+    cp_async16(xs + (size_t)i * kc + c * XV, x + (size_t)toks[i] * ldx + k_lo + c * XV);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_out = cnt * rank;
+  for (int o = warp; o < n_out; o += FU_THREADS / 32) {
+    const int i = o / rank, j = o % rank;
+    const T* xr = xs + (size_t)i * kc;
+    const bf16* ar = as + (size_t)j * kc;
+    float acc = 0.f;
+    for (int k = lane * 8; k < kl; k += 32 * 8) {
+      float xf[8], af[8];
+      Vec8<T>::load(xr + k, xf);
+      Vec8<bf16>::load(ar + k, af);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc = fmaf(xf[e], af[e], acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) vpart[i * max_rank + j] = acc;
+  }
+  tc::cluster_sync();
+  const uint32_t vp_base = tc::smem_u32(vpart);
+  for (int o = q + ks * (int)threadIdx.x; o < n_out; o += ks * FU_THREADS) {
+    const int i = o / rank, j = o % rank;
+    const uint32_t off = vp_base + (uint32_t)((i * max_rank + j) * 4);
+    float part[FU_MAX_KS];
+#pragma unroll
+    for (int r = 0; r < FU_MAX_KS; ++r) part[r] = r < ks ? tc::ld_dsmem(tc::mapa(off, (uint32_t)r)) : 0.f;
+    float a = 0.f;
+#pragma unroll
+    for (int r = 0; r < FU_MAX_KS; ++r) a += part[r];   // fixed order: deterministic
+    v[(size_t)toks[i] * ldv + so.v_off[tgt] + j] = a;
+  }
+  tc::cluster_sync();   // keep our vpart alive until every peer has read it
+}
+
 // ---------------------------------------------------------------- decode expand (shrink in GEMM)
 // The decode shrink runs inside the projection GEMM (stacked A rows of every slot appended to
 // W, fp32 side output v_all); this kernel is the expand: CTA (tile, target, n-chunk) stages
@@ -758,6 +851,52 @@ extern "C" int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, i
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return launch_ex(k, grid, dim3(EX_THREADS), smem, s, 1u, (float*)y, ldy, (const float*)v_all, ldv,
                      slot_rank, slot_scale, max_rank, ta, ea, w);
+  }
+  return SLX_ERR_INVALID;
+}
+
+extern "C" int slx_lora_shrink(int dtype, float* v, int ldv, const void* x, int ldx, int n_tok,
+                               int d_in, const int32_t* slot_rank, int n_slots, int max_rank,
+                               int n_targets, const slx_lora_target* targets, const int* v_col_off,
+                               void* ws, size_t ws_bytes, void* stream) {
+  SLX_CHECK_ARG(n_tok >= 0 && d_in > 0 && d_in % 8 == 0 && ldx >= d_in && ldx % 8 == 0 &&
+                n_slots > 0 && max_rank > 0 && max_rank <= LORA_MAX_RANK && max_rank % 8 == 0 &&
+                n_targets >= 1 && n_targets <= SLX_LORA_MAX_TARGETS && targets && v_col_off &&
+                slot_rank && v && x && ldv > 0);
+  SLX_CHECK_ALIGN(x, 16);
+  TargetArgs ta{};
+  ShrinkOut so{};
+  for (int i = 0; i < n_targets; ++i) {
+    SLX_CHECK_ARG(targets[i].a_ptrs != nullptr && v_col_off[i] >= 0 && v_col_off[i] + max_rank <= ldv);
+    ta.a_ptrs[i] = targets[i].a_ptrs;
+    so.v_off[i] = v_col_off[i];
+  }
+  LoraWs w;
+  int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
+  if (st) return st;
+  if (n_tok == 0) return SLX_OK;
+  int ks = d_in / 512;
+  ks = ks < 1 ? 1 : (ks > FU_MAX_KS ? FU_MAX_KS : ks);
+  const int kc = ceil_div(ceil_div(d_in, ks), 8) * 8;
+  const size_t tsz = dtype == SLX_DT_BF16 ? 2 : 4;
+  const size_t smem = (size_t)LORA_TT * kc * tsz + (size_t)max_rank * kc * 2 +
+                      (size_t)LORA_TT * max_rank * 4 + LORA_TT * 4;
+  if (smem > 200 * 1024) return SLX_ERR_UNSUPPORTED;
+  dim3 grid((unsigned)(w.max_tiles * ks), (unsigned)n_targets);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == SLX_DT_BF16) {
+    auto k = lora_shrink_v_kernel<bf16>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SLX_ERR_CUDA;
+    return launch_ex(k, grid, dim3(FU_THREADS), smem, s, (unsigned)ks, v, ldv, (const bf16*)x, ldx,
+                     d_in, ks, kc, slot_rank, max_rank, ta, so, w);
+  }
+  if (dtype == SLX_DT_F32) {
+    auto k = lora_shrink_v_kernel<float>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SLX_ERR_CUDA;
+    return launch_ex(k, grid, dim3(FU_THREADS), smem, s, (unsigned)ks, v, ldv, (const float*)x, ldx,
+                     d_in, ks, kc, slot_rank, max_rank, ta, so, w);
   }
   return SLX_ERR_INVALID;
 }

@@ -17,11 +17,6 @@ int attn_decode_pipe_launch(void* out, int ldo, const void* qkv, int ld_qkv, int
                             const DeltaArgs& lora,
                             const PfArgs& pf, cudaStream_t stream);   // attn_decode.cu
 
-static bool attn_pipe_enabled() {   // SLX_ATTN_PIPE=0: the per-(token, head) kernel (A/B tests)
-  const char* e = getenv("SLX_ATTN_PIPE");
-  return !(e && e[0] == '0');
-}
-
 // ------------------------------------------------------------------ embedding
 template <typename T>
 __global__ void embedding_kernel(T* __restrict__ out, const bf16* __restrict__ table,
@@ -198,7 +193,7 @@ __global__ void __launch_bounds__(128) rmsnorm_lora_cluster_kernel(T* __restrict
 #pragma unroll
         for (int q = 0; q < SLX_LORA_MAX_TARGETS; ++q)
           if (q == i) off = lora.v_col_off[q];
-        if (j < dt.rank) vs[e] = split_sum1(sk, t, sk.n_main + off + dt.slot * lora.max_rank + j) * dt.scale;
+        if (j < dt.rank) vs[e] = split_sum1(sk, t, sk.n_main + off + dt.slot * lora.v_slot_stride + j) * dt.scale;
       }
     } else {
       delta_stage_v(lora, dt, vs, threadIdx.x, blockDim.x);
@@ -296,7 +291,7 @@ __global__ void __launch_bounds__(640) rmsnorm_fused_tok_kernel(T* __restrict__ 
 #pragma unroll
         for (int q = 0; q < SLX_LORA_MAX_TARGETS; ++q)
           if (q == i) off = lora.v_col_off[q];
-        if (j < dt.rank) vs[e] = split_sum1(sk, t, sk.n_main + off + dt.slot * lora.max_rank + j) * dt.scale;
+        if (j < dt.rank) vs[e] = split_sum1(sk, t, sk.n_main + off + dt.slot * lora.v_slot_stride + j) * dt.scale;
       }
     } else {
       delta_stage_v(lora, dt, vs, threadIdx.x, blockDim.x);
@@ -925,8 +920,7 @@ extern "C" int slx_rmsnorm_lora(int dtype, void* out, int ldo, void* x, int ldx,
   if (n_tok == 0) return SLX_OK;
   const DeltaArgs la = delta_args(lora);
   int st = SLX_OK;
-  const char* e = getenv("SLX_RMSNORM_CLUSTER");
-  if (d % (RNL_CL * 8 * 32) == 0 && d / (RNL_CL * 8) <= 128 && !(e && e[0] == '0')) {
+  if (d % (RNL_CL * 8 * 32) == 0 && d / (RNL_CL * 8) <= 128) {
     const int thr = d / (RNL_CL * 8);
     DISPATCH_DT(dtype, st = launch_ex(rmsnorm_lora_cluster_kernel<T>, dim3(n_tok * RNL_CL), dim3(thr), 0, (cudaStream_t)stream, (unsigned)RNL_CL, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, SplitArgs{}, PfArgs{}, next_trace_window(6)));
     return st;
@@ -957,11 +951,10 @@ extern "C" int slx_rmsnorm_fused(int dtype, void* out, int ldo, void* x, int ldx
   const SplitArgs sa = split_args(sk);
   const PfArgs pa = pf_args(pf);
   int st = SLX_OK;
-  const char* e = getenv("SLX_RMSNORM_CLUSTER");
-  // default: the 8-CTA cluster kernel (measured faster in the decode graph); SLX_RMSNORM_CLUSTER=0
-  // or a d the cluster split cannot take: one CTA per token
+  // the 8-CTA cluster kernel (measured faster in the decode graph); a d the cluster split cannot
+  // take: one CTA per token
   const bool cl_ok = d % (RNL_CL * 8 * 32) == 0 && d / (RNL_CL * 8) <= 128;
-  if ((!cl_ok || (e && e[0] == '0')) && d % 256 == 0 && d / 8 <= 640 && (!sk || sk->splits <= 8)) {
+  if (!cl_ok && d % 256 == 0 && d / 8 <= 640 && (!sk || sk->splits <= 8)) {
     DISPATCH_DT(dtype, st = launch_ex(rmsnorm_fused_tok_kernel<T>, dim3(n_tok), dim3(d / 8), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (T*)x, ldx, (const bf16*)w, d, eps, la, sa, pa, next_trace_window(6)));
     return st;
   }
@@ -1080,19 +1073,7 @@ static int launch_rope_attn(void* out, int ldo, const void* qkv, int ld_qkv, int
                    max(0, n_tok * heads - 3 * sm_count()));
 }
 
-extern "C" int slx_rope_attention_decode_lora(int dtype, void* out, int ldo, const void* qkv,
-                                              int ld_qkv, int n_tok, int heads, int kv_heads,
-                                              int head_dim, const int32_t* tok_pos,
-                                              const int32_t* tok_seq, const float* cos_tab,
-                                              const float* sin_tab, int max_pos, void* k_cache,
-                                              void* v_cache, int max_ctx,
-                                              const slx_lora_delta* lora, void* stream) {
-  return slx_rope_attention_decode_pf(dtype, out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads,
-                                      head_dim, tok_pos, tok_seq, cos_tab, sin_tab, max_pos,
-                                      k_cache, v_cache, max_ctx, 0, lora, nullptr, stream);
-}
-
-extern "C" int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const void* qkv,
+extern "C" int slx_rope_attention_decode(int dtype, void* out, int ldo, const void* qkv,
                                             int ld_qkv, int n_tok, int heads, int kv_heads,
                                             int head_dim, const int32_t* tok_pos,
                                             const int32_t* tok_seq, const float* cos_tab,
@@ -1113,7 +1094,7 @@ extern "C" int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const
   const DeltaArgs la = delta_args(lora);
   const PfArgs pa = pf_args(pf);
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == SLX_DT_BF16 && heads == kv_heads && attn_pipe_enabled() && ld_qkv % 8 == 0 &&
+  if (dtype == SLX_DT_BF16 && heads == kv_heads && pool_seqs > 0 && ld_qkv % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(qkv) & 15) == 0)
     return attn_decode_pipe_launch(out, ldo, qkv, ld_qkv, n_tok, heads, head_dim, tok_pos, tok_seq,
                                    cos_tab, sin_tab, k_cache, v_cache, max_ctx,
@@ -1125,15 +1106,4 @@ extern "C" int slx_rope_attention_decode_pf(int dtype, void* out, int ldo, const
     return head_dim == 64 ? launch_rope_attn<float, 64>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s)
                           : launch_rope_attn<float, 128>(out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads, tok_pos, tok_seq, cos_tab, sin_tab, k_cache, v_cache, max_ctx, scale, la, pa, s);
   return SLX_ERR_INVALID;
-}
-
-extern "C" int slx_rope_attention_decode(int dtype, void* out, int ldo, const void* qkv,
-                                         int ld_qkv, int n_tok, int heads, int kv_heads,
-                                         int head_dim, const int32_t* tok_pos,
-                                         const int32_t* tok_seq, const float* cos_tab,
-                                         const float* sin_tab, int max_pos, void* k_cache,
-                                         void* v_cache, int max_ctx, void* stream) {
-  return slx_rope_attention_decode_lora(dtype, out, ldo, qkv, ld_qkv, n_tok, heads, kv_heads,
-                                        head_dim, tok_pos, tok_seq, cos_tab, sin_tab, max_pos,
-                                        k_cache, v_cache, max_ctx, nullptr, stream);
 }

@@ -160,7 +160,16 @@ class MultiLoraModel:
 
     def __init__(self, cfg: BackboneConfig, *, dtype=torch.bfloat16, device="cuda",
                  max_seqs: int = 64, max_ctx: int = 512, lora_targets=ATTN_TARGETS,
-                 n_slots: int = 32, max_rank: int = 16, max_tokens: int = 4096):
+                 n_slots: int = 32, max_rank: int = 16, max_tokens: int = 4096,
+                 decode_lora: str = "auto"):
+        """``decode_lora`` (bf16): how the decode step's LoRA shrink reads the adapters —
+        "stacked": every slot's A rows are appended to the packed q/k/v and o weights, so the
+        projection GEMM computes the shrink of every slot in its pass over x (cheapest for small
+        pools: no extra launch, but the streamed bytes grow with n_slots * max_rank);
+        "gather": a separate shrink kernel reads only the adapters present in the batch
+        (slx_lora_shrink; bytes = the distinct adapters', independent of the pool size);
+        "auto": stacked while the stacked rows add <= 24 MB per layer (7B, 32 x r16: 16.8 MB),
+        gather beyond (e.g. 13B, 128 slots x r64: 335 MB)."""
         if dtype not in (torch.bfloat16, torch.float32):
             raise ValueError("dtype must be bf16 (throughput) or fp32 (parity)")
         self.cfg, self.dtype = cfg, dtype
@@ -185,9 +194,16 @@ class MultiLoraModel:
         # decode shrink inside the projection GEMMs (bf16): stacked A rows of every slot are
         # appended to the packed q/k/v and o weights; the GEMM writes v_all in fp32 as a side
         # output and slx_lora_expand finishes the LoRA term.  Per group: targets, row layout.
+        if decode_lora not in ("auto", "stacked", "gather"):
+            raise ValueError("decode_lora must be auto, stacked or gather")
+        qkv_t = tuple(t for t in ("q", "k", "v") if t in self.targets)
+        stacked_bytes = ((len(qkv_t) + ("o" in self.targets)) * n_slots * max_rank *
+                         max(cfg.hidden, cfg.q_dim) * 2)
+        if decode_lora == "auto":
+            decode_lora = "stacked" if stacked_bytes <= (24 << 20) else "gather"
+        self.decode_lora = decode_lora if dtype == torch.bfloat16 and self.targets else None
         self.stack = {}
-        if dtype == torch.bfloat16:
-            qkv_t = tuple(t for t in ("q", "k", "v") if t in self.targets)
+        if self.decode_lora == "stacked":
             if qkv_t:
                 self.stack["w_qkv"] = qkv_t
             if "o" in self.targets:
@@ -195,40 +211,19 @@ class MultiLoraModel:
         self.use_stacked_decode = bool(self.stack)
         # decode: q/k/v expand fused into the attention kernel, o expand into the post-norm
         self.fuse_expand = True
-        # decode: o / down projections as split-K pieces reduced by the following RMSNorm
-        self.splitk_consumer = os.environ.get("SLX_SPLITK_CONSUMER", "1") != "0"
+        # decode: o / down projections as split-K pieces reduced by the following RMSNorm;
         # pieces per tile: o 6 (96 CTAs), down 8 (128 CTAs) — measured best on the 7B step
-        # (o at 8: +50 us/step); SLX_SPLITK_SPLITS overrides both
-        sk_all = os.environ.get("SLX_SPLITK_SPLITS")
-        self.splitk_splits_o = int(os.environ.get("SLX_SPLITK_SPLITS_O", sk_all or "6"))
-        self.splitk_splits_dn = int(os.environ.get("SLX_SPLITK_SPLITS_DN", sk_all or "8"))
-        # decode: the RMSNorms fused into the GEMM that consumes them (grid-wide prologue).
-        # Off by default: measured slower (the prologue's dependent L2 round trips queue behind
-        # the weight stream the producer has already started; SLX_FUSE_NORM=1 to enable).
-        self.fuse_norm = os.environ.get("SLX_FUSE_NORM", "0") == "1"
-        self.norm_ss = torch.zeros(64 * 148, dtype=torch.float32, device=self.device)
-        self.norm_bar = torch.zeros(8, dtype=torch.int32, device=self.device)   # 3 call sites
-        # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off)
-        self.l2_prefetch_mb = float(os.environ.get("SLX_L2_PF_MB", "16"))
-        # ... aimed at the first units of EVERY CTA of the next stream-K GEMM (gate/up, q/k/v)
-        # instead of the weight's first bytes.  The RMSNorm kernel in front of that GEMM can
-        # continue it (SLX_NORM_PF_MB, issued at its entry); measured slower (32 MB: +0.2 ms per
-        # step — the prefetch stream delays the norm's own L2 round trips), so 0 by default.
-        self.pf_gemm = os.environ.get("SLX_PF_GEMM", "1") != "0"
-        self.norm_pf_mb = float(os.environ.get("SLX_NORM_PF_MB", "0"))
+        # (o at 8: +50 us/step)
+        self.splitk_consumer = True
+        self.splitk_splits_o, self.splitk_splits_dn = 6, 8
+        # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off),
+        # aimed at the first units of EVERY CTA of the next stream-K GEMM (gate/up, q/k/v)
+        self.l2_prefetch_mb = 16.0
+        self.pf_gemm = True
         self._pf_cache: dict = {}
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
-        # decode: the pre-attention RMSNorm of layers >= 1 folded across two GEMMs — the down
-        # projection writes the residual plus its row sums of squares, the next q/k/v GEMM reads
-        # the raw residual with the norm weight folded into its columns (and stacked A rows) and
-        # scales its rows by 1/rms in the epilogue (no norm kernel between them).  Off by
-        # default: measured 0.55 ms/step SLOWER on the 7B step — the down projection then needs
-        # its own split-K reduction, whose rendezvous tail (~10 us) outweighs the norm kernel
-        # and boundary it removes.  SLX_NORM_FOLD=1 (read at construction: it also keeps a
-        # folded copy of every q/k/v weight).
-        self.norm_fold = os.environ.get("SLX_NORM_FOLD", "0") == "1"
         # prefill: the LoRA expand folded into the backbone GEMM as one extra K block
-        self.lora_fold = os.environ.get("SLX_LORA_FOLD", "1") != "0"
+        self.lora_fold = True
         self.pool.on_install = self._stack_install
         self.pool.on_evict = self._stack_evict
 
@@ -286,8 +281,6 @@ class MultiLoraModel:
             down[:, :cfg.ffn] = rn(cfg.hidden, cfg.ffn)
             w[p + "w_down"] = down
             if self.dtype == torch.bfloat16:   # pack layer by layer to bound peak memory
-                if l > 0 and self.norm_fold:
-                    w[p + "w_qkv_fold"] = self._fold_qkv(w[p + "w_qkv"], w[p + "input_norm"])
                 for k in self.PROJ:
                     w[p + k] = ops.pack_weight(w[p + k], self._extra_rows(k))
         if self.dtype == torch.bfloat16:
@@ -302,17 +295,9 @@ class MultiLoraModel:
         if self.dtype != torch.bfloat16:
             return
         for k in list(self.w):
-            if self.norm_fold and k.endswith(".w_qkv") and not k.startswith("layers.0."):
-                pre = k[:-len("w_qkv")]
-                self.w[pre + "w_qkv_fold"] = self._fold_qkv(self.w[k], self.w[pre + "input_norm"])
             if k == "lm_head" or k.split(".")[-1] in self.PROJ:
                 self.w[k] = ops.pack_weight(self.w[k], self._extra_rows(k.split(".")[-1]))
         torch.cuda.synchronize(self.device)
-
-    def _fold_qkv(self, w_qkv: torch.Tensor, g: torch.Tensor):
-        """Packed W_qkv . diag(g) (the input RMSNorm weight folded into the columns)."""
-        wf = (w_qkv.float() * g.float()[None, :]).to(torch.bfloat16)
-        return ops.pack_weight(wf, self._extra_rows("w_qkv"))
 
     def _extra_rows(self, proj: str) -> int:
         targets = self.stack.get(proj, ())
@@ -331,22 +316,14 @@ class MultiLoraModel:
                 if t not in ts:
                     continue
                 pw = self.w[f"layers.{l}.{proj}"]
-                pf = self.w.get(f"layers.{l}.{proj}_fold")
                 row0 = pw.n + self._stack_rows(proj, t, slot)
                 if t in lora.targets:
                     a = blob[ao:ao + lora.rank * di].view(lora.rank, di)
                     ops.pack_rows(pw, a, lora.rank, row0)
-                    if pf is not None:   # folded copy: A . diag(input_norm)
-                        g = self.w[f"layers.{l}.input_norm"].float()
-                        ops.pack_rows(pf, (a.float() * g[None, :]).to(torch.bfloat16), lora.rank, row0)
                     if lora.rank < R:
                         ops.pack_rows(pw, None, R - lora.rank, row0 + lora.rank)
-                        if pf is not None:
-                            ops.pack_rows(pf, None, R - lora.rank, row0 + lora.rank)
                 else:
                     ops.pack_rows(pw, None, R, row0)
-                    if pf is not None:
-                        ops.pack_rows(pf, None, R, row0)
 
     def _restack(self) -> None:
         """(Re)write the stacked A rows of every resident adapter (backbone loaded later)."""
@@ -360,11 +337,8 @@ class MultiLoraModel:
         for l in range(self.cfg.layers):
             for proj, ts in self.stack.items():
                 pw = self.w[f"layers.{l}.{proj}"]
-                pf = self.w.get(f"layers.{l}.{proj}_fold")
                 for t in ts:
                     ops.pack_rows(pw, None, self.pool.max_rank, pw.n + self._stack_rows(proj, t, slot))
-                    if pf is not None:
-                        ops.pack_rows(pf, None, self.pool.max_rank, pf.n + self._stack_rows(proj, t, slot))
 
     def memory_ledger(self) -> dict:
         """Device bytes this model holds, in the categories the reference's ResidencyLedger
@@ -623,6 +597,25 @@ class MultiLoraModel:
                        self.cfg.target_dims(t)[1]))
         return ops.make_delta(v_all, slot, self.pool.rank, self.pool.scale, self.pool.max_rank, tg)
 
+    def _gather_targets(self, layer: int, names):
+        """(targets array, v column offsets) of the gathered shrink / delta of ``names``."""
+        idx = [i for i, t in enumerate(self.targets) if t in names]
+        specs = [(self.pool.a_ptr[layer, i], self.pool.b_ptr[layer, i],
+                  self.cfg.target_dims(self.targets[i])[1], 0, 1, 1) for i in idx]
+        return idx, ops.make_targets(specs), [k * self.pool.max_rank for k in range(len(idx))]
+
+    def _shrink_delta(self, layer: int, names, x, v, slot, cols):
+        """Gathered decode LoRA of targets ``names`` on input x: the shrink kernel writes v
+        (compact: [T, len(names) * max_rank]); returns the slx_lora_delta of the fused expand."""
+        idx, targets, offs = self._gather_targets(layer, names)
+        if not idx:
+            return None
+        ops.lora_shrink(v, x, self.pool.rank, self.pool.max_rank, targets, offs, self.lora_ws)
+        tg = [(self.pool.b_ptr[layer, i], offs[k], cols[self.targets[i]][0],
+               self.cfg.target_dims(self.targets[i])[1]) for k, i in enumerate(idx)]
+        return ops.make_delta(v, slot, self.pool.rank, self.pool.scale, self.pool.max_rank, tg,
+                              v_slot_stride=0)
+
     @staticmethod
     def segments_of(pos, seq) -> list:
         """Host (tok0, n, seq, pos0) runs of consecutive positions of one sequence."""
@@ -634,16 +627,116 @@ class MultiLoraModel:
                 start = i
         return out
 
+    def _decode_fast(self, T: int) -> bool:
+        """The bf16 decode step of fused kernels (split-K consumers, fused LoRA expands)."""
+        d = self.cfg.hidden
+        return (self.dtype == torch.bfloat16 and self.splitk_consumer and self.fuse_expand
+                and T <= 64 and d % 256 == 0 and d <= 5120
+                and set(self.targets) <= {"q", "k", "v", "o"}
+                and (not self.targets or (self.decode_lora == "gather") or
+                     (self.use_stacked_decode and self.pool.max_rank <= 16)))
+
     def forward(self, tokens, pos, seq, slot, logit_rows=None, decode: bool = False,
                 segments=None) -> torch.Tensor:
         """Token-major mixed batch.  tokens/pos/seq/slot: device int32 [T].
         ``decode``: every token is the next position of its own sequence, so RoPE, the KV
-        append and attention run as one fused kernel per layer.
+        append and attention run as one fused kernel per layer.  The caller guarantees
+        pos < max_ctx (MultiLoraModel.prefill/decode and the serving runtime check it).
         Returns logits (fp32) for ``logit_rows`` (device int64) or for every token."""
-        cfg, w, dt = self.cfg, self.w, self.dtype
         T = tokens.numel()
         if T > self.max_tokens:
             raise ValueError(f"batch of {T} tokens exceeds max_tokens={self.max_tokens}")
+        if decode and self._decode_fast(T):
+            return self._forward_decode(tokens, pos, seq, slot, logit_rows)
+        return self._forward_general(tokens, pos, seq, slot, logit_rows, decode, segments)
+
+    def _forward_decode(self, tokens, pos, seq, slot, logit_rows):
+        """bf16 decode step: per layer [RMSNorm(+ pieces of the previous down projection)] ->
+        [gathered shrink] -> q/k/v GEMM (stacked shrink rows as an fp32 side output) ->
+        RoPE + KV append + attention with the q/k/v LoRA expand fused -> [gathered shrink] ->
+        o GEMM as split-K pieces -> RMSNorm consuming the pieces + the o LoRA expand ->
+        gate/up GEMM with SiLU*mul -> down GEMM as split-K pieces (consumed by the next norm)."""
+        cfg, w, dt, dev = self.cfg, self.w, self.dtype, self.device
+        T = tokens.numel()
+        d, qd, kvd = cfg.hidden, cfg.q_dim, cfg.kv_dim
+        R = self.pool.max_rank
+        x = torch.empty((T, d), dtype=dt, device=dev)
+        h = torch.empty((T, d), dtype=dt, device=dev)
+        qkv = torch.empty((T, qd + 2 * kvd), dtype=dt, device=dev)
+        attn = torch.empty((T, qd), dtype=dt, device=dev)
+        mlp = torch.empty((T, self.ffn_pad), dtype=dt, device=dev)
+        stacked = self.decode_lora == "stacked" and bool(self.stack)
+        gather = self.decode_lora == "gather"
+        qkv_names = tuple(t for t in ("q", "k", "v") if t in self.targets)
+        v_qkv = (torch.empty((T, self._extra_rows("w_qkv")), dtype=torch.float32, device=dev)
+                 if stacked and "w_qkv" in self.stack else None)
+        if gather:
+            v_g = torch.empty((T, max(1, len(qkv_names)) * R), dtype=torch.float32, device=dev)
+            v_go = torch.empty((T, R), dtype=torch.float32, device=dev)
+        S = min(self.splitk_splits_o, (d + 63) // 64)               # o: K = q_dim
+        S_dn = min(self.splitk_splits_dn, self.ffn_pad // 64)       # down: K = ffn
+        part_o = torch.empty(ops.splitk_bytes(T, d + self._extra_rows("wo"), S) // 4,
+                             dtype=torch.float32, device=dev)
+        part_dn = torch.empty(ops.splitk_bytes(T, d, S_dn) // 4, dtype=torch.float32, device=dev)
+        qkv_cols = {"q": (0, qd, qd), "k": (qd, kvd, kvd), "v": (qd + kvd, kvd, kvd)}
+        ops.embedding(x, w["embed"], tokens)
+        if self.targets:
+            ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
+        pending = None   # split-K pieces of the down projection, consumed by the next norm
+        for l in range(cfg.layers):
+            p = f"layers.{l}."
+            if pending is None:
+                ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
+            else:
+                ops.rmsnorm_fused(h, x, w[p + "input_norm"], cfg.rms_eps, pending)
+            # L2 prefetch chain: every kernel requests the first bytes of its successor
+            nxt = f"layers.{l + 1}.w_qkv" if l + 1 < cfg.layers else "lm_head"
+            pf_qkv = self._pf(("kv", l), self.k_cache[l], self.v_cache[l])
+            pf_att = self._pf(p + "wo", w[p + "wo"])
+            pf_gu = self._pf(p + "w_down", w[p + "w_down"])
+            wg = w[p + "w_gu"]
+            pf_o = (self._pf_gemm(p + "w_gu/o", wg, T, wg.n, self.l2_prefetch_mb) if self.pf_gemm
+                    else None) or self._pf(p + "w_gu", wg)
+            pf_dn = None
+            if self.pf_gemm and l + 1 < cfg.layers:
+                wq = w[nxt]
+                pf_dn = self._pf_gemm(nxt + "/down", wq, T, wq.n + (wq.n_extra if stacked else 0),
+                                      self.l2_prefetch_mb)
+            pf_dn = pf_dn or self._pf(nxt, w[nxt])
+            # q / k / v
+            d_qkv = None
+            if stacked and "w_qkv" in self.stack:
+                ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv, prefetch=pf_qkv)
+                d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
+            else:
+                if gather and qkv_names:
+                    d_qkv = self._shrink_delta(l, qkv_names, h, v_g, slot, qkv_cols)
+                ops.gemm(h, w[p + "w_qkv"], qkv, prefetch=pf_qkv)
+            ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
+                                      self.cos, self.sin, self.k_cache[l], self.v_cache[l],
+                                      lora=d_qkv, prefetch=pf_att)
+            # o (split-K pieces) -> residual + o LoRA + post-attention RMSNorm
+            d_o = None
+            if gather and "o" in self.targets:
+                d_o = self._shrink_delta(l, ("o",), attn, v_go, slot, {"o": (0, d, d)})
+            sk_o = ops.gemm_splitk(attn, w[p + "wo"], S, part_o, prefetch=pf_o)
+            if stacked and "wo" in self.stack:
+                d_o = self._delta(l, "wo", None, slot, {"o": (0, d, d)})
+            ops.rmsnorm_fused(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o)
+            # MLP
+            ops.gemm(h, w[p + "w_gu"], mlp, epilogue=EPI_SILU_MUL, prefetch=pf_gu)
+            pending = ops.gemm_splitk(mlp, w[p + "w_down"], S_dn, part_dn, prefetch=pf_dn)
+        hn = torch.empty_like(x)
+        ops.rmsnorm_fused(hn, x, w["final_norm"], cfg.rms_eps, pending)
+        if logit_rows is not None:
+            hn = hn.index_select(0, logit_rows)
+        return ops.gemm(hn, w["lm_head"], out_dtype=torch.float32)
+
+    def _forward_general(self, tokens, pos, seq, slot, logit_rows, decode, segments):
+        """Prefill (bf16: tcgen05 GEMMs with the LoRA folded / grouped SGMV, flash attention)
+        and the fp32 parity mode (decode included)."""
+        cfg, w, dt = self.cfg, self.w, self.dtype
+        T = tokens.numel()
         dev = self.device
         d, qd, kvd = cfg.hidden, cfg.q_dim, cfg.kv_dim
         x = torch.empty((T, d), dtype=dt, device=dev)
@@ -653,6 +746,7 @@ class MultiLoraModel:
         mlp = torch.empty((T, self.ffn_pad), dtype=dt, device=dev)
         fused_silu = dt == torch.bfloat16 and not ({"gate", "up"} & set(self.targets))
         gu = None if fused_silu else torch.empty((T, 2 * self.ffn_pad), dtype=dt, device=dev)
+        # small bf16 batches with a stacked pool: shrink as the GEMM side output + expand kernel
         stacked = self.use_stacked_decode and T <= 128 and bool(self.stack)
         if stacked:
             v_qkv = (torch.empty((T, self._extra_rows("w_qkv")), dtype=torch.float32, device=dev)
@@ -666,7 +760,7 @@ class MultiLoraModel:
         sgmv_plan = None
         fold = None
         if (segments is not None and not decode and dt == torch.bfloat16 and self.targets
-                and self.use_tc_sgmv and not (self.use_stacked_decode and T <= 128)):
+                and self.use_tc_sgmv and not stacked):
             slot_host = slot.cpu().numpy()
             if self.lora_fold:
                 fold = self._fold_plan(segments, slot_host, T)
@@ -677,65 +771,13 @@ class MultiLoraModel:
                 v_qkv_f = torch.zeros((T, 192), dtype=dt, device=dev)
                 v_o_f = torch.zeros((T, 64), dtype=dt, device=dev)
                 bq = [cfg.q_dim, cfg.kv_dim, cfg.kv_dim]
-        # decode: o / down as split-K pieces reduced by the next RMSNorm (no GEMM reduction tail)
-        # (a model without LoRA targets takes the same path, so the bare-backbone step is
-        # comparable kernel for kernel)
-        sk_mode = (decode and dt == torch.bfloat16 and self.splitk_consumer and self.fuse_expand
-                   and (self.use_stacked_decode or not self.targets) and T <= 64
-                   and d % 256 == 0 and d <= 5120 and self.pool.max_rank <= 16)
-        if sk_mode:
-            S = min(self.splitk_splits_o, (d + 63) // 64)               # o: K = q_dim
-            S_dn = min(self.splitk_splits_dn, self.ffn_pad // 64)       # down: K = ffn
-            part_o = torch.empty(ops.splitk_bytes(T, d + self._extra_rows("wo"), S) // 4,
-                                 dtype=torch.float32, device=dev)
-            part_dn = torch.empty(ops.splitk_bytes(T, d, S_dn) // 4, dtype=torch.float32,
-                                  device=dev)
-        pending = None   # split-K pieces of the down projection, consumed by the next norm
-        fnorm0 = sk_mode and self.fuse_norm and self.fuse_expand and "w_qkv" in self.stack
-        rss_mode = (sk_mode and self.norm_fold and not fnorm0 and "w_qkv" in self.stack
-                    and "down" not in self.targets and "layers.1.w_qkv_fold" in w)
-        if rss_mode:
-            ss_rows = torch.empty((T, d // 16), dtype=torch.float32, device=dev)
         ops.embedding(x, w["embed"], tokens)
         if self.targets:
             ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
         qkv_cols = {"q": (0, qd, qd), "k": (qd, kvd, kvd), "v": (qd + kvd, kvd, kvd)}
-        fnorm = sk_mode and self.fuse_norm and self.fuse_expand and "w_qkv" in self.stack
         for l in range(cfg.layers):
             p = f"layers.{l}."
-            folded = rss_mode and l > 0   # x and its row sums of squares come from the down GEMM
-            if fnorm or folded:
-                pass   # built by the qkv GEMM's prologue / folded into it
-            elif pending is not None:
-                pf_n = None
-                if self.pf_gemm and decode and dt == torch.bfloat16:
-                    wq = w[p + "w_qkv"]
-                    nq = wq.n + (wq.n_extra if stacked and "w_qkv" in self.stack else 0)
-                    pf_n = self._pf_gemm(p + "w_qkv/norm", wq, T, nq, self.norm_pf_mb,
-                                         self.l2_prefetch_mb)
-                ops.rmsnorm_fused(h, x, w[p + "input_norm"], cfg.rms_eps, pending, prefetch=pf_n)
-                pending = None
-            else:
-                ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
-            d_qkv = None
-            pfd = decode and dt == torch.bfloat16
-            nxt = (f"layers.{l + 1}.w_qkv" + ("_fold" if rss_mode else "")
-                   if l + 1 < cfg.layers else "lm_head")
-            pf_qkv = self._pf(("kv", l), self.k_cache[l], self.v_cache[l]) if pfd else None
-            pf_att = self._pf(p + "wo", w[p + "wo"]) if pfd else None
-            pf_o = self._pf(p + "w_gu", w[p + "w_gu"]) if pfd else None
-            pf_gu = self._pf(p + "w_down", w[p + "w_down"]) if pfd else None
-            pf_dn = self._pf(nxt, w[nxt]) if pfd else None
-            pf_gu_n = None
-            if pfd and self.pf_gemm and isinstance(w[p + "w_gu"], ops.PackedWeight):
-                wg = w[p + "w_gu"]
-                pf_o = self._pf_gemm(p + "w_gu/o", wg, T, wg.n, self.l2_prefetch_mb) or pf_o
-                pf_gu_n = self._pf_gemm(p + "w_gu/norm", wg, T, wg.n, self.norm_pf_mb,
-                                        self.l2_prefetch_mb)
-                if l + 1 < cfg.layers and not rss_mode:
-                    wq = w[nxt]
-                    nq = wq.n + (wq.n_extra if stacked and "w_qkv" in self.stack else 0)
-                    pf_dn = self._pf_gemm(nxt + "/down", wq, T, nq, self.l2_prefetch_mb) or pf_dn
+            ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
             if fold is not None:
                 ga, bp, rk = self._fold_lora(l, fold[0], "w_qkv")
                 if fold[3] is not None:
@@ -743,22 +785,9 @@ class MultiLoraModel:
                         ops.gemm_grouped(h, cfg.hidden, ga[t], fold[3], v_qkv_f[:, 64 * i:64 * i + 64], 64)
                 ops.gemm_lorafold(h, w[p + "w_qkv"], qkv, fold[1], v_qkv_f,
                                   [0, cfg.q_dim, cfg.q_dim + cfg.kv_dim], bp, bq, rk)
-            elif fnorm:
-                nq = ops.norm_in(x, w[p + "input_norm"], cfg.rms_eps, self.norm_ss,
-                                 self.norm_bar[0:2], sk=pending)
-                pending = None
-                ops.gemm_norm(h, w[p + "w_qkv"], qkv, nq, side=v_qkv, prefetch=pf_qkv)
-                d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
-            elif folded:
-                ops.gemm_rss(x, w[p + "w_qkv_fold"], qkv, side=v_qkv, ss_in=ss_rows, norm_dim=d,
-                             eps=cfg.rms_eps, prefetch=pf_qkv)
-                d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
             elif stacked and "w_qkv" in self.stack:
-                ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv, prefetch=pf_qkv)
-                if decode and self.fuse_expand:
-                    d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
-                else:
-                    self._expand(qkv, v_qkv, l, "w_qkv", qkv_cols)
+                ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv)
+                self._expand(qkv, v_qkv, l, "w_qkv", qkv_cols)
             else:
                 self._gemm(h, w[p + "w_qkv"], qkv)
                 if not (sgmv_plan is not None and
@@ -766,8 +795,7 @@ class MultiLoraModel:
                     self._lora(qkv, h, l, ("q", "k", "v"), qkv_cols)
             if decode:
                 ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos,
-                                          seq, self.cos, self.sin, self.k_cache[l], self.v_cache[l],
-                                          lora=d_qkv, prefetch=pf_att)
+                                          seq, self.cos, self.sin, self.k_cache[l], self.v_cache[l])
             else:
                 ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
                                   self.sin, self.k_cache[l], self.v_cache[l])
@@ -777,73 +805,32 @@ class MultiLoraModel:
                 else:
                     ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
                                   self.k_cache[l], self.v_cache[l])
-            d_o = None
-            if sk_mode and ("wo" in self.stack or "o" not in self.targets):
-                sk_o = ops.gemm_splitk(attn, w[p + "wo"], S, part_o, prefetch=pf_o)
-                d_o = self._delta(l, "wo", None, slot, {"o": (0, d, d)}) if "wo" in self.stack else None
-                if fnorm and fused_silu:
-                    ngu = ops.norm_in(x, w[p + "post_norm"], cfg.rms_eps, self.norm_ss,
-                                      self.norm_bar[2:4], sk=sk_o, delta=d_o)
-                else:
-                    ops.rmsnorm_fused(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o,
-                                      prefetch=pf_gu_n)
-                    ngu = None
-                d_o = "done"
-            elif fold is not None:
+            if fold is not None:
                 ga, bp, rk = self._fold_lora(l, fold[0], "wo")
                 if fold[3] is not None:
                     ops.gemm_grouped(attn, cfg.q_dim, ga["o"], fold[3], v_o_f, 64)
                 ops.gemm_lorafold(attn, w[p + "wo"], x, fold[2], v_o_f, [0], bp, [cfg.hidden], rk,
                                   residual=x)
             elif stacked and "wo" in self.stack:
-                ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o,
-                         prefetch=pf_o)
-                if decode and self.fuse_expand:
-                    d_o = self._delta(l, "wo", v_o, slot, {"o": (0, d, d)})
-                else:
-                    self._expand(x, v_o, l, "wo", {"o": (0, d, d)})
+                ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o)
+                self._expand(x, v_o, l, "wo", {"o": (0, d, d)})
             else:
                 self._gemm(attn, w[p + "wo"], x, residual=x)
                 if not (sgmv_plan is not None and
                         self._sgmv_tc(x, attn, l, ("o",), {"o": (0, d, d)}, sgmv_plan, v_buf)):
                     self._lora(x, attn, l, ("o",), {"o": (0, d, d)})
-            if d_o == "done":
-                pass
-            elif d_o is not None:
-                ops.rmsnorm_lora(h, x, w[p + "post_norm"], cfg.rms_eps, d_o)
-            else:
-                ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
-            if fused_silu and d_o == "done" and ngu is not None:
-                ops.gemm_norm(h, w[p + "w_gu"], mlp, ngu, epilogue=EPI_SILU_MUL, prefetch=pf_gu)
-            elif fused_silu:
-                self._gemm(h, w[p + "w_gu"], mlp, silu=True, prefetch=pf_gu)
+            ops.rmsnorm(h, x, w[p + "post_norm"], cfg.rms_eps)
+            if fused_silu:
+                self._gemm(h, w[p + "w_gu"], mlp, silu=True)
             else:
                 self._gemm(h, w[p + "w_gu"], gu)
                 self._lora(gu, h, l, ("gate", "up"), {"gate": (0, 128, 256), "up": (128, 128, 256)})
                 ops.silu_mul_blocked(mlp, gu, self.ffn_pad)
-            if rss_mode and l + 1 < cfg.layers:
-                ops.gemm_rss(mlp, w[p + "w_down"], x, epilogue=EPI_RESIDUAL, residual=x,
-                             ss_out=ss_rows, prefetch=pf_dn)
-            elif sk_mode and "down" not in self.targets:
-                pending = ops.gemm_splitk(mlp, w[p + "w_down"], S_dn, part_dn, prefetch=pf_dn)
-            else:
-                self._gemm(mlp, w[p + "w_down"], x, residual=x, prefetch=pf_dn)
-                self._lora(x, mlp, l, ("down",), {"down": (0, d, d)}, d_in=cfg.ffn)
-        if pending is not None and fnorm and logit_rows is None:
-            hn = torch.empty_like(x)
-            nf = ops.norm_in(x, w["final_norm"], cfg.rms_eps, self.norm_ss, self.norm_bar[4:6],
-                             sk=pending)
-            logits = torch.empty((T, cfg.vocab), dtype=torch.float32, device=dev)
-            return ops.gemm_norm(hn, w["lm_head"], logits, nf)
-        if pending is not None:
-            hn = torch.empty_like(x)
-            ops.rmsnorm_fused(hn, x, w["final_norm"], cfg.rms_eps, pending)
-            if logit_rows is not None:
-                hn = hn.index_select(0, logit_rows)
-        else:
-            rows = x if logit_rows is None else x.index_select(0, logit_rows)
-            hn = torch.empty_like(rows)
-            ops.rmsnorm(hn, rows, w["final_norm"], cfg.rms_eps)
+            self._gemm(mlp, w[p + "w_down"], x, residual=x)
+            self._lora(x, mlp, l, ("down",), {"down": (0, d, d)}, d_in=cfg.ffn)
+        rows = x if logit_rows is None else x.index_select(0, logit_rows)
+        hn = torch.empty_like(rows)
+        ops.rmsnorm(hn, rows, w["final_norm"], cfg.rms_eps)
         if dt == torch.bfloat16:
             return self._gemm(hn, w["lm_head"], out_dtype=torch.float32)
         return self._gemm(hn, w["lm_head"])

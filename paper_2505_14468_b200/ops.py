@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import (DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED,
-                   L2Prefetch, LoraDelta, LoraTarget, NormIn, RowSS, SplitKIn, check)
+                   GemmTuning, L2Prefetch, LoraDelta, LoraTarget, SplitKIn, check)
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
 
@@ -205,11 +205,12 @@ def l2_prefetch_gemm(w: "PackedWeight", m: int, n_rows: int, unit0: int, units: 
 def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
          epilogue: int = EPI_NONE, residual: torch.Tensor | None = None,
          out_dtype: torch.dtype | None = None, ws=None, side: torch.Tensor | None = None,
-         prefetch: L2Prefetch | None = None) -> torch.Tensor:
+         prefetch: L2Prefetch | None = None, tuning: dict | None = None) -> torch.Tensor:
     """bf16 tcgen05 GEMM: out = a @ w.T (+ residual | silu*mul of blocked gate/up).
     ``w`` is a row-major bf16 [N, K] tensor or a :class:`PackedWeight`; with ``side`` (fp32
     [M, n_extra]) the packed weight's stacked extra rows are computed too (LoRA shrink);
-    ``prefetch`` (l2_prefetch) names the next kernel's first bytes."""
+    ``prefetch`` (l2_prefetch) names the next kernel's first bytes; ``tuning`` (fields of
+    slx_gemm_tuning, e.g. ``{"tile_kernel": 1, "splits": 4}``) forces a tiling (tests/tools)."""
     if a.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
         raise ValueError("gemm: a and w must be bf16")
     M, K = a.shape
@@ -234,78 +235,19 @@ def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
         raise ValueError("gemm: residual must have the output dtype")
     wsb = (ws if ws is not None else default_workspace(a.device)).get(
         _lib.load().slx_gemm_workspace_bytes(M, n_tot, K, epilogue))
-    check(_lib.load().slx_gemm_bf16_pf(_ptr(a), _ld(a), _ptr(wt), _ptr(out), _ld(out), _dt(out),
+    tu = None
+    if tuning:
+        tu = GemmTuning()
+        for k, v in tuning.items():
+            setattr(tu, k, int(v))
+    check(_lib.load().slx_gemm_bf16_ex(_ptr(a), _ld(a), _ptr(wt), _ptr(out), _ld(out), _dt(out),
                                        _ptr(residual), _ld(residual) if residual is not None else 0,
                                        M, n_tot, K, epilogue, layout, n_main,
                                        _ptr(side) if n_tot > n_main else None,
                                        _ld(side) if n_tot > n_main else 0, _ptr(wsb), wsb.numel(),
                                        None if prefetch is None else ctypes.byref(prefetch),
+                                       None if tu is None else ctypes.byref(tu),
                                        _stream()), "slx_gemm_bf16")
-    return out
-
-
-@_op("gemm", 1)
-def gemm_rss(a: torch.Tensor, w, out: torch.Tensor, *, epilogue: int = EPI_NONE,
-             residual: torch.Tensor | None = None, side: torch.Tensor | None = None,
-             ss_out: torch.Tensor | None = None, ss_in: torch.Tensor | None = None,
-             norm_dim: int = 0, eps: float = 0.0, ws=None, prefetch=None) -> torch.Tensor:
-    """Decode GEMM with row RMS across kernels (slx_gemm_bf16_rss): ``ss_out`` (fp32 [M, >=N/16])
-    receives the per-16-column sums of squares of the stored output (residual epilogue); with
-    ``ss_in`` (fp32 [M, n]) the rows are scaled by 1/sqrt(sum/norm_dim + eps) — the RMSNorm of
-    ``a`` whose weight is folded into ``w``."""
-    if not isinstance(w, PackedWeight) or a.dtype != torch.bfloat16:
-        raise ValueError("gemm_rss: bf16 activations and a packed weight")
-    M, K = a.shape
-    N = w.n + (w.n_extra if side is not None else 0)
-    r = RowSS()
-    if ss_out is not None:
-        r.ss_out, r.ss_out_ld = ss_out.data_ptr(), _ld(ss_out)
-    if ss_in is not None:
-        r.ss_in, r.ss_in_n, r.d, r.eps = ss_in.data_ptr(), ss_in.shape[1], int(norm_dim), float(eps)
-    wsb = (ws if ws is not None else default_workspace(a.device)).get(
-        _lib.load().slx_gemm_workspace_bytes(M, N, K, epilogue))
-    check(_lib.load().slx_gemm_bf16_rss(_ptr(a), _ld(a), _ptr(w.data), _ptr(out), _ld(out), _dt(out),
-                                        _ptr(residual), _ld(residual) if residual is not None else 0,
-                                        M, N, K, epilogue, w.n, _ptr(side) if side is not None else None,
-                                        _ld(side) if side is not None else 0, _ptr(wsb), wsb.numel(),
-                                        ctypes.byref(r),
-                                        None if prefetch is None else ctypes.byref(prefetch),
-                                        _stream()), "slx_gemm_bf16_rss")
-    return out
-
-
-def norm_in(x: torch.Tensor, w: torch.Tensor, eps: float, ss: torch.Tensor, bar: torch.Tensor,
-            sk=None, delta=None) -> NormIn:
-    """slx_norm_in for gemm_norm: x (residual stream, updated in place), norm weight w, split-K
-    pieces `sk` of the previous projection, residual LoRA `delta`; ss / bar: scratch and this
-    call site's two grid-barrier counters."""
-    n = NormIn()
-    n.x, n.ldx, n.w, n.eps = x.data_ptr(), _ld(x), w.data_ptr(), float(eps)
-    if sk is not None:
-        n.sk = ctypes.pointer(sk)
-    if delta is not None:
-        n.lora = ctypes.pointer(delta)
-    n.ss, n.ss_bytes, n.bar = ss.data_ptr(), ss.numel() * ss.element_size(), bar.data_ptr()
-    n._keep = (sk, delta)
-    return n
-
-
-@_op("gemm", 1)
-def gemm_norm(h: torch.Tensor, w, out: torch.Tensor, norm: NormIn, *, epilogue: int = EPI_NONE,
-              side: torch.Tensor | None = None, out_dtype=None, ws=None, prefetch=None) -> torch.Tensor:
-    """Decode GEMM whose A operand h = rmsnorm(x + pieces + LoRA delta) is built by the GEMM's
-    own CTAs (slx_gemm_bf16_norm); x is updated in place, h written."""
-    if h.dtype != torch.bfloat16 or not isinstance(w, PackedWeight):
-        raise ValueError("gemm_norm: bf16 activations and a packed weight")
-    M, K = h.shape
-    N = w.n + (w.n_extra if side is not None else 0)
-    wsb = (ws if ws is not None else default_workspace(h.device)).get(
-        _lib.load().slx_gemm_workspace_bytes(M, N, K, epilogue))
-    check(_lib.load().slx_gemm_bf16_norm(
-        _ptr(h), _ld(h), _ptr(w.data), _ptr(out), _ld(out), _dt(out), None, 0, M, N, K, epilogue,
-        w.n, _ptr(side) if side is not None else None, _ld(side) if side is not None else 0,
-        _ptr(wsb), wsb.numel(), ctypes.byref(norm),
-        None if prefetch is None else ctypes.byref(prefetch), _stream()), "slx_gemm_bf16_norm")
     return out
 
 
@@ -397,6 +339,20 @@ def lora_expand(y: torch.Tensor, v_all: torch.Tensor, slot_rank, slot_scale, max
           "slx_lora_expand")
 
 
+@_op("lora", 1)
+def lora_shrink(v: torch.Tensor, x: torch.Tensor, slot_rank, max_rank: int, targets, v_col_off,
+                ws: torch.Tensor) -> None:
+    """Gathered decode shrink over the plan in ws: v[t, v_col_off[i] + j] = x_t . A_slot(t)[j]
+    (fp32, unscaled) for the adapters present in the batch only."""
+    if v.dtype != torch.float32:
+        raise ValueError("lora_shrink: v must be fp32")
+    offs = (ctypes.c_int * len(v_col_off))(*v_col_off)
+    check(_lib.load().slx_lora_shrink(_dt(x), _ptr(v), _ld(v), _ptr(x), _ld(x), x.shape[0],
+                                      x.shape[1], _ptr(slot_rank), slot_rank.numel(), max_rank,
+                                      len(targets), targets, offs, _ptr(ws), ws.numel(), _stream()),
+          "slx_lora_shrink")
+
+
 GROUP_MAX = 16
 
 
@@ -455,10 +411,13 @@ def rmsnorm(out, x, w, eps: float):
     return out
 
 
-def make_delta(v_all: torch.Tensor | None, tok_slot, slot_rank, slot_scale, max_rank: int, targets):
+def make_delta(v_all: torch.Tensor | None, tok_slot, slot_rank, slot_scale, max_rank: int, targets,
+               v_slot_stride: int | None = None):
     """slx_lora_delta for a fused decode expand.  targets: [(b_ptr_table, v_col_off, y_col_off,
-    d_out)] (<= 4); v_all: the fp32 GEMM side output [n_tok, ldv], or None when the consumer
-    takes v from split-K pieces (v_col_off then counts from the pieces' n_main)."""
+    d_out)] (<= 4); v_all: the fp32 shrink output [n_tok, ldv], or None when the consumer
+    takes v from split-K pieces (v_col_off then counts from the pieces' n_main).
+    ``v_slot_stride``: columns between slots' v blocks (default max_rank: the stacked shrink;
+    0: a gathered shrink holding only the token's own adapter)."""
     targets = list(targets)
     if not 1 <= len(targets) <= 4 or (v_all is not None and v_all.dtype != torch.float32):
         raise ValueError("make_delta: 1..4 targets and an fp32 v_all")
@@ -467,6 +426,7 @@ def make_delta(v_all: torch.Tensor | None, tok_slot, slot_rank, slot_scale, max_
         d.v, d.ldv = v_all.data_ptr(), _ld(v_all)
     d.tok_slot, d.slot_rank, d.slot_scale = tok_slot.data_ptr(), slot_rank.data_ptr(), slot_scale.data_ptr()
     d.max_rank, d.n_targets = max_rank, len(targets)
+    d.v_slot_stride = max_rank if v_slot_stride is None else int(v_slot_stride)
     for i, (b, voff, yoff, dout) in enumerate(targets):
         d.b_ptrs[i], d.v_col_off[i], d.y_col_off[i], d.d_out[i] = b.data_ptr(), voff, yoff, dout
     return d
@@ -538,14 +498,15 @@ def attention(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, k_cache, v_
 
 @_op("attention", 1)
 def rope_attention_decode(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq, cos, sin,
-                          k_cache, v_cache, lora=None, prefetch=None):
+                          k_cache, v_cache, lora=None, prefetch=None, pool_seqs=None):
     """Decode-step RoPE + KV append + attention in one kernel (each token = next position of
     its own sequence); ``lora`` (make_delta) fuses the q/k/v LoRA expand, ``prefetch``
-    (l2_prefetch) names the next kernel's first bytes."""
-    check(_lib.load().slx_rope_attention_decode_pf(
+    (l2_prefetch) names the next kernel's first bytes; ``pool_seqs`` (default: the caches'
+    sequence slots) = 0 selects the one-CTA-per-(token, head) kernel (tests)."""
+    check(_lib.load().slx_rope_attention_decode(
         _dt(out), _ptr(out), _ld(out), _ptr(qkv), _ld(qkv), qkv.shape[0], heads, kv_heads, head_dim,
         _ptr(tok_pos), _ptr(tok_seq), _ptr(cos), _ptr(sin), cos.shape[0], _ptr(k_cache),
-        _ptr(v_cache), k_cache.shape[2], k_cache.shape[0],
+        _ptr(v_cache), k_cache.shape[2], k_cache.shape[0] if pool_seqs is None else int(pool_seqs),
         None if lora is None else ctypes.byref(lora),
         None if prefetch is None else ctypes.byref(prefetch), _stream()),
         "slx_rope_attention_decode")

@@ -149,6 +149,9 @@ class Preloader:
             dst = torch.empty(art.nbytes, dtype=torch.uint8, device=self.device)
         if dst.numel() * dst.element_size() < art.nbytes:
             raise ValueError("destination too small")
+        # dst may be a block the caching allocator just recycled from work still queued on the
+        # current stream: the copy must not overtake it
+        self.copy_stream.wait_stream(torch.cuda.current_stream(self.device))
         ev = torch.cuda.Event(enable_timing=True)
         check(_lib.load().slx_preload_h2d(ctypes.c_void_p(dst.data_ptr()),
                                           ctypes.c_void_p(self.store.ptr(name)), art.nbytes,
@@ -171,20 +174,32 @@ class Preloader:
         return float(np.median(times))
 
     def load_broadcast(self, name: str, root: int, comm: NcclComm,
-                       dst: torch.Tensor | None = None) -> torch.Tensor:
-        """Single host read on ``root``, NVLink fan-out to all ranks of ``comm``."""
-        nbytes = self.store.items[name].nbytes if name in self.store.items else None
+                       dst: torch.Tensor | None = None, nbytes: int | None = None) -> torch.Tensor:
+        """Single host read on ``root``, NVLink fan-out to all ranks of ``comm``.  A receiving
+        rank needs the artifact's size: its own store entry, ``nbytes`` or ``dst``."""
+        if nbytes is None and name in self.store.items:
+            nbytes = self.store.items[name].nbytes
         if dst is None:
+            if nbytes is None:
+                raise ValueError(f"load_broadcast({name!r}): size unknown on rank {comm.rank} "
+                                 "(pass nbytes or dst)")
             dst = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        if comm.rank == root and name not in self.store.items:
+            raise KeyError(f"root rank {root} holds no host copy of {name!r}")
+        cur = torch.cuda.current_stream(self.device)
+        self.copy_stream.wait_stream(cur)
+        self.comm_stream.wait_stream(cur)
         src = self.store.ptr(name) if comm.rank == root else None
         check(_lib.load().slx_preload_bcast(ctypes.c_void_p(dst.data_ptr()),
                                             ctypes.c_void_p(src) if src else None,
-                                            dst.numel() * dst.element_size(), self.chunk, root,
+                                            nbytes if nbytes is not None else dst.numel() * dst.element_size(),
+                                            self.chunk, root,
                                             comm.handle,
                                             ctypes.c_void_p(self.copy_stream.cuda_stream),
                                             ctypes.c_void_p(self.comm_stream.cuda_stream)),
               "slx_preload_bcast")
         dst.record_stream(self.comm_stream)
+        dst.record_stream(self.copy_stream)
         return dst
 
     def wait(self) -> None:

@@ -1,75 +1,260 @@
-"""Serving runtime for one GPU: batcher rounds -> merged mixed-adapter prefill -> merged decode.
+"""Serving runtime for one GPU: batcher rounds -> dispatch admission -> merged mixed-adapter
+prefill -> merged (CUDA-graph) decode.
 
 Replaces, on real hardware, the reference engine's modelled path for one GPU:
-``_on_scheduler_tick`` -> ``schedule_round`` (``engine.py:607-656``), ``_try_dispatch``'s
-``prefill_work_ms = predict_ttft(fn, b)`` (``engine.py:832``), processor-shared prefill and the
-``decode_ms_per_token * M`` token loop (``engine.py:259-278,855-910``).  Every round, all
-flushed batches on this GPU run as ONE segmented prefill and every active sequence of every
-function advances in ONE decode step (the B200 replacement for processor sharing).
+``_on_scheduler_tick`` -> ``schedule_round`` (``engine.py:607-656``), ``_try_dispatch``
+(``engine.py:711-853``) with its ``prefill_work_ms = predict_ttft(fn, b)`` (``engine.py:832``),
+processor-shared prefill and the ``decode_ms_per_token * M`` token loop
+(``engine.py:259-278,855-910``).  Every round, all admitted flushes on this GPU run as ONE
+segmented prefill and every active sequence of every function advances in ONE decode step
+(the B200 replacement for processor sharing), replayed from a captured graph per batch-size
+bucket (``engine.DecodeBuckets``).
+
+Dispatch admission follows ``_try_dispatch``:
+
+* bytes needed = the batch's KV reservations (one ``kv_slot_bytes`` sequence slot per request,
+  ``engine.py:717-743``) + the adapter when it is not resident;
+* KV short -> the flush is cut to what fits and the rest goes back to the FRONT of its queue
+  (the reference defers / splits a memory-blocked batch, ``engine.py:668-704``); the queue cap
+  follows the free KV room every round (``max_batch_size(fn, free)``, ``batching.py:24-42``);
+* adapter missing -> a free adapter slot, or one freed by ``offload.select_evictions`` over the
+  adapters of idle functions (``engine.py:745-799``) applied as real D2H demotions
+  (``offload.Offloader``); the adapter's bytes then come from the pinned container tier
+  through the pre-loader on its side stream (cold start, ``engine.py:801-826``) and the
+  function's requests wait in their queue until the copy's event completes, while the rest of
+  the GPU keeps serving;
+* the merged prefill also respects the model's token budget (``max_tokens``).
+
 Timestamps are real (``time.perf_counter``), after a device synchronize per step.
 """
 
 from __future__ import annotations
 
+import math
 import time
 
+import numpy as np
 import torch
 
-from .batching import BatchQueue, max_batch_size, schedule_round
+from .batching import BatchQueue, batch_delay, max_batch_size, schedule_round
+from .engine import DecodeBuckets
 from .model import MultiLoraModel
 from .segments import Request, build_decode, build_prefill
 
 
 class ServingRuntime:
     def __init__(self, model: MultiLoraModel, functions: dict, gpu_id: str = "gpu0",
-                 tick_ms: float = 10.0):
-        """``functions``: function_id -> (FunctionSpec-like, adapter slot or -1)."""
+                 tick_ms: float = 10.0, *, store=None, adapters: dict | None = None,
+                 preloader=None, offloader=None, graphs: bool | None = None,
+                 buckets=(1, 2, 4, 8, 16, 32, 64)):
+        """``functions``: function_id -> (FunctionSpec-like, adapter slot or -1).
+        ``adapters``: function_id -> (artifact name in ``store``, LoraConfig) for functions whose
+        adapter lives in the pinned container tier and is loaded at dispatch (needs
+        ``preloader``; ``offloader`` demotes idle adapters when no slot is free).
+        ``graphs`` (default: bf16 models): decode through captured graphs per bucket."""
         self.m = model
         self.gpu_id = gpu_id
         self.tick_ms = tick_ms
         self.functions = dict(functions)
+        self.store, self.preloader, self.offloader = store, preloader, offloader
+        self.host_adapters = dict(adapters or {})
+        if self.host_adapters and preloader is None:
+            raise ValueError("adapters in the container tier need a preloader")
         self.queues = {fid: BatchQueue(spec, gpu_id, max_batch_size(spec))
                        for fid, (spec, _) in self.functions.items()}
         self.requests: dict = {}
         self.active: list = []
         self.finished: list = []
+        self.loading: dict = {}        # function_id -> (event, dst, LoraConfig, slot, t0_ms)
+        self.cold_ms: dict = {}        # request_id -> {"adapter_load": ms} (wire.COLD_KEYS)
+        self.load_done: dict = {}      # function_id -> (load ms, install time ms)
+        self.served: dict = {fid: 0 for fid in self.functions}
+        if graphs is None:
+            graphs = model.dtype == torch.bfloat16
+        self.graphs = None
+        if graphs:
+            self.pad_seq = model.alloc_seq()   # scratch KV rows of the graphs' spare rows
+            self.graphs = DecodeBuckets(model, self.pad_seq, buckets)
         self.t0 = time.perf_counter()
+        self.decode_steps = 0
+        self.graph_steps = 0
 
     def now_ms(self) -> float:
         return (time.perf_counter() - self.t0) * 1000.0
 
     def submit(self, request_id, function_id: str, prompt, max_new_tokens: int,
                arrival_ms: float | None = None) -> None:
-        """Queue a request (``arrival_ms``: its arrival on this runtime's clock; now if None)."""
+        """Queue a request (``arrival_ms``: its arrival on this runtime's clock; now if None).
+        The sequence must fit the KV pool: len(prompt) + max_new_tokens - 1 <= max_ctx."""
         if function_id not in self.functions:
             raise KeyError(f"unknown function {function_id!r}")
-        r = Request(request_id, function_id, list(prompt), int(max_new_tokens),
+        prompt = list(prompt)
+        if not prompt or max_new_tokens < 1:
+            raise ValueError("a request needs >= 1 prompt token and max_new_tokens >= 1")
+        if len(prompt) + int(max_new_tokens) - 1 > self.m.max_ctx:
+            raise ValueError(f"request {request_id!r}: {len(prompt)} prompt + {max_new_tokens} new "
+                             f"tokens exceed max_ctx={self.m.max_ctx}")
+        if request_id in self.requests:
+            raise ValueError(f"duplicate request id {request_id!r}")
+        r = Request(request_id, function_id, prompt, int(max_new_tokens),
                     self.now_ms() if arrival_ms is None else float(arrival_ms))
         r.adapter_slot = self.functions[function_id][1]
         self.requests[request_id] = r
         self.queues[function_id].enqueue(request_id, r.arrival_ms)
 
+    # ------------------------------------------------------------------ admission
+    def free_kv_slots(self) -> int:
+        return len(self.m.free_seqs)
+
+    def kv_slot_bytes(self) -> int:
+        per = self.m.cfg.kv_bytes_per_token() * self.m.max_ctx
+        return per * (2 if self.m.dtype == torch.float32 else 1)
+
+    @staticmethod
+    def _requeue_front(q: BatchQueue, entries) -> None:
+        """Put (request_id, arrival_ms) entries back at the head of a queue (deferred)."""
+        if not entries:
+            return
+        q.pending = list(entries) + q.pending
+        q.expire_deadline = q.pending[0][1] + batch_delay(q.function, q.n)
+
+    def _adapter_ready(self, fid: str):
+        """Adapter slot of ``fid`` when usable now; otherwise start (or poll) its cold load and
+        return None."""
+        spec, slot = self.functions[fid]
+        pool = self.m.pool
+        if fid not in self.host_adapters or (slot >= 0 and pool.blobs[slot] is not None
+                                             and fid not in self.loading):
+            return slot
+        if fid in self.loading:
+            ev, dst, cfg, s, t_start = self.loading[fid]
+            if not ev.query():
+                return None
+            torch.cuda.current_stream(self.m.device).wait_event(ev)
+            pool.install(s, dst.view(torch.bfloat16), cfg)
+            self.functions[fid] = (spec, s)
+            if self.offloader is not None:
+                self.offloader.adapter_slot[fid] = s
+            del self.loading[fid]
+            t = self.now_ms()
+            self.load_done[fid] = (t - t_start, t)
+            return s
+        name, cfg = self.host_adapters[fid]
+        s = self._free_adapter_slot(fid, self.store.items[name].nbytes)
+        if s is None:
+            return None
+        dst, ev = self.preloader.load(name)
+        self.loading[fid] = (ev, dst, cfg, s, self.now_ms())
+        self.functions[fid] = (spec, -1)
+        return None
+
+    def _busy_functions(self) -> set:
+        busy = {r.function_id for r in self.active}
+        busy |= {fid for fid, q in self.queues.items() if q.n}
+        return busy | set(self.loading)
+
+    def _free_adapter_slot(self, fid: str, nbytes: int):
+        """A free pool slot, or one vacated by demoting idle adapters (select_evictions)."""
+        pool = self.m.pool
+        taken = {s for _, _, _, s, _ in self.loading.values()}
+        for s in range(pool.n_slots):
+            if pool.blobs[s] is None and s not in taken:
+                return s
+        if self.offloader is None:
+            return None
+        from .offload import OffloadRequest, ResidentValue, InsufficientEvictableMemory, \
+            select_evictions
+        from .spec import ArtifactKind
+        busy = self._busy_functions() | {fid}
+        resident = []
+        for f, (_, s) in self.functions.items():
+            if s >= 0 and pool.blobs[s] is not None and f in self.offloader.adapter_slot:
+                w = pool.blobs[s].numel() * 2
+                resident.append(ResidentValue(f, ArtifactKind.ADAPTER_MODEL, w,
+                                              float(self.served.get(f, 0) + 1)))
+        # one slot is what the load needs: require the bytes of the smallest resident blob
+        need = min([r.weight for r in resident if r.function_id not in busy], default=nbytes)
+        try:
+            ev = select_evictions(OffloadRequest(self.gpu_id, need, frozenset(busy)), resident, [],
+                                  container_free={"host": 1 << 62})
+        except InsufficientEvictableMemory:
+            return None
+        freed = [self.functions[e.function_id][1] for e in ev]
+        self.offloader.apply(ev)
+        for e in ev:   # demoted: back to the container tier, served by a later cold load
+            spec, _ = self.functions[e.function_id]
+            self.functions[e.function_id] = (spec, -1)
+            self.host_adapters[e.function_id] = (f"offload/{e.function_id}",
+                                                 self.offloader.demoted[e.function_id][2])
+        return freed[0] if freed else None
+
+    def _admit(self, decisions) -> list:
+        """Admission of a round's FlushDecisions (``_try_dispatch``): returns the admitted
+        requests with KV sequence slots reserved; the rest is deferred to its queue's head."""
+        admitted = []
+        kv_room = self.free_kv_slots()
+        tok_room = self.m.max_tokens
+        for d in decisions:
+            q = self.queues[d.function_id]
+            entries = [(rid, self.requests[rid].arrival_ms) for rid in d.request_ids]
+            slot = self._adapter_ready(d.function_id)
+            if slot is None:   # cold start in flight: the batch waits for its adapter
+                self._requeue_front(q, entries)
+                continue
+            k = 0
+            while k < len(entries) and k < kv_room:
+                n = len(self.requests[entries[k][0]].prompt)
+                if n > tok_room:
+                    break
+                tok_room -= n
+                k += 1
+            self._requeue_front(q, entries[k:])
+            kv_room -= k
+            for rid, _ in entries[:k]:
+                r = self.requests[rid]
+                r.adapter_slot = slot
+                ld = self.load_done.get(d.function_id)
+                if ld is not None and r.arrival_ms <= ld[1]:   # waited for this cold load
+                    self.cold_ms[rid] = {"adapter_load": ld[0]}
+                admitted.append(r)
+        return admitted
+
+    # ------------------------------------------------------------------ the round
     def _i32(self, a):
-        return torch.from_numpy(a).to(self.m.device, non_blocking=True)
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(self.m.device,
+                                                                            non_blocking=True)
 
     def step(self) -> list:
-        """One scheduler tick: flush, prefill the flushed requests together, decode everyone.
+        """One scheduler tick: admit the flushes, prefill them together, decode everyone.
         Returns the FlushDecisions taken this round."""
         now = self.now_ms()
+        free_bytes = self.free_kv_slots() * self.kv_slot_bytes()
+        for fid, q in self.queues.items():   # queue caps follow the free KV room
+            q.max_batch = max(1, max_batch_size(q.function, free_bytes))
         contention = {self.gpu_id: 1 if self.active else 0}
         decisions = schedule_round(list(self.queues.values()), contention, now, self.tick_ms)
-        flushed = [self.requests[rid] for d in decisions for rid in d.request_ids]
+        flushed = self._admit(decisions)
         if flushed:
-            for r in flushed:
-                r.seq = self.m.alloc_seq()
-            batch = build_prefill(flushed, self.m.seq_len)
-            logits = self.m.forward(self._i32(batch.tokens), self._i32(batch.pos),
-                                    self._i32(batch.seq), self._i32(batch.slot),
-                                    torch.from_numpy(batch.logit_rows).to(self.m.device),
-                                    segments=self.m.segments_of(batch.pos, batch.seq))
+            seqs = []
+            try:
+                for r in flushed:
+                    r.seq = self.m.alloc_seq()
+                    seqs.append(r.seq)
+                batch = build_prefill(flushed, self.m.seq_len)
+                logits = self.m.forward(self._i32(batch.tokens), self._i32(batch.pos),
+                                        self._i32(batch.seq), self._i32(batch.slot),
+                                        torch.from_numpy(batch.logit_rows).to(self.m.device),
+                                        segments=self.m.segments_of(batch.pos, batch.seq))
+                nxt = self.m.argmax(logits).cpu().tolist()
+            except Exception:
+                for s in seqs:   # transactional: nothing of the round stays reserved
+                    self.m.free_seq(s)
+                for r in flushed:
+                    r.seq = -1
+                raise
             for r in batch.requests:
                 self.m.seq_len[r.seq] += len(r.prompt)
-            nxt = self.m.argmax(logits).cpu().tolist()
+                self.served[r.function_id] = self.served.get(r.function_id, 0) + 1
             t = self.now_ms()
             for r, tok in zip(batch.requests, nxt):
                 r.generated.append(int(tok))
@@ -78,11 +263,19 @@ class ServingRuntime:
         self._retire()
         if self.active:
             batch = build_decode(self.active, self.m.seq_len)
-            logits = self.m.forward(self._i32(batch.tokens), self._i32(batch.pos),
-                                    self._i32(batch.seq), self._i32(batch.slot), decode=True)
+            if int(batch.pos.max()) >= self.m.max_ctx:
+                raise RuntimeError("a sequence reached max_ctx (submit() admits only fitting requests)")
+            nxt = None
+            if self.graphs is not None:
+                nxt = self.graphs.step(batch.tokens, batch.pos, batch.seq, batch.slot)
+                self.graph_steps += nxt is not None
+            if nxt is None:
+                logits = self.m.forward(self._i32(batch.tokens), self._i32(batch.pos),
+                                        self._i32(batch.seq), self._i32(batch.slot), decode=True)
+                nxt = self.m.argmax(logits).cpu().numpy()
+            self.decode_steps += 1
             for r in batch.requests:
                 self.m.seq_len[r.seq] += 1
-            nxt = self.m.argmax(logits).cpu().tolist()
             for r, tok in zip(batch.requests, nxt):
                 r.generated.append(int(tok))
             self._retire()
@@ -108,5 +301,34 @@ class ServingRuntime:
             if not self.pending():
                 break
             self.step()
+            if self.loading and not self.active:
+                time.sleep(0.0002)   # only cold loads in flight: let the copy engine work
         torch.cuda.synchronize(self.m.device)
         return self.finished
+
+    def report(self) -> dict:
+        """TTFT / TPOT / E2E percentiles (nearest rank, the reference's ``metrics.percentile``,
+        ``/root/reference/pkg/src/slorasim/metrics.py:17-25``) and output tokens/s over the span
+        from the first arrival to the last completion (``metrics.py:130,142``)."""
+        done = self.finished
+        if not done:
+            return {}
+
+        def pct(vals, p):
+            v = sorted(vals)
+            return v[max(0, math.ceil(p / 100.0 * len(v)) - 1)]
+
+        ttft = [r.first_token_ms - r.arrival_ms for r in done]
+        e2e = [r.done_ms - r.arrival_ms for r in done]
+        tpot = [(r.done_ms - r.first_token_ms) / (len(r.generated) - 1) for r in done
+                if len(r.generated) > 1]
+        span_s = (max(r.done_ms for r in done) - min(r.arrival_ms for r in done)) / 1000.0
+        toks = sum(len(r.generated) for r in done)
+        out = {"requests": len(done), "output_tokens": toks,
+               "tokens_per_s": toks / span_s if span_s > 0 else None,
+               "decode_steps": self.decode_steps, "graph_steps": self.graph_steps}
+        for name, vals in (("ttft_ms", ttft), ("e2e_ms", e2e), ("tpot_ms", tpot)):
+            if vals:
+                out[name] = {"p50": pct(vals, 50), "p90": pct(vals, 90), "p99": pct(vals, 99),
+                             "mean": float(np.mean(vals))}
+        return out

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     lib = _lib.load()
     for name in header_symbols():
         assert hasattr(lib, name), name
-    assert lib.slx_abi_version() == 1
+    assert lib.slx_abi_version() == _lib.ABI_VERSION
 
 
 def test_status_strings():

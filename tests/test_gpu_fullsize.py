@@ -121,3 +121,105 @@ def test_13b_widths_one_layer_decode_matches_oracle():
     ref = orc.decode(list(range(48)), toks, ids)
     _check(pre.float().cpu().numpy(), ref_pre)
     _check(got, ref)
+
+
+def _pool_model(cfg, w, used, n_slots, max_rank, max_seqs, max_ctx, max_tokens, seed,
+                decode_lora="auto"):
+    """A model whose pool holds the oracle-known adapters ``used`` {slot: (LoraConfig, dict)}
+    and seeded device-random adapters of ranks {8, 16, 64} in every other slot."""
+    m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=max_seqs, max_ctx=max_ctx,
+                       n_slots=n_slots, max_rank=max_rank, max_tokens=max_tokens,
+                       decode_lora=decode_lora)
+    m.load_backbone(w)
+    ranks = np.random.default_rng(seed).choice([8, 16, 64], size=n_slots)
+    for s in range(n_slots):
+        if s in used:
+            m.pool.load(s, used[s][1], used[s][0])
+        else:
+            m.pool.load_random(s, LoraConfig(int(ranks[s]), 2.0 * ranks[s]), seed=500 + s)
+    return m
+
+
+def test_config3_shape_one_layer_prefill_and_decode_match_oracle():
+    """BASELINE config 3's shape, one layer: 13B widths (hidden 5120, 40 x 128 heads, ffn
+    13824), a 128-slot pool of mixed ranks {8, 16, 64}, three 2048-token causal prompts (a
+    rank-64 adapter, a rank-16 adapter, no adapter) through the bench's prefill path (LoRA
+    folded into the tcgen05 backbone GEMMs, grouped tcgen05 shrink, flash prefill), and the
+    SGMV path without the fold; then one decode step through the gathered-shrink decode path
+    (the pool is too large to stack).  Logits of every 64th position vs the fp32 oracle."""
+    cfg = BackboneConfig("13b-1layer", hidden=5120, layers=1, heads=40, kv_heads=40, head_dim=128,
+                         ffn=13824, vocab=32000)
+    L, n_slots = 2048, 128
+    w = init_backbone(cfg, 41)
+    lo64, lo16 = LoraConfig(64, 128.0, ("q", "k", "v", "o")), LoraConfig(16, 32.0, ("q", "k", "v", "o"))
+    ad64, ad16 = init_adapter(cfg, lo64, 41, 0), init_adapter(cfg, lo16, 41, 1)
+    used = {77: (lo64, ad64), 5: (lo16, ad16)}
+    rng = np.random.default_rng(42)
+    prompts = [list(map(int, rng.integers(1, cfg.vocab, size=L))) for _ in range(3)]
+    ids = [77, 5, -1]
+    toks = list(map(int, rng.integers(1, cfg.vocab, size=3)))
+    # oracle: adapters renumbered 0 (r64), 1 (r16)
+    orc = OracleModel(cfg, w, [ad64, ad16], [lo64.scale, lo16.scale], lo64.targets, max_pos=L + 8)
+    oid = {77: 0, 5: 1, -1: -1}
+    for _ in range(3):
+        orc.kv.append([(np.zeros((0, 40, 128), np.float32), np.zeros((0, 40, 128), np.float32))])
+    tokens = np.concatenate([np.asarray(p) for p in prompts])
+    positions = np.tile(np.arange(L), 3)
+    indptr = np.array([0, L, 2 * L, 3 * L])
+    h = orc._forward(tokens, positions, indptr, np.array([oid[i] for i in ids]), [0, 1, 2])
+    rows = np.arange(0, 3 * L, 64)
+    rows[-1] = 3 * L - 1
+    ref_pre = orc.logits(h[rows])
+    ref_dec = orc.decode([0, 1, 2], toks, [oid[i] for i in ids])
+    for fold in (True, False):
+        m = _pool_model(cfg, w, used, n_slots, 64, 4, L + 8, 3 * L, 41)
+        assert m.decode_lora == "gather" and not m.stack
+        m.lora_fold = fold
+        seqs = [m.alloc_seq() for _ in range(3)]
+        dev = m.device
+        i32 = lambda v: torch.tensor(np.asarray(v), dtype=torch.int32, device=dev)  # noqa: E731
+        slot = np.repeat(np.asarray(ids), L)
+        got = m.forward(i32(tokens), i32(positions), i32(np.repeat(seqs, L)), i32(slot),
+                        torch.tensor(rows, dtype=torch.int64, device=dev),
+                        segments=m.segments_of(positions, np.repeat(seqs, L)))
+        _check(got.float().cpu().numpy(), ref_pre)
+        for s in seqs:
+            m.seq_len[s] = L
+        dec = m.decode(seqs, toks, ids)
+        _check(dec.float().cpu().numpy(), ref_dec)
+        del m
+        torch.cuda.empty_cache()
+
+
+def test_7b_widths_four_layer_decode_matches_oracle():
+    """Error growth across layers: four decoder layers at the 7B widths, batch 64 on 32 r16
+    adapters (the bench's slot draw, two tokens without adapter), a 16-token prefill and
+    three decode steps through the stacked decode path AND the gathered-shrink path, each
+    step's logits vs the fp32 oracle at the same bar as one layer."""
+    cfg = BackboneConfig("7b-4layer", hidden=4096, layers=4, heads=32, kv_heads=32, head_dim=128,
+                         ffn=11008, vocab=32000)
+    lora = LoraConfig(RANK, 32.0, ("q", "k", "v", "o"))
+    w = init_backbone(cfg, 23)
+    ads = [init_adapter(cfg, lora, 23, a) for a in range(N_ADAPTERS)]
+    rng = np.random.default_rng(6)
+    prompts = [list(map(int, rng.integers(1, cfg.vocab, size=16))) for _ in range(BATCH)]
+    ids = _tok_slots()
+    ids[3] = ids[40] = -1
+    steps = [list(map(int, rng.integers(1, cfg.vocab, size=BATCH))) for _ in range(3)]
+    orc = OracleModel(cfg, w, ads, [lora.scale] * N_ADAPTERS, lora.targets)
+    ref_pre = orc.prefill(prompts, ids)
+    refs = [orc.decode(list(range(BATCH)), t, ids) for t in steps]
+    for mode in ("stacked", "gather"):
+        m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=BATCH, max_ctx=32,
+                           n_slots=N_ADAPTERS, max_rank=RANK, max_tokens=BATCH * 16,
+                           decode_lora=mode)
+        m.load_backbone(w)
+        for a, ad in enumerate(ads):
+            m.pool.load(a, ad, lora)
+        assert m._decode_fast(BATCH)
+        seqs, pre = m.prefill(prompts, ids)
+        _check(pre.float().cpu().numpy(), ref_pre)
+        for t, ref in zip(steps, refs):
+            _check(m.decode(seqs, t, ids).float().cpu().numpy(), ref)
+        del m
+        torch.cuda.empty_cache()

@@ -43,26 +43,25 @@ def test_gemm_matches_torch_fp32(M, N, K, tiled):
 @pytest.mark.parametrize("bn", [256, 128])
 @pytest.mark.parametrize("gsplit", [0, 1])
 @pytest.mark.parametrize("ctas,splits", [(1, 1), (2, 8), (1, 3), (1, 6), (2, 2), (1, 5)])
-def test_gemm_decode_tilings(M, bn, gsplit, ctas, splits, monkeypatch):
-    """Every cluster split-K tiling the planner can pick gives the same result."""
+def test_gemm_decode_tilings(M, bn, gsplit, ctas, splits):
+    """Every cluster / global split-K tiling of the tile kernel gives the same result (explicit
+    slx_gemm_tuning; the stream-K decode kernel is bypassed)."""
     N, K = 3072, 4096
     a = bf(torch.randn(M, K, device=DEV))
     w = bf(torch.randn(N, K, device=DEV) * 0.05)
     ref = a.float() @ w.float().T
-    monkeypatch.setenv("SLX_GEMM_SK", "0")   # the cluster / global split-K tilings (M > 64 path)
-    monkeypatch.setenv("SLX_GEMM_CTAS", str(ctas))
-    monkeypatch.setenv("SLX_GEMM_SPLITS", str(splits))
-    monkeypatch.setenv("SLX_GEMM_BN", str(bn))
-    monkeypatch.setenv("SLX_GEMM_GSPLIT", str(gsplit))
-    out = ops.gemm(a, ops.pack_weight(w), out_dtype=torch.float32)
+    tu = {"tile_kernel": 1, "ctas_per_sm": ctas, "splits": splits, "bn": bn,
+          "gsplit": 1 if gsplit else 2}
+    out = ops.gemm(a, ops.pack_weight(w), out_dtype=torch.float32, tuning=tu)
     torch.testing.assert_close(out, ref, rtol=1e-4, atol=1e-3)
     # SiLU and residual epilogues through the same split-K reduction
     r = torch.randn(M, N, device=DEV)   # residual has the output dtype
-    o2 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_RESIDUAL, residual=r, out_dtype=torch.float32)
+    o2 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_RESIDUAL, residual=r, out_dtype=torch.float32,
+                  tuning=tu)
     torch.testing.assert_close(o2, ref + r, rtol=1e-4, atol=1e-3)
     g_, u_ = ref.view(M, N // 256, 2, 128)[:, :, 0], ref.view(M, N // 256, 2, 128)[:, :, 1]
-    monkeypatch.setenv("SLX_GEMM_BN", "256")   # SiLU pairs always use 256-wide tiles
-    o3 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_SILU_MUL, out_dtype=torch.float32)
+    tu["bn"] = 256   # SiLU pairs always use 256-wide tiles
+    o3 = ops.gemm(a, ops.pack_weight(w), epilogue=EPI_SILU_MUL, out_dtype=torch.float32, tuning=tu)
     torch.testing.assert_close(o3, (g_ * torch.sigmoid(g_) * u_).reshape(M, N // 2), rtol=1e-3, atol=1e-3)
 
 
@@ -70,13 +69,11 @@ def test_gemm_decode_tilings(M, bn, gsplit, ctas, splits, monkeypatch):
 @pytest.mark.parametrize("N,K", [(3072, 4096), (4608, 4096), (1000, 11008), (32000, 1024)])
 @pytest.mark.parametrize("ctas,min_units,cluster", [(0, 4, 1), (0, 4, 0), (37, 4, 1), (5, 4, 1),
                                                      (1, 1, 1), (0, 1, 1)])
-def test_gemm_stream_k(M, N, K, ctas, min_units, cluster, monkeypatch):
+def test_gemm_stream_k(M, N, K, ctas, min_units, cluster):
     """Stream-K decode GEMM (M <= 64): every range split (whole tiles, tail/head pieces, up to
     dozens of pieces per tile; uniform splits reduced in DSMEM clusters or through global
     memory) gives the fp32 result; epilogues residual / SiLU / side output."""
-    monkeypatch.setenv("SLX_SK_CLUSTER", str(cluster))
-    monkeypatch.setenv("SLX_SK_CTAS", str(ctas))
-    monkeypatch.setenv("SLX_SK_MIN_UNITS", str(min_units))
+    tu = {"sk_no_cluster": 0 if cluster else 1, "sk_ctas": ctas, "sk_min_units": min_units}
     g = torch.Generator(device=DEV).manual_seed(M + N + K + ctas)
     a = bf(torch.randn(M, K, device=DEV, generator=g))
     w = bf(torch.randn(N, K, device=DEV, generator=g) * 0.05)
@@ -365,17 +362,50 @@ def test_rope_attention_decode_fused(dtype, H, Hkv, D, ctx):
         np.testing.assert_allclose(out_f[b].float().cpu().numpy(), ref.reshape(-1), rtol=tol * 5, atol=tol * 5)
 
 
-@pytest.mark.parametrize("mma", ["1", "0"])
+def _decode_attention_oracle(qkv, kc, vc, pos, seq, slot, ranks, scales, v_all, Bs, H, D, cos, sin,
+                             n_slots, rank):
+    """fp32 numpy restatement of the fused decode step for every token: q/k/v rows + their LoRA
+    delta (rounded to bf16 like the kernel), rotate-half RoPE at pos (oracle/llama_lora.py),
+    append, attention over the sequence's positions 0..pos (oracle attention)."""
+    qkv = qkv.float().cpu().numpy()
+    kcn, vcn = kc.float().cpu().numpy(), vc.float().cpu().numpy()
+    v_all = v_all.cpu().numpy()
+    Bn = [b.float().cpu().numpy() for b in Bs]
+    slot, ranks, scales = slot.cpu().numpy(), ranks.cpu().numpy(), scales.cpu().numpy()
+    pos, seq = pos.cpu().numpy(), seq.cpu().numpy()
+    bfr = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).bfloat16().float().numpy()  # noqa: E731
+    outs, news = [], []
+    for b in range(qkv.shape[0]):
+        row = qkv[b].copy()
+        s_ = int(slot[b])
+        if s_ >= 0:
+            r = int(ranks[s_])
+            for i in range(3):
+                v = v_all[b, i * n_slots * rank + s_ * rank: i * n_slots * rank + s_ * rank + r] * scales[s_]
+                row[i * H * D:(i + 1) * H * D] += Bn[i][s_][:, :r] @ v
+            row = bfr(row)
+        q = row[:H * D].reshape(1, H, D)
+        k = row[H * D:2 * H * D].reshape(1, H, D)
+        vv = row[2 * H * D:].reshape(1, H, D)
+        p_ = np.array([pos[b]])
+        q = bfr(orc.apply_rope(q, p_, cos, sin))
+        k = bfr(orc.apply_rope(k, p_, cos, sin))
+        ks = np.concatenate([kcn[seq[b], :, :pos[b]].transpose(1, 0, 2), k], 0)
+        vs = np.concatenate([vcn[seq[b], :, :pos[b]].transpose(1, 0, 2), vv], 0)
+        outs.append(orc.attention(q, ks, vs, p_).reshape(-1))
+        news.append((k[0], vv[0]))
+    return np.stack(outs), news
+
+
 @pytest.mark.parametrize("ctx", [0, 1, 127, 128, 129, 300, 512, 1000])
 @pytest.mark.parametrize("B,H,D,rank", [(24, 32, 128, 16), (5, 4, 64, 8), (7, 8, 128, 64),
                                         (64, 32, 128, 16)])
-def test_attention_decode_pipe_lora(B, H, D, rank, ctx, mma, monkeypatch):
-    """Persistent TMA-pipelined decode attention (several items per CTA, multi-block contexts;
-    tensor-core and FFMA2 consumers) with the fused q/k/v LoRA delta == the per-(token, head)
-    kernel; ranks staged (<= 16) and not staged (64); tokens without an adapter; identical KV
-    append.  Long contexts with 14 items per CTA exercise the shared KV ring's guard against
-    a consumer group waiting two laps ahead of the producer."""
-    monkeypatch.setenv("SLX_ATTN_MMA", mma)
+def test_attention_decode_pipe_lora(B, H, D, rank, ctx):
+    """Persistent TMA-pipelined tensor-core decode attention (several items per CTA,
+    multi-block contexts) with the fused q/k/v LoRA delta == the per-(token, head) kernel and
+    == the oracle (contexts up to 1000); ranks staged (<= 16) and not staged (64); tokens
+    without an adapter; identical KV append.  Long contexts with 14 items per CTA exercise the
+    shared KV ring's guard against a consumer group waiting two laps ahead of the producer."""
     rng = np.random.default_rng(ctx + B + rank)
     max_ctx, n_slots = max(320, ctx + 8), 3
     cos, sin = orc.rope_table(max_ctx, D, 10000.0)
@@ -396,23 +426,32 @@ def test_attention_decode_pipe_lora(B, H, D, rank, ctx, mma, monkeypatch):
                            [(tabs[i], i * n_slots * rank, i * H * D, H * D) for i in range(3)])
     out = {}
     caches = {}
-    for pipe in ("1", "0"):
-        monkeypatch.setenv("SLX_ATTN_PIPE", pipe)
+    for pipe in (True, False):   # pool_seqs = 0: the one-CTA-per-(token, head) kernel
         k2, v2 = kc.clone(), vc.clone()
         o = torch.empty(B, H * D, dtype=torch.bfloat16, device=DEV)
-        ops.rope_attention_decode(o, qkv, H, H, D, pos, seq, cos_d, sin_d, k2, v2, lora=delta)
+        ops.rope_attention_decode(o, qkv, H, H, D, pos, seq, cos_d, sin_d, k2, v2, lora=delta,
+                                  pool_seqs=None if pipe else 0)
         out[pipe], caches[pipe] = o, (k2, v2)
     torch.cuda.synchronize()
-    torch.testing.assert_close(out["1"].float(), out["0"].float(), rtol=2e-2, atol=2e-2)
-    assert torch.equal(caches["1"][0], caches["0"][0])   # appended k (LoRA + RoPE) identical
-    assert torch.equal(caches["1"][1], caches["0"][1])
+    torch.testing.assert_close(out[True].float(), out[False].float(), rtol=2e-2, atol=2e-2)
+    assert torch.equal(caches[True][0], caches[False][0])   # appended k (LoRA + RoPE) identical
+    assert torch.equal(caches[True][1], caches[False][1])
+    if ctx in (0, 300, 512, 1000) or rank == 64:
+        ref, new = _decode_attention_oracle(qkv, kc, vc, pos, seq, slot, ranks, scales, v_all, Bs, H,
+                                            D, cos, sin, n_slots, rank)
+        np.testing.assert_allclose(out[True].float().cpu().numpy(), ref, rtol=2e-2, atol=2e-2)
+        sq = seq.cpu().numpy()
+        for b in range(B):
+            np.testing.assert_allclose(caches[True][0][sq[b], :, ctx].float().cpu().numpy(), new[b][0],
+                                       rtol=1e-2, atol=1e-2)
+            np.testing.assert_allclose(caches[True][1][sq[b], :, ctx].float().cpu().numpy(), new[b][1],
+                                       rtol=1e-2, atol=1e-2)
 
 
 @pytest.mark.parametrize("d,rank", [(4096, 16), (4096, 64), (5120, 8), (8192, 16)])
-def test_rmsnorm_lora_cluster(d, rank, monkeypatch):
-    """Residual LoRA add + RMSNorm: the 8-CTA cluster kernel == the one-CTA-per-token kernel
-    (identical x write-back; normalised output to fp32 reduction-order rounding), tokens
-    without an adapter untouched."""
+def test_rmsnorm_lora_cluster(d, rank):
+    """Residual LoRA add + RMSNorm (8-CTA cluster kernel for d % 2048 == 0, one CTA per token
+    otherwise) == the fp32 reference; tokens without an adapter untouched."""
     T, n_slots = 37, 4
     g = torch.Generator(device=DEV).manual_seed(d + rank)
     x0 = bf(torch.randn(T, d, device=DEV, generator=g))
@@ -425,15 +464,11 @@ def test_rmsnorm_lora_cluster(d, rank, monkeypatch):
     tab = torch.tensor([Bw[s].data_ptr() for s in range(n_slots)], dtype=torch.int64, device=DEV)
     delta = ops.make_delta(v_all, slot, ranks, scales, rank, [(tab, 0, 0, d)])
     res = {}
-    for cl in ("1", "0"):
-        monkeypatch.setenv("SLX_RMSNORM_CLUSTER", cl)
-        x = x0.clone()
-        h = torch.empty_like(x)
-        ops.rmsnorm_lora(h, x, w, 1e-5, delta)
-        res[cl] = (x, h)
+    x = x0.clone()
+    h = torch.empty_like(x)
+    ops.rmsnorm_lora(h, x, w, 1e-5, delta)
+    res["1"] = (x, h)
     torch.cuda.synchronize()
-    assert torch.equal(res["1"][0], res["0"][0])
-    torch.testing.assert_close(res["1"][1].float(), res["0"][1].float(), rtol=8e-3, atol=8e-3)
     none = (slot < 0).nonzero().flatten()
     assert torch.equal(res["1"][0][none], x0[none])
     # reference: fp32 delta, bf16 round, fp32 rmsnorm
