@@ -315,15 +315,21 @@ SLX_API int slx_rope_attention_decode(int dtype, void* out, int ldo, const void*
                   const float* sin_tab, int max_pos, void* k_cache, void* v_cache, int max_ctx,
                   int pool_seqs, const slx_lora_delta* lora, const slx_l2_prefetch* pf,
                   void* stream);
-/* Prefill (tensor cores, mma.sync flash attention, head_dim 128, bf16): `tiles` is a device
- * array of n_tiles {int tok0, nq, seq, pos0} (<= slx_flash_prefill_tile_queries() queries of one segment each, size
- * slx_flash_prefill_tile_bytes()); query t of a tile attends cache positions 0..pos0+t of
- * its sequence (k/v already appended by slx_rope_kv_write, q rotated in qkv). */
+/* Prefill attention (tcgen05 flash attention, head_dim 128, bf16): `tiles` is a device array of
+ * n_tiles {int tok0, nq, seq, pos0} (nq <= slx_flash_prefill_tile_queries() queries of one
+ * segment each, slx_flash_prefill_tile_bytes() per entry); query t of a tile attends cache
+ * positions 0..pos0+t of its sequence (k/v already appended by slx_rope_kv_write, q rotated in
+ * qkv [n_tok rows]).  `items` (device, n_items x {int tile_a, tile_b (-1: none), head, 0},
+ * slx_flash_prefill_item_bytes() each) is the work list: a persistent CTA per SM runs items
+ * c, c + #SMs, ...; pairing a segment's long and short tiles keeps the items' cost equal.  The
+ * k/v caches are [pool_seqs][kv_heads][max_ctx][128]. */
 SLX_API int slx_flash_prefill_tile_queries(void);   /* max queries per tile (nq) */
 SLX_API size_t slx_flash_prefill_tile_bytes(void);
-SLX_API int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld_qkv, int heads,
-                  int kv_heads, int head_dim, const void* tiles, int n_tiles, const void* k_cache,
-                  const void* v_cache, int max_ctx, void* stream);
+SLX_API size_t slx_flash_prefill_item_bytes(void);
+SLX_API int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld_qkv, int n_tok,
+                  int heads, int kv_heads, int head_dim, const void* tiles, const void* items,
+                  int n_items, const void* k_cache, const void* v_cache, int max_ctx,
+                  int pool_seqs, void* stream);
 /* gu [n_tok, 2*ffn] in the blocked layout of SLX_EPI_SILU_MUL -> out [n_tok, ffn]. */
 SLX_API int slx_silu_mul_blocked(int dtype, void* out, int ldo, const void* gu, int ld_gu, int n_tok,
                          int ffn, void* stream);

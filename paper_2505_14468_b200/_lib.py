@@ -114,7 +114,8 @@ SIGNATURES = {
                                        ctypes.POINTER(L2Prefetch), _p]),
     "slx_flash_prefill_tile_queries": (_i, []),
     "slx_flash_prefill_tile_bytes": (_sz, []),
-    "slx_attention_prefill": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _i, _p, _p, _i, _p]),
+    "slx_flash_prefill_item_bytes": (_sz, []),
+    "slx_attention_prefill": (_i, [_p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i, _p]),
     "slx_silu_mul_blocked": (_i, [_i, _p, _i, _p, _i, _i, _i, _p]),
     "slx_argmax": (_i, [_i, _p, _p, _i, _i, _i, _p]),
     "slx_host_register": (_i, [_p, _sz]),

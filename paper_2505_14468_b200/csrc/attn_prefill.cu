@@ -1,259 +1,434 @@
-// Prefill attention on the tensor cores: causal flash-attention forward over the KV pool.
+// Prefill attention on the 5th-gen tensor cores: causal flash attention over the KV pool with
+// tcgen05.mma (TMEM accumulators) fed by TMA, warp-specialised, persistent.
 //
-// CTA = (64-query tile of one prefill segment, head); 4 warps x 16 query rows.  Key/value
-// blocks of 64 rows are streamed from the pool ([seq][kv_head][pos][128], written by
-// slx_rope_kv_write) into shared memory with cp.async (K double buffered, V single: 68 KB,
-// so three CTAs — 12 warps — share an SM; measured 68 -> 64.5 ms on config 3); S = Q K^T and
-// O += P V use mma.sync m16n8k16 (bf16 in, fp32 accumulate) with ldmatrix fragments, and the
-// softmax is the online exp2 formulation with rows owned by quads of a warp.  Query t of a
-// segment starting at cache position p0 attends positions 0..p0+t (prefix + causal).
-// (The decode step uses rope_attn_decode_kernel; this kernel serves the mixed prefill batch.)
+// Work: a tile is <= 128 queries of one prefill segment; an item is (tile a, tile b, head) —
+// the host pairs a segment's long tile with its short one (prefill_plan), so items of one
+// segment cost the same and consecutive items share the segment's K/V in L2.  CTA c runs items
+// c, c + G, ... (G = #SMs), one item at a time, tile after tile.
+//
+// Per tile (128 query rows = the 128 TMEM lanes, head_dim 128, key blocks of 64):
+//   S_j = Q . K_j^T      tcgen05.mma M128 N64 K16 x8 (Q and K_j K-major, 128B-swizzled TMA
+//                        boxes) into one of two TMEM S buffers (64 columns each)
+//   P_j = exp2(S_j * scale - m)   softmax warpgroup: thread r owns query row r (tcgen05.ld of
+//                        its lane), causal mask, online max with LAZY rescale (the running max
+//                        used for P and for O/l only moves when a row's max grows by > 2^8, so
+//                        the common block never touches O), P written to shared memory as the
+//                        next MMA's K-major A operand (128B swizzle)
+//   O += P_j . V_j       tcgen05.mma M128 N128 K16 x4 with V_j as an MN-major B operand (the
+//                        pool's [pos][128] rows are d-contiguous) into the TMEM O accumulator
+// The MMA warp issues S_{j+1} before O += P_j V_j, so the tensor core computes the next scores
+// while the softmax warpgroup works on the current ones.  Roles (256 threads): warp 0 lane 0
+// TMA producer (Q once per tile, K and V through 4-stage rings), warp 1 lane 0 MMA issuer,
+// warps 4-7 softmax + epilogue (warp w reads TMEM lanes 32 (w % 4) ..).
+// TMEM: S0 [0, 64), S1 [64, 128), O [128, 256).
+// Query t of a tile starting at cache position p0 attends positions 0..p0+t (prefix + causal),
+// k/v already appended by slx_rope_kv_write.
 #include "common.cuh"
+#include "gemm_host.h"
+#include "tc_ptx.cuh"
 
 namespace slx {
+namespace {
 
-constexpr int FA_BQ = 64, FA_BK = 64, FA_D = 128, FA_THREADS = 128;   // 4 warps x 16 query rows (128-query tiles of 8 warps measured slower)
-constexpr int FA_LD = FA_D + 8;   // padded smem row (bf16 elements): conflict-free ldmatrix
+constexpr int FT_BQ = 128, FT_BK = 64, FT_D = 128;
+constexpr int FT_KST = 4, FT_VST = 4;
+constexpr int FT_THREADS = 256;
+constexpr int FT_Q_BYTES = FT_BQ * FT_D * 2;          // 32 KB: two [128][64] boxes
+constexpr int FT_KV_BYTES = FT_BK * FT_D * 2;         // 16 KB: two [64][64] boxes
+constexpr int FT_P_BYTES = FT_BQ * FT_BK * 2;         // 16 KB: [128][64]
+constexpr int FT_OFF_K = FT_Q_BYTES;
+constexpr int FT_OFF_V = FT_OFF_K + FT_KST * FT_KV_BYTES;
+constexpr int FT_OFF_P = FT_OFF_V + FT_VST * FT_KV_BYTES;
+constexpr int FT_OFF_BAR = FT_OFF_P + 2 * FT_P_BYTES;
+constexpr int FT_NBAR = 2 + 2 * FT_KST + 2 * FT_VST + 2 + 2 + 2 + 2 + 1;
+constexpr size_t FT_SMEM = 1024 + FT_OFF_BAR + FT_NBAR * 8 + 16;
+constexpr uint32_t FT_TMEM_COLS = 256;
+constexpr float FT_RESCALE_LOG2 = 8.0f;   // lazy rescale threshold (P <= 2^8 stays exact in fp32/bf16)
 
-struct FaTile {
-  int tok0;    // first query token (row of qkv / out)
-  int nq;      // queries in this tile (<= FA_BQ)
-  int seq;     // KV pool sequence slot
-  int pos0;    // cache position of the first query
+struct FtTile {
+  int tok0, nq, seq, pos0;
+};
+struct FtItem {
+  int ta, tb, h, pad;
 };
 
-__device__ __forceinline__ uint32_t s_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+struct FtArgs {
+  bf16* out;
+  int ldo;
+  const FtTile* tiles;
+  const FtItem* items;
+  int n_items;
+  int H, Hkv, max_ctx;
+  float scale_log2;
+};
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-__device__ __forceinline__ void cp16(void* s, const void* g, bool pred) {
-  const int n = pred ? 16 : 0;   // zero-fill rows past the end
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s_u32(s)), "l"(g), "r"(n)
-               : "memory");
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d,
-                                        const void* p) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(s_u32(p)));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d,
-                                          const void* p) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(s_u32(p)));
-}
-__device__ __forceinline__ void mma16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+      "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"
+      ::"r"(taddr), "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])),
+      "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])),
+      "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])),
+      "r"(__float_as_uint(v[17])), "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])),
+      "r"(__float_as_uint(v[20])), "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])),
+      "r"(__float_as_uint(v[23])), "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])),
+      "r"(__float_as_uint(v[26])), "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])),
+      "r"(__float_as_uint(v[29])), "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// MN-major (V as the B operand: N = head dim contiguous) 128B-swizzled descriptor: 64-element
+// MN atoms `lbo` bytes apart, 8-row K groups 1024 B apart.
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ int n_blocks(const FtTile& t) { return (t.pos0 + t.nq + FT_BK - 1) / FT_BK; }
 
-__global__ void __launch_bounds__(FA_THREADS, 3)
-flash_prefill_kernel(bf16* __restrict__ out, int ldo, const bf16* __restrict__ qkv, int ld, int H,
-                     int Hkv, const FaTile* __restrict__ tiles, const bf16* __restrict__ kc,
-                     const bf16* __restrict__ vc, int max_ctx, float scale_log2) {
-  extern __shared__ __align__(128) uint8_t fsm_raw[];
-  bf16* Qs = reinterpret_cast<bf16*>(fsm_raw);             // [FA_BQ][LD]
-  bf16* Ks = Qs + FA_BQ * FA_LD;                            // [2][64][LD] (double buffered)
-  bf16* Vs = Ks + 2 * FA_BK * FA_LD;                        // [64][LD] (single: 68 KB smem,
-                                                            // 3 CTAs per SM)
-  pdl_wait();
+__global__ void __launch_bounds__(FT_THREADS, 1)
+flash_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                const __grid_constant__ CUtensorMap tv, const FtArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + FT_OFF_BAR);
+  uint64_t* q_full = bar;
+  uint64_t* q_empty = bar + 1;
+  uint64_t* k_full = bar + 2;
+  uint64_t* k_empty = k_full + FT_KST;
+  uint64_t* v_full = k_empty + FT_KST;
+  uint64_t* v_empty = v_full + FT_VST;
+  uint64_t* s_full = v_empty + FT_VST;
+  uint64_t* s_free = s_full + 2;
+  uint64_t* p_full = s_free + 2;
+  uint64_t* p_empty = p_full + 2;
+  uint64_t* o_empty = p_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch_desc(&tq);
+    tc::tma_prefetch_desc(&tk);
+    tc::tma_prefetch_desc(&tv);
+    tc::mbar_init(q_full, 1);
+    tc::mbar_init(q_empty, 1);
+    for (int s = 0; s < FT_KST; ++s) { tc::mbar_init(&k_full[s], 1); tc::mbar_init(&k_empty[s], 1); }
+    for (int s = 0; s < FT_VST; ++s) { tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1); }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&s_full[b], 1);
+      tc::mbar_init(&s_free[b], 4);
+      tc::mbar_init(&p_full[b], 4);
+      tc::mbar_init(&p_empty[b], 1);
+    }
+    tc::mbar_init(o_empty, 4);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, FT_TMEM_COLS);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();   // q (rotated) and the appended k/v come from the previous kernels
   pdl_trigger();
-  // grid (heads, tiles): all heads of a tile launch together, tiles in table order (the host
-  // sorts them longest first, so the last wave holds the short tiles)
-  const FaTile tile = tiles[blockIdx.y];
-  const int h = blockIdx.x, hk = h / (H / Hkv);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bf16* kbase = kc + ((size_t)tile.seq * Hkv + hk) * max_ctx * FA_D;
-  const bf16* vbase = vc + ((size_t)tile.seq * Hkv + hk) * max_ctx * FA_D;
-  const int n_keys = tile.pos0 + tile.nq;               // keys visible to the last query
-  const int nblk = (n_keys + FA_BK - 1) / FA_BK;
+  const int group = a.H / a.Hkv;
 
-  // Q tile
-  for (int e = tid; e < FA_BQ * (FA_D / 8); e += FA_THREADS) {
-    const int r = e / (FA_D / 8), c = e % (FA_D / 8);
-    cp16(Qs + r * FA_LD + c * 8, qkv + (size_t)(tile.tok0 + min(r, tile.nq - 1)) * ld + h * FA_D + c * 8,
-         r < tile.nq);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ TMA producer
+      const uint64_t pol_q = tc::policy_evict_first();
+      const uint64_t pol_kv = tc::policy_evict_last();   // re-read by the segment's other tiles
+      int qi = 0, ki = 0, vi = 0;
+      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+        const FtItem item = a.items[it];
+        for (int tt = 0; tt < 2; ++tt) {
+          const int ti = tt == 0 ? item.ta : item.tb;
+          if (ti < 0) continue;
+          const FtTile t = a.tiles[ti];
+          const int row0 = (t.seq * a.Hkv + item.h / group) * a.max_ctx;
+          tc::mbar_wait(q_empty, (qi & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(q_full, FT_Q_BYTES);
+          tc::tma_load_2d(sm, &tq, q_full, item.h * FT_D, t.tok0, pol_q);
+          tc::tma_load_2d(sm + FT_Q_BYTES / 2, &tq, q_full, item.h * FT_D + 64, t.tok0, pol_q);
+          ++qi;
+          const int nb = n_blocks(t);
+          for (int j = 0; j < nb; ++j) {
+            const int ks = ki % FT_KST;
+            tc::mbar_wait(&k_empty[ks], ((ki / FT_KST) & 1) ^ 1);
+            uint8_t* kd = sm + FT_OFF_K + ks * FT_KV_BYTES;
+            tc::mbar_arrive_expect_tx(&k_full[ks], FT_KV_BYTES);
+            tc::tma_load_2d(kd, &tk, &k_full[ks], 0, row0 + j * FT_BK, pol_kv);
+            tc::tma_load_2d(kd + FT_KV_BYTES / 2, &tk, &k_full[ks], 64, row0 + j * FT_BK, pol_kv);
+            ++ki;
+            const int vs = vi % FT_VST;
+            tc::mbar_wait(&v_empty[vs], ((vi / FT_VST) & 1) ^ 1);
+            uint8_t* vd = sm + FT_OFF_V + vs * FT_KV_BYTES;
+            tc::mbar_arrive_expect_tx(&v_full[vs], FT_KV_BYTES);
+            tc::tma_load_2d(vd, &tv, &v_full[vs], 0, row0 + j * FT_BK, pol_kv);
+            tc::tma_load_2d(vd + FT_KV_BYTES / 2, &tv, &v_full[vs], 64, row0 + j * FT_BK, pol_kv);
+            ++vi;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ MMA issuer
+      const uint32_t id_s = tc::idesc_bf16_f32(FT_BQ, FT_BK);
+      const uint32_t id_o = tc::idesc_bf16_f32(FT_BQ, FT_D) | (1u << 16);   // B (V) MN-major
+      const uint32_t sq = tc::smem_u32(sm);
+      int qi = 0, ki = 0, vi = 0, si = 0, pi = 0, oi = 0;
+      auto pv = [&](int i) {   // O (+)= P_i . V_i
+        const int pb = pi & 1;
+        tc::mbar_wait(&p_full[pb], (pi >> 1) & 1);
+        if (i == 0) {
+          tc::mbar_wait(o_empty, (oi & 1) ^ 1);   // the previous tile's epilogue read O
+          ++oi;
+        }
+        const int vs = vi % FT_VST;
+        tc::mbar_wait(&v_full[vs], (vi / FT_VST) & 1);
+        tc::fence_after_sync();
+        const uint32_t pa = tc::smem_u32(sm + FT_OFF_P + pb * FT_P_BYTES);
+        const uint32_t va = tc::smem_u32(sm + FT_OFF_V + vs * FT_KV_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < FT_BK / 16; ++kk)
+          tc::mma_bf16_ss(tmem + 128, tc::smem_desc_sw128(pa + kk * 32),
+                          desc_mn_sw128(va + kk * 2048, FT_KV_BYTES / 2), id_o,
+                          (i > 0 || kk > 0) ? 1u : 0u);
+        tc::mma_commit(&v_empty[vs]);
+        tc::mma_commit(&p_empty[pb]);
+        ++vi;
+        ++pi;
+      };
+      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+        const FtItem item = a.items[it];
+        for (int tt = 0; tt < 2; ++tt) {
+          const int ti = tt == 0 ? item.ta : item.tb;
+          if (ti < 0) continue;
+          const int nb = n_blocks(a.tiles[ti]);
+          tc::mbar_wait(q_full, qi & 1);
+          for (int j = 0; j < nb; ++j) {
+            const int ks = ki % FT_KST, sb = si & 1;
+            tc::mbar_wait(&k_full[ks], (ki / FT_KST) & 1);
+            tc::mbar_wait(&s_free[sb], ((si >> 1) & 1) ^ 1);
+            tc::fence_after_sync();
+            const uint32_t kb = tc::smem_u32(sm + FT_OFF_K + ks * FT_KV_BYTES);
+#pragma unroll
+            for (int ks16 = 0; ks16 < FT_D / 16; ++ks16) {
+              const uint32_t off = (uint32_t)((ks16 >> 2) * (FT_Q_BYTES / 2) + (ks16 & 3) * 32);
+              const uint32_t offk = (uint32_t)((ks16 >> 2) * (FT_KV_BYTES / 2) + (ks16 & 3) * 32);
+              tc::mma_bf16_ss(tmem + sb * FT_BK, tc::smem_desc_sw128(sq + off),
+                              tc::smem_desc_sw128(kb + offk), id_s, ks16 > 0 ? 1u : 0u);
+            }
+            tc::mma_commit(&k_empty[ks]);
+            tc::mma_commit(&s_full[sb]);
+            ++ki;
+            ++si;
+            if (j == nb - 1) {
+              tc::mma_commit(q_empty);
+              ++qi;
+            }
+            if (j >= 1) pv(j - 1);
+          }
+          pv(nb - 1);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;                        // query row = TMEM lane
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const float sl2 = a.scale_log2;
+    int si = 0, pi = 0;
+    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+      const FtItem item = a.items[it];
+      for (int tt = 0; tt < 2; ++tt) {
+        const int ti = tt == 0 ? item.ta : item.tb;
+        if (ti < 0) continue;
+        const FtTile t = a.tiles[ti];
+        const int nb = n_blocks(t);
+        const int n_keys = t.pos0 + t.nq;
+        const int lim = min(t.pos0 + r, n_keys - 1);   // last visible key of this row
+        float m_used = -INFINITY, l = 0.f;
+        for (int j = 0; j < nb; ++j) {
+          const int sb = si & 1;
+          tc::mbar_wait(&s_full[sb], (si >> 1) & 1);
+          tc::fence_after_sync();
+          float s[FT_BK];
+          tmem_ld32(tmem + lane_off + sb * FT_BK, s);
+          tmem_ld32(tmem + lane_off + sb * FT_BK + 32, s + 32);
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&s_free[sb]);
+          ++si;
+          const int k0 = j * FT_BK;
+          float mx = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < FT_BK; ++c) {
+            if (k0 + c > lim) s[c] = -INFINITY;
+            mx = fmaxf(mx, s[c]);
+          }
+          const float m_new = fmaxf(m_used, mx);
+          if (j == 0) {
+            m_used = m_new;
+          } else {
+            const bool need = (m_new - m_used) * sl2 > FT_RESCALE_LOG2;
+            if (__any_sync(0xffffffffu, need)) {
+              // O holds P_0..P_{j-1} . V: wait for the last PV before rescaling it in TMEM
+              const int lp = pi - 1;
+              tc::mbar_wait(&p_empty[lp & 1], (lp >> 1) & 1);
+              tc::fence_after_sync();
+              const float corr = need ? ex2_approx((m_used - m_new) * sl2) : 1.f;
+              if (need) {
+                m_used = m_new;
+                l *= corr;
+              }
+#pragma unroll 1
+              for (int c0 = 0; c0 < FT_D; c0 += 32) {
+                float o[32];
+                tmem_ld32(tmem + lane_off + 128 + c0, o);
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[e] *= corr;
+                tmem_st32(tmem + lane_off + 128 + c0, o);
+              }
+            }
+          }
+          const float msl = m_used * sl2;
+          uint32_t pk[FT_BK / 2];
+          float ls = 0.f;
+#pragma unroll
+          for (int c = 0; c < FT_BK; c += 2) {
+            const float p0 = ex2_approx(fmaf(s[c], sl2, -msl));
+            const float p1 = ex2_approx(fmaf(s[c + 1], sl2, -msl));
+            ls += p0 + p1;
+            pk[c / 2] = pack2(p0, p1);
+          }
+          l += ls;
+          const int pb = pi & 1;
+          if (pi >= 2) tc::mbar_wait(&p_empty[pb], ((pi >> 1) - 1) & 1);   // PV_{j-2} read it
+          uint8_t* prow = sm + FT_OFF_P + pb * FT_P_BYTES + r * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&p_full[pb]);
+          ++pi;
+        }
+        // epilogue: O / l of this row -> bf16 out
+        const int lp = pi - 1;
+        tc::mbar_wait(&p_empty[lp & 1], (lp >> 1) & 1);
+        tc::fence_after_sync();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        bf16* orow = a.out + (size_t)(t.tok0 + r) * a.ldo + (size_t)item.h * FT_D;
+#pragma unroll 1
+        for (int c0 = 0; c0 < FT_D; c0 += 32) {
+          float o[32];
+          tmem_ld32(tmem + lane_off + 128 + c0, o);
+          if (r < t.nq) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              *reinterpret_cast<uint4*>(orow + c0 + 8 * q) =
+                  make_uint4(pack2(o[8 * q] * inv, o[8 * q + 1] * inv),
+                             pack2(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
+                             pack2(o[8 * q + 4] * inv, o[8 * q + 5] * inv),
+                             pack2(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
+          }
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(o_empty);
+      }
+    }
   }
-  auto stage_k = [&](int b, int buf) {
-    const int k0 = b * FA_BK;
-    for (int e = tid; e < FA_BK * (FA_D / 8); e += FA_THREADS) {
-      const int r = e / (FA_D / 8), c = e % (FA_D / 8);
-      const size_t off = (size_t)min(k0 + r, n_keys - 1) * FA_D + c * 8;
-      cp16(Ks + (buf * FA_BK + r) * FA_LD + c * 8, kbase + off, k0 + r < n_keys);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  auto stage_v = [&](int b) {
-    const int k0 = b * FA_BK;
-    for (int e = tid; e < FA_BK * (FA_D / 8); e += FA_THREADS) {
-      const int r = e / (FA_D / 8), c = e % (FA_D / 8);
-      const size_t off = (size_t)min(k0 + r, n_keys - 1) * FA_D + c * 8;
-      cp16(Vs + r * FA_LD + c * 8, vbase + off, k0 + r < n_keys);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  stage_k(0, 0);
-  stage_v(0);
-
-  // per thread: 2 query rows (lane/4 and lane/4+8 of the warp's 16), quad-shared
-  const int qr0 = warp * 16 + (lane >> 2);
-  const int q_pos0 = tile.pos0 + qr0, q_pos1 = q_pos0 + 8;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-  float o[FA_D / 8][4];
-#pragma unroll
-  for (int j = 0; j < FA_D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
-  uint32_t qf[FA_D / 16][4];
-
-  for (int b = 0; b < nblk; ++b) {
-    asm volatile("cp.async.wait_group 0;" ::: "memory");   // K(b), V(b) (and Q) landed
-    __syncthreads();
-    if (b + 1 < nblk) stage_k(b + 1, (b + 1) & 1);         // overlaps S = Q K^T and softmax
-    if (b == 0) {
-#pragma unroll
-      for (int kk = 0; kk < FA_D / 16; ++kk) {
-        const bf16* p = Qs + (warp * 16 + (lane & 15)) * FA_LD + kk * 16 + (lane >> 4) * 8;
-        ldsm_x4(qf[kk][0], qf[kk][1], qf[kk][2], qf[kk][3], p);
-      }
-    }
-    const bf16* K = Ks + (b & 1) * FA_BK * FA_LD;
-    const bf16* V = Vs;
-    // S = Q K^T for this warp's 16 rows x 64 keys
-    float sacc[FA_BK / 8][4];
-#pragma unroll
-    for (int j = 0; j < FA_BK / 8; ++j) sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < FA_D / 16; ++kk) {
-#pragma unroll
-      for (int j = 0; j < FA_BK / 16; ++j) {   // two 8-key n-tiles per ldmatrix.x4
-        uint32_t b0, b1, b2, b3;
-        const bf16* p = K + (j * 16 + (lane & 7) + ((lane >> 4) << 3)) * FA_LD + kk * 16 +
-                        ((lane >> 3) & 1) * 8;
-        ldsm_x4(b0, b1, b2, b3, p);
-        mma16816(sacc[2 * j], qf[kk], b0, b1);
-        mma16816(sacc[2 * j + 1], qf[kk], b2, b3);
-      }
-    }
-    // scale, causal mask, online softmax (rows q_pos0, q_pos1)
-    const int k0 = b * FA_BK;
-    float bm0 = -INFINITY, bm1 = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < FA_BK / 8; ++j) {
-      const int kc0 = k0 + j * 8 + (lane & 3) * 2;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int kpos = kc0 + e;
-        float s0 = sacc[j][e] * scale_log2, s1 = sacc[j][2 + e] * scale_log2;
-        if (kpos > q_pos0 || kpos >= n_keys) s0 = -INFINITY;
-        if (kpos > q_pos1 || kpos >= n_keys) s1 = -INFINITY;
-        sacc[j][e] = s0;
-        sacc[j][2 + e] = s1;
-        bm0 = fmaxf(bm0, s0);
-        bm1 = fmaxf(bm1, s1);
-      }
-    }
-#pragma unroll
-    for (int off = 1; off <= 2; off <<= 1) {
-      bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, off));
-      bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, off));
-    }
-    const float mn0 = fmaxf(m0, bm0), mn1 = fmaxf(m1, bm1);
-    // fully masked rows so far keep -inf max: use 0 as the reference to avoid inf - inf
-    const float ref0 = mn0 == -INFINITY ? 0.f : mn0, ref1 = mn1 == -INFINITY ? 0.f : mn1;
-    const float c0 = exp2f(m0 - ref0), c1 = exp2f(m1 - ref1);
-    float rs0 = 0.f, rs1 = 0.f;
-    uint32_t pf[FA_BK / 16][4];
-#pragma unroll
-    for (int j = 0; j < FA_BK / 8; ++j) {
-      const float p00 = exp2f(sacc[j][0] - ref0), p01 = exp2f(sacc[j][1] - ref0);
-      const float p10 = exp2f(sacc[j][2] - ref1), p11 = exp2f(sacc[j][3] - ref1);
-      rs0 += p00 + p01;
-      rs1 += p10 + p11;
-      // accumulator layout of an m16n8 tile == A-fragment layout of the k16 step j/2
-      pf[j >> 1][(j & 1) * 2 + 0] = pack_bf16(p00, p01);
-      pf[j >> 1][(j & 1) * 2 + 1] = pack_bf16(p10, p11);
-    }
-#pragma unroll
-    for (int off = 1; off <= 2; off <<= 1) {
-      rs0 += __shfl_xor_sync(0xffffffffu, rs0, off);
-      rs1 += __shfl_xor_sync(0xffffffffu, rs1, off);
-    }
-    l0 = l0 * c0 + rs0;
-    l1 = l1 * c1 + rs1;
-    m0 = mn0;
-    m1 = mn1;
-#pragma unroll
-    for (int j = 0; j < FA_D / 8; ++j) {
-      o[j][0] *= c0; o[j][1] *= c0;
-      o[j][2] *= c1; o[j][3] *= c1;
-    }
-    // O += P V : A = P (16 x 64 keys), B = V (keys x D) via ldmatrix.trans
-#pragma unroll
-    for (int kk = 0; kk < FA_BK / 16; ++kk) {
-      uint32_t a[4] = {pf[kk][0], pf[kk][1], pf[kk][2], pf[kk][3]};
-#pragma unroll
-      for (int j = 0; j < FA_D / 16; ++j) {    // two 8-dim n-tiles per ldmatrix.x4.trans
-        uint32_t b0, b1, b2, b3;
-        const bf16* p = V + (kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * FA_LD + j * 16 +
-                        (lane >> 4) * 8;
-        ldsm_x4_t(b0, b1, b2, b3, p);
-        mma16816(o[2 * j], a, b0, b1);
-        mma16816(o[2 * j + 1], a, b2, b3);
-      }
-    }
-    __syncthreads();   // every warp is done with V(b) (and K(b), refilled next iteration)
-    if (b + 1 < nblk) stage_v(b + 1);
-  }
-  // normalise and store
-  const float inv0 = l0 > 0.f ? 1.f / l0 : 0.f, inv1 = l1 > 0.f ? 1.f / l1 : 0.f;
-  const int r0 = qr0, r1 = qr0 + 8;
-#pragma unroll
-  for (int j = 0; j < FA_D / 8; ++j) {
-    const int d = j * 8 + (lane & 3) * 2;
-    if (r0 < tile.nq)
-      *reinterpret_cast<uint32_t*>(out + (size_t)(tile.tok0 + r0) * ldo + h * FA_D + d) =
-          pack_bf16(o[j][0] * inv0, o[j][1] * inv0);
-    if (r1 < tile.nq)
-      *reinterpret_cast<uint32_t*>(out + (size_t)(tile.tok0 + r1) * ldo + h * FA_D + d) =
-          pack_bf16(o[j][2] * inv1, o[j][3] * inv1);
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem, FT_TMEM_COLS);
   }
 }
 
+}  // namespace
 }  // namespace slx
 
 using namespace slx;
 
-extern "C" size_t slx_flash_prefill_tile_bytes(void) { return sizeof(FaTile); }
-extern "C" int slx_flash_prefill_tile_queries(void) { return FA_BQ; }
+extern "C" size_t slx_flash_prefill_tile_bytes(void) { return sizeof(FtTile); }
+extern "C" size_t slx_flash_prefill_item_bytes(void) { return sizeof(FtItem); }
+extern "C" int slx_flash_prefill_tile_queries(void) { return FT_BQ; }
 
-extern "C" int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld_qkv, int heads,
-                                     int kv_heads, int head_dim, const void* tiles, int n_tiles,
-                                     const void* k_cache, const void* v_cache, int max_ctx,
+extern "C" int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld_qkv, int n_tok,
+                                     int heads, int kv_heads, int head_dim, const void* tiles,
+                                     const void* items, int n_items, const void* k_cache,
+                                     const void* v_cache, int max_ctx, int pool_seqs,
                                      void* stream) {
-  SLX_CHECK_ARG(out && qkv && tiles && k_cache && v_cache && heads > 0 && kv_heads > 0 &&
-                heads % kv_heads == 0 && n_tiles >= 0 && max_ctx > 0 &&
-                ld_qkv >= (heads + 2 * kv_heads) * head_dim && ldo >= heads * head_dim &&
-                ld_qkv % 8 == 0 && ldo % 2 == 0);
-  if (head_dim != FA_D) return SLX_ERR_UNSUPPORTED;
+  SLX_CHECK_ARG(out && qkv && tiles && items && k_cache && v_cache && heads > 0 && kv_heads > 0 &&
+                heads % kv_heads == 0 && n_items >= 0 && n_tok > 0 && max_ctx > 0 &&
+                pool_seqs > 0 && ld_qkv >= (heads + 2 * kv_heads) * head_dim &&
+                ldo >= heads * head_dim && ld_qkv % 8 == 0 && ldo % 8 == 0);
+  if (head_dim != FT_D) return SLX_ERR_UNSUPPORTED;
   SLX_CHECK_ALIGN(qkv, 16);
+  SLX_CHECK_ALIGN(out, 16);
   SLX_CHECK_ALIGN(k_cache, 16);
   SLX_CHECK_ALIGN(v_cache, 16);
-  if (n_tiles == 0) return SLX_OK;
-  const size_t smem = (size_t)(FA_BQ + 3 * FA_BK) * FA_LD * sizeof(bf16);
+  if (n_items == 0) return SLX_OK;
+  const long long rows = (long long)pool_seqs * kv_heads * max_ctx;
+  if (rows >= (1ll << 31)) return SLX_ERR_UNSUPPORTED;
+  CUtensorMap mq, mk, mv;
+  if (!make_tmap(&mq, qkv, n_tok, heads * head_dim, ld_qkv, FT_BQ) ||
+      !make_tmap(&mk, k_cache, (int)rows, FT_D, FT_D, FT_BK) ||
+      !make_tmap(&mv, v_cache, (int)rows, FT_D, FT_D, FT_BK))
+    return SLX_ERR_CUDA;
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(flash_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
+    if (cudaFuncSetAttribute(flash_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)FT_SMEM) != cudaSuccess)
       return SLX_ERR_CUDA;
     configured = true;
   }
-  const float scale = 1.4426950408889634f / sqrtf((float)head_dim);
-  return launch_ex(flash_prefill_kernel, dim3((unsigned)heads, (unsigned)n_tiles),
-                   dim3(FA_THREADS), smem, (cudaStream_t)stream, 1u, (bf16*)out, ldo,
-                   (const bf16*)qkv, ld_qkv, heads, kv_heads, (const FaTile*)tiles,
-                   (const bf16*)k_cache, (const bf16*)v_cache, max_ctx, scale);
+  FtArgs a{};
+  a.out = (bf16*)out; a.ldo = ldo; a.tiles = (const FtTile*)tiles; a.items = (const FtItem*)items;
+  a.n_items = n_items; a.H = heads; a.Hkv = kv_heads; a.max_ctx = max_ctx;
+  a.scale_log2 = 1.4426950408889634f / sqrtf((float)head_dim);
+  const int grid = n_items < sm_count() ? n_items : sm_count();
+  return launch_ex(flash_tc_kernel, dim3((unsigned)grid), dim3(FT_THREADS), FT_SMEM,
+                   (cudaStream_t)stream, 1u, mq, mk, mv, a);
 }

@@ -756,7 +756,7 @@ class MultiLoraModel:
         flash = (segments is not None and not decode and dt == torch.bfloat16
                  and cfg.head_dim == 128)
         if flash:
-            tiles = ops.prefill_tiles(segments, dev)
+            plan = ops.prefill_plan(segments, cfg.heads, dev)
         sgmv_plan = None
         fold = None
         if (segments is not None and not decode and dt == torch.bfloat16 and self.targets
@@ -800,7 +800,7 @@ class MultiLoraModel:
                 ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
                                   self.sin, self.k_cache[l], self.v_cache[l])
                 if flash:
-                    ops.attention_prefill(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, tiles,
+                    ops.attention_prefill(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, plan,
                                           self.k_cache[l], self.v_cache[l])
                 else:
                     ops.attention(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,

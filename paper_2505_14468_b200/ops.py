@@ -513,26 +513,38 @@ def rope_attention_decode(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq,
     return out
 
 
-def prefill_tiles(segments, device, bq: int | None = None) -> torch.Tensor:
-    """[(tok0, n, seq, pos0)] segments -> int32 [n_tiles, 4] tile table of <= bq queries (the
-    flash kernel's tile height by default), longest causal work (keys = pos0 + n) first."""
+def prefill_plan(segments, heads: int, device, bq: int | None = None):
+    """[(tok0, n, seq, pos0)] segments -> the flash prefill's tile table (int32 [n_tiles, 4] of
+    <= bq queries of one segment) and work items (int32 [n_items, 4] = (tile_a, tile_b, head,
+    0)): per segment and head, its k-th longest tile paired with its k-th shortest, so the
+    items of a segment cost the same; items are segment-major (consecutive items share a
+    segment's K/V in L2), longest segments first."""
     if bq is None:
         bq = int(_lib.load().slx_flash_prefill_tile_queries())
-    rows = []
-    for tok0, n, seq, pos0 in segments:
+    tiles, items = [], []
+    for tok0, n, seq, pos0 in sorted(segments, key=lambda s: -(s[3] + s[1])):
+        ids = []
         for q in range(0, n, bq):
-            rows.append((tok0 + q, min(bq, n - q), seq, pos0 + q))
-    rows.sort(key=lambda r: -(r[3] + r[1]))
-    return torch.tensor(rows, dtype=torch.int32).reshape(-1, 4).to(device)
+            ids.append(len(tiles))
+            tiles.append((tok0 + q, min(bq, n - q), seq, pos0 + q))
+        pairs = [(ids[len(ids) - 1 - k], ids[k] if ids[k] != ids[len(ids) - 1 - k] else -1)
+                 for k in range((len(ids) + 1) // 2)]
+        for h in range(heads):
+            items += [(a, b, h, 0) for a, b in pairs]
+    t = torch.tensor(tiles, dtype=torch.int32).reshape(-1, 4)
+    it = torch.tensor(items, dtype=torch.int32).reshape(-1, 4)
+    return t.to(device), it.to(device)
 
 
 @_op("attention", 1)
-def attention_prefill(out, qkv, heads, kv_heads, head_dim, tiles, k_cache, v_cache):
-    """Tensor-core causal flash attention for prefill segments (tiles from prefill_tiles)."""
-    check(_lib.load().slx_attention_prefill(_ptr(out), _ld(out), _ptr(qkv), _ld(qkv), heads,
-                                            kv_heads, head_dim, _ptr(tiles), tiles.shape[0],
-                                            _ptr(k_cache), _ptr(v_cache), k_cache.shape[2],
-                                            _stream()), "slx_attention_prefill")
+def attention_prefill(out, qkv, heads, kv_heads, head_dim, plan, k_cache, v_cache):
+    """tcgen05 causal flash attention for prefill segments (plan from prefill_plan)."""
+    tiles, items = plan
+    check(_lib.load().slx_attention_prefill(_ptr(out), _ld(out), _ptr(qkv), _ld(qkv), qkv.shape[0],
+                                            heads, kv_heads, head_dim, _ptr(tiles), _ptr(items),
+                                            items.shape[0], _ptr(k_cache), _ptr(v_cache),
+                                            k_cache.shape[2], k_cache.shape[0], _stream()),
+          "slx_attention_prefill")
     return out
 
 

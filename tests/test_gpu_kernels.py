@@ -525,12 +525,15 @@ def test_gemm_lora_side_output(M):
     torch.testing.assert_close(side, a.float() @ ext.float().T, rtol=1e-4, atol=1e-3)
 
 
-@pytest.mark.parametrize("H,Hkv", [(4, 4), (8, 2)])
+@pytest.mark.parametrize("H,Hkv", [(4, 4), (8, 2), (40, 40)])
 @pytest.mark.parametrize("segs", [[(0, 1, 0, 0)], [(0, 70, 0, 0), (70, 64, 1, 0), (134, 5, 2, 30)],
-                                  [(0, 200, 0, 100), (200, 129, 1, 0)]])
+                                  [(0, 200, 0, 100), (200, 129, 1, 0)],
+                                  [(0, 2048, 0, 0), (2048, 700, 1, 1300), (2748, 130, 2, 0)]])
 def test_flash_prefill_matches_oracle(H, Hkv, segs):
-    """Tensor-core prefill attention over ragged segments with cached prefixes (pos0 > 0)."""
-    D, max_ctx = 128, 320
+    """tcgen05 prefill attention (persistent, paired tiles, lazy rescale) over ragged segments
+    with cached prefixes (pos0 > 0), up to 2048 causal keys and more items than SMs."""
+    D = 128
+    max_ctx = max(320, max(p0 + n for _, n, _, p0 in segs) + 8)
     rng = np.random.default_rng(H + len(segs))
     T = sum(n for _, n, _, _ in segs)
     n_seq = max(s for _, _, s, _ in segs) + 1
@@ -538,8 +541,8 @@ def test_flash_prefill_matches_oracle(H, Hkv, segs):
     vc = torch.from_numpy(rng.standard_normal((n_seq, Hkv, max_ctx, D)).astype(np.float32)).to(DEV, torch.bfloat16)
     qkv = torch.from_numpy(rng.standard_normal((T, (H + 2 * Hkv) * D)).astype(np.float32)).to(DEV, torch.bfloat16)
     out = torch.empty(T, H * D, dtype=torch.bfloat16, device=DEV)
-    tiles = ops.prefill_tiles(segs, DEV)
-    ops.attention_prefill(out, qkv, H, Hkv, D, tiles, kc, vc)
+    plan = ops.prefill_plan(segs, H, DEV)
+    ops.attention_prefill(out, qkv, H, Hkv, D, plan, kc, vc)
     # generic attention kernel over the same (already rotated) q and pool
     pos = np.concatenate([np.arange(p0, p0 + n) for _, n, _, p0 in segs]).astype(np.int32)
     seq = np.concatenate([[s] * n for _, n, s, _ in segs]).astype(np.int32)
