@@ -121,6 +121,12 @@ class DecodeBuckets:
         self.buckets = tuple(sorted(b for b in buckets if b <= model.max_tokens))
         self.graphs: dict = {}
 
+    def warm(self) -> None:
+        """Capture every bucket's graph now (not inside a timed serving step)."""
+        for b in self.buckets:
+            if b not in self.graphs:
+                self.graphs[b] = DecodeGraph(self.m, [self.pad_seq] * b, [-1] * b, fixed_pos=0).capture()
+
     def bucket(self, n: int) -> int | None:
         for b in self.buckets:
             if b >= n:

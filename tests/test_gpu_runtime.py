@@ -16,12 +16,12 @@ from paper_2505_14468_b200.spec import ArtifactKind, ArtifactSpec, FunctionSpec
 pytestmark = pytest.mark.gpu
 
 
-def _model(golden, dtype=torch.float32, max_seqs=16):
+def _model(golden, dtype=torch.float32, max_seqs=16, n_slots=8):
     seed = int(golden["seed"])
     w = init_backbone(TINY, seed)
     ads = [init_adapter(TINY, TINY_LORA, seed, a) for a in range(4)]
-    m = MultiLoraModel(TINY, dtype=dtype, max_seqs=max_seqs, max_ctx=128, n_slots=8, max_rank=16,
-                       max_tokens=2048)
+    m = MultiLoraModel(TINY, dtype=dtype, max_seqs=max_seqs, max_ctx=128, n_slots=n_slots,
+                       max_rank=16, max_tokens=2048)
     m.load_backbone(w)
     return m, w, ads
 
@@ -89,7 +89,8 @@ def test_calibration_feeds_the_batcher(golden):
                                       max_new_tokens=8, batch_sizes=(1, 2, 4, 8))
     assert spec.prefill_base_ms > 0 and spec.prefill_marginal_ms >= 0
     assert spec.decode_ms_per_token > 0
-    assert spec.kv_cache_bytes_per_request == TINY.kv_bytes_per_token() * 32
+    # the pool reserves max_ctx positions per sequence slot (memory_ledger's kv_slot_bytes)
+    assert spec.kv_cache_bytes_per_request == m.memory_ledger()["kv_slot_bytes"]
     assert spec.slo_ttft_ms == pytest.approx(5 * spec.prefill_base_ms)
     assert predict_ttft(spec, 1) == spec.prefill_base_ms
     assert max_batch_size(spec) >= 1
@@ -140,3 +141,64 @@ def test_memory_ledger_matches_allocator(golden, dtype):
     r = subprocess.run([sys.executable, "-c", _LEDGER_CHECK, dtype, str(int(golden["seed"]))],
                        cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ledger ok" in r.stdout, r.stdout[-2000:] + r.stderr[-4000:]
+
+
+def test_runtime_admission_cold_loads_and_offload_keep_golden_tokens(golden):
+    """Dispatch admission (reference _try_dispatch, engine.py:711-853) with a pool of TWO adapter
+    slots for four functions whose adapters live in the pinned container tier: missing
+    adapters are loaded at dispatch through the pre-loader (cold start), idle ones are demoted
+    by select_evictions + Offloader (D2H) to make room, KV-short flushes are deferred; the
+    fp32 greedy tokens stay bit-exact with the transformers golden."""
+    from paper_2505_14468_b200.offload import Offloader
+    m, w, ads = _model(golden, max_seqs=6, n_slots=2)   # 6 KV slots for 16 requests: deferrals
+    store = HostArtifactStore(64 << 20)
+    pre = Preloader(store, m.device, chunk_bytes=1 << 20)
+    for a, ad in enumerate(ads):
+        store.put(f"adapter{a}", m.pool.pack(ad, TINY_LORA.rank))
+    funcs = {f"fn{a}": (_spec(f"fn{a}"), -1) for a in range(4)}
+    adapters = {f"fn{a}": (f"adapter{a}", TINY_LORA) for a in range(4)}
+    off = Offloader(m, store, {})
+    rt = ServingRuntime(m, funcs, store=store, adapters=adapters, preloader=pre, offloader=off)
+    prompts = _prompts(golden)
+    ids = list(map(int, golden["adapter_ids"]))
+    n_new = int(golden["n_new"])
+    for i, (p, a) in enumerate(zip(prompts, ids)):
+        rt.submit(i, f"fn{a}", p, n_new)
+    with pytest.raises(ValueError):
+        rt.submit(99, "fn0", [1] * 120, 10)   # prompt + new tokens > max_ctx: rejected
+    done = rt.run_until_idle()
+    assert len(done) == len(prompts)
+    toks = np.stack([np.asarray(sorted(done, key=lambda r: r.request_id)[i].generated[:n_new])
+                     for i in range(len(prompts))])
+    assert np.array_equal(toks, golden["tokens"])
+    assert any(v for v in rt.cold_ms.values())      # some requests waited for a cold load
+    assert off.demoted or len({f for f, (_, s) in rt.functions.items() if s >= 0}) <= 2
+    assert len(m.free_seqs) == 6                      # every KV slot returned
+    store.close()
+
+
+def test_runtime_graph_decode_buckets_bf16(golden):
+    """bf16 serving with the captured decode graphs (batch-size buckets, padded rows on the
+    reserved scratch sequence): greedy tokens agree with the golden up to each request's first
+    position whose oracle margin is below TAU, and every decode step ran from a graph."""
+    m, w, ads = _model(golden, dtype=torch.bfloat16, max_seqs=17)
+    for a, ad in enumerate(ads):
+        m.pool.load(a, ad, TINY_LORA)
+    funcs = {f"fn{a}": (_spec(f"fn{a}"), a) for a in range(4)}
+    rt = ServingRuntime(m, funcs)
+    assert rt.graphs is not None
+    prompts = _prompts(golden)
+    ids = list(map(int, golden["adapter_ids"]))
+    n_new = int(golden["n_new"])
+    for i, (p, a) in enumerate(zip(prompts, ids)):
+        rt.submit(i, f"fn{a}", p, n_new)
+    done = sorted(rt.run_until_idle(), key=lambda r: r.request_id)
+    assert rt.graph_steps == rt.decode_steps > 0
+    gold, margin = golden["tokens"], golden["margin"]
+    for r in range(gold.shape[0]):
+        for s in range(gold.shape[1]):
+            assert done[r].generated[s] == gold[r, s] or margin[r, s] < 0.05
+            if margin[r, s] < 0.05:
+                break
+    rep = rt.report()
+    assert rep["requests"] == len(prompts) and rep["ttft_ms"]["p50"] > 0
