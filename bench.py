@@ -166,7 +166,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ CPU oracle
-def _oracle_layer_model(cfg_full, n_adapters, ranks, n_seqs, ctx, seed=0):
+def _oracle_layer_model(cfg_full, n_adapters, ranks, n_seqs, ctx, seed=0, max_pos=None):
     """One decoder layer of ``cfg_full`` in the numpy fp32 oracle with ``n_adapters`` adapters
     (ranks[a]) on q,k,v,o and ``n_seqs`` sequences of ``ctx`` cached positions."""
     from oracle.llama_lora import OracleModel
@@ -194,7 +194,8 @@ def _oracle_layer_model(cfg_full, n_adapters, ranks, n_seqs, ctx, seed=0):
             ad[f"layers.0.{t}.A"] = rn(int(ranks[a]), d, s=1 / np.sqrt(d))
             ad[f"layers.0.{t}.B"] = rn(d, int(ranks[a]))
         ads.append(ad)
-    m = OracleModel(cfg1, w, ads, [2.0] * n_adapters, ("q", "k", "v", "o"), max_pos=ctx + 8)
+    m = OracleModel(cfg1, w, ads, [2.0] * n_adapters, ("q", "k", "v", "o"),
+                    max_pos=max_pos or ctx + 8)
     for _ in range(n_seqs):
         m.kv.append([(rn(ctx, cfg1.kv_heads, cfg1.head_dim, s=1.0),
                       rn(ctx, cfg1.kv_heads, cfg1.head_dim, s=1.0))])
@@ -215,7 +216,7 @@ class CpuOracleSample:
         if workload == "config3":
             self.full = LLAMA2_13B
             ranks = np.random.default_rng(0).choice([8, 16, 64], size=N_AD3)
-            self.m, rng = _oracle_layer_model(self.full, 4, ranks[:4], 0, 0)
+            self.m, rng = _oracle_layer_model(self.full, 4, ranks[:4], 0, 0, max_pos=L3 + 8)
             self.toks = rng.integers(1, self.full.vocab, size=L3)
             self.units = P3 * L3
             self.sample = (f"numpy fp32 oracle on {self.cores} host threads ({cpu_model()}): 1 of 40 "

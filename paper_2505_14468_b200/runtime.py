@@ -69,6 +69,7 @@ class ServingRuntime:
         self.cold_ms: dict = {}        # request_id -> {"adapter_load": ms} (wire.COLD_KEYS)
         self.load_done: dict = {}      # function_id -> (load ms, install time ms)
         self.served: dict = {fid: 0 for fid in self.functions}
+        self._admitted_now: set = set()   # functions admitted in the round being formed
         if graphs is None:
             graphs = model.dtype == torch.bfloat16
         self.graphs = None
@@ -151,6 +152,7 @@ class ServingRuntime:
     def _busy_functions(self) -> set:
         busy = {r.function_id for r in self.active}
         busy |= {fid for fid, q in self.queues.items() if q.n}
+        busy |= self._admitted_now   # admitted this round, not yet prefilled
         return busy | set(self.loading)
 
     def _free_adapter_slot(self, fid: str, nbytes: int):
@@ -192,6 +194,7 @@ class ServingRuntime:
         """Admission of a round's FlushDecisions (``_try_dispatch``): returns the admitted
         requests with KV sequence slots reserved; the rest is deferred to its queue's head."""
         admitted = []
+        self._admitted_now = set()
         kv_room = self.free_kv_slots()
         tok_room = self.m.max_tokens
         for d in decisions:
@@ -210,6 +213,8 @@ class ServingRuntime:
                 k += 1
             self._requeue_front(q, entries[k:])
             kv_room -= k
+            if k:
+                self._admitted_now.add(d.function_id)
             for rid, _ in entries[:k]:
                 r = self.requests[rid]
                 r.adapter_slot = slot
