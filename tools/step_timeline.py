@@ -17,17 +17,17 @@ from paper_2505_14468_b200.model import MultiLoraModel  # noqa: E402
 lib = _lib.load()
 cfg = LLAMA2_7B
 lora = LoraConfig(bench.RANK, bench.ALPHA, ("q", "k", "v", "o"))
-m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=bench.BATCH, max_ctx=bench.CTX + 1,
+m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=bench.BATCH, max_ctx=128 + 1,
                    n_slots=bench.N_ADAPTERS, max_rank=bench.RANK, max_tokens=bench.BATCH)
 m.random_backbone(seed=0)
 for a in range(bench.N_ADAPTERS):
     m.pool.load_random(a, lora, seed=1000 + a)
 seqs = [m.alloc_seq() for _ in range(bench.BATCH)]
-dg = DecodeGraph(m, seqs, bench.tok_slots().tolist(), fixed_pos=bench.CTX)
+dg = DecodeGraph(m, seqs, bench.my_slots(0, 1).tolist(), fixed_pos=128)
 dg.capture()      # untraced warm-up / plans
 buf = torch.zeros(200 * 4096, dtype=torch.int64, device="cuda")
 lib.slx_debug_gemm_trace(buf.data_ptr())
-dgt = DecodeGraph(m, seqs, bench.tok_slots().tolist(), fixed_pos=bench.CTX)
+dgt = DecodeGraph(m, seqs, bench.my_slots(0, 1).tolist(), fixed_pos=128)
 dgt.capture()
 lib.slx_debug_gemm_trace(None)
 for _ in range(3):
