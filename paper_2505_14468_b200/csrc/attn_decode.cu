@@ -151,7 +151,9 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
   // group's block) is still pending; an mbarrier parity wait cannot tell phase i from phase
   // i - 2 STAGES.  A consumer therefore waits until block i has been issued (which implies
   // phase i - STAGES completed) before its parity wait.
-  volatile int* kv_issued = reinterpret_cast<volatile int*>(h_empty + AD_HSLOTS);
+  // The counter is written and polled with shared-memory atomics (release / acquire through the
+  // CTA fences), so the handoff is a synchronised access for the memory model and racecheck.
+  int* kv_issued = reinterpret_cast<int*>(h_empty + AD_HSLOTS);
 
   const int tid = threadIdx.x;
   const int n_items = a.n_tok * a.H;
@@ -193,7 +195,8 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
         tc::tma_load_2d(st + KB * D * 2 + hf * KB * 128, &a.tmv, &kv_full[s], hf * 64, row, pol_kv);
       }
       ++kv_it;
-      *kv_issued = kv_it;   // published by the st.volatile; ordered after the TMA issue above
+      __threadfence_block();            // the expect-tx above is ordered before the publication
+      atomicExch(kv_issued, kv_it);
     };
     bool waited = false;
     if (pl == 0 && (int)blockIdx.x < n_items) {
@@ -435,7 +438,9 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       for (int b = 0; b < nb; ++b) {
         const int it = kv0 + b, s = it % AD_STAGES;
         const int nk = min(KB, pos - b * KB);
-        while (*kv_issued <= it) {}
+        if (lane == 0)
+          while (atomicAdd(kv_issued, 0) <= it) {}
+        __syncwarp();
         tc::mbar_wait(&kv_full[s], (it / AD_STAGES) & 1);
         const uint32_t kbase = tc::smem_u32(ring + (size_t)s * ad_stage_bytes<D, KB>());
         const uint32_t vbase = kbase + KB * D * 2;

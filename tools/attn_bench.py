@@ -1,6 +1,5 @@
 """Decode attention (7B shape: 64 tokens x 32 heads x D 128, ctx 128) timed as a CUDA graph of
-back-to-back launches over 3 KV pools (> L2), pipelined vs per-(token, head) kernel, with and
-without the fused LoRA delta.  python tools/attn_bench.py [reps]"""
+back-to-back launches over 3 KV pools (> L2), with and without the fused LoRA delta.  python tools/attn_bench.py [reps]"""
 import json
 import os
 import sys
@@ -33,9 +32,7 @@ delta = ops.make_delta(v_all, slot, ranks, scales, R, [(tabs[i], i * NS * R, i *
 kv_bytes = B * H * CTX * D * 2 * 2
 
 
-def run(pipe, lora):
-    os.environ["SLX_ATTN_PIPE"] = pipe
-
+def run(lora):
     def body():
         for i in range(REPS):
             kc, vc = pools[i % 3]
@@ -60,11 +57,8 @@ def run(pipe, lora):
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1) * 1000 / REPS)
     us = sorted(ts)[2]
-    return {"pipe": pipe, "lora": lora, "ctx": CTX, "us": round(us, 2), "GB/s": round(kv_bytes / us / 1e3, 1)}
+    return {"lora": lora, "ctx": CTX, "us": round(us, 2), "GB/s": round(kv_bytes / us / 1e3, 1)}
 
 
-for pipe in (("1",) if os.environ.get("SLX_ATTN_DBG_STREAM") or os.environ.get("PIPE_ONLY") else ("1", "0")):
-    for lora in (False, True):
-        r = run(pipe, lora)
-        r["cfg"] = os.environ.get("SLX_ATTN_CFG", "0")
-        print(json.dumps(r), flush=True)
+for lora in (False, True):
+    print(json.dumps(run(lora)), flush=True)

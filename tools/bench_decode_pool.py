@@ -51,7 +51,13 @@ def run(targets):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    info = {"decode_lora": m.decode_lora, "stacked_rows_gb": m.memory_ledger()["adapter_stacked_rows"] / 1e9,
+    from paper_2505_14468_b200 import ops
+    with ops.KernelTimer() as kt:   # eager step, events around every launch (per class)
+        torch.cuda._sleep(200_000_000)
+        dg._step()
+    torch.cuda.synchronize()
+    classes = {k: [round(v[0], 3), v[1]] for k, v in kt.durations().items()}
+    info = {"eager_ms_by_class": classes, "decode_lora": m.decode_lora, "stacked_rows_gb": m.memory_ledger()["adapter_stacked_rows"] / 1e9,
             "kernels_per_step": dg.kernels_per_step}
     del dg, m
     torch.cuda.empty_cache()
@@ -59,7 +65,7 @@ def run(targets):
 
 
 ms, info = run(("q", "k", "v", "o"))
-ms0, _ = run(())
+ms0, info0 = run(())
 d, qd, kvd = cfg.hidden, cfg.q_dim, cfg.kv_dim
 distinct = sorted(set(slots.tolist()))
 moved = cfg.layers * sum(int(ranks[a]) * (3 * d + qd + qd + 2 * kvd + d) * 2 for a in distinct)
@@ -72,5 +78,6 @@ out = {"workload": "13B-shape decode, batch 64, ctx 128, 128 slots r{8,16,64} on
        "distinct_adapters": len(distinct), "lora_bytes_moved_per_step": moved,
        "lora_GB/s": round(moved / (lora_ms / 1000.0) / 1e9, 1) if lora_ms > 0 else None,
        "lora_frac_hbm": round(moved / (lora_ms / 1000.0) / 1e9 / hbm, 4) if lora_ms > 0 else None,
-       "floor_ms_at_hbm_peak": round(moved / hbm / 1e6, 3), **info}
+       "floor_ms_at_hbm_peak": round(moved / hbm / 1e6, 3),
+       "bare_eager_ms_by_class": info0["eager_ms_by_class"], **info}
 print(json.dumps(out))
