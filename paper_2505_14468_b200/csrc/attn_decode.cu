@@ -33,7 +33,7 @@ constexpr int AD_GW = 4;                      // warps per consumer group
 constexpr int AD_GROUPS = 2;
 constexpr int AD_GT = AD_GW * 32;             // threads per group
 constexpr int AD_CONS = AD_GROUPS * AD_GT;    // consumer threads
-constexpr int AD_THREADS = AD_CONS + 32;      // + producer warp
+constexpr int AD_THREADS = AD_CONS + 64;      // + header producer warp + KV producer warp
 constexpr int AD_STAGES = 4;                  // KV ring
 constexpr int AD_HSLOTS = 4;                  // header ring (2 per group)
 constexpr int AD_VMAX = 64;                   // LoRA rank staged in the header (v)
@@ -96,6 +96,18 @@ struct __align__(16) AdScratch {
   float red[2 * AD_GW];
   bf16 qb[D];
 };
+
+// shared-memory atomics on a 32-bit word (explicit .shared state space: ATOMS, not generic ATOM)
+__device__ __forceinline__ int smem_atom_add(uint32_t addr, int v) {
+  int old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void smem_atom_exch(uint32_t addr, int v) {
+  int old;
+  asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
+  (void)old;
+}
 
 __device__ __forceinline__ void ad_ldsm_x4(uint32_t* r, uint32_t addr) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -176,12 +188,18 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
   __syncthreads();
 
   if (tid >= AD_CONS) {
-    // ================================================================ producer warp
-    const int pl = tid - AD_CONS;
+    // ============================================================ producer warps
+    // Warp P (tid AD_CONS..+31) resolves the metadata of 32 items at a time (one per lane) and
+    // its lane 0 issues the items' headers; warp K's lane 0 issues their KV blocks.  Separate
+    // issuers: a header never waits behind ring space for an earlier item's KV (a consumer
+    // group would otherwise wait on its next header while the ring drains).
+    const bool kvw = tid >= AD_CONS + 32;
+    const int pl = tid & 31;
     const uint64_t pol_kv = tc::policy_evict_first();    // cache rows are read once
     const uint64_t pol_h = tc::policy_evict_normal();
-    int kv_it = 0, j = 0, n_pre = 0;
-    auto issue_kv = [&](int seq, int h, int blk, int pos) {
+    const uint32_t kv_issued_s = tc::smem_u32(kv_issued);
+    int kv_it = 0, j = 0, n_pre = 0, kv_base = 0;
+    auto issue_kv = [&](int seq, int h, int blk) {
       const int s = kv_it % AD_STAGES;
       tc::mbar_wait(&kv_empty[s], ((kv_it / AD_STAGES) & 1) ^ 1);
       const size_t off = (((size_t)seq * a.H + h) * a.max_ctx + (size_t)blk * KB) * D;
@@ -196,20 +214,19 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
       }
       ++kv_it;
       __threadfence_block();            // the expect-tx above is ordered before the publication
-      atomicExch(kv_issued, kv_it);
+      smem_atom_exch(kv_issued_s, kv_it);
     };
-    bool waited = false;
-    if (pl == 0 && (int)blockIdx.x < n_items) {
+    if (kvw && pl == 0 && (int)blockIdx.x < n_items) {
       // item 0's cached keys were written >= 2 launches back: request them first, before the
       // metadata of the batch (slot / rank / B pointers: dependent loads) is resolved
       const int t0 = blockIdx.x / a.H, h0 = blockIdx.x % a.H;
       const int pos0 = a.tok_pos[t0], seq0 = a.tok_seq[t0];
       n_pre = min((pos0 + KB - 1) / KB, AD_STAGES);
-      for (int b = 0; b < n_pre; ++b) issue_kv(seq0, h0, b, pos0);
+      for (int b = 0; b < n_pre; ++b) issue_kv(seq0, h0, b);
     }
     for (int w0 = blockIdx.x; w0 < n_items; w0 += 32 * gridDim.x) {
-      // ---- metadata of items w0 + i * gridDim.x, lane i (inputs / adapter pool: >= 2 launches old)
-      {
+      if (!kvw) {
+        // ---- metadata of items w0 + i * gridDim.x, lane i (inputs / adapter pool: >= 2 launches old)
         const int w = w0 + pl * (int)gridDim.x;
         ItemMeta mt{};
         mt.valid = w < n_items;
@@ -242,14 +259,19 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
         }
         meta[pl] = mt;
       }
-      __syncwarp();
-      if (pl == 0) {
-        const int nloc = min(32, (n_items - w0 + (int)gridDim.x - 1) / (int)gridDim.x);
-        if (!waited) {
-          pdl_wait();
-          pdl_trigger();
-          if (a.trace) a.trace[blockIdx.x * 16 + 2] = ad_timer();
+      tc::named_bar_sync(3, 64);   // meta of this batch visible to both producer warps
+      const int nloc = min(32, (n_items - w0 + (int)gridDim.x - 1) / (int)gridDim.x);
+      if (w0 == (int)blockIdx.x) {
+        pdl_wait();
+        pdl_trigger();
+        if (!kvw && pl == 0 && a.trace) a.trace[blockIdx.x * 16 + 2] = ad_timer();
+      }
+      if (pl == 0 && kvw) {
+        for (int i = 0; i < nloc; ++i, ++j) {
+          const ItemMeta& mt = meta[i];
+          for (int b = (j == 0 ? n_pre : 0); b < (mt.pos + KB - 1) / KB; ++b) issue_kv(mt.seq, mt.h, b);
         }
+      } else if (pl == 0) {
         for (int i = 0; i < nloc; ++i, ++j) {
           const ItemMeta& mt = meta[i];
           const int hs = j % AD_HSLOTS;
@@ -262,7 +284,8 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
           tc::mbar_wait(&h_empty[hs], ((j / AD_HSLOTS) & 1) ^ 1);
           AdHeader<D>* hd = hdr + hs;
           for (int p = 0; p < 3; ++p) hd->b[p] = (stage_v && mt.ti[p] >= 0) ? mt.b[p] : nullptr;
-          hd->kv_base = j == 0 ? 0 : kv_it;   // item 0's first blocks went out before the wait
+          hd->kv_base = kv_base;   // ring counter of the item's first KV block (same order)
+          kv_base += (mt.pos + KB - 1) / KB;
           hd->bstaged = stage_b ? 1 : 0;
           hd->rank = mt.rank; hd->pos = mt.pos; hd->seq = mt.seq;
           hd->slot = mt.slot; hd->lscale = mt.scale;
@@ -282,20 +305,18 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
                   tc::bulk_g2s(hd->bs[p], mt.b[p], (uint32_t)(D * mt.rank * 2), &h_full[hs], pol_h);
               }
           }
-          for (int b = (j == 0 ? n_pre : 0); b < (mt.pos + KB - 1) / KB; ++b) issue_kv(mt.seq, mt.h, b, mt.pos);
         }
-      } else if (!waited) {
-        pdl_wait();
-        pdl_trigger();
+      } else {
+        j += nloc;
       }
-      waited = true;
       __syncwarp();
+      tc::named_bar_sync(3, 64);   // both issuers done with this batch's meta
     }
-    if (!waited) {   // no items for this CTA
+    if ((int)blockIdx.x >= n_items) {   // no items for this CTA
       pdl_wait();
       pdl_trigger();
     }
-    if (pl == 0) l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);
+    if (!kvw && pl == 0) l2_prefetch_part(a.pf, blockIdx.x, gridDim.x);
     __syncwarp();
     return;
   }
@@ -307,6 +328,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
   pdl_trigger();
   const int g = tid / AD_GT, gt = tid % AD_GT;
   const int gw = gt >> 5, lane = tid & 31;
+  const uint32_t kv_issued_c = tc::smem_u32(kv_issued);
   AdScratch<D>& sc_ = scr[g];
   constexpr int DPL = D / 32;            // dims per lane of the new key's score
   for (int j = g; (int)blockIdx.x + j * (int)gridDim.x < n_items; j += AD_GROUPS) {
@@ -439,7 +461,7 @@ __global__ void __launch_bounds__(AD_THREADS, 1) attn_decode_pipe_kernel(const _
         const int it = kv0 + b, s = it % AD_STAGES;
         const int nk = min(KB, pos - b * KB);
         if (lane == 0)
-          while (atomicAdd(kv_issued, 0) <= it) {}
+          while (smem_atom_add(kv_issued_c, 0) <= it) {}
         __syncwarp();
         tc::mbar_wait(&kv_full[s], (it / AD_STAGES) & 1);
         const uint32_t kbase = tc::smem_u32(ring + (size_t)s * ad_stage_bytes<D, KB>());
