@@ -330,51 +330,6 @@ SLX_API int slx_attention_prefill(void* out, int ldo, const void* qkv, int ld_qk
                   int heads, int kv_heads, int head_dim, const void* tiles, const void* items,
                   int n_items, const void* k_cache, const void* v_cache, int max_ctx,
                   int pool_seqs, void* stream);
-/* ------------------------------------------------------------------ K1+K4: decode layer chain
- * One persistent launch runs a list of decode phases back to back (the projections and norms
- * between two attention launches of the decode step: o -> post-attention norm -> gate/up ->
- * down -> next layer's input norm -> q/k/v -> q/k/v reduction).  Replaces, like the separate
- * kernels above, the decode gap of the latency law (engine.py:888,909).  One CTA per SM; the
- * phases are separated by grid-wide barriers (counters in `sync`, zeroed once by the caller and
- * left zeroed), and the TMA producer of every CTA keeps streaming the weights of its NEXT GEMM
- * phase into its shared-memory ring across the barriers, so HBM does not idle while the
- * reductions and norms run.  Phases (M <= 64 token rows, bf16):
- *   SLX_CHAIN_GEMM_PIECES  A[M,K] . W^T over the tiled weight W (N rows, stacked included), every
- *                          256-row tile's K range cut in `splits` pieces, written to `part` in the
- *                          slx_gemm_bf16_splitk layout (the consumer phase reduces them);
- *   SLX_CHAIN_GEMM_SILU    whole tiles (splits = 1) of a gate/up weight with the SiLU*mul
- *                          epilogue -> C [M, N/2];
- *   SLX_CHAIN_NORM         slx_rmsnorm_fused semantics: x = round(x + pieces `sk`) (has_sk),
- *                          x += LoRA delta with v from the pieces (has_lora; ranks <= 16),
- *                          out = rmsnorm(x) * norm_w — bit-identical to slx_rmsnorm_fused;
- *   SLX_CHAIN_REDUCE       pieces `sk` of an N-column projection -> C (bf16, columns < n_main)
- *                          and C2 (fp32, columns >= n_main: the stacked LoRA shrink) —
- *                          bit-identical to slx_gemm_bf16's reduction of the same pieces. */
-enum { SLX_CHAIN_GEMM_PIECES = 0, SLX_CHAIN_GEMM_SILU = 1, SLX_CHAIN_NORM = 2, SLX_CHAIN_REDUCE = 3 };
-#define SLX_CHAIN_MAX_PHASES 8
-typedef struct slx_chain_phase {
-  int kind;
-  const void* A; int lda;        /* GEMM: activations [M, K] */
-  const void* W; int N; int K;   /* GEMM: SLX_W_TILED weight, N computed rows; REDUCE: N */
-  int splits;                    /* GEMM_PIECES: pieces per tile (1..16) */
-  float* part; size_t part_bytes;
-  void* C; int ldc;              /* GEMM_SILU / REDUCE output (bf16) */
-  float* C2; int ldc2;           /* REDUCE: fp32 side output */
-  void* x; int ldx;              /* NORM: residual stream (in place) */
-  void* out; int ldo;            /* NORM: normalised rows */
-  const void* norm_w; int d; float eps;
-  int has_sk; slx_splitk_in sk;  /* NORM / REDUCE: pieces in */
-  int has_lora; slx_lora_delta lora;
-} slx_chain_phase;
-/* Counter words `sync` must hold (zero-initialised once). */
-SLX_API size_t slx_decode_chain_sync_bytes(void);
-/* CTAs the chain launches for these phases (0: outside the kernel's envelope). */
-SLX_API int slx_decode_chain_ctas(const slx_chain_phase* phases, int n_phases, int M);
-/* `pf` (may be NULL): L2 prefetch of the next kernel's first bytes, issued by each CTA after its
- * last weight load.  `trace` (may be NULL, debug): per CTA 32 u64 globaltimer stamps. */
-SLX_API int slx_decode_chain(const slx_chain_phase* phases, int n_phases, int M, void* sync,
-                  const slx_l2_prefetch* pf, void* trace, void* stream);
-
 /* gu [n_tok, 2*ffn] in the blocked layout of SLX_EPI_SILU_MUL -> out [n_tok, ffn]. */
 SLX_API int slx_silu_mul_blocked(int dtype, void* out, int ldo, const void* gu, int ld_gu, int n_tok,
                          int ffn, void* stream);

@@ -66,19 +66,6 @@ class L2Prefetch(ctypes.Structure):
                 ("gemm_n", _i), ("gemm_k", _i), ("unit0", _i), ("units", _i)]
 
 
-CHAIN_GEMM_PIECES, CHAIN_GEMM_SILU, CHAIN_NORM, CHAIN_REDUCE = 0, 1, 2, 3
-CHAIN_MAX_PHASES = 8
-
-
-class ChainPhase(ctypes.Structure):
-    """slx_chain_phase: one phase of the decode layer chain (slx_decode_chain)."""
-    _fields_ = [("kind", _i), ("A", _p), ("lda", _i), ("W", _p), ("N", _i), ("K", _i),
-                ("splits", _i), ("part", _p), ("part_bytes", _sz), ("C", _p), ("ldc", _i),
-                ("C2", _p), ("ldc2", _i), ("x", _p), ("ldx", _i), ("out", _p), ("ldo", _i),
-                ("norm_w", _p), ("d", _i), ("eps", _f), ("has_sk", _i), ("sk", SplitKIn),
-                ("has_lora", _i), ("lora", LoraDelta)]
-
-
 # name -> (restype, argtypes): every symbol declared in include/slora_b200.h
 SIGNATURES = {
     "slx_status_string": (ctypes.c_char_p, [_i]),
@@ -129,10 +116,6 @@ SIGNATURES = {
     "slx_flash_prefill_tile_bytes": (_sz, []),
     "slx_flash_prefill_item_bytes": (_sz, []),
     "slx_attention_prefill": (_i, [_p, _i, _p, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i, _p]),
-    "slx_decode_chain_sync_bytes": (_sz, []),
-    "slx_decode_chain_ctas": (_i, [ctypes.POINTER(ChainPhase), _i, _i]),
-    "slx_decode_chain": (_i, [ctypes.POINTER(ChainPhase), _i, _i, _p, ctypes.POINTER(L2Prefetch),
-                              _p, _p]),
     "slx_silu_mul_blocked": (_i, [_i, _p, _i, _p, _i, _i, _i, _p]),
     "slx_argmax": (_i, [_i, _p, _p, _i, _i, _i, _p]),
     "slx_host_register": (_i, [_p, _sz]),

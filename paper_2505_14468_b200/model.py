@@ -221,13 +221,6 @@ class MultiLoraModel:
         self.l2_prefetch_mb = 16.0
         self.pf_gemm = True
         self._pf_cache: dict = {}
-        # decode: the projections and norms between two attention launches as ONE persistent
-        # launch per layer (slx_decode_chain: grid barriers between phases, the weight stream
-        # carried across them); the separate-kernel step above when the shape is outside it
-        self.use_chain = dtype == torch.bfloat16
-        self.chain_sync = (torch.zeros(ops.chain_sync_bytes() // 4, dtype=torch.int32,
-                                       device=self.device) if self.use_chain else None)
-        self.chain_trace = None   # debug: device int64 buffer for per-CTA phase stamps
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
         # prefill: the LoRA expand folded into the backbone GEMM as one extra K block
         self.lora_fold = True
@@ -653,8 +646,6 @@ class MultiLoraModel:
         T = tokens.numel()
         if T > self.max_tokens:
             raise ValueError(f"batch of {T} tokens exceeds max_tokens={self.max_tokens}")
-        if decode and self._chain_ok(T):
-            return self._forward_decode_chain(tokens, pos, seq, slot, logit_rows)
         if decode and self._decode_fast(T):
             return self._forward_decode(tokens, pos, seq, slot, logit_rows)
         return self._forward_general(tokens, pos, seq, slot, logit_rows, decode, segments)
@@ -737,102 +728,6 @@ class MultiLoraModel:
             pending = ops.gemm_splitk(mlp, w[p + "w_down"], S_dn, part_dn, prefetch=pf_dn)
         hn = torch.empty_like(x)
         ops.rmsnorm_fused(hn, x, w["final_norm"], cfg.rms_eps, pending)
-        if logit_rows is not None:
-            hn = hn.index_select(0, logit_rows)
-        return ops.gemm(hn, w["lm_head"], out_dtype=torch.float32)
-
-    def _chain_ok(self, T: int) -> bool:
-        """Decode shapes the layer chain covers: the fused bf16 step with every LoRA target's
-        shrink stacked in the projections (ranks <= 16) and hidden <= 4096."""
-        d = self.cfg.hidden
-        return (self.use_chain and self._decode_fast(T) and d <= 4096 and d % 256 == 0
-                and (not self.targets or (self.decode_lora == "stacked" and self.pool.max_rank <= 16
-                                          and set(self.targets) <= set(sum(self.stack.values(), ())))))
-
-    def _chain_splits(self, n_rows: int, k: int) -> int:
-        """Pieces per 256-row tile of a chain GEMM: every tile split evenly over the SMs (<= 8
-        pieces of >= 4 k-blocks), as the stream-K decode GEMM's uniform plan."""
-        n_tiles = -(-n_rows // 256)
-        s = min(8, max(1, self._sms // n_tiles))
-        while s > 1 and (k // 64) // s < 4:
-            s -= 1
-        return s
-
-    @property
-    def _sms(self) -> int:
-        if not hasattr(self, "_sm_count"):
-            self._sm_count = torch.cuda.get_device_properties(self.device).multi_processor_count
-        return self._sm_count
-
-    def _forward_decode_chain(self, tokens, pos, seq, slot, logit_rows):
-        """bf16 decode step as 2 launches per layer: attention (RoPE + KV append + attention +
-        fused q/k/v LoRA expand) and ONE chain of o -> post-norm (+ o LoRA) -> gate/up -> down ->
-        next input norm -> q/k/v -> q/k/v reduction (slx_decode_chain).  Same arithmetic as
-        _forward_decode (bit-identical pieces, reductions and norms)."""
-        cfg, w, dt, dev = self.cfg, self.w, self.dtype, self.device
-        T = tokens.numel()
-        d, qd, kvd = cfg.hidden, cfg.q_dim, cfg.kv_dim
-        L = cfg.layers
-        x = torch.empty((T, d), dtype=dt, device=dev)
-        h = torch.empty((T, d), dtype=dt, device=dev)
-        hn = torch.empty((T, d), dtype=dt, device=dev)
-        qkv = torch.empty((T, qd + 2 * kvd), dtype=dt, device=dev)
-        attn = torch.empty((T, qd), dtype=dt, device=dev)
-        mlp = torch.empty((T, self.ffn_pad), dtype=dt, device=dev)
-        wq0 = w["layers.0.w_qkv"]
-        n_qkv = wq0.n + wq0.n_extra
-        v_qkv = (torch.empty((T, wq0.n_extra), dtype=torch.float32, device=dev)
-                 if wq0.n_extra else None)
-        s_qkv = self._chain_splits(n_qkv, d)
-        wo0 = w["layers.0.wo"]
-        S_o = min(self.splitk_splits_o, (qd + 63) // 64)
-        S_dn = min(self.splitk_splits_dn, self.ffn_pad // 64)
-        part_qkv = torch.empty(ops.splitk_bytes(T, n_qkv, s_qkv) // 4, dtype=torch.float32, device=dev)
-        part_o = torch.empty(ops.splitk_bytes(T, wo0.n + wo0.n_extra, S_o) // 4, dtype=torch.float32,
-                             device=dev)
-        part_dn = torch.empty(ops.splitk_bytes(T, d, S_dn) // 4, dtype=torch.float32, device=dev)
-        qkv_cols = {"q": (0, qd, qd), "k": (qd, kvd, kvd), "v": (qd + kvd, kvd, kvd)}
-        trace = self.chain_trace
-        n_launch = [0]
-
-        def launch(phases, pf=None):
-            tp = None
-            if trace is not None:
-                tp = trace.data_ptr() + n_launch[0] * self._sms * 64 * 8
-            ops.decode_chain(phases, T, self.chain_sync, prefetch=pf, trace=tp)
-            n_launch[0] += 1
-
-        def qkv_phases(l):
-            ph, sk = ops.chain_gemm_pieces(h, w[f"layers.{l}.w_qkv"], s_qkv, part_qkv)
-            return [ph, ops.chain_reduce(sk, n_qkv, qkv, v_qkv)]
-
-        ops.embedding(x, w["embed"], tokens)
-        if self.targets:
-            ops.lora_plan_tokens(slot, self.pool.n_slots, self.lora_ws)
-        launch([ops.chain_norm(h, x, w["layers.0.input_norm"], cfg.rms_eps)] + qkv_phases(0),
-               self._pf(("kv", 0), self.k_cache[0], self.v_cache[0]))
-        for l in range(L):
-            p = f"layers.{l}."
-            d_qkv = (self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
-                     if "w_qkv" in self.stack else None)
-            ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
-                                      self.cos, self.sin, self.k_cache[l], self.v_cache[l],
-                                      lora=d_qkv, prefetch=self._pf(p + "wo", w[p + "wo"]))
-            ph_o, sk_o = ops.chain_gemm_pieces(attn, w[p + "wo"], S_o, part_o)
-            d_o = (self._delta(l, "wo", None, slot, {"o": (0, d, d)}) if "wo" in self.stack
-                   else None)
-            ph_dn, sk_dn = ops.chain_gemm_pieces(mlp, w[p + "w_down"], S_dn, part_dn)
-            phases = [ph_o, ops.chain_norm(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o),
-                      ops.chain_gemm_silu(h, w[p + "w_gu"], mlp), ph_dn]
-            if l + 1 < L:
-                phases.append(ops.chain_norm(h, x, w[f"layers.{l + 1}.input_norm"], cfg.rms_eps,
-                                             sk_dn))
-                phases += qkv_phases(l + 1)
-                pf = self._pf(("kv", l + 1), self.k_cache[l + 1], self.v_cache[l + 1])
-            else:
-                phases.append(ops.chain_norm(hn, x, w["final_norm"], cfg.rms_eps, sk_dn))
-                pf = self._pf("lm_head", w["lm_head"])
-            launch(phases, pf)
         if logit_rows is not None:
             hn = hn.index_select(0, logit_rows)
         return ops.gemm(hn, w["lm_head"], out_dtype=torch.float32)

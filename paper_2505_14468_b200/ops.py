@@ -12,8 +12,7 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import (CHAIN_GEMM_PIECES, CHAIN_GEMM_SILU, CHAIN_NORM, CHAIN_REDUCE, DT_BF16, DT_F32,
-                   EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED, ChainPhase,
+from ._lib import (DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED,
                    GemmTuning, L2Prefetch, LoraDelta, LoraTarget, SplitKIn, check)
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
@@ -561,82 +560,3 @@ def argmax(out, logits):
     check(_lib.load().slx_argmax(_dt(logits), _ptr(out), _ptr(logits), _ld(logits),
                                  logits.shape[0], logits.shape[1], _stream()), "slx_argmax")
     return out
-
-
-# ---------------------------------------------------------------------- decode layer chain
-def chain_gemm_pieces(a: torch.Tensor, w: "PackedWeight", splits: int, part: torch.Tensor):
-    """Chain phase: a @ w.T (main + stacked rows) as split-K pieces in ``part``; returns
-    (phase, slx_splitk_in of the pieces for the consuming phase / kernel)."""
-    if a.dtype != torch.bfloat16 or not isinstance(w, PackedWeight) or part.dtype != torch.float32:
-        raise ValueError("chain_gemm_pieces: bf16 activations, a packed weight, fp32 pieces")
-    M, K = a.shape
-    if K != w.k:
-        raise ValueError("chain_gemm_pieces: K mismatch")
-    ph = ChainPhase()
-    ph.kind, ph.A, ph.lda, ph.W = CHAIN_GEMM_PIECES, a.data_ptr(), _ld(a), w.data.data_ptr()
-    ph.N, ph.K, ph.splits = w.n + w.n_extra, K, int(splits)
-    ph.part, ph.part_bytes = part.data_ptr(), part.numel() * part.element_size()
-    sk = SplitKIn()
-    sk.part, sk.splits, sk.bm, sk.n_main = part.data_ptr(), int(splits), (M + 15) // 16 * 16, w.n
-    return ph, sk
-
-
-def chain_gemm_silu(a: torch.Tensor, w: "PackedWeight", out: torch.Tensor) -> ChainPhase:
-    """Chain phase: out = silu(gate) * up of the blocked gate/up weight (whole tiles)."""
-    if a.dtype != torch.bfloat16 or not isinstance(w, PackedWeight) or out.dtype != torch.bfloat16:
-        raise ValueError("chain_gemm_silu: bf16 activations / output and a packed weight")
-    ph = ChainPhase()
-    ph.kind, ph.A, ph.lda, ph.W = CHAIN_GEMM_SILU, a.data_ptr(), _ld(a), w.data.data_ptr()
-    ph.N, ph.K, ph.splits = w.n, a.shape[1], 1
-    ph.C, ph.ldc = out.data_ptr(), _ld(out)
-    return ph
-
-
-def chain_norm(out: torch.Tensor, x: torch.Tensor, w: torch.Tensor, eps: float, sk=None,
-               delta=None) -> ChainPhase:
-    """Chain phase with slx_rmsnorm_fused semantics (x += pieces, + LoRA delta, out = norm)."""
-    if x.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
-        raise ValueError("chain_norm: bf16 rows")
-    ph = ChainPhase()
-    ph.kind = CHAIN_NORM
-    ph.x, ph.ldx, ph.out, ph.ldo = x.data_ptr(), _ld(x), out.data_ptr(), _ld(out)
-    ph.norm_w, ph.d, ph.eps = w.data_ptr(), w.numel(), float(eps)
-    if sk is not None:
-        ph.has_sk, ph.sk = 1, sk
-    if delta is not None:
-        ph.has_lora, ph.lora = 1, delta
-    return ph
-
-
-def chain_reduce(sk, n_cols: int, out: torch.Tensor, side: torch.Tensor | None = None) -> ChainPhase:
-    """Chain phase: pieces ``sk`` of an n_cols projection -> out (bf16, columns < sk.n_main) and
-    side (fp32, the stacked shrink columns)."""
-    ph = ChainPhase()
-    ph.kind, ph.N = CHAIN_REDUCE, int(n_cols)
-    ph.has_sk, ph.sk = 1, sk
-    ph.C, ph.ldc = out.data_ptr(), _ld(out)
-    if side is not None:
-        if side.dtype != torch.float32:
-            raise ValueError("chain_reduce: fp32 side output")
-        ph.C2, ph.ldc2 = side.data_ptr(), _ld(side)
-    return ph
-
-
-def chain_sync_bytes() -> int:
-    return int(_lib.load().slx_decode_chain_sync_bytes())
-
-
-def chain_ctas(phases, M: int) -> int:
-    arr = (ChainPhase * len(phases))(*phases)
-    return int(_lib.load().slx_decode_chain_ctas(arr, len(phases), int(M)))
-
-
-@_op("chain", 1)
-def decode_chain(phases, M: int, sync: torch.Tensor, prefetch=None, trace=None) -> None:
-    """One persistent launch of the decode phases (slx_decode_chain); ``sync``: zeroed device
-    counters (left zeroed)."""
-    arr = (ChainPhase * len(phases))(*phases)
-    check(_lib.load().slx_decode_chain(arr, len(phases), int(M), _ptr(sync),
-                                       None if prefetch is None else ctypes.byref(prefetch),
-                                       None if trace is None else ctypes.c_void_p(trace),
-                                       _stream()), "slx_decode_chain")
