@@ -1,27 +1,29 @@
 // Prefill attention on the 5th-gen tensor cores: causal flash attention over the KV pool with
-// tcgen05.mma (TMEM accumulators) fed by TMA, warp-specialised, persistent.
+// tcgen05.mma (TMEM accumulators) fed by TMA, warp-specialised, persistent, two query tiles
+// per CTA in ping-pong.
 //
-// Work: a tile is <= 128 queries of one prefill segment; an item is (tile a, tile b, head) —
-// the host pairs a segment's long tile with its short one (prefill_plan), so items of one
-// segment cost the same and consecutive items share the segment's K/V in L2.  CTA c runs items
-// c, c + G, ... (G = #SMs), one item at a time, tile after tile.
+// Work: a tile is <= 128 queries of one prefill segment; an item is (tile a, tile b, head) with
+// tile b the segment's tile just before tile a (its keys a prefix of a's), so both tiles stream
+// the SAME K/V blocks (b stops two 64-key blocks earlier).  Items are ordered longest first and
+// CTA c runs items c, c + G, ... (G = #SMs).
 //
-// Per tile (128 query rows = the 128 TMEM lanes, head_dim 128, key blocks of 64):
-//   S_j = Q . K_j^T      tcgen05.mma M128 N64 K16 x8 (Q and K_j K-major, 128B-swizzled TMA
-//                        boxes) into one of two TMEM S buffers (64 columns each)
-//   P_j = exp2(S_j * scale - m)   softmax warpgroup: thread r owns query row r (tcgen05.ld of
-//                        its lane), causal mask, online max with LAZY rescale (the running max
-//                        used for P and for O/l only moves when a row's max grows by > 2^8, so
-//                        the common block never touches O), P written to shared memory as the
-//                        next MMA's K-major A operand (128B swizzle)
-//   O += P_j . V_j       tcgen05.mma M128 N128 K16 x4 with V_j as an MN-major B operand (the
-//                        pool's [pos][128] rows are d-contiguous) into the TMEM O accumulator
-// The MMA warp issues S_{j+1} before O += P_j V_j, so the tensor core computes the next scores
-// while the softmax warpgroup works on the current ones.  Roles (256 threads): warp 0 lane 0
-// TMA producer (Q once per tile, K and V through 4-stage rings), warp 1 lane 0 MMA issuer,
-// warps 4-7 softmax + epilogue (warp w reads TMEM lanes 32 (w % 4) ..).
-// TMEM: S0 [0, 64), S1 [64, 128), O [128, 256).
-// Query t of a tile starting at cache position p0 attends positions 0..p0+t (prefix + causal),
+// Per tile t in {a, b} (128 query rows = the 128 TMEM lanes, head_dim 128, key blocks of 64):
+//   S_j = Q_t . K_j^T     tcgen05.mma M128 N64 K16 x8 (K-major, 128B-swizzled TMA boxes) into one
+//                         of the tile's two TMEM S buffers (64 columns each)
+//   P_j = exp2(S_j * scale - m)   softmax warpgroup t: thread r owns query row r (tcgen05.ld of
+//                         its lane), causal mask, online max with LAZY rescale (the running max
+//                         used for P and O/l only moves when a row's max grows by > 2^8), P
+//                         written to shared memory as the next MMA's K-major A operand
+//   O_t += P_j . V_j      tcgen05.mma M128 N128 K16 x4, V_j as an MN-major B operand
+// Two softmax warpgroups (one per tile) give every SM sub-partition two softmax warps, so one
+// warp's exp2 / max / pack chain overlaps the other's, and each tile has its own MMA issuer
+// (P.V(j), then S(j+2)) — the tensor core computes one tile's scores while the other tile's
+// softmax runs; scores run two blocks ahead of the softmax.  Roles (352
+// threads): warp 0 lane 0 TMA producer (Q_a, Q_b once per item, K and V through 4-stage rings
+// shared by both tiles; one P buffer per tile), warps 1 / 2 lane 0 the MMA issuers of tiles a / b
+// (one issuer would convoy the tiles), warps 3-6 softmax + epilogue of tile a, warps 7-10 of
+// tile b (warp w reads TMEM lanes 32 (w % 4) ..).  TMEM: tile t at 256 t: S0 [0, 64), S1 [64, 128), O [128, 256).
+// Query i of a tile starting at cache position p0 attends positions 0..p0+i (prefix + causal),
 // k/v already appended by slx_rope_kv_write.
 #include "common.cuh"
 #include "gemm_host.h"
@@ -32,17 +34,20 @@ namespace {
 
 constexpr int FT_BQ = 128, FT_BK = 64, FT_D = 128;
 constexpr int FT_KST = 4, FT_VST = 4;
-constexpr int FT_THREADS = 256;
+constexpr int FT_PBUF = 1;                            // P buffers per tile
+constexpr int FT_THREADS = 352;
 constexpr int FT_Q_BYTES = FT_BQ * FT_D * 2;          // 32 KB: two [128][64] boxes
 constexpr int FT_KV_BYTES = FT_BK * FT_D * 2;         // 16 KB: two [64][64] boxes
 constexpr int FT_P_BYTES = FT_BQ * FT_BK * 2;         // 16 KB: [128][64]
-constexpr int FT_OFF_K = FT_Q_BYTES;
+constexpr int FT_OFF_K = 2 * FT_Q_BYTES;
 constexpr int FT_OFF_V = FT_OFF_K + FT_KST * FT_KV_BYTES;
-constexpr int FT_OFF_P = FT_OFF_V + FT_VST * FT_KV_BYTES;
-constexpr int FT_OFF_BAR = FT_OFF_P + 2 * FT_P_BYTES;
-constexpr int FT_NBAR = 2 + 2 * FT_KST + 2 * FT_VST + 2 + 2 + 2 + 2 + 1;
+constexpr int FT_OFF_P = FT_OFF_V + FT_VST * FT_KV_BYTES;     // [tile][FT_PBUF][16 KB]
+constexpr int FT_OFF_BAR = FT_OFF_P + 2 * FT_PBUF * FT_P_BYTES;
+// per tile: q_full, q_empty, s_full[2], s_free[2], p_full[2], p_empty[2], o_empty = 11
+constexpr int FT_TBAR = 11;
+constexpr int FT_NBAR = 2 * FT_KST + 2 * FT_VST + 2 * FT_TBAR + 1;
 constexpr size_t FT_SMEM = 1024 + FT_OFF_BAR + FT_NBAR * 8 + 16;
-constexpr uint32_t FT_TMEM_COLS = 256;
+constexpr uint32_t FT_TMEM_COLS = 512;
 constexpr float FT_RESCALE_LOG2 = 8.0f;   // lazy rescale threshold (P <= 2^8 stays exact in fp32/bf16)
 
 struct FtTile {
@@ -125,35 +130,39 @@ flash_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + FT_OFF_BAR);
-  uint64_t* q_full = bar;
-  uint64_t* q_empty = bar + 1;
-  uint64_t* k_full = bar + 2;
+  uint64_t* k_full = bar;
   uint64_t* k_empty = k_full + FT_KST;
   uint64_t* v_full = k_empty + FT_KST;
   uint64_t* v_empty = v_full + FT_VST;
-  uint64_t* s_full = v_empty + FT_VST;
-  uint64_t* s_free = s_full + 2;
-  uint64_t* p_full = s_free + 2;
-  uint64_t* p_empty = p_full + 2;
-  uint64_t* o_empty = p_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+  uint64_t* tb0 = v_empty + FT_VST;   // per-tile barriers: tb0 + FT_TBAR * t
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tb0 + 2 * FT_TBAR);
+  auto q_full = [&](int t) { return tb0 + FT_TBAR * t; };
+  auto q_empty = [&](int t) { return tb0 + FT_TBAR * t + 1; };
+  auto s_full = [&](int t, int b) { return tb0 + FT_TBAR * t + 2 + b; };
+  auto s_free = [&](int t, int b) { return tb0 + FT_TBAR * t + 4 + b; };
+  auto p_full = [&](int t, int b) { return tb0 + FT_TBAR * t + 6 + b; };
+  auto p_empty = [&](int t, int b) { return tb0 + FT_TBAR * t + 8 + b; };
+  auto o_empty = [&](int t) { return tb0 + FT_TBAR * t + 10; };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     tc::tma_prefetch_desc(&tq);
     tc::tma_prefetch_desc(&tk);
     tc::tma_prefetch_desc(&tv);
-    tc::mbar_init(q_full, 1);
-    tc::mbar_init(q_empty, 1);
-    for (int s = 0; s < FT_KST; ++s) { tc::mbar_init(&k_full[s], 1); tc::mbar_init(&k_empty[s], 1); }
-    for (int s = 0; s < FT_VST; ++s) { tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 1); }
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&s_full[b], 1);
-      tc::mbar_init(&s_free[b], 4);
-      tc::mbar_init(&p_full[b], 4);
-      tc::mbar_init(&p_empty[b], 1);
+    // K / V stages are released by both tiles' MMA warps (every block, used or not)
+    for (int s = 0; s < FT_KST; ++s) { tc::mbar_init(&k_full[s], 1); tc::mbar_init(&k_empty[s], 2); }
+    for (int s = 0; s < FT_VST; ++s) { tc::mbar_init(&v_full[s], 1); tc::mbar_init(&v_empty[s], 2); }
+    for (int t = 0; t < 2; ++t) {
+      tc::mbar_init(q_full(t), 1);
+      tc::mbar_init(q_empty(t), 1);
+      for (int b = 0; b < 2; ++b) {
+        tc::mbar_init(s_full(t, b), 1);
+        tc::mbar_init(s_free(t, b), 4);
+        tc::mbar_init(p_full(t, b), 4);
+        tc::mbar_init(p_empty(t, b), 1);
+      }
+      tc::mbar_init(o_empty(t), 4);
     }
-    tc::mbar_init(o_empty, 4);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, FT_TMEM_COLS);
@@ -170,212 +179,226 @@ flash_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       // ------------------------------------------------------------ TMA producer
       const uint64_t pol_q = tc::policy_evict_first();
       const uint64_t pol_kv = tc::policy_evict_last();   // re-read by the segment's other tiles
-      int qi = 0, ki = 0, vi = 0;
+      int qi[2] = {0, 0}, ki = 0, vi = 0;
       for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
         const FtItem item = a.items[it];
-        for (int tt = 0; tt < 2; ++tt) {
-          const int ti = tt == 0 ? item.ta : item.tb;
+        const FtTile ta = a.tiles[item.ta];
+        const int row0 = (ta.seq * a.Hkv + item.h / group) * a.max_ctx;
+        for (int t = 0; t < 2; ++t) {
+          const int ti = t == 0 ? item.ta : item.tb;
           if (ti < 0) continue;
-          const FtTile t = a.tiles[ti];
-          const int row0 = (t.seq * a.Hkv + item.h / group) * a.max_ctx;
-          tc::mbar_wait(q_empty, (qi & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(q_full, FT_Q_BYTES);
-          tc::tma_load_2d(sm, &tq, q_full, item.h * FT_D, t.tok0, pol_q);
-          tc::tma_load_2d(sm + FT_Q_BYTES / 2, &tq, q_full, item.h * FT_D + 64, t.tok0, pol_q);
-          ++qi;
-          const int nb = n_blocks(t);
-          for (int j = 0; j < nb; ++j) {
-            const int ks = ki % FT_KST;
-            tc::mbar_wait(&k_empty[ks], ((ki / FT_KST) & 1) ^ 1);
-            uint8_t* kd = sm + FT_OFF_K + ks * FT_KV_BYTES;
-            tc::mbar_arrive_expect_tx(&k_full[ks], FT_KV_BYTES);
-            tc::tma_load_2d(kd, &tk, &k_full[ks], 0, row0 + j * FT_BK, pol_kv);
-            tc::tma_load_2d(kd + FT_KV_BYTES / 2, &tk, &k_full[ks], 64, row0 + j * FT_BK, pol_kv);
-            ++ki;
-            const int vs = vi % FT_VST;
-            tc::mbar_wait(&v_empty[vs], ((vi / FT_VST) & 1) ^ 1);
-            uint8_t* vd = sm + FT_OFF_V + vs * FT_KV_BYTES;
-            tc::mbar_arrive_expect_tx(&v_full[vs], FT_KV_BYTES);
-            tc::tma_load_2d(vd, &tv, &v_full[vs], 0, row0 + j * FT_BK, pol_kv);
-            tc::tma_load_2d(vd + FT_KV_BYTES / 2, &tv, &v_full[vs], 64, row0 + j * FT_BK, pol_kv);
-            ++vi;
-          }
+          const int tok0 = a.tiles[ti].tok0;
+          tc::mbar_wait(q_empty(t), (qi[t] & 1) ^ 1);
+          uint8_t* qd = sm + t * FT_Q_BYTES;
+          tc::mbar_arrive_expect_tx(q_full(t), FT_Q_BYTES);
+          tc::tma_load_2d(qd, &tq, q_full(t), item.h * FT_D, tok0, pol_q);
+          tc::tma_load_2d(qd + FT_Q_BYTES / 2, &tq, q_full(t), item.h * FT_D + 64, tok0, pol_q);
+          ++qi[t];
+        }
+        const int nb = n_blocks(ta);
+        for (int j = 0; j < nb; ++j) {
+          const int ks = ki % FT_KST;
+          tc::mbar_wait(&k_empty[ks], ((ki / FT_KST) & 1) ^ 1);
+          uint8_t* kd = sm + FT_OFF_K + ks * FT_KV_BYTES;
+          tc::mbar_arrive_expect_tx(&k_full[ks], FT_KV_BYTES);
+          tc::tma_load_2d(kd, &tk, &k_full[ks], 0, row0 + j * FT_BK, pol_kv);
+          tc::tma_load_2d(kd + FT_KV_BYTES / 2, &tk, &k_full[ks], 64, row0 + j * FT_BK, pol_kv);
+          ++ki;
+          const int vs = vi % FT_VST;
+          tc::mbar_wait(&v_empty[vs], ((vi / FT_VST) & 1) ^ 1);
+          uint8_t* vd = sm + FT_OFF_V + vs * FT_KV_BYTES;
+          tc::mbar_arrive_expect_tx(&v_full[vs], FT_KV_BYTES);
+          tc::tma_load_2d(vd, &tv, &v_full[vs], 0, row0 + j * FT_BK, pol_kv);
+          tc::tma_load_2d(vd + FT_KV_BYTES / 2, &tv, &v_full[vs], 64, row0 + j * FT_BK, pol_kv);
+          ++vi;
         }
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp <= 2) {
     if (lane == 0) {
-      // ------------------------------------------------------------ MMA issuer
+      // ------------------------------------------------------------ MMA issuers
+      // warp 1 issues tile a's MMAs, warp 2 tile b's: each tile's S / P.V pipeline advances at
+      // its own softmax's pace (one issuer would convoy them).  Both walk every K / V block of
+      // the item and release it (count-2 barriers); the full-barrier waits keep a warp from
+      // releasing a stage's next use before the other released this one.
+      const int t = warp - 1;
       const uint32_t id_s = tc::idesc_bf16_f32(FT_BQ, FT_BK);
       const uint32_t id_o = tc::idesc_bf16_f32(FT_BQ, FT_D) | (1u << 16);   // B (V) MN-major
-      const uint32_t sq = tc::smem_u32(sm);
-      int qi = 0, ki = 0, vi = 0, si = 0, pi = 0, oi = 0;
-      auto pv = [&](int i) {   // O (+)= P_i . V_i
-        const int pb = pi & 1;
-        tc::mbar_wait(&p_full[pb], (pi >> 1) & 1);
-        if (i == 0) {
-          tc::mbar_wait(o_empty, (oi & 1) ^ 1);   // the previous tile's epilogue read O
-          ++oi;
-        }
-        const int vs = vi % FT_VST;
-        tc::mbar_wait(&v_full[vs], (vi / FT_VST) & 1);
-        tc::fence_after_sync();
-        const uint32_t pa = tc::smem_u32(sm + FT_OFF_P + pb * FT_P_BYTES);
-        const uint32_t va = tc::smem_u32(sm + FT_OFF_V + vs * FT_KV_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < FT_BK / 16; ++kk)
-          tc::mma_bf16_ss(tmem + 128, tc::smem_desc_sw128(pa + kk * 32),
-                          desc_mn_sw128(va + kk * 2048, FT_KV_BYTES / 2), id_o,
-                          (i > 0 || kk > 0) ? 1u : 0u);
-        tc::mma_commit(&v_empty[vs]);
-        tc::mma_commit(&p_empty[pb]);
-        ++vi;
-        ++pi;
-      };
+      const uint32_t sq = tc::smem_u32(sm + t * FT_Q_BYTES);
+      int qi = 0, si = 0, pi = 0, oi = 0, ki = 0, vi = 0;
       for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
         const FtItem item = a.items[it];
-        for (int tt = 0; tt < 2; ++tt) {
-          const int ti = tt == 0 ? item.ta : item.tb;
-          if (ti < 0) continue;
-          const int nb = n_blocks(a.tiles[ti]);
-          tc::mbar_wait(q_full, qi & 1);
-          for (int j = 0; j < nb; ++j) {
-            const int ks = ki % FT_KST, sb = si & 1;
-            tc::mbar_wait(&k_full[ks], (ki / FT_KST) & 1);
-            tc::mbar_wait(&s_free[sb], ((si >> 1) & 1) ^ 1);
-            tc::fence_after_sync();
+        const int nb = n_blocks(a.tiles[item.ta]);
+        const int ti = t == 0 ? item.ta : item.tb;
+        const int mine = ti >= 0 ? n_blocks(a.tiles[ti]) : 0;
+        if (mine > 0) tc::mbar_wait(q_full(t), qi & 1);
+        // scores of block jj (this tile), or just the release of K_jj
+        auto issue_s = [&](int jj) {
+          const int ks = ki % FT_KST;
+          tc::mbar_wait(&k_full[ks], (ki / FT_KST) & 1);
+          if (jj < mine) {
             const uint32_t kb = tc::smem_u32(sm + FT_OFF_K + ks * FT_KV_BYTES);
+            const int sb = si & 1;
+            tc::mbar_wait(s_free(t, sb), ((si >> 1) & 1) ^ 1);
+            tc::fence_after_sync();
 #pragma unroll
             for (int ks16 = 0; ks16 < FT_D / 16; ++ks16) {
               const uint32_t off = (uint32_t)((ks16 >> 2) * (FT_Q_BYTES / 2) + (ks16 & 3) * 32);
               const uint32_t offk = (uint32_t)((ks16 >> 2) * (FT_KV_BYTES / 2) + (ks16 & 3) * 32);
-              tc::mma_bf16_ss(tmem + sb * FT_BK, tc::smem_desc_sw128(sq + off),
+              tc::mma_bf16_ss(tmem + 256 * t + sb * FT_BK, tc::smem_desc_sw128(sq + off),
                               tc::smem_desc_sw128(kb + offk), id_s, ks16 > 0 ? 1u : 0u);
             }
-            tc::mma_commit(&k_empty[ks]);
-            tc::mma_commit(&s_full[sb]);
-            ++ki;
+            tc::mma_commit(s_full(t, sb));
             ++si;
-            if (j == nb - 1) {
-              tc::mma_commit(q_empty);
+            if (jj == mine - 1) {
+              tc::mma_commit(q_empty(t));
               ++qi;
             }
-            if (j >= 1) pv(j - 1);
           }
-          pv(nb - 1);
+          tc::mma_commit(&k_empty[ks]);
+          ++ki;
+        };
+        // scores run two blocks ahead of the softmax (two S buffers)
+        int sj = 0;
+        for (; sj < 2 && sj < nb; ++sj) issue_s(sj);
+        for (int j = 0; j < nb; ++j) {
+          const int vs = vi % FT_VST;
+          tc::mbar_wait(&v_full[vs], (vi / FT_VST) & 1);
+          if (j < mine) {   // O += P(j) . V(j)
+            const int pb = pi % FT_PBUF;
+            tc::mbar_wait(p_full(t, pb), (pi / FT_PBUF) & 1);
+            if (j == 0) {
+              tc::mbar_wait(o_empty(t), (oi & 1) ^ 1);   // the previous tile's epilogue read O
+              ++oi;
+            }
+            tc::fence_after_sync();
+            const uint32_t va = tc::smem_u32(sm + FT_OFF_V + vs * FT_KV_BYTES);
+            const uint32_t pa = tc::smem_u32(sm + FT_OFF_P + (FT_PBUF * t + pb) * FT_P_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < FT_BK / 16; ++kk)
+              tc::mma_bf16_ss(tmem + 256 * t + 128, tc::smem_desc_sw128(pa + kk * 32),
+                              desc_mn_sw128(va + kk * 2048, FT_KV_BYTES / 2), id_o,
+                              (j > 0 || kk > 0) ? 1u : 0u);
+            tc::mma_commit(p_empty(t, pb));
+            ++pi;
+          }
+          tc::mma_commit(&v_empty[vs]);
+          ++vi;
+          if (sj < nb) issue_s(sj++);
         }
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else {
     // ------------------------------------------------------------ softmax + epilogue
+    const int t = (warp - 3) >> 2;                       // tile slot of this warpgroup
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;                        // query row = TMEM lane
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tbase = tmem + 256 * t;
     const float sl2 = a.scale_log2;
     int si = 0, pi = 0;
     for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
       const FtItem item = a.items[it];
-      for (int tt = 0; tt < 2; ++tt) {
-        const int ti = tt == 0 ? item.ta : item.tb;
-        if (ti < 0) continue;
-        const FtTile t = a.tiles[ti];
-        const int nb = n_blocks(t);
-        const int n_keys = t.pos0 + t.nq;
-        const int lim = min(t.pos0 + r, n_keys - 1);   // last visible key of this row
-        float m_used = -INFINITY, l = 0.f;
-        for (int j = 0; j < nb; ++j) {
-          const int sb = si & 1;
-          tc::mbar_wait(&s_full[sb], (si >> 1) & 1);
-          tc::fence_after_sync();
-          float s[FT_BK];
-          tmem_ld32(tmem + lane_off + sb * FT_BK, s);
-          tmem_ld32(tmem + lane_off + sb * FT_BK + 32, s + 32);
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&s_free[sb]);
-          ++si;
-          const int k0 = j * FT_BK;
-          float mx = -INFINITY;
-#pragma unroll
-          for (int c = 0; c < FT_BK; ++c) {
-            if (k0 + c > lim) s[c] = -INFINITY;
-            mx = fmaxf(mx, s[c]);
-          }
-          const float m_new = fmaxf(m_used, mx);
-          if (j == 0) {
-            m_used = m_new;
-          } else {
-            const bool need = (m_new - m_used) * sl2 > FT_RESCALE_LOG2;
-            if (__any_sync(0xffffffffu, need)) {
-              // O holds P_0..P_{j-1} . V: wait for the last PV before rescaling it in TMEM
-              const int lp = pi - 1;
-              tc::mbar_wait(&p_empty[lp & 1], (lp >> 1) & 1);
-              tc::fence_after_sync();
-              const float corr = need ? ex2_approx((m_used - m_new) * sl2) : 1.f;
-              if (need) {
-                m_used = m_new;
-                l *= corr;
-              }
-#pragma unroll 1
-              for (int c0 = 0; c0 < FT_D; c0 += 32) {
-                float o[32];
-                tmem_ld32(tmem + lane_off + 128 + c0, o);
-#pragma unroll
-                for (int e = 0; e < 32; ++e) o[e] *= corr;
-                tmem_st32(tmem + lane_off + 128 + c0, o);
-              }
-            }
-          }
-          const float msl = m_used * sl2;
-          uint32_t pk[FT_BK / 2];
-          float ls = 0.f;
-#pragma unroll
-          for (int c = 0; c < FT_BK; c += 2) {
-            const float p0 = ex2_approx(fmaf(s[c], sl2, -msl));
-            const float p1 = ex2_approx(fmaf(s[c + 1], sl2, -msl));
-            ls += p0 + p1;
-            pk[c / 2] = pack2(p0, p1);
-          }
-          l += ls;
-          const int pb = pi & 1;
-          if (pi >= 2) tc::mbar_wait(&p_empty[pb], ((pi >> 1) - 1) & 1);   // PV_{j-2} read it
-          uint8_t* prow = sm + FT_OFF_P + pb * FT_P_BYTES + r * 128;
-#pragma unroll
-          for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
-                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&p_full[pb]);
-          ++pi;
-        }
-        // epilogue: O / l of this row -> bf16 out
-        const int lp = pi - 1;
-        tc::mbar_wait(&p_empty[lp & 1], (lp >> 1) & 1);
+      const int ti = t == 0 ? item.ta : item.tb;
+      if (ti < 0) continue;
+      const FtTile tl = a.tiles[ti];
+      const int nb = n_blocks(tl);
+      const int n_keys = tl.pos0 + tl.nq;
+      const int lim = min(tl.pos0 + r, n_keys - 1);   // last visible key of this row
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < nb; ++j) {
+        const int sb = si & 1;
+        tc::mbar_wait(s_full(t, sb), (si >> 1) & 1);
         tc::fence_after_sync();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        bf16* orow = a.out + (size_t)(t.tok0 + r) * a.ldo + (size_t)item.h * FT_D;
-#pragma unroll 1
-        for (int c0 = 0; c0 < FT_D; c0 += 32) {
-          float o[32];
-          tmem_ld32(tmem + lane_off + 128 + c0, o);
-          if (r < t.nq) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              *reinterpret_cast<uint4*>(orow + c0 + 8 * q) =
-                  make_uint4(pack2(o[8 * q] * inv, o[8 * q + 1] * inv),
-                             pack2(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
-                             pack2(o[8 * q + 4] * inv, o[8 * q + 5] * inv),
-                             pack2(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
-          }
-        }
+        float s[FT_BK];
+        tmem_ld32(tbase + lane_off + sb * FT_BK, s);
+        tmem_ld32(tbase + lane_off + sb * FT_BK + 32, s + 32);
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(o_empty);
+        if (lane == 0) tc::mbar_arrive(s_free(t, sb));
+        ++si;
+        const int k0 = j * FT_BK;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < FT_BK; ++c) {
+          if (k0 + c > lim) s[c] = -INFINITY;
+          mx = fmaxf(mx, s[c]);
+        }
+        const float m_new = fmaxf(m_used, mx);
+        if (j == 0) {
+          m_used = m_new;
+        } else {
+          const bool need = (m_new - m_used) * sl2 > FT_RESCALE_LOG2;
+          if (__any_sync(0xffffffffu, need)) {
+            // O holds P_0..P_{j-1} . V: wait for the last PV before rescaling it in TMEM
+            const int lp = pi - 1;
+            tc::mbar_wait(p_empty(t, lp % FT_PBUF), (lp / FT_PBUF) & 1);
+            tc::fence_after_sync();
+            const float corr = need ? ex2_approx((m_used - m_new) * sl2) : 1.f;
+            if (need) {
+              m_used = m_new;
+              l *= corr;
+            }
+#pragma unroll 1
+            for (int c0 = 0; c0 < FT_D; c0 += 32) {
+              float o[32];
+              tmem_ld32(tbase + lane_off + 128 + c0, o);
+#pragma unroll
+              for (int e = 0; e < 32; ++e) o[e] *= corr;
+              tmem_st32(tbase + lane_off + 128 + c0, o);
+            }
+          }
+        }
+        const float msl = m_used * sl2;
+        uint32_t pk[FT_BK / 2];
+        float ls = 0.f;
+#pragma unroll
+        for (int c = 0; c < FT_BK; c += 2) {
+          const float p0 = ex2_approx(fmaf(s[c], sl2, -msl));
+          const float p1 = ex2_approx(fmaf(s[c + 1], sl2, -msl));
+          ls += p0 + p1;
+          pk[c / 2] = pack2(p0, p1);
+        }
+        l += ls;
+        const int pb = pi % FT_PBUF;
+        if (pi >= FT_PBUF)   // the P.V that last read this buffer has completed
+          tc::mbar_wait(p_empty(t, pb), ((pi - FT_PBUF) / FT_PBUF) & 1);
+        uint8_t* prow = sm + FT_OFF_P + (FT_PBUF * t + pb) * FT_P_BYTES + r * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(prow + ((c ^ (r & 7)) << 4)) =
+              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_full(t, pb));
+        ++pi;
       }
+      // epilogue: O / l of this row -> bf16 out
+      const int lp = pi - 1;
+      tc::mbar_wait(p_empty(t, lp % FT_PBUF), (lp / FT_PBUF) & 1);
+      tc::fence_after_sync();
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      bf16* orow = a.out + (size_t)(tl.tok0 + r) * a.ldo + (size_t)item.h * FT_D;
+#pragma unroll 1
+      for (int c0 = 0; c0 < FT_D; c0 += 32) {
+        float o[32];
+        tmem_ld32(tbase + lane_off + 128 + c0, o);
+        if (r < tl.nq) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            *reinterpret_cast<uint4*>(orow + c0 + 8 * q) =
+                make_uint4(pack2(o[8 * q] * inv, o[8 * q + 1] * inv),
+                           pack2(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
+                           pack2(o[8 * q + 4] * inv, o[8 * q + 5] * inv),
+                           pack2(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
+        }
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(o_empty(t));
     }
   }
   tc::fence_before_sync();

@@ -516,21 +516,27 @@ def rope_attention_decode(out, qkv, heads, kv_heads, head_dim, tok_pos, tok_seq,
 def prefill_plan(segments, heads: int, device, bq: int | None = None):
     """[(tok0, n, seq, pos0)] segments -> the flash prefill's tile table (int32 [n_tiles, 4] of
     <= bq queries of one segment) and work items (int32 [n_items, 4] = (tile_a, tile_b, head,
-    0)): per segment and head, its k-th longest tile paired with its k-th shortest, so the
-    items of a segment cost the same; items are segment-major (consecutive items share a
-    segment's K/V in L2), longest segments first."""
+    0)): per segment and head, consecutive tiles are paired (tile_b = the tile before tile_a,
+    so its keys are a prefix of a's and both stream the same K/V blocks in one CTA); items are
+    ordered by cost (key blocks of both tiles), longest first, so the persistent CTAs' strided
+    shares come out even."""
     if bq is None:
         bq = int(_lib.load().slx_flash_prefill_tile_queries())
     tiles, items = [], []
-    for tok0, n, seq, pos0 in sorted(segments, key=lambda s: -(s[3] + s[1])):
+    for tok0, n, seq, pos0 in segments:
         ids = []
         for q in range(0, n, bq):
             ids.append(len(tiles))
             tiles.append((tok0 + q, min(bq, n - q), seq, pos0 + q))
-        pairs = [(ids[len(ids) - 1 - k], ids[k] if ids[k] != ids[len(ids) - 1 - k] else -1)
-                 for k in range((len(ids) + 1) // 2)]
+        pairs = [(ids[k + 1], ids[k]) if k + 1 < len(ids) else (ids[k], -1)
+                 for k in range(0, len(ids), 2)]
         for h in range(heads):
             items += [(a, b, h, 0) for a, b in pairs]
+
+    def cost(it):
+        a, b = tiles[it[0]], (tiles[it[1]] if it[1] >= 0 else None)
+        return -(-(a[3] + a[1]) // 64) + (-(-(b[3] + b[1]) // 64) if b else 0)
+    items.sort(key=lambda it: -cost(it))
     t = torch.tensor(tiles, dtype=torch.int32).reshape(-1, 4)
     it = torch.tensor(items, dtype=torch.int32).reshape(-1, 4)
     return t.to(device), it.to(device)
