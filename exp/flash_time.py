@@ -42,6 +42,8 @@ if "dbg" in _lib.LIB_PATH:
     st = buf.reshape(1024, 8)[:400].astype(np.int64)
     d = np.diff(st[:, 0])
     print("block period (clk) median", np.median(d[1:300]), "mean", d[1:300].mean())
+    tokw = st[1:300, 5] - st[1:300, 2]
+    print("  token wait     median", np.median(tokw), "mean", tokw.mean(), "(0 if no token build)")
     for name, a, b in (("wait S", 0, 1), ("tmem ld", 1, 2), ("compute", 2, 3), ("P store+fence", 3, 4), ("arrive->next", 4, 0)):
         if name == "arrive->next":
             v = st[1:300, 0] - st[0:299, 4]

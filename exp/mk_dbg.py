@@ -12,5 +12,6 @@ src = src.replace("        if (pi >= FT_PBUF)   // the P.V that last read this b
                   f"        if ({T} && si < 1001) g_dbg[(si - 1) * 8 + 3] = clock64();\n        if (pi >= FT_PBUF)   // the P.V that last read this buffer has completed")
 src = src.replace("        if (lane == 0) tc::mbar_arrive(p_full(t, pb));",
                   f"        if ({T} && si < 1001) g_dbg[(si - 1) * 8 + 4] = clock64();\n        if (lane == 0) tc::mbar_arrive(p_full(t, pb));")
+src = src.replace("          ++tw;\n        }", "          ++tw;\n        }\n        if (" + T + " && si < 1001) g_dbg[(si - 1) * 8 + 5] = clock64();")
 src += '\nextern "C" SLX_API int slx_dbg_copy(void* host, size_t n) {\n  return cudaMemcpyFromSymbol(host, slx::g_dbg, n) == cudaSuccess ? 0 : -5;\n}\n'
 open(sys.argv[2], "w").write(src)

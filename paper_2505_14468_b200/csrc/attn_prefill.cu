@@ -72,6 +72,28 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// (d0, d1) = (a0, a1) * (b, b) + (c, c) as one FFMA2
+__device__ __forceinline__ void fma2s(float& d0, float& d1, float a0, float a1, float b, float c) {
+  uint64_t d, av, bv, cv;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(av) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(bv) : "f"(b));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(cv) : "f"(c));
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(av), "l"(bv), "l"(cv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+}
+// (s0, s1) += (a0, a1) as one FADD2
+__device__ __forceinline__ void add2(float& s0, float& s1, float a0, float a1) {
+  uint64_t d, sv, av;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(sv) : "f"(s0), "f"(s1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(av) : "f"(a0), "f"(a1));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(sv), "l"(av));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(d));
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
   asm volatile(
@@ -320,12 +342,19 @@ flash_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         if (lane == 0) tc::mbar_arrive(s_free(t, sb));
         ++si;
         const int k0 = j * FT_BK;
-        float mx = -INFINITY;
+        if (k0 + FT_BK - 1 > lim) {   // only blocks on the diagonal (or past the end) mask keys
 #pragma unroll
-        for (int c = 0; c < FT_BK; ++c) {
-          if (k0 + c > lim) s[c] = -INFINITY;
-          mx = fmaxf(mx, s[c]);
+          for (int c = 0; c < FT_BK; ++c)
+            if (k0 + c > lim) s[c] = -INFINITY;
         }
+        float mq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {   // four independent 3-input max chains
+          mq[q] = fmaxf(s[16 * q], s[16 * q + 1]);
+#pragma unroll
+          for (int c = 16 * q + 2; c < 16 * q + 16; c += 2) mq[q] = max3f(mq[q], s[c], s[c + 1]);
+        }
+        const float mx = max3f(fmaxf(mq[0], mq[1]), mq[2], mq[3]);
         const float m_new = fmaxf(m_used, mx);
         if (j == 0) {
           m_used = m_new;
@@ -353,15 +382,16 @@ flash_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         const float msl = m_used * sl2;
         uint32_t pk[FT_BK / 2];
-        float ls = 0.f;
+        float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
         for (int c = 0; c < FT_BK; c += 2) {
-          const float p0 = ex2_approx(fmaf(s[c], sl2, -msl));
-          const float p1 = ex2_approx(fmaf(s[c + 1], sl2, -msl));
-          ls += p0 + p1;
+          float x0, x1;
+          fma2s(x0, x1, s[c], s[c + 1], sl2, -msl);
+          const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+          add2(ls0, ls1, p0, p1);
           pk[c / 2] = pack2(p0, p1);
         }
-        l += ls;
+        l += ls0 + ls1;
         const int pb = pi % FT_PBUF;
         if (pi >= FT_PBUF)   // the P.V that last read this buffer has completed
           tc::mbar_wait(p_empty(t, pb), ((pi - FT_PBUF) / FT_PBUF) & 1);
