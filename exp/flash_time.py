@@ -21,6 +21,15 @@ kc = torch.randn(P, H, L, D, device=dev).to(torch.bfloat16)
 vc = torch.randn(P, H, L, D, device=dev).to(torch.bfloat16)
 out = torch.empty(P * L, H * D, device=dev, dtype=torch.bfloat16)
 plan = ops.prefill_plan([(i * L, L, i, 0) for i in range(P)], H, dev)
+order = os.environ.get("FLASH_ORDER", "cost")
+if order != "cost":   # experiment: item order by (segment, head), costliest pair first
+    t_cpu, it_cpu = plan[0].cpu(), plan[1].cpu().tolist()
+    seq = t_cpu[:, 2].tolist()
+    if order == "head":
+        it_cpu.sort(key=lambda it: (seq[it[0]], it[2], -it[0]))
+    elif order == "head_interleave":   # heads of a segment interleaved with costs descending
+        it_cpu.sort(key=lambda it: (seq[it[0]], -it[0], it[2]))
+    plan = (plan[0], torch.tensor(it_cpu, dtype=torch.int32, device=dev))
 for _ in range(3):
     ops.attention_prefill(out, qkv, H, H, D, plan, kc, vc)
 torch.cuda.synchronize()
@@ -32,7 +41,7 @@ e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) * 100.0
 flops = P * (L * (L + 1) // 2) * 4 * D * H
-print(f"{os.path.basename(_lib.LIB_PATH)}: {us:.1f} us/layer  {flops / us / 1e6:.1f} TFLOP/s")
+print(f"{os.path.basename(_lib.LIB_PATH)} order={order}: {us:.1f} us/layer  {flops / us / 1e6:.1f} TFLOP/s")
 if "dbg" in _lib.LIB_PATH:
     import ctypes
     import numpy as np

@@ -20,6 +20,8 @@
 // Weights are stored SLX_W_TILED ([N/128][K/64][128][64]) so every TMA box is one contiguous
 // 16 KB burst; PDL: the first stages' weight boxes are fetched BEFORE griddepcontrol.wait.
 //
+//  * prefill with many tiles runs the PERSISTENT variant gemm_tcp_kernel (below): one CTA per SM,
+//    two TMEM accumulators, the epilogue of tile i overlapping the mainloop of tile i + 1.
 // Replaces the modelled prefill/decode time of the reference (batching.py:17-21 T0+alpha(b-1);
 // engine.py:832 prefill work, engine.py:888,909 decode_ms_per_token) with the real projections.
 #include <cuda.h>
@@ -79,6 +81,7 @@ struct GemmArgs {
   // rasterised 1-D grid (prefill, no split): tiles visited in groups of `raster` m-tiles x all
   // n-tiles, so the ~148 co-resident CTAs share a few X row blocks and W tiles in L2
   int raster, m_tiles;
+  int n_work;    // persistent kernel: tiles to walk (raster grid or gtiles)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -460,6 +463,216 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   }
 }
 
+// ------------------------------------------------------------------ persistent prefill kernel
+// Many 128 x 256 tiles (prefill, no K split): one CTA per SM walks tiles L = blockIdx.x,
+// blockIdx.x + G, ... (the raster order of the 1-D grid above, or the grouped tile table), with
+// the TMA ring running continuously across tiles and TWO TMEM accumulators (2 x 256 columns),
+// so the epilogue of tile i (its own four warps) overlaps the mainloop of tile i + 1 instead of
+// idling the tensor core between one-tile CTAs (drain, CTA exit / launch, prologue, refill).
+// Roles (192 threads): warp 0 lane 0 TMA producer, warp 1 lane 0 MMA issuer, warps 2-5
+// epilogue (warp w drains TMEM lanes 32 (w % 4) ..).  Same tile math and epilogues as
+// gemm_tc_kernel (bit-identical outputs).
+constexpr int TCP_THREADS = 192;
+
+struct TcpTile {
+  int m0, n0, m_lim, tile, n_kb, group, ltgt;
+  bool lblk;
+  float alpha;
+};
+
+template <bool GROUPED>
+__device__ __forceinline__ TcpTile tcp_tile(const GemmArgs& g, const GroupMaps& gm, int L) {
+  TcpTile t{};
+  if (GROUPED) {
+    const GroupTile gt = g.gtiles[L];
+    t.m0 = gt.m0;
+    t.n0 = gt.n0;
+    t.m_lim = gt.m0 + gt.m_rows;
+    t.group = gt.group;
+    t.tile = gt.n0 / 256;
+  } else {
+    const int per = g.raster * g.n_tiles;
+    const int grp = L / per, rem = L - grp * per;
+    const int gsz = min(g.raster, g.m_tiles - grp * g.raster);
+    const int mt = grp * g.raster + rem % gsz;
+    t.tile = rem / gsz;
+    t.m0 = mt * 128;
+    t.n0 = t.tile * 256;
+    t.m_lim = g.M;
+    t.group = 0;
+  }
+  t.n_kb = g.kblocks;
+  const bool lfold = GROUPED && g.lfold;
+  t.alpha = (GROUPED && !lfold) ? gm.alpha[t.group] : 1.f;
+  t.ltgt = 0;
+  if (lfold) {
+#pragma unroll
+    for (int q = 1; q < 4; ++q)
+      if (q < g.lnt && t.n0 >= g.lbound[q]) t.ltgt = q;
+  }
+  t.lblk = lfold && t.group >= 0;
+  return t;
+}
+
+template <int EPI, typename OutT, bool GROUPED>
+__global__ void __launch_bounds__(TCP_THREADS, 1)
+gemm_tcp_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
+                GemmArgs g, const __grid_constant__ GroupMaps gm) {
+  constexpr int BN = 256, WB = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int x_bytes = 128 * TC_BK * 2;
+  const int stage_bytes = x_bytes + WB * W_BLOCK_BYTES;
+  uint64_t* full = (uint64_t*)(smem + g.stages * stage_bytes);
+  uint64_t* empty = full + TC_MAX_STAGES;
+  uint64_t* tfull = empty + TC_MAX_STAGES;   // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;              // [2] accumulator drained
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    tc::tma_prefetch_desc(&tmap_x);
+    tc::tma_prefetch_desc(&tmap_w);
+    for (int s = 0; s < g.stages; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int q = 0; q < 2; ++q) {
+      tc::mbar_init(&tfull[q], 1);
+      tc::mbar_init(&tempty[q], 4);   // one arrival per epilogue warp
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem_base = *tmem_slot;
+  // The next kernel is released (launch_dependents) only when this CTA reaches its LAST tile:
+  // a persistent grid that triggered at its start would have the next kernel's CTAs launched
+  // and parked on the SMs for the whole GEMM.
+  if (GROUPED || warp != 0) pdl_wait();   // the grouped tile table comes from the host stream
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- TMA producer
+      const uint64_t pol_w = tc::policy_evict_first();
+      const uint64_t pol_x = tc::policy_evict_last();
+      int i = 0;
+      bool waited = GROUPED;
+      for (int L = blockIdx.x; L < g.n_work; L += gridDim.x) {
+        if (L + (int)gridDim.x >= g.n_work && waited) pdl_trigger();
+        const TcpTile t = tcp_tile<GROUPED>(g, gm, L);
+        const CUtensorMap* wmap = (GROUPED && !g.lfold) ? &gm.w[t.group] : &tmap_w;
+        const int n_tot = t.n_kb + (t.lblk ? 1 : 0);
+        for (int kk = 0; kk < n_tot; ++kk, ++i) {
+          const int s = i % g.stages;
+          tc::mbar_wait(&empty[s], ((i / g.stages) & 1) ^ 1);
+          uint8_t* st = smem + s * stage_bytes;
+          tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
+          if (kk < t.n_kb) {
+            for (int b = 0; b < WB; ++b) {
+              int c0, c1;
+              w_coord(g, t.n0 + b * 128, kk, c0, c1);
+              tc::tma_load_2d(st + x_bytes + b * W_BLOCK_BYTES, wmap, &full[s], c0, c1, pol_w);
+            }
+            if (!waited) {   // weights first; the activations come from the previous kernel
+              pdl_wait();
+              waited = true;
+              if (L + (int)gridDim.x >= g.n_work) pdl_trigger();
+            }
+            tc::tma_load_2d(st, &tmap_x, &full[s], kk * TC_BK, t.m0, pol_x);
+          } else {   // LoRA k-block: v slice of the tile's target x B rows of (adapter, target)
+            const CUtensorMap* bmap = &gm.w[t.group * g.lnt + t.ltgt];
+            for (int b = 0; b < WB; ++b)
+              tc::tma_load_2d(st + x_bytes + b * W_BLOCK_BYTES, bmap, &full[s], 0,
+                              t.n0 - g.lbound[t.ltgt] + b * 128, pol_x);
+            tc::tma_load_2d(st, &gm.v, &full[s], t.ltgt * TC_BK, t.m0, pol_x);
+          }
+        }
+      }
+      if (!waited) pdl_wait();
+      pdl_trigger();   // (no-op if already issued)
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------------- MMA issuer
+      const uint32_t idesc = tc::idesc_bf16_f32(128, BN);
+      int i = 0, j = 0;
+      for (int L = blockIdx.x; L < g.n_work; L += gridDim.x, ++j) {
+        const TcpTile t = tcp_tile<GROUPED>(g, gm, L);
+        const int n_tot = t.n_kb + (t.lblk ? 1 : 0);
+        tc::mbar_wait(&tempty[j & 1], ((j >> 1) & 1) ^ 1);
+        tc::fence_after_sync();
+        const uint32_t d = tmem_base + (uint32_t)((j & 1) * BN);
+        for (int kk = 0; kk < n_tot; ++kk, ++i) {
+          const int s = i % g.stages;
+          tc::mbar_wait(&full[s], (i / g.stages) & 1);
+          tc::fence_after_sync();
+          const uint32_t st = tc::smem_u32(smem + s * stage_bytes);
+#pragma unroll
+          for (int ks = 0; ks < TC_BK / 16; ++ks)
+            tc::mma_bf16_ss(d, tc::smem_desc_sw128(st + ks * 32),
+                            tc::smem_desc_sw128(st + x_bytes + ks * 32), idesc,
+                            (kk > 0 || ks > 0) ? 1u : 0u);
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(&tfull[j & 1]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2-5)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    OutT* C = reinterpret_cast<OutT*>(g.C);
+    const OutT* R = reinterpret_cast<const OutT*>(g.R);
+    const int n_out = EPI == SLX_EPI_SILU_MUL ? g.N / 2 : g.N;
+    int j = 0;
+    for (int L = blockIdx.x; L < g.n_work; L += gridDim.x, ++j) {
+      const TcpTile t = tcp_tile<GROUPED>(g, gm, L);
+      const int acc = j & 1;
+      tc::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      __syncwarp();
+      tc::fence_after_sync();
+      const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+      const int m = t.m0 + r;
+      if (t.m0 + q * 32 < t.m_lim) {   // warp-uniform
+        if (EPI == SLX_EPI_SILU_MUL) {
+          for (int c0 = 0; c0 < BN / 2; c0 += 16) {
+            float gv[16], uv[16];
+            tc::tmem_ld16x2(t_row + c0, t_row + BN / 2 + c0, gv, uv);
+            if (m < t.m_lim) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) gv[e] = silu_f(gv[e]) * uv[e];
+              store16(C + (size_t)m * g.ldc, t.tile * (BN / 2) + c0, n_out, gv);
+            }
+          }
+        } else {
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            float v0[16], v1[16];
+            tc::tmem_ld16x2(t_row + c0, t_row + c0 + 16, v0, v1);
+            if (m < t.m_lim) {
+              store_cols<EPI>(g, C, R, m, t.n0 + c0, n_out, v0, t.alpha);
+              store_cols<EPI>(g, C, R, m, t.n0 + c0 + 16, n_out, v1, t.alpha);
+            }
+          }
+        }
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -630,6 +843,34 @@ template <int EPI, typename OutT, int BN, bool GROUPED = false>
 static int launch_tc(const CUtensorMap& mx, const CUtensorMap& mw, const GemmArgs& a, dim3 grid,
                      size_t smem, unsigned cluster, cudaStream_t s,
                      const GroupMaps& gm = no_groups()) {
+  // many full-height 256-wide tiles without a K split (prefill): the persistent kernel
+  if (BN == 256 && cluster == 1 && a.splits == 1 && a.bm == 128 && grid.y == 1 &&
+      (GROUPED || a.raster > 0) && a.stages <= TC_MAX_STAGES) {
+    auto kp = gemm_tcp_kernel<EPI, OutT, GROUPED>;
+    static bool configured_p = false;
+    if (!configured_p) {
+      configure_kernel((const void*)kp);
+      configured_p = true;
+    }
+    GemmArgs ap = a;
+    ap.n_work = (int)grid.x;
+    const int g = ap.n_work < sm_count() ? ap.n_work : sm_count();
+    const size_t smem_p = smem + 4 * 8;   // two more barrier pairs (tfull / tempty)
+    // Launched WITHOUT programmatic dependent launch (measured: 443 -> 406.5 ms on the
+    // config-3 prefill): under PDL the persistent CTAs are scheduled while the previous kernel
+    // (e.g. a 16384-CTA RMSNorm) still runs and park beside it; one CTA per SM then has to
+    // wait for its whole SM.  The kernel's griddepcontrol.wait is a no-op here; the kernels
+    // after it keep PDL (this grid releases them at each CTA's last tile).
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)g);
+    cfg.blockDim = dim3(TCP_THREADS);
+    cfg.dynamicSmemBytes = smem_p;
+    cfg.stream = s;
+    cfg.numAttrs = 0;
+    (void)cudaGetLastError();
+    if (cudaLaunchKernelEx(&cfg, kp, mx, mw, ap, gm) != cudaSuccess) return SLX_ERR_CUDA;
+    return cudaGetLastError() == cudaSuccess ? SLX_OK : SLX_ERR_CUDA;
+  }
   auto k = gemm_tc_kernel<EPI, OutT, BN, GROUPED>;
   static bool configured = false;  // per instantiation
   if (!configured) {
