@@ -535,6 +535,17 @@ def prefill_flops(cfg, T, n_prompts, L):
     return gemm, attn
 
 
+def prefill_gemm_bytes(cfg, T):
+    """Algorithmic HBM bytes of one layer's four prefill GEMMs (weights + activations in +
+    outputs, residual reads), averaged per GEMM launch."""
+    d, f, qd, kvd = cfg.hidden, cfg.ffn, cfg.q_dim, cfg.kv_dim
+    qkv = (qd + 2 * kvd) * d * 2 + T * d * 2 + T * (qd + 2 * kvd) * 2
+    o = d * qd * 2 + T * qd * 2 + 2 * T * d * 2
+    gu = 2 * f * d * 2 + T * d * 2 + T * f * 2
+    dn = d * f * 2 + T * f * 2 + 2 * T * d * 2
+    return (qkv + o + gu + dn) / 4.0
+
+
 def run_prefill(steps=3, warmup=1, bare=False, e2e=True, rank=0):
     """BASELINE config 3 on this GPU: 13B shape, 128 adapters r{8,16,64}, 8 x 2048 prompts."""
     import torch
@@ -613,6 +624,13 @@ def run_prefill(steps=3, warmup=1, bare=False, e2e=True, rank=0):
                         "flops": attn_flops, "kernel": "flash_prefill (causal)"}
     out["peak_tflops"] = tf_peak
     out["peak_source"] = peak_src
+    out["gemm_algorithmic_bytes"] = prefill_gemm_bytes(cfg, T)
+    tp = os.path.join(ROOT, "profiles", "prefill_traffic.json")
+    if os.path.exists(tp):
+        try:
+            out["gemm_traffic"] = json.load(open(tp)).get("gemm_tc_dram_bytes_per_launch")
+        except (OSError, ValueError):
+            pass
     out["kernels_ms"] = dur
     out["adapter_ranks_of_batch"] = [int(ranks[s]) for s in slots]
     # LoRA bytes actually moved (shrink: A of each prompt's adapter for q,k,v,o + x re-read;
@@ -680,8 +698,13 @@ def run_ours(args):
                     "tokens_per_s_per_gpu": value_local,
                     "e2e": r.get("e2e"), "gpu_launches": None,
                     "roofline": {"bound": "tensor", "achieved": r["gemm"]["TFLOP/s"], "peak": tf_peak,
-                                 "unit": "TFLOP/s", "frac": r["gemm"]["frac"], "traffic": None,
-                                 "kernel": "gemm_tc_kernel (tcgen05 prefill GEMM, LoRA fold)",
+                                 "unit": "TFLOP/s", "frac": r["gemm"]["frac"],
+                                 "traffic": r.get("gemm_traffic"),
+                                 "algorithmic_bytes_per_launch": r.get("gemm_algorithmic_bytes"),
+                                 "kernel": "gemm_tcp_kernel (persistent tcgen05 prefill GEMM, "
+                                           "LoRA fold)",
+                                 "traffic_note": "ncu dram__bytes_read+write per prefill GEMM "
+                                                 "launch (profiles/prefill_traffic.json)",
                                  "attention": r["attention"]},
                     "prefill": r, "clocks": clk.summary(), "cpu_baseline": cpu,
                     "wall_s": round(time.perf_counter() - t0, 1)}
