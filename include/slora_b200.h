@@ -206,13 +206,15 @@ SLX_API int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ldx, 
                    const int32_t* slot_rank, const float* slot_scale, int n_slots, int max_rank,
                    int n_targets, const slx_lora_target* targets,
                    void* ws, size_t ws_bytes, void* stream);
-/* Decode expand when the shrink ran inside the projection GEMM (slx_gemm_bf16 side output):
- * v_all [n_tok, ldv] fp32 holds, for target i, column v_col_off[i] + slot*max_rank + j =
- * x_t . A_slot[j]; adds scale * v . B_slot^T into y over the plan in ws (a_ptrs unused). */
+/* Decode expand over the plan in ws (a_ptrs unused): v_all [n_tok, ldv] fp32 holds, for
+ * target i, column v_col_off[i] + slot * v_slot_stride + j = x_t . A_slot[j] — the stacked
+ * shrink inside the projection GEMM (slx_gemm_bf16 side output, v_slot_stride = max_rank) or
+ * the gathered shrink (slx_lora_shrink, v_slot_stride = 0); adds scale * v . B_slot^T into y in
+ * place (sequential fmaf in j, one rounding: bit-identical to the fused slx_lora_delta). */
 SLX_API int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, int ldv, int n_tok,
                   const int32_t* slot_rank, const float* slot_scale, int n_slots, int max_rank,
                   int n_targets, const slx_lora_target* targets, const int* v_col_off,
-                  void* ws, size_t ws_bytes, void* stream);
+                  int v_slot_stride, void* ws, size_t ws_bytes, void* stream);
 /* Gathered shrink (decode with a large adapter pool): over the plan in ws (slx_lora_plan_tokens)
  * v[t, v_col_off[i] + j] = x_t . A_{slot(t), i}[j] for j < rank (fp32, unscaled), reading each
  * adapter present in the batch once per plan tile of <= 8 tokens (a_ptrs of the targets; b_ptrs

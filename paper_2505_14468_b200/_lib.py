@@ -87,7 +87,7 @@ SIGNATURES = {
     "slx_gemm_grouped_bf16": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p, _i, _i,
                                    _i, _p, _i, _p]),
     "slx_lora_expand": (_i, [_i, _p, _i, _p, _i, _i, _p, _p, _i, _i, _i,
-                             ctypes.POINTER(LoraTarget), ctypes.POINTER(_i), _p, _sz, _p]),
+                             ctypes.POINTER(LoraTarget), ctypes.POINTER(_i), _i, _p, _sz, _p]),
     "slx_lora_shrink": (_i, [_i, _p, _i, _p, _i, _i, _i, _p, _i, _i, _i,
                              ctypes.POINTER(LoraTarget), ctypes.POINTER(_i), _p, _sz, _p]),
     "slx_packed_weight_elems": (_sz, [_i, _i]),

@@ -462,106 +462,81 @@ lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, 
 // ---------------------------------------------------------------- gathered decode shrink
 // Large adapter pools (decode): instead of stacking every slot's A rows into the projection
 // GEMM (bytes grow with the pool), the shrink reads only the adapters present in the batch,
-// each ONCE per plan tile.  One cluster of KS CTAs per (tile, target): CTA q stages x[tile
-// tokens, k-chunk q] and A_s[:, k-chunk q] with one burst of cp.async, computes the partial
-// dot products (warp per output, shuffle reduce), and the cluster reduces the KS partials
-// through DSMEM in a fixed order (deterministic); CTA q writes outputs o = q, q + KS, ...
+// each ONCE per plan tile.  The work is a list of A rows (tile, target, j < rank): one WARP per
+// row streams the row (16 B per lane per step, five steps in flight) against the tile's
+// <= LORA_TT token rows of x (L2) and reduces with a warp_sum (fixed order: deterministic).
+// No clusters and no shared memory (grid = tiles x targets x rank / 8 warps).
 //   v[t, v_col_off[tgt] + j] = x_t . A_{slot(t), tgt}[j]   (j < rank; unscaled)
-// The fused expands (slx_lora_delta with v_slot_stride = 0) consume v.
+// Consumers: slx_lora_expand with v_slot_stride = 0, or the fused slx_lora_delta.
+constexpr int SH_WARPS = 8;
 struct ShrinkOut {
   int v_off[SLX_LORA_MAX_TARGETS];
 };
 
 template <typename T>
-__global__ void __launch_bounds__(FU_THREADS)
+__global__ void __launch_bounds__(SH_WARPS * 32, 4)
 lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, int ldx, int d_in,
-                     int ks, int kc, const int32_t* __restrict__ slot_rank, int max_rank,
-                     TargetArgs ta, ShrinkOut so, LoraWs ws) {
-  extern __shared__ __align__(16) uint8_t ssm[];
-  const int q = (int)tc::cluster_ctarank();
-  const int tile_id = blockIdx.x / ks;
-  const int tgt = blockIdx.y;
+                     const int32_t* __restrict__ slot_rank, int max_rank, TargetArgs ta,
+                     ShrinkOut so, LoraWs ws) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile_id = blockIdx.x, tgt = blockIdx.y;
+  const int j = blockIdx.z * SH_WARPS + warp;
   // plan (start of the step) and adapter pool (static): >= 2 launches back, read before the wait
-  const bool live = tile_id < *ws.n_tiles;   // uniform over the cluster
+  const bool live = tile_id < *ws.n_tiles;
   LoraTile tile{0, 0, 0, 0};
   int rank = 0;
   const bf16* A = nullptr;
-  const int k_lo = min(d_in, q * kc), k_hi = min(d_in, k_lo + kc);
-  const int kl = k_hi - k_lo;
-  // smem: xs [TT][kc] T | as [max_rank][kc] bf16 | vpart [TT][max_rank] f32 | toks [TT]
-  T* xs = reinterpret_cast<T*>(ssm);
-  bf16* as = reinterpret_cast<bf16*>(xs + (size_t)LORA_TT * kc);
-  float* vpart = reinterpret_cast<float*>(as + (size_t)max_rank * kc);
-  int* toks = reinterpret_cast<int*>(vpart + LORA_TT * max_rank);
   if (live) {
     tile = ws.tiles[tile_id];
     rank = min(slot_rank[tile.slot], max_rank);
     A = reinterpret_cast<const bf16*>(ta.a_ptrs[tgt][tile.slot]);
-    if (A == nullptr) rank = 0;   // the adapter does not target this projection
-    const int achunks = kl / 8;
-    for (int e = threadIdx.x; e < rank * achunks; e += FU_THREADS) {
-      const int j = e / achunks, c = e % achunks;
-      cp_async16(as + (size_t)j * kc + c * 8, A + (size_t)j * d_in + k_lo + c * 8);
-    }
-    if (threadIdx.x < LORA_TT)
-      toks[threadIdx.x] = threadIdx.x < tile.count ? ws.perm[tile.start + threadIdx.x] : 0;
   }
+  const bool mine = A != nullptr && j < rank;   // warp-uniform
+  int tok[LORA_TT];
+#pragma unroll
+  for (int i = 0; i < LORA_TT; ++i) tok[i] = (mine && i < tile.count) ? ws.perm[tile.start + i] : -1;
   pdl_wait();   // x comes from the kernel just before us
   pdl_trigger();
-  if (!live) return;
-  __syncthreads();
-  const int cnt = tile.count;
-  constexpr int XV = 16 / sizeof(T);
-  const int xchunks = kl / XV;
-  for (int e = threadIdx.x; e < cnt * xchunks; e += FU_THREADS) {
-    const int i = e / xchunks, c = e % xchunks;
-    cp_async16(xs + (size_t)i * kc + c * XV, x + (size_t)toks[i] * ldx + k_lo + c * XV);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_out = cnt * rank;
-  for (int o = warp; o < n_out; o += FU_THREADS / 32) {
-    const int i = o / rank, j = o % rank;
-    const T* xr = xs + (size_t)i * kc;
-    const bf16* ar = as + (size_t)j * kc;
-    float acc = 0.f;
-    for (int k = lane * 8; k < kl; k += 32 * 8) {
-      float xf[8], af[8];
-      Vec8<T>::load(xr + k, xf);
-      Vec8<bf16>::load(ar + k, af);
+  if (!mine) return;
+  const bf16* ar = A + (size_t)j * d_in;
+  float acc[LORA_TT];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc = fmaf(xf[e], af[e], acc);
+  for (int i = 0; i < LORA_TT; ++i) acc[i] = 0.f;
+  // unrolled so several 16-byte steps of the row (and of the tokens' x) are in flight at once
+#pragma unroll 5
+  for (int k = lane * 8; k < d_in; k += 32 * 8) {
+    float af[8];
+    Vec8<bf16>::load(ar + k, af);
+#pragma unroll
+    for (int i = 0; i < LORA_TT; ++i) {
+      if (tok[i] < 0) continue;
+      float xf[8];
+      Vec8<T>::load(x + (size_t)tok[i] * ldx + k, xf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[i] = fmaf(xf[e], af[e], acc[i]);
     }
-    acc = warp_sum(acc);
-    if (lane == 0) vpart[i * max_rank + j] = acc;
   }
-  tc::cluster_sync();
-  const uint32_t vp_base = tc::smem_u32(vpart);
-  for (int o = q + ks * (int)threadIdx.x; o < n_out; o += ks * FU_THREADS) {
-    const int i = o / rank, j = o % rank;
-    const uint32_t off = vp_base + (uint32_t)((i * max_rank + j) * 4);
-    float part[FU_MAX_KS];
 #pragma unroll
-    for (int r = 0; r < FU_MAX_KS; ++r) part[r] = r < ks ? tc::ld_dsmem(tc::mapa(off, (uint32_t)r)) : 0.f;
-    float a = 0.f;
-#pragma unroll
-    for (int r = 0; r < FU_MAX_KS; ++r) a += part[r];   // fixed order: deterministic
-    v[(size_t)toks[i] * ldv + so.v_off[tgt] + j] = a;
+  for (int i = 0; i < LORA_TT; ++i) {
+    if (tok[i] < 0) continue;   // warp-uniform
+    const float sum = warp_sum(acc[i]);
+    if (lane == 0) v[(size_t)tok[i] * ldv + so.v_off[tgt] + j] = sum;
   }
-  tc::cluster_sync();   // keep our vpart alive until every peer has read it
 }
 
-// ---------------------------------------------------------------- decode expand (shrink in GEMM)
-// The decode shrink runs inside the projection GEMM (stacked A rows of every slot appended to
-// W, fp32 side output v_all); this kernel is the expand: CTA (tile, target, n-chunk) stages
-// the tile adapter's B rows of its n-chunk and the tokens' y slices with one burst of
-// cp.async, then y[t, col(n)] += scale * sum_j v_all[t, off + slot*max_rank + j] * B[n, j].
+// ---------------------------------------------------------------- decode expand
+// y[t, col(n)] += scale * sum_j v[t, off + slot * v_slot_stride + j] * B_slot[n, j] over the
+// plan: v from the stacked shrink inside the projection GEMM (stride max_rank) or the gathered
+// shrink (stride 0).  CTA (tile, target, 256-column chunk): the tile's scaled v in shared memory,
+// one THREAD per output column n with its B row (rank <= 64 bf16: up to eight 16-byte loads, all
+// in flight) in registers, then a read-modify-write of y for each of the tile's tokens
+// (coalesced over n).  Sequential fmaf in j with v pre-scaled and one rounding of y:
+// bit-identical to the fused slx_lora_delta.
 constexpr int EX_THREADS = 256;
-constexpr int EX_CHUNK = 512;   // output features per CTA
 
 struct ExpandArgs {
   int v_off[SLX_LORA_MAX_TARGETS];
+  int v_slot_stride;   // columns between slots' v blocks: max_rank (stacked) or 0 (gathered)
 };
 
 template <typename T>
@@ -569,91 +544,65 @@ __global__ void __launch_bounds__(EX_THREADS)
 lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, int ldv,
                      const int32_t* __restrict__ slot_rank, const float* __restrict__ slot_scale,
                      int max_rank, TargetArgs ta, ExpandArgs ea, LoraWs ws) {
-  extern __shared__ __align__(16) uint8_t esm[];
-  // The plan (kernel at the start of the step) and the adapter pool (static) are >= 2
-  // launches back: read them and start streaming B before waiting on the shrink GEMM.
-  const int tile_id = blockIdx.x;
+  __shared__ float vs[LORA_TT][LORA_MAX_RANK];
+  __shared__ int toks[LORA_TT];
+  // The plan and the adapter pool are >= 2 launches back: read them and fetch the B rows
+  // before waiting on the kernel that produced v / y.
+  const int tile_id = blockIdx.x, tgt = blockIdx.y;
   const bool live = tile_id < *ws.n_tiles;
-  const int tgt = blockIdx.y;
   const int d_out = ta.d_out[tgt];
-  const int n_lo = blockIdx.z * EX_CHUNK;
-  if (!live || n_lo >= d_out) {
+  const int n = blockIdx.z * EX_THREADS + threadIdx.x;
+  LoraTile tile{0, 0, 0, 0};
+  int rank = 0;
+  float scale = 0.f;
+  const bf16* B = nullptr;
+  if (live) {
+    tile = ws.tiles[tile_id];
+    rank = min(slot_rank[tile.slot], max_rank);
+    scale = slot_scale[tile.slot];
+    B = reinterpret_cast<const bf16*>(ta.b_ptrs[tgt][tile.slot]);
+  }
+  if (B == nullptr || rank == 0 || blockIdx.z * EX_THREADS >= d_out) {   // CTA-uniform
     pdl_wait();
     pdl_trigger();
     return;
   }
-  const LoraTile tile = ws.tiles[tile_id];
-  const int nn = min(EX_CHUNK, d_out - n_lo);
-  const int cnt = tile.count;
-  const int rank = min(slot_rank[tile.slot], max_rank);
-  const float scale = slot_scale[tile.slot];
-  const bf16* B = reinterpret_cast<const bf16*>(ta.b_ptrs[tgt][tile.slot]);
-  const int cb = ta.col_blk[tgt], cstr = ta.col_stride[tgt], co = ta.col_off[tgt];
-  const int col_lo = co + (n_lo / cb) * cstr + (n_lo % cb);
-  const bool y_contig = (n_lo / cb) == ((n_lo + nn - 1) / cb) && (col_lo % 8) == 0 &&
-                        (ldy % 8) == 0 && (nn % 8) == 0;
-  // smem: bs [EX_CHUNK][max_rank] bf16 | ys [TT][EX_CHUNK] T | vs [TT][max_rank] f32 | toks
-  bf16* bs = reinterpret_cast<bf16*>(esm);
-  T* ys = reinterpret_cast<T*>(bs + (size_t)EX_CHUNK * max_rank);
-  float* vs = reinterpret_cast<float*>(ys + (size_t)LORA_TT * EX_CHUNK);
-  int* toks = reinterpret_cast<int*>(vs + LORA_TT * max_rank);
-  if (threadIdx.x < LORA_TT) toks[threadIdx.x] = threadIdx.x < cnt ? ws.perm[tile.start + threadIdx.x] : 0;
-  const int bchunks = nn * rank / 8;   // rows n_lo..n_lo+nn of B are contiguous
-  for (int e = threadIdx.x; e < bchunks; e += EX_THREADS) {
-    const int flat = e * 8;
-    cp_async16(bs + (size_t)(flat / rank) * max_rank + flat % rank, B + (size_t)n_lo * rank + flat);
+  uint4 br[LORA_MAX_RANK / 8];
+  const int R8 = (rank + 7) >> 3;   // pool invariant: rank % 8 == 0
+  if (n < d_out) {
+    const uint4* src = reinterpret_cast<const uint4*>(B + (size_t)n * rank);
+#pragma unroll
+    for (int q = 0; q < LORA_MAX_RANK / 8; ++q) br[q] = q < R8 ? __ldg(src + q) : make_uint4(0, 0, 0, 0);
   }
-  pdl_wait();       // v_all and y come from the GEMM just before us
+  if (threadIdx.x < LORA_TT) toks[threadIdx.x] = threadIdx.x < tile.count ? ws.perm[tile.start + threadIdx.x] : 0;
+  pdl_wait();       // v and y come from the kernels just before us
   pdl_trigger();
-  __syncthreads();  // toks visible
-  constexpr int XV = 16 / sizeof(T);
-  if (y_contig) {
-    const int ych = nn / XV;
-    for (int e = threadIdx.x; e < cnt * ych; e += EX_THREADS) {
-      const int i = e / ych, c = e % ych;
-      cp_async16(ys + (size_t)i * EX_CHUNK + c * XV, y + (size_t)toks[i] * ldy + col_lo + c * XV);
-    }
+  __syncthreads();  // toks
+  const int voff = ea.v_off[tgt] + tile.slot * ea.v_slot_stride;
+  for (int e = threadIdx.x; e < tile.count * LORA_MAX_RANK; e += EX_THREADS) {
+    const int i = e / LORA_MAX_RANK, jj = e % LORA_MAX_RANK;
+    vs[i][jj] = jj < rank ? v[(size_t)toks[i] * ldv + voff + jj] * scale : 0.f;
   }
-  const int voff = ea.v_off[tgt] + tile.slot * max_rank;
-  for (int e = threadIdx.x; e < cnt * max_rank; e += EX_THREADS) {
-    const int i = e / max_rank, j = e % max_rank;
-    vs[e] = j < rank ? v[(size_t)toks[i] * ldv + voff + j] * scale : 0.f;
-  }
-  cp_async_wait_all();
   __syncthreads();
-  const int R8 = (rank + 7) & ~7;
-  const int ngrp = (nn + 7) / 8;
-  for (int e = threadIdx.x; e < cnt * ngrp; e += EX_THREADS) {
-    const int i = e / ngrp, n0 = (e % ngrp) * 8;
-    const float* vr = vs + i * max_rank;
-    float d[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int j = 0; j < R8; j += 8) {
-      float vv[8];
+  if (n >= d_out) return;
+  const int cb = ta.col_blk[tgt], cstr = ta.col_stride[tgt], co = ta.col_off[tgt];
+  const int col = co + (n / cb) * cstr + (n % cb);
+  for (int i = 0; i < tile.count; ++i) {
+    float d = 0.f;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) vv[u] = vr[j + u];
+    for (int q = 0; q < LORA_MAX_RANK / 8; ++q) {
+      if (q < R8) {
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&br[q]);
 #pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        if (n0 + r >= nn) break;
-        float b[8];
-        Vec8<bf16>::load(bs + (size_t)(n0 + r) * max_rank + j, b);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) d[r] = fmaf(vv[u], b[u], d[r]);
+        for (int u = 0; u < 4; ++u) {
+          const float2 f = __bfloat1622float2(h2[u]);
+          d = fmaf(vs[i][8 * q + 2 * u], f.x, d);
+          d = fmaf(vs[i][8 * q + 2 * u + 1], f.y, d);
+        }
       }
     }
-    T* yr = y + (size_t)toks[i] * ldy;
-    if (y_contig) {
-      float yv[8];
-      Vec8<T>::load(ys + (size_t)i * EX_CHUNK + n0, yv);
-#pragma unroll
-      for (int r = 0; r < 8; ++r) yv[r] += d[r];
-      Vec8<T>::store(yr + col_lo + n0, yv);
-    } else {
-      for (int r = 0; r < 8 && n0 + r < nn; ++r) {
-        const int n = n_lo + n0 + r;
-        const int col = co + (n / cb) * cstr + (n % cb);
-        yr[col] = from_f32<T>(to_f32(yr[col]) + d[r]);
-      }
-    }
+    T* yp = y + (size_t)toks[i] * ldy + col;
+    *yp = from_f32<T>(to_f32(*yp) + d);
   }
 }
 
@@ -810,18 +759,21 @@ extern "C" int slx_lora_sgmv(int dtype, void* y, int ldy, const void* x, int ldx
 extern "C" int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, int ldv, int n_tok,
                                const int32_t* slot_rank, const float* slot_scale, int n_slots,
                                int max_rank, int n_targets, const slx_lora_target* targets,
-                               const int* v_col_off, void* ws, size_t ws_bytes, void* stream) {
+                               const int* v_col_off, int v_slot_stride, void* ws, size_t ws_bytes,
+                               void* stream) {
   SLX_CHECK_ARG(n_tok >= 0 && n_slots > 0 && max_rank > 0 && max_rank <= LORA_MAX_RANK &&
                 max_rank % 8 == 0 && n_targets >= 1 && n_targets <= SLX_LORA_MAX_TARGETS &&
-                targets && v_col_off && slot_rank && slot_scale && y && v_all && ldv > 0);
+                targets && v_col_off && slot_rank && slot_scale && y && v_all && ldv > 0 &&
+                v_slot_stride >= 0);
   TargetArgs ta;
   ExpandArgs ea;
+  ea.v_slot_stride = v_slot_stride;
   int max_dout = 0;
   for (int i = 0; i < n_targets; ++i) {
     const slx_lora_target& t = targets[i];
     SLX_CHECK_ARG(t.b_ptrs && t.d_out > 0 && t.d_out % 8 == 0 && t.y_col_block > 0 &&
                   t.y_col_stride >= t.y_col_block && v_col_off[i] >= 0 &&
-                  v_col_off[i] + n_slots * max_rank <= ldv);
+                  v_col_off[i] + (n_slots - 1) * v_slot_stride + max_rank <= ldv);
     ta.a_ptrs[i] = t.a_ptrs;
     ta.b_ptrs[i] = t.b_ptrs;
     ta.d_out[i] = t.d_out;
@@ -835,23 +787,14 @@ extern "C" int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, i
   int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
   if (st) return st;
   if (n_tok == 0) return SLX_OK;
-  const size_t tsz = dtype == SLX_DT_BF16 ? 2 : 4;
-  const size_t smem = (size_t)EX_CHUNK * max_rank * 2 + (size_t)LORA_TT * EX_CHUNK * tsz +
-                      (size_t)LORA_TT * max_rank * 4 + LORA_TT * 4;
-  dim3 grid((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)ceil_div(max_dout, EX_CHUNK));
+  dim3 grid((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)ceil_div(max_dout, EX_THREADS));
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == SLX_DT_BF16) {
-    auto k = lora_expand_v_kernel<bf16>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_ex(k, grid, dim3(EX_THREADS), smem, s, 1u, (bf16*)y, ldy, (const float*)v_all, ldv,
-                     slot_rank, slot_scale, max_rank, ta, ea, w);
-  }
-  if (dtype == SLX_DT_F32) {
-    auto k = lora_expand_v_kernel<float>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_ex(k, grid, dim3(EX_THREADS), smem, s, 1u, (float*)y, ldy, (const float*)v_all, ldv,
-                     slot_rank, slot_scale, max_rank, ta, ea, w);
-  }
+  if (dtype == SLX_DT_BF16)
+    return launch_ex(lora_expand_v_kernel<bf16>, grid, dim3(EX_THREADS), 0, s, 1u, (bf16*)y, ldy,
+                     (const float*)v_all, ldv, slot_rank, slot_scale, max_rank, ta, ea, w);
+  if (dtype == SLX_DT_F32)
+    return launch_ex(lora_expand_v_kernel<float>, grid, dim3(EX_THREADS), 0, s, 1u, (float*)y, ldy,
+                     (const float*)v_all, ldv, slot_rank, slot_scale, max_rank, ta, ea, w);
   return SLX_ERR_INVALID;
 }
 
@@ -875,28 +818,13 @@ extern "C" int slx_lora_shrink(int dtype, float* v, int ldv, const void* x, int 
   int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
   if (st) return st;
   if (n_tok == 0) return SLX_OK;
-  int ks = d_in / 512;
-  ks = ks < 1 ? 1 : (ks > FU_MAX_KS ? FU_MAX_KS : ks);
-  const int kc = ceil_div(ceil_div(d_in, ks), 8) * 8;
-  const size_t tsz = dtype == SLX_DT_BF16 ? 2 : 4;
-  const size_t smem = (size_t)LORA_TT * kc * tsz + (size_t)max_rank * kc * 2 +
-                      (size_t)LORA_TT * max_rank * 4 + LORA_TT * 4;
-  if (smem > 200 * 1024) return SLX_ERR_UNSUPPORTED;
-  dim3 grid((unsigned)(w.max_tiles * ks), (unsigned)n_targets);
+  dim3 grid((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)ceil_div(max_rank, SH_WARPS));
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == SLX_DT_BF16) {
-    auto k = lora_shrink_v_kernel<bf16>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return SLX_ERR_CUDA;
-    return launch_ex(k, grid, dim3(FU_THREADS), smem, s, (unsigned)ks, v, ldv, (const bf16*)x, ldx,
-                     d_in, ks, kc, slot_rank, max_rank, ta, so, w);
-  }
-  if (dtype == SLX_DT_F32) {
-    auto k = lora_shrink_v_kernel<float>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-      return SLX_ERR_CUDA;
-    return launch_ex(k, grid, dim3(FU_THREADS), smem, s, (unsigned)ks, v, ldv, (const float*)x, ldx,
-                     d_in, ks, kc, slot_rank, max_rank, ta, so, w);
-  }
+  if (dtype == SLX_DT_BF16)
+    return launch_ex(lora_shrink_v_kernel<bf16>, grid, dim3(SH_WARPS * 32), 0, s, 1u, v, ldv,
+                     (const bf16*)x, ldx, d_in, slot_rank, max_rank, ta, so, w);
+  if (dtype == SLX_DT_F32)
+    return launch_ex(lora_shrink_v_kernel<float>, grid, dim3(SH_WARPS * 32), 0, s, 1u, v, ldv,
+                     (const float*)x, ldx, d_in, slot_rank, max_rank, ta, so, w);
   return SLX_ERR_INVALID;
 }

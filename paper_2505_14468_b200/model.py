@@ -604,17 +604,24 @@ class MultiLoraModel:
                   self.cfg.target_dims(self.targets[i])[1], 0, 1, 1) for i in idx]
         return idx, ops.make_targets(specs), [k * self.pool.max_rank for k in range(len(idx))]
 
-    def _shrink_delta(self, layer: int, names, x, v, slot, cols):
-        """Gathered decode LoRA of targets ``names`` on input x: the shrink kernel writes v
-        (compact: [T, len(names) * max_rank]); returns the slx_lora_delta of the fused expand."""
+    def _gather_shrink(self, layer: int, names, x, v) -> None:
+        """Gathered decode shrink of targets ``names`` on input x into v (compact:
+        [T, len(names) * max_rank], only the batch's adapters read)."""
         idx, targets, offs = self._gather_targets(layer, names)
+        if idx:
+            ops.lora_shrink(v, x, self.pool.rank, self.pool.max_rank, targets, offs, self.lora_ws)
+
+    def _gather_expand(self, layer: int, names, y, v, cols) -> None:
+        """y[t, col] += scale * v . B^T for the gathered v of targets ``names`` (in place; the
+        expand kernel reads each present adapter's B rows once per plan tile)."""
+        idx = [i for i, t in enumerate(self.targets) if t in names]
         if not idx:
-            return None
-        ops.lora_shrink(v, x, self.pool.rank, self.pool.max_rank, targets, offs, self.lora_ws)
-        tg = [(self.pool.b_ptr[layer, i], offs[k], cols[self.targets[i]][0],
-               self.cfg.target_dims(self.targets[i])[1]) for k, i in enumerate(idx)]
-        return ops.make_delta(v, slot, self.pool.rank, self.pool.scale, self.pool.max_rank, tg,
-                              v_slot_stride=0)
+            return
+        specs = [(self.pool.a_ptr[layer, i], self.pool.b_ptr[layer, i],
+                  self.cfg.target_dims(self.targets[i])[1], *cols[self.targets[i]]) for i in idx]
+        ops.lora_expand(y, v, self.pool.rank, self.pool.scale, self.pool.max_rank,
+                        ops.make_targets(specs), [k * self.pool.max_rank for k in range(len(idx))],
+                        self.lora_ws, v_slot_stride=0)
 
     @staticmethod
     def segments_of(pos, seq) -> list:
@@ -710,16 +717,20 @@ class MultiLoraModel:
                 d_qkv = self._delta(l, "w_qkv", v_qkv, slot, qkv_cols)
             else:
                 if gather and qkv_names:
-                    d_qkv = self._shrink_delta(l, qkv_names, h, v_g, slot, qkv_cols)
+                    self._gather_shrink(l, qkv_names, h, v_g)
                 ops.gemm(h, w[p + "w_qkv"], qkv, prefetch=pf_qkv)
+                if gather and qkv_names:   # q/k/v deltas added in place (== the fused expand)
+                    self._gather_expand(l, qkv_names, qkv, v_g, qkv_cols)
             ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
                                       self.cos, self.sin, self.k_cache[l], self.v_cache[l],
                                       lora=d_qkv, prefetch=pf_att)
             # o (split-K pieces) -> residual + o LoRA + post-attention RMSNorm
             d_o = None
             if gather and "o" in self.targets:
-                d_o = self._shrink_delta(l, ("o",), attn, v_go, slot, {"o": (0, d, d)})
+                self._gather_shrink(l, ("o",), attn, v_go)
             sk_o = ops.gemm_splitk(attn, w[p + "wo"], S, part_o, prefetch=pf_o)
+            if gather and "o" in self.targets:   # the o delta into the residual before the norm
+                self._gather_expand(l, ("o",), x, v_go, {"o": (0, d, d)})
             if stacked and "wo" in self.stack:
                 d_o = self._delta(l, "wo", None, slot, {"o": (0, d, d)})
             ops.rmsnorm_fused(h, x, w[p + "post_norm"], cfg.rms_eps, sk_o, d_o)

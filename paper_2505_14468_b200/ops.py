@@ -330,13 +330,16 @@ def lora_sgmv(y, x, seg_indptr, seg_slot, slot_rank, slot_scale, max_rank, targe
 
 @_op("lora", 1)
 def lora_expand(y: torch.Tensor, v_all: torch.Tensor, slot_rank, slot_scale, max_rank: int,
-                targets, v_col_off, ws: torch.Tensor) -> None:
-    """Decode expand after the GEMM-side shrink: y[t, col(n)] += scale * v . B_slot^T."""
+                targets, v_col_off, ws: torch.Tensor, v_slot_stride: int | None = None) -> None:
+    """Decode expand in place: y[t, col(n)] += scale * v . B_slot^T over the plan in ws.  v from
+    the GEMM-side stacked shrink (``v_slot_stride`` = max_rank, the default) or from the
+    gathered shrink (``v_slot_stride=0``)."""
     offs = (ctypes.c_int * len(v_col_off))(*v_col_off)
+    stride = max_rank if v_slot_stride is None else int(v_slot_stride)
     check(_lib.load().slx_lora_expand(_dt(y), _ptr(y), _ld(y), _ptr(v_all), _ld(v_all), y.shape[0],
                                       _ptr(slot_rank), _ptr(slot_scale), slot_rank.numel(), max_rank,
-                                      len(targets), targets, offs, _ptr(ws), ws.numel(), _stream()),
-          "slx_lora_expand")
+                                      len(targets), targets, offs, stride, _ptr(ws), ws.numel(),
+                                      _stream()), "slx_lora_expand")
 
 
 @_op("lora", 1)
