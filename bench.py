@@ -572,18 +572,21 @@ def run_prefill(steps=3, warmup=1, bare=False, e2e=True, rank=0):
     slot = torch.from_numpy(np.repeat(slots.astype(np.int32), L3)).to(dev)
     last = torch.from_numpy((np.arange(P3) + 1) * L3 - 1).to(dev)
     segs = [(i * L3, L3, i, 0) for i in range(P3)]
-    step = lambda: m.forward(toks, pos, seq, slot, last, segments=segs)  # noqa: E731
+    slot_host = np.repeat(slots.astype(np.int32), L3)
+    step = lambda: m.forward(toks, pos, seq, slot, last, segments=segs, slot_host=slot_host)  # noqa: E731
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = ops.launch_count()
     e0.record()
     for _ in range(steps):
         step()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    out = {"prefill_ms": round(ms, 2), "tokens_per_s": round(T / (ms / 1000.0), 1)}
+    out = {"prefill_ms": round(ms, 2), "tokens_per_s": round(T / (ms / 1000.0), 1),
+           "gpu_launches": ops.launch_count() - n0}
     # end to end through the public API: host token lists in (H2D), first tokens out (D2H)
     if e2e:
         prompts = [h_toks[i * L3:(i + 1) * L3].tolist() for i in range(P3)]
@@ -643,7 +646,7 @@ def run_prefill(steps=3, warmup=1, bare=False, e2e=True, rank=0):
         m0 = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=P3, max_ctx=L3, n_slots=N_AD3,
                             max_rank=64, max_tokens=P3 * L3, lora_targets=())
         m0.random_backbone(seed=0)
-        step0 = lambda: m0.forward(toks, pos, seq, slot, last, segments=segs)  # noqa: E731
+        step0 = lambda: m0.forward(toks, pos, seq, slot, last, segments=segs, slot_host=slot_host)  # noqa: E731
         for _ in range(warmup):
             step0()
         torch.cuda.synchronize()
@@ -696,7 +699,7 @@ def run_ours(args):
                     "dtype": "bf16", "data": "synthetic (random-init 13B-shape weights and adapters)",
                     "config": config_dict("config3", args.ctx, world),
                     "tokens_per_s_per_gpu": value_local,
-                    "e2e": r.get("e2e"), "gpu_launches": None,
+                    "e2e": r.get("e2e"), "gpu_launches": r.get("gpu_launches"),
                     "roofline": {"bound": "tensor", "achieved": r["gemm"]["TFLOP/s"], "peak": tf_peak,
                                  "unit": "TFLOP/s", "frac": r["gemm"]["frac"],
                                  "traffic": r.get("gemm_traffic"),

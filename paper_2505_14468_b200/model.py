@@ -224,6 +224,7 @@ class MultiLoraModel:
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
         # prefill: the LoRA expand folded into the backbone GEMM as one extra K block
         self.lora_fold = True
+        self._plan_cache: dict = {}   # prefill plans by segment layout (_prefill_plans)
         self.pool.on_install = self._stack_install
         self.pool.on_evict = self._stack_evict
 
@@ -644,18 +645,21 @@ class MultiLoraModel:
                      (self.use_stacked_decode and self.pool.max_rank <= 16)))
 
     def forward(self, tokens, pos, seq, slot, logit_rows=None, decode: bool = False,
-                segments=None) -> torch.Tensor:
+                segments=None, slot_host=None) -> torch.Tensor:
         """Token-major mixed batch.  tokens/pos/seq/slot: device int32 [T].
         ``decode``: every token is the next position of its own sequence, so RoPE, the KV
         append and attention run as one fused kernel per layer.  The caller guarantees
         pos < max_ctx (MultiLoraModel.prefill/decode and the serving runtime check it).
+        ``slot_host``: the same per-token slots on the host when the caller has them (prefill
+        plans need them; otherwise they are read back from the device, a stream sync).
         Returns logits (fp32) for ``logit_rows`` (device int64) or for every token."""
         T = tokens.numel()
         if T > self.max_tokens:
             raise ValueError(f"batch of {T} tokens exceeds max_tokens={self.max_tokens}")
         if decode and self._decode_fast(T):
             return self._forward_decode(tokens, pos, seq, slot, logit_rows)
-        return self._forward_general(tokens, pos, seq, slot, logit_rows, decode, segments)
+        return self._forward_general(tokens, pos, seq, slot, logit_rows, decode, segments,
+                                     slot_host)
 
     def _forward_decode(self, tokens, pos, seq, slot, logit_rows):
         """bf16 decode step: per layer [RMSNorm(+ pieces of the previous down projection)] ->
@@ -743,7 +747,28 @@ class MultiLoraModel:
             hn = hn.index_select(0, logit_rows)
         return ops.gemm(hn, w["lm_head"], out_dtype=torch.float32)
 
-    def _forward_general(self, tokens, pos, seq, slot, logit_rows, decode, segments):
+    def _prefill_plans(self, segments, slot_host, T: int, flash: bool, sgmv: bool):
+        """(flash plan, LoRA-fold plan, SGMV plan) of a segmented prefill batch, cached by the
+        segment layout and the segments' adapter slots (a serving loop re-plans only when the
+        batch shape changes; the plans are device tensors built once)."""
+        key = (tuple(tuple(int(v) for v in sg) for sg in segments),
+               tuple(int(slot_host[sg[0]]) for sg in segments), T, flash, sgmv)
+        hit = self._plan_cache.get(key)
+        if hit is not None:
+            return hit
+        plan = ops.prefill_plan(segments, self.cfg.heads, self.device) if flash else None
+        fold = sgmv_plan = None
+        if sgmv:
+            if self.lora_fold:
+                fold = self._fold_plan(segments, slot_host, T)
+            if fold is None:
+                sgmv_plan = self._sgmv_plan(segments, slot_host)
+        if len(self._plan_cache) >= 16:
+            self._plan_cache.pop(next(iter(self._plan_cache)))
+        self._plan_cache[key] = (plan, fold, sgmv_plan)
+        return plan, fold, sgmv_plan
+
+    def _forward_general(self, tokens, pos, seq, slot, logit_rows, decode, segments, slot_host=None):
         """Prefill (bf16: tcgen05 GEMMs with the LoRA folded / grouped SGMV, flash attention)
         and the fp32 parity mode (decode included)."""
         cfg, w, dt = self.cfg, self.w, self.dtype
@@ -766,17 +791,15 @@ class MultiLoraModel:
                    if "wo" in self.stack else None)
         flash = (segments is not None and not decode and dt == torch.bfloat16
                  and cfg.head_dim == 128)
-        if flash:
-            plan = ops.prefill_plan(segments, cfg.heads, dev)
-        sgmv_plan = None
-        fold = None
-        if (segments is not None and not decode and dt == torch.bfloat16 and self.targets
-                and self.use_tc_sgmv and not stacked):
-            slot_host = slot.cpu().numpy()
-            if self.lora_fold:
-                fold = self._fold_plan(segments, slot_host, T)
+        sgmv = (segments is not None and not decode and dt == torch.bfloat16 and bool(self.targets)
+                and self.use_tc_sgmv and not stacked)
+        plan = fold = sgmv_plan = None
+        if flash or sgmv:
+            if sgmv and slot_host is None:
+                slot_host = slot.cpu().numpy()
+            plan, fold, sgmv_plan = self._prefill_plans(segments, slot_host, T, flash, sgmv)
+        if sgmv:
             if fold is None:
-                sgmv_plan = self._sgmv_plan(segments, slot_host)
                 v_buf = torch.empty((T, 64), dtype=dt, device=dev)
             else:
                 v_qkv_f = torch.zeros((T, 192), dtype=dt, device=dev)
@@ -866,7 +889,7 @@ class MultiLoraModel:
         i32 = lambda v: torch.tensor(v, dtype=torch.int32, device=dev)  # noqa: E731
         logits = self.forward(i32(toks), i32(pos), i32(sq), i32(sl),
                               torch.tensor(last, dtype=torch.int64, device=dev),
-                              segments=self.segments_of(pos, sq))
+                              segments=self.segments_of(pos, sq), slot_host=np.asarray(sl))
         return seqs, logits
 
     def decode(self, seqs, tokens, adapter_slots) -> torch.Tensor:

@@ -249,7 +249,8 @@ class ServingRuntime:
                 logits = self.m.forward(self._i32(batch.tokens), self._i32(batch.pos),
                                         self._i32(batch.seq), self._i32(batch.slot),
                                         torch.from_numpy(batch.logit_rows).to(self.m.device),
-                                        segments=self.m.segments_of(batch.pos, batch.seq))
+                                        segments=self.m.segments_of(batch.pos, batch.seq),
+                                        slot_host=batch.slot)
                 nxt = self.m.argmax(logits).cpu().tolist()
             except Exception:
                 for s in seqs:   # transactional: nothing of the round stays reserved
