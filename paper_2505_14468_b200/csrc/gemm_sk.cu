@@ -11,8 +11,9 @@
 // of one tile, whole tiles, and the head of another ("segments").
 //
 // Roles (192 threads): warp 0 lane 0 TMA producer (weights are fetched before the PDL wait),
-// warp 1 lane 0 MMA issuer into one of TWO TMEM accumulators (2 x 256 columns), warps 2-5
-// epilogue.  Because the epilogue has its own warps and the accumulator is double-buffered,
+// warp 1 lane 0 MMA issuer (M = 64: the <= 64 token rows spread over all four TMEM lane
+// quadrants) into one of TWO TMEM accumulators (2 x 256 columns), warps 2-5 epilogue, each
+// draining 16 rows.  Because the epilogue has its own warps and the accumulator is double-buffered,
 // draining segment j overlaps the MMAs of segment j+1.
 //
 // Split tiles are reduced deterministically without clusters: every piece is written in fp32
@@ -223,7 +224,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       // ------------------------------------------------------------ MMA issuer
       // D[128 tok x 256 w] (+)= X[128 x 16] . W[256 x 16]^T; X rows >= bm read stale smem and
       // only feed D rows that are never read.
-      const uint32_t idesc = tc::idesc_bf16_f32(128, SK_BN);
+      // M = 64 (bm <= 64 token rows): the accumulator's row r lands in lane r % 16 of TMEM lane
+      // quadrant r / 16 (tools/probe/m64_layout.cu), so all four epilogue warps drain it
+      const uint32_t idesc = tc::idesc_bf16_f32(64, SK_BN);
       int j = -1;
       uint32_t d = 0;
       bool first = true;
@@ -258,8 +261,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     // This CTA holds piece `rank` of tile c / cs (exactly one segment).  Pieces are staged in
     // each CTA's own (now idle) pipeline smem as [chunk][row][16] fp32 and reduced through
     // DSMEM: CTA `rank` sums a 1/cs slice of the tile over the cs peers in rank order.
-    const int q = warp & 3, r = q * 32 + lane, et = threadIdx.x - 64;
-    const bool qlive = q * 32 < g.bm;
+    const int q = warp & 3, r = q * 16 + (lane & 15), et = threadIdx.x - 64;
+    const bool qlive = q * 16 < g.bm;   // warp-uniform
+    const bool rv = lane < 16;          // lanes 16-31 of the quadrant hold no row (M = 64)
     const bool silu = EPI == SLX_EPI_SILU_MUL;
     const int cs = g.cs, rank = c % cs, tile = c / cs;
     const int n_out = silu ? g.N / 2 : g.N;
@@ -273,7 +277,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       for (int ch = 0; ch < 16; ch += 2) {
         float v0[16], v1[16];
         tc::tmem_ld16x2(tacc + ch * 16, tacc + ch * 16 + 16, v0, v1);
-        if (r < g.bm) {
+        if (rv && r < g.bm) {
           float4* p0 = reinterpret_cast<float4*>(stg + ((size_t)ch * g.bm + r) * 16);
           float4* p1 = reinterpret_cast<float4*>(stg + ((size_t)(ch + 1) * g.bm + r) * 16);
 #pragma unroll
@@ -347,9 +351,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   } else {
     // -------------------------------------------------------------- epilogue (warps 2-5)
     const int q = warp & 3;              // TMEM lane quadrant this warp may access
-    const int r = q * 32 + lane;         // token row of this thread in the accumulator
+    const int r = q * 16 + (lane & 15);  // token row of this thread (M = 64 layout)
+    const bool rv = lane < 16;           // lanes 16-31 of the quadrant hold no row
     const int et = threadIdx.x - 64;     // 0..127
-    const bool qlive = q * 32 < g.bm;    // warp-uniform
+    const bool qlive = q * 16 < g.bm;    // warp-uniform
     const bool silu = EPI == SLX_EPI_SILU_MUL;
     const int piece_floats = g.bm * SK_BN;
     const int n_out = silu ? g.N / 2 : g.N;
@@ -388,7 +393,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
             for (int ch = 0; ch < 8; ++ch) {
               float gv[16], uv[16];
               tc::tmem_ld16x2(tacc + ch * 16, tacc + 128 + ch * 16, gv, uv);
-              if (m < g.M) {
+              if (rv && m < g.M) {
 #pragma unroll
                 for (int e = 0; e < 16; ++e) gv[e] = sk_silu(gv[e]) * uv[e];
                 sk_store16(reinterpret_cast<OutT*>(g.C) + (size_t)m * g.ldc, tile * 128 + ch * 16,
@@ -400,7 +405,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
               float v0[16], v1[16], r0[16], r1[16];
               tc::tmem_ld16x2(tacc + ch * 16, tacc + ch * 16 + 16, v0, v1);
               const int n = tile * SK_BN + ch * 16;
-              if (m < g.M && n < g.N) {
+              if (rv && m < g.M && n < g.N) {
                 if (EPI == SLX_EPI_RESIDUAL) {
                   const int lim = g.C2 != nullptr ? g.n_main : g.N;
                   sk_load_res<OutT>(g, m, n, lim, r0);
@@ -419,7 +424,7 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
           for (int ch = 0; ch < 16; ch += 2) {
             float v0[16], v1[16];
             tc::tmem_ld16x2(tacc + ch * 16, tacc + ch * 16 + 16, v0, v1);
-            if (r < g.bm) {
+            if (rv && r < g.bm) {
               float4* p0 = reinterpret_cast<float4*>(dst + ((size_t)ch * g.bm + r) * 16);
               float4* p1 = reinterpret_cast<float4*>(dst + ((size_t)(ch + 1) * g.bm + r) * 16);
 #pragma unroll
