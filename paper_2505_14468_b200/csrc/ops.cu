@@ -73,6 +73,50 @@ __global__ void rmsnorm_kernel(T* __restrict__ out, int ldo, const T* __restrict
   }
 }
 
+// Four 8-column chunks per thread (d / 32 threads: 160 for d = 5120), the row kept in
+// registers between the sum of squares and the scaling: one read of x, one write of out, and
+// small CTAs so an SM keeps ~12 rows (~120 KB) of loads in flight — the prefill norms are
+// HBM-bound (16384 x 5120 bf16 rows in and out per config-3 layer).
+constexpr int RN_CH = 4;
+template <typename T>
+__global__ void __launch_bounds__(256) rmsnorm_row_kernel(T* __restrict__ out, int ldo,
+                                                          const T* __restrict__ x, int ldx,
+                                                          const bf16* __restrict__ w, int d,
+                                                          float eps) {
+  __shared__ float red[33];
+  const int t = blockIdx.x;
+  const int nt = blockDim.x;
+  pdl_wait();
+  pdl_trigger();
+  float f[RN_CH][8];
+#pragma unroll
+  for (int c = 0; c < RN_CH; ++c) Vec8<T>::load(x + (size_t)t * ldx + (c * nt + threadIdx.x) * 8, f[c]);
+  float ss = 0.f;
+#pragma unroll
+  for (int c = 0; c < RN_CH; ++c)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ss += f[c][j] * f[c][j];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (nt >> 5) ? red[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[32] = v;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[32] / (float)d + eps);
+#pragma unroll
+  for (int c = 0; c < RN_CH; ++c) {
+    const int i0 = (c * nt + threadIdx.x) * 8;
+    float g[8];
+    Vec8<bf16>::load(w + i0, g);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) f[c][j] = (f[c][j] * inv) * g[j];
+    Vec8<T>::store(out + (size_t)t * ldo + i0, f[c]);
+  }
+}
+
 // x[t] += LoRA delta (rounded to T, written back), then out = rmsnorm(x).  The o-projection
 // expand of the decode step fused into the post-attention norm (slx_rmsnorm_lora).
 template <typename T>
@@ -903,8 +947,12 @@ extern "C" int slx_rmsnorm(int dtype, void* out, int ldo, const void* x, int ldx
   SLX_CHECK_ALIGN(x, 16);
   SLX_CHECK_ALIGN(w, 16);
   if (n_tok == 0) return SLX_OK;
-  int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
   int st = SLX_OK;
+  if (d % (RN_CH * 8 * 32) == 0 && d / (RN_CH * 8) <= 256) {   // the row in registers
+    DISPATCH_DT(dtype, st = launch_ex(rmsnorm_row_kernel<T>, dim3(n_tok), dim3(d / (RN_CH * 8)), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (const T*)x, ldx, (const bf16*)w, d, eps));
+    return st;
+  }
+  int threads = d >= 4096 ? 512 : (d >= 1024 ? 128 : 32);
   DISPATCH_DT(dtype, st = launch_ex(rmsnorm_kernel<T>, dim3(n_tok), dim3(threads), 0, (cudaStream_t)stream, 1u, (T*)out, ldo, (const T*)x, ldx, (const bf16*)w, d, eps));
   return st;
 }
