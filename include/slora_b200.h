@@ -96,17 +96,7 @@ typedef struct slx_splitk_in slx_splitk_in;     /* defined with the K4 entry poi
 typedef struct slx_l2_prefetch {
   const void* ptr[2];
   size_t bytes[2];
-  /* and/or: a window of every CTA's unit range of the NEXT decode GEMM (stream-K partition of
-   * the tiled weight gemm_w with gemm_n rows, gemm_k columns, for gemm_m tokens): units
-   * [unit0, unit0 + units) after each CTA's first unit (a unit = 256 weight rows x 64 k = two
-   * 16 KB boxes), so every CTA of that GEMM finds its first bytes in L2.  gemm_w NULL: off. */
-  const void* gemm_w;
-  int gemm_m, gemm_n, gemm_k;
-  int unit0, units;
 } slx_l2_prefetch;
-/* CTAs of the stream-K decode GEMM slx_gemm_bf16 launches for (M, N, K) on tiled weights
- * (0: another kernel) — sizes slx_l2_prefetch unit windows. */
-SLX_API int slx_gemm_sk_ctas(int M, int N, int K);
 /* Explicit tiling choices (tests / tuning tools; NULL or all-zero = the planner's choice, which
  * is what the product uses).  The library reads no environment variables. */
 typedef struct slx_gemm_tuning {

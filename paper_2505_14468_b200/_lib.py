@@ -62,8 +62,7 @@ class GemmTuning(ctypes.Structure):
 
 class L2Prefetch(ctypes.Structure):
     """slx_l2_prefetch: the next kernel's first bytes (two regions)."""
-    _fields_ = [("ptr", _p * 2), ("bytes", _sz * 2), ("gemm_w", _p), ("gemm_m", _i),
-                ("gemm_n", _i), ("gemm_k", _i), ("unit0", _i), ("units", _i)]
+    _fields_ = [("ptr", _p * 2), ("bytes", _sz * 2)]
 
 
 # name -> (restype, argtypes): every symbol declared in include/slora_b200.h
@@ -77,7 +76,6 @@ SIGNATURES = {
     "slx_debug_gemm_trace": (_i, [_p]),
     "slx_gemm_splitk_bytes": (_sz, [_i, _i, _i]),
     "slx_gemm_bf16_splitk": (_i, [_p, _i, _p, _i, _i, _i, _i, _p, _sz, ctypes.POINTER(L2Prefetch), _p]),
-    "slx_gemm_sk_ctas": (_i, [_i, _i, _i]),
     "slx_gemm_bf16_ex": (_i, [_p, _i, _p, _p, _i, _i, _p, _i, _i, _i, _i, _i, _i, _i, _p, _i, _p,
                               _sz, ctypes.POINTER(L2Prefetch), ctypes.POINTER(GemmTuning), _p]),
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),

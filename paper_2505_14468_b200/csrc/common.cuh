@@ -254,13 +254,7 @@ namespace slx {
 struct PfArgs {
   const char* ptr[2];
   unsigned long long bytes[2];
-  // stream-K window of the next decode GEMM (slx_l2_prefetch.gemm_w): weight base, k-blocks,
-  // units, CTAs, 128-row blocks, unit window [u0, u0 + m) of every CTA's range
-  const char* gw;
-  int g_kb, g_U, g_G, g_nb, g_u0, g_m;
 };
-// stream-K partition of a decode GEMM (gemm_sk.cu): kblocks, units, CTAs; false: not that kernel
-bool sk_partition(int M, int N, int K, int* kblocks, int* units, int* ctas);
 inline PfArgs pf_args(const slx_l2_prefetch* p) {
   PfArgs a{};
   if (p == nullptr) return a;
@@ -268,35 +262,10 @@ inline PfArgs pf_args(const slx_l2_prefetch* p) {
     a.ptr[i] = static_cast<const char*>(p->ptr[i]);
     a.bytes[i] = p->ptr[i] ? (p->bytes[i] & ~15ull) : 0;
   }
-  int kb, U, G;
-  if (p->gemm_w != nullptr && p->units > 0 && p->unit0 >= 0 &&
-      sk_partition(p->gemm_m, p->gemm_n, p->gemm_k, &kb, &U, &G)) {
-    a.gw = static_cast<const char*>(p->gemm_w);
-    a.g_kb = kb; a.g_U = U; a.g_G = G;
-    a.g_nb = (p->gemm_n + 127) / 128;
-    a.g_u0 = p->unit0; a.g_m = p->units;
-  }
   return a;
 }
 // Part `part` of `parts` of both regions, as bulk L2 prefetches of <= 64 KB (one thread).
-__device__ __forceinline__ void l2_prefetch_gemm_part(const PfArgs& pf, int part, int parts) {
-  const int items = pf.g_G * pf.g_m;
-  const int lo = (int)((long long)part * items / parts), hi = (int)((long long)(part + 1) * items / parts);
-  for (int i = lo; i < hi; ++i) {
-    const int c = i / pf.g_m, j = pf.g_u0 + i % pf.g_m;
-    const int u = (int)((long long)c * pf.g_U / pf.g_G) + j;
-    if (u >= (int)((long long)(c + 1) * pf.g_U / pf.g_G)) continue;
-    const int tile = u / pf.g_kb, k = u - tile * pf.g_kb;
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      if (2 * tile + b >= pf.g_nb) continue;
-      const char* p = pf.gw + ((size_t)(2 * tile + b) * pf.g_kb + k) * 16384;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(16384u) : "memory");
-    }
-  }
-}
 __device__ __forceinline__ void l2_prefetch_part(const PfArgs& pf, int part, int parts) {
-  if (pf.gw != nullptr) l2_prefetch_gemm_part(pf, part, parts);
 #pragma unroll
   for (int r = 0; r < 2; ++r) {
     const unsigned long long n = pf.bytes[r];

@@ -723,18 +723,4 @@ int gemm_sk_launch(const SkCall& c) {
   }
 }
 
-bool sk_partition(int M, int N, int K, int* kblocks, int* units, int* ctas) {
-  SkPlan p;
-  if (!sk_plan(M, N, K, &p, nullptr)) return false;
-  *kblocks = p.kblocks;
-  *units = (int)p.U;
-  *ctas = p.G;
-  return true;
-}
-
 }  // namespace slx
-
-extern "C" int slx_gemm_sk_ctas(int M, int N, int K) {
-  int kb, U, G;
-  return slx::sk_partition(M, N, K, &kb, &U, &G) ? G : 0;
-}

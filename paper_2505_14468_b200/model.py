@@ -216,10 +216,8 @@ class MultiLoraModel:
         # (o at 8: +50 us/step)
         self.splitk_consumer = True
         self.splitk_splits_o, self.splitk_splits_dn = 6, 8
-        # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off),
-        # aimed at the first units of EVERY CTA of the next stream-K GEMM (gate/up, q/k/v)
+        # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off)
         self.l2_prefetch_mb = 16.0
-        self.pf_gemm = True
         self._pf_cache: dict = {}
         self.use_tc_sgmv = dtype == torch.bfloat16   # prefill LoRA as grouped tcgen05 GEMMs
         # prefill: the LoRA expand folded into the backbone GEMM as one extra K block
@@ -562,24 +560,6 @@ class MultiLoraModel:
             self._pf_cache[key] = ops.l2_prefetch(*[(getattr(t, "data", t), n) for t in tensors])
         return self._pf_cache[key]
 
-    def _pf_gemm(self, key, w, m: int, n_rows: int, mb: float, after_mb: float = 0.0):
-        """Cached slx_l2_prefetch of a window of every CTA's unit range of the decode GEMM over
-        packed weight ``w`` (``n_rows`` computed rows, ``m`` tokens): ``mb`` MB in total,
-        after the first ``after_mb`` MB (the window an earlier kernel prefetched)."""
-        if mb <= 0:
-            return None
-        key = (key, m)
-        if key not in self._pf_cache:
-            G = ops.gemm_sk_ctas(m, n_rows, w.k)
-            if G <= 0:
-                self._pf_cache[key] = None
-            else:
-                per = G * 32768.0
-                u0 = int(round(after_mb * (1 << 20) / per))
-                units = int(round(mb * (1 << 20) / per))
-                self._pf_cache[key] = ops.l2_prefetch_gemm(w, m, n_rows, u0, units)
-        return self._pf_cache[key]
-
     def _pf_all(self, key, t):
         """slx_l2_prefetch of a whole (packed) weight (spread over a long kernel)."""
         if self.l2_prefetch_mb <= 0:
@@ -705,15 +685,8 @@ class MultiLoraModel:
             pf_qkv = self._pf(("kv", l), self.k_cache[l], self.v_cache[l])
             pf_att = self._pf(p + "wo", w[p + "wo"])
             pf_gu = self._pf(p + "w_down", w[p + "w_down"])
-            wg = w[p + "w_gu"]
-            pf_o = (self._pf_gemm(p + "w_gu/o", wg, T, wg.n, self.l2_prefetch_mb) if self.pf_gemm
-                    else None) or self._pf(p + "w_gu", wg)
-            pf_dn = None
-            if self.pf_gemm and l + 1 < cfg.layers:
-                wq = w[nxt]
-                pf_dn = self._pf_gemm(nxt + "/down", wq, T, wq.n + (wq.n_extra if stacked else 0),
-                                      self.l2_prefetch_mb)
-            pf_dn = pf_dn or self._pf(nxt, w[nxt])
+            pf_o = self._pf(p + "w_gu", w[p + "w_gu"])
+            pf_dn = self._pf(nxt, w[nxt])
             # q / k / v
             d_qkv = None
             if stacked and "w_qkv" in self.stack:

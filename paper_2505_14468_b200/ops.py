@@ -184,23 +184,6 @@ def l2_prefetch(*regions) -> L2Prefetch | None:
     return pf
 
 
-def gemm_sk_ctas(m: int, n: int, k: int) -> int:
-    return int(_lib.load().slx_gemm_sk_ctas(m, n, k))
-
-
-def l2_prefetch_gemm(w: "PackedWeight", m: int, n_rows: int, unit0: int, units: int,
-                     base: L2Prefetch | None = None) -> L2Prefetch | None:
-    """slx_l2_prefetch of units [unit0, unit0 + units) of every CTA's range of the next decode
-    GEMM over the packed weight ``w`` (``n_rows`` = rows it computes, main + stacked) for ``m``
-    tokens; added to ``base``'s regions when given."""
-    if units <= 0:
-        return base
-    pf = base if base is not None else L2Prefetch()
-    pf.gemm_w, pf.gemm_m, pf.gemm_n, pf.gemm_k = w.data.data_ptr(), int(m), int(n_rows), int(w.k)
-    pf.unit0, pf.units = int(unit0), int(units)
-    return pf
-
-
 @_op("gemm", 1)
 def gemm(a: torch.Tensor, w, out: torch.Tensor | None = None, *,
          epilogue: int = EPI_NONE, residual: torch.Tensor | None = None,

@@ -1,7 +1,7 @@
 """Decode-step variants on the config-2 workload (7B shape, 32 x r16, batch 64, ctx 128): the
 same model re-captured under different host-side schedule parameters (L2 prefetch window,
 split-K pieces of o / down), CUDA-graph step time per variant.
-python tools/decode_sweep.py [steps]"""
+python tools/decode_sweep.py [steps] [--combos]"""
 import json
 import os
 import sys
@@ -14,7 +14,7 @@ from paper_2505_14468_b200.config import LLAMA2_7B, LoraConfig  # noqa: E402
 from paper_2505_14468_b200.engine import DecodeGraph  # noqa: E402
 from paper_2505_14468_b200.model import MultiLoraModel  # noqa: E402
 
-steps = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+steps = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 30
 CTX = 128
 cfg = LLAMA2_7B
 torch.cuda.set_device(0)
@@ -56,13 +56,17 @@ def timed(**kw):
 
 
 variants = [{}]
-for mb in (0.0, 8.0, 24.0, 32.0, 48.0):
-    variants.append({"l2_prefetch_mb": mb})
-variants.append({"pf_gemm": False})
-for so in (4, 8):
-    variants.append({"splitk_splits_o": so})
-for sd in (6, 9):
-    variants.append({"splitk_splits_dn": sd})
+if "--combos" in sys.argv:
+    for mb in (8.0, 12.0, 16.0):
+        variants.append({"l2_prefetch_mb": mb})
+    variants.append({})
+else:
+    for mb in (0.0, 8.0, 24.0, 32.0, 48.0):
+        variants.append({"l2_prefetch_mb": mb})
+    for so in (4, 8):
+        variants.append({"splitk_splits_o": so})
+    for sd in (6, 9):
+        variants.append({"splitk_splits_dn": sd})
 for v in variants:
     ms = timed(**v)
     print(json.dumps({"variant": v, "ms_per_step": round(ms, 4),
