@@ -148,11 +148,28 @@ SLX_API int slx_gemm_grouped_bf16(const void* A, int lda, int M, int K, int n_gr
  * == 0).  v [M, ldv] bf16 is the LoRA shrink with the scale folded in (slx_gemm_grouped_bf16
  * with alpha = scale), zero beyond each adapter's rank; b_ptrs[a * n_targets + t] = B [b_rows[t],
  * ranks[a]] row-major.  <= 16 adapters, <= 3 targets.  No separate expand, no y read-modify-write. */
+/* RoPE + KV append fused into the q/k/v projection's epilogue (prefill): with `rope` non-NULL
+ * the GEMM output columns [0, H*D) are q, rotated (rotate-half, cos/sin tables fp32
+ * [max_pos, D/2] at tok_pos[m]) and stored to C; [H*D, (H+Hkv)*D) are k, rotated and stored to
+ * k_cache[tok_seq[m]][kv head][tok_pos[m]][:]; the rest is v, stored to v_cache — the same
+ * arithmetic as slx_rope_kv_write on the bf16-rounded projection, without the round trip through
+ * C (k and v columns of C are not written).  D = 128, H*D and Hkv*D multiples of 256. */
+typedef struct slx_rope_kv {
+  const int32_t* tok_pos;
+  const int32_t* tok_seq;
+  const float* cos_tab;
+  const float* sin_tab;
+  int max_pos;
+  void* k_cache;
+  void* v_cache;
+  int max_ctx;
+  int heads, kv_heads, head_dim;
+} slx_rope_kv;
 SLX_API int slx_gemm_bf16_lorafold(const void* A, int lda, const void* W, int w_layout, void* C,
                   int ldc, int c_dtype, const void* R, int ldr, int M, int N, int K, int epilogue,
                   const void* gtiles, int n_gtiles, const void* v, int ldv, int n_targets,
                   const int* t_bound, int n_adapters, const uint64_t* b_ptrs, const int* b_rows,
-                  const int* ranks, void* stream);
+                  const int* ranks, const slx_rope_kv* rope, void* stream);
 /* Pack a row-major bf16 W[N, K] (row stride ld) into the SLX_W_TILED layout (device kernel).
  * dst must hold slx_packed_weight_elems(N, K) elements. */
 SLX_API size_t slx_packed_weight_elems(int N, int K);

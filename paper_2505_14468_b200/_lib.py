@@ -60,6 +60,13 @@ class GemmTuning(ctypes.Structure):
                 ("gsplit", _i), ("sk_ctas", _i), ("sk_min_units", _i), ("sk_no_cluster", _i)]
 
 
+class RopeKV(ctypes.Structure):
+    """slx_rope_kv: RoPE + KV append fused into the q/k/v projection's epilogue."""
+    _fields_ = [("tok_pos", _p), ("tok_seq", _p), ("cos_tab", _p), ("sin_tab", _p), ("max_pos", _i),
+                ("k_cache", _p), ("v_cache", _p), ("max_ctx", _i), ("heads", _i), ("kv_heads", _i),
+                ("head_dim", _i)]
+
+
 class L2Prefetch(ctypes.Structure):
     """slx_l2_prefetch: the next kernel's first bytes (two regions)."""
     _fields_ = [("ptr", _p * 2), ("bytes", _sz * 2)]
@@ -81,7 +88,7 @@ SIGNATURES = {
     "slx_pack_weight_rows": (_i, [_p, _p, _i, _i, _i, _i, _p]),
     "slx_gemm_group_tile_bytes": (_sz, []),
     "slx_gemm_bf16_lorafold": (_i, [_p, _i, _p, _i, _p, _i, _i, _p, _i, _i, _i, _i, _i, _p, _i, _p, _i,
-                                    _i, _p, _i, _p, _p, _p, _p]),
+                                    _i, _p, _i, _p, _p, _p, ctypes.POINTER(RopeKV), _p]),
     "slx_gemm_grouped_bf16": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p, _i, _i,
                                    _i, _p, _i, _p]),
     "slx_lora_expand": (_i, [_i, _p, _i, _p, _i, _i, _p, _p, _i, _i, _i,

@@ -82,6 +82,14 @@ struct GemmArgs {
   // n-tiles, so the ~148 co-resident CTAs share a few X row blocks and W tiles in L2
   int raster, m_tiles;
   int n_work;    // persistent kernel: tiles to walk (raster grid or gtiles)
+  // RoPE + KV append in the epilogue (slx_rope_kv; persistent kernel, EPI_NONE, bf16 out)
+  int rope, r_h, r_hkv, r_max_ctx;
+  const int32_t* r_pos;
+  const int32_t* r_seq;
+  const float* r_cos;
+  const float* r_sin;
+  bf16* r_kc;
+  bf16* r_vc;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -639,7 +647,60 @@ gemm_tcp_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
       const int m = t.m0 + r;
       if (t.m0 + q * 32 < t.m_lim) {   // warp-uniform
-        if (EPI == SLX_EPI_SILU_MUL) {
+        if (EPI == SLX_EPI_NONE && sizeof(OutT) == 2 && g.rope) {
+          // q: rotate-half RoPE into C; k: rotated into the k cache; v: into the v cache — the
+          // arithmetic of slx_rope_kv_write on the bf16-rounded projection (head_dim 128: two
+          // heads per 256-column tile, pairs (c, c + 64) of a head)
+          const bool row_ok = m < t.m_lim;
+          const int pos = row_ok ? g.r_pos[m] : 0, seq = row_ok ? g.r_seq[m] : 0;
+          const int qc = g.r_h * 128, kcol = qc + g.r_hkv * 128;
+          for (int hh = 0; hh < 2; ++hh) {
+            const int col0 = t.n0 + hh * 128;   // first column of this head
+            const uint32_t th = t_row + hh * 128;
+            if (col0 >= kcol) {   // v
+              bf16* dst = g.r_vc + (((size_t)seq * g.r_hkv + (col0 - kcol) / 128) * g.r_max_ctx + pos) * 128;
+              for (int c0 = 0; c0 < 128; c0 += 32) {
+                float v0[16], v1[16];
+                tc::tmem_ld16x2(th + c0, th + c0 + 16, v0, v1);
+                if (row_ok) {
+                  Vec8<bf16>::store(dst + c0, v0);
+                  Vec8<bf16>::store(dst + c0 + 8, v0 + 8);
+                  Vec8<bf16>::store(dst + c0 + 16, v1);
+                  Vec8<bf16>::store(dst + c0 + 24, v1 + 8);
+                }
+              }
+            } else {   // q or k: rotate
+              bf16* dst = col0 < qc
+                  ? reinterpret_cast<bf16*>(g.C) + (size_t)m * g.ldc + col0
+                  : g.r_kc + (((size_t)seq * g.r_hkv + (col0 - qc) / 128) * g.r_max_ctx + pos) * 128;
+              const float* cr = g.r_cos + (size_t)pos * 64;
+              const float* sr = g.r_sin + (size_t)pos * 64;
+              for (int c0 = 0; c0 < 64; c0 += 16) {
+                float x1[16], x2[16];
+                tc::tmem_ld16x2(th + c0, th + c0 + 64, x1, x2);
+                if (row_ok) {
+                  float cs[16], sn[16], r1[16], r2[16];
+#pragma unroll
+                  for (int e = 0; e < 16; e += 8) {
+                    Vec8<float>::load(cr + c0 + e, cs + e);
+                    Vec8<float>::load(sr + c0 + e, sn + e);
+                  }
+#pragma unroll
+                  for (int e = 0; e < 16; ++e) {
+                    const float a1 = __bfloat162float(__float2bfloat16_rn(x1[e]));
+                    const float a2 = __bfloat162float(__float2bfloat16_rn(x2[e]));
+                    r1[e] = a1 * cs[e] - a2 * sn[e];
+                    r2[e] = a2 * cs[e] + a1 * sn[e];
+                  }
+                  Vec8<bf16>::store(dst + c0, r1);
+                  Vec8<bf16>::store(dst + c0 + 8, r1 + 8);
+                  Vec8<bf16>::store(dst + c0 + 64, r2);
+                  Vec8<bf16>::store(dst + c0 + 72, r2 + 8);
+                }
+              }
+            }
+          }
+        } else if (EPI == SLX_EPI_SILU_MUL) {
           for (int c0 = 0; c0 < BN / 2; c0 += 16) {
             float gv[16], uv[16];
             tc::tmem_ld16x2(t_row + c0, t_row + BN / 2 + c0, gv, uv);
@@ -1101,7 +1162,7 @@ extern "C" int slx_gemm_bf16_lorafold(const void* A, int lda, const void* W, int
                                       int K, int epilogue, const void* gtiles, int n_gtiles,
                                       const void* v, int ldv, int n_targets, const int* t_bound,
                                       int n_adapters, const uint64_t* b_ptrs, const int* b_rows,
-                                      const int* ranks, void* stream) {
+                                      const int* ranks, const slx_rope_kv* rope, void* stream) {
   SLX_CHECK_ARG(A && W && C && v && gtiles && t_bound && M > 0 && N > 0 && K > 0 &&
                 K % 8 == 0 && lda >= K && lda % 8 == 0 && ldc % 8 == 0 && n_gtiles >= 0 &&
                 n_targets >= 1 && n_targets <= 3 && n_adapters >= 0 && n_adapters <= 16 &&
@@ -1138,6 +1199,23 @@ extern "C" int slx_gemm_bf16_lorafold(const void* A, int lda, const void* W, int
   a.C = C; a.ldc = ldc; a.R = R; a.ldr = ldr; a.w_tiled = w_layout == SLX_W_TILED; a.n_main = N;
   a.gtiles = (const GroupTile*)gtiles;
   a.lfold = 1;
+  if (rope != nullptr) {
+    SLX_CHECK_ARG(epilogue == SLX_EPI_NONE && c_dtype == SLX_DT_BF16 && rope->head_dim == 128 &&
+                  rope->tok_pos && rope->tok_seq && rope->cos_tab && rope->sin_tab &&
+                  rope->k_cache && rope->v_cache && rope->max_ctx > 0 && rope->heads > 0 &&
+                  rope->kv_heads > 0 && rope->heads % rope->kv_heads == 0 &&
+                  (rope->heads * 128) % 256 == 0 && (rope->kv_heads * 128) % 256 == 0 &&
+                  N == (rope->heads + 2 * rope->kv_heads) * 128);
+    SLX_CHECK_ALIGN(rope->k_cache, 16);
+    SLX_CHECK_ALIGN(rope->v_cache, 16);
+    SLX_CHECK_ALIGN(rope->cos_tab, 16);
+    SLX_CHECK_ALIGN(rope->sin_tab, 16);
+    a.rope = 1;
+    a.r_h = rope->heads; a.r_hkv = rope->kv_heads; a.r_max_ctx = rope->max_ctx;
+    a.r_pos = rope->tok_pos; a.r_seq = rope->tok_seq;
+    a.r_cos = rope->cos_tab; a.r_sin = rope->sin_tab;
+    a.r_kc = (bf16*)rope->k_cache; a.r_vc = (bf16*)rope->v_cache;
+  }
   a.lnt = n_targets;
   for (int t = 0; t < 4; ++t) a.lbound[t] = t < n_targets ? t_bound[t] : 0;
   CUtensorMap mx, mw;

@@ -771,6 +771,9 @@ class MultiLoraModel:
             if sgmv and slot_host is None:
                 slot_host = slot.cpu().numpy()
             plan, fold, sgmv_plan = self._prefill_plans(segments, slot_host, T, flash, sgmv)
+        # RoPE + KV append fused into the q/k/v GEMM's epilogue (LoRA-fold path, head_dim 128)
+        rope_fused = (fold is not None and not decode and cfg.head_dim == 128
+                      and (cfg.heads * 128) % 256 == 0 and (cfg.kv_heads * 128) % 256 == 0)
         if sgmv:
             if fold is None:
                 v_buf = torch.empty((T, 64), dtype=dt, device=dev)
@@ -791,7 +794,10 @@ class MultiLoraModel:
                     for i, t in enumerate(("q", "k", "v")):
                         ops.gemm_grouped(h, cfg.hidden, ga[t], fold[3], v_qkv_f[:, 64 * i:64 * i + 64], 64)
                 ops.gemm_lorafold(h, w[p + "w_qkv"], qkv, fold[1], v_qkv_f,
-                                  [0, cfg.q_dim, cfg.q_dim + cfg.kv_dim], bp, bq, rk)
+                                  [0, cfg.q_dim, cfg.q_dim + cfg.kv_dim], bp, bq, rk,
+                                  rope=(ops.rope_kv(cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,
+                                                    self.cos, self.sin, self.k_cache[l],
+                                                    self.v_cache[l]) if rope_fused else None))
             elif stacked and "w_qkv" in self.stack:
                 ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv)
                 self._expand(qkv, v_qkv, l, "w_qkv", qkv_cols)
@@ -804,8 +810,9 @@ class MultiLoraModel:
                 ops.rope_attention_decode(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos,
                                           seq, self.cos, self.sin, self.k_cache[l], self.v_cache[l])
             else:
-                ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
-                                  self.sin, self.k_cache[l], self.v_cache[l])
+                if not (rope_fused and fold is not None):
+                    ops.rope_kv_write(qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq, self.cos,
+                                      self.sin, self.k_cache[l], self.v_cache[l])
                 if flash:
                     ops.attention_prefill(attn, qkv, cfg.heads, cfg.kv_heads, cfg.head_dim, plan,
                                           self.k_cache[l], self.v_cache[l])

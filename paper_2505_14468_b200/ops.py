@@ -13,7 +13,7 @@ import torch
 
 from . import _lib
 from ._lib import (DT_BF16, DT_F32, EPI_NONE, EPI_RESIDUAL, EPI_SILU_MUL, W_ROWMAJOR, W_TILED,
-                   GemmTuning, L2Prefetch, LoraDelta, LoraTarget, SplitKIn, check)
+                   GemmTuning, L2Prefetch, LoraDelta, LoraTarget, RopeKV, SplitKIn, check)
 
 _DT = {torch.bfloat16: DT_BF16, torch.float32: DT_F32}
 
@@ -342,12 +342,24 @@ def lora_shrink(v: torch.Tensor, x: torch.Tensor, slot_rank, max_rank: int, targ
 GROUP_MAX = 16
 
 
+def rope_kv(heads, kv_heads, head_dim, tok_pos, tok_seq, cos, sin, k_cache, v_cache) -> RopeKV:
+    """slx_rope_kv: fuse RoPE + the KV append into a q/k/v projection (gemm_lorafold)."""
+    r = RopeKV()
+    r.tok_pos, r.tok_seq = tok_pos.data_ptr(), tok_seq.data_ptr()
+    r.cos_tab, r.sin_tab, r.max_pos = cos.data_ptr(), sin.data_ptr(), cos.shape[0]
+    r.k_cache, r.v_cache, r.max_ctx = k_cache.data_ptr(), v_cache.data_ptr(), k_cache.shape[2]
+    r.heads, r.kv_heads, r.head_dim = heads, kv_heads, head_dim
+    return r
+
+
 @_op("gemm", 1)
 def gemm_lorafold(a: torch.Tensor, w, out: torch.Tensor, gtiles: torch.Tensor, v: torch.Tensor,
-                  t_bound, b_ptrs, b_rows, ranks, residual: torch.Tensor | None = None) -> torch.Tensor:
+                  t_bound, b_ptrs, b_rows, ranks, residual: torch.Tensor | None = None,
+                  rope: RopeKV | None = None) -> torch.Tensor:
     """Prefill backbone GEMM with the LoRA expand as one extra K block per grouped tile
     (slx_gemm_bf16_lorafold).  w: PackedWeight; v: bf16 [T, 64 * targets] shrink (scale folded);
-    b_ptrs: per (adapter, target) B addresses (adapter-major)."""
+    b_ptrs: per (adapter, target) B addresses (adapter-major); ``rope`` (rope_kv): RoPE + KV
+    append fused into the epilogue (q/k/v projection)."""
     if a.dtype != torch.bfloat16 or not isinstance(w, PackedWeight) or v.dtype != torch.bfloat16:
         raise ValueError("gemm_lorafold: bf16 activations, packed weight, bf16 v")
     M, K = a.shape
@@ -359,7 +371,8 @@ def gemm_lorafold(a: torch.Tensor, w, out: torch.Tensor, gtiles: torch.Tensor, v
         _ld(residual) if residual is not None else 0, M, w.n, K, epi, _ptr(gtiles), gtiles.shape[0],
         _ptr(v), _ld(v), nt, arr(ctypes.c_int, list(t_bound)), len(ranks),
         arr(ctypes.c_uint64, list(b_ptrs)), arr(ctypes.c_int, list(b_rows)),
-        arr(ctypes.c_int, list(ranks)), _stream()), "slx_gemm_bf16_lorafold")
+        arr(ctypes.c_int, list(ranks)), None if rope is None else ctypes.byref(rope), _stream()),
+        "slx_gemm_bf16_lorafold")
     return out
 
 
