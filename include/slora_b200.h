@@ -135,9 +135,12 @@ SLX_API int slx_debug_gemm_trace(void* buf);
  * W_group is row-major [w_rows, w_cols] (row stride w_ld) and columns >= w_cols read as 0.
  * Up to 16 groups per call; host arrays w_ptrs/w_rows/w_cols/w_ld/alpha; gtiles on device
  * (slx_gemm_group_tile_bytes() each).  Prefill LoRA: shrink with W = A_adapter (alpha =
- * scale), expand with A = v and W = B_adapter (residual in place). */
+ * scale), expand with A = v and W = B_adapter (residual in place).  n_seg > 1 (<= 4): the
+ * arrays hold n_groups x n_seg entries (group-major) and output columns [64 s, 64 s + 64) of a
+ * tile come from W entry group * n_seg + s (<= 64 rows each; N <= 64 n_seg): e.g. the q, k and
+ * v shrinks of one adapter in ONE pass over A. */
 SLX_API size_t slx_gemm_group_tile_bytes(void);
-SLX_API int slx_gemm_grouped_bf16(const void* A, int lda, int M, int K, int n_groups,
+SLX_API int slx_gemm_grouped_bf16(const void* A, int lda, int M, int K, int n_groups, int n_seg,
                   const uint64_t* w_ptrs, const int* w_rows, const int* w_cols, const int* w_ld,
                   const float* alpha, void* C, int ldc, int c_dtype, const void* R, int ldr, int N,
                   int epilogue, const void* gtiles, int n_gtiles, void* stream);

@@ -89,8 +89,8 @@ SIGNATURES = {
     "slx_gemm_group_tile_bytes": (_sz, []),
     "slx_gemm_bf16_lorafold": (_i, [_p, _i, _p, _i, _p, _i, _i, _p, _i, _i, _i, _i, _i, _p, _i, _p, _i,
                                     _i, _p, _i, _p, _p, _p, ctypes.POINTER(RopeKV), _p]),
-    "slx_gemm_grouped_bf16": (_i, [_p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p, _i, _i,
-                                   _i, _p, _i, _p]),
+    "slx_gemm_grouped_bf16": (_i, [_p, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _i, _i, _p, _i,
+                                   _i, _i, _p, _i, _p]),
     "slx_lora_expand": (_i, [_i, _p, _i, _p, _i, _i, _p, _p, _i, _i, _i,
                              ctypes.POINTER(LoraTarget), ctypes.POINTER(_i), _i, _p, _sz, _p]),
     "slx_lora_shrink": (_i, [_i, _p, _i, _p, _i, _i, _i, _p, _i, _i, _i,

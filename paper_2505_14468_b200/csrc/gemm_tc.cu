@@ -82,6 +82,9 @@ struct GemmArgs {
   // n-tiles, so the ~148 co-resident CTAs share a few X row blocks and W tiles in L2
   int raster, m_tiles;
   int n_work;    // persistent kernel: tiles to walk (raster grid or gtiles)
+  // grouped mode with gseg > 1: every tile's B operand is gseg 64-row segments, segment s from
+  // map [group * gseg + s] (e.g. the q, k, v A matrices of one adapter: one shrink launch)
+  int gseg;
   // RoPE + KV append in the epilogue (slx_rope_kv; persistent kernel, EPI_NONE, bf16 out)
   int rope, r_h, r_hkv, r_max_ctx;
   const int32_t* r_pos;
@@ -511,7 +514,7 @@ __device__ __forceinline__ TcpTile tcp_tile(const GemmArgs& g, const GroupMaps& 
   }
   t.n_kb = g.kblocks;
   const bool lfold = GROUPED && g.lfold;
-  t.alpha = (GROUPED && !lfold) ? gm.alpha[t.group] : 1.f;
+  t.alpha = (GROUPED && !lfold) ? gm.alpha[t.group * (g.gseg > 1 ? g.gseg : 1)] : 1.f;
   t.ltgt = 0;
   if (lfold) {
 #pragma unroll
@@ -568,6 +571,8 @@ gemm_tcp_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       const uint64_t pol_x = tc::policy_evict_last();
       int i = 0;
       bool waited = GROUPED;
+      const bool segs = GROUPED && !g.lfold && g.gseg > 1;
+      const int stage_tx = segs ? x_bytes + g.gseg * (W_BLOCK_BYTES / 2) : stage_bytes;
       for (int L = blockIdx.x; L < g.n_work; L += gridDim.x) {
         if (L + (int)gridDim.x >= g.n_work && waited) pdl_trigger();
         const TcpTile t = tcp_tile<GROUPED>(g, gm, L);
@@ -577,13 +582,19 @@ gemm_tcp_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           const int s = i % g.stages;
           tc::mbar_wait(&empty[s], ((i / g.stages) & 1) ^ 1);
           uint8_t* st = smem + s * stage_bytes;
-          tc::mbar_arrive_expect_tx(&full[s], stage_bytes);
-          if (kk < t.n_kb) {
+          tc::mbar_arrive_expect_tx(&full[s], t.lblk && kk >= t.n_kb ? stage_bytes : stage_tx);
+          if (kk < t.n_kb && segs) {   // 64-row segments, each from its own map
+            for (int sg = 0; sg < g.gseg; ++sg)
+              tc::tma_load_2d(st + x_bytes + sg * (W_BLOCK_BYTES / 2), &gm.w[t.group * g.gseg + sg],
+                              &full[s], kk * TC_BK, 0, pol_w);
+          } else if (kk < t.n_kb) {
             for (int b = 0; b < WB; ++b) {
               int c0, c1;
               w_coord(g, t.n0 + b * 128, kk, c0, c1);
               tc::tma_load_2d(st + x_bytes + b * W_BLOCK_BYTES, wmap, &full[s], c0, c1, pol_w);
             }
+          }
+          if (kk < t.n_kb) {
             if (!waited) {   // weights first; the activations come from the previous kernel
               pdl_wait();
               waited = true;
@@ -1237,13 +1248,14 @@ extern "C" int slx_gemm_bf16_lorafold(const void* A, int lda, const void* W, int
 }
 
 extern "C" int slx_gemm_grouped_bf16(const void* A, int lda, int M, int K, int n_groups,
-                                     const uint64_t* w_ptrs, const int* w_rows, const int* w_cols,
-                                     const int* w_ld, const float* alpha, void* C, int ldc, int c_dtype,
-                                     const void* R, int ldr, int N, int epilogue,
+                                     int n_seg, const uint64_t* w_ptrs, const int* w_rows,
+                                     const int* w_cols, const int* w_ld, const float* alpha, void* C,
+                                     int ldc, int c_dtype, const void* R, int ldr, int N, int epilogue,
                                      const void* gtiles, int n_gtiles, void* stream) {
   SLX_CHECK_ARG(A && C && w_ptrs && w_rows && w_cols && w_ld && alpha && gtiles && M > 0 && K > 0 &&
                 K % 8 == 0 && lda >= K && lda % 8 == 0 && ldc % 8 == 0 && N > 0 &&
-                n_groups >= 1 && n_groups <= TC_MAX_GROUPS && n_gtiles >= 0);
+                n_groups >= 1 && n_groups <= TC_MAX_GROUPS && n_gtiles >= 0 && n_seg >= 1 &&
+                n_seg <= 4 && n_groups * n_seg <= TC_MAX_MAPS && (n_seg == 1 || N <= 64 * n_seg));
   SLX_CHECK_ARG(epilogue == SLX_EPI_NONE || epilogue == SLX_EPI_RESIDUAL);
   SLX_CHECK_ARG(c_dtype == SLX_DT_BF16 || c_dtype == SLX_DT_F32);
   if (epilogue == SLX_EPI_RESIDUAL) SLX_CHECK_ARG(R != nullptr && ldr % 8 == 0);
@@ -1251,17 +1263,20 @@ extern "C" int slx_gemm_grouped_bf16(const void* A, int lda, int M, int K, int n
   SLX_CHECK_ALIGN(C, 16);
   if (n_gtiles == 0) return SLX_OK;
   GroupMaps gm{};
-  for (int i = 0; i < n_groups; ++i) {
-    // per-group K extent: columns >= w_cols[i] (e.g. beyond an adapter's rank) read as zeros
+  for (int i = 0; i < n_groups * n_seg; ++i) {
+    // per-map K extent: columns >= w_cols[i] read as zeros; with segments (n_seg > 1) map i is
+    // segment i % n_seg of group i / n_seg: <= 64 rows (rows beyond w_rows read as zeros)
     SLX_CHECK_ARG(w_ptrs[i] != 0 && w_rows[i] > 0 && w_cols[i] > 0 && w_cols[i] <= K &&
-                  w_ld[i] >= w_cols[i] && w_ld[i] % 8 == 0);
-    if (!make_tmap(&gm.w[i], (const void*)w_ptrs[i], w_rows[i], w_cols[i], w_ld[i], 128))
+                  w_ld[i] >= w_cols[i] && w_ld[i] % 8 == 0 && (n_seg == 1 || w_rows[i] <= 64));
+    if (!make_tmap(&gm.w[i], (const void*)w_ptrs[i], w_rows[i], w_cols[i], w_ld[i],
+                   n_seg > 1 ? 64 : 128))
       return SLX_ERR_CUDA;
     gm.alpha[i] = alpha[i];
   }
   GemmArgs a{};
   a.M = M; a.N = N; a.K = K;
   a.bm = 128; a.kblocks = ceil_div(K, TC_BK); a.splits = 1; a.n_tiles = 1;
+  a.gseg = n_seg;
   const size_t stage = (size_t)128 * TC_BK * 2 + 2 * W_BLOCK_BYTES;
   a.stages = a.kblocks < 4 ? (a.kblocks < 2 ? 2 : a.kblocks) : 4;
   const size_t smem = (size_t)a.stages * stage + BAR_BYTES + 1024;

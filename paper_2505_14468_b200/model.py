@@ -790,9 +790,9 @@ class MultiLoraModel:
             ops.rmsnorm(h, x, w[p + "input_norm"], cfg.rms_eps)
             if fold is not None:
                 ga, bp, rk = self._fold_lora(l, fold[0], "w_qkv")
-                if fold[3] is not None:
-                    for i, t in enumerate(("q", "k", "v")):
-                        ops.gemm_grouped(h, cfg.hidden, ga[t], fold[3], v_qkv_f[:, 64 * i:64 * i + 64], 64)
+                if fold[3] is not None:   # q, k, v shrinks in one pass over h
+                    segs = [e for a in range(len(fold[0])) for e in (ga["q"][a], ga["k"][a], ga["v"][a])]
+                    ops.gemm_grouped(h, cfg.hidden, segs, fold[3], v_qkv_f, 192, n_seg=3)
                 ops.gemm_lorafold(h, w[p + "w_qkv"], qkv, fold[1], v_qkv_f,
                                   [0, cfg.q_dim, cfg.q_dim + cfg.kv_dim], bp, bq, rk,
                                   rope=(ops.rope_kv(cfg.heads, cfg.kv_heads, cfg.head_dim, pos, seq,

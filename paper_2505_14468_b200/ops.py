@@ -378,16 +378,18 @@ def gemm_lorafold(a: torch.Tensor, w, out: torch.Tensor, gtiles: torch.Tensor, v
 
 @_op("lora", 1)
 def gemm_grouped(a: torch.Tensor, k: int, groups, gtiles: torch.Tensor, out: torch.Tensor, n: int,
-                 residual: torch.Tensor | None = None) -> torch.Tensor:
-    """Grouped tcgen05 GEMM.  groups: [(w_ptr, w_rows, w_cols, w_ld, alpha)] (<= 16);
-    gtiles: device int32 [n_tiles, 4] of (group, m0, m_rows, n0)."""
+                 residual: torch.Tensor | None = None, n_seg: int = 1) -> torch.Tensor:
+    """Grouped tcgen05 GEMM.  groups: [(w_ptr, w_rows, w_cols, w_ld, alpha)] (<= 16 groups;
+    with ``n_seg`` > 1, n_seg entries per group, group-major: output columns [64 s, 64 s + 64)
+    from entry s of the tile's group); gtiles: device int32 [n_tiles, 4] of (group, m0, m_rows,
+    n0)."""
     g = list(groups)
-    if not 1 <= len(g) <= GROUP_MAX:
-        raise ValueError("gemm_grouped: 1..16 groups per call")
+    if not 1 <= len(g) // n_seg <= GROUP_MAX or len(g) % n_seg:
+        raise ValueError("gemm_grouped: 1..16 groups per call (n_seg entries each)")
     arr = lambda t, vals: (t * len(vals))(*vals)  # noqa: E731
     epi = EPI_RESIDUAL if residual is not None else EPI_NONE
     check(_lib.load().slx_gemm_grouped_bf16(
-        _ptr(a), _ld(a), a.shape[0], k, len(g), arr(ctypes.c_uint64, [x[0] for x in g]),
+        _ptr(a), _ld(a), a.shape[0], k, len(g) // n_seg, n_seg, arr(ctypes.c_uint64, [x[0] for x in g]),
         arr(ctypes.c_int, [x[1] for x in g]), arr(ctypes.c_int, [x[2] for x in g]),
         arr(ctypes.c_int, [x[3] for x in g]), arr(ctypes.c_float, [x[4] for x in g]),
         _ptr(out), _ld(out), _dt(out), _ptr(residual), _ld(residual) if residual is not None else 0,

@@ -8,6 +8,10 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2505_14468_b200 import _lib  # noqa: E402
+
+if len(sys.argv) > 2:   # experiment builds: python tools/attn_bench.py reps path/to/lib.so
+    _lib.LIB_PATH = os.path.abspath(sys.argv[2])
 from paper_2505_14468_b200.model import rope_tables  # noqa: E402
 from paper_2505_14468_b200 import ops  # noqa: E402
 

@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 evidence after the persistent prefill GEMM: config-3 bench line, prefill launch list
+# Round evidence, config 3: config-3 bench line, prefill launch list
 # (tensor pipe, DRAM bytes per launch), decode against the config-3 adapter pool.
 set -u
 mkdir -p gpurun_out
