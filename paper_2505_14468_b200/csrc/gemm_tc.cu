@@ -147,9 +147,18 @@ __device__ __forceinline__ void store_cols(const GemmArgs& g, OutT* C, const Out
   }
   const int lim = g.C2 != nullptr ? g.n_main : n_out;
   if (EPI == SLX_EPI_RESIDUAL) {
+    const OutT* rr = R + (size_t)m * g.ldr + n;
+    if (n + 16 <= lim && (reinterpret_cast<uintptr_t>(rr) & 15) == 0) {   // two 16 B loads
+      float r[16];
+      Vec8<OutT>::load(rr, r);
+      Vec8<OutT>::load(rr + 8, r + 8);
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (n + j < lim) v[j] += to_f32(R[(size_t)m * g.ldr + n + j]);
+      for (int j = 0; j < 16; ++j) v[j] += r[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (n + j < lim) v[j] += to_f32(rr[j]);
+    }
   }
   store16(C + (size_t)m * g.ldc, n, lim, v);
 }
