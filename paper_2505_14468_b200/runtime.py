@@ -79,6 +79,9 @@ class ServingRuntime:
         self.t0 = time.perf_counter()
         self.decode_steps = 0
         self.graph_steps = 0
+        # host wall time per phase of step() (seconds): batcher round + admission, merged
+        # prefill (through its sampled tokens on the host), decode step, bookkeeping
+        self.phase_s = {"schedule": 0.0, "prefill": 0.0, "decode": 0.0, "retire": 0.0}
 
     def now_ms(self) -> float:
         return (time.perf_counter() - self.t0) * 1000.0
@@ -232,6 +235,7 @@ class ServingRuntime:
     def step(self) -> list:
         """One scheduler tick: admit the flushes, prefill them together, decode everyone.
         Returns the FlushDecisions taken this round."""
+        c0 = time.perf_counter()
         now = self.now_ms()
         free_bytes = self.free_kv_slots() * self.kv_slot_bytes()
         for fid, q in self.queues.items():   # queue caps follow the free KV room
@@ -239,6 +243,8 @@ class ServingRuntime:
         contention = {self.gpu_id: 1 if self.active else 0}
         decisions = schedule_round(list(self.queues.values()), contention, now, self.tick_ms)
         flushed = self._admit(decisions)
+        c1 = time.perf_counter()
+        self.phase_s["schedule"] += c1 - c0
         if flushed:
             seqs = []
             try:
@@ -266,8 +272,11 @@ class ServingRuntime:
                 r.generated.append(int(tok))
                 r.first_token_ms = t
             self.active += batch.requests
+        c2 = time.perf_counter()
+        self.phase_s["prefill"] += c2 - c1
         self._retire()
         if self.active:
+            c3 = time.perf_counter()
             batch = build_decode(self.active, self.m.seq_len)
             if int(batch.pos.max()) >= self.m.max_ctx:
                 raise RuntimeError("a sequence reached max_ctx (submit() admits only fitting requests)")
@@ -280,11 +289,14 @@ class ServingRuntime:
                                         self._i32(batch.seq), self._i32(batch.slot), decode=True)
                 nxt = self.m.argmax(logits).cpu().numpy()
             self.decode_steps += 1
+            c4 = time.perf_counter()
+            self.phase_s["decode"] += c4 - c3
             for r in batch.requests:
                 self.m.seq_len[r.seq] += 1
             for r, tok in zip(batch.requests, nxt):
                 r.generated.append(int(tok))
             self._retire()
+            self.phase_s["retire"] += time.perf_counter() - c4
         return decisions
 
     def _retire(self) -> None:
@@ -332,7 +344,8 @@ class ServingRuntime:
         toks = sum(len(r.generated) for r in done)
         out = {"requests": len(done), "output_tokens": toks,
                "tokens_per_s": toks / span_s if span_s > 0 else None,
-               "decode_steps": self.decode_steps, "graph_steps": self.graph_steps}
+               "decode_steps": self.decode_steps, "graph_steps": self.graph_steps,
+               "host_s_by_phase": {k: round(v, 3) for k, v in self.phase_s.items()}}
         for name, vals in (("ttft_ms", ttft), ("e2e_ms", e2e), ("tpot_ms", tpot)):
             if vals:
                 out[name] = {"p50": pct(vals, 50), "p90": pct(vals, 90), "p99": pct(vals, 99),
