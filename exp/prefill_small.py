@@ -20,7 +20,11 @@ m.random_backbone(seed=0)
 for a in range(24):
     m.pool.load_random(a, LoraConfig(16, 32.0), seed=100 + a)
 rng = np.random.default_rng(0)
-for nseg, L in ((4, 64), (8, 60), (2, 200)):
+cases = [(4, 64, "stacked"), (4, 64, "gather"), (8, 60, "stacked"), (8, 60, "gather"), (2, 200, True),
+         (2, 200, "stacked"), (4, 128, True), (4, 128, "stacked"), (16, 64, "stacked"), (16, 64, "gather")]
+for nseg, L, fold in cases:
+    m.lora_fold = fold is True
+    m.prefill_small_lora = fold if isinstance(fold, str) else "stacked"
     prompts = [list(map(int, rng.integers(1, cfg.vocab, size=L))) for _ in range(nseg)]
     ids = list(range(nseg))
     for _ in range(3):
@@ -47,9 +51,11 @@ for nseg, L in ((4, 64), (8, 60), (2, 200)):
     seqs, lg = m.prefill(prompts, ids)
     for s_ in seqs:
         m.free_seq(s_)
-    print(f"{nseg} x {L} tokens: host launch {np.median(host):.2f} ms, device {np.median(dev):.2f} ms, "
+    print(f"{nseg} x {L} tokens (fold {fold}): host launch {np.median(host):.2f} ms, device {np.median(dev):.2f} ms, "
           f"{ops.launch_count() - n0} launches")
-for nseg, L in ((4, 64), (2, 200)):
+for nseg, L, fold in cases:
+    m.lora_fold = fold is True
+    m.prefill_small_lora = fold if isinstance(fold, str) else "stacked"
     prompts = [list(map(int, rng.integers(1, cfg.vocab, size=L))) for _ in range(nseg)]
     with ops.KernelTimer() as kt:
         torch.cuda._sleep(100_000_000)
@@ -57,4 +63,4 @@ for nseg, L in ((4, 64), (2, 200)):
     torch.cuda.synchronize()
     for s_ in seqs:
         m.free_seq(s_)
-    print(nseg, L, {k: (round(v[0], 2), v[1]) for k, v in kt.durations().items()})
+    print(nseg, L, fold, {k: (round(v[0], 2), v[1]) for k, v in kt.durations().items()})

@@ -223,6 +223,9 @@ class MultiLoraModel:
         # prefill: the LoRA expand folded into the backbone GEMM as one extra K block
         self.lora_fold = True
         self._plan_cache: dict = {}   # prefill plans by segment layout (_prefill_plans)
+        # prefill batches the fold rejects, up to this many tokens: gathered LoRA kernels
+        self.prefill_gather_max_tokens = 1024
+        self.prefill_small_lora = "stacked"   # or "gather" (no stacked pool: always gather)
         self.pool.on_install = self._stack_install
         self.pool.on_evict = self._stack_evict
 
@@ -725,7 +728,7 @@ class MultiLoraModel:
         segment layout and the segments' adapter slots (a serving loop re-plans only when the
         batch shape changes; the plans are device tensors built once)."""
         key = (tuple(tuple(int(v) for v in sg) for sg in segments),
-               tuple(int(slot_host[sg[0]]) for sg in segments), T, flash, sgmv)
+               tuple(int(slot_host[sg[0]]) for sg in segments), T, flash, sgmv, self.lora_fold)
         hit = self._plan_cache.get(key)
         if hit is not None:
             return hit
@@ -774,6 +777,24 @@ class MultiLoraModel:
         # RoPE + KV append fused into the q/k/v GEMM's epilogue (LoRA-fold path, head_dim 128)
         rope_fused = (fold is not None and not decode and cfg.head_dim == 128
                       and (cfg.heads * 128) % 256 == 0 and (cfg.kv_heads * 128) % 256 == 0)
+        # short-segment batches the fold rejects (a serving round's merged small prompts): the
+        # gathered shrink / expand kernels of the decode path, parallel over token tiles, instead
+        # of per-segment grouped GEMMs whose few CTAs each walk the whole K
+        small = (sgmv and fold is None and T <= self.prefill_gather_max_tokens
+                 and set(self.targets) <= {"q", "k", "v", "o"} and self.pool.max_rank <= 64)
+        if small and self.prefill_small_lora == "stacked" and self.use_stacked_decode and self.stack:
+            # or the stacked shrink as the projection GEMM's side output (no shrink launches)
+            stacked, small, sgmv_plan = True, False, None
+            v_qkv = (torch.empty((T, self._extra_rows("w_qkv")), dtype=torch.float32, device=dev)
+                     if "w_qkv" in self.stack else None)
+            v_o = (torch.empty((T, self._extra_rows("wo")), dtype=torch.float32, device=dev)
+                   if "wo" in self.stack else None)
+        gather_pf = small
+        if gather_pf:
+            qkv_names = tuple(t for t in ("q", "k", "v") if t in self.targets)
+            v_g = torch.empty((T, max(1, len(qkv_names)) * self.pool.max_rank), dtype=torch.float32,
+                              device=dev)
+            sgmv_plan = None
         if sgmv:
             if fold is None:
                 v_buf = torch.empty((T, 64), dtype=dt, device=dev)
@@ -801,6 +822,11 @@ class MultiLoraModel:
             elif stacked and "w_qkv" in self.stack:
                 ops.gemm(h, w[p + "w_qkv"], qkv, side=v_qkv)
                 self._expand(qkv, v_qkv, l, "w_qkv", qkv_cols)
+            elif gather_pf:
+                self._gemm(h, w[p + "w_qkv"], qkv)
+                if qkv_names:
+                    self._gather_shrink(l, qkv_names, h, v_g)
+                    self._gather_expand(l, qkv_names, qkv, v_g, qkv_cols)
             else:
                 self._gemm(h, w[p + "w_qkv"], qkv)
                 if not (sgmv_plan is not None and
@@ -828,6 +854,11 @@ class MultiLoraModel:
             elif stacked and "wo" in self.stack:
                 ops.gemm(attn, w[p + "wo"], x, epilogue=EPI_RESIDUAL, residual=x, side=v_o)
                 self._expand(x, v_o, l, "wo", {"o": (0, d, d)})
+            elif gather_pf:
+                self._gemm(attn, w[p + "wo"], x, residual=x)
+                if "o" in self.targets:
+                    self._gather_shrink(l, ("o",), attn, v_g)
+                    self._gather_expand(l, ("o",), x, v_g, {"o": (0, d, d)})
             else:
                 self._gemm(attn, w[p + "wo"], x, residual=x)
                 if not (sgmv_plan is not None and

@@ -216,9 +216,12 @@ def test_bf16_decode_splitk_consumer_matches_oracle():
     np.testing.assert_allclose(out[True], ref, rtol=BF16_RTOL, atol=BF16_ATOL)
 
 
-def test_bf16_prefill_tc_path_matches_oracle():
-    """Prefill with the tensor-core paths (flash attention, SGMV as grouped tcgen05 GEMMs) on a
-    head_dim-128 GQA model with mixed adapter ranks {8,16,64} == SIMT paths == oracle."""
+@pytest.mark.parametrize("small_lora", ["stacked", "gather"])
+def test_bf16_prefill_tc_path_matches_oracle(small_lora):
+    """Prefill with the tensor-core paths on a head_dim-128 GQA model with mixed adapter ranks
+    {8,16,64} == SIMT paths == oracle.  The short ragged segments make the LoRA fold decline,
+    so the LoRA runs as the small-batch path: the stacked shrink as the projection GEMM's side
+    output + expand kernel, or the gathered shrink / expand kernels."""
     from paper_2505_14468_b200.config import BackboneConfig
     cfg = BackboneConfig("small128", hidden=512, layers=2, heads=4, kv_heads=2, head_dim=128,
                          ffn=1024, vocab=1000)
@@ -233,6 +236,7 @@ def test_bf16_prefill_tc_path_matches_oracle():
         m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=8, max_ctx=512, n_slots=4,
                            max_rank=64, max_tokens=1024)
         m.use_tc_sgmv = tc
+        m.prefill_small_lora = small_lora
         m.load_backbone(w)
         for a, (ad, lo) in enumerate(zip(ads, loras)):
             m.pool.load(a, ad, lo)
