@@ -115,7 +115,7 @@ SLX_API int slx_gemm_bf16_ex(const void* A, int lda, const void* W, void* C, int
                   const void* R, int ldr, int M, int N, int K, int epilogue, int w_layout,
                   int n_main, void* C2, int ldc2, void* ws, size_t ws_bytes,
                   const slx_l2_prefetch* pf, const slx_gemm_tuning* tuning, void* stream);
-/* Decode split-K handed to the consumer: W tiled, M <= 64; the N columns are cut in 256-wide
+/* Decode split-K handed to the consumer: W tiled, M <= 128; the N columns are cut in 256-wide
  * tiles and the K range of each tile in `splits` equal pieces, one CTA per piece; every piece
  * is written in fp32 to `part` with no reduction and no epilogue, so the kernel has no tail.
  * Layout (the consumer's contract, e.g. slx_rmsnorm_fused): with bm = M rounded up to 16,

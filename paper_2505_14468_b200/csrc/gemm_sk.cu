@@ -1,4 +1,4 @@
-// K1, decode path: stream-K tcgen05 GEMM for skinny activations (M <= 64 token rows).
+// K1, decode path: stream-K tcgen05 GEMM for skinny activations (M <= 128 token rows).
 //
 //   C[M,N] = A[M,K] . W[N,K]^T (+ residual | SiLU*mul | fp32 side output), W in SLX_W_TILED.
 //
@@ -39,7 +39,7 @@ constexpr int SK_BN = 256;
 constexpr int SK_BK = 64;
 constexpr int SK_MAX_STAGES = 8;
 constexpr int SK_MAX_SEGS = 8;
-constexpr int SK_MAX_M = 64;
+constexpr int SK_MAX_M = 128;
 constexpr int SK_PB = 8;                        // pieces loaded per batch in the reduction
 constexpr int SK_WBOX = 128 * SK_BK * 2;        // one contiguous 16 KB weight box
 constexpr size_t SK_CNT_BYTES = 32 * 1024;      // counters at the head of ws: 2 u32 per tile
@@ -225,8 +225,9 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
       // D[128 tok x 256 w] (+)= X[128 x 16] . W[256 x 16]^T; X rows >= bm read stale smem and
       // only feed D rows that are never read.
       // M = 64 (bm <= 64 token rows): the accumulator's row r lands in lane r % 16 of TMEM lane
-      // quadrant r / 16 (tools/probe/m64_layout.cu), so all four epilogue warps drain it
-      const uint32_t idesc = tc::idesc_bf16_f32(64, SK_BN);
+      // quadrant r / 16 (tools/probe/m64_layout.cu), so all four epilogue warps drain it;
+      // M = 128 (65..128 rows): row r is lane r
+      const uint32_t idesc = g.bm > 64 ? tc::idesc_bf16_f32(128, SK_BN) : tc::idesc_bf16_f32(64, SK_BN);
       int j = -1;
       uint32_t d = 0;
       bool first = true;
@@ -261,9 +262,10 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
     // This CTA holds piece `rank` of tile c / cs (exactly one segment).  Pieces are staged in
     // each CTA's own (now idle) pipeline smem as [chunk][row][16] fp32 and reduced through
     // DSMEM: CTA `rank` sums a 1/cs slice of the tile over the cs peers in rank order.
-    const int q = warp & 3, r = q * 16 + (lane & 15), et = threadIdx.x - 64;
-    const bool qlive = q * 16 < g.bm;   // warp-uniform
-    const bool rv = lane < 16;          // lanes 16-31 of the quadrant hold no row (M = 64)
+    const bool m128 = g.bm > 64;
+    const int q = warp & 3, r = m128 ? q * 32 + lane : q * 16 + (lane & 15), et = threadIdx.x - 64;
+    const bool qlive = (m128 ? q * 32 : q * 16) < g.bm;   // warp-uniform
+    const bool rv = m128 || lane < 16;   // M = 64: lanes 16-31 of the quadrant hold no row
     const bool silu = EPI == SLX_EPI_SILU_MUL;
     const int cs = g.cs, rank = c % cs, tile = c / cs;
     const int n_out = silu ? g.N / 2 : g.N;
@@ -351,10 +353,11 @@ gemm_sk_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant
   } else {
     // -------------------------------------------------------------- epilogue (warps 2-5)
     const int q = warp & 3;              // TMEM lane quadrant this warp may access
-    const int r = q * 16 + (lane & 15);  // token row of this thread (M = 64 layout)
-    const bool rv = lane < 16;           // lanes 16-31 of the quadrant hold no row
+    const bool m128 = g.bm > 64;         // M = 128 MMA: row r is TMEM lane r
+    const int r = m128 ? q * 32 + lane : q * 16 + (lane & 15);   // token row of this thread
+    const bool rv = m128 || lane < 16;   // M = 64: lanes 16-31 of the quadrant hold no row
     const int et = threadIdx.x - 64;     // 0..127
-    const bool qlive = q * 16 < g.bm;    // warp-uniform
+    const bool qlive = (m128 ? q * 32 : q * 16) < g.bm;   // warp-uniform
     const bool silu = EPI == SLX_EPI_SILU_MUL;
     const int piece_floats = g.bm * SK_BN;
     const int n_out = silu ? g.N / 2 : g.N;

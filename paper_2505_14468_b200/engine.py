@@ -115,7 +115,7 @@ class DecodeBuckets:
     of a bucket decode a reserved padding sequence slot at position 0 without an adapter;
     their KV append only ever touches that slot."""
 
-    def __init__(self, model: MultiLoraModel, pad_seq: int, buckets=(1, 2, 4, 8, 16, 32, 64)):
+    def __init__(self, model: MultiLoraModel, pad_seq: int, buckets=(1, 2, 4, 8, 16, 32, 64, 96, 128)):
         self.m = model
         self.pad_seq = pad_seq
         self.buckets = tuple(sorted(b for b in buckets if b <= model.max_tokens))

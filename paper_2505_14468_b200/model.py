@@ -622,7 +622,7 @@ class MultiLoraModel:
         """The bf16 decode step of fused kernels (split-K consumers, fused LoRA expands)."""
         d = self.cfg.hidden
         return (self.dtype == torch.bfloat16 and self.splitk_consumer and self.fuse_expand
-                and T <= 64 and d % 256 == 0 and d <= 5120
+                and T <= 128 and d % 256 == 0 and d <= 5120
                 and set(self.targets) <= {"q", "k", "v", "o"}
                 and (not self.targets or (self.decode_lora == "gather") or
                      (self.use_stacked_decode and self.pool.max_rank <= 16)))

@@ -46,7 +46,7 @@ class ServingRuntime:
     def __init__(self, model: MultiLoraModel, functions: dict, gpu_id: str = "gpu0",
                  tick_ms: float = 10.0, *, store=None, adapters: dict | None = None,
                  preloader=None, offloader=None, graphs: bool | None = None,
-                 buckets=(1, 2, 4, 8, 16, 32, 64)):
+                 buckets=(1, 2, 4, 8, 16, 32, 64, 96, 128)):
         """``functions``: function_id -> (FunctionSpec-like, adapter slot or -1).
         ``adapters``: function_id -> (artifact name in ``store``, LoraConfig) for functions whose
         adapter lives in the pinned container tier and is loaded at dispatch (needs

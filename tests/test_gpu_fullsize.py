@@ -37,31 +37,34 @@ def _check(got, ref, layers: int = 1):
     assert rel <= REL_FRO * k and mx <= MAX_ABS * k and flips == 0, (rel, mx, flips)
 
 
-def _tok_slots(seed=0):
-    return np.random.default_rng(seed).integers(0, N_ADAPTERS, size=BATCH).astype(np.int64).tolist()
+def _tok_slots(seed=0, batch=BATCH):
+    return np.random.default_rng(seed).integers(0, N_ADAPTERS, size=batch).astype(np.int64).tolist()
 
 
-def test_config2_widths_one_layer_decode_matches_oracle():
+@pytest.mark.parametrize("batch", [BATCH, 128])
+def test_config2_widths_one_layer_decode_matches_oracle(batch):
+    """Batch 64 (the bench's) and 128 (the decode path's M = 128 stream-K GEMMs)."""
     cfg = BackboneConfig("7b-1layer", hidden=4096, layers=1, heads=32, kv_heads=32, head_dim=128,
                          ffn=11008, vocab=32000)
     lora = LoraConfig(RANK, 32.0, ("q", "k", "v", "o"))
     w = init_backbone(cfg, 21)
     ads = [init_adapter(cfg, lora, 21, a) for a in range(N_ADAPTERS)]
-    m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=BATCH, max_ctx=32, n_slots=N_ADAPTERS,
-                       max_rank=RANK, max_tokens=BATCH * 16)
+    m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=batch, max_ctx=32, n_slots=N_ADAPTERS,
+                       max_rank=RANK, max_tokens=batch * 16)
     m.load_backbone(w)
     for a, ad in enumerate(ads):
         m.pool.load(a, ad, lora)
     rng = np.random.default_rng(3)
-    prompts = [list(map(int, rng.integers(1, cfg.vocab, size=16))) for _ in range(BATCH)]
-    ids = _tok_slots()
+    prompts = [list(map(int, rng.integers(1, cfg.vocab, size=16))) for _ in range(batch)]
+    ids = _tok_slots(batch=batch)
     ids[5] = ids[17] = -1   # tokens without an adapter ride along
     seqs, pre = m.prefill(prompts, ids)
-    toks = list(map(int, rng.integers(1, cfg.vocab, size=BATCH)))
+    toks = list(map(int, rng.integers(1, cfg.vocab, size=batch)))
+    assert m._decode_fast(batch)
     got = m.decode(seqs, toks, ids).float().cpu().numpy()
     orc = OracleModel(cfg, w, ads, [lora.scale] * N_ADAPTERS, lora.targets)
     ref_pre = orc.prefill(prompts, ids)
-    ref = orc.decode(list(range(BATCH)), toks, ids)
+    ref = orc.decode(list(range(batch)), toks, ids)
     _check(pre.float().cpu().numpy(), ref_pre)
     _check(got, ref)
 

@@ -65,12 +65,12 @@ def test_gemm_decode_tilings(M, bn, gsplit, ctas, splits):
     torch.testing.assert_close(o3, (g_ * torch.sigmoid(g_) * u_).reshape(M, N // 2), rtol=1e-3, atol=1e-3)
 
 
-@pytest.mark.parametrize("M", [1, 17, 64])
+@pytest.mark.parametrize("M", [1, 17, 64, 65, 100, 128])
 @pytest.mark.parametrize("N,K", [(3072, 4096), (4608, 4096), (1000, 11008), (32000, 1024)])
 @pytest.mark.parametrize("ctas,min_units,cluster", [(0, 4, 1), (0, 4, 0), (37, 4, 1), (5, 4, 1),
                                                      (1, 1, 1), (0, 1, 1)])
 def test_gemm_stream_k(M, N, K, ctas, min_units, cluster):
-    """Stream-K decode GEMM (M <= 64): every range split (whole tiles, tail/head pieces, up to
+    """Stream-K decode GEMM (M <= 128; M = 64 / M = 128 MMAs): every range split (whole tiles, tail/head pieces, up to
     dozens of pieces per tile; uniform splits reduced in DSMEM clusters or through global
     memory) gives the fp32 result; epilogues residual / SiLU / side output."""
     tu = {"sk_no_cluster": 0 if cluster else 1, "sk_ctas": ctas, "sk_min_units": min_units}
@@ -481,7 +481,8 @@ def test_rmsnorm_lora_cluster(d, rank):
     torch.testing.assert_close(res["1"][1].float(), hr, rtol=2e-2, atol=2e-2)
 
 
-@pytest.mark.parametrize("M,N,K,splits", [(64, 4608, 4096, 8), (17, 4096, 11008, 8), (1, 512, 256, 3)])
+@pytest.mark.parametrize("M,N,K,splits", [(64, 4608, 4096, 8), (17, 4096, 11008, 8), (1, 512, 256, 3),
+                                           (128, 4096, 11008, 8), (100, 4608, 4096, 6)])
 def test_gemm_splitk_pieces_and_consumer(M, N, K, splits):
     """Split-K pieces (slx_gemm_bf16_splitk) sum to the fp32 product in the documented layout;
     the fused RMSNorm consumer reproduces residual add + norm."""

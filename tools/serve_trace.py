@@ -6,7 +6,7 @@ of idle adapters by the offloader when the adapter pool is full), merged mixed-a
 prefill, CUDA-graph decode buckets.  Reports the reference's metrics (nearest-rank TTFT /
 TPOT / E2E percentiles, output tokens/s, metrics.py:17-25,114-147) and writes the request CSV
 in the reference's format.
-python tools/serve_trace.py TRACE.csv OUT_PREFIX [resident_slots] [time_scale]"""
+python tools/serve_trace.py TRACE.csv OUT_PREFIX [resident_slots] [time_scale] [max_sequences]"""
 import json
 import os
 import sys
@@ -27,7 +27,8 @@ from paper_2505_14468_b200.spec import ArtifactKind, ArtifactSpec, FunctionSpec 
 trace_path, out_prefix = sys.argv[1], sys.argv[2]
 n_slots = int(sys.argv[3]) if len(sys.argv) > 3 else 24
 time_scale = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
-MAX_CTX, MAX_SEQS, RANK = 512, 64, 16
+MAX_SEQS = int(sys.argv[5]) if len(sys.argv) > 5 else 128   # concurrent sequences (decode batch)
+MAX_CTX, RANK = 512, 16
 torch.cuda.set_device(0)
 recs = wire.read_trace_csv(trace_path)
 fids = sorted({r.function_id for r in recs})
@@ -75,6 +76,7 @@ wall = time.perf_counter() - t_start
 rep = rt.report()
 rep.update({"trace": os.path.basename(trace_path), "requests_in_trace": len(recs),
             "functions": len(fids), "resident_adapter_slots": n_slots, "time_scale": time_scale,
+            "max_concurrent_sequences": MAX_SEQS,
             "wall_s": round(wall, 2), "cold_loads": sum(1 for v in rt.cold_ms.values() if v),
             "demotions_in_container_tier": len(off.demoted),
             "model": "llama2-7b shape bf16, random init; r16 adapters on q,k,v,o",
