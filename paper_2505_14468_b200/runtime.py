@@ -246,6 +246,7 @@ class ServingRuntime:
         c1 = time.perf_counter()
         self.phase_s["schedule"] += c1 - c0
         if flushed:
+            torch.cuda.nvtx.range_push(f"slx.prefill[{len(flushed)} req]")   # nsys / ncu ranges
             seqs = []
             try:
                 for r in flushed:
@@ -263,6 +264,7 @@ class ServingRuntime:
                     self.m.free_seq(s)
                 for r in flushed:
                     r.seq = -1
+                torch.cuda.nvtx.range_pop()
                 raise
             for r in batch.requests:
                 self.m.seq_len[r.seq] += len(r.prompt)
@@ -272,6 +274,7 @@ class ServingRuntime:
                 r.generated.append(int(tok))
                 r.first_token_ms = t
             self.active += batch.requests
+            torch.cuda.nvtx.range_pop()
         c2 = time.perf_counter()
         self.phase_s["prefill"] += c2 - c1
         self._retire()
@@ -280,6 +283,7 @@ class ServingRuntime:
             batch = build_decode(self.active, self.m.seq_len)
             if int(batch.pos.max()) >= self.m.max_ctx:
                 raise RuntimeError("a sequence reached max_ctx (submit() admits only fitting requests)")
+            torch.cuda.nvtx.range_push(f"slx.decode[{len(self.active)} seq]")
             nxt = None
             if self.graphs is not None:
                 nxt = self.graphs.step(batch.tokens, batch.pos, batch.seq, batch.slot)
@@ -289,6 +293,7 @@ class ServingRuntime:
                                         self._i32(batch.seq), self._i32(batch.slot), decode=True)
                 nxt = self.m.argmax(logits).cpu().numpy()
             self.decode_steps += 1
+            torch.cuda.nvtx.range_pop()
             c4 = time.perf_counter()
             self.phase_s["decode"] += c4 - c3
             for r in batch.requests:
