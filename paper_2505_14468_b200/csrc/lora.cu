@@ -462,147 +462,364 @@ lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, 
 // ---------------------------------------------------------------- gathered decode shrink
 // Large adapter pools (decode): instead of stacking every slot's A rows into the projection
 // GEMM (bytes grow with the pool), the shrink reads only the adapters present in the batch,
-// each ONCE per plan tile.  The work is a list of A rows (tile, target, j < rank): one WARP per
-// row streams the row (16 B per lane per step, five steps in flight) against the tile's
-// <= LORA_TT token rows of x (L2) and reduces with a warp_sum (fixed order: deterministic).
-// No clusters and no shared memory (grid = tiles x targets x rank / 8 warps).
+// each ONCE per plan tile.
+// Work unit = (plan tile, target, 8 rows j0..j0+7 of A): a slot's rows are contiguous
+// ([rank][d_in]), so a unit is ONE bulk copy (TMA engine, 80 KB at d_in 5120).  Persistent
+// grid (one CTA per SM), units dealt round robin over a dense table (block scan of the
+// (tile, target) unit counts, tile data cached in shared memory: no dead CTAs, no dependent
+// global loads per unit).  Two shared-memory stages, each holding a unit's A rows and the
+// first SH_XT of its tile's token rows of x, both brought by bulk copies on the stage's
+// mbarriers: the adapter pool is static, so thread 0 issues the A rows of the CTA's first two
+// units BEFORE griddepcontrol.wait (they stream while the producer of x -- the norm /
+// attention -- is still running) and their x rows right after it; a consumed stage is refilled
+// (A and x) at once, so unit k+2's bytes are in flight while unit k+1 is computed.  Tiles with
+// more than SH_XT tokens stage the rest synchronously.  Each warp dots one A row against the
+// staged x rows (16 B per lane per step, conflict-free); per lane the k order
+// (lane*8 + 256*c, e inner) is sequential fmaf, then a warp_sum: deterministic and
+// independent of the token grouping.
 //   v[t, v_col_off[tgt] + j] = x_t . A_{slot(t), tgt}[j]   (j < rank; unscaled)
 // Consumers: slx_lora_expand with v_slot_stride = 0, or the fused slx_lora_delta.
 constexpr int SH_WARPS = 8;
+constexpr int SH_XT = 2;        // token rows of x per stage (at most)
+constexpr int SH_STAGES = 2;
+constexpr int SH_MAX_PAIRS = 1024;
+constexpr int SH_PAIRS_PT = SH_MAX_PAIRS / (SH_WARPS * 32);
+constexpr int SH_MAX_TILES = 384;
+constexpr size_t SH_DYN_SMEM = 204 * 1024;   // dynamic shared memory (static ~21 KB on top)
 struct ShrinkOut {
   int v_off[SLX_LORA_MAX_TARGETS];
+  int n_targets;
 };
+inline size_t shrink_smem_bytes(int d_in, size_t x_elem, int xt) {
+  return 64 + (size_t)SH_STAGES * ((size_t)SH_WARPS * d_in * 2 + (size_t)xt * d_in * x_elem);
+}
+// token rows of x per stage that fit next to the A rows (0: d_in too large)
+inline int shrink_xt(int d_in, size_t x_elem) {
+  for (int xt = SH_XT; xt >= 1; --xt)
+    if (shrink_smem_bytes(d_in, x_elem, xt) <= SH_DYN_SMEM) return xt;
+  return 0;
+}
 
 template <typename T>
-__global__ void __launch_bounds__(SH_WARPS * 32, 4)
+__global__ void __launch_bounds__(SH_WARPS * 32, 1)
 lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, int ldx, int d_in,
                      const int32_t* __restrict__ slot_rank, int max_rank, TargetArgs ta,
-                     ShrinkOut so, LoraWs ws) {
+                     ShrinkOut so, LoraWs ws, int xt) {
+  constexpr int NT = SH_WARPS * 32;
+  extern __shared__ __align__(128) unsigned char sh_raw[];
+  uint64_t* afull = reinterpret_cast<uint64_t*>(sh_raw);        // [SH_STAGES]
+  uint64_t* xfull = afull + SH_STAGES;                            // [SH_STAGES]
+  const size_t a_stage = (size_t)SH_WARPS * d_in;                 // bf16 elements
+  const size_t x_stage = (size_t)xt * d_in;                       // T elements
+  bf16* As = reinterpret_cast<bf16*>(sh_raw + 64);                // [SH_STAGES][8][d_in]
+  T* Xs = reinterpret_cast<T*>(sh_raw + 64 + SH_STAGES * a_stage * 2);   // [SH_STAGES][xt][d_in]
+  using Scan = cub::BlockScan<int, NT>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int pair_end[SH_MAX_PAIRS];
+  __shared__ int tile_rank[SH_MAX_TILES];
+  __shared__ int tile_slot[SH_MAX_TILES];
+  __shared__ int tile_tok[SH_MAX_TILES][LORA_TT];
+  __shared__ int tile_count[SH_MAX_TILES];
+  __shared__ int total_units;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile_id = blockIdx.x, tgt = blockIdx.y;
-  const int j = blockIdx.z * SH_WARPS + warp;
-  // plan (start of the step) and adapter pool (static): >= 2 launches back, read before the wait
-  const bool live = tile_id < *ws.n_tiles;
-  LoraTile tile{0, 0, 0, 0};
-  int rank = 0;
-  const bf16* A = nullptr;
-  if (live) {
-    tile = ws.tiles[tile_id];
-    rank = min(slot_rank[tile.slot], max_rank);
-    A = reinterpret_cast<const bf16*>(ta.a_ptrs[tgt][tile.slot]);
-  }
-  const bool mine = A != nullptr && j < rank;   // warp-uniform
-  int tok[LORA_TT];
+  const int NTG = so.n_targets;
+  // ---- the unit table (plan and adapter pool are >= 2 launches back: before the wait)
+  const int n_tiles = min(min(*ws.n_tiles, ws.max_tiles), SH_MAX_TILES);
+  const int n_pairs = min(n_tiles * NTG, SH_MAX_PAIRS);
+  for (int tl = threadIdx.x; tl < n_tiles; tl += NT) {
+    const LoraTile tile = ws.tiles[tl];
+    tile_rank[tl] = tile.count > 0 ? min(slot_rank[tile.slot], max_rank) : 0;
+    tile_slot[tl] = tile.slot;
+    tile_count[tl] = min(tile.count, LORA_TT);
 #pragma unroll
-  for (int i = 0; i < LORA_TT; ++i) tok[i] = (mine && i < tile.count) ? ws.perm[tile.start + i] : -1;
+    for (int i = 0; i < LORA_TT; ++i) tile_tok[tl][i] = i < tile.count ? ws.perm[tile.start + i] : 0;
+  }
+  __syncthreads();
+  int cnt[SH_PAIRS_PT];
+  int run = 0;
+#pragma unroll
+  for (int k = 0; k < SH_PAIRS_PT; ++k) {
+    const int p = threadIdx.x * SH_PAIRS_PT + k;
+    int c = 0;
+    if (p < n_pairs) {
+      const int tl = p / NTG, tg = p - tl * NTG;
+      const int r = tile_rank[tl];
+      if (r > 0 && ta.a_ptrs[tg][tile_slot[tl]] != 0) c = ceil_div(r, SH_WARPS);
+    }
+    run += c;
+    cnt[k] = run;
+  }
+  int excl, tot;
+  Scan(scan_tmp).ExclusiveSum(run, excl, tot);
+#pragma unroll
+  for (int k = 0; k < SH_PAIRS_PT; ++k) pair_end[threadIdx.x * SH_PAIRS_PT + k] = excl + cnt[k];
+  if (threadIdx.x == 0) total_units = tot;
+  __syncthreads();
+  const int U = total_units;
+  auto locate = [&](int u, int& pair, int& j0) {   // unit u -> (pair, first row)
+    int lo = 0, hi = n_pairs - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (pair_end[mid] > u) hi = mid; else lo = mid + 1;
+    }
+    pair = lo;
+    j0 = (u - (lo ? pair_end[lo - 1] : 0)) * SH_WARPS;
+  };
+  auto issue_a = [&](int u, int stage) {   // thread 0: the unit's A rows -> stage
+    int pair, j0;
+    locate(u, pair, j0);
+    const int tl = pair / NTG, tg = pair - tl * NTG;
+    const bf16* A = reinterpret_cast<const bf16*>(ta.a_ptrs[tg][tile_slot[tl]]);
+    const uint32_t bytes = (uint32_t)min(SH_WARPS, tile_rank[tl] - j0) * d_in * 2;
+    tc::mbar_arrive_expect_tx(&afull[stage], bytes);
+    tc::bulk_g2s(As + stage * a_stage, A + (size_t)j0 * d_in, bytes, &afull[stage],
+                 tc::policy_evict_first());
+  };
+  auto issue_x = [&](int u, int stage) {   // thread 0: the tile's first xt token rows -> stage
+    int pair, j0;
+    locate(u, pair, j0);
+    const int tl = pair / NTG;
+    const int nt = min(xt, tile_count[tl]);
+    const uint32_t row = (uint32_t)d_in * sizeof(T);
+    tc::mbar_arrive_expect_tx(&xfull[stage], row * nt);
+    for (int i = 0; i < nt; ++i)
+      tc::bulk_g2s(Xs + stage * x_stage + (size_t)i * d_in, x + (size_t)tile_tok[tl][i] * ldx, row,
+                   &xfull[stage], tc::policy_evict_normal());
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < SH_STAGES; ++st) {
+      tc::mbar_init(&afull[st], 1);
+      tc::mbar_init(&xfull[st], 1);
+    }
+    tc::fence_barrier_init();
+    for (int k = 0; k < SH_STAGES; ++k)
+      if (blockIdx.x + k * gridDim.x < U) issue_a(blockIdx.x + k * gridDim.x, k);
+  }
   pdl_wait();   // x comes from the kernel just before us
   pdl_trigger();
-  if (!mine) return;
-  const bf16* ar = A + (size_t)j * d_in;
-  float acc[LORA_TT];
+  if (threadIdx.x == 0)
+    for (int k = 0; k < SH_STAGES; ++k)
+      if (blockIdx.x + k * gridDim.x < U) issue_x(blockIdx.x + k * gridDim.x, k);
+  constexpr int EPC = 16 / sizeof(T);   // elements per 16-byte copy chunk of x
+  const int per = d_in / EPC, nch = d_in >> 3;
+  int k = 0;
+  for (int u = blockIdx.x; u < U; u += gridDim.x, ++k) {
+    const int stage = k % SH_STAGES;
+    const uint32_t parity = (uint32_t)((k / SH_STAGES) & 1);
+    int pair, j0;
+    locate(u, pair, j0);
+    const int tl = pair / NTG, tg = pair - tl * NTG;
+    const int nrows = min(SH_WARPS, tile_rank[tl] - j0), count = tile_count[tl];
+    const bool mine = warp < nrows;   // warp-uniform
+    const bf16* ar = As + stage * a_stage + (size_t)warp * d_in;
+    T* xs = Xs + stage * x_stage;
+    tc::mbar_wait(&xfull[stage], parity);
+    tc::mbar_wait(&afull[stage], parity);
+    for (int i0 = 0; i0 < count; i0 += xt) {
+      const int nt = min(xt, count - i0);
+      if (i0) {   // tokens beyond the first xt: staged synchronously in the stage's x buffer
+        __syncthreads();
+        for (int e = threadIdx.x; e < nt * per; e += NT) {
+          const int i = e / per, c = e - i * per;
+          reinterpret_cast<uint4*>(xs + (size_t)i * d_in)[c] =
+              reinterpret_cast<const uint4*>(x + (size_t)tile_tok[tl][i0 + i] * ldx)[c];
+        }
+        __syncthreads();
+      }
+      if (!mine) continue;
+      for (int i = 0; i < nt; ++i) {
+        const T* xr = xs + (size_t)i * d_in;
+        float acc = 0.f;
+#pragma unroll 4
+        for (int ch = lane; ch < nch; ch += 32) {
+          float af[8], xf[8];
+          Vec8<bf16>::load(ar + ch * 8, af);
+          Vec8<T>::load(xr + ch * 8, xf);
 #pragma unroll
-  for (int i = 0; i < LORA_TT; ++i) acc[i] = 0.f;
-  // unrolled so several 16-byte steps of the row (and of the tokens' x) are in flight at once
-#pragma unroll 5
-  for (int k = lane * 8; k < d_in; k += 32 * 8) {
-    float af[8];
-    Vec8<bf16>::load(ar + k, af);
-#pragma unroll
-    for (int i = 0; i < LORA_TT; ++i) {
-      if (tok[i] < 0) continue;
-      float xf[8];
-      Vec8<T>::load(x + (size_t)tok[i] * ldx + k, xf);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[i] = fmaf(xf[e], af[e], acc[i]);
+          for (int e = 0; e < 8; ++e) acc = fmaf(xf[e], af[e], acc);
+        }
+        const float sum = warp_sum(acc);
+        if (lane == 0) v[(size_t)tile_tok[tl][i0 + i] * ldv + so.v_off[tg] + j0 + warp] = sum;
+      }
     }
-  }
-#pragma unroll
-  for (int i = 0; i < LORA_TT; ++i) {
-    if (tok[i] < 0) continue;   // warp-uniform
-    const float sum = warp_sum(acc[i]);
-    if (lane == 0) v[(size_t)tok[i] * ldv + so.v_off[tgt] + j] = sum;
+    __syncthreads();   // every warp is done with this stage
+    const int un = u + SH_STAGES * gridDim.x;
+    if (threadIdx.x == 0 && un < U) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+      issue_a(un, stage);
+      issue_x(un, stage);
+    }
   }
 }
 
 // ---------------------------------------------------------------- decode expand
 // y[t, col(n)] += scale * sum_j v[t, off + slot * v_slot_stride + j] * B_slot[n, j] over the
 // plan: v from the stacked shrink inside the projection GEMM (stride max_rank) or the gathered
-// shrink (stride 0).  CTA (tile, target, 256-column chunk): the tile's scaled v in shared memory,
-// one THREAD per output column n with its B row (rank <= 64 bf16: up to eight 16-byte loads, all
-// in flight) in registers, then a read-modify-write of y for each of the tile's tokens
-// (coalesced over n).  Sequential fmaf in j with v pre-scaled and one rounding of y:
-// bit-identical to the fused slx_lora_delta.
+// shrink (stride 0).
+// Work unit = (plan tile, target, column block) holding 32 KB of B: a thread owns
+// cpt = 8 / (rank / 8) output columns 256 apart (rank 8: eight, rank 64: one) and their B rows
+// (eight 16-byte registers whatever the rank), so every unit is the same size and a mixed-rank
+// batch balances.  Persistent grid (2 CTAs per SM), units dealt round robin; a CTA locates its
+// units by a block scan of the (tile, target) unit counts.  B is static: the first unit's rows
+// are fetched before griddepcontrol.wait, and while a unit is being applied the NEXT unit's
+// rows are already in flight (register double buffer), so the HBM stream never waits on the
+// v / y round trips.  Per unit: the tile's scaled v in shared memory, then for each token the
+// y reads of the thread's columns together, the sequential fmaf chains over j (v pre-scaled,
+// one rounding of y: bit-identical to the fused slx_lora_delta) and the stores.
 constexpr int EX_THREADS = 256;
+constexpr int EX_REGS = LORA_MAX_RANK / 8;   // 16-byte B chunks per thread and unit
+constexpr int EX_MAX_PAIRS = 2048;           // (plan tile, target) pairs per launch
+constexpr int EX_PAIRS_PT = EX_MAX_PAIRS / EX_THREADS;
+constexpr int EX_MAX_TILES = 384;           // plan tiles per launch (1024 tokens over <= 254 slots)
 
 struct ExpandArgs {
   int v_off[SLX_LORA_MAX_TARGETS];
   int v_slot_stride;   // columns between slots' v blocks: max_rank (stacked) or 0 (gathered)
+  int n_targets;
+};
+
+struct ExUnit {
+  int tile, tgt, n0, r8;   // r8 = rank / 8 (0: no unit)
 };
 
 template <typename T>
-__global__ void __launch_bounds__(EX_THREADS)
+__global__ void __launch_bounds__(EX_THREADS, 2)
 lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, int ldv,
                      const int32_t* __restrict__ slot_rank, const float* __restrict__ slot_scale,
                      int max_rank, TargetArgs ta, ExpandArgs ea, LoraWs ws) {
+  using Scan = cub::BlockScan<int, EX_THREADS>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int pair_end[EX_MAX_PAIRS];   // inclusive prefix of the units per pair
   __shared__ float vs[LORA_TT][LORA_MAX_RANK];
-  __shared__ int toks[LORA_TT];
-  // The plan and the adapter pool are >= 2 launches back: read them and fetch the B rows
-  // before waiting on the kernel that produced v / y.
-  const int tile_id = blockIdx.x, tgt = blockIdx.y;
-  const bool live = tile_id < *ws.n_tiles;
-  const int d_out = ta.d_out[tgt];
-  const int n = blockIdx.z * EX_THREADS + threadIdx.x;
-  LoraTile tile{0, 0, 0, 0};
-  int rank = 0;
-  float scale = 0.f;
-  const bf16* B = nullptr;
-  if (live) {
-    tile = ws.tiles[tile_id];
-    rank = min(slot_rank[tile.slot], max_rank);
-    scale = slot_scale[tile.slot];
-    B = reinterpret_cast<const bf16*>(ta.b_ptrs[tgt][tile.slot]);
-  }
-  if (B == nullptr || rank == 0 || blockIdx.z * EX_THREADS >= d_out) {   // CTA-uniform
-    pdl_wait();
-    pdl_trigger();
-    return;
-  }
-  uint4 br[LORA_MAX_RANK / 8];
-  const int R8 = (rank + 7) >> 3;   // pool invariant: rank % 8 == 0
-  if (n < d_out) {
-    const uint4* src = reinterpret_cast<const uint4*>(B + (size_t)n * rank);
+  __shared__ int total_units;
+  // per plan tile, cached so a unit is located and fetched with no dependent global loads:
+  __shared__ const bf16* tile_b[EX_MAX_PAIRS];   // per pair: the slot's B of the target
+  __shared__ int tile_r8[EX_MAX_TILES];
+  __shared__ int tile_slot[EX_MAX_TILES];
+  __shared__ int tile_tok[EX_MAX_TILES][LORA_TT];
+  __shared__ int tile_count[EX_MAX_TILES];
+  // ---- the unit table (plan and adapter pool are >= 2 launches back: before the wait)
+  const int n_tiles = min(min(*ws.n_tiles, ws.max_tiles), EX_MAX_TILES);
+  const int n_pairs = min(n_tiles * ea.n_targets, EX_MAX_PAIRS);
+  for (int tl = threadIdx.x; tl < n_tiles; tl += EX_THREADS) {
+    const LoraTile tile = ws.tiles[tl];
+    const int r = tile.count > 0 ? min(slot_rank[tile.slot], max_rank) : 0;
+    tile_r8[tl] = (r + 7) >> 3;
+    tile_slot[tl] = tile.slot;
+    tile_count[tl] = min(tile.count, LORA_TT);
 #pragma unroll
-    for (int q = 0; q < LORA_MAX_RANK / 8; ++q) br[q] = q < R8 ? __ldg(src + q) : make_uint4(0, 0, 0, 0);
-  }
-  if (threadIdx.x < LORA_TT) toks[threadIdx.x] = threadIdx.x < tile.count ? ws.perm[tile.start + threadIdx.x] : 0;
-  pdl_wait();       // v and y come from the kernels just before us
-  pdl_trigger();
-  __syncthreads();  // toks
-  const int voff = ea.v_off[tgt] + tile.slot * ea.v_slot_stride;
-  for (int e = threadIdx.x; e < tile.count * LORA_MAX_RANK; e += EX_THREADS) {
-    const int i = e / LORA_MAX_RANK, jj = e % LORA_MAX_RANK;
-    vs[i][jj] = jj < rank ? v[(size_t)toks[i] * ldv + voff + jj] * scale : 0.f;
+    for (int i = 0; i < LORA_TT; ++i) tile_tok[tl][i] = i < tile.count ? ws.perm[tile.start + i] : 0;
   }
   __syncthreads();
-  if (n >= d_out) return;
-  const int cb = ta.col_blk[tgt], cstr = ta.col_stride[tgt], co = ta.col_off[tgt];
-  const int col = co + (n / cb) * cstr + (n % cb);
-  for (int i = 0; i < tile.count; ++i) {
-    float d = 0.f;
+  int cnt[EX_PAIRS_PT];
+  int run = 0;
 #pragma unroll
-    for (int q = 0; q < LORA_MAX_RANK / 8; ++q) {
-      if (q < R8) {
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&br[q]);
+  for (int k = 0; k < EX_PAIRS_PT; ++k) {
+    const int p = threadIdx.x * EX_PAIRS_PT + k;
+    int c = 0;
+    if (p < n_pairs) {
+      const int tl = p / ea.n_targets, tg = p - tl * ea.n_targets;
+      const int r8 = tile_r8[tl];
+      const bf16* B = r8 ? reinterpret_cast<const bf16*>(ta.b_ptrs[tg][tile_slot[tl]]) : nullptr;
+      tile_b[p] = B;
+      if (B != nullptr) c = ceil_div(ta.d_out[tg], EX_THREADS * (EX_REGS / r8));
+    }
+    run += c;
+    cnt[k] = run;
+  }
+  int excl, tot;
+  Scan(scan_tmp).ExclusiveSum(run, excl, tot);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float2 f = __bfloat1622float2(h2[u]);
-          d = fmaf(vs[i][8 * q + 2 * u], f.x, d);
-          d = fmaf(vs[i][8 * q + 2 * u + 1], f.y, d);
+  for (int k = 0; k < EX_PAIRS_PT; ++k) pair_end[threadIdx.x * EX_PAIRS_PT + k] = excl + cnt[k];
+  if (threadIdx.x == 0) total_units = tot;
+  __syncthreads();
+  const int U = total_units;
+  auto locate = [&](int u) -> ExUnit {
+    ExUnit e{0, 0, 0, 0};
+    if (u >= U) return e;
+    int lo = 0, hi = n_pairs - 1;   // first pair with pair_end > u
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (pair_end[mid] > u) hi = mid; else lo = mid + 1;
+    }
+    const int first = lo ? pair_end[lo - 1] : 0;
+    e.tile = lo / ea.n_targets;
+    e.tgt = lo - e.tile * ea.n_targets;
+    e.r8 = tile_r8[e.tile];
+    e.n0 = (u - first) * EX_THREADS * (EX_REGS / e.r8);
+    return e;
+  };
+  // B rows of unit e into registers: chunk q belongs to column c = q / r8, 16-byte piece q % r8
+  auto fetch = [&](const ExUnit& e, uint4* br) {
+    const bf16* B = tile_b[e.tile * ea.n_targets + e.tgt];
+    const int d_out = ta.d_out[e.tgt], rank = e.r8 * 8, cpt = e.r8 ? EX_REGS / e.r8 : 0;
+#pragma unroll
+    for (int q = 0; q < EX_REGS; ++q) {
+      const int c = e.r8 ? q / e.r8 : 0, qq = q - c * e.r8;
+      const int n = e.n0 + c * EX_THREADS + threadIdx.x;
+      br[q] = (c < cpt && n < d_out)
+                  ? __ldg(reinterpret_cast<const uint4*>(B + (size_t)n * rank) + qq)
+                  : make_uint4(0, 0, 0, 0);
+    }
+  };
+  uint4 bn[EX_REGS], bc[EX_REGS];
+  int u = blockIdx.x;
+  ExUnit nxt = locate(u);
+  if (nxt.r8) fetch(nxt, bn);
+  pdl_wait();       // v and y come from the kernels just before us
+  pdl_trigger();
+  for (; u < U; u += gridDim.x) {
+    const ExUnit cur = nxt;
+#pragma unroll
+    for (int q = 0; q < EX_REGS; ++q) bc[q] = bn[q];
+    nxt = locate(u + gridDim.x);
+    if (nxt.r8) fetch(nxt, bn);   // in flight while this unit is applied
+    const int slot = tile_slot[cur.tile], count = tile_count[cur.tile];
+    const int* toks = tile_tok[cur.tile];
+    const int rank = cur.r8 * 8, cpt = EX_REGS / cur.r8;
+    const int d_out = ta.d_out[cur.tgt];
+    const float scale = slot_scale[slot];
+    const int voff = ea.v_off[cur.tgt] + slot * ea.v_slot_stride;
+    __syncthreads();   // the previous unit's vs consumed
+    for (int e = threadIdx.x; e < count * rank; e += EX_THREADS) {
+      const int i = e / rank, jj = e - i * rank;
+      vs[i][jj] = v[(size_t)toks[i] * ldv + voff + jj] * scale;
+    }
+    const int cb = ta.col_blk[cur.tgt], cstr = ta.col_stride[cur.tgt], co = ta.col_off[cur.tgt];
+    // y column of the chunk that closes each column (q % r8 == r8 - 1), -1 otherwise
+    int colq[EX_REGS];
+#pragma unroll
+    for (int q = 0; q < EX_REGS; ++q) {
+      const int c = q / cur.r8, qq = q - c * cur.r8;
+      const int n = cur.n0 + c * EX_THREADS + threadIdx.x;
+      colq[q] = (c < cpt && qq == cur.r8 - 1 && n < d_out) ? co + (n / cb) * cstr + (n % cb) : -1;
+    }
+    __syncthreads();   // vs
+    for (int i = 0; i < count; ++i) {
+      T* yr = y + (size_t)toks[i] * ldy;
+      float yq[EX_REGS];
+#pragma unroll
+      for (int q = 0; q < EX_REGS; ++q) yq[q] = colq[q] >= 0 ? to_f32(yr[colq[q]]) : 0.f;
+      const float* vr = vs[i];
+      float d = 0.f;
+#pragma unroll
+      for (int q = 0; q < EX_REGS; ++q) {
+        if (q < cpt * cur.r8) {
+          const int qq = q - (q / cur.r8) * cur.r8;
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&bc[q]);
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const float2 f = __bfloat1622float2(h2[w]);
+            d = fmaf(vr[8 * qq + 2 * w], f.x, d);
+            d = fmaf(vr[8 * qq + 2 * w + 1], f.y, d);
+          }
+          if (qq == cur.r8 - 1) {   // column complete
+            if (colq[q] >= 0) yr[colq[q]] = from_f32<T>(yq[q] + d);
+            d = 0.f;
+          }
         }
       }
     }
-    T* yp = y + (size_t)toks[i] * ldy + col;
-    *yp = from_f32<T>(to_f32(*yp) + d);
   }
 }
 
@@ -765,8 +982,8 @@ extern "C" int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, i
                 max_rank % 8 == 0 && n_targets >= 1 && n_targets <= SLX_LORA_MAX_TARGETS &&
                 targets && v_col_off && slot_rank && slot_scale && y && v_all && ldv > 0 &&
                 v_slot_stride >= 0);
-  TargetArgs ta;
-  ExpandArgs ea;
+  TargetArgs ta{};
+  ExpandArgs ea{};
   ea.v_slot_stride = v_slot_stride;
   int max_dout = 0;
   for (int i = 0; i < n_targets; ++i) {
@@ -787,14 +1004,17 @@ extern "C" int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, i
   int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
   if (st) return st;
   if (n_tok == 0) return SLX_OK;
-  dim3 grid((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)ceil_div(max_dout, EX_THREADS));
+  if (w.max_tiles * n_targets > EX_MAX_PAIRS || w.max_tiles > EX_MAX_TILES) return SLX_ERR_UNSUPPORTED;
+  ea.n_targets = n_targets;
+  const int grid = 2 * sm_count();
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == SLX_DT_BF16)
-    return launch_ex(lora_expand_v_kernel<bf16>, grid, dim3(EX_THREADS), 0, s, 1u, (bf16*)y, ldy,
-                     (const float*)v_all, ldv, slot_rank, slot_scale, max_rank, ta, ea, w);
+    return launch_ex(lora_expand_v_kernel<bf16>, dim3(grid), dim3(EX_THREADS), 0, s, 1u, (bf16*)y,
+                     ldy, (const float*)v_all, ldv, slot_rank, slot_scale, max_rank, ta, ea, w);
   if (dtype == SLX_DT_F32)
-    return launch_ex(lora_expand_v_kernel<float>, grid, dim3(EX_THREADS), 0, s, 1u, (float*)y, ldy,
-                     (const float*)v_all, ldv, slot_rank, slot_scale, max_rank, ta, ea, w);
+    return launch_ex(lora_expand_v_kernel<float>, dim3(grid), dim3(EX_THREADS), 0, s, 1u,
+                     (float*)y, ldy, (const float*)v_all, ldv, slot_rank, slot_scale, max_rank, ta,
+                     ea, w);
   return SLX_ERR_INVALID;
 }
 
@@ -814,17 +1034,33 @@ extern "C" int slx_lora_shrink(int dtype, float* v, int ldv, const void* x, int 
     ta.a_ptrs[i] = targets[i].a_ptrs;
     so.v_off[i] = v_col_off[i];
   }
+  so.n_targets = n_targets;
   LoraWs w;
   int st = carve(ws, ws_bytes, n_tok, n_slots, 1, 1, &w);
   if (st) return st;
   if (n_tok == 0) return SLX_OK;
-  dim3 grid((unsigned)w.max_tiles, (unsigned)n_targets, (unsigned)ceil_div(max_rank, SH_WARPS));
+  if (w.max_tiles * n_targets > SH_MAX_PAIRS || w.max_tiles > SH_MAX_TILES) return SLX_ERR_UNSUPPORTED;
+  const dim3 grid((unsigned)sm_count());
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == SLX_DT_BF16)
-    return launch_ex(lora_shrink_v_kernel<bf16>, grid, dim3(SH_WARPS * 32), 0, s, 1u, v, ldv,
-                     (const bf16*)x, ldx, d_in, slot_rank, max_rank, ta, so, w);
-  if (dtype == SLX_DT_F32)
-    return launch_ex(lora_shrink_v_kernel<float>, grid, dim3(SH_WARPS * 32), 0, s, 1u, v, ldv,
-                     (const float*)x, ldx, d_in, slot_rank, max_rank, ta, so, w);
+  if (dtype == SLX_DT_BF16) {
+    const int xt = shrink_xt(d_in, sizeof(bf16));
+    if (xt == 0) return SLX_ERR_UNSUPPORTED;
+    const size_t smem = shrink_smem_bytes(d_in, sizeof(bf16), xt);
+    if (cudaFuncSetAttribute(lora_shrink_v_kernel<bf16>,
+            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SLX_ERR_CUDA;
+    return launch_ex(lora_shrink_v_kernel<bf16>, grid, dim3(SH_WARPS * 32), smem, s, 1u, v, ldv,
+                     (const bf16*)x, ldx, d_in, slot_rank, max_rank, ta, so, w, xt);
+  }
+  if (dtype == SLX_DT_F32) {
+    const int xt = shrink_xt(d_in, sizeof(float));
+    if (xt == 0) return SLX_ERR_UNSUPPORTED;
+    const size_t smem = shrink_smem_bytes(d_in, sizeof(float), xt);
+    if (cudaFuncSetAttribute(lora_shrink_v_kernel<float>,
+            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return SLX_ERR_CUDA;
+    return launch_ex(lora_shrink_v_kernel<float>, grid, dim3(SH_WARPS * 32), smem, s, 1u, v, ldv,
+                     (const float*)x, ldx, d_in, slot_rank, max_rank, ta, so, w, xt);
+  }
   return SLX_ERR_INVALID;
 }
