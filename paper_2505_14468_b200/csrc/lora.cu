@@ -656,21 +656,28 @@ lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, in
 // y[t, col(n)] += scale * sum_j v[t, off + slot * v_slot_stride + j] * B_slot[n, j] over the
 // plan: v from the stacked shrink inside the projection GEMM (stride max_rank) or the gathered
 // shrink (stride 0).
-// Work unit = (plan tile, target, column block) holding 32 KB of B: a thread owns
-// cpt = 8 / (rank / 8) output columns 256 apart (rank 8: eight, rank 64: one) and their B rows
-// (eight 16-byte registers whatever the rank), so every unit is the same size and a mixed-rank
-// batch balances.  Persistent grid (2 CTAs per SM), units dealt round robin; a CTA locates its
-// units by a block scan of the (tile, target) unit counts.  B is static: the first unit's rows
-// are fetched before griddepcontrol.wait, and while a unit is being applied the NEXT unit's
-// rows are already in flight (register double buffer), so the HBM stream never waits on the
-// v / y round trips.  Per unit: the tile's scaled v in shared memory, then for each token the
-// y reads of the thread's columns together, the sequential fmaf chains over j (v pre-scaled,
-// one rounding of y: bit-identical to the fused slx_lora_delta) and the stores.
+// Work unit = (plan tile, target, column block) = 32 KB of B: cpt = 8 / (rank / 8) blocks of
+// 256 columns (rank 8: 2048 columns, rank 64: 256), so every unit is the same size and a
+// mixed-rank batch balances.  A block's B rows [n0, n0 + 256 * cpt) x rank are contiguous: ONE
+// bulk copy (TMA engine) per unit, plus one per token for its v row, on the stage's mbarriers.
+// Persistent grid (2 CTAs per SM), units dealt round robin over a dense table (block scan of the
+// (tile, target) unit counts, tile data cached in shared memory); two stages per CTA: B is
+// static, so the B rows of the CTA's first two units are issued BEFORE griddepcontrol.wait,
+// their v rows right after it, and a consumed stage is refilled at once.  Per unit a thread
+// owns cpt columns 256 apart: it reads its columns' B rows from shared memory with the 16-byte
+// chunks in a per-thread rotated order (conflict-free for power-of-two rank / 8), rotates them
+// back in registers, then per token issues the y reads of its columns, runs the sequential
+// fmaf chain over j (v * scale first, one rounding of y: bit-identical to the fused
+// slx_lora_delta) and stores.
 constexpr int EX_THREADS = 256;
 constexpr int EX_REGS = LORA_MAX_RANK / 8;   // 16-byte B chunks per thread and unit
+constexpr int EX_UNIT_BYTES = EX_THREADS * EX_REGS * 16;   // 32 KB
+constexpr int EX_STAGES = 2;
 constexpr int EX_MAX_PAIRS = 2048;           // (plan tile, target) pairs per launch
 constexpr int EX_PAIRS_PT = EX_MAX_PAIRS / EX_THREADS;
-constexpr int EX_MAX_TILES = 384;           // plan tiles per launch (1024 tokens over <= 254 slots)
+constexpr int EX_MAX_TILES = 384;            // plan tiles per launch (1024 tokens over <= 254 slots)
+constexpr size_t EX_STAGE_BYTES = EX_UNIT_BYTES + LORA_TT * LORA_MAX_RANK * 4;
+constexpr size_t EX_DYN_SMEM = 64 + EX_STAGES * EX_STAGE_BYTES;
 
 struct ExpandArgs {
   int v_off[SLX_LORA_MAX_TARGETS];
@@ -678,29 +685,90 @@ struct ExpandArgs {
   int n_targets;
 };
 
-struct ExUnit {
-  int tile, tgt, n0, r8;   // r8 = rank / 8 (0: no unit)
-};
+// One unit for a compile-time R8 = rank / 8 (CPT = EX_REGS / R8 columns per thread).
+template <typename T, int R8>
+__device__ __forceinline__ void expand_unit(T* __restrict__ y, int ldy, const unsigned char* bs,
+                                            const float* vsm, float scale, int n0, int d_out,
+                                            int count, const int* toks, int co, int cb, int cstr) {
+  constexpr int CPT = EX_REGS / R8;
+  constexpr bool POW2 = (R8 & (R8 - 1)) == 0;
+  const int t = threadIdx.x;
+  // chunk rotation that spreads a quarter-warp's 16-byte reads over all 32 banks
+  const int rot = POW2 ? ((t * R8) >> 3) & (R8 - 1) : 0;
+  uint4 b[CPT][R8];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const uint4* row = reinterpret_cast<const uint4*>(bs) + (size_t)(c * EX_THREADS + t) * R8;
+    uint4 tmp[R8];
+#pragma unroll
+    for (int q = 0; q < R8; ++q) tmp[q] = row[POW2 ? ((q + rot) & (R8 - 1)) : q];
+    // tmp[q] holds chunk (q + rot) mod R8: rotate right by rot (barrel, log2(R8) stages)
+    if (POW2) {
+#pragma unroll
+      for (int sh = 1; sh < R8; sh <<= 1) {
+        if (rot & sh) {
+          uint4 r2[R8];
+#pragma unroll
+          for (int q = 0; q < R8; ++q) r2[(q + sh) & (R8 - 1)] = tmp[q];
+#pragma unroll
+          for (int q = 0; q < R8; ++q) tmp[q] = r2[q];
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R8; ++q) b[c][q] = tmp[q];
+  }
+  int col[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int n = n0 + c * EX_THREADS + t;
+    col[c] = n < d_out ? co + (n / cb) * cstr + (n % cb) : -1;
+  }
+  for (int i = 0; i < count; ++i) {
+    T* yr = y + (size_t)toks[i] * ldy;
+    float yv[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) yv[c] = col[c] >= 0 ? to_f32(yr[col[c]]) : 0.f;
+    const float* vr = vsm + i * LORA_MAX_RANK;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      float d = 0.f;
+#pragma unroll
+      for (int q = 0; q < R8; ++q) {
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&b[c][q]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float2 f = __bfloat1622float2(h2[u]);
+          d = fmaf(vr[8 * q + 2 * u] * scale, f.x, d);
+          d = fmaf(vr[8 * q + 2 * u + 1] * scale, f.y, d);
+        }
+      }
+      if (col[c] >= 0) yr[col[c]] = from_f32<T>(yv[c] + d);
+    }
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(EX_THREADS, 2)
 lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, int ldv,
                      const int32_t* __restrict__ slot_rank, const float* __restrict__ slot_scale,
                      int max_rank, TargetArgs ta, ExpandArgs ea, LoraWs ws) {
+  extern __shared__ __align__(128) unsigned char ex_raw[];
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(ex_raw);   // [EX_STAGES]
+  uint64_t* vfull = bfull + EX_STAGES;                       // [EX_STAGES]
+  unsigned char* stages = ex_raw + 64;                       // [EX_STAGES][B 32 KB | v 8 x 64 fp32]
   using Scan = cub::BlockScan<int, EX_THREADS>;
   __shared__ typename Scan::TempStorage scan_tmp;
   __shared__ int pair_end[EX_MAX_PAIRS];   // inclusive prefix of the units per pair
-  __shared__ float vs[LORA_TT][LORA_MAX_RANK];
-  __shared__ int total_units;
-  // per plan tile, cached so a unit is located and fetched with no dependent global loads:
-  __shared__ const bf16* tile_b[EX_MAX_PAIRS];   // per pair: the slot's B of the target
   __shared__ int tile_r8[EX_MAX_TILES];
   __shared__ int tile_slot[EX_MAX_TILES];
   __shared__ int tile_tok[EX_MAX_TILES][LORA_TT];
   __shared__ int tile_count[EX_MAX_TILES];
+  __shared__ int total_units;
+  const int NTG = ea.n_targets;
   // ---- the unit table (plan and adapter pool are >= 2 launches back: before the wait)
   const int n_tiles = min(min(*ws.n_tiles, ws.max_tiles), EX_MAX_TILES);
-  const int n_pairs = min(n_tiles * ea.n_targets, EX_MAX_PAIRS);
+  const int n_pairs = min(n_tiles * NTG, EX_MAX_PAIRS);
   for (int tl = threadIdx.x; tl < n_tiles; tl += EX_THREADS) {
     const LoraTile tile = ws.tiles[tl];
     const int r = tile.count > 0 ? min(slot_rank[tile.slot], max_rank) : 0;
@@ -718,11 +786,9 @@ lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, in
     const int p = threadIdx.x * EX_PAIRS_PT + k;
     int c = 0;
     if (p < n_pairs) {
-      const int tl = p / ea.n_targets, tg = p - tl * ea.n_targets;
+      const int tl = p / NTG, tg = p - tl * NTG;
       const int r8 = tile_r8[tl];
-      const bf16* B = r8 ? reinterpret_cast<const bf16*>(ta.b_ptrs[tg][tile_slot[tl]]) : nullptr;
-      tile_b[p] = B;
-      if (B != nullptr) c = ceil_div(ta.d_out[tg], EX_THREADS * (EX_REGS / r8));
+      if (r8 && ta.b_ptrs[tg][tile_slot[tl]] != 0) c = ceil_div(ta.d_out[tg], EX_THREADS * (EX_REGS / r8));
     }
     run += c;
     cnt[k] = run;
@@ -734,91 +800,82 @@ lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, in
   if (threadIdx.x == 0) total_units = tot;
   __syncthreads();
   const int U = total_units;
-  auto locate = [&](int u) -> ExUnit {
-    ExUnit e{0, 0, 0, 0};
-    if (u >= U) return e;
+  auto locate = [&](int u, int& tl, int& tg, int& n0) {
     int lo = 0, hi = n_pairs - 1;   // first pair with pair_end > u
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
       if (pair_end[mid] > u) hi = mid; else lo = mid + 1;
     }
-    const int first = lo ? pair_end[lo - 1] : 0;
-    e.tile = lo / ea.n_targets;
-    e.tgt = lo - e.tile * ea.n_targets;
-    e.r8 = tile_r8[e.tile];
-    e.n0 = (u - first) * EX_THREADS * (EX_REGS / e.r8);
-    return e;
+    tl = lo / NTG;
+    tg = lo - tl * NTG;
+    n0 = (u - (lo ? pair_end[lo - 1] : 0)) * EX_THREADS * (EX_REGS / tile_r8[tl]);
   };
-  // B rows of unit e into registers: chunk q belongs to column c = q / r8, 16-byte piece q % r8
-  auto fetch = [&](const ExUnit& e, uint4* br) {
-    const bf16* B = tile_b[e.tile * ea.n_targets + e.tgt];
-    const int d_out = ta.d_out[e.tgt], rank = e.r8 * 8, cpt = e.r8 ? EX_REGS / e.r8 : 0;
-#pragma unroll
-    for (int q = 0; q < EX_REGS; ++q) {
-      const int c = e.r8 ? q / e.r8 : 0, qq = q - c * e.r8;
-      const int n = e.n0 + c * EX_THREADS + threadIdx.x;
-      br[q] = (c < cpt && n < d_out)
-                  ? __ldg(reinterpret_cast<const uint4*>(B + (size_t)n * rank) + qq)
-                  : make_uint4(0, 0, 0, 0);
+  auto issue_b = [&](int u, int stage) {   // thread 0: the unit's B rows -> stage
+    int tl, tg, n0;
+    locate(u, tl, tg, n0);
+    const int rank = tile_r8[tl] * 8;
+    const int cols = min(EX_THREADS * (EX_REGS / tile_r8[tl]), ta.d_out[tg] - n0);
+    const bf16* B = reinterpret_cast<const bf16*>(ta.b_ptrs[tg][tile_slot[tl]]);
+    const uint32_t bytes = (uint32_t)cols * rank * 2;
+    tc::mbar_arrive_expect_tx(&bfull[stage], bytes);
+    tc::bulk_g2s(stages + stage * EX_STAGE_BYTES, B + (size_t)n0 * rank, bytes, &bfull[stage],
+                 tc::policy_evict_first());
+  };
+  auto issue_v = [&](int u, int stage) {   // thread 0: the tile's v rows -> stage
+    int tl, tg, n0;
+    locate(u, tl, tg, n0);
+    const int rank = tile_r8[tl] * 8, count = tile_count[tl];
+    const int voff = ea.v_off[tg] + tile_slot[tl] * ea.v_slot_stride;
+    float* dst = reinterpret_cast<float*>(stages + stage * EX_STAGE_BYTES + EX_UNIT_BYTES);
+    tc::mbar_arrive_expect_tx(&vfull[stage], (uint32_t)(count * rank * 4));
+    for (int i = 0; i < count; ++i)
+      tc::bulk_g2s(dst + i * LORA_MAX_RANK, v + (size_t)tile_tok[tl][i] * ldv + voff,
+                   (uint32_t)(rank * 4), &vfull[stage], tc::policy_evict_normal());
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < EX_STAGES; ++st) {
+      tc::mbar_init(&bfull[st], 1);
+      tc::mbar_init(&vfull[st], 1);
     }
-  };
-  uint4 bn[EX_REGS], bc[EX_REGS];
-  int u = blockIdx.x;
-  ExUnit nxt = locate(u);
-  if (nxt.r8) fetch(nxt, bn);
+    tc::fence_barrier_init();
+    for (int k = 0; k < EX_STAGES; ++k)
+      if (blockIdx.x + k * gridDim.x < U) issue_b(blockIdx.x + k * gridDim.x, k);
+  }
   pdl_wait();       // v and y come from the kernels just before us
   pdl_trigger();
-  for (; u < U; u += gridDim.x) {
-    const ExUnit cur = nxt;
-#pragma unroll
-    for (int q = 0; q < EX_REGS; ++q) bc[q] = bn[q];
-    nxt = locate(u + gridDim.x);
-    if (nxt.r8) fetch(nxt, bn);   // in flight while this unit is applied
-    const int slot = tile_slot[cur.tile], count = tile_count[cur.tile];
-    const int* toks = tile_tok[cur.tile];
-    const int rank = cur.r8 * 8, cpt = EX_REGS / cur.r8;
-    const int d_out = ta.d_out[cur.tgt];
-    const float scale = slot_scale[slot];
-    const int voff = ea.v_off[cur.tgt] + slot * ea.v_slot_stride;
-    __syncthreads();   // the previous unit's vs consumed
-    for (int e = threadIdx.x; e < count * rank; e += EX_THREADS) {
-      const int i = e / rank, jj = e - i * rank;
-      vs[i][jj] = v[(size_t)toks[i] * ldv + voff + jj] * scale;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < EX_STAGES; ++k)
+      if (blockIdx.x + k * gridDim.x < U) issue_v(blockIdx.x + k * gridDim.x, k);
+  int k = 0;
+  for (int u = blockIdx.x; u < U; u += gridDim.x, ++k) {
+    const int stage = k % EX_STAGES;
+    const uint32_t parity = (uint32_t)((k / EX_STAGES) & 1);
+    int tl, tg, n0;
+    locate(u, tl, tg, n0);
+    const int r8 = tile_r8[tl], count = tile_count[tl];
+    const float scale = slot_scale[tile_slot[tl]];
+    const int d_out = ta.d_out[tg];
+    const int cb = ta.col_blk[tg], cstr = ta.col_stride[tg], co = ta.col_off[tg];
+    const unsigned char* bs = stages + stage * EX_STAGE_BYTES;
+    const float* vsm = reinterpret_cast<const float*>(bs + EX_UNIT_BYTES);
+    tc::mbar_wait(&bfull[stage], parity);
+    tc::mbar_wait(&vfull[stage], parity);
+#define SLX_EXPAND_CASE(r)                                                                    \
+  case r:                                                                                     \
+    expand_unit<T, r>(y, ldy, bs, vsm, scale, n0, d_out, count, tile_tok[tl], co, cb, cstr);  \
+    break;
+    switch (r8) {
+      SLX_EXPAND_CASE(1) SLX_EXPAND_CASE(2) SLX_EXPAND_CASE(3) SLX_EXPAND_CASE(4)
+      SLX_EXPAND_CASE(5) SLX_EXPAND_CASE(6) SLX_EXPAND_CASE(7) SLX_EXPAND_CASE(8)
+      default: break;
     }
-    const int cb = ta.col_blk[cur.tgt], cstr = ta.col_stride[cur.tgt], co = ta.col_off[cur.tgt];
-    // y column of the chunk that closes each column (q % r8 == r8 - 1), -1 otherwise
-    int colq[EX_REGS];
-#pragma unroll
-    for (int q = 0; q < EX_REGS; ++q) {
-      const int c = q / cur.r8, qq = q - c * cur.r8;
-      const int n = cur.n0 + c * EX_THREADS + threadIdx.x;
-      colq[q] = (c < cpt && qq == cur.r8 - 1 && n < d_out) ? co + (n / cb) * cstr + (n % cb) : -1;
-    }
-    __syncthreads();   // vs
-    for (int i = 0; i < count; ++i) {
-      T* yr = y + (size_t)toks[i] * ldy;
-      float yq[EX_REGS];
-#pragma unroll
-      for (int q = 0; q < EX_REGS; ++q) yq[q] = colq[q] >= 0 ? to_f32(yr[colq[q]]) : 0.f;
-      const float* vr = vs[i];
-      float d = 0.f;
-#pragma unroll
-      for (int q = 0; q < EX_REGS; ++q) {
-        if (q < cpt * cur.r8) {
-          const int qq = q - (q / cur.r8) * cur.r8;
-          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&bc[q]);
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const float2 f = __bfloat1622float2(h2[w]);
-            d = fmaf(vr[8 * qq + 2 * w], f.x, d);
-            d = fmaf(vr[8 * qq + 2 * w + 1], f.y, d);
-          }
-          if (qq == cur.r8 - 1) {   // column complete
-            if (colq[q] >= 0) yr[colq[q]] = from_f32<T>(yq[q] + d);
-            d = 0.f;
-          }
-        }
-      }
+#undef SLX_EXPAND_CASE
+    __syncthreads();   // every thread is done with this stage
+    const int un = u + EX_STAGES * gridDim.x;
+    if (threadIdx.x == 0 && un < U) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic -> async proxy
+      issue_b(un, stage);
+      issue_v(un, stage);
     }
   }
 }
@@ -981,7 +1038,8 @@ extern "C" int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, i
   SLX_CHECK_ARG(n_tok >= 0 && n_slots > 0 && max_rank > 0 && max_rank <= LORA_MAX_RANK &&
                 max_rank % 8 == 0 && n_targets >= 1 && n_targets <= SLX_LORA_MAX_TARGETS &&
                 targets && v_col_off && slot_rank && slot_scale && y && v_all && ldv > 0 &&
-                v_slot_stride >= 0);
+                ldv % 4 == 0 && v_slot_stride >= 0 && v_slot_stride % 4 == 0);
+  SLX_CHECK_ALIGN(v_all, 16);
   TargetArgs ta{};
   ExpandArgs ea{};
   ea.v_slot_stride = v_slot_stride;
@@ -989,7 +1047,7 @@ extern "C" int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, i
   for (int i = 0; i < n_targets; ++i) {
     const slx_lora_target& t = targets[i];
     SLX_CHECK_ARG(t.b_ptrs && t.d_out > 0 && t.d_out % 8 == 0 && t.y_col_block > 0 &&
-                  t.y_col_stride >= t.y_col_block && v_col_off[i] >= 0 &&
+                  t.y_col_stride >= t.y_col_block && v_col_off[i] >= 0 && v_col_off[i] % 4 == 0 &&
                   v_col_off[i] + (n_slots - 1) * v_slot_stride + max_rank <= ldv);
     ta.a_ptrs[i] = t.a_ptrs;
     ta.b_ptrs[i] = t.b_ptrs;
@@ -1008,13 +1066,22 @@ extern "C" int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, i
   ea.n_targets = n_targets;
   const int grid = 2 * sm_count();
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == SLX_DT_BF16)
-    return launch_ex(lora_expand_v_kernel<bf16>, dim3(grid), dim3(EX_THREADS), 0, s, 1u, (bf16*)y,
-                     ldy, (const float*)v_all, ldv, slot_rank, slot_scale, max_rank, ta, ea, w);
-  if (dtype == SLX_DT_F32)
-    return launch_ex(lora_expand_v_kernel<float>, dim3(grid), dim3(EX_THREADS), 0, s, 1u,
+  if (dtype == SLX_DT_BF16) {
+    if (cudaFuncSetAttribute(lora_expand_v_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)EX_DYN_SMEM) != cudaSuccess)
+      return SLX_ERR_CUDA;
+    return launch_ex(lora_expand_v_kernel<bf16>, dim3(grid), dim3(EX_THREADS), EX_DYN_SMEM, s, 1u,
+                     (bf16*)y, ldy, (const float*)v_all, ldv, slot_rank, slot_scale, max_rank, ta,
+                     ea, w);
+  }
+  if (dtype == SLX_DT_F32) {
+    if (cudaFuncSetAttribute(lora_expand_v_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)EX_DYN_SMEM) != cudaSuccess)
+      return SLX_ERR_CUDA;
+    return launch_ex(lora_expand_v_kernel<float>, dim3(grid), dim3(EX_THREADS), EX_DYN_SMEM, s, 1u,
                      (float*)y, ldy, (const float*)v_all, ldv, slot_rank, slot_scale, max_rank, ta,
                      ea, w);
+  }
   return SLX_ERR_INVALID;
 }
 
