@@ -220,7 +220,12 @@ SLX_API int slx_lora_apply(int dtype, void* y, int ldy, const void* x, int ldx, 
  * target i, column v_col_off[i] + slot * v_slot_stride + j = x_t . A_slot[j] — the stacked
  * shrink inside the projection GEMM (slx_gemm_bf16 side output, v_slot_stride = max_rank) or
  * the gathered shrink (slx_lora_shrink, v_slot_stride = 0); adds scale * v . B_slot^T into y in
- * place (sequential fmaf in j, one rounding: bit-identical to the fused slx_lora_delta). */
+ * place (sequential fmaf in j, one rounding: bit-identical to the fused slx_lora_delta).
+ * Persistent, B rows and v rows by TMA bulk copies: ldv, v_col_off[i] and v_slot_stride are
+ * multiples of 4 and v_all is 16-byte aligned (else SLX_ERR_INVALID); B tables 16-byte aligned;
+ * the plan's tile bound (slx_lora_workspace_bytes' n_tok / n_slots) must satisfy
+ * max_tiles <= 384 and max_tiles * n_targets <= 2048, max_tiles = ceil(n_tok / 8) +
+ * min(n_slots, n_tok) + 1 (else SLX_ERR_UNSUPPORTED). */
 SLX_API int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, int ldv, int n_tok,
                   const int32_t* slot_rank, const float* slot_scale, int n_slots, int max_rank,
                   int n_targets, const slx_lora_target* targets, const int* v_col_off,
@@ -229,7 +234,10 @@ SLX_API int slx_lora_expand(int dtype, void* y, int ldy, const void* v_all, int 
  * v[t, v_col_off[i] + j] = x_t . A_{slot(t), i}[j] for j < rank (fp32, unscaled), reading each
  * adapter present in the batch once per plan tile of <= 8 tokens (a_ptrs of the targets; b_ptrs
  * unused).  Rows of tokens without an adapter are not written.  Consumers: slx_lora_delta with
- * v_slot_stride = 0. */
+ * v_slot_stride = 0.  Persistent, A rows and x rows by TMA bulk copies (x 16-byte aligned);
+ * max_tiles <= 384 and max_tiles * n_targets <= 1024 (see slx_lora_expand), and two stages of
+ * >= 1 A row + 1 x row must fit 204 KB of shared memory (bf16 x: d_in <= 26112), else
+ * SLX_ERR_UNSUPPORTED. */
 SLX_API int slx_lora_shrink(int dtype, float* v, int ldv, const void* x, int ldx, int n_tok,
                   int d_in, const int32_t* slot_rank, int n_slots, int max_rank, int n_targets,
                   const slx_lora_target* targets, const int* v_col_off, void* ws,

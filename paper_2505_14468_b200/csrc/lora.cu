@@ -463,8 +463,9 @@ lora_fused_kernel(T* __restrict__ y, int ldy, const T* __restrict__ x, int ldx, 
 // Large adapter pools (decode): instead of stacking every slot's A rows into the projection
 // GEMM (bytes grow with the pool), the shrink reads only the adapters present in the batch,
 // each ONCE per plan tile.
-// Work unit = (plan tile, target, 8 rows j0..j0+7 of A): a slot's rows are contiguous
-// ([rank][d_in]), so a unit is ONE bulk copy (TMA engine, 80 KB at d_in 5120).  Persistent
+// Work unit = (plan tile, target, 8 rows j0..j0+7 of A; 4 / 2 / 1 rows when d_in is too wide
+// for two stages of 8): a slot's rows are contiguous ([rank][d_in]), so a unit is ONE bulk copy
+// (TMA engine, 80 KB at d_in 5120).  Persistent
 // grid (one CTA per SM), units dealt round robin over a dense table (block scan of the
 // (tile, target) unit counts, tile data cached in shared memory: no dead CTAs, no dependent
 // global loads per unit).  Two shared-memory stages, each holding a unit's A rows and the
@@ -490,28 +491,34 @@ struct ShrinkOut {
   int v_off[SLX_LORA_MAX_TARGETS];
   int n_targets;
 };
-inline size_t shrink_smem_bytes(int d_in, size_t x_elem, int xt) {
-  return 64 + (size_t)SH_STAGES * ((size_t)SH_WARPS * d_in * 2 + (size_t)xt * d_in * x_elem);
+inline size_t shrink_smem_bytes(int d_in, size_t x_elem, int rpu, int xt) {
+  return 64 + (size_t)SH_STAGES * ((size_t)rpu * d_in * 2 + (size_t)xt * d_in * x_elem);
 }
-// token rows of x per stage that fit next to the A rows (0: d_in too large)
-inline int shrink_xt(int d_in, size_t x_elem) {
-  for (int xt = SH_XT; xt >= 1; --xt)
-    if (shrink_smem_bytes(d_in, x_elem, xt) <= SH_DYN_SMEM) return xt;
-  return 0;
+// A rows per unit (8, or fewer for wide d_in) and token rows of x per stage that fit the
+// shared memory (false: d_in too large)
+inline bool shrink_geometry(int d_in, size_t x_elem, int* rpu, int* xt) {
+  for (int r = SH_WARPS; r >= 1; r >>= 1)
+    for (int t = SH_XT; t >= 1; --t)
+      if (shrink_smem_bytes(d_in, x_elem, r, t) <= SH_DYN_SMEM) {
+        *rpu = r;
+        *xt = t;
+        return true;
+      }
+  return false;
 }
 
 template <typename T>
 __global__ void __launch_bounds__(SH_WARPS * 32, 1)
 lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, int ldx, int d_in,
                      const int32_t* __restrict__ slot_rank, int max_rank, TargetArgs ta,
-                     ShrinkOut so, LoraWs ws, int xt) {
+                     ShrinkOut so, LoraWs ws, int rpu, int xt) {
   constexpr int NT = SH_WARPS * 32;
   extern __shared__ __align__(128) unsigned char sh_raw[];
   uint64_t* afull = reinterpret_cast<uint64_t*>(sh_raw);        // [SH_STAGES]
   uint64_t* xfull = afull + SH_STAGES;                            // [SH_STAGES]
-  const size_t a_stage = (size_t)SH_WARPS * d_in;                 // bf16 elements
+  const size_t a_stage = (size_t)rpu * d_in;                      // bf16 elements
   const size_t x_stage = (size_t)xt * d_in;                       // T elements
-  bf16* As = reinterpret_cast<bf16*>(sh_raw + 64);                // [SH_STAGES][8][d_in]
+  bf16* As = reinterpret_cast<bf16*>(sh_raw + 64);                // [SH_STAGES][rpu][d_in]
   T* Xs = reinterpret_cast<T*>(sh_raw + 64 + SH_STAGES * a_stage * 2);   // [SH_STAGES][xt][d_in]
   using Scan = cub::BlockScan<int, NT>;
   __shared__ typename Scan::TempStorage scan_tmp;
@@ -544,7 +551,7 @@ lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, in
     if (p < n_pairs) {
       const int tl = p / NTG, tg = p - tl * NTG;
       const int r = tile_rank[tl];
-      if (r > 0 && ta.a_ptrs[tg][tile_slot[tl]] != 0) c = ceil_div(r, SH_WARPS);
+      if (r > 0 && ta.a_ptrs[tg][tile_slot[tl]] != 0) c = ceil_div(r, rpu);
     }
     run += c;
     cnt[k] = run;
@@ -563,14 +570,14 @@ lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, in
       if (pair_end[mid] > u) hi = mid; else lo = mid + 1;
     }
     pair = lo;
-    j0 = (u - (lo ? pair_end[lo - 1] : 0)) * SH_WARPS;
+    j0 = (u - (lo ? pair_end[lo - 1] : 0)) * rpu;
   };
   auto issue_a = [&](int u, int stage) {   // thread 0: the unit's A rows -> stage
     int pair, j0;
     locate(u, pair, j0);
     const int tl = pair / NTG, tg = pair - tl * NTG;
     const bf16* A = reinterpret_cast<const bf16*>(ta.a_ptrs[tg][tile_slot[tl]]);
-    const uint32_t bytes = (uint32_t)min(SH_WARPS, tile_rank[tl] - j0) * d_in * 2;
+    const uint32_t bytes = (uint32_t)min(rpu, tile_rank[tl] - j0) * d_in * 2;
     tc::mbar_arrive_expect_tx(&afull[stage], bytes);
     tc::bulk_g2s(As + stage * a_stage, A + (size_t)j0 * d_in, bytes, &afull[stage],
                  tc::policy_evict_first());
@@ -609,7 +616,7 @@ lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, in
     int pair, j0;
     locate(u, pair, j0);
     const int tl = pair / NTG, tg = pair - tl * NTG;
-    const int nrows = min(SH_WARPS, tile_rank[tl] - j0), count = tile_count[tl];
+    const int nrows = min(rpu, tile_rank[tl] - j0), count = tile_count[tl];
     const bool mine = warp < nrows;   // warp-uniform
     const bf16* ar = As + stage * a_stage + (size_t)warp * d_in;
     T* xs = Xs + stage * x_stage;
@@ -1110,24 +1117,24 @@ extern "C" int slx_lora_shrink(int dtype, float* v, int ldv, const void* x, int 
   const dim3 grid((unsigned)sm_count());
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == SLX_DT_BF16) {
-    const int xt = shrink_xt(d_in, sizeof(bf16));
-    if (xt == 0) return SLX_ERR_UNSUPPORTED;
-    const size_t smem = shrink_smem_bytes(d_in, sizeof(bf16), xt);
+    int rpu, xt;
+    if (!shrink_geometry(d_in, sizeof(bf16), &rpu, &xt)) return SLX_ERR_UNSUPPORTED;
+    const size_t smem = shrink_smem_bytes(d_in, sizeof(bf16), rpu, xt);
     if (cudaFuncSetAttribute(lora_shrink_v_kernel<bf16>,
             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return SLX_ERR_CUDA;
     return launch_ex(lora_shrink_v_kernel<bf16>, grid, dim3(SH_WARPS * 32), smem, s, 1u, v, ldv,
-                     (const bf16*)x, ldx, d_in, slot_rank, max_rank, ta, so, w, xt);
+                     (const bf16*)x, ldx, d_in, slot_rank, max_rank, ta, so, w, rpu, xt);
   }
   if (dtype == SLX_DT_F32) {
-    const int xt = shrink_xt(d_in, sizeof(float));
-    if (xt == 0) return SLX_ERR_UNSUPPORTED;
-    const size_t smem = shrink_smem_bytes(d_in, sizeof(float), xt);
+    int rpu, xt;
+    if (!shrink_geometry(d_in, sizeof(float), &rpu, &xt)) return SLX_ERR_UNSUPPORTED;
+    const size_t smem = shrink_smem_bytes(d_in, sizeof(float), rpu, xt);
     if (cudaFuncSetAttribute(lora_shrink_v_kernel<float>,
             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return SLX_ERR_CUDA;
     return launch_ex(lora_shrink_v_kernel<float>, grid, dim3(SH_WARPS * 32), smem, s, 1u, v, ldv,
-                     (const float*)x, ldx, d_in, slot_rank, max_rank, ta, so, w, xt);
+                     (const float*)x, ldx, d_in, slot_rank, max_rank, ta, so, w, rpu, xt);
   }
   return SLX_ERR_INVALID;
 }

@@ -33,7 +33,7 @@ def _pool(n_slots, ranks, d_in, d_outs, seed):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-@pytest.mark.parametrize("d_in,n_tok", [(512, 24), (5120, 64), (1024, 37)])
+@pytest.mark.parametrize("d_in,n_tok", [(512, 24), (5120, 64), (1024, 37), (8192, 16)])
 def test_gathered_shrink_expand_matches_oracle(dtype, d_in, n_tok):
     torch.manual_seed(0)
     rng = np.random.default_rng(d_in + n_tok)
