@@ -531,16 +531,27 @@ lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, in
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NTG = so.n_targets;
   // ---- the unit table (plan and adapter pool are >= 2 launches back: before the wait)
-  const int n_tiles = min(min(*ws.n_tiles, ws.max_tiles), SH_MAX_TILES);
-  const int n_pairs = min(n_tiles * NTG, SH_MAX_PAIRS);
-  for (int tl = threadIdx.x; tl < n_tiles; tl += NT) {
+  // Two dependent round trips: {tile count, tiles (read speculatively up to the plan's bound)}
+  // -> {slot rank, the targets' A pointers, token ids}; a pair's "has A" flag is parked in
+  // pair_end until the scan.
+  const int nt_plan = *ws.n_tiles;
+  const int tmax = min(ws.max_tiles, SH_MAX_TILES);
+  for (int tl = threadIdx.x; tl < tmax; tl += NT) {
     const LoraTile tile = ws.tiles[tl];
-    tile_rank[tl] = tile.count > 0 ? min(slot_rank[tile.slot], max_rank) : 0;
-    tile_slot[tl] = tile.slot;
-    tile_count[tl] = min(tile.count, LORA_TT);
+    const bool ok = tl < nt_plan && tile.count > 0;
+    const int r = ok ? min(slot_rank[tile.slot], max_rank) : 0;
 #pragma unroll
-    for (int i = 0; i < LORA_TT; ++i) tile_tok[tl][i] = i < tile.count ? ws.perm[tile.start + i] : 0;
+    for (int tg = 0; tg < SLX_LORA_MAX_TARGETS; ++tg)
+      if (tg < NTG && tl * NTG + tg < SH_MAX_PAIRS)
+        pair_end[tl * NTG + tg] = ok && ta.a_ptrs[tg][tile.slot] != 0;
+    tile_rank[tl] = r;
+    tile_slot[tl] = tile.slot;
+    tile_count[tl] = ok ? min(tile.count, LORA_TT) : 0;
+#pragma unroll
+    for (int i = 0; i < LORA_TT; ++i) tile_tok[tl][i] = ok && i < tile.count ? ws.perm[tile.start + i] : 0;
   }
+  const int n_tiles = min(nt_plan, tmax);
+  const int n_pairs = min(n_tiles * NTG, SH_MAX_PAIRS);
   __syncthreads();
   int cnt[SH_PAIRS_PT];
   int run = 0;
@@ -549,9 +560,8 @@ lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, in
     const int p = threadIdx.x * SH_PAIRS_PT + k;
     int c = 0;
     if (p < n_pairs) {
-      const int tl = p / NTG, tg = p - tl * NTG;
-      const int r = tile_rank[tl];
-      if (r > 0 && ta.a_ptrs[tg][tile_slot[tl]] != 0) c = ceil_div(r, rpu);
+      const int r = tile_rank[p / NTG];
+      if (r > 0 && pair_end[p]) c = ceil_div(r, rpu);
     }
     run += c;
     cnt[k] = run;
@@ -774,17 +784,26 @@ lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, in
   __shared__ int total_units;
   const int NTG = ea.n_targets;
   // ---- the unit table (plan and adapter pool are >= 2 launches back: before the wait)
-  const int n_tiles = min(min(*ws.n_tiles, ws.max_tiles), EX_MAX_TILES);
-  const int n_pairs = min(n_tiles * NTG, EX_MAX_PAIRS);
-  for (int tl = threadIdx.x; tl < n_tiles; tl += EX_THREADS) {
+  // Two dependent round trips (as in the shrink): {tile count, tiles} -> {slot rank, the
+  // targets' B pointers, token ids}; a pair's "has B" flag is parked in pair_end until the scan.
+  const int nt_plan = *ws.n_tiles;
+  const int tmax = min(ws.max_tiles, EX_MAX_TILES);
+  for (int tl = threadIdx.x; tl < tmax; tl += EX_THREADS) {
     const LoraTile tile = ws.tiles[tl];
-    const int r = tile.count > 0 ? min(slot_rank[tile.slot], max_rank) : 0;
+    const bool ok = tl < nt_plan && tile.count > 0;
+    const int r = ok ? min(slot_rank[tile.slot], max_rank) : 0;
+#pragma unroll
+    for (int tg = 0; tg < SLX_LORA_MAX_TARGETS; ++tg)
+      if (tg < NTG && tl * NTG + tg < EX_MAX_PAIRS)
+        pair_end[tl * NTG + tg] = ok && ta.b_ptrs[tg][tile.slot] != 0;
     tile_r8[tl] = (r + 7) >> 3;
     tile_slot[tl] = tile.slot;
-    tile_count[tl] = min(tile.count, LORA_TT);
+    tile_count[tl] = ok ? min(tile.count, LORA_TT) : 0;
 #pragma unroll
-    for (int i = 0; i < LORA_TT; ++i) tile_tok[tl][i] = i < tile.count ? ws.perm[tile.start + i] : 0;
+    for (int i = 0; i < LORA_TT; ++i) tile_tok[tl][i] = ok && i < tile.count ? ws.perm[tile.start + i] : 0;
   }
+  const int n_tiles = min(nt_plan, tmax);
+  const int n_pairs = min(n_tiles * NTG, EX_MAX_PAIRS);
   __syncthreads();
   int cnt[EX_PAIRS_PT];
   int run = 0;
@@ -795,7 +814,7 @@ lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, in
     if (p < n_pairs) {
       const int tl = p / NTG, tg = p - tl * NTG;
       const int r8 = tile_r8[tl];
-      if (r8 && ta.b_ptrs[tg][tile_slot[tl]] != 0) c = ceil_div(ta.d_out[tg], EX_THREADS * (EX_REGS / r8));
+      if (r8 && pair_end[p]) c = ceil_div(ta.d_out[tg], EX_THREADS * (EX_REGS / r8));
     }
     run += c;
     cnt[k] = run;
