@@ -58,3 +58,35 @@ def test_argument_validation_without_device():
     buf = (ctypes.c_char * 64)()
     addr = ctypes.addressof(buf) | 1
     assert lib.slx_embedding(0, addr, addr, addr, 1, 8, 10, null) == -2
+
+
+def test_gathered_lora_argument_validation_without_device():
+    """slx_lora_expand / slx_lora_shrink reject what their bulk copies cannot move (v rows not
+    16-byte aligned: ldv, v_col_off or v_slot_stride not multiples of 4; misaligned v) before any
+    CUDA call."""
+    LoraTarget = _lib.LoraTarget
+    lib = _lib.load()
+    buf = (ctypes.c_char * 4096)()
+    base = (ctypes.addressof(buf) + 255) // 256 * 256
+    tg = (LoraTarget * 1)()
+    tg[0] = LoraTarget(base, base, 64, 0, 64, 64)
+    offs = (ctypes.c_int * 1)(0)
+    ws, wsb = base, 2048
+    # ldv not a multiple of 4
+    assert lib.slx_lora_expand(0, base, 64, base, 66, 4, base, base, 2, 16, 1, tg, offs, 0,
+                               ws, wsb, None) == -1
+    # v_slot_stride not a multiple of 4
+    assert lib.slx_lora_expand(0, base, 64, base, 64, 4, base, base, 2, 16, 1, tg, offs, 18,
+                               ws, wsb, None) == -1
+    # v_col_off not a multiple of 4
+    offs2 = (ctypes.c_int * 1)(2)
+    assert lib.slx_lora_expand(0, base, 64, base, 64, 4, base, base, 2, 16, 1, tg, offs2, 0,
+                               ws, wsb, None) == -1
+    # misaligned v
+    assert lib.slx_lora_expand(0, base, 64, base + 4, 64, 4, base, base, 2, 16, 1, tg, offs, 0,
+                               ws, wsb, None) == -2
+    # shrink: max_rank beyond the 64-row limit, misaligned x
+    assert lib.slx_lora_shrink(0, base, 64, base, 64, 4, 64, base, 2, 128, 1, tg, offs, ws, wsb,
+                               None) == -1
+    assert lib.slx_lora_shrink(0, base, 64, base + 2, 64, 4, 64, base, 2, 16, 1, tg, offs, ws, wsb,
+                               None) == -2
