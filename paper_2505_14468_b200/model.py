@@ -216,6 +216,7 @@ class MultiLoraModel:
         # (o at 8: +50 us/step)
         self.splitk_consumer = True
         self.splitk_splits_o, self.splitk_splits_dn = 6, 8
+        self._n_sm = None
         # decode: each kernel prefetches the next kernel's first bytes into L2 (MB; 0 = off)
         self.l2_prefetch_mb = 16.0
         self._pf_cache: dict = {}
@@ -618,6 +619,20 @@ class MultiLoraModel:
                 start = i
         return out
 
+    def _sk_splits(self, n_out: int, k: int, pieces: int) -> int:
+        """Split-K pieces of a decode projection (o, down): the tuned count (7B: o 6, down 8)
+        unless its grid -- ceil(n_out / 256) tiles x pieces, one tcgen05 CTA per SM -- exceeds
+        the SMs; then pieces filling ~70 % of them, since a second wave doubles the launch
+        (13B down: 20 x 8 = 160 CTAs -> 20 x 5; pool decode 10.06 -> 9.45 ms/step,
+        exp/sk_splits_13b.py)."""
+        tiles = (n_out + 255) // 256
+        s = max(1, min(pieces, k // 64))
+        if self._n_sm is None:
+            self._n_sm = ops.sm_count()
+        if tiles * s > self._n_sm:
+            s = max(1, int(0.7 * self._n_sm) // tiles)
+        return s
+
     def _decode_fast(self, T: int) -> bool:
         """The bf16 decode step of fused kernels (split-K consumers, fused LoRA expands)."""
         d = self.cfg.hidden
@@ -667,8 +682,8 @@ class MultiLoraModel:
         if gather:
             v_g = torch.empty((T, max(1, len(qkv_names)) * R), dtype=torch.float32, device=dev)
             v_go = torch.empty((T, R), dtype=torch.float32, device=dev)
-        S = min(self.splitk_splits_o, (d + 63) // 64)               # o: K = q_dim
-        S_dn = min(self.splitk_splits_dn, self.ffn_pad // 64)       # down: K = ffn
+        S = self._sk_splits(d + self._extra_rows("wo"), cfg.q_dim, self.splitk_splits_o)
+        S_dn = self._sk_splits(d, self.ffn_pad, self.splitk_splits_dn)
         part_o = torch.empty(ops.splitk_bytes(T, d + self._extra_rows("wo"), S) // 4,
                              dtype=torch.float32, device=dev)
         part_dn = torch.empty(ops.splitk_bytes(T, d, S_dn) // 4, dtype=torch.float32, device=dev)

@@ -252,6 +252,13 @@ def gemm_f32(a: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None, 
 
 
 # ---------------------------------------------------------------------------------- K2/K3
+def sm_count() -> int:
+    """SMs of the current device (slx_device_sm_count)."""
+    n = ctypes.c_int(0)
+    check(_lib.load().slx_device_sm_count(ctypes.byref(n)), "slx_device_sm_count")
+    return n.value
+
+
 def lora_workspace_bytes(n_tok: int, n_slots: int, max_rank: int, n_targets: int) -> int:
     return _lib.load().slx_lora_workspace_bytes(n_tok, n_slots, max_rank, n_targets)
 
