@@ -63,9 +63,9 @@ if "--combos" in sys.argv:
 else:
     for mb in (0.0, 8.0, 24.0, 32.0, 48.0):
         variants.append({"l2_prefetch_mb": mb})
-    for so in (4, 8):
+    for so in (4, 5, 7, 8):
         variants.append({"splitk_splits_o": so})
-    for sd in (6, 9):
+    for sd in (6, 7, 9):
         variants.append({"splitk_splits_dn": sd})
 for v in variants:
     ms = timed(**v)
