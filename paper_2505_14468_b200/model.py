@@ -742,8 +742,9 @@ class MultiLoraModel:
         """(flash plan, LoRA-fold plan, SGMV plan) of a segmented prefill batch, cached by the
         segment layout and the segments' adapter slots (a serving loop re-plans only when the
         batch shape changes; the plans are device tensors built once)."""
-        key = (tuple(tuple(int(v) for v in sg) for sg in segments),
-               tuple(int(slot_host[sg[0]]) for sg in segments), T, flash, sgmv, self.lora_fold)
+        slots = tuple(int(slot_host[sg[0]]) for sg in segments) if sgmv else None
+        key = (tuple(tuple(int(v) for v in sg) for sg in segments), slots, T, flash, sgmv,
+               self.lora_fold)
         hit = self._plan_cache.get(key)
         if hit is not None:
             return hit

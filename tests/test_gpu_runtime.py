@@ -202,3 +202,21 @@ def test_runtime_graph_decode_buckets_bf16(golden):
                 break
     rep = rt.report()
     assert rep["requests"] == len(prompts) and rep["ttft_ms"]["p50"] > 0
+
+
+def test_calibration_on_the_flash_prefill_path():
+    """profile_function_spec at head_dim 128 (the tcgen05 flash prefill + stacked small-batch
+    LoRA path of the 7B/13B calibration, tools/calibrate_b200.py): forward() called with
+    segments and no host slots must plan without them (regression: the plan cache keyed on
+    host slots the non-SGMV path does not have)."""
+    from paper_2505_14468_b200.config import BackboneConfig, LoraConfig
+    cfg = BackboneConfig("small128", hidden=512, layers=2, heads=4, kv_heads=4, head_dim=128,
+                         ffn=1024, vocab=1000)
+    m = MultiLoraModel(cfg, dtype=torch.bfloat16, max_seqs=8, max_ctx=64, n_slots=2, max_rank=16,
+                       max_tokens=8 * 32)
+    m.random_backbone(seed=0)
+    m.pool.load_random(0, LoraConfig(16, 32.0, ("q", "k", "v", "o")), seed=1)
+    spec, raw = profile_function_spec(m, "small-chat", 0, backbone_id="small128", prompt_len=24,
+                                      max_new_tokens=8, batch_sizes=(1, 2, 4))
+    assert spec.prefill_base_ms > 0 and spec.decode_ms_per_token > 0
+    assert len(raw["prefill_ms"]) == 3

@@ -2,8 +2,9 @@
 B200 with the real kernels — T0 and alpha of predict_ttft(b) = T0 + alpha (b - 1) over mixed
 prefills of b 60-token prompts (the reference trace's median prompt), decode ms/token of a
 batch-1 step, KV bytes per request, and the pre-loader's host->HBM artifact loads — for the
-Llama-2-7B and -13B shapes, r16 adapters on q,k,v,o.  Writes profiles/r01_calibrated_specs.json
-(consumed by tools/run_config4.py, which runs the unchanged reference simulator).
+Llama-2-7B and -13B shapes, r16 adapters on q,k,v,o.  Writes gpurun_out/calibrated_specs.json
+(committed as profiles/r0N_calibrated_specs.json, consumed by tools/run_config4.py --cal, which
+runs the unchanged reference simulator).
 python tools/calibrate_b200.py"""
 import json
 import os

@@ -95,8 +95,11 @@ def main():
     ap.add_argument("--replan-period", type=float, default=10.0,
                     help="SimConfig.replan_period_s (reference default 10 s; SURVEY 8d: raise it at 130 fns)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_config4_sim.json"))
+    ap.add_argument("--cal", default=os.path.join(ROOT, "profiles", "r01_calibrated_specs.json"),
+                    help="calibrated specs written by tools/calibrate_b200.py")
     a = ap.parse_args()
-    cal = json.load(open(os.path.join(ROOT, "profiles", "r01_calibrated_specs.json")))
+    cal = json.load(open(a.cal))
+    print("calibration:", a.cal, flush=True)
     cl = cluster(a.gpus)
     res = {"setup": {"adapters_per_family": a.adapters, "functions": 2 * (a.adapters + 1),
                      "gpus": a.gpus, "gpu_mem_bytes": 180e9, "duration_s": a.duration,
