@@ -48,7 +48,21 @@ def measure_prefill_ms(model, adapter_slot: int, b: int, prompt_len: int, seed: 
 
 
 def measure_decode_ms(model, adapter_slot: int, b: int, ctx: int) -> float:
+    """One merged decode step of ``b`` sequences at context ``ctx`` as the serving runtime runs
+    it: a captured CUDA graph (engine.DecodeGraph, as runtime.DecodeBuckets replays) when the
+    model has the graph-capturable bf16 decode path, else the eager forward."""
+    from .engine import DecodeGraph
+
     dev = model.device
+    if model.dtype == torch.bfloat16 and len(model.free_seqs) >= b:
+        seqs = [model.alloc_seq() for _ in range(b)]
+        try:
+            dg = DecodeGraph(model, seqs, [adapter_slot] * b, fixed_pos=ctx)
+            dg.capture()
+            return _time_ms(dg.replay)
+        finally:
+            for s_ in seqs:
+                model.free_seq(s_)
     toks = torch.ones(b, dtype=torch.int32, device=dev)
     pos = torch.full((b,), ctx, dtype=torch.int32, device=dev)
     seq = torch.arange(b, dtype=torch.int32, device=dev)
