@@ -39,19 +39,23 @@ import torch
 from .batching import BatchQueue, batch_delay, max_batch_size, schedule_round
 from .engine import DecodeBuckets
 from .model import MultiLoraModel
-from .segments import Request, build_decode, build_prefill
+from .segments import Request, build_decode, build_mixed, build_prefill
 
 
 class ServingRuntime:
     def __init__(self, model: MultiLoraModel, functions: dict, gpu_id: str = "gpu0",
                  tick_ms: float = 10.0, *, store=None, adapters: dict | None = None,
                  preloader=None, offloader=None, graphs: bool | None = None,
-                 buckets=(1, 2, 4, 8, 16, 32, 64, 96, 128)):
+                 buckets=(1, 2, 4, 8, 16, 32, 64, 96, 128), mixed_rounds: bool = True):
         """``functions``: function_id -> (FunctionSpec-like, adapter slot or -1).
         ``adapters``: function_id -> (artifact name in ``store``, LoraConfig) for functions whose
         adapter lives in the pinned container tier and is loaded at dispatch (needs
         ``preloader``; ``offloader`` demotes idle adapters when no slot is free).
-        ``graphs`` (default: bf16 models): decode through captured graphs per bucket."""
+        ``graphs`` (default: bf16 models): decode through captured graphs per bucket.
+        ``mixed_rounds``: a round with new prompts AND running sequences runs ONE forward --
+        the prompts' segments plus one 1-token segment per running sequence -- instead of a
+        prefill forward followed by a decode step (each of which streams every weight once);
+        the just-prefilled requests then decode from the next round on."""
         self.m = model
         self.gpu_id = gpu_id
         self.tick_ms = tick_ms
@@ -79,6 +83,8 @@ class ServingRuntime:
         self.t0 = time.perf_counter()
         self.decode_steps = 0
         self.graph_steps = 0
+        self.mixed_rounds = mixed_rounds
+        self.mixed_steps = 0
         # host wall time per phase of step() (seconds): batcher round + admission, merged
         # prefill (through its sampled tokens on the host), decode step, bookkeeping
         self.phase_s = {"schedule": 0.0, "prefill": 0.0, "decode": 0.0, "retire": 0.0}
@@ -245,14 +251,24 @@ class ServingRuntime:
         flushed = self._admit(decisions)
         c1 = time.perf_counter()
         self.phase_s["schedule"] += c1 - c0
+        decoded = False
         if flushed:
-            torch.cuda.nvtx.range_push(f"slx.prefill[{len(flushed)} req]")   # nsys / ncu ranges
+            n_pf_tok = sum(len(r.prompt) for r in flushed)
+            mix = (self.mixed_rounds and bool(self.active)
+                   and n_pf_tok + len(self.active) <= self.m.max_tokens
+                   and max(self.m.seq_len[r.seq] for r in self.active) < self.m.max_ctx)
+            torch.cuda.nvtx.range_push(f"slx.prefill[{len(flushed)} req"
+                                       + (f" + {len(self.active)} decode]" if mix else "]"))
             seqs = []
             try:
                 for r in flushed:
                     r.seq = self.m.alloc_seq()
                     seqs.append(r.seq)
-                batch = build_prefill(flushed, self.m.seq_len)
+                if mix:
+                    batch, n_pf = build_mixed(flushed, self.active, self.m.seq_len)
+                else:
+                    batch = build_prefill(flushed, self.m.seq_len)
+                    n_pf = len(batch.requests)
                 logits = self.m.forward(self._i32(batch.tokens), self._i32(batch.pos),
                                         self._i32(batch.seq), self._i32(batch.slot),
                                         torch.from_numpy(batch.logit_rows).to(self.m.device),
@@ -266,19 +282,27 @@ class ServingRuntime:
                     r.seq = -1
                 torch.cuda.nvtx.range_pop()
                 raise
-            for r in batch.requests:
+            new = batch.requests[:n_pf]
+            for r in new:
                 self.m.seq_len[r.seq] += len(r.prompt)
                 self.served[r.function_id] = self.served.get(r.function_id, 0) + 1
             t = self.now_ms()
-            for r, tok in zip(batch.requests, nxt):
+            for r, tok in zip(new, nxt[:n_pf]):
                 r.generated.append(int(tok))
                 r.first_token_ms = t
-            self.active += batch.requests
+            if mix:   # the running sequences' tokens of this round
+                for r, tok in zip(batch.requests[n_pf:], nxt[n_pf:]):
+                    self.m.seq_len[r.seq] += 1
+                    r.generated.append(int(tok))
+                self.decode_steps += 1
+                self.mixed_steps += 1
+                decoded = True
+            self.active += new
             torch.cuda.nvtx.range_pop()
         c2 = time.perf_counter()
         self.phase_s["prefill"] += c2 - c1
         self._retire()
-        if self.active:
+        if self.active and not decoded:
             c3 = time.perf_counter()
             batch = build_decode(self.active, self.m.seq_len)
             if int(batch.pos.max()) >= self.m.max_ctx:
@@ -350,6 +374,7 @@ class ServingRuntime:
         out = {"requests": len(done), "output_tokens": toks,
                "tokens_per_s": toks / span_s if span_s > 0 else None,
                "decode_steps": self.decode_steps, "graph_steps": self.graph_steps,
+               "mixed_steps": self.mixed_steps,
                "host_s_by_phase": {k: round(v, 3) for k, v in self.phase_s.items()}}
         for name, vals in (("ttft_ms", ttft), ("e2e_ms", e2e), ("tpot_ms", tpot)):
             if vals:

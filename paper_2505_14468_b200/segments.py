@@ -84,6 +84,22 @@ def build_decode(requests: list, seq_len: list) -> MixedBatch:
                       i32([r.adapter_slot for r in requests]), np.arange(n, dtype=np.int64))
 
 
+def build_mixed(prefill: list, decode: list, seq_len: list) -> tuple[MixedBatch, int]:
+    """One forward for a round with both new prompts and running sequences: the prefill
+    segments followed by one 1-token segment per running sequence (its last generated token
+    at its next position, a segment with a cached prefix).  Returns the batch and the number
+    of prefill requests (``batch.requests[:n]``; the rest are the decode rows)."""
+    p = build_prefill(prefill, seq_len)
+    d = build_decode(decode, seq_len)
+    T = p.n_tokens
+    cat = np.concatenate
+    return MixedBatch(p.requests + d.requests, cat([p.tokens, d.tokens]), cat([p.pos, d.pos]),
+                      cat([p.seq, d.seq]), cat([p.slot, d.slot]),
+                      cat([p.seg_indptr, d.seg_indptr[1:] + T]).astype(np.int32),
+                      cat([p.seg_slot, d.seg_slot]),
+                      cat([p.logit_rows, d.logit_rows + T])), len(p.requests)
+
+
 def group_by_gpu(decisions) -> dict:
     """FlushDecisions of one round grouped per target GPU (one mixed batch each)."""
     out: dict = {}

@@ -66,6 +66,42 @@ def test_preloader_h2d_then_runtime_serves_golden_tokens(golden):
     store.close()
 
 
+def test_mixed_rounds_serve_golden_tokens(golden):
+    """Staggered arrivals, so rounds have new prompts AND running sequences: with mixed rounds
+    the running sequences' tokens ride in the round's prefill forward (1-token segments with a
+    cached prefix); fp32 greedy tokens stay bit-exact with the transformers golden, and equal
+    the separate prefill + decode rounds'."""
+    out = {}
+    for mixed in (True, False):
+        m, w, ads = _model(golden)
+        for a, ad in enumerate(ads):
+            m.pool.load(a, ad, TINY_LORA)
+        funcs = {f"fn{a}": (_spec(f"fn{a}"), a) for a in range(4)}
+        rt = ServingRuntime(m, funcs, mixed_rounds=mixed)
+        prompts = _prompts(golden)
+        ids = list(map(int, golden["adapter_ids"]))
+        n_new = int(golden["n_new"])
+        half = len(prompts) // 2
+        for i in range(half):
+            rt.submit(i, f"fn{ids[i]}", prompts[i], n_new)
+        for _ in range(200):       # the first half is running before the rest arrives
+            rt.step()
+            if rt.active:
+                break
+        for k in range(3):
+            rt.step()
+        for i in range(half, len(prompts)):
+            rt.submit(i, f"fn{ids[i]}", prompts[i], n_new)
+        done = rt.run_until_idle()
+        assert len(done) == len(prompts)
+        toks = np.stack([np.asarray(sorted(done, key=lambda r: r.request_id)[i].generated[:n_new])
+                         for i in range(len(prompts))])
+        assert np.array_equal(toks, golden["tokens"])
+        out[mixed] = (toks, rt.mixed_steps)
+    assert out[True][1] > 0 and out[False][1] == 0
+    assert np.array_equal(out[True][0], out[False][0])
+
+
 def test_nccl_broadcast_world1_roundtrip():
     """The pre-loader's own NCCL communicator (world 1 on the single-GPU box): one host read,
     pipelined H2D + broadcast, bytes land intact."""

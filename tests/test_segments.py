@@ -3,7 +3,8 @@
 import numpy as np
 
 from paper_2505_14468_b200.batching import FlushDecision
-from paper_2505_14468_b200.segments import Request, build_decode, build_prefill, group_by_gpu
+from paper_2505_14468_b200.segments import (Request, build_decode, build_mixed, build_prefill,
+                                             group_by_gpu)
 
 
 def _reqs():
@@ -46,3 +47,24 @@ def test_group_by_gpu():
           FlushDecision("c", "g0", (3, 4), "margin", 1.0)]
     g = group_by_gpu(ds)
     assert [d.function_id for d in g["g0"]] == ["a", "c"] and len(g["g1"]) == 1
+
+
+def test_mixed_round_prefill_then_one_token_per_running_sequence():
+    rs = _reqs()
+    new, running = rs[:4], rs[4:]
+    for r in running:
+        r.generated = [r.request_id + 100]
+    seq_len = [0] * 8
+    for r in running:
+        seq_len[r.seq] = 7 + r.seq
+    b, n = build_mixed(new, running, seq_len)
+    p = build_prefill(new, seq_len)
+    d = build_decode(running, seq_len)
+    assert n == len(new) and b.requests[:n] == p.requests and b.requests[n:] == running
+    T = p.n_tokens
+    assert b.n_tokens == T + len(running)
+    assert b.tokens.tolist() == p.tokens.tolist() + d.tokens.tolist()
+    assert b.pos[T:].tolist() == [seq_len[r.seq] for r in running]     # cached-prefix segments
+    assert b.seg_indptr.tolist() == p.seg_indptr.tolist() + [T + i + 1 for i in range(len(running))]
+    assert b.logit_rows.tolist() == p.logit_rows.tolist() + [T + i for i in range(len(running))]
+    assert b.seg_slot.tolist() == p.seg_slot.tolist() + [r.adapter_slot for r in running]
