@@ -77,7 +77,8 @@ def test_mixed_rounds_serve_golden_tokens(golden):
         for a, ad in enumerate(ads):
             m.pool.load(a, ad, TINY_LORA)
         funcs = {f"fn{a}": (_spec(f"fn{a}"), a) for a in range(4)}
-        rt = ServingRuntime(m, funcs, mixed_rounds=mixed)
+        # a tick far beyond every deadline margin: each queue flushes at the next round
+        rt = ServingRuntime(m, funcs, tick_ms=1e6, mixed_rounds=mixed)
         prompts = _prompts(golden)
         ids = list(map(int, golden["adapter_ids"]))
         n_new = int(golden["n_new"])

@@ -7,8 +7,9 @@ prefill, CUDA-graph decode buckets.  Reports the reference's metrics (nearest-ra
 TPOT / E2E percentiles, output tokens/s, metrics.py:17-25,114-147) and writes the request CSV
 in the reference's format.
 python tools/serve_trace.py TRACE.csv OUT_PREFIX [resident_slots] [time_scale] [max_sequences]
-                            [7b|13b] [r16|mixed]
-(13b mixed: Llama-2-13B shape, each function's adapter rank drawn from {8, 16, 64} -- BASELINE
+                            [7b|13b] [r16|mixed] [mix]
+(mix: ServingRuntime(mixed_rounds=True), decode tokens riding in the round's prefill forward.
+13b mixed: Llama-2-13B shape, each function's adapter rank drawn from {8, 16, 64} -- BASELINE
 config 4's 13B family; the adapter pool then exceeds the stacked-decode budget and decode takes
 the gathered LoRA kernels.)"""
 import json
@@ -34,6 +35,7 @@ time_scale = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
 MAX_SEQS = int(sys.argv[5]) if len(sys.argv) > 5 else 128   # concurrent sequences (decode batch)
 BACKBONE = sys.argv[6] if len(sys.argv) > 6 else "7b"
 RANKS = sys.argv[7] if len(sys.argv) > 7 else "r16"
+MIXED_ROUNDS = len(sys.argv) > 8 and sys.argv[8] == "mix"
 MAX_CTX = 512
 torch.cuda.set_device(0)
 recs = wire.read_trace_csv(trace_path)
@@ -79,7 +81,8 @@ for f in fids:
     funcs[f] = (spec, slot_of.get(f, -1))
 adapters = {f: (f"adapter/{f}", lora_of[f]) for f in fids}
 off = Offloader(m, store, dict(slot_of))
-rt = ServingRuntime(m, funcs, store=store, adapters=adapters, preloader=pre, offloader=off)
+rt = ServingRuntime(m, funcs, store=store, adapters=adapters, preloader=pre, offloader=off,
+                    mixed_rounds=MIXED_ROUNDS)
 rt.graphs.warm()
 t_start = time.perf_counter()
 done = wire.replay(rt, recs, cfg.vocab, seed=0, time_scale=time_scale, max_ctx=MAX_CTX)
@@ -92,7 +95,7 @@ rep.update({"trace": os.path.basename(trace_path), "requests_in_trace": len(recs
             "demotions_in_container_tier": len(off.demoted),
             "model": f"{cfg.name} shape bf16, random init; adapters on q,k,v,o of rank "
                      f"{'8/16/64 (seeded per function)' if RANKS == 'mixed' else '16'}",
-            "decode_lora": m.decode_lora,
+            "decode_lora": m.decode_lora, "mixed_rounds": MIXED_ROUNDS,
             "slo_ttft_ms": 5.0 * t0})
 rep["slo_attainment"] = float(np.mean([(r.first_token_ms - r.arrival_ms) <= 5.0 * t0 for r in done]))
 wire.write_requests_csv(sorted(done, key=lambda r: r.request_id), out_prefix + "_requests.csv",
