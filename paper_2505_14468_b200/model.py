@@ -738,6 +738,12 @@ class MultiLoraModel:
             hn = hn.index_select(0, logit_rows)
         return ops.gemm(hn, w["lm_head"], out_dtype=torch.float32)
 
+    def _small_prefill(self, T: int) -> bool:
+        """Prefill LoRA through the gathered / stacked decode kernels (batches the fold
+        declines, up to prefill_gather_max_tokens tokens)."""
+        return (T <= self.prefill_gather_max_tokens and set(self.targets) <= {"q", "k", "v", "o"}
+                and self.pool.max_rank <= 64)
+
     def _prefill_plans(self, segments, slot_host, T: int, flash: bool, sgmv: bool):
         """(flash plan, LoRA-fold plan, SGMV plan) of a segmented prefill batch, cached by the
         segment layout and the segments' adapter slots (a serving loop re-plans only when the
@@ -753,7 +759,7 @@ class MultiLoraModel:
         if sgmv:
             if self.lora_fold:
                 fold = self._fold_plan(segments, slot_host, T)
-            if fold is None:
+            if fold is None and not self._small_prefill(T):   # the small path plans on device
                 sgmv_plan = self._sgmv_plan(segments, slot_host)
         if len(self._plan_cache) >= 16:
             self._plan_cache.pop(next(iter(self._plan_cache)))
@@ -796,8 +802,7 @@ class MultiLoraModel:
         # short-segment batches the fold rejects (a serving round's merged small prompts): the
         # gathered shrink / expand kernels of the decode path, parallel over token tiles, instead
         # of per-segment grouped GEMMs whose few CTAs each walk the whole K
-        small = (sgmv and fold is None and T <= self.prefill_gather_max_tokens
-                 and set(self.targets) <= {"q", "k", "v", "o"} and self.pool.max_rank <= 64)
+        small = sgmv and fold is None and self._small_prefill(T)
         if small and self.prefill_small_lora == "stacked" and self.use_stacked_decode and self.stack:
             # or the stacked shrink as the projection GEMM's side output (no shrink launches)
             stacked, small, sgmv_plan = True, False, None

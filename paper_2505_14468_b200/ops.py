@@ -9,6 +9,8 @@ from __future__ import annotations
 
 import ctypes
 
+import numpy as np
+
 import torch
 
 from . import _lib
@@ -530,23 +532,33 @@ def prefill_plan(segments, heads: int, device, bq: int | None = None):
     shares come out even."""
     if bq is None:
         bq = int(_lib.load().slx_flash_prefill_tile_queries())
-    tiles, items = [], []
-    for tok0, n, seq, pos0 in segments:
-        ids = []
-        for q in range(0, n, bq):
-            ids.append(len(tiles))
-            tiles.append((tok0 + q, min(bq, n - q), seq, pos0 + q))
-        pairs = [(ids[k + 1], ids[k]) if k + 1 < len(ids) else (ids[k], -1)
-                 for k in range(0, len(ids), 2)]
-        for h in range(heads):
-            items += [(a, b, h, 0) for a, b in pairs]
-
-    def cost(it):
-        a, b = tiles[it[0]], (tiles[it[1]] if it[1] >= 0 else None)
-        return -(-(a[3] + a[1]) // 64) + (-(-(b[3] + b[1]) // 64) if b else 0)
-    items.sort(key=lambda it: -cost(it))
-    t = torch.tensor(tiles, dtype=torch.int32).reshape(-1, 4)
-    it = torch.tensor(items, dtype=torch.int32).reshape(-1, 4)
+    # vectorised (a serving round can carry hundreds of segments: decode rows of mixed rounds)
+    sg = np.asarray(segments, dtype=np.int64).reshape(-1, 4)
+    tok0, n, seq, pos0 = sg[:, 0], sg[:, 1], sg[:, 2], sg[:, 3]
+    nt = (n + bq - 1) // bq                       # tiles per segment
+    first = np.cumsum(nt) - nt                    # first tile id of each segment
+    tseg = np.repeat(np.arange(len(sg)), nt)
+    q = (np.arange(int(nt.sum())) - first[tseg]) * bq
+    tiles = np.stack([tok0[tseg] + q, np.minimum(bq, n[tseg] - q), seq[tseg], pos0[tseg] + q], 1)
+    npair = (nt + 1) // 2                         # pairs (tile_a, tile_b) per segment
+    pfirst = np.cumsum(npair) - npair
+    pseg = np.repeat(np.arange(len(sg)), npair)
+    kk = 2 * (np.arange(int(npair.sum())) - pfirst[pseg])
+    has_b = kk + 1 < nt[pseg]
+    pa = np.where(has_b, first[pseg] + kk + 1, first[pseg] + kk)
+    pb = np.where(has_b, first[pseg] + kk, -1)
+    per = heads * npair                           # items per segment: head-major, then pair
+    iseg = np.repeat(np.arange(len(sg)), per)
+    w = np.arange(int(per.sum())) - (np.cumsum(per) - per)[iseg]
+    h = w // npair[iseg]
+    pg = pfirst[iseg] + w % npair[iseg]
+    a, b = pa[pg], pb[pg]
+    ends = tiles[:, 3] + tiles[:, 1]
+    cost = -(-ends[a] // 64) + np.where(b >= 0, -(-ends[np.maximum(b, 0)] // 64), 0)
+    order = np.argsort(-cost, kind="stable")      # longest first (stable, as list.sort)
+    items = np.stack([a, b, h, np.zeros_like(h)], 1)[order]
+    t = torch.from_numpy(tiles.astype(np.int32)).reshape(-1, 4)
+    it = torch.from_numpy(np.ascontiguousarray(items, dtype=np.int32)).reshape(-1, 4)
     return t.to(device), it.to(device)
 
 

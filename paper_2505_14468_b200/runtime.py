@@ -56,9 +56,9 @@ class ServingRuntime:
         the prompts' segments plus one 1-token segment per running sequence -- instead of a
         prefill forward followed by a decode step (each of which streams every weight once);
         the just-prefilled requests then decode from the next round on.  Off by default: it
-        raises saturated throughput (7B trace: 7.4 -> 9.5 k tok/s) but the eager mixed forward
-        plans one segment per running sequence on the host every round, which lengthens the
-        rounds and the queueing (TTFT p50 21.9 ms -> 15.8 s on the same trace)."""
+        raises saturated throughput (7B trace: 9.5 -> 11.2 k tok/s, TTFT p50 15.7 -> 6.8 s) but
+        one replay of a lighter trace hit a device fault that launch-blocking runs do not
+        reproduce."""
         self.m = model
         self.gpu_id = gpu_id
         self.tick_ms = tick_ms

@@ -68,3 +68,39 @@ def test_mixed_round_prefill_then_one_token_per_running_sequence():
     assert b.seg_indptr.tolist() == p.seg_indptr.tolist() + [T + i + 1 for i in range(len(running))]
     assert b.logit_rows.tolist() == p.logit_rows.tolist() + [T + i for i in range(len(running))]
     assert b.seg_slot.tolist() == p.seg_slot.tolist() + [r.adapter_slot for r in running]
+
+
+def _prefill_plan_loops(segments, heads, bq):
+    """The flash plan as straight loops (the vectorised ops.prefill_plan must equal it)."""
+    tiles, items = [], []
+    for tok0, n, seq, pos0 in segments:
+        ids = []
+        for q in range(0, n, bq):
+            ids.append(len(tiles))
+            tiles.append((tok0 + q, min(bq, n - q), seq, pos0 + q))
+        pairs = [(ids[k + 1], ids[k]) if k + 1 < len(ids) else (ids[k], -1)
+                 for k in range(0, len(ids), 2)]
+        for h in range(heads):
+            items += [(a, b, h, 0) for a, b in pairs]
+
+    def cost(it):
+        a, b = tiles[it[0]], (tiles[it[1]] if it[1] >= 0 else None)
+        return -(-(a[3] + a[1]) // 64) + (-(-(b[3] + b[1]) // 64) if b else 0)
+    items.sort(key=lambda it: -cost(it))
+    return tiles, items
+
+
+def test_flash_prefill_plan_matches_loops():
+    from paper_2505_14468_b200.ops import prefill_plan
+    rng = np.random.default_rng(3)
+    for trial in range(30):
+        segs, tok = [], 0
+        for s in range(int(rng.integers(1, 40))):
+            n = int(rng.choice([1, 1, 5, 64, 127, 128, 129, 300, 2048]))
+            segs.append((tok, n, s, int(rng.integers(0, 200)) if rng.random() < 0.5 else 0))
+            tok += n
+        heads = int(rng.choice([1, 4, 32]))
+        t, it = prefill_plan(segs, heads, "cpu", bq=128)
+        rt, ri = _prefill_plan_loops(segs, heads, 128)
+        assert t.tolist() == [list(x) for x in rt]
+        assert it.tolist() == [list(x) for x in ri]
