@@ -530,6 +530,15 @@ lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, in
   __shared__ int total_units;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NTG = so.n_targets;
+  // The stage barriers are initialised first, so the prologue's __syncthreads order the init
+  // before any thread's first wait (a wait on an uninitialised mbarrier is undefined).
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < SH_STAGES; ++st) {
+      tc::mbar_init(&afull[st], 1);
+      tc::mbar_init(&xfull[st], 1);
+    }
+    tc::fence_barrier_init();
+  }
   // ---- the unit table (plan and adapter pool are >= 2 launches back: before the wait)
   // Two dependent round trips: {tile count, tiles (read speculatively up to the plan's bound)}
   // -> {slot rank, the targets' A pointers, token ids}; a pair's "has A" flag is parked in
@@ -603,15 +612,9 @@ lora_shrink_v_kernel(float* __restrict__ v, int ldv, const T* __restrict__ x, in
       tc::bulk_g2s(Xs + stage * x_stage + (size_t)i * d_in, x + (size_t)tile_tok[tl][i] * ldx, row,
                    &xfull[stage], tc::policy_evict_normal());
   };
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < SH_STAGES; ++st) {
-      tc::mbar_init(&afull[st], 1);
-      tc::mbar_init(&xfull[st], 1);
-    }
-    tc::fence_barrier_init();
+  if (threadIdx.x == 0)   // barriers were initialised before the prologue's block syncs
     for (int k = 0; k < SH_STAGES; ++k)
       if (blockIdx.x + k * gridDim.x < U) issue_a(blockIdx.x + k * gridDim.x, k);
-  }
   pdl_wait();   // x comes from the kernel just before us
   pdl_trigger();
   if (threadIdx.x == 0)
@@ -783,6 +786,15 @@ lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, in
   __shared__ int tile_count[EX_MAX_TILES];
   __shared__ int total_units;
   const int NTG = ea.n_targets;
+  // The stage barriers are initialised first, so the prologue's __syncthreads order the init
+  // before any thread's first wait (a wait on an uninitialised mbarrier is undefined).
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < EX_STAGES; ++st) {
+      tc::mbar_init(&bfull[st], 1);
+      tc::mbar_init(&vfull[st], 1);
+    }
+    tc::fence_barrier_init();
+  }
   // ---- the unit table (plan and adapter pool are >= 2 launches back: before the wait)
   // Two dependent round trips (as in the shrink): {tile count, tiles} -> {slot rank, the
   // targets' B pointers, token ids}; a pair's "has B" flag is parked in pair_end until the scan.
@@ -858,15 +870,9 @@ lora_expand_v_kernel(T* __restrict__ y, int ldy, const float* __restrict__ v, in
       tc::bulk_g2s(dst + i * LORA_MAX_RANK, v + (size_t)tile_tok[tl][i] * ldv + voff,
                    (uint32_t)(rank * 4), &vfull[stage], tc::policy_evict_normal());
   };
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < EX_STAGES; ++st) {
-      tc::mbar_init(&bfull[st], 1);
-      tc::mbar_init(&vfull[st], 1);
-    }
-    tc::fence_barrier_init();
+  if (threadIdx.x == 0)   // barriers were initialised before the prologue's block syncs
     for (int k = 0; k < EX_STAGES; ++k)
       if (blockIdx.x + k * gridDim.x < U) issue_b(blockIdx.x + k * gridDim.x, k);
-  }
   pdl_wait();       // v and y come from the kernels just before us
   pdl_trigger();
   if (threadIdx.x == 0)

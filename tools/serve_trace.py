@@ -7,8 +7,9 @@ prefill, CUDA-graph decode buckets.  Reports the reference's metrics (nearest-ra
 TPOT / E2E percentiles, output tokens/s, metrics.py:17-25,114-147) and writes the request CSV
 in the reference's format.
 python tools/serve_trace.py TRACE.csv OUT_PREFIX [resident_slots] [time_scale] [max_sequences]
-                            [7b|13b] [r16|mixed] [mix]
-(mix: ServingRuntime(mixed_rounds=True), decode tokens riding in the round's prefill forward.
+                            [7b|13b] [r16|mixed] [mix|sep]
+(mix (default): decode tokens ride in the round's prefill forward; sep: separate prefill and
+decode forwards, ServingRuntime(mixed_rounds=False).
 13b mixed: Llama-2-13B shape, each function's adapter rank drawn from {8, 16, 64} -- BASELINE
 config 4's 13B family; the adapter pool then exceeds the stacked-decode budget and decode takes
 the gathered LoRA kernels.)"""
@@ -35,7 +36,7 @@ time_scale = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
 MAX_SEQS = int(sys.argv[5]) if len(sys.argv) > 5 else 128   # concurrent sequences (decode batch)
 BACKBONE = sys.argv[6] if len(sys.argv) > 6 else "7b"
 RANKS = sys.argv[7] if len(sys.argv) > 7 else "r16"
-MIXED_ROUNDS = len(sys.argv) > 8 and sys.argv[8] == "mix"
+MIXED_ROUNDS = not (len(sys.argv) > 8 and sys.argv[8] == "sep")
 MAX_CTX = 512
 torch.cuda.set_device(0)
 recs = wire.read_trace_csv(trace_path)
