@@ -611,13 +611,15 @@ class MultiLoraModel:
     @staticmethod
     def segments_of(pos, seq) -> list:
         """Host (tok0, n, seq, pos0) runs of consecutive positions of one sequence."""
-        pos, seq = np.asarray(pos), np.asarray(seq)
-        out, start = [], 0
-        for i in range(1, len(pos) + 1):
-            if i == len(pos) or seq[i] != seq[start] or pos[i] != pos[i - 1] + 1:
-                out.append((start, i - start, int(seq[start]), int(pos[start])))
-                start = i
-        return out
+        pos, seq = np.asarray(pos, dtype=np.int64), np.asarray(seq, dtype=np.int64)
+        if pos.size == 0:
+            return []
+        # a run breaks where the sequence changes or the position does not advance by one
+        brk = np.flatnonzero((seq[1:] != seq[:-1]) | (pos[1:] != pos[:-1] + 1)) + 1
+        starts = np.concatenate([[0], brk])
+        lens = np.diff(np.concatenate([starts, [pos.size]]))
+        return [(int(a), int(n), int(q), int(p0))
+                for a, n, q, p0 in zip(starts, lens, seq[starts], pos[starts])]
 
     def _sk_splits(self, n_out: int, k: int, pieces: int) -> int:
         """Split-K pieces of a decode projection (o, down): the tuned count (7B: o 6, down 8)

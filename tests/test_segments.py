@@ -104,3 +104,23 @@ def test_flash_prefill_plan_matches_loops():
         rt, ri = _prefill_plan_loops(segs, heads, 128)
         assert t.tolist() == [list(x) for x in rt]
         assert it.tolist() == [list(x) for x in ri]
+
+
+def test_segments_of_runs_match_loop():
+    from paper_2505_14468_b200.model import MultiLoraModel
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        pos, seq = [], []
+        for s in range(int(rng.integers(1, 12))):
+            n = int(rng.integers(1, 9))
+            p0 = int(rng.integers(0, 30))
+            q = int(rng.integers(0, 4))
+            pos += list(range(p0, p0 + n))
+            seq += [q] * n
+        ref, start = [], 0
+        for i in range(1, len(pos) + 1):
+            if i == len(pos) or seq[i] != seq[start] or pos[i] != pos[i - 1] + 1:
+                ref.append((start, i - start, seq[start], pos[start]))
+                start = i
+        assert MultiLoraModel.segments_of(np.array(pos, np.int32), np.array(seq, np.int32)) == ref
+    assert MultiLoraModel.segments_of(np.zeros(0, np.int32), np.zeros(0, np.int32)) == []
